@@ -1,0 +1,15 @@
+"""CPU oracle for the QEM MPIW E-step -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import anything here.  The
+product (``paper_2503_08264_b200``) never imports this package, and this
+package never imports the product.  The two share only the seeded input
+generators in ``paper_2503_08264_b200/synth.py`` (which holds none of the
+method's arithmetic).
+
+Modules:
+  qem_oracle.c   fp64 nested-sum elimination (Eq. 7a-c), M-step, EMA, Philox.
+  oracle.py      ctypes wrapper + the QEM step (Algorithm 1) around it.
+  brute.py       literal K^n enumeration in numpy (pins qem_oracle.c).
+  closed_form.py conjugate-Gaussian posterior and evidence (pins the K->inf limit).
+"""

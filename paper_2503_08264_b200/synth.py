@@ -1,0 +1,186 @@
+"""Seeded synthetic inputs for the five BASELINE configs.
+
+This module is shared by the product tests, the oracle tests and bench.py.
+It holds NO arithmetic of the method (no log-factors, weights, moments,
+M-step or EMA): only model *shapes*, ancestral data generation from the prior
+(numpy PCG64, data seed = config id) and standard-normal
+draws for the parity mode of the sampler.
+
+Configs (BASELINE.json ``configs``; readings in DESIGN.md):
+  1  tiny conjugate Gaussian:  mu~N(0,1); z_i~N(mu,1), M=4; x_ij~N(z_i,1), J=5; K=8, T=20
+  2  hierarchical logistic:    mu in R^18, psi~N(0,1); z_i~N(mu, e^psi I), M=300;
+                               x_ij in {0,1}^18 ~ Bern(0.2); y~Bern(sigmoid(z.x)), J=5; K=30, T=100
+  3  three-level Poisson:      g, beta in R^6 ~ N(0,1); u_a~N(g,1), A=6; v_ab~N(u_a,0.5^2), B=30;
+                               x~N(0,I_6); y~Pois(exp(v+beta.x)), J=10; K=30, T=100
+  4  large Gaussian:           mu, logsigma ~N(0,1); z_i~N(mu, e^{2 logsigma}), M=1e5; x~N(z,1), J=32;
+                               K=256, T=50
+  5  large-K logistic:         as 2 with d=16, M=1e4, J=20, K=1024, T=10
+The paper's datasets are not in the container; these
+prior-drawn synthetic sets stand in for them (Radon-shaped: 1 and 4,
+PAPER.md:1245-1262; MovieLens-shaped: 2 and 5, PAPER.md:1002-1029;
+Bus-like nesting: 3).
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+
+# Family / kind codes (plain ints; the C-ABI and the oracle each define their own).
+FAMILY_TWO_LEVEL = 2
+FAMILY_THREE_LEVEL = 3
+SCALE_FIXED = 0
+SCALE_LOGSIGMA = 1  # group variance exp(2 s)
+SCALE_LOGVAR = 2    # group variance exp(s)  (psi)
+OBS_GAUSS = 1
+OBS_BERNOULLI_LOGIT = 2
+OBS_POISSON_LOG = 3
+
+
+@dataclasses.dataclass
+class Model:
+    family: int
+    K: int
+    T: int
+    # two-level
+    d: int = 1
+    scale_kind: int = SCALE_FIXED
+    fixed_var: float = 1.0
+    obs_kind: int = OBS_GAUSS
+    obs_var: float = 1.0
+    n: int = 0          # groups (two-level) / top-level groups A (three-level)
+    J: int = 0
+    # three-level
+    B: int = 0
+    P: int = 0
+    top_var: float = 1.0
+    sub_var: float = 0.25
+    prior_mean: float = 0.0
+    prior_var: float = 1.0
+    config_id: int = 0
+    name: str = ""
+
+    @property
+    def R(self) -> int:
+        """Root latent dims (one shared copy index, R2)."""
+        if self.family == FAMILY_TWO_LEVEL:
+            return self.d + (1 if self.scale_kind != SCALE_FIXED else 0)
+        return 1 + self.P
+
+    @property
+    def pairs(self) -> int:
+        """Factor pairs N*K^2 of one E-step."""
+        if self.family == FAMILY_TWO_LEVEL:
+            return self.n * self.K * self.K
+        return (self.n * self.B) * self.K * self.K
+
+
+def config(cid: int, *, n: Optional[int] = None, K: Optional[int] = None, J: Optional[int] = None,
+           d: Optional[int] = None, B: Optional[int] = None) -> Model:
+    """The BASELINE config ``cid`` (1..5), optionally resized (mini shapes for tests)."""
+    if cid == 1:
+        m = Model(FAMILY_TWO_LEVEL, K=8, T=20, d=1, scale_kind=SCALE_FIXED, fixed_var=1.0,
+                  obs_kind=OBS_GAUSS, obs_var=1.0, n=4, J=5, config_id=1, name="tiny-conjugate-gaussian")
+    elif cid == 2:
+        m = Model(FAMILY_TWO_LEVEL, K=30, T=100, d=18, scale_kind=SCALE_LOGVAR, obs_kind=OBS_BERNOULLI_LOGIT,
+                  n=300, J=5, config_id=2, name="hier-logistic-d18")
+    elif cid == 3:
+        m = Model(FAMILY_THREE_LEVEL, K=30, T=100, n=6, B=30, J=10, P=6, top_var=1.0, sub_var=0.25,
+                  obs_kind=OBS_POISSON_LOG, config_id=3, name="three-level-poisson")
+    elif cid == 4:
+        m = Model(FAMILY_TWO_LEVEL, K=256, T=50, d=1, scale_kind=SCALE_LOGSIGMA, obs_kind=OBS_GAUSS,
+                  obs_var=1.0, n=100_000, J=32, config_id=4, name="large-gaussian-M1e5-K256")
+    elif cid == 5:
+        m = Model(FAMILY_TWO_LEVEL, K=1024, T=10, d=16, scale_kind=SCALE_LOGVAR, obs_kind=OBS_BERNOULLI_LOGIT,
+                  n=10_000, J=20, config_id=5, name="large-K-logistic-d16-K1024")
+    else:
+        raise ValueError(f"unknown config {cid}")
+    if n is not None:
+        m.n = n
+    if K is not None:
+        m.K = K
+    if J is not None:
+        m.J = J
+    if d is not None:
+        m.d = d
+    if B is not None:
+        m.B = B
+    return m
+
+
+@dataclasses.dataclass
+class Data:
+    """Observations (host numpy) plus the true latents they were drawn from."""
+    xg: Optional[np.ndarray] = None   # [n][J] f32 (OBS_GAUSS)
+    xb: Optional[np.ndarray] = None   # [n][J][d] u8 (OBS_BERNOULLI_LOGIT)
+    yb: Optional[np.ndarray] = None   # [n][J] u8
+    xp: Optional[np.ndarray] = None   # [A*B][J][P] f32 (OBS_POISSON_LOG)
+    yp: Optional[np.ndarray] = None   # [A*B][J] i32
+    truth: dict = dataclasses.field(default_factory=dict)
+
+
+def make_data(m: Model, seed: Optional[int] = None) -> Data:
+    """Ancestral draw from the prior (data seed = config id unless given)."""
+    rng = np.random.Generator(np.random.PCG64(m.config_id if seed is None else seed))
+    if m.family == FAMILY_TWO_LEVEL:
+        mu = rng.standard_normal(m.d)
+        s = rng.standard_normal() if m.scale_kind != SCALE_FIXED else 0.0
+        if m.scale_kind == SCALE_FIXED:
+            var = m.fixed_var
+        elif m.scale_kind == SCALE_LOGSIGMA:
+            var = np.exp(2.0 * s)
+        else:
+            var = np.exp(s)
+        z = mu[None, :] + np.sqrt(var) * rng.standard_normal((m.n, m.d))
+        out = Data(truth={"mu": mu, "s": s, "z": z})
+        if m.obs_kind == OBS_GAUSS:
+            assert m.d == 1
+            x = z[:, 0:1] + np.sqrt(m.obs_var) * rng.standard_normal((m.n, m.J))
+            out.xg = x.astype(np.float32)
+        else:
+            xb = (rng.random((m.n, m.J, m.d)) < 0.2).astype(np.uint8)
+            eta = np.einsum("njd,nd->nj", xb.astype(np.float64), z)
+            p = 1.0 / (1.0 + np.exp(-eta))
+            out.xb = xb
+            out.yb = (rng.random((m.n, m.J)) < p).astype(np.uint8)
+        return out
+    # three-level
+    g = rng.standard_normal()
+    beta = rng.standard_normal(m.P)
+    u = g + np.sqrt(m.top_var) * rng.standard_normal(m.n)
+    v = np.repeat(u, m.B) + np.sqrt(m.sub_var) * rng.standard_normal(m.n * m.B)
+    x = rng.standard_normal((m.n * m.B, m.J, m.P)).astype(np.float32)
+    eta = v[:, None] + np.einsum("sjp,p->sj", x.astype(np.float64), beta)
+    y = rng.poisson(np.exp(eta)).astype(np.int32)
+    return Data(xp=x, yp=y, truth={"g": g, "beta": beta, "u": u, "v": v})
+
+
+def eps_normal(shape, seed: int) -> np.ndarray:
+    """Host standard-normal draws (fp32) for the sampler's parity mode."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.standard_normal(shape).astype(np.float32)
+
+
+def latent_shapes(m: Model):
+    """Per-level (instances, dims) of the sample bank, root first."""
+    if m.family == FAMILY_TWO_LEVEL:
+        return [(1, m.R), (m.n, m.d)]
+    return [(1, m.R), (m.n, 1), (m.n * m.B, 1)]
+
+
+def initial_q(m: Model):
+    """Q initialised to N(0,1) per latent dim (App. F Q blocks, e.g. PAPER.md:883-893, 1023-1025)."""
+    return [(np.zeros(n * dd, np.float32), np.ones(n * dd, np.float32)) for n, dd in latent_shapes(m)]
+
+
+def random_q(m: Model, seed: int, spread: float = 1.0):
+    """A non-trivial Q (seeded) for E-step parity cases: means near the data truth, various widths."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = []
+    for n, dd in latent_shapes(m):
+        mean = (0.5 * rng.standard_normal(n * dd)).astype(np.float32)
+        var = (spread * np.exp(0.3 * rng.standard_normal(n * dd))).astype(np.float32)
+        out.append((mean, var))
+    return out
+
