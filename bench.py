@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark: one QEM iteration (sample -> MPIW E-step -> EMA/M-step) per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+Contract:
+  * a step is one whole hot-path pass = one QEM iteration (Alg. 1):
+    Philox sampler (K1) -> forward pair tiles (K2) -> [NCCL all-reduce of the
+    (K+1) fp64 plate sums when N > 1] -> root + backward weights/moments (K3, K4)
+    -> EMA + M-step (K5), on BASELINE config C (default 5; config 4 with --config 4);
+  * metric: E-step factor-pairs/s (N*K^2 per step over the whole iteration), plus
+    QEM iterations/s; strong scaling (the config's M groups split over N ranks);
+  * timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
+    CUDA events on the launching stream, max over ranks; inputs exceed L2;
+  * roofline: the dominant kernel's pair rate vs the ALU ceiling;
+  * e2e: the same iteration through the public API with the observations
+    copied host->device from pinned memory and log Pe + Q read back every step;
+  * cpu_baseline: the fp64 CPU oracle on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Algorithmic per-pair counts: per pass, d+2 FP32 ops + 1 exp.
+SFU_PER_SM_CLK = 16.0     # MUFU.EX2 lanes/clk/SM (guide; measured 15.3, profiles/r01_microbench_pipes.txt)
+FP32_PER_SM_CLK = 128.0   # FFMA lanes/clk/SM (guide; measured 124-126)
+SMS = 148
+SM_MAX_MHZ = 1965.0
+
+
+def pair_ceiling(d: int, mhz: float = SM_MAX_MHZ) -> dict:
+    """Pairs/s ceiling of ONE pass (forward or backward) from the binding pipe."""
+    f = mhz * 1e6 * SMS
+    sfu = f * SFU_PER_SM_CLK / 1.0
+    fp32 = f * FP32_PER_SM_CLK / (d + 2.0)
+    return {"pairs_per_s": min(sfu, fp32), "pipe": "sfu" if sfu <= fp32 else "fp32",
+            "sfu_pairs_per_s": sfu, "fp32_pairs_per_s": fp32}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=1)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------- CPU oracle
+
+
+def oracle_sample(cfg: int, budget_s: float = 15.0, threads: int | None = None):
+    """Time the fp64 oracle E-step + EMA on a bounded sample of groups of config ``cfg``.
+
+    Returns (pairs/s, iters/s extrapolated to the full config, cores, description)."""
+    import numpy as np
+    from oracle import oracle as orc
+    from paper_2503_08264_b200 import synth
+    full = synth.config(cfg)
+    cores = threads or os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    n = max(1, min(full.n, cores))
+    spent, done_pairs, n_runs = 0.0, 0, 0
+    while True:
+        m = synth.config(cfg, n=n)
+        data = synth.make_data(m)
+        q = synth.initial_q(m)
+        eps = orc.eps_for_iteration(m, 1, 100 + cfg)
+        state = orc.initial_state(m)
+        t0 = time.perf_counter()
+        orc.qem_step(m, state, q, eps, 1, data=data)
+        dt = time.perf_counter() - t0
+        spent += dt
+        done_pairs += m.pairs
+        n_runs += 1
+        if spent > budget_s * 0.3 or n >= full.n:
+            break
+        # grow the sample towards the budget
+        n = min(full.n, max(n + 1, int(n * min(8.0, (budget_s * 0.3) / max(dt, 1e-3)))))
+    pairs_per_s = done_pairs / spent
+    iters_per_s = pairs_per_s / full.pairs
+    desc = (f"oracle fp64 E-step+EMA of config {cfg} on {n} of {full.n} groups (K={full.K}), "
+            f"{n_runs} run(s), {spent:.1f} s, OMP threads={os.environ.get('OMP_NUM_THREADS')}")
+    return pairs_per_s, iters_per_s, int(os.environ.get("OMP_NUM_THREADS", cores)), desc
+
+
+# ---------------------------------------------------------------- GPU bench
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2503_08264_b200 import synth
+    from paper_2503_08264_b200.qem import QEM, shard_range
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    m = synth.config(args.config)
+    data = synth.make_data(m)
+    gb, ge = shard_range(m.n, rank, world)
+    g = QEM(m, group_begin=gb, group_end=ge, device=dev)
+    g.set_data(data)
+    seed = 100 + args.config
+    stream = torch.cuda.current_stream()
+
+    def allreduce():
+        if world > 1:
+            dist.all_reduce(g.plate_sum, op=dist.ReduceOp.SUM)
+
+    def step(t, ev=None):
+        g.sample_q(seed=seed, iter=t)
+        if ev:
+            ev[0].record(stream)
+        g.estep_forward()
+        if ev:
+            ev[1].record(stream)
+        allreduce()
+        if ev:
+            ev[2].record(stream)
+        g.estep_backward()
+        if ev:
+            ev[3].record(stream)
+        g.mstep(t)
+
+    t = 1
+    for _ in range(args.warmup):
+        step(t)
+        t += 1
+    torch.cuda.synchronize()
+    launches_per_step = 0
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start.record(stream)
+    for s in range(args.steps):
+        step(t, evs[s])
+        t += 1
+    stop.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_total = start.elapsed_time(stop)
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    bwd_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    comm_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    # launches: sample(1) + forward(root_prep, forward) + backward(root, backward) + mstep(1)
+    launches_per_step = 6
+    flags, clamps = g.read_flags()
+    if world > 1:
+        tt = torch.tensor([ms_total, fwd_ms, bwd_ms, comm_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total, fwd_ms, bwd_ms, comm_ms = tt.tolist()
+    ms_step = ms_total / args.steps
+    pairs_step = m.pairs  # whole job
+    value = pairs_step / (ms_step * 1e-3)
+
+    # ------------------------------------------------------------- e2e leg
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce)
+
+    # ----------------------------------------------------------- roofline
+    local_pairs = (ge - gb) * m.K * m.K
+    dom, dom_ms = ("forward", fwd_ms) if fwd_ms >= bwd_ms else ("backward", bwd_ms)
+    ceil = pair_ceiling(m.d)
+    achieved = local_pairs / (dom_ms * 1e-3)
+    roof = {"bound": "alu", "pipe": ceil["pipe"], "kernel": f"k_{dom}", "unit": "Gpair/s",
+            "achieved": achieved / 1e9, "peak": ceil["pairs_per_s"] / 1e9,
+            "frac": achieved / ceil["pairs_per_s"], "traffic": None,
+            "per_pair": {"exp": 1, "fp32": m.d + 2},
+            "peak_basis": f"{SMS} SMs x {SM_MAX_MHZ:.0f} MHz x min({SFU_PER_SM_CLK:.0f} MUFU.EX2/clk, "
+                          f"{FP32_PER_SM_CLK:.0f} FP32/clk / (d+2)) per pass (DESIGN.md Roofline)",
+            "kernels_ms": {"forward": fwd_ms, "backward": bwd_ms, "allreduce": comm_ms}}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            pps, ips, cores, desc = oracle_sample(args.config, budget_s=args.cpu_budget)
+            cpu = {"value": pps, "unit": "factor-pairs/s", "cores": cores, "kind": "oracle", "sample": desc,
+                   "qem_iters_per_s": ips}
+        except Exception as exc:  # the baseline must not sink the bench line
+            cpu = {"value": None, "unit": "factor-pairs/s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"failed: {exc}"}
+    line = {
+        "metric": "E-step factor-pairs/sec (N*K^2) and QEM iters/sec",
+        "value": value,
+        "unit": "factor-pairs/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 pair tiles, f64 unary/plate sums",
+        "data": "synthetic (ancestral draw from the config's prior, numpy PCG64 seed = config id)",
+        "qem_iters_per_s": 1e3 / ms_step,
+        "config": {"workload": f"config{args.config}:{m.name}", "M_groups": m.n, "K": m.K, "d": m.d,
+                   "J": m.J, "pairs_per_step": pairs_step, "parallelism": f"groups sharded over {world} rank(s)",
+                   "l2": "inputs larger than L2 (samples + per-group messages > 126 MB)",
+                   "sampler": "device Philox4x32-10"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+        "flags": {"device_flags": flags, "var_clamps": clamps},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce):
+    """Same iteration through the public API with host buffers: observations H2D from pinned
+    memory each step, log Pe and the new Q (M-step result) read back D2H each step."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream()
+    x_host = g.x.cpu().pin_memory()
+    y_host = g.y.cpu().pin_memory() if g.y is not None else None
+    outs = [torch.empty_like(lv["q_mean"], device="cpu").pin_memory() for lv in g.levels]
+    outv = [torch.empty_like(lv["q_var"], device="cpu").pin_memory() for lv in g.levels]
+    lp_host = torch.empty(1, dtype=torch.float64).pin_memory()
+    h2d = x_host.numel() * x_host.element_size() + (y_host.numel() * y_host.element_size() if y_host is not None else 0)
+    d2h = 8 + sum(o.numel() * 4 * 2 for o in outs)
+
+    def one(tt):
+        g.x.copy_(x_host, non_blocking=True)
+        if y_host is not None:
+            g.y.copy_(y_host, non_blocking=True)
+        g.sample_q(seed=seed, iter=tt)
+        g.estep_forward()
+        allreduce()
+        g.estep_backward()
+        g.mstep(tt)
+        lp_host.copy_(g.log_pe, non_blocking=True)
+        for o, ov, lv in zip(outs, outv, g.levels):
+            o.copy_(lv["q_mean"], non_blocking=True)
+            ov.copy_(lv["q_var"], non_blocking=True)
+
+    for _ in range(2):
+        one(t)
+        t += 1
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record(stream)
+    for _ in range(args.steps):
+        one(t)
+        t += 1
+    en.record(stream)
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = tt.item()
+    ms_step = ms / args.steps
+    return {"value": m.pairs / (ms_step * 1e-3), "unit": "factor-pairs/s", "ms_per_step": ms_step,
+            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    budget = max(5.0, min(60.0, args.cpu_budget))
+    pps, ips, cores, desc = oracle_sample(args.config, budget_s=budget)
+    ms_step = 1e3 / ips
+    from paper_2503_08264_b200 import synth
+    m = synth.config(args.config)
+    line = {
+        "impl": "reference",
+        "metric": "E-step factor-pairs/sec (N*K^2) and QEM iters/sec",
+        "value": pps,
+        "unit": "factor-pairs/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (ancestral draw from the config's prior, numpy PCG64 seed = config id)",
+        "qem_iters_per_s": ips,
+        "config": {"workload": f"config{args.config}:{m.name}", "M_groups": m.n, "K": m.K, "d": m.d, "J": m.J,
+                   "pairs_per_step": m.pairs, "parallelism": "CPU oracle, OpenMP over groups"},
+        "cpu_baseline": {"value": pps, "unit": "factor-pairs/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": pps, "unit": "factor-pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="qem", choices=["qem", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

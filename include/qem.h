@@ -1,0 +1,225 @@
+/*
+ * qem.h -- C-ABI of the B200-native QEM MPIW E-step library (libqem.so).
+ *
+ * Implements the data-parallel hot path of QEM (arXiv 2503.08264): sample K
+ * copies of every latent from the factorised Gaussian Q, evaluate every
+ * (parent sample k, child sample k') log-factor of every plate instance,
+ * reduce them by max-shifted log-sum-exp along the plate tree into the
+ * log-marginal estimate log Pe over all K^n index tuples, run the backward
+ * (marginal) pass for each latent's per-sample weights, form first/second
+ * moments, and apply the EMA + closed-form Gaussian M-step.
+ *
+ * Citations are PAPER.md:<line> (section / equation) of the paper text:
+ *   Eq. 7a-c  (Sec. 3.2)  MPIW moment, weight, evidence
+ *   Alg. 1            QEM loop
+ *   Eq. 9     (Sec. 4)    EMA over mean parameters
+ *   PAPER.md:393-394 (Limitations)          elimination over the plate tree,
+ *                                           grouping, chunking
+ * Readings of ambiguous points (R1..R22) are listed in DESIGN.md.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Plain C types only.  Pointers named d_* are DEVICE pointers owned by the
+ *    caller (e.g. torch tensors); h_* are host pointers.  The library never
+ *    frees caller memory; it performs no cudaMalloc except inside
+ *    qem_create (its own small device workspace, freed by qem_destroy).
+ *  - `stream` is a cudaStream_t passed as void*; NULL = legacy default stream.
+ *    All device work is stream-ordered; no call synchronises the host except
+ *    qem_read_flags and the h_* readbacks documented below.
+ *  - Status codes are returned, never thrown.  On error, qem_last_error()
+ *    returns a NUL-terminated description (thread-local).
+ *  - Numerical conditions never abort: degenerate evidence (all terms -inf),
+ *    NaN, and variance clamps are recorded in device flags (qem_read_flags).
+ *  - Determinism: identical inputs, launch configuration and world size give
+ *    bit-identical outputs (fixed-order reductions, no float atomics).
+ *
+ * LAYOUTS (row-major, k fastest)
+ *  Latent levels: level 0 = root group (1 instance, R dims, one SHARED copy
+ *  index, R2); level 1 = groups (two-level: n instances x d dims;
+ *  three-level: A top-level groups x 1 dim); level 2 = subgroups (three-level
+ *  only: A*B instances x 1 dim, instance ab = a*B + b).
+ *   q_mean, q_var   float  [instances*dims]        Q_t (mean, variance)
+ *   ema_m1, ema_v   double [instances*dims]        EMA state (E z, Var z)
+ *   z               float  [instances][dims][K]    samples
+ *   w               float  [instances][K]          marginal weights (out)
+ *   m1, v           double [instances*dims]        one-step moments (out)
+ *  Root dims: two-level = mu[0..d-1] then s (if scale_kind != FIXED);
+ *             three-level = g then beta[0..P-1].
+ *  Observations (device, per LOCAL instance):
+ *   OBS_GAUSS            x float [n][J]                          (d == 1)
+ *   OBS_BERNOULLI_LOGIT  x uint8 [n][J][d] in {0,1}; y uint8 [n][J]
+ *   OBS_POISSON_LOG      x float [A*B][J][P];  y int32 [A*B][J]
+ */
+#ifndef QEM_H_
+#define QEM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t qem_status;
+#define QEM_OK 0
+#define QEM_INVALID_ARGUMENT 1 /* null pointer, size, K or d out of range */
+#define QEM_INVALID_MODEL 2    /* model description fails validation */
+#define QEM_UNSUPPORTED 3      /* valid but not implemented (e.g. world>1 on three-level) */
+#define QEM_CUDA_ERROR 4       /* a CUDA call failed; see qem_last_error() */
+
+#define QEM_FAMILY_TWO_LEVEL 2
+#define QEM_FAMILY_THREE_LEVEL 3
+#define QEM_SCALE_FIXED 0    /* group prior variance = fixed_var                  */
+#define QEM_SCALE_LOGSIGMA 1 /* group prior variance = exp(2 s)  (config 4)       */
+#define QEM_SCALE_LOGVAR 2   /* group prior variance = exp(s)    (psi, configs 2,5) */
+#define QEM_OBS_GAUSS 1
+#define QEM_OBS_BERNOULLI_LOGIT 2
+#define QEM_OBS_POISSON_LOG 3
+
+/* Device flag bits (qem_read_flags). */
+#define QEM_FLAG_DEGENERATE 1u /* log-evidence is -inf       */
+#define QEM_FLAG_NAN 2u        /* a NaN reached a weight or moment          */
+#define QEM_FLAG_CLAMP 4u      /* an M-step variance hit the floor (R8)     */
+
+#define QEM_MAX_K 1024
+#define QEM_MAX_D 32
+
+/*
+ * Plate-structured model description (a fixed menu).
+ * Two-level (PAPER.md:1245-1262 Radon-like / 1002-1029 MovieLens-like):
+ *   root mu[d] ~ N(prior_mean, prior_var), s ~ N(prior_mean, prior_var) (if scaled)
+ *   z_i ~ N(mu, V I), V by scale_kind;   obs by obs_kind (GAUSS: x ~ N(z, obs_var))
+ * Three-level (PAPER.md:847-851 nesting):
+ *   g, beta[P] ~ N(prior_mean, prior_var); u_a ~ N(g, top_var);
+ *   v_ab ~ N(u_a, sub_var); y_abj ~ Poisson(exp(v_ab + beta . x_abj))
+ * n = GLOBAL number of level-1 instances; K samples per latent (1..QEM_MAX_K).
+ */
+typedef struct {
+  int32_t family;
+  int32_t d;          /* two-level latent dim (1..QEM_MAX_D); 1 for three-level */
+  int32_t scale_kind;
+  int32_t obs_kind;
+  int64_t n;          /* groups (two-level) or top-level groups A (three-level) */
+  int32_t n_sub;      /* B (three-level) */
+  int32_t n_obs;      /* J observations per group / subgroup */
+  int32_t n_cov;      /* P covariates (three-level) */
+  int32_t K;
+  double fixed_var, obs_var, top_var, sub_var, prior_mean, prior_var;
+} qem_model_desc;
+
+/* EMA / M-step options (Eq. 9, Theorem 1, R5, R8). */
+typedef struct {
+  double new_weight; /* w in (0,1]: m_t = (1-w) m_{t-1} + w m_one  (history lambda = 1-w) */
+  double schedule_p; /* if > 0: lambda_t = 1 - t^{-p} (Theorem 1) overrides new_weight   */
+  double var_floor;  /* Gaussian M-step variance floor (> 0), default 1e-8              */
+} qem_opts;
+
+typedef struct {
+  float* q_mean;
+  float* q_var;
+  double* ema_m1;
+  double* ema_v;
+  float* z;
+  float* w;
+  double* m1;
+  double* v;
+} qem_level;
+
+/* Device buffers bound to a context (all caller-owned).  Unused levels may be
+   zeroed.  x/y are the observation arrays of the LOCAL shard. */
+typedef struct {
+  qem_level level[3];
+  const void* x;
+  const void* y;
+  double* log_pe;      /* [1] log Pe of the last E-step (replicated on every rank) */
+  double* trace;       /* [trace_len] optional: log Pe of iteration t0+j at [j],
+                          written by qem_iterate only (never by the eager calls) */
+  int64_t trace_len;
+  double* plate_sum;   /* [K+1] optional caller-owned plate-sum / all-reduce buffer;
+                          NULL = the context's own (see qem_reduce_buffer)          */
+} qem_buffers;
+
+typedef struct qem_ctx qem_ctx;
+
+/* Validate a model description.  Returns QEM_OK or QEM_INVALID_MODEL with a
+   one-line reason in msg (truncated to cap bytes, always NUL-terminated). */
+qem_status qem_model_validate(const qem_model_desc* desc, char* msg, size_t cap);
+
+/* Shard of level-1 instances owned by `rank` of `world`: a contiguous block
+   [r*n/world, (r+1)*n/world).  Integer-exact. */
+qem_status qem_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
+
+/* Create a context for LOCAL level-1 instances [group_begin, group_end) of the
+   model (global indices key the Philox counters, so samples do not depend on
+   the world size).  world > 1 is supported for the two-level family only.
+   Device workspace is allocated here (O(n_local*K) floats) and freed by
+   qem_destroy.  opts may be NULL (w=0.3, no schedule, floor 1e-8). */
+qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin,
+                      int64_t group_end, qem_ctx** out);
+void qem_destroy(qem_ctx* ctx);
+
+/* Bind the caller's device buffers.  Must precede every compute call; may be
+   called again to re-bind (invalidates a captured qem_iterate graph). */
+qem_status qem_bind(qem_ctx* ctx, const qem_buffers* bufs);
+
+/* K1 -- Q sampler (Alg. 1 line 4 "z ~ Q_t"; location-scale sampling,
+   PAPER.md:708-719).  For every bound level: z = fmaf(sqrtf(q_var), eps, q_mean)
+   (fp32, R22).  eps comes from d_eps[level] ([instances*dims][K]
+   float, host-generated parity mode) when d_eps != NULL and d_eps[level] !=
+   NULL, else from Philox4x32-10 keyed by (seed, iter, level, GLOBAL instance,
+   dim, k) + Box-Muller. */
+qem_status qem_sample_q(qem_ctx* ctx, uint64_t seed, int32_t iter, const float* const* d_eps,
+                        void* stream);
+
+/* K2..K4 -- one MPIW E-step on the bound samples (Eq. 7a-c):
+   log Pe -> bufs.log_pe, weights -> level[*].w, moments (E z, Var z) ->
+   level[*].m1 / .v.  For world > 1 use the two phases below instead, with a
+   SUM all-reduce of the (K+1) doubles returned by qem_reduce_buffer between
+   them; qem_estep == forward + backward when world == 1. */
+qem_status qem_estep(qem_ctx* ctx, void* stream);
+/* Phase 1: sample prep, unary terms, pair-tile forward log-sum-exp; leaves the
+   local plate sum [G(0..K-1), sum_i c_i] (fp64) in the reduce buffer. */
+qem_status qem_estep_forward(qem_ctx* ctx, void* stream);
+/* Device pointer + count of the plate-sum buffer (fp64, K+1 entries). */
+qem_status qem_reduce_buffer(qem_ctx* ctx, double** d_buf, int64_t* count);
+/* Phase 2: root softmax + log Pe (from the reduced buffer), backward weights,
+   moments. */
+qem_status qem_estep_backward(qem_ctx* ctx, void* stream);
+
+/* K5 -- EMA over mean parameters + Gaussian M-step for every bound level
+   (Alg. 1 lines 3 and 6; Eq. 9): with lambda = history weight of iteration t,
+     m1 <- lam m1 + (1-lam) m1_new
+     v  <- lam v + (1-lam) v_new + lam (1-lam) (m1_old - m1_new)^2
+   (exactly the EMA of (E z, E z^2), R19), then
+     q_mean = (float) m1,  q_var = (float) max(v, var_floor).            */
+qem_status qem_mstep(qem_ctx* ctx, int32_t t, void* stream);
+
+/* K6 -- T QEM iterations t = t0 .. t0+T-1 of sample (Philox, seed) ->
+   E-step -> M-step, replayed from one captured CUDA graph (world == 1), or
+   issued eagerly when `use_graph` == 0.  log Pe of iteration t0+j goes to
+   bufs.trace[j] when bufs.trace != NULL. */
+qem_status qem_iterate(qem_ctx* ctx, int32_t t0, int32_t T, uint64_t seed, int32_t use_graph,
+                       void* stream);
+
+/* Synchronises `stream` and returns the OR of all device flags since the last
+   call (then clears them), and the number of M-step variance clamps. */
+qem_status qem_read_flags(qem_ctx* ctx, void* stream, uint32_t* flags, int64_t* clamps);
+
+/* Number of kernels the last qem_* call launched (for the bench's
+   gpu_launches claim). */
+int64_t qem_kernel_launches(const qem_ctx* ctx);
+
+/* Copy the per-group reference-differenced messages Delta g_i(k)
+   (float [n_local][K]) and per-group constants c_i (double [n_local]) of the
+   last forward pass into caller buffers (stream-ordered D2D copies):
+   g_i(k) = c_i + Delta g_i(k) = log (1/K) sum_k' exp(B_i(k,k') + A_i(k'))
+   (DESIGN.md "Forward").  For sampled full-size parity checks; two-level only. */
+qem_status qem_copy_messages(qem_ctx* ctx, float* d_dg, double* d_c, void* stream);
+
+const char* qem_status_str(qem_status s);
+const char* qem_last_error(void);
+const char* qem_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QEM_H_ */

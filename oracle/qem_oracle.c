@@ -27,11 +27,11 @@
  *    PAPER.md:242-245) with the history-weight reading (R5).
  *
  * Readings of silent/ambiguous points (R1..R21) are listed in DESIGN.md.
- * Pins: tests/test_oracle_*.py check this file against literal K^n
+ * Pins: tests/test_oracle.py check this file against literal K^n
  * enumeration (oracle/brute.py, independent numpy code), closed-form
  * conjugate posteriors (oracle/closed_form.py), textbook special cases and
- * invariants.  The Philox stream is "parity unpinned" against an external
- * known-answer vector (none is available offline); see DESIGN.md.
+ * invariants.  Philox4x32-10 is pinned by the published Random123
+ * known-answer vectors (tests/golden/philox4x32_10_kat.txt).
  *
  * All arithmetic is fp64 and uses the C library (exp, log, log1p, lgamma).
  * The only fp32 operations are the two places where the paper's method
@@ -478,9 +478,11 @@ void orc_sample(long n, int K, const float* q_m, const float* q_v, const float* 
 /* Philox4x32-10 (Salmon et al. 2011), written out from its definition:
    10 rounds of the two multiply-xor S-boxes with Weyl key schedule.
    Counter layout for sample k of latent (level, instance, dim) at iteration
-   t:  ctr = {k >> 1, dim, instance, (level << 24) | (t & 0xffffff)},
-   key = {seed lo, seed hi}.  Outputs 0,1 feed one Box-Muller pair:
-   u = ((x >> 8) + 0.5) * 2^-24;  eps = sqrt(-2 ln u0) * (k even ? cos : sin)(2 pi u1). */
+   t:  ctr = {k >> 2, dim, instance, (level << 24) | (t & 0xffffff)},
+   key = {seed lo, seed hi}.  The four outputs feed two Box-Muller pairs:
+   k%4 in {0,1} uses (o0, o1), k%4 in {2,3} uses (o2, o3);
+   u = ((x >> 9) + 0.5) * 2^-23 (exact in fp32);
+   eps = sqrt(-2 ln u_a) * (k even ? cos : sin)(2 pi u_b). */
 void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
   uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
   uint32_t k0 = key_in[0], k1 = key_in[1];
@@ -507,13 +509,15 @@ void orc_normal_eps(uint64_t seed, uint32_t iter, uint32_t level, uint32_t insta
   const double PI = 3.14159265358979323846;
   for (int r = 0; r < ndim; ++r) {
     for (int k = 0; k < K; ++k) {
-      uint32_t ctr[4] = {(uint32_t)(k >> 1), (uint32_t)r, instance, (level << 24) | (iter & 0xffffffu)};
+      uint32_t ctr[4] = {(uint32_t)(k >> 2), (uint32_t)r, instance, (level << 24) | (iter & 0xffffffu)};
       uint32_t o[4];
       orc_philox4x32_10(ctr, key, o);
-      double u0 = ((double)(o[0] >> 8) + 0.5) * (1.0 / 16777216.0);
-      double u1 = ((double)(o[1] >> 8) + 0.5) * (1.0 / 16777216.0);
-      double rad = sqrt(-2.0 * log(u0));
-      eps[(size_t)r * K + k] = (k & 1) ? rad * sin(2.0 * PI * u1) : rad * cos(2.0 * PI * u1);
+      uint32_t xa = (k & 2) ? o[2] : o[0];
+      uint32_t xb = (k & 2) ? o[3] : o[1];
+      double ua = ((double)(xa >> 9) + 0.5) * (1.0 / 8388608.0);
+      double ub = ((double)(xb >> 9) + 0.5) * (1.0 / 8388608.0);
+      double rad = sqrt(-2.0 * log(ua));
+      eps[(size_t)r * K + k] = (k & 1) ? rad * sin(2.0 * PI * ub) : rad * cos(2.0 * PI * ub);
     }
   }
 }

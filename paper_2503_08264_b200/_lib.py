@@ -1,0 +1,98 @@
+"""ctypes binding of libqem.so (include/qem.h).  Argument marshalling only.
+
+Loading fails loudly if the in-tree CUDA library is missing: there is no CPU
+fallback anywhere in the product path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libqem.so")
+
+FAMILY_TWO_LEVEL, FAMILY_THREE_LEVEL = 2, 3
+OK, INVALID_ARGUMENT, INVALID_MODEL, UNSUPPORTED, CUDA_ERROR = 0, 1, 2, 3, 4
+FLAG_DEGENERATE, FLAG_NAN, FLAG_CLAMP = 1, 2, 4
+
+# Every symbol include/qem.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "qem_model_validate", "qem_shard_range", "qem_create", "qem_destroy", "qem_bind", "qem_sample_q",
+    "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_mstep", "qem_iterate",
+    "qem_read_flags", "qem_kernel_launches", "qem_copy_messages", "qem_status_str", "qem_last_error",
+    "qem_version",
+]
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int32), ("d", ctypes.c_int32), ("scale_kind", ctypes.c_int32),
+                ("obs_kind", ctypes.c_int32), ("n", ctypes.c_int64), ("n_sub", ctypes.c_int32),
+                ("n_obs", ctypes.c_int32), ("n_cov", ctypes.c_int32), ("K", ctypes.c_int32),
+                ("fixed_var", ctypes.c_double), ("obs_var", ctypes.c_double), ("top_var", ctypes.c_double),
+                ("sub_var", ctypes.c_double), ("prior_mean", ctypes.c_double), ("prior_var", ctypes.c_double)]
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("new_weight", ctypes.c_double), ("schedule_p", ctypes.c_double), ("var_floor", ctypes.c_double)]
+
+
+class Level(ctypes.Structure):
+    _fields_ = [("q_mean", ctypes.c_void_p), ("q_var", ctypes.c_void_p), ("ema_m1", ctypes.c_void_p),
+                ("ema_v", ctypes.c_void_p), ("z", ctypes.c_void_p), ("w", ctypes.c_void_p),
+                ("m1", ctypes.c_void_p), ("v", ctypes.c_void_p)]
+
+
+class Buffers(ctypes.Structure):
+    _fields_ = [("level", Level * 3), ("x", ctypes.c_void_p), ("y", ctypes.c_void_p),
+                ("log_pe", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_len", ctypes.c_int64),
+                ("plate_sum", ctypes.c_void_p)]
+
+
+class QemError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise QemError(f"{LIB_PATH} is missing: build it with `python -m paper_2503_08264_b200.build` "
+                           "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+        L.qem_model_validate.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_char_p, ctypes.c_size_t]
+        L.qem_shard_range.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.qem_create.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(Opts), i64, i64, ctypes.POINTER(vp)]
+        L.qem_destroy.argtypes = [vp]
+        L.qem_destroy.restype = None
+        L.qem_bind.argtypes = [vp, ctypes.POINTER(Buffers)]
+        L.qem_sample_q.argtypes = [vp, u64, i32, ctypes.POINTER(vp), vp]
+        L.qem_estep.argtypes = [vp, vp]
+        L.qem_estep_forward.argtypes = [vp, vp]
+        L.qem_estep_backward.argtypes = [vp, vp]
+        L.qem_reduce_buffer.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i64)]
+        L.qem_mstep.argtypes = [vp, i32, vp]
+        L.qem_iterate.argtypes = [vp, i32, i32, u64, i32, vp]
+        L.qem_read_flags.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(i64)]
+        L.qem_kernel_launches.argtypes = [vp]
+        L.qem_kernel_launches.restype = i64
+        L.qem_copy_messages.argtypes = [vp, vp, vp, vp]
+        L.qem_status_str.argtypes = [i32]
+        L.qem_status_str.restype = ctypes.c_char_p
+        L.qem_last_error.restype = ctypes.c_char_p
+        L.qem_version.restype = ctypes.c_char_p
+        for name in ["qem_model_validate", "qem_shard_range", "qem_create", "qem_bind", "qem_sample_q", "qem_estep",
+                     "qem_estep_forward", "qem_estep_backward", "qem_reduce_buffer", "qem_mstep", "qem_iterate",
+                     "qem_read_flags", "qem_copy_messages"]:
+            getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status != OK:
+        L = lib()
+        raise QemError(f"{what}: {L.qem_status_str(status).decode()}: {L.qem_last_error().decode()}")

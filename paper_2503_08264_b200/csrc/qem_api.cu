@@ -1,0 +1,379 @@
+// qem_api.cu -- the C-ABI (include/qem.h): validation, context/workspace,
+// phase orchestration and the CUDA-graph QEM loop.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "qem_internal.h"
+
+namespace {
+thread_local char g_err[512] = "";
+
+qem_status fail(qem_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+qem_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(QEM_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int pad4(int x) { return (x + 3) & ~3; }
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+qem_status validate(const qem_model_desc* d, char* msg, size_t cap) {
+  char buf[256] = "";
+  qem_status s = QEM_OK;
+#define BAD(...)                                \
+  do {                                          \
+    snprintf(buf, sizeof buf, __VA_ARGS__);     \
+    s = QEM_INVALID_MODEL;                      \
+    goto done;                                  \
+  } while (0)
+  if (!d) BAD("null model description");
+  if (d->K < 1 || d->K > QEM_MAX_K) BAD("K=%d out of range [1, %d]", d->K, QEM_MAX_K);
+  if (d->n < 1) BAD("n=%lld must be >= 1", (long long)d->n);
+  if (d->n_obs < 0) BAD("n_obs=%d must be >= 0", d->n_obs);
+  if (!(d->prior_var > 0)) BAD("prior_var must be > 0");
+  if (d->family == QEM_FAMILY_TWO_LEVEL) {
+    if (d->d < 1 || d->d > QEM_MAX_D) BAD("d=%d out of range [1, %d]", d->d, QEM_MAX_D);
+    if (!qem::tl_supported_d(d->d)) BAD("d=%d has no compiled kernel (supported: 1,2,3,4,8,16,18)", d->d);
+    if (d->scale_kind < QEM_SCALE_FIXED || d->scale_kind > QEM_SCALE_LOGVAR) BAD("unknown scale_kind %d", d->scale_kind);
+    if (d->scale_kind == QEM_SCALE_FIXED && !(d->fixed_var > 0)) BAD("fixed_var must be > 0");
+    if (d->obs_kind == QEM_OBS_GAUSS) {
+      if (d->d != 1) BAD("OBS_GAUSS requires d == 1 (got %d)", d->d);
+      if (!(d->obs_var > 0)) BAD("obs_var must be > 0");
+    } else if (d->obs_kind != QEM_OBS_BERNOULLI_LOGIT) {
+      BAD("obs_kind %d not valid for the two-level family", d->obs_kind);
+    }
+  } else if (d->family == QEM_FAMILY_THREE_LEVEL) {
+    if (d->obs_kind != QEM_OBS_POISSON_LOG) BAD("three-level family requires OBS_POISSON_LOG");
+    if (d->n_sub < 1) BAD("n_sub=%d must be >= 1", d->n_sub);
+    if (d->n_cov < 0 || d->n_cov > QEM_MAX_D) BAD("n_cov=%d out of range", d->n_cov);
+    if (!(d->top_var > 0) || !(d->sub_var > 0)) BAD("top_var and sub_var must be > 0");
+    if (d->n > (1 << 20) || (int64_t)d->n * d->n_sub * d->K * d->K > (int64_t)1 << 31)
+      BAD("three-level model too large for the replicated fp64 tables");
+  } else {
+    BAD("unknown family %d", d->family);
+  }
+#undef BAD
+done:
+  if (msg && cap) {
+    strncpy(msg, buf, cap - 1);
+    msg[cap - 1] = 0;
+  }
+  if (s != QEM_OK) fail(s, "%s", buf);
+  return s;
+}
+
+// Carve the workspace; with base == nullptr only measures.
+size_t carve(qem_ctx* c, char* base) {
+  const qem_model_desc& d = c->desc;
+  const int K = d.K;
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    char* p = base ? base + off : nullptr;
+    off += align256(bytes);
+    return p;
+  };
+  c->cnt = reinterpret_cast<qem::Counters*>(take(sizeof(qem::Counters)));
+  if (d.family == QEM_FAMILY_TWO_LEVEL) {
+    const int D = d.d;
+    c->tw.fwd_coef = reinterpret_cast<float*>(take(sizeof(float) * K * (D + 2)));
+    c->tw.bwd_table = reinterpret_cast<float*>(take(sizeof(float) * K * pad4(D + 3)));
+    c->tw.f_root = reinterpret_cast<double*>(take(sizeof(double) * K));
+    c->tw.ref = reinterpret_cast<qem::RefInfo*>(take(sizeof(qem::RefInfo)));
+    c->tw.partial = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->grid_fwd * (K + 1)));
+    c->tw.red = reinterpret_cast<double*>(take(sizeof(double) * (K + 1)));
+    c->tw.dg = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
+    c->tw.lnP = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
+    c->tw.cvec = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->n_local));
+  } else {
+    const int64_t A = d.n, AB = d.n * d.n_sub, KK = (int64_t)K * K;
+    c->th.f_root = reinterpret_cast<double*>(take(sizeof(double) * K));
+    c->th.Lab = reinterpret_cast<double*>(take(sizeof(double) * AB * KK));
+    c->th.Mab = reinterpret_cast<double*>(take(sizeof(double) * AB * KK));
+    c->th.Ta = reinterpret_cast<double*>(take(sizeof(double) * A * KK));
+    c->th.ha = reinterpret_cast<double*>(take(sizeof(double) * A * K));
+    c->th.red = reinterpret_cast<double*>(take(sizeof(double) * (K + 1)));
+  }
+  return off;
+}
+
+bool level_ok(const qem_level& l) { return l.q_mean && l.q_var && l.ema_m1 && l.ema_v && l.z && l.w && l.m1 && l.v; }
+
+qem_status need_bound(qem_ctx* c) {
+  if (!c) return fail(QEM_INVALID_ARGUMENT, "null context");
+  if (!c->bound) return fail(QEM_INVALID_ARGUMENT, "no buffers bound (call qem_bind first)");
+  return QEM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+qem_status qem_model_validate(const qem_model_desc* desc, char* msg, size_t cap) { return validate(desc, msg, cap); }
+
+qem_status qem_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin, int64_t* end) {
+  if (!begin || !end) return fail(QEM_INVALID_ARGUMENT, "null output pointer");
+  if (n < 0 || world < 1 || rank < 0 || rank >= world)
+    return fail(QEM_INVALID_ARGUMENT, "bad shard request n=%lld rank=%d world=%d", (long long)n, rank, world);
+  *begin = (int64_t)((__int128)n * rank / world);
+  *end = (int64_t)((__int128)n * (rank + 1) / world);
+  return QEM_OK;
+}
+
+qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin, int64_t group_end,
+                      qem_ctx** out) {
+  if (!out) return fail(QEM_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  qem_status s = validate(desc, nullptr, 0);
+  if (s != QEM_OK) return s;
+  if (group_begin < 0 || group_end > desc->n || group_begin >= group_end)
+    return fail(QEM_INVALID_ARGUMENT, "bad local group range [%lld, %lld) of n=%lld", (long long)group_begin,
+                (long long)group_end, (long long)desc->n);
+  if (desc->family == QEM_FAMILY_THREE_LEVEL && (group_begin != 0 || group_end != desc->n))
+    return fail(QEM_UNSUPPORTED, "three-level models run as replicas only (no group sharding)");
+  qem_ctx* c = new (std::nothrow) qem_ctx();
+  if (!c) return fail(QEM_INVALID_ARGUMENT, "out of host memory");
+  c->desc = *desc;
+  c->opts.new_weight = 0.3;
+  c->opts.schedule_p = 0.0;
+  c->opts.var_floor = 1e-8;
+  if (opts) c->opts = *opts;
+  if (!(c->opts.var_floor > 0) || !(c->opts.new_weight > 0 && c->opts.new_weight <= 1) || c->opts.schedule_p < 0 ||
+      c->opts.schedule_p >= 1) {
+    delete c;
+    return fail(QEM_INVALID_ARGUMENT, "bad options (need 0<new_weight<=1, 0<=schedule_p<1, var_floor>0)");
+  }
+  c->g_begin = group_begin;
+  c->g_end = group_end;
+  c->n_local = group_end - group_begin;
+  c->R = desc->family == QEM_FAMILY_TWO_LEVEL ? desc->d + (desc->scale_kind != QEM_SCALE_FIXED) : 1 + desc->n_cov;
+  c->grid_fwd = c->grid_bwd = 1;
+  if (desc->family == QEM_FAMILY_TWO_LEVEL) qem::tl_grids(desc, c->n_local, sm_count(), &c->grid_fwd, &c->grid_bwd);
+  c->ws_bytes = carve(c, nullptr);
+  cudaError_t e = cudaMalloc(&c->ws, c->ws_bytes);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(workspace)");
+  }
+  carve(c, reinterpret_cast<char*>(c->ws));
+  e = cudaMemset(c->cnt, 0, sizeof(qem::Counters));
+  if (e != cudaSuccess) {
+    cudaFree(c->ws);
+    delete c;
+    return cuda_fail(e, "cudaMemset");
+  }
+  *out = c;
+  return QEM_OK;
+}
+
+void qem_destroy(qem_ctx* c) {
+  if (!c) return;
+  if (c->graph_valid) cudaGraphExecDestroy(c->graph);
+  if (c->ws) cudaFree(c->ws);
+  delete c;
+}
+
+qem_status qem_bind(qem_ctx* c, const qem_buffers* b) {
+  if (!c || !b) return fail(QEM_INVALID_ARGUMENT, "null argument");
+  const int nlev = c->desc.family == QEM_FAMILY_TWO_LEVEL ? 2 : 3;
+  for (int l = 0; l < nlev; ++l)
+    if (!level_ok(b->level[l])) return fail(QEM_INVALID_ARGUMENT, "level %d has a null buffer", l);
+  if (!b->x || !b->log_pe) return fail(QEM_INVALID_ARGUMENT, "null observation or log_pe buffer");
+  if ((c->desc.obs_kind == QEM_OBS_BERNOULLI_LOGIT || c->desc.obs_kind == QEM_OBS_POISSON_LOG) && !b->y)
+    return fail(QEM_INVALID_ARGUMENT, "null label buffer y");
+  c->bufs = *b;
+  c->bound = 1;
+  if (c->graph_valid) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph_valid = 0;
+  }
+  return QEM_OK;
+}
+
+qem_status qem_sample_q(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (iter < 1 && !d_eps) return fail(QEM_INVALID_ARGUMENT, "iter must be >= 1 in Philox mode");
+  c->launches = 0;
+  cudaError_t e = qem::launch_sample(c, seed, iter < 1 ? 1 : iter, d_eps, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_sample_q");
+}
+
+qem_status qem_estep_forward(qem_ctx* c, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  c->launches = 0;
+  cudaError_t e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_forward(c, (cudaStream_t)stream)
+                                                         : qem::th_forward(c, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_forward");
+}
+
+qem_status qem_reduce_buffer(qem_ctx* c, double** d_buf, int64_t* count) {
+  if (!c || !d_buf || !count) return fail(QEM_INVALID_ARGUMENT, "null argument");
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "three-level has no sharded reduction");
+  *d_buf = c->bufs.plate_sum ? c->bufs.plate_sum : c->tw.red;
+  *count = c->desc.K + 1;
+  return QEM_OK;
+}
+
+qem_status qem_estep_backward(qem_ctx* c, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  c->launches = 0;
+  cudaError_t e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_backward(c, (cudaStream_t)stream)
+                                                         : qem::th_backward(c, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_backward");
+}
+
+qem_status qem_estep(qem_ctx* c, void* stream) {
+  qem_status s = qem_estep_forward(c, stream);
+  if (s) return s;
+  const int64_t l = c->launches;
+  s = qem_estep_backward(c, stream);
+  c->launches += l;
+  return s;
+}
+
+qem_status qem_mstep(qem_ctx* c, int32_t t, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (t < 1) return fail(QEM_INVALID_ARGUMENT, "t must be >= 1");
+  c->launches = 0;
+  cudaError_t e = qem::launch_mstep(c, t, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_mstep");
+}
+
+static cudaError_t iterate_body(qem_ctx* c, uint64_t seed, cudaStream_t st) {
+  struct Guard {
+    qem_ctx* c;
+    ~Guard() { c->in_iterate = 0; }
+  } guard{c};
+  c->in_iterate = 1;
+  cudaError_t e = qem::launch_sample(c, seed, 0, nullptr, st);
+  if (e != cudaSuccess) return e;
+  e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_forward(c, st) : qem::th_forward(c, st);
+  if (e != cudaSuccess) return e;
+  e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_backward(c, st) : qem::th_backward(c, st);
+  if (e != cudaSuccess) return e;
+  return qem::launch_mstep(c, 0, st);
+}
+
+qem_status qem_iterate(qem_ctx* c, int32_t t0, int32_t T, uint64_t seed, int32_t use_graph, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (t0 < 1 || T < 0) return fail(QEM_INVALID_ARGUMENT, "need t0 >= 1 and T >= 0");
+  if (c->g_begin != 0 || c->g_end != c->desc.n)
+    return fail(QEM_UNSUPPORTED, "qem_iterate drives a single-rank context; sharded runs use the phase calls");
+  cudaStream_t st = (cudaStream_t)stream;
+  // device iteration counter and trace base
+  int32_t hdr[2] = {t0, t0};
+  cudaError_t e = cudaMemcpyAsync(&c->cnt->iter, hdr, sizeof hdr, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "qem_iterate: counter upload");
+  e = cudaStreamSynchronize(st);  // hdr is a host stack buffer
+  if (e != cudaSuccess) return cuda_fail(e, "qem_iterate: sync");
+  int64_t per_iter = 0;
+  if (!use_graph) {
+    for (int j = 0; j < T; ++j) {
+      c->launches = 0;
+      e = iterate_body(c, seed, st);
+      if (e != cudaSuccess) return cuda_fail(e, "qem_iterate (eager)");
+      per_iter = c->launches;
+    }
+    c->launches = per_iter * T;
+    return QEM_OK;
+  }
+  if (!c->graph_valid || c->graph_seed_ != seed) {
+    if (c->graph_valid) {
+      cudaGraphExecDestroy(c->graph);
+      c->graph_valid = 0;
+    }
+    cudaStream_t cap;
+    e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "stream create");
+    cudaGraph_t g;
+    e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      c->launches = 0;
+      cudaError_t eb = iterate_body(c, seed, cap);
+      e = cudaStreamEndCapture(cap, &g);
+      if (eb != cudaSuccess) e = eb;
+    }
+    if (e == cudaSuccess) {
+      e = cudaGraphInstantiate(&c->graph, g, 0);
+      cudaGraphDestroy(g);
+    }
+    cudaStreamDestroy(cap);
+    if (e != cudaSuccess) return cuda_fail(e, "qem_iterate: graph capture");
+    c->graph_valid = 1;
+    c->graph_seed_ = seed;
+    c->graph_launches_ = c->launches;
+  }
+  for (int j = 0; j < T; ++j) {
+    e = cudaGraphLaunch(c->graph, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+  }
+  c->launches = c->graph_launches_ * T;
+  return QEM_OK;
+}
+
+qem_status qem_read_flags(qem_ctx* c, void* stream, uint32_t* flags, int64_t* clamps) {
+  if (!c || !flags) return fail(QEM_INVALID_ARGUMENT, "null argument");
+  qem::Counters h;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaMemcpy(&h, c->cnt, sizeof h, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "qem_read_flags");
+  *flags = h.flags;
+  if (clamps) *clamps = (int64_t)h.clamps;
+  uint32_t z = 0;
+  unsigned long long zc = 0;
+  cudaMemcpy(&c->cnt->flags, &z, sizeof z, cudaMemcpyHostToDevice);
+  cudaMemcpy(&c->cnt->clamps, &zc, sizeof zc, cudaMemcpyHostToDevice);
+  return QEM_OK;
+}
+
+int64_t qem_kernel_launches(const qem_ctx* c) { return c ? c->launches : 0; }
+
+qem_status qem_copy_messages(qem_ctx* c, float* d_dg, double* d_c, void* stream) {
+  if (!c || !d_dg || !d_c) return fail(QEM_INVALID_ARGUMENT, "null argument");
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "messages are two-level only");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(d_dg, c->tw.dg, sizeof(float) * c->n_local * c->desc.K, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_c, c->tw.cvec, sizeof(double) * c->n_local, cudaMemcpyDeviceToDevice, st);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_copy_messages");
+}
+
+const char* qem_status_str(qem_status s) {
+  switch (s) {
+    case QEM_OK: return "QEM_OK";
+    case QEM_INVALID_ARGUMENT: return "QEM_INVALID_ARGUMENT";
+    case QEM_INVALID_MODEL: return "QEM_INVALID_MODEL";
+    case QEM_UNSUPPORTED: return "QEM_UNSUPPORTED";
+    case QEM_CUDA_ERROR: return "QEM_CUDA_ERROR";
+  }
+  return "QEM_UNKNOWN_STATUS";
+}
+
+const char* qem_last_error(void) { return g_err; }
+
+const char* qem_version(void) { return "qem-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+// qem_common.cu -- K1 (Q sampler) and K5 (EMA + Gaussian M-step) for every
+// model family.  sm_100a.
+#include "qem_device.cuh"
+#include "qem_internal.h"
+
+namespace qem {
+
+struct SampleLevel {
+  float* z;            // [inst][dims][K]
+  const float* qm;     // [inst*dims]
+  const float* qv;
+  const float* eps;    // [inst*dims][K] or nullptr (Philox)
+  int64_t rows;        // inst*dims
+  int64_t quads_begin; // prefix over levels, in units of 4 samples
+  int dims;
+  int level;
+  int64_t inst_offset; // global instance index of local instance 0
+};
+
+struct SampleArgs {
+  SampleLevel lv[3];
+  int nlev;
+  int K;
+  int quads_per_row;
+  int64_t total_quads;
+  uint2 key;
+  int t_host;
+  const int32_t* d_iter;
+};
+
+// K1: z = fmaf(sqrtf(v), eps, m)  (Alg. 1 line 4; location-scale
+// sampling, App. E; fp32 definition DESIGN.md R22).
+// One thread = 4 consecutive samples k of one latent dim (one Philox call,
+// two Box-Muller pairs).
+__global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= a.total_quads) return;
+  int L = 0;
+#pragma unroll
+  for (int l = 1; l < 3; ++l)
+    if (l < a.nlev && q >= a.lv[l].quads_begin) L = l;
+  const SampleLevel& s = a.lv[L];
+  const int64_t local = q - s.quads_begin;
+  const int64_t row = local / a.quads_per_row;
+  const int k0 = (int)(local - row * a.quads_per_row) * 4;
+  const float m = s.qm[row];
+  const float sd = __fsqrt_rn(s.qv[row]);
+  float e[4];
+  if (s.eps != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e[j] = (k0 + j < a.K) ? s.eps[row * a.K + k0 + j] : 0.f;
+  } else {
+    const int t = resolve_iter(a.t_host, a.d_iter);
+    const int64_t inst = row / s.dims;
+    const int dim = (int)(row - inst * s.dims);
+    const uint32_t ginst = (uint32_t)(inst + s.inst_offset);
+    const uint4 o = philox4x32_10(
+        make_uint4((uint32_t)(k0 >> 2), (uint32_t)dim, ginst, ((uint32_t)s.level << 24) | ((uint32_t)t & 0xffffffu)),
+        a.key);
+    // u = ((x >> 9) + 0.5) * 2^-23, exact in fp32.
+    const float ua = ((float)(o.x >> 9) + 0.5f) * 1.1920928955078125e-07f;
+    const float ub = ((float)(o.y >> 9) + 0.5f) * 1.1920928955078125e-07f;
+    const float uc = ((float)(o.z >> 9) + 0.5f) * 1.1920928955078125e-07f;
+    const float ud = ((float)(o.w >> 9) + 0.5f) * 1.1920928955078125e-07f;
+    const float r0 = sqrtf(-2.f * logf(ua)), r1 = sqrtf(-2.f * logf(uc));
+    float s0, c0, s1, c1;
+    sincospif(2.f * ub, &s0, &c0);
+    sincospif(2.f * ud, &s1, &c1);
+    e[0] = r0 * c0;
+    e[1] = r0 * s0;
+    e[2] = r1 * c1;
+    e[3] = r1 * s1;
+  }
+  float* zr = s.z + row * a.K + k0;
+  if (k0 + 4 <= a.K && (a.K & 3) == 0) {
+    *reinterpret_cast<float4*>(zr) =
+        make_float4(__fmaf_rn(sd, e[0], m), __fmaf_rn(sd, e[1], m), __fmaf_rn(sd, e[2], m), __fmaf_rn(sd, e[3], m));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (k0 + j < a.K) zr[j] = __fmaf_rn(sd, e[j], m);
+  }
+}
+
+cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps, cudaStream_t st) {
+  SampleArgs a{};
+  const int K = c->desc.K;
+  a.K = K;
+  a.quads_per_row = (K + 3) / 4;
+  a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  a.t_host = iter;
+  a.d_iter = &c->cnt->iter;
+  int nlev = c->desc.family == QEM_FAMILY_TWO_LEVEL ? 2 : 3;
+  int64_t quads = 0;
+  for (int l = 0; l < nlev; ++l) {
+    SampleLevel& s = a.lv[l];
+    const qem_level& b = c->bufs.level[l];
+    int64_t inst, dims, off = 0;
+    if (l == 0) {
+      inst = 1;
+      dims = c->R;
+    } else if (c->desc.family == QEM_FAMILY_TWO_LEVEL) {
+      inst = c->n_local;
+      dims = c->desc.d;
+      off = c->g_begin;
+    } else if (l == 1) {
+      inst = c->desc.n;
+      dims = 1;
+    } else {
+      inst = c->desc.n * c->desc.n_sub;
+      dims = 1;
+    }
+    s.z = b.z;
+    s.qm = b.q_mean;
+    s.qv = b.q_var;
+    s.eps = d_eps ? d_eps[l] : nullptr;
+    s.rows = inst * dims;
+    s.dims = (int)dims;
+    s.level = l;
+    s.inst_offset = off;
+    s.quads_begin = quads;
+    quads += s.rows * a.quads_per_row;
+  }
+  a.nlev = nlev;
+  a.total_quads = quads;
+  const int threads = 256;
+  const int64_t blocks = (quads + threads - 1) / threads;
+  if (blocks == 0) return cudaSuccess;
+  k_sample<<<(unsigned)blocks, threads, 0, st>>>(a);
+  c->launches += 1;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ M-step
+
+struct MstepLevel {
+  double* m1;
+  double* v;
+  const double* m1n;
+  const double* vn;
+  float* qm;
+  float* qv;
+  int64_t begin;  // prefix offset
+};
+
+struct MstepArgs {
+  MstepLevel lv[3];
+  int nlev;
+  int64_t total;
+  double new_weight, p, floor_v;
+  int t_host;
+  Counters* cnt;
+};
+
+// K5: EMA over mean parameters (Eq. 9; Alg. 1 line 6) in
+// centred form (R19), then the Gaussian M-step (Alg. 1
+// line 3) with the variance floor (R8).  lambda = history weight (R5).
+__global__ void __launch_bounds__(256) k_mstep(MstepArgs a) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = resolve_iter(a.t_host, &a.cnt->iter);
+  const double lam = a.p > 0.0 ? 1.0 - pow((double)t, -a.p) : 1.0 - a.new_weight;
+  if (e < a.total) {
+    int L = 0;
+#pragma unroll
+    for (int l = 1; l < 3; ++l)
+      if (l < a.nlev && e >= a.lv[l].begin) L = l;
+    const MstepLevel& s = a.lv[L];
+    const int64_t j = e - s.begin;
+    const double m1 = s.m1[j], v = s.v[j], a1 = s.m1n[j], av = s.vn[j];
+    const double d = m1 - a1;
+    const double nm1 = lam * m1 + (1.0 - lam) * a1;
+    const double nv = lam * v + (1.0 - lam) * av + lam * (1.0 - lam) * d * d;
+    s.m1[j] = nm1;
+    s.v[j] = nv;
+    double qv = nv;
+    if (!(nv >= a.floor_v)) {
+      qv = a.floor_v;
+      atomicAdd(&a.cnt->clamps, 1ull);
+      atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_CLAMP);
+    }
+    if (isnan(nm1) || isnan(nv)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+    s.qm[j] = (float)nm1;
+    s.qv[j] = (float)qv;
+  }
+  if (a.t_host <= 0) {
+    // graph mode: the last block advances the device iteration counter.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const uint32_t tk = atomicAdd(&a.cnt->ticket_mstep, 1u);
+      if (tk == gridDim.x - 1) {
+        a.cnt->iter = t + 1;
+        a.cnt->ticket_mstep = 0;
+        __threadfence();
+      }
+    }
+  }
+}
+
+cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t st) {
+  MstepArgs a{};
+  int nlev = c->desc.family == QEM_FAMILY_TWO_LEVEL ? 2 : 3;
+  int64_t tot = 0;
+  for (int l = 0; l < nlev; ++l) {
+    const qem_level& b = c->bufs.level[l];
+    int64_t cnt;
+    if (l == 0)
+      cnt = c->R;
+    else if (c->desc.family == QEM_FAMILY_TWO_LEVEL)
+      cnt = c->n_local * c->desc.d;
+    else if (l == 1)
+      cnt = c->desc.n;
+    else
+      cnt = c->desc.n * c->desc.n_sub;
+    a.lv[l] = MstepLevel{b.ema_m1, b.ema_v, b.m1, b.v, b.q_mean, b.q_var, tot};
+    tot += cnt;
+  }
+  a.nlev = nlev;
+  a.total = tot;
+  a.new_weight = c->opts.new_weight;
+  a.p = c->opts.schedule_p;
+  a.floor_v = c->opts.var_floor;
+  a.t_host = t;
+  a.cnt = c->cnt;
+  const int threads = 256;
+  const int64_t blocks = (tot + threads - 1) / threads;
+  k_mstep<<<(unsigned)(blocks > 0 ? blocks : 1), threads, 0, st>>>(a);
+  c->launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace qem

@@ -1,0 +1,89 @@
+// qem_internal.h -- context layout and launcher prototypes shared by the
+// library's translation units (not part of the public C-ABI, include/qem.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/qem.h"
+
+namespace qem {
+
+// Reference-row data for the differenced forward.
+struct RefInfo {
+  float mu_ref[QEM_MAX_D];  // parent mean of the reference root sample
+  double e_ref;             // 1 / V_ref
+  double bref_const;        // -(d/2)(ln 2pi + ln V_ref)
+  int k_ref;
+  int pad;
+};
+
+// Two-level workspace (device pointers, carved out of one allocation).
+struct TwoLevelWs {
+  float* fwd_coef;    // [K][D+2]   alpha, gamma, c[0..D-1]
+  float* bwd_table;   // [K][RS]    alpha*log2e, gamma*log2e, c*log2e, w_root (RS = pad4(D+3))
+  double* f_root;     // [K]        log p(root^k) - log q(root^k)
+  RefInfo* ref;       // [1]
+  double* partial;    // [grid][K+1] per-CTA plate sums
+  double* red;        // [K+1]      local plate sum (all-reduce buffer)
+  float* dg;          // [n_local][K] Delta g_i(k)
+  float* lnP;         // [n_local][K] ln P_ref,i(k')
+  double* cvec;       // [n_local]  c_i = g_i(k_ref)
+};
+
+struct ThreeLevelWs {
+  double* f_root;  // [K]
+  double* Lab;     // [AB][K kab][K kr]  Poisson table
+  double* Mab;     // [AB][K ka][K kr]
+  double* Ta;      // [A][K kr][K ka]
+  double* ha;      // [A][K]
+  double* red;     // [K+1]
+};
+
+struct Counters {
+  uint32_t ticket_fwd;
+  uint32_t ticket_mstep;
+  uint32_t flags;
+  uint32_t pad;
+  unsigned long long clamps;
+  int32_t iter;        // current iteration t (graph mode)
+  int32_t trace_base;  // t0 of the running qem_iterate
+};
+
+}  // namespace qem
+
+struct qem_ctx {
+  qem_model_desc desc;
+  qem_opts opts;
+  int64_t g_begin, g_end, n_local;
+  int R;  // root dims
+  int grid_fwd;
+  int grid_bwd;
+  void* ws;
+  size_t ws_bytes;
+  qem::TwoLevelWs tw;
+  qem::ThreeLevelWs th;
+  qem::Counters* cnt;
+  qem_buffers bufs;
+  int bound;
+  int64_t launches;
+  cudaGraphExec_t graph;
+  int graph_valid;
+  int in_iterate;
+  uint64_t graph_seed_;
+  int64_t graph_launches_;
+};
+
+namespace qem {
+// two-level launchers (qem_two_level.cu)
+cudaError_t tl_forward(qem_ctx* c, cudaStream_t s);
+cudaError_t tl_backward(qem_ctx* c, cudaStream_t s);
+int tl_supported_d(int d);
+void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* grid_fwd, int* grid_bwd);
+// three-level launchers (qem_three_level.cu)
+cudaError_t th_forward(qem_ctx* c, cudaStream_t s);
+cudaError_t th_backward(qem_ctx* c, cudaStream_t s);
+// common (qem_common.cu)
+cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps,
+                          cudaStream_t s);
+cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t s);
+}  // namespace qem

@@ -1,0 +1,850 @@
+// qem_two_level.cu -- MPIW E-step kernels for two-level plate models (root
+// group -> n groups), sm_100a.  Configs 1, 2, 4, 5.
+//
+// Math (DESIGN.md "Forward" / "Backward"; Eq. 7a-c):
+//   B_i(k,k') = log N(z_i^{k'}; mu^k, V^k I)             (parent->child factor)
+//   A_i(k')   = sum_j log p(x_ij | z_i^{k'}) - log q(z_i^{k'})  (unary, fp64)
+//   g_i(k)    = log (1/K) sum_k' exp(B_i(k,k') + A_i(k'))       (plate message)
+// evaluated reference-differenced around one root sample k_ref:
+//   t_i(k')   = B_i(k_ref,k') + A_i(k')  (fp64),  P_i = softmax(t_i),
+//   c_i       = lse(t_i) - log K  = g_i(k_ref),
+//   D_k(k')   = B(k,k') - B(k_ref,k') = alpha_k + gamma_k |u|^2 + c_k . u,
+//               u = z - mu_ref   (coefficients differenced in fp64, H1)
+//   dg_i(k)   = g_i(k) - c_i = log sum_k' P_i(k') exp(D_k(k'))
+//             = log1p(sum_k' P_i(k') expm1(D_k(k')))   (small |D|: FMA-pipe polynomial)
+// Root:  a(k) = f_root(k) + sum_i dg_i(k);  log Pe = sum_i c_i + lse(a) - log K.
+// Backward: w_i(k') = sum_k w_root(k) exp(ln P_i(k') + D_k(k') - dg_i(k)).
+#include <cstdio>
+
+#include "qem_device.cuh"
+#include "qem_internal.h"
+
+namespace qem {
+
+__host__ __device__ constexpr int pad4(int x) { return (x + 3) & ~3; }
+
+struct TLArgs {
+  int K, J, scale_kind;
+  int64_t n_local;
+  double fixed_var, obs_var, prior_mean, prior_var;
+  const float* z_root;
+  const float* qr_m;
+  const float* qr_v;
+  const float* z;
+  const float* q_m;
+  const float* q_v;
+  const void* x;
+  const void* y;
+  float* w_root;
+  double* m1_root;
+  double* v_root;
+  float* w;
+  double* m1;
+  double* v;
+  double* log_pe;
+  double* trace;
+  int64_t trace_len;
+  int t_host;
+  TwoLevelWs ws;
+  Counters* cnt;
+};
+
+// --------------------------------------------------------------- root prep
+// One block.  Chooses k_ref (root sample nearest Q_root's mean in the
+// Q-metric; ties -> lowest k), builds the differenced row coefficients
+// (fp64 -> fp32) and the root factor f_root(k) = log p(root^k) - log q(root^k).
+template <int D>
+__global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
+  __shared__ double s_val[32];
+  __shared__ int s_idx[32];
+  __shared__ double s_lnv_ref;
+  const int K = a.K, tid = threadIdx.x;
+  const int R = D + (a.scale_kind != QEM_SCALE_FIXED);
+  // k_ref = argmin_k sum_r (z_r^k - m_r)^2 / v_r
+  double best = CUDART_INF;
+  int bidx = 0x7fffffff;
+  for (int k = tid; k < K; k += blockDim.x) {
+    double q = 0.0;
+    for (int r = 0; r < R; ++r) {
+      const double dz = (double)a.z_root[r * K + k] - (double)a.qr_m[r];
+      q += dz * dz / (double)a.qr_v[r];
+    }
+    if (q < best || (q == best && k < bidx)) {
+      best = q;
+      bidx = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ov < best || (ov == best && oi < bidx)) {
+      best = ov;
+      bidx = oi;
+    }
+  }
+  if ((tid & 31) == 0) {
+    s_val[tid >> 5] = best;
+    s_idx[tid >> 5] = bidx;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double bv = s_val[0];
+    int bi = s_idx[0];
+    for (int w = 1; w < (int)((blockDim.x + 31) >> 5); ++w)
+      if (s_val[w] < bv || (s_val[w] == bv && s_idx[w] < bi)) {
+        bv = s_val[w];
+        bi = s_idx[w];
+      }
+    RefInfo* ref = a.ws.ref;
+    ref->k_ref = bi;
+    for (int r = 0; r < D; ++r) ref->mu_ref[r] = a.z_root[r * K + bi];
+    double lnv;
+    if (a.scale_kind == QEM_SCALE_FIXED)
+      lnv = log(a.fixed_var);
+    else if (a.scale_kind == QEM_SCALE_LOGSIGMA)
+      lnv = 2.0 * (double)a.z_root[D * K + bi];
+    else
+      lnv = (double)a.z_root[D * K + bi];
+    s_lnv_ref = lnv;
+    ref->e_ref = exp(-lnv);
+    ref->bref_const = -0.5 * D * (kLn2Pi + lnv);
+  }
+  __syncthreads();
+  const int kref = a.ws.ref->k_ref;
+  const double lnv_ref = s_lnv_ref;
+  const double e_ref = exp(-lnv_ref);
+  constexpr int CW = D + 2;
+  constexpr int RS = pad4(D + 3);
+  for (int k = tid; k < K; k += blockDim.x) {
+    double lnv, dlnv;
+    if (a.scale_kind == QEM_SCALE_FIXED) {
+      lnv = lnv_ref;
+      dlnv = 0.0;
+    } else if (a.scale_kind == QEM_SCALE_LOGSIGMA) {
+      lnv = 2.0 * (double)a.z_root[D * K + k];
+      dlnv = 2.0 * ((double)a.z_root[D * K + k] - (double)a.z_root[D * K + kref]);
+    } else {
+      lnv = (double)a.z_root[D * K + k];
+      dlnv = (double)a.z_root[D * K + k] - (double)a.z_root[D * K + kref];
+    }
+    const double ek = exp(-lnv);
+    double dd = 0.0;
+    float* fc = a.ws.fwd_coef + (size_t)k * CW;
+    float* bt = a.ws.bwd_table + (size_t)k * RS;
+    for (int r = 0; r < D; ++r) {
+      const double del = (double)a.z_root[r * K + k] - (double)a.z_root[r * K + kref];
+      dd += del * del;
+      const double cr = ek * del;
+      fc[2 + r] = (float)cr;
+      bt[2 + r] = (float)(cr * kLog2eD);
+    }
+    const double alpha = -0.5 * D * dlnv - 0.5 * ek * dd;
+    const double gamma = -0.5 * (ek - e_ref);
+    fc[0] = (float)alpha;
+    fc[1] = (float)gamma;
+    bt[0] = (float)(alpha * kLog2eD);
+    bt[1] = (float)(gamma * kLog2eD);
+    double f = 0.0;
+    for (int r = 0; r < R; ++r) {
+      const double v = (double)a.z_root[r * K + k];
+      f += lnN(v, a.prior_mean, a.prior_var) - lnN(v, (double)a.qr_m[r], (double)a.qr_v[r]);
+    }
+    a.ws.f_root[k] = f;
+  }
+}
+
+// ------------------------------------------------------------ forward (K2)
+
+__host__ __device__ constexpr double inv_fact(int n) {
+  double f = 1.0;
+  for (int i = 2; i <= n; ++i) f *= i;
+  return 1.0 / f;
+}
+
+// expm1(x) by its Taylor polynomial of degree N (Horner, FMA pipe).
+template <int N>
+__device__ __forceinline__ float2 expm1_poly(float2 x) {
+  float2 p = f2((float)inv_fact(N));
+#pragma unroll
+  for (int n = N - 1; n >= 1; --n) p = fma2(p, x, f2((float)inv_fact(n)));
+  return mul2(p, x);
+}
+
+template <int D>
+struct FwdLayout {
+  static constexpr int CS = pad4(D + 3);  // u[D], U2, P, lnP
+  __host__ __device__ static size_t bytes(int K, int J) {
+    size_t b = (size_t)K * CS * sizeof(float);      // col
+    b += (size_t)K * sizeof(double);                // tref
+    b += 32 * sizeof(double);                       // scratch
+    b += 3 * QEM_MAX_D * sizeof(double);            // qconst
+    b += 4 * sizeof(double);                        // obs stats
+    b += (size_t)(2 * J + 4) * sizeof(uint32_t);    // bern masks + y
+    return b;
+  }
+};
+
+template <int D, int RP>
+__device__ __forceinline__ float2 pair_D(const float2 (&al)[RP], const float2 (&ga)[RP], const float2 (&cc)[RP][D],
+                                         int p, const float* u, float U2) {
+  if constexpr (D == 1) {
+    return fma2(fma2(ga[p], f2(u[0]), cc[p][0]), f2(u[0]), al[p]);
+  } else {
+    float2 acc = fma2(ga[p], f2(U2), al[p]);
+#pragma unroll
+    for (int r = 0; r < D; ++r) acc = fma2(cc[p][r], f2(u[r]), acc);
+    return acc;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void load_col(const float* cr, float (&u)[D], float& U2, float& P, float& lnP) {
+  constexpr int CS = pad4(D + 3);
+  float buf[CS];
+#pragma unroll
+  for (int q = 0; q < CS / 4; ++q) {
+    const float4 v = reinterpret_cast<const float4*>(cr)[q];
+    buf[4 * q] = v.x;
+    buf[4 * q + 1] = v.y;
+    buf[4 * q + 2] = v.z;
+    buf[4 * q + 3] = v.w;
+  }
+#pragma unroll
+  for (int r = 0; r < D; ++r) u[r] = buf[r];
+  U2 = buf[D];
+  P = buf[D + 1];
+  lnP = buf[D + 2];
+}
+
+// One CTA processes groups i = blockIdx.x, += gridDim.x.  Thread t owns rows
+// k = t + NT*(2p+h) (p < RP row pairs, h = lane of the float2); the row
+// coefficients live in registers for the whole kernel (they depend only on the
+// root samples).  Column data (u, |u|^2, P, ln P) of the current group are in
+// shared memory and read as warp-broadcasts.
+template <int D, int OBS, int RP>
+__global__ void __launch_bounds__(256) k_forward(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int CS = pad4(D + 3);
+  constexpr int CW = D + 2;
+  const int K = a.K, J = a.J, tid = threadIdx.x, NT = blockDim.x;
+  float* col = reinterpret_cast<float*>(smem);
+  double* tref = reinterpret_cast<double*>(col + (size_t)K * CS);
+  double* scratch = tref + K;
+  double* qconst = scratch + 32;  // [3][QEM_MAX_D]
+  double* ostat = qconst + 3 * QEM_MAX_D;
+  uint32_t* bmask = reinterpret_cast<uint32_t*>(ostat + 4);
+  uint32_t* ybits = bmask + J;
+
+  const RefInfo ref = *a.ws.ref;
+  // Row coefficients in registers.
+  float2 al[RP], ga[RP], cc[RP][D];
+  float rb_a[2 * RP], rb_g[2 * RP], rb_c[2 * RP];
+#pragma unroll
+  for (int p = 0; p < RP; ++p) {
+    float av[2], gv[2], cv[2][D];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = tid + NT * (2 * p + h);
+      const bool ok = k < K;
+      const float* fc = a.ws.fwd_coef + (size_t)(ok ? k : 0) * CW;
+      av[h] = ok ? fc[0] : 0.f;
+      gv[h] = ok ? fc[1] : 0.f;
+      float cn = 0.f;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        cv[h][r] = ok ? fc[2 + r] : 0.f;
+        cn = fmaf(cv[h][r], cv[h][r], cn);
+      }
+      rb_a[2 * p + h] = fabsf(av[h]);
+      rb_g[2 * p + h] = fabsf(gv[h]);
+      rb_c[2 * p + h] = sqrtf(cn);
+    }
+    al[p] = make_float2(av[0], av[1]);
+    ga[p] = make_float2(gv[0], gv[1]);
+#pragma unroll
+    for (int r = 0; r < D; ++r) cc[p][r] = make_float2(cv[0][r], cv[1][r]);
+  }
+  double G[2 * RP];
+#pragma unroll
+  for (int j = 0; j < 2 * RP; ++j) G[j] = 0.0;
+  double csum = 0.0;
+  const double logK = log((double)K);
+
+  for (int64_t i = blockIdx.x; i < a.n_local; i += gridDim.x) {
+    __syncthreads();
+    // ---- per-group constants: Q_i (log q) and observation summaries
+    if (tid < D) {
+      const double m = a.q_m[i * D + tid], v = a.q_v[i * D + tid];
+      qconst[tid] = m;
+      qconst[QEM_MAX_D + tid] = 0.5 / v;
+      qconst[2 * QEM_MAX_D + tid] = -0.5 * (kLn2Pi + log(v));
+    }
+    if constexpr (OBS == QEM_OBS_GAUSS) {
+      if (tid < 32) {
+        const float* x = reinterpret_cast<const float*>(a.x) + i * J;
+        double sx = 0.0, sxx = 0.0;
+        for (int j = tid; j < J; j += 32) {
+          const double xv = x[j];
+          sx += xv;
+          sxx += xv * xv;
+        }
+        sx = warp_sum(sx);
+        sxx = warp_sum(sxx);
+        if (tid == 0) {
+          ostat[0] = sx;
+          ostat[1] = sxx;
+        }
+      }
+    } else {
+      const uint8_t* x = reinterpret_cast<const uint8_t*>(a.x) + (size_t)i * J * D;
+      const uint8_t* y = reinterpret_cast<const uint8_t*>(a.y) + (size_t)i * J;
+      for (int j = tid; j < J; j += NT) {
+        uint32_t mk = 0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) mk |= (x[j * D + r] ? 1u : 0u) << r;
+        bmask[j] = mk;
+        ybits[j] = y[j] ? 1u : 0u;
+      }
+    }
+    __syncthreads();
+    // ---- unary terms A_i(k') (fp64) and the reference row t_i(k')
+    double tmax = -CUDART_INF;
+    float u2max = 0.f;
+    for (int kc = tid; kc < K; kc += NT) {
+      float zr[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) zr[r] = a.z[((size_t)i * D + r) * K + kc];
+      double lq = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const double dz = (double)zr[r] - qconst[r];
+        lq += qconst[2 * QEM_MAX_D + r] - dz * dz * qconst[QEM_MAX_D + r];
+      }
+      double ll;
+      if constexpr (OBS == QEM_OBS_GAUSS) {
+        const double zz = zr[0];
+        ll = -0.5 * J * (kLn2Pi + log(a.obs_var)) -
+             (ostat[1] - 2.0 * zz * ostat[0] + (double)J * zz * zz) * (0.5 / a.obs_var);
+      } else {
+        ll = 0.0;
+        for (int j = 0; j < J; ++j) {
+          const uint32_t mk = bmask[j];
+          float eta = 0.f;
+#pragma unroll
+          for (int r = 0; r < D; ++r)
+            if ((mk >> r) & 1u) eta += zr[r];
+          const float sp = fmaxf(eta, 0.f) + log1pf(__expf(-fabsf(eta)));
+          ll += (ybits[j] ? (double)eta : 0.0) - (double)sp;
+        }
+      }
+      float U2 = 0.f;
+      double U2d = 0.0;
+      float* cp = col + (size_t)kc * CS;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const float u = zr[r] - ref.mu_ref[r];
+        cp[r] = u;
+        U2 = fmaf(u, u, U2);
+        U2d += (double)u * (double)u;
+      }
+      cp[D] = U2;
+      const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
+      tref[kc] = t;
+      tmax = fmax(tmax, t);
+      u2max = fmaxf(u2max, U2);
+    }
+    const double M = block_max(tmax, scratch);
+    const float U2max = (float)block_max((double)u2max, scratch);
+    double s = 0.0;
+    for (int kc = tid; kc < K; kc += NT) s += exp(tref[kc] - M);
+    const double S = block_sum(s, scratch);
+    const double logS = log(S);
+    for (int kc = tid; kc < K; kc += NT) {
+      const double lp = tref[kc] - M - logS;
+      float* cp = col + (size_t)kc * CS;
+      cp[D + 1] = (float)exp(lp);
+      cp[D + 2] = (float)lp;
+      a.ws.lnP[(size_t)i * K + kc] = (float)lp;
+    }
+    if (tid == 0) {
+      const double ci = M + logS - logK;
+      a.ws.cvec[i] = ci;
+      csum += ci;
+    }
+    __syncthreads();
+
+    // ---- pair tile: dg_i(k) for the owned rows
+    const float umax = sqrtf(U2max);
+    float tb = 0.f;
+#pragma unroll
+    for (int j = 0; j < 2 * RP; ++j) tb = fmaxf(tb, rb_a[j] + rb_g[j] * U2max + rb_c[j] * umax);
+    float dgv[2 * RP];
+    if (tb <= 0.0625f || tb <= 0.5f) {
+      float2 acc[RP];
+#pragma unroll
+      for (int p = 0; p < RP; ++p) acc[p] = f2(0.f);
+      if (tb <= 0.0625f) {
+#pragma unroll 2
+        for (int kc = 0; kc < K; ++kc) {
+          float u[D], U2, P, lnP;
+          load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
+#pragma unroll
+          for (int p = 0; p < RP; ++p) {
+            const float2 Dv = pair_D<D, RP>(al, ga, cc, p, u, U2);
+            acc[p] = fma2(f2(P), expm1_poly<5>(Dv), acc[p]);
+          }
+        }
+      } else {
+#pragma unroll 2
+        for (int kc = 0; kc < K; ++kc) {
+          float u[D], U2, P, lnP;
+          load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
+#pragma unroll
+          for (int p = 0; p < RP; ++p) {
+            const float2 Dv = pair_D<D, RP>(al, ga, cc, p, u, U2);
+            acc[p] = fma2(f2(P), expm1_poly<9>(Dv), acc[p]);
+          }
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < RP; ++p) {
+        dgv[2 * p] = log1pf(acc[p].x);
+        dgv[2 * p + 1] = log1pf(acc[p].y);
+      }
+    } else {
+      // large |D| (early iterations): exact shifted log-sum-exp, two passes
+      float2 mx[RP];
+#pragma unroll
+      for (int p = 0; p < RP; ++p) mx[p] = f2(-CUDART_INF_F);
+      for (int kc = 0; kc < K; ++kc) {
+        float u[D], U2, P, lnP;
+        load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
+#pragma unroll
+        for (int p = 0; p < RP; ++p) {
+          const float2 t = add2(pair_D<D, RP>(al, ga, cc, p, u, U2), f2(lnP));
+          mx[p] = make_float2(fmaxf(mx[p].x, t.x), fmaxf(mx[p].y, t.y));
+        }
+      }
+      float2 sm[RP];
+      float2 nmx[RP];
+#pragma unroll
+      for (int p = 0; p < RP; ++p) {
+        sm[p] = f2(0.f);
+        nmx[p] = make_float2(-mx[p].x * kLog2e, -mx[p].y * kLog2e);
+      }
+      for (int kc = 0; kc < K; ++kc) {
+        float u[D], U2, P, lnP;
+        load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
+#pragma unroll
+        for (int p = 0; p < RP; ++p) {
+          const float2 t = add2(pair_D<D, RP>(al, ga, cc, p, u, U2), f2(lnP));
+          const float2 e2 = fma2(t, f2(kLog2e), nmx[p]);
+          sm[p] = add2(sm[p], make_float2(ex2(e2.x), ex2(e2.y)));
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < RP; ++p) {
+        dgv[2 * p] = mx[p].x + logf(sm[p].x);
+        dgv[2 * p + 1] = mx[p].y + logf(sm[p].y);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < RP; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = tid + NT * (2 * p + h);
+        if (k < K) {
+          a.ws.dg[(size_t)i * K + k] = dgv[2 * p + h];
+          G[2 * p + h] += (double)dgv[2 * p + h];
+        }
+      }
+  }
+
+  // ---- per-CTA partial plate sums, then the last CTA reduces them in order.
+  double* part = a.ws.partial + (size_t)blockIdx.x * (K + 1);
+#pragma unroll
+  for (int p = 0; p < RP; ++p)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = tid + NT * (2 * p + h);
+      if (k < K) part[k] = G[2 * p + h];
+    }
+  if (tid == 0) part[K] = csum;
+  __threadfence();
+  __syncthreads();
+  __shared__ uint32_t s_last;
+  if (tid == 0) s_last = (atomicAdd(&a.cnt->ticket_fwd, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    for (int k = tid; k <= K; k += NT) {
+      double sum = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(a.ws.partial + (size_t)b * (K + 1) + k);
+      a.ws.red[k] = sum;
+    }
+    if (tid == 0) a.cnt->ticket_fwd = 0;
+  }
+}
+
+// -------------------------------------------------------------- root (K3)
+// One block: w_root = softmax(f_root + G), log Pe, root moments.
+template <int D>
+__global__ void __launch_bounds__(1024) k_root(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* wsh = reinterpret_cast<double*>(smem);  // [K]
+  double* scratch = wsh + a.K;                    // [32]
+  const int K = a.K, tid = threadIdx.x;
+  const int R = D + (a.scale_kind != QEM_SCALE_FIXED);
+  constexpr int RS = pad4(D + 3);
+  double mx = -CUDART_INF;
+  for (int k = tid; k < K; k += blockDim.x) {
+    const double av = a.ws.f_root[k] + a.ws.red[k];
+    wsh[k] = av;
+    mx = fmax(mx, av);
+  }
+  const double M = block_max(mx, scratch);
+  double s = 0.0;
+  for (int k = tid; k < K; k += blockDim.x) s += exp(wsh[k] - M);
+  const double S = block_sum(s, scratch);
+  const double L = M + log(S);
+  const bool degenerate = !(L > -CUDART_INF) || isnan(L);
+  for (int k = tid; k < K; k += blockDim.x) {
+    const double w = exp(wsh[k] - L);
+    wsh[k] = w;
+    a.w_root[k] = (float)w;
+    a.ws.bwd_table[(size_t)k * RS + 2 + D] = (float)w;
+  }
+  if (tid == 0) {
+    const double lp = a.ws.red[K] + L - log((double)K);
+    *a.log_pe = lp;
+    if (a.trace) {
+      const int t = resolve_iter(a.t_host, &a.cnt->iter);
+      const int64_t j = (int64_t)t - a.cnt->trace_base;
+      if (j >= 0 && j < a.trace_len) a.trace[j] = lp;
+    }
+    if (degenerate) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_DEGENERATE);
+    if (isnan(L)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+  }
+  __syncthreads();
+  const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  for (int r = wid; r < R; r += nw) {
+    double s1 = 0.0;
+    for (int k = lane; k < K; k += 32) s1 += wsh[k] * (double)a.z_root[r * K + k];
+    s1 = warp_sum(s1);
+    double s2 = 0.0;
+    for (int k = lane; k < K; k += 32) {
+      const double dz = (double)a.z_root[r * K + k] - s1;
+      s2 += wsh[k] * dz * dz;
+    }
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      a.m1_root[r] = s1;
+      a.v_root[r] = s2;
+    }
+  }
+}
+
+// ----------------------------------------------------------- backward (K4)
+// Thread t owns columns k' = t + NT*(2p+h); the row table (alpha'', gamma',
+// c', w_root) is in shared memory and read as warp-broadcasts.
+template <int D, int CP>
+__global__ void __launch_bounds__(256) k_backward(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int RS = pad4(D + 3);
+  const int K = a.K, tid = threadIdx.x, NT = blockDim.x;
+  float* rows = reinterpret_cast<float*>(smem);          // [K][RS]
+  float* alpha0 = rows + (size_t)K * RS;                 // [K] (padded to even)
+  double* red = reinterpret_cast<double*>(alpha0 + ((K + 1) & ~1));  // [32][D]
+  double* mom = red + 32 * D;                            // [D]
+  for (int e = tid; e < K * RS; e += NT) rows[e] = a.ws.bwd_table[e];
+  for (int k = tid; k < K; k += NT) alpha0[k] = a.ws.bwd_table[(size_t)k * RS];
+  float mur[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) mur[r] = a.ws.ref->mu_ref[r];
+  const int lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
+
+  for (int64_t i = blockIdx.x; i < a.n_local; i += gridDim.x) {
+    __syncthreads();
+    for (int k = tid; k < K; k += NT) rows[(size_t)k * RS] = alpha0[k] - a.ws.dg[(size_t)i * K + k] * kLog2e;
+    float2 u[CP][D], U2[CP], Lc[CP];
+#pragma unroll
+    for (int p = 0; p < CP; ++p) {
+      float uu[2][D], u2[2], lc[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kc = tid + NT * (2 * p + h);
+        const bool ok = kc < K;
+        float acc = 0.f;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          const float zv = ok ? a.z[((size_t)i * D + r) * K + kc] : 0.f;
+          uu[h][r] = zv - mur[r];
+          acc = fmaf(uu[h][r], uu[h][r], acc);
+        }
+        u2[h] = acc;
+        lc[h] = ok ? a.ws.lnP[(size_t)i * K + kc] * kLog2e : -CUDART_INF_F;
+      }
+#pragma unroll
+      for (int r = 0; r < D; ++r) u[p][r] = make_float2(uu[0][r], uu[1][r]);
+      U2[p] = make_float2(u2[0], u2[1]);
+      Lc[p] = make_float2(lc[0], lc[1]);
+    }
+    __syncthreads();
+    float2 acc[CP];
+#pragma unroll
+    for (int p = 0; p < CP; ++p) acc[p] = f2(0.f);
+#pragma unroll 2
+    for (int k = 0; k < K; ++k) {
+      const float* rp = rows + (size_t)k * RS;
+      float rb[RS];
+#pragma unroll
+      for (int q = 0; q < RS / 4; ++q) {
+        const float4 v = reinterpret_cast<const float4*>(rp)[q];
+        rb[4 * q] = v.x;
+        rb[4 * q + 1] = v.y;
+        rb[4 * q + 2] = v.z;
+        rb[4 * q + 3] = v.w;
+      }
+      const float2 w2 = f2(rb[2 + D]);
+#pragma unroll
+      for (int p = 0; p < CP; ++p) {
+        float2 t;
+        if constexpr (D == 1) {
+          t = add2(fma2(fma2(f2(rb[1]), u[p][0], f2(rb[2])), u[p][0], f2(rb[0])), Lc[p]);
+        } else {
+          t = add2(fma2(f2(rb[1]), U2[p], f2(rb[0])), Lc[p]);
+#pragma unroll
+          for (int r = 0; r < D; ++r) t = fma2(f2(rb[2 + r]), u[p][r], t);
+        }
+        acc[p] = fma2(w2, make_float2(ex2(t.x), ex2(t.y)), acc[p]);
+      }
+    }
+    // ---- weights out + moments (fp64)
+    double s1[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) s1[r] = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int p = 0; p < CP; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kc = tid + NT * (2 * p + h);
+        if (kc < K) {
+          const float wv = h ? acc[p].y : acc[p].x;
+          bad |= isnan(wv);
+          a.w[(size_t)i * K + kc] = wv;
+#pragma unroll
+          for (int r = 0; r < D; ++r) s1[r] += (double)wv * (double)a.z[((size_t)i * D + r) * K + kc];
+        }
+      }
+    if (bad) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      const double v = warp_sum(s1[r]);
+      if (lane == 0) red[wid * D + r] = v;
+    }
+    __syncthreads();
+    if (tid < D) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += red[w * D + tid];
+      mom[tid] = t;
+    }
+    __syncthreads();
+    double s2[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) s2[r] = 0.0;
+#pragma unroll
+    for (int p = 0; p < CP; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kc = tid + NT * (2 * p + h);
+        if (kc < K) {
+          const double wv = h ? acc[p].y : acc[p].x;
+#pragma unroll
+          for (int r = 0; r < D; ++r) {
+            const double dz = (double)a.z[((size_t)i * D + r) * K + kc] - mom[r];
+            s2[r] += wv * dz * dz;
+          }
+        }
+      }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      const double v = warp_sum(s2[r]);
+      if (lane == 0) red[wid * D + r] = v;
+    }
+    __syncthreads();
+    if (tid < D) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += red[w * D + tid];
+      a.m1[i * D + tid] = mom[tid];
+      a.v[i * D + tid] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+
+static TLArgs make_args(qem_ctx* c) {
+  TLArgs a{};
+  const qem_model_desc& d = c->desc;
+  a.K = d.K;
+  a.J = d.n_obs;
+  a.scale_kind = d.scale_kind;
+  a.n_local = c->n_local;
+  a.fixed_var = d.fixed_var;
+  a.obs_var = d.obs_var;
+  a.prior_mean = d.prior_mean;
+  a.prior_var = d.prior_var;
+  const qem_level& r = c->bufs.level[0];
+  const qem_level& g = c->bufs.level[1];
+  a.z_root = r.z;
+  a.qr_m = r.q_mean;
+  a.qr_v = r.q_var;
+  a.w_root = r.w;
+  a.m1_root = r.m1;
+  a.v_root = r.v;
+  a.z = g.z;
+  a.q_m = g.q_mean;
+  a.q_v = g.q_var;
+  a.w = g.w;
+  a.m1 = g.m1;
+  a.v = g.v;
+  a.x = c->bufs.x;
+  a.y = c->bufs.y;
+  a.log_pe = c->bufs.log_pe;
+  a.trace = c->in_iterate ? c->bufs.trace : nullptr;
+  a.trace_len = c->bufs.trace_len;
+  a.t_host = 0;
+  a.ws = c->tw;
+  if (c->bufs.plate_sum) a.ws.red = c->bufs.plate_sum;
+  a.cnt = c->cnt;
+  return a;
+}
+
+static int rows_threads(int K, int rp) {
+  int nt = (K + 2 * rp - 1) / (2 * rp);
+  nt = (nt + 31) & ~31;
+  return nt < 32 ? 32 : nt;
+}
+static int pick_rp(int K) { return K >= 512 ? 2 : 1; }
+
+template <int D>
+static size_t bwd_smem(int K) {
+  constexpr int RS = pad4(D + 3);
+  size_t sm = (size_t)K * RS * sizeof(float) + (size_t)((K + 1) & ~1) * sizeof(float) + (32 * D + D) * sizeof(double);
+  return (sm + 15) & ~(size_t)15;
+}
+
+using KernelFn = void (*)(TLArgs);
+
+template <int D, int OBS>
+static KernelFn fwd_fn(int rp) {
+  return rp == 1 ? k_forward<D, OBS, 1> : k_forward<D, OBS, 2>;
+}
+template <int D>
+static KernelFn bwd_fn(int cp) {
+  return cp == 1 ? k_backward<D, 1> : k_backward<D, 2>;
+}
+
+// Resident CTAs per SM for a kernel at (threads, dynamic smem).
+static int occupancy(KernelFn f, int nt, size_t sm) {
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, nt, sm) != cudaSuccess || nb < 1) nb = 1;
+  return nb;
+}
+
+template <int D>
+static void grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb) {
+  const int K = d->K, rp = pick_rp(K);
+  KernelFn ff = d->obs_kind == QEM_OBS_GAUSS ? fwd_fn<D, QEM_OBS_GAUSS>(rp) : fwd_fn<D, QEM_OBS_BERNOULLI_LOGIT>(rp);
+  const int of = occupancy(ff, rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
+  const int ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
+  // Persistent-style grids: one full wave of resident CTAs, capped by the groups.
+  int64_t f = (int64_t)sms * of, b = (int64_t)sms * ob;
+  *gf = (int)(f < n_local ? f : n_local);
+  *gb = (int)(b < n_local ? b : n_local);
+}
+
+template <int D, int OBS>
+static cudaError_t fwd_launch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
+  const int K = a.K, rp = pick_rp(K);
+  fwd_fn<D, OBS>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
+  int nt = (a.K + 31) & ~31;
+  k_root_prep<D><<<1, nt, 0, st>>>(a);
+  c->launches += 2;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (c->desc.obs_kind == QEM_OBS_GAUSS) {
+    if constexpr (D == 1) return fwd_launch<D, QEM_OBS_GAUSS>(c, a, st);
+    return cudaErrorInvalidValue;
+  }
+  return fwd_launch<D, QEM_OBS_BERNOULLI_LOGIT>(c, a, st);
+}
+
+template <int D>
+static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
+  const int K = a.K;
+  const int nt = (K + 31) & ~31;
+  k_root<D><<<1, nt, (size_t)(K + 32) * sizeof(double), st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int cp = pick_rp(K);
+  bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
+  c->launches += 2;
+  return cudaGetLastError();
+}
+
+#define QEM_D_LIST(X) X(1) X(2) X(3) X(4) X(8) X(16) X(18)
+
+int tl_supported_d(int d) {
+#define X(v) if (d == v) return 1;
+  QEM_D_LIST(X)
+#undef X
+  return 0;
+}
+
+void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb) {
+  *gf = *gb = 1;
+  switch (d->d) {
+#define X(v)                              \
+  case v:                                 \
+    grids<v>(d, n_local, sms, gf, gb);    \
+    return;
+    QEM_D_LIST(X)
+#undef X
+  }
+}
+
+cudaError_t tl_forward(qem_ctx* c, cudaStream_t st) {
+  TLArgs a = make_args(c);
+  switch (c->desc.d) {
+#define X(v) \
+  case v:    \
+    return fwd_dispatch_obs<v>(c, a, st);
+    QEM_D_LIST(X)
+#undef X
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t tl_backward(qem_ctx* c, cudaStream_t st) {
+  TLArgs a = make_args(c);
+  switch (c->desc.d) {
+#define X(v) \
+  case v:    \
+    return bwd_dispatch<v>(c, a, st);
+    QEM_D_LIST(X)
+#undef X
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace qem

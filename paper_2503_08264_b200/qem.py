@@ -1,0 +1,211 @@
+"""Python binding of the QEM C-ABI: same names as include/qem.h, argument marshalling only.
+
+Torch supplies device memory and streams; every step of the hot path runs in
+libqem.so kernels.  A ``QEM`` object owns one ``qem_ctx`` and the torch
+buffers bound to it (Q parameters, EMA state, samples, weights, moments,
+observations).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from . import synth
+
+
+def _desc(m) -> _lib.ModelDesc:
+    return _lib.ModelDesc(m.family, m.d if m.family == 2 else 1, m.scale_kind, m.obs_kind, m.n,
+                          m.B, m.J, m.P, m.K, m.fixed_var, m.obs_var, m.top_var, m.sub_var,
+                          m.prior_mean, m.prior_var)
+
+
+def model_validate(m) -> Optional[str]:
+    """None if the model is valid, else the library's one-line reason."""
+    buf = ctypes.create_string_buffer(256)
+    d = _desc(m)
+    st = lib().qem_model_validate(ctypes.byref(d), buf, 256)
+    return None if st == _lib.OK else buf.value.decode()
+
+
+def shard_range(n: int, rank: int, world: int):
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    check(lib().qem_shard_range(n, rank, world, ctypes.byref(b), ctypes.byref(e)), "qem_shard_range")
+    return b.value, e.value
+
+
+def _stream(stream=None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class QEM:
+    """One context over LOCAL level-1 instances [group_begin, group_end)."""
+
+    def __init__(self, m, *, new_weight=0.3, schedule_p=0.0, var_floor=1e-8, group_begin=0, group_end=None,
+                 device="cuda", trace_len=0):
+        if not torch.cuda.is_available():
+            raise _lib.QemError("QEM needs a CUDA device (there is no CPU fallback)")
+        self.m = m
+        self.device = torch.device(device)
+        if group_end is None:
+            group_end = m.n
+        self.g_begin, self.g_end = int(group_begin), int(group_end)
+        self.n_local = self.g_end - self.g_begin
+        d = _desc(m)
+        o = _lib.Opts(new_weight, schedule_p, var_floor)
+        ctx = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(lib().qem_create(ctypes.byref(d), ctypes.byref(o), self.g_begin, self.g_end, ctypes.byref(ctx)),
+                  "qem_create")
+        self.ctx = ctx
+        K = m.K
+        f32 = dict(dtype=torch.float32, device=self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        shapes = synth.latent_shapes(m)
+        if m.family == synth.FAMILY_TWO_LEVEL:
+            shapes = [shapes[0], (self.n_local, m.d)]
+        self.shapes = shapes
+        self.levels = []
+        for inst, dims in shapes:
+            nl = inst * dims
+            lv = dict(q_mean=torch.zeros(nl, **f32), q_var=torch.ones(nl, **f32),
+                      ema_m1=torch.zeros(nl, **f64), ema_v=torch.ones(nl, **f64),
+                      z=torch.zeros(inst, dims, K, **f32), w=torch.zeros(inst, K, **f32),
+                      m1=torch.zeros(nl, **f64), v=torch.zeros(nl, **f64))
+            self.levels.append(lv)
+        self.log_pe = torch.zeros(1, **f64)
+        self.plate_sum = torch.zeros(K + 1, **f64)
+        self.trace = torch.zeros(max(trace_len, 1), **f64)
+        self.x = self.y = None
+        self._bound = False
+
+    # ------------------------------------------------------------ buffers
+    def set_data(self, data: synth.Data) -> None:
+        """Upload the LOCAL shard of the observations (host numpy -> device)."""
+        m, b, e = self.m, self.g_begin, self.g_end
+        dev = self.device
+        if m.obs_kind == synth.OBS_GAUSS:
+            self.x = torch.from_numpy(np.ascontiguousarray(data.xg[b:e], np.float32)).to(dev)
+            self.y = None
+        elif m.obs_kind == synth.OBS_BERNOULLI_LOGIT:
+            self.x = torch.from_numpy(np.ascontiguousarray(data.xb[b:e], np.uint8)).to(dev)
+            self.y = torch.from_numpy(np.ascontiguousarray(data.yb[b:e], np.uint8)).to(dev)
+        else:
+            self.x = torch.from_numpy(np.ascontiguousarray(data.xp, np.float32)).to(dev)
+            self.y = torch.from_numpy(np.ascontiguousarray(data.yp, np.int32)).to(dev)
+        self.bind()
+
+    def bind(self) -> None:
+        b = _lib.Buffers()
+        for l, lv in enumerate(self.levels):
+            b.level[l] = _lib.Level(*[lv[k].data_ptr() for k in ("q_mean", "q_var", "ema_m1", "ema_v", "z", "w",
+                                                                  "m1", "v")])
+        b.x = self.x.data_ptr() if self.x is not None else None
+        b.y = self.y.data_ptr() if self.y is not None else None
+        b.log_pe = self.log_pe.data_ptr()
+        b.trace = self.trace.data_ptr()
+        b.trace_len = self.trace.numel()
+        b.plate_sum = self.plate_sum.data_ptr()
+        check(lib().qem_bind(self.ctx, ctypes.byref(b)), "qem_bind")
+        self._bound = True
+
+    def set_q(self, q: Sequence) -> None:
+        """Q_t per level: (mean [inst*dims], var [inst*dims]) host arrays (local shard for level 1)."""
+        for lv, (qm, qv) in zip(self.levels, self._local(q)):
+            lv["q_mean"].copy_(torch.as_tensor(np.asarray(qm, np.float32)))
+            lv["q_var"].copy_(torch.as_tensor(np.asarray(qv, np.float32)))
+
+    def set_state(self, state: Sequence) -> None:
+        """EMA state per level: (m1, v) fp64 host arrays."""
+        for lv, (a, b) in zip(self.levels, self._local(state)):
+            lv["ema_m1"].copy_(torch.as_tensor(np.asarray(a, np.float64)))
+            lv["ema_v"].copy_(torch.as_tensor(np.asarray(b, np.float64)))
+
+    def set_z(self, z: Sequence) -> None:
+        """Samples per level [inst*dims][K] fp32 host arrays (bypasses the sampler)."""
+        for lv, zz in zip(self.levels, self._local(z)):
+            lv["z"].copy_(torch.as_tensor(np.asarray(zz, np.float32)).reshape(lv["z"].shape))
+
+    def _local(self, per_level):
+        out = list(per_level)
+        if self.m.family == synth.FAMILY_TWO_LEVEL and len(out) > 1:
+            d = self.m.d
+            sl = slice(self.g_begin * d, self.g_end * d)
+
+            def cut(a):
+                if isinstance(a, tuple):
+                    return tuple(np.asarray(x)[sl] for x in a)
+                return np.asarray(a)[sl]
+            out[1] = cut(out[1])
+        return out
+
+    # ---------------------------------------------------------- the C-ABI
+    def sample_q(self, seed: int = 0, iter: int = 1, eps: Optional[Sequence] = None, stream=None) -> None:
+        """K1: z = fmaf(sqrtf(v), eps, m); eps per level (host arrays) or Philox(seed, iter)."""
+        keep = None
+        arr = None
+        if eps is not None:
+            keep = [torch.as_tensor(np.asarray(e, np.float32)).to(self.device).contiguous()
+                    for e in self._local(eps)]
+            arr = (ctypes.c_void_p * 3)(*[t.data_ptr() for t in keep] + [None] * (3 - len(keep)))
+        check(lib().qem_sample_q(self.ctx, seed, iter, arr, _stream(stream)), "qem_sample_q")
+        if keep is not None:
+            torch.cuda.current_stream().synchronize()  # keep eps alive until consumed
+
+    def estep(self, stream=None) -> None:
+        check(lib().qem_estep(self.ctx, _stream(stream)), "qem_estep")
+
+    def estep_forward(self, stream=None) -> None:
+        check(lib().qem_estep_forward(self.ctx, _stream(stream)), "qem_estep_forward")
+
+    def estep_backward(self, stream=None) -> None:
+        check(lib().qem_estep_backward(self.ctx, _stream(stream)), "qem_estep_backward")
+
+    def mstep(self, t: int, stream=None) -> None:
+        check(lib().qem_mstep(self.ctx, t, _stream(stream)), "qem_mstep")
+
+    def iterate(self, t0: int, T: int, seed: int, use_graph: bool = True, stream=None) -> None:
+        if T > self.trace.numel():
+            self.trace = torch.zeros(T, dtype=torch.float64, device=self.device)
+            self.bind()
+        check(lib().qem_iterate(self.ctx, t0, T, seed, int(use_graph), _stream(stream)), "qem_iterate")
+
+    def read_flags(self, stream=None):
+        f, c = ctypes.c_uint32(), ctypes.c_int64()
+        check(lib().qem_read_flags(self.ctx, _stream(stream), ctypes.byref(f), ctypes.byref(c)), "qem_read_flags")
+        return f.value, c.value
+
+    def kernel_launches(self) -> int:
+        return int(lib().qem_kernel_launches(self.ctx))
+
+    def messages(self):
+        """(Delta g [n_local][K] f32, c [n_local] f64) of the last forward (device tensors)."""
+        dg = torch.empty(self.n_local, self.m.K, dtype=torch.float32, device=self.device)
+        c = torch.empty(self.n_local, dtype=torch.float64, device=self.device)
+        check(lib().qem_copy_messages(self.ctx, dg.data_ptr(), c.data_ptr(), _stream()), "qem_copy_messages")
+        return dg, c
+
+    # ---------------------------------------------------------- readback
+    def result(self):
+        """Host copies of the last E-step: log_pe, w / m1 / v per level, plus Q and EMA state."""
+        torch.cuda.current_stream().synchronize()
+        out = dict(log_pe=float(self.log_pe.item()))
+        for key in ("w", "m1", "v", "q_mean", "q_var", "ema_m1", "ema_v", "z"):
+            out[key] = [lv[key].cpu().numpy() for lv in self.levels]
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "ctx", None):
+            lib().qem_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,93 @@
+"""The C-ABI library loads and exports every symbol include/qem.h declares (CPU; no kernel calls).
+
+Also exercises the pure-host entry points (validation, shard ranges) and the
+"fail loudly" contract of the product when the extension is missing.
+"""
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2503_08264_b200 import build
+    build.build()
+    from paper_2503_08264_b200 import _lib
+    return _lib.lib()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "qem.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(qem_[a-z_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    from paper_2503_08264_b200 import _lib
+    decl = declared_functions()
+    assert set(decl) == set(_lib.EXPORTS), set(decl) ^ set(_lib.EXPORTS)
+    for name in decl:
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for name in decl:
+        assert re.search(rf"\bT {name}$", out, re.M), name
+
+
+def test_library_is_sm100a(lib):
+    from paper_2503_08264_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_validate_and_shard_range(lib):
+    from paper_2503_08264_b200 import qem, synth
+    for cid in (1, 2, 3, 4, 5):
+        assert qem.model_validate(synth.config(cid)) is None
+    bad = synth.config(4, K=2000)
+    assert "K=2000" in qem.model_validate(bad)
+    bad = synth.config(1)
+    bad.d = 5
+    assert "d=5" in qem.model_validate(bad) or "OBS_GAUSS" in qem.model_validate(bad)
+    bad = synth.config(2, d=5)
+    assert "no compiled kernel" in qem.model_validate(bad)
+    # shards tile [0, n) exactly, contiguous, balanced within 1
+    for n in (1, 7, 100_000, 10_000):
+        for world in (1, 2, 3, 8):
+            prev = 0
+            sizes = []
+            for r in range(world):
+                b, e = qem.shard_range(n, r, world)
+                assert b == prev
+                prev = e
+                sizes.append(e - b)
+            assert prev == n and max(sizes) - min(sizes) <= 1
+    with pytest.raises(Exception):
+        qem.shard_range(10, 3, 2)
+
+
+def test_product_fails_loudly_without_extension(tmp_path):
+    """With libqem.so absent, the binding raises instead of falling back."""
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "from paper_2503_08264_b200 import _lib\n"
+        "_lib.LIB_PATH = %r\n"
+        "try:\n    _lib.lib()\nexcept _lib.QemError as e:\n    print('RAISED', e)\n" % (ROOT, str(tmp_path / "nope.so")))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True).stdout
+    assert "RAISED" in out
+
+
+def test_product_does_not_import_oracle():
+    """No module of the product package imports, links or executes anything under oracle/."""
+    pkg = os.path.join(ROOT, "paper_2503_08264_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"(^\s*(from|import)\s+oracle\b|liboracle|qem_oracle|orc_)", src, re.M), f
