@@ -28,6 +28,7 @@ struct TwoLevelWs {
   float* dg;          // [n_local][K] Delta g_i(k)
   float* lnP;         // [n_local][K] ln P_ref,i(k')
   double* cvec;       // [n_local]  c_i = g_i(k_ref)
+  int* perm;          // [K]        forward row order (rows sorted by coefficient magnitude)
 };
 
 struct ThreeLevelWs {

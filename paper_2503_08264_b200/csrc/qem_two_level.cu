@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
   __shared__ double s_val[32];
   __shared__ int s_idx[32];
   __shared__ double s_lnv_ref;
+  __shared__ float s_key[QEM_MAX_K];
   const int K = a.K, tid = threadIdx.x;
   const int R = D + (a.scale_kind != QEM_SCALE_FIXED);
   // k_ref = argmin_k sum_r (z_r^k - m_r)^2 / v_r
@@ -151,6 +152,21 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
       f += lnN(v, a.prior_mean, a.prior_var) - lnN(v, (double)a.qr_m[r], (double)a.qr_v[r]);
     }
     a.ws.f_root[k] = f;
+    // sort key: |D| bound at unit column scale
+    float cn = 0.f;
+    for (int r = 0; r < D; ++r) cn = fmaf(fc[2 + r], fc[2 + r], cn);
+    s_key[k] = fabsf(fc[0]) + fabsf(fc[1]) + sqrtf(cn);
+  }
+  __syncthreads();
+  // rank sort (ties by index): perm[rank] = k
+  for (int k = tid; k < K; k += blockDim.x) {
+    const float kk = s_key[k];
+    int rank = 0;
+    for (int j = 0; j < K; ++j) {
+      const float kj = s_key[j];
+      rank += (kj < kk || (kj == kk && j < k)) ? 1 : 0;
+    }
+    a.ws.perm[rank] = k;
   }
 }
 
@@ -171,321 +187,7 @@ __device__ __forceinline__ float2 expm1_poly(float2 x) {
   return mul2(p, x);
 }
 
-template <int D>
-struct FwdLayout {
-  static constexpr int CS = pad4(D + 3);  // u[D], U2, P, lnP
-  __host__ __device__ static size_t bytes(int K, int J) {
-    size_t b = (size_t)K * CS * sizeof(float);      // col
-    b += (size_t)K * sizeof(double);                // tref
-    b += 32 * sizeof(double);                       // scratch
-    b += 3 * QEM_MAX_D * sizeof(double);            // qconst
-    b += 4 * sizeof(double);                        // obs stats
-    b += (size_t)(2 * J + 4) * sizeof(uint32_t);    // bern masks + y
-    return b;
-  }
-};
-
-template <int D, int RP>
-__device__ __forceinline__ float2 pair_D(const float2 (&al)[RP], const float2 (&ga)[RP], const float2 (&cc)[RP][D],
-                                         int p, const float* u, float U2) {
-  if constexpr (D == 1) {
-    return fma2(fma2(ga[p], f2(u[0]), cc[p][0]), f2(u[0]), al[p]);
-  } else {
-    float2 acc = fma2(ga[p], f2(U2), al[p]);
-#pragma unroll
-    for (int r = 0; r < D; ++r) acc = fma2(cc[p][r], f2(u[r]), acc);
-    return acc;
-  }
-}
-
-template <int D>
-__device__ __forceinline__ void load_col(const float* cr, float (&u)[D], float& U2, float& P, float& lnP) {
-  constexpr int CS = pad4(D + 3);
-  float buf[CS];
-#pragma unroll
-  for (int q = 0; q < CS / 4; ++q) {
-    const float4 v = reinterpret_cast<const float4*>(cr)[q];
-    buf[4 * q] = v.x;
-    buf[4 * q + 1] = v.y;
-    buf[4 * q + 2] = v.z;
-    buf[4 * q + 3] = v.w;
-  }
-#pragma unroll
-  for (int r = 0; r < D; ++r) u[r] = buf[r];
-  U2 = buf[D];
-  P = buf[D + 1];
-  lnP = buf[D + 2];
-}
-
-// One CTA processes groups i = blockIdx.x, += gridDim.x.  Thread t owns rows
-// k = t + NT*(2p+h) (p < RP row pairs, h = lane of the float2); the row
-// coefficients live in registers for the whole kernel (they depend only on the
-// root samples).  Column data (u, |u|^2, P, ln P) of the current group are in
-// shared memory and read as warp-broadcasts.
-template <int D, int OBS, int RP>
-__global__ void __launch_bounds__(256) k_forward(TLArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int CS = pad4(D + 3);
-  constexpr int CW = D + 2;
-  const int K = a.K, J = a.J, tid = threadIdx.x, NT = blockDim.x;
-  float* col = reinterpret_cast<float*>(smem);
-  double* tref = reinterpret_cast<double*>(col + (size_t)K * CS);
-  double* scratch = tref + K;
-  double* qconst = scratch + 32;  // [3][QEM_MAX_D]
-  double* ostat = qconst + 3 * QEM_MAX_D;
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(ostat + 4);
-  uint32_t* ybits = bmask + J;
-
-  const RefInfo ref = *a.ws.ref;
-  // Row coefficients in registers.
-  float2 al[RP], ga[RP], cc[RP][D];
-  float rb_a[2 * RP], rb_g[2 * RP], rb_c[2 * RP];
-#pragma unroll
-  for (int p = 0; p < RP; ++p) {
-    float av[2], gv[2], cv[2][D];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = tid + NT * (2 * p + h);
-      const bool ok = k < K;
-      const float* fc = a.ws.fwd_coef + (size_t)(ok ? k : 0) * CW;
-      av[h] = ok ? fc[0] : 0.f;
-      gv[h] = ok ? fc[1] : 0.f;
-      float cn = 0.f;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        cv[h][r] = ok ? fc[2 + r] : 0.f;
-        cn = fmaf(cv[h][r], cv[h][r], cn);
-      }
-      rb_a[2 * p + h] = fabsf(av[h]);
-      rb_g[2 * p + h] = fabsf(gv[h]);
-      rb_c[2 * p + h] = sqrtf(cn);
-    }
-    al[p] = make_float2(av[0], av[1]);
-    ga[p] = make_float2(gv[0], gv[1]);
-#pragma unroll
-    for (int r = 0; r < D; ++r) cc[p][r] = make_float2(cv[0][r], cv[1][r]);
-  }
-  double G[2 * RP];
-#pragma unroll
-  for (int j = 0; j < 2 * RP; ++j) G[j] = 0.0;
-  double csum = 0.0;
-  const double logK = log((double)K);
-
-  for (int64_t i = blockIdx.x; i < a.n_local; i += gridDim.x) {
-    __syncthreads();
-    // ---- per-group constants: Q_i (log q) and observation summaries
-    if (tid < D) {
-      const double m = a.q_m[i * D + tid], v = a.q_v[i * D + tid];
-      qconst[tid] = m;
-      qconst[QEM_MAX_D + tid] = 0.5 / v;
-      qconst[2 * QEM_MAX_D + tid] = -0.5 * (kLn2Pi + log(v));
-    }
-    if constexpr (OBS == QEM_OBS_GAUSS) {
-      if (tid < 32) {
-        const float* x = reinterpret_cast<const float*>(a.x) + i * J;
-        double sx = 0.0, sxx = 0.0;
-        for (int j = tid; j < J; j += 32) {
-          const double xv = x[j];
-          sx += xv;
-          sxx += xv * xv;
-        }
-        sx = warp_sum(sx);
-        sxx = warp_sum(sxx);
-        if (tid == 0) {
-          ostat[0] = sx;
-          ostat[1] = sxx;
-        }
-      }
-    } else {
-      const uint8_t* x = reinterpret_cast<const uint8_t*>(a.x) + (size_t)i * J * D;
-      const uint8_t* y = reinterpret_cast<const uint8_t*>(a.y) + (size_t)i * J;
-      for (int j = tid; j < J; j += NT) {
-        uint32_t mk = 0;
-#pragma unroll
-        for (int r = 0; r < D; ++r) mk |= (x[j * D + r] ? 1u : 0u) << r;
-        bmask[j] = mk;
-        ybits[j] = y[j] ? 1u : 0u;
-      }
-    }
-    __syncthreads();
-    // ---- unary terms A_i(k') (fp64) and the reference row t_i(k')
-    double tmax = -CUDART_INF;
-    float u2max = 0.f;
-    for (int kc = tid; kc < K; kc += NT) {
-      float zr[D];
-#pragma unroll
-      for (int r = 0; r < D; ++r) zr[r] = a.z[((size_t)i * D + r) * K + kc];
-      double lq = 0.0;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        const double dz = (double)zr[r] - qconst[r];
-        lq += qconst[2 * QEM_MAX_D + r] - dz * dz * qconst[QEM_MAX_D + r];
-      }
-      double ll;
-      if constexpr (OBS == QEM_OBS_GAUSS) {
-        const double zz = zr[0];
-        ll = -0.5 * J * (kLn2Pi + log(a.obs_var)) -
-             (ostat[1] - 2.0 * zz * ostat[0] + (double)J * zz * zz) * (0.5 / a.obs_var);
-      } else {
-        ll = 0.0;
-        for (int j = 0; j < J; ++j) {
-          const uint32_t mk = bmask[j];
-          float eta = 0.f;
-#pragma unroll
-          for (int r = 0; r < D; ++r)
-            if ((mk >> r) & 1u) eta += zr[r];
-          const float sp = fmaxf(eta, 0.f) + log1pf(__expf(-fabsf(eta)));
-          ll += (ybits[j] ? (double)eta : 0.0) - (double)sp;
-        }
-      }
-      float U2 = 0.f;
-      double U2d = 0.0;
-      float* cp = col + (size_t)kc * CS;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        const float u = zr[r] - ref.mu_ref[r];
-        cp[r] = u;
-        U2 = fmaf(u, u, U2);
-        U2d += (double)u * (double)u;
-      }
-      cp[D] = U2;
-      const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
-      tref[kc] = t;
-      tmax = fmax(tmax, t);
-      u2max = fmaxf(u2max, U2);
-    }
-    const double M = block_max(tmax, scratch);
-    const float U2max = (float)block_max((double)u2max, scratch);
-    double s = 0.0;
-    for (int kc = tid; kc < K; kc += NT) s += exp(tref[kc] - M);
-    const double S = block_sum(s, scratch);
-    const double logS = log(S);
-    for (int kc = tid; kc < K; kc += NT) {
-      const double lp = tref[kc] - M - logS;
-      float* cp = col + (size_t)kc * CS;
-      cp[D + 1] = (float)exp(lp);
-      cp[D + 2] = (float)lp;
-      a.ws.lnP[(size_t)i * K + kc] = (float)lp;
-    }
-    if (tid == 0) {
-      const double ci = M + logS - logK;
-      a.ws.cvec[i] = ci;
-      csum += ci;
-    }
-    __syncthreads();
-
-    // ---- pair tile: dg_i(k) for the owned rows
-    const float umax = sqrtf(U2max);
-    float tb = 0.f;
-#pragma unroll
-    for (int j = 0; j < 2 * RP; ++j) tb = fmaxf(tb, rb_a[j] + rb_g[j] * U2max + rb_c[j] * umax);
-    float dgv[2 * RP];
-    if (tb <= 0.0625f || tb <= 0.5f) {
-      float2 acc[RP];
-#pragma unroll
-      for (int p = 0; p < RP; ++p) acc[p] = f2(0.f);
-      if (tb <= 0.0625f) {
-#pragma unroll 2
-        for (int kc = 0; kc < K; ++kc) {
-          float u[D], U2, P, lnP;
-          load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
-#pragma unroll
-          for (int p = 0; p < RP; ++p) {
-            const float2 Dv = pair_D<D, RP>(al, ga, cc, p, u, U2);
-            acc[p] = fma2(f2(P), expm1_poly<5>(Dv), acc[p]);
-          }
-        }
-      } else {
-#pragma unroll 2
-        for (int kc = 0; kc < K; ++kc) {
-          float u[D], U2, P, lnP;
-          load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
-#pragma unroll
-          for (int p = 0; p < RP; ++p) {
-            const float2 Dv = pair_D<D, RP>(al, ga, cc, p, u, U2);
-            acc[p] = fma2(f2(P), expm1_poly<9>(Dv), acc[p]);
-          }
-        }
-      }
-#pragma unroll
-      for (int p = 0; p < RP; ++p) {
-        dgv[2 * p] = log1pf(acc[p].x);
-        dgv[2 * p + 1] = log1pf(acc[p].y);
-      }
-    } else {
-      // large |D| (early iterations): exact shifted log-sum-exp, two passes
-      float2 mx[RP];
-#pragma unroll
-      for (int p = 0; p < RP; ++p) mx[p] = f2(-CUDART_INF_F);
-      for (int kc = 0; kc < K; ++kc) {
-        float u[D], U2, P, lnP;
-        load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
-#pragma unroll
-        for (int p = 0; p < RP; ++p) {
-          const float2 t = add2(pair_D<D, RP>(al, ga, cc, p, u, U2), f2(lnP));
-          mx[p] = make_float2(fmaxf(mx[p].x, t.x), fmaxf(mx[p].y, t.y));
-        }
-      }
-      float2 sm[RP];
-      float2 nmx[RP];
-#pragma unroll
-      for (int p = 0; p < RP; ++p) {
-        sm[p] = f2(0.f);
-        nmx[p] = make_float2(-mx[p].x * kLog2e, -mx[p].y * kLog2e);
-      }
-      for (int kc = 0; kc < K; ++kc) {
-        float u[D], U2, P, lnP;
-        load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
-#pragma unroll
-        for (int p = 0; p < RP; ++p) {
-          const float2 t = add2(pair_D<D, RP>(al, ga, cc, p, u, U2), f2(lnP));
-          const float2 e2 = fma2(t, f2(kLog2e), nmx[p]);
-          sm[p] = add2(sm[p], make_float2(ex2(e2.x), ex2(e2.y)));
-        }
-      }
-#pragma unroll
-      for (int p = 0; p < RP; ++p) {
-        dgv[2 * p] = mx[p].x + logf(sm[p].x);
-        dgv[2 * p + 1] = mx[p].y + logf(sm[p].y);
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < RP; ++p)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int k = tid + NT * (2 * p + h);
-        if (k < K) {
-          a.ws.dg[(size_t)i * K + k] = dgv[2 * p + h];
-          G[2 * p + h] += (double)dgv[2 * p + h];
-        }
-      }
-  }
-
-  // ---- per-CTA partial plate sums, then the last CTA reduces them in order.
-  double* part = a.ws.partial + (size_t)blockIdx.x * (K + 1);
-#pragma unroll
-  for (int p = 0; p < RP; ++p)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = tid + NT * (2 * p + h);
-      if (k < K) part[k] = G[2 * p + h];
-    }
-  if (tid == 0) part[K] = csum;
-  __threadfence();
-  __syncthreads();
-  __shared__ uint32_t s_last;
-  if (tid == 0) s_last = (atomicAdd(&a.cnt->ticket_fwd, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    for (int k = tid; k <= K; k += NT) {
-      double sum = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(a.ws.partial + (size_t)b * (K + 1) + k);
-      a.ws.red[k] = sum;
-    }
-    if (tid == 0) a.cnt->ticket_fwd = 0;
-  }
-}
+#include "qem_forward.cuh"
 
 // -------------------------------------------------------------- root (K3)
 // One block: w_root = softmax(f_root + G), log Pe, root moments.
