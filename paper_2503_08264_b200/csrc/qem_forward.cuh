@@ -1,33 +1,39 @@
-// qem_forward.cuh -- K2: fused unary terms + pair-tile forward log-sum-exp for
-// two-level models (included by qem_two_level.cu; needs TLArgs, pad4, inv_fact).
+// qem_forward.cuh -- K2: unary terms + pair-tile forward log-sum-exp for
+// two-level models (included inside namespace qem by qem_two_level.cu; needs
+// TLArgs, pad4, inv_fact, expm1_poly).
 //
-// Per group i (one CTA at a time, persistent grid):
-//  prep   columns k': A_i(k') = loglik - log q (fp64), u = z - mu_ref, |u|^2,
-//         t_i(k') = B(k_ref,k') + A_i(k') (fp64), c_i = lse t_i - log K,
-//         P_i = softmax t_i (fp32 in SMEM), ln P_i (-> HBM for the backward).
-//  tile   rows k (registers, sorted by coefficient magnitude so a warp's rows
-//         share a mode): dg_i(k) = log sum_k' P_i(k') exp(D_k(k')), by
-//           mode 0: log1p(sum P expm1_5(D))   bound(|D|) <= 1/16
-//           mode 1: log1p(sum P expm1_9(D))   bound(|D|) <= 1/2
-//           mode 2: single-pass online log-sum-exp of D + ln P (ex2 on the SFU)
-//         The mode is warp-uniform (max over the warp's rows).
+// K2a k_colprep  (one warp per group, persistent): for every column k'
+//     A_i(k') = sum_j log p(x_ij|z^k') - log q(z^k')            (fp64)
+//     t_i(k') = B(k_ref,k') + A_i(k')                            (fp64)
+//     c_i = lse_k' t_i - log K;  P_i = softmax t_i;  u = z - mu_ref
+//   -> column record colrec[i][k'] = {u[D], |u|^2, P_i, ln P_i} (fp32),
+//      cvec[i] = c_i, gstat[i] = max |u|^2.
+// K2b k_forward  (persistent, TMA double-buffered): the group's column
+//   records arrive in shared memory by cp.async.bulk (mbarrier completion)
+//   while the previous group's tile is computed; rows k live in registers
+//   (sorted by coefficient magnitude so a warp's rows share a mode):
+//     dg_i(k) = log sum_k' P_i(k') exp(D_k(k')), by
+//       mode 0: log1p(sum P expm1_5(D))   bound(|D|) <= 1/16
+//       mode 1: log1p(sum P expm1_9(D))   bound(|D|) <= 1/2
+//       mode 2: single-pass online log-sum-exp of D + ln P (ex2 on the SFU)
+//   The mode is warp-uniform (max over the warp's rows).
 #pragma once
-// (included inside namespace qem)
 
 template <int D>
 struct FwdLayout {
   static constexpr int CS = pad4(D + 3);  // u[D], U2, P, lnP
   static constexpr int CH = 4;            // column chunk of the online log-sum-exp
   __host__ __device__ static int kpad(int K) { return (K + CH - 1) / CH * CH; }
-  __host__ __device__ static size_t bytes(int K, int J) {
-    size_t b = (size_t)kpad(K) * CS * sizeof(float);  // col
-    b += (size_t)K * sizeof(double);                  // tref
-    b += 32 * sizeof(double);                         // scratch
-    b += 3 * QEM_MAX_D * sizeof(double);              // qconst
-    b += 4 * sizeof(double);                          // obs stats
-    b += (size_t)(2 * J + 4) * sizeof(uint32_t);      // bern masks + y
-    return b;
+  __host__ __device__ static size_t stage_bytes(int K) { return (size_t)kpad(K) * CS * sizeof(float); }
+  // k_forward: two stages + two mbarriers
+  __host__ __device__ static size_t bytes(int K, int /*J*/) { return 2 * stage_bytes(K) + 16; }
+  // k_colprep, per warp: tref[K] + qconst[3][D] + bern masks/labels [2J]
+  __host__ __device__ static size_t prep_warp_bytes(int K, int J) {
+    size_t b = (size_t)K * sizeof(double) + 3 * D * sizeof(double) + (size_t)2 * J * sizeof(uint32_t);
+    return (b + 15) & ~(size_t)15;
   }
+  static constexpr int PREP_WARPS = 8;
+  __host__ __device__ static size_t prep_bytes(int K, int J) { return PREP_WARPS * prep_warp_bytes(K, J); }
 };
 
 template <int D, int RP>
@@ -137,27 +143,149 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
   }
 }
 
-// One CTA processes groups i = blockIdx.x, += gridDim.x.  Thread t owns the
-// row slots s = 2(t*RP+p)+h (p < RP float2 pairs), i.e. rows k = perm[s];
-// the row coefficients stay in registers for the whole kernel (they depend
-// only on the root samples).  Column data (u, |u|^2, P, ln P) of the current
-// group sit in shared memory and are read as warp-broadcasts.
-template <int D, int OBS, int RP>
+// ------------------------------------------------------------------ K2a
+// One WARP per group (warp-shuffle reductions only, no block barriers); the
+// CTA's warps work on different groups.
+template <int D, int OBS>
+__global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int CS = pad4(D + 3);
+  const int K = a.K, J = a.J, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int Kp = FwdLayout<D>::kpad(K);
+  unsigned char* wbase = smem + (size_t)wid * FwdLayout<D>::prep_warp_bytes(K, J);
+  double* tref = reinterpret_cast<double*>(wbase);      // [K]
+  double* qconst = tref + K;                            // [3][D]
+  uint32_t* bmask = reinterpret_cast<uint32_t*>(qconst + 3 * D);  // [J]
+  uint32_t* ybits = bmask + J;                          // [J]
+  const RefInfo ref = *a.ws.ref;
+  const double logK = log((double)K);
+  double gc0 = 0.0, gc1 = 0.0;
+  if constexpr (OBS == QEM_OBS_GAUSS) {
+    gc0 = -0.5 * J * (kLn2Pi + log(a.obs_var));
+    gc1 = 0.5 / a.obs_var;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * nwarps + wid; i < a.n_local; i += (int64_t)gridDim.x * nwarps) {
+    __syncwarp();
+    if (lane < D) {
+      const double m = a.q_m[i * D + lane], v = a.q_v[i * D + lane];
+      qconst[lane] = m;
+      qconst[D + lane] = 0.5 / v;
+      qconst[2 * D + lane] = -0.5 * (kLn2Pi + log(v));
+    }
+    double sx = 0.0, sxx = 0.0;
+    if constexpr (OBS == QEM_OBS_GAUSS) {
+      const float* x = reinterpret_cast<const float*>(a.x) + i * J;
+      for (int j = lane; j < J; j += 32) {
+        const double xv = x[j];
+        sx += xv;
+        sxx += xv * xv;
+      }
+      sx = warp_sum(sx);
+      sxx = warp_sum(sxx);
+    } else {
+      const uint8_t* x = reinterpret_cast<const uint8_t*>(a.x) + (size_t)i * J * D;
+      const uint8_t* y = reinterpret_cast<const uint8_t*>(a.y) + (size_t)i * J;
+      for (int j = lane; j < J; j += 32) {
+        uint32_t mk = 0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) mk |= (x[j * D + r] ? 1u : 0u) << r;
+        bmask[j] = mk;
+        ybits[j] = y[j] ? 1u : 0u;
+      }
+    }
+    __syncwarp();
+    float* rec0 = a.ws.colrec + (size_t)i * Kp * CS;
+    double tmax = -CUDART_INF;
+    float u2max = 0.f;
+    for (int kc = lane; kc < K; kc += 32) {
+      float zr[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) zr[r] = a.z[((size_t)i * D + r) * K + kc];
+      double lq = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const double dz = (double)zr[r] - qconst[r];
+        lq += qconst[2 * D + r] - dz * dz * qconst[D + r];
+      }
+      double ll;
+      if constexpr (OBS == QEM_OBS_GAUSS) {
+        const double zz = zr[0];
+        ll = gc0 - (sxx - 2.0 * zz * sx + (double)J * zz * zz) * gc1;
+      } else {
+        ll = 0.0;
+        for (int j = 0; j < J; ++j) {
+          const uint32_t mk = bmask[j];
+          float eta = 0.f;
+#pragma unroll
+          for (int r = 0; r < D; ++r)
+            if ((mk >> r) & 1u) eta += zr[r];
+          const float sp = fmaxf(eta, 0.f) + log1pf(__expf(-fabsf(eta)));
+          ll += (ybits[j] ? (double)eta : 0.0) - (double)sp;
+        }
+      }
+      float rec[CS];
+      float U2 = 0.f;
+      double U2d = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const float u = zr[r] - ref.mu_ref[r];
+        rec[r] = u;
+        U2 = fmaf(u, u, U2);
+        U2d += (double)u * (double)u;
+      }
+#pragma unroll
+      for (int r = D; r < CS; ++r) rec[r] = 0.f;
+      rec[D] = U2;
+      float4* dst = reinterpret_cast<float4*>(rec0 + (size_t)kc * CS);
+#pragma unroll
+      for (int q = 0; q < CS / 4; ++q)
+        dst[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
+      const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
+      tref[kc] = t;
+      tmax = fmax(tmax, t);
+      u2max = fmaxf(u2max, U2);
+    }
+    // padding columns: P = 0, ln P = -inf (contribute nothing)
+    for (int kc = K + lane; kc < Kp; kc += 32) {
+      float4* dst = reinterpret_cast<float4*>(rec0 + (size_t)kc * CS);
+#pragma unroll
+      for (int q = 0; q < CS / 4; ++q) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      rec0[(size_t)kc * CS + D + 2] = -CUDART_INF_F;
+    }
+    const double M = warp_max(tmax);
+    const float U2max = warp_maxf(u2max);
+    double s = 0.0;
+    for (int kc = lane; kc < K; kc += 32) s += (double)expf((float)(tref[kc] - M));
+    const double logS = log(warp_sum(s));
+    for (int kc = lane; kc < K; kc += 32) {
+      const float lp = (float)(tref[kc] - M - logS);
+      float* pc = rec0 + (size_t)kc * CS;
+      pc[D + 1] = expf(lp);
+      pc[D + 2] = lp;
+    }
+    if (lane == 0) {
+      a.ws.cvec[i] = M + logS - logK;
+      a.ws.gstat[i] = U2max;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K2b
+// Thread t owns the row slots s = 2(t*RP+p)+h (p < RP float2 pairs), i.e.
+// rows k = perm[s]; the row coefficients stay in registers for the whole
+// kernel (they depend only on the root samples).
+template <int D, int RP>
 __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int CS = pad4(D + 3);
   constexpr int CW = D + 2;
-  const int K = a.K, J = a.J, tid = threadIdx.x, NT = blockDim.x;
+  const int K = a.K, tid = threadIdx.x;
   const int Kp = FwdLayout<D>::kpad(K);
-  float* col = reinterpret_cast<float*>(smem);
-  double* tref = reinterpret_cast<double*>(col + (size_t)Kp * CS);
-  double* scratch = tref + K;
-  double* qconst = scratch + 32;  // [3][QEM_MAX_D]
-  double* ostat = qconst + 3 * QEM_MAX_D;
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(ostat + 4);
-  uint32_t* ybits = bmask + J;
+  const uint32_t sbytes = (uint32_t)FwdLayout<D>::stage_bytes(K);
+  float* stage[2] = {reinterpret_cast<float*>(smem), reinterpret_cast<float*>(smem + sbytes)};
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sbytes);
 
-  const RefInfo ref = *a.ws.ref;
   // Row coefficients in registers.
   float2 al[RP], ga[RP], cc[RP][D];
   float rb_a[2 * RP], rb_g[2 * RP], rb_c[2 * RP];
@@ -193,123 +321,38 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
 #pragma unroll
   for (int j = 0; j < 2 * RP; ++j) G[j] = 0.0;
   double csum = 0.0;
-  const double logK = log((double)K);
-  // padding columns contribute nothing: P = 0, ln P = -inf
-  for (int kc = K + tid; kc < Kp; kc += NT) {
-    float* cp = col + (size_t)kc * CS;
-    for (int r = 0; r < CS; ++r) cp[r] = 0.f;
-    cp[D + 2] = -CUDART_INF_F;
-  }
 
-  for (int64_t i = blockIdx.x; i < a.n_local; i += gridDim.x) {
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t i0 = blockIdx.x;
+  if (tid == 0 && i0 < a.n_local) {
+    mbar_expect_tx(&bar[0], sbytes);
+    tma_bulk_g2s(stage[0], a.ws.colrec + (size_t)i0 * Kp * CS, sbytes, &bar[0]);
+  }
+  int j = 0;
+  for (int64_t i = i0; i < a.n_local; i += gridDim.x, ++j) {
+    const int st = j & 1;
+    // all warps are done with the other stage (group j-1): refill it with group j+1
     __syncthreads();
-    // ---- per-group constants: Q_i (log q) and observation summaries
-    if (tid < D) {
-      const double m = a.q_m[i * D + tid], v = a.q_v[i * D + tid];
-      qconst[tid] = m;
-      qconst[QEM_MAX_D + tid] = 0.5 / v;
-      qconst[2 * QEM_MAX_D + tid] = -0.5 * (kLn2Pi + log(v));
+    const int64_t inext = i + gridDim.x;
+    if (tid == 0 && inext < a.n_local) {
+      mbar_expect_tx(&bar[st ^ 1], sbytes);
+      tma_bulk_g2s(stage[st ^ 1], a.ws.colrec + (size_t)inext * Kp * CS, sbytes, &bar[st ^ 1]);
     }
-    if constexpr (OBS == QEM_OBS_GAUSS) {
-      if (tid < 32) {
-        const float* x = reinterpret_cast<const float*>(a.x) + i * J;
-        double sx = 0.0, sxx = 0.0;
-        for (int j = tid; j < J; j += 32) {
-          const double xv = x[j];
-          sx += xv;
-          sxx += xv * xv;
-        }
-        sx = warp_sum(sx);
-        sxx = warp_sum(sxx);
-        if (tid == 0) {
-          ostat[0] = sx;
-          ostat[1] = sxx;
-          ostat[2] = -0.5 * J * (kLn2Pi + log(a.obs_var));
-          ostat[3] = 0.5 / a.obs_var;
-        }
-      }
-    } else {
-      const uint8_t* x = reinterpret_cast<const uint8_t*>(a.x) + (size_t)i * J * D;
-      const uint8_t* y = reinterpret_cast<const uint8_t*>(a.y) + (size_t)i * J;
-      for (int j = tid; j < J; j += NT) {
-        uint32_t mk = 0;
-#pragma unroll
-        for (int r = 0; r < D; ++r) mk |= (x[j * D + r] ? 1u : 0u) << r;
-        bmask[j] = mk;
-        ybits[j] = y[j] ? 1u : 0u;
-      }
-    }
-    __syncthreads();
-    // ---- unary terms A_i(k') (fp64) and the reference row t_i(k')
-    double tmax = -CUDART_INF;
-    float u2max = 0.f;
-    for (int kc = tid; kc < K; kc += NT) {
-      float zr[D];
-#pragma unroll
-      for (int r = 0; r < D; ++r) zr[r] = a.z[((size_t)i * D + r) * K + kc];
-      double lq = 0.0;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        const double dz = (double)zr[r] - qconst[r];
-        lq += qconst[2 * QEM_MAX_D + r] - dz * dz * qconst[QEM_MAX_D + r];
-      }
-      double ll;
-      if constexpr (OBS == QEM_OBS_GAUSS) {
-        const double zz = zr[0];
-        ll = ostat[2] - (ostat[1] - 2.0 * zz * ostat[0] + (double)J * zz * zz) * ostat[3];
-      } else {
-        ll = 0.0;
-        for (int j = 0; j < J; ++j) {
-          const uint32_t mk = bmask[j];
-          float eta = 0.f;
-#pragma unroll
-          for (int r = 0; r < D; ++r)
-            if ((mk >> r) & 1u) eta += zr[r];
-          const float sp = fmaxf(eta, 0.f) + log1pf(__expf(-fabsf(eta)));
-          ll += (ybits[j] ? (double)eta : 0.0) - (double)sp;
-        }
-      }
-      float U2 = 0.f;
-      double U2d = 0.0;
-      float* cp = col + (size_t)kc * CS;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        const float u = zr[r] - ref.mu_ref[r];
-        cp[r] = u;
-        U2 = fmaf(u, u, U2);
-        U2d += (double)u * (double)u;
-      }
-      cp[D] = U2;
-      const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
-      tref[kc] = t;
-      tmax = fmax(tmax, t);
-      u2max = fmaxf(u2max, U2);
-    }
-    const double M = block_max(tmax, scratch);
-    const float U2max = (float)block_max((double)u2max, scratch);
-    double s = 0.0;
-    for (int kc = tid; kc < K; kc += NT) s += (double)expf((float)(tref[kc] - M));
-    const double S = block_sum(s, scratch);
-    const double logS = log(S);
-    for (int kc = tid; kc < K; kc += NT) {
-      const float lp = (float)(tref[kc] - M - logS);
-      float* cp = col + (size_t)kc * CS;
-      cp[D + 1] = expf(lp);
-      cp[D + 2] = lp;
-      a.ws.lnP[(size_t)i * K + kc] = lp;
-    }
-    if (tid == 0) {
-      const double ci = M + logS - logK;
-      a.ws.cvec[i] = ci;
-      csum += ci;
-    }
-    __syncthreads();
+    const float U2max = a.ws.gstat[i];
+    if (tid == 0) csum += a.ws.cvec[i];
+    mbar_wait(&bar[st], (uint32_t)((j >> 1) & 1));
+    const float* col = stage[st];
 
     // ---- pair tile: dg_i(k) for the owned rows, warp-uniform mode
     const float umax = sqrtf(U2max);
     float tb = 0.f;
 #pragma unroll
-    for (int j = 0; j < 2 * RP; ++j) tb = fmaxf(tb, rb_a[j] + rb_g[j] * U2max + rb_c[j] * umax);
+    for (int q = 0; q < 2 * RP; ++q) tb = fmaxf(tb, rb_a[q] + rb_g[q] * U2max + rb_c[q] * umax);
     int md = tb <= 0.0625f ? 0 : (tb <= 0.5f ? 1 : 2);
     md = __reduce_max_sync(0xffffffffu, md);
     float dgv[2 * RP];
@@ -320,10 +363,10 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
     else
       tile_online<D, RP>(col, Kp, al, ga, cc, dgv);
 #pragma unroll
-    for (int j = 0; j < 2 * RP; ++j) {
-      if (kid[j] >= 0) {
-        a.ws.dg[(size_t)i * K + kid[j]] = dgv[j];
-        G[j] += (double)dgv[j];
+    for (int q = 0; q < 2 * RP; ++q) {
+      if (kid[q] >= 0) {
+        a.ws.dg[(size_t)i * K + kid[q]] = dgv[q];
+        G[q] += (double)dgv[q];
       }
     }
   }
@@ -331,8 +374,8 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
   // ---- per-CTA partial plate sums, then the last CTA reduces them in order.
   double* part = a.ws.partial + (size_t)blockIdx.x * (K + 1);
 #pragma unroll
-  for (int j = 0; j < 2 * RP; ++j)
-    if (kid[j] >= 0) part[kid[j]] = G[j];
+  for (int q = 0; q < 2 * RP; ++q)
+    if (kid[q] >= 0) part[kid[q]] = G[q];
   if (tid == 0) part[K] = csum;
   __threadfence();
   __syncthreads();
@@ -341,7 +384,7 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
   __syncthreads();
   if (s_last) {
     __threadfence();
-    for (int k = tid; k <= K; k += NT) {
+    for (int k = tid; k <= K; k += blockDim.x) {
       double sum = 0.0;
       for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(a.ws.partial + (size_t)b * (K + 1) + k);
       a.ws.red[k] = sum;
@@ -349,4 +392,3 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
     if (tid == 0) a.cnt->ticket_fwd = 0;
   }
 }
-

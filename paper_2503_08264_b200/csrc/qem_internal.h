@@ -26,7 +26,8 @@ struct TwoLevelWs {
   double* partial;    // [grid][K+1] per-CTA plate sums
   double* red;        // [K+1]      local plate sum (all-reduce buffer)
   float* dg;          // [n_local][K] Delta g_i(k)
-  float* lnP;         // [n_local][K] ln P_ref,i(k')
+  float* colrec;      // [n_local][Kp][pad4(D+3)] column records u[D], |u|^2, P_i, ln P_i
+  float* gstat;       // [n_local]  max_k' |u|^2 (forward mode bound)
   double* cvec;       // [n_local]  c_i = g_i(k_ref)
   int* perm;          // [K]        forward row order (rows sorted by coefficient magnitude)
 };
@@ -59,6 +60,7 @@ struct qem_ctx {
   int R;  // root dims
   int grid_fwd;
   int grid_bwd;
+  int grid_prep;
   void* ws;
   size_t ws_bytes;
   qem::TwoLevelWs tw;
@@ -79,7 +81,7 @@ namespace qem {
 cudaError_t tl_forward(qem_ctx* c, cudaStream_t s);
 cudaError_t tl_backward(qem_ctx* c, cudaStream_t s);
 int tl_supported_d(int d);
-void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* grid_fwd, int* grid_bwd);
+void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* grid_fwd, int* grid_bwd, int* grid_prep);
 // three-level launchers (qem_three_level.cu)
 cudaError_t th_forward(qem_ctx* c, cudaStream_t s);
 cudaError_t th_backward(qem_ctx* c, cudaStream_t s);

@@ -270,22 +270,30 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
     __syncthreads();
     for (int k = tid; k < K; k += NT) rows[(size_t)k * RS] = alpha0[k] - a.ws.dg[(size_t)i * K + k] * kLog2e;
     float2 u[CP][D], U2[CP], Lc[CP];
+    constexpr int CS = pad4(D + 3);
+    const int Kp = FwdLayout<D>::kpad(K);
 #pragma unroll
     for (int p = 0; p < CP; ++p) {
       float uu[2][D], u2[2], lc[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
+        // column record (u, |u|^2, P, ln P) written by the column prep (K2a)
         const int kc = tid + NT * (2 * p + h);
         const bool ok = kc < K;
-        float acc = 0.f;
+        float rec[CS];
+        const float4* src = reinterpret_cast<const float4*>(a.ws.colrec + ((size_t)i * Kp + (ok ? kc : 0)) * CS);
 #pragma unroll
-        for (int r = 0; r < D; ++r) {
-          const float zv = ok ? a.z[((size_t)i * D + r) * K + kc] : 0.f;
-          uu[h][r] = zv - mur[r];
-          acc = fmaf(uu[h][r], uu[h][r], acc);
+        for (int q = 0; q < CS / 4; ++q) {
+          const float4 v = src[q];
+          rec[4 * q] = v.x;
+          rec[4 * q + 1] = v.y;
+          rec[4 * q + 2] = v.z;
+          rec[4 * q + 3] = v.w;
         }
-        u2[h] = acc;
-        lc[h] = ok ? a.ws.lnP[(size_t)i * K + kc] * kLog2e : -CUDART_INF_F;
+#pragma unroll
+        for (int r = 0; r < D; ++r) uu[h][r] = ok ? rec[r] : 0.f;
+        u2[h] = ok ? rec[D] : 0.f;
+        lc[h] = ok ? rec[D + 2] * kLog2e : -CUDART_INF_F;
       }
 #pragma unroll
       for (int r = 0; r < D; ++r) u[p][r] = make_float2(uu[0][r], uu[1][r]);
@@ -441,9 +449,15 @@ static size_t bwd_smem(int K) {
 
 using KernelFn = void (*)(TLArgs);
 
-template <int D, int OBS>
+template <int D>
 static KernelFn fwd_fn(int rp) {
-  return rp == 1 ? k_forward<D, OBS, 1> : k_forward<D, OBS, 2>;
+  return rp == 1 ? k_forward<D, 1> : k_forward<D, 2>;
+}
+template <int D>
+static KernelFn prep_fn(int obs) {
+  if constexpr (D == 1)
+    if (obs == QEM_OBS_GAUSS) return k_colprep<D, QEM_OBS_GAUSS>;
+  return k_colprep<D, QEM_OBS_BERNOULLI_LOGIT>;
 }
 template <int D>
 static KernelFn bwd_fn(int cp) {
@@ -459,36 +473,35 @@ static int occupancy(KernelFn f, int nt, size_t sm) {
 }
 
 template <int D>
-static void grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb) {
+static int prep_threads(int) { return 32 * FwdLayout<D>::PREP_WARPS; }
+
+template <int D>
+static void grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb, int* gp) {
   const int K = d->K, rp = pick_rp(K);
-  KernelFn ff = d->obs_kind == QEM_OBS_GAUSS ? fwd_fn<D, QEM_OBS_GAUSS>(rp) : fwd_fn<D, QEM_OBS_BERNOULLI_LOGIT>(rp);
-  const int of = occupancy(ff, rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
+  const int of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
   const int ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
+  const int op = occupancy(prep_fn<D>(d->obs_kind), prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, d->n_obs));
   // Persistent-style grids: one full wave of resident CTAs, capped by the groups.
-  int64_t f = (int64_t)sms * of, b = (int64_t)sms * ob;
+  int64_t f = (int64_t)sms * of, b = (int64_t)sms * ob, p = (int64_t)sms * op;
   *gf = (int)(f < n_local ? f : n_local);
   *gb = (int)(b < n_local ? b : n_local);
-}
-
-template <int D, int OBS>
-static cudaError_t fwd_launch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
-  const int K = a.K, rp = pick_rp(K);
-  fwd_fn<D, OBS>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
-  return cudaGetLastError();
+  *gp = (int)(p < n_local ? p : n_local);
 }
 
 template <int D>
 static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
-  int nt = (a.K + 31) & ~31;
+  const int K = a.K, rp = pick_rp(K);
+  int nt = (K + 31) & ~31;
   k_root_prep<D><<<1, nt, 0, st>>>(a);
-  c->launches += 2;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (c->desc.obs_kind == QEM_OBS_GAUSS) {
-    if constexpr (D == 1) return fwd_launch<D, QEM_OBS_GAUSS>(c, a, st);
-    return cudaErrorInvalidValue;
-  }
-  return fwd_launch<D, QEM_OBS_BERNOULLI_LOGIT>(c, a, st);
+  if (c->desc.obs_kind == QEM_OBS_GAUSS && D != 1) return cudaErrorInvalidValue;
+  prep_fn<D>(c->desc.obs_kind)<<<c->grid_prep, prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, a.J), st>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  fwd_fn<D>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
+  c->launches += 3;
+  return cudaGetLastError();
 }
 
 template <int D>
@@ -513,12 +526,12 @@ int tl_supported_d(int d) {
   return 0;
 }
 
-void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb) {
-  *gf = *gb = 1;
+void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb, int* gp) {
+  *gf = *gb = *gp = 1;
   switch (d->d) {
 #define X(v)                              \
   case v:                                 \
-    grids<v>(d, n_local, sms, gf, gb);    \
+    grids<v>(d, n_local, sms, gf, gb, gp);\
     return;
     QEM_D_LIST(X)
 #undef X
