@@ -204,6 +204,11 @@ qem_status qem_iterate(qem_ctx* ctx, int32_t t0, int32_t T, uint64_t seed, int32
    call (then clears them), and the number of M-step variance clamps. */
 qem_status qem_read_flags(qem_ctx* ctx, void* stream, uint32_t* flags, int64_t* clamps);
 
+/* Synchronises `stream`, copies the forward tile-mode histogram (counts of
+   (CTA-warp, group) tiles evaluated in mode 0..5) into
+   h_hist[6] and clears it.  Two-level only; diagnostics. */
+qem_status qem_read_mode_hist(qem_ctx* ctx, void* stream, uint64_t* h_hist);
+
 /* Number of kernels the last qem_* call launched (for the bench's
    gpu_launches claim). */
 int64_t qem_kernel_launches(const qem_ctx* ctx);

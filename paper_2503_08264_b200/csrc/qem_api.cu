@@ -352,6 +352,17 @@ qem_status qem_read_flags(qem_ctx* c, void* stream, uint32_t* flags, int64_t* cl
   return QEM_OK;
 }
 
+qem_status qem_read_mode_hist(qem_ctx* c, void* stream, uint64_t* h) {
+  if (!c || !h) return fail(QEM_INVALID_ARGUMENT, "null argument");
+  unsigned long long tmp[8];
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaMemcpy(tmp, c->cnt->mode_hist, sizeof tmp, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(c->cnt->mode_hist, 0, sizeof tmp);
+  if (e != cudaSuccess) return cuda_fail(e, "qem_read_mode_hist");
+  for (int m = 0; m < 6; ++m) h[m] = tmp[m];
+  return QEM_OK;
+}
+
 int64_t qem_kernel_launches(const qem_ctx* c) { return c ? c->launches : 0; }
 
 qem_status qem_copy_messages(qem_ctx* c, float* d_dg, double* d_c, void* stream) {

@@ -6,17 +6,18 @@
 //     A_i(k') = sum_j log p(x_ij|z^k') - log q(z^k')            (fp64)
 //     t_i(k') = B(k_ref,k') + A_i(k')                            (fp64)
 //     c_i = lse_k' t_i - log K;  P_i = softmax t_i;  u = z - mu_ref
-//   -> column record colrec[i][k'] = {u[D], |u|^2, P_i, ln P_i} (fp32),
-//      cvec[i] = c_i, gstat[i] = max |u|^2.
+//   -> column record colrec[i][k'] = {w[D], |w|^2, P_i, ln P_i} (fp32), w = z - m_i,
+//      cvec[i] = c_i, gstat[i] = max |w|^2.
 // K2b k_forward  (persistent, TMA double-buffered): the group's column
 //   records arrive in shared memory by cp.async.bulk (mbarrier completion)
 //   while the previous group's tile is computed; rows k live in registers
 //   (sorted by coefficient magnitude so a warp's rows share a mode):
-//     dg_i(k) = log sum_k' P_i(k') exp(D_k(k')), by
-//       mode 0: log1p(sum P expm1_5(D))   bound(|D|) <= 1/16
-//       mode 1: log1p(sum P expm1_9(D))   bound(|D|) <= 1/2
-//       mode 2: single-pass online log-sum-exp of D + ln P (ex2 on the SFU)
-//   The mode is warp-uniform (max over the warp's rows).
+//     dg_i(k) = alpha'_k + log sum_k' P_i(k') exp(D'_k(k')), D' re-centred on the
+//     group's Q mean, by
+//       modes 0-4: log1p(sum P expm1_n(D')), n = 3/4/5/7/9 while the Taylor
+//                  remainder at bound(|D'|), times N groups, stays <= 2e-6
+//       mode 5:    single-pass online log-sum-exp of D' + ln P (ex2 on the SFU)
+//   The mode is CTA-uniform (max over the CTA's rows) so warps stay in step.
 #pragma once
 
 template <int D>
@@ -224,19 +225,22 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
           ll += (ybits[j] ? (double)eta : 0.0) - (double)sp;
         }
       }
+      // record the group-centred offsets w = z - m_i (DESIGN.md "Forward":
+      // recentring); the reference row uses u = z - mu_ref exactly in fp64.
       float rec[CS];
-      float U2 = 0.f;
+      float W2 = 0.f;
       double U2d = 0.0;
 #pragma unroll
       for (int r = 0; r < D; ++r) {
-        const float u = zr[r] - ref.mu_ref[r];
-        rec[r] = u;
-        U2 = fmaf(u, u, U2);
-        U2d += (double)u * (double)u;
+        const float w = zr[r] - (float)qconst[r];
+        rec[r] = w;
+        W2 = fmaf(w, w, W2);
+        const double u = (double)zr[r] - (double)ref.mu_ref[r];
+        U2d += u * u;
       }
 #pragma unroll
       for (int r = D; r < CS; ++r) rec[r] = 0.f;
-      rec[D] = U2;
+      rec[D] = W2;
       float4* dst = reinterpret_cast<float4*>(rec0 + (size_t)kc * CS);
 #pragma unroll
       for (int q = 0; q < CS / 4; ++q)
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
       const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
       tref[kc] = t;
       tmax = fmax(tmax, t);
-      u2max = fmaxf(u2max, U2);
+      u2max = fmaxf(u2max, W2);
     }
     // padding columns: P = 0, ln P = -inf (contribute nothing)
     for (int kc = K + lane; kc < Kp; kc += 32) {
@@ -273,8 +277,12 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
 
 // ------------------------------------------------------------------ K2b
 // Thread t owns the row slots s = 2(t*RP+p)+h (p < RP float2 pairs), i.e.
-// rows k = perm[s]; the row coefficients stay in registers for the whole
-// kernel (they depend only on the root samples).
+// rows k = perm[s].  Per group the row coefficients are re-centred on the
+// group's Q mean m_i (u = u0 + w, u0 = m_i - mu_ref, w = z - m_i):
+//   D_k(k') = alpha'_k + gamma_k |w|^2 + c'_k . w,
+//   alpha'_k = alpha_k + gamma_k |u0|^2 + c_k . u0,   c'_k = c_k + 2 gamma_k u0,
+// so the column loop only sees the small within-group part and alpha'_k is
+// added back to dg at the end (exact algebra).
 template <int D, int RP>
 __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -283,44 +291,35 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
   const int K = a.K, tid = threadIdx.x;
   const int Kp = FwdLayout<D>::kpad(K);
   const uint32_t sbytes = (uint32_t)FwdLayout<D>::stage_bytes(K);
-  float* stage[2] = {reinterpret_cast<float*>(smem), reinterpret_cast<float*>(smem + sbytes)};
+  // stage s lives at smem + s*sbytes (pointer arithmetic on the __shared__ symbol keeps LDS addressing)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sbytes);
 
-  // Row coefficients in registers.
-  float2 al[RP], ga[RP], cc[RP][D];
-  float rb_a[2 * RP], rb_g[2 * RP], rb_c[2 * RP];
+  float mur[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) mur[r] = a.ws.ref->mu_ref[r];
   int kid[2 * RP];
+  float2 ga[RP];
 #pragma unroll
   for (int p = 0; p < RP; ++p) {
-    float av[2], gv[2], cv[2][D];
+    float gv[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int s = 2 * (tid * RP + p) + h;  // a warp owns a contiguous run of sorted slots
       const bool ok = s < K;
       const int k = ok ? a.ws.perm[s] : 0;
       kid[2 * p + h] = ok ? k : -1;
-      const float* fc = a.ws.fwd_coef + (size_t)k * CW;
-      av[h] = ok ? fc[0] : 0.f;
-      gv[h] = ok ? fc[1] : 0.f;
-      float cn = 0.f;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        cv[h][r] = ok ? fc[2 + r] : 0.f;
-        cn = fmaf(cv[h][r], cv[h][r], cn);
-      }
-      rb_a[2 * p + h] = fabsf(av[h]);
-      rb_g[2 * p + h] = fabsf(gv[h]);
-      rb_c[2 * p + h] = sqrtf(cn);
+      gv[h] = ok ? a.ws.fwd_coef[(size_t)k * CW + 1] : 0.f;
     }
-    al[p] = make_float2(av[0], av[1]);
     ga[p] = make_float2(gv[0], gv[1]);
-#pragma unroll
-    for (int r = 0; r < D; ++r) cc[p][r] = make_float2(cv[0][r], cv[1][r]);
   }
+  float2 az[RP];
+#pragma unroll
+  for (int p = 0; p < RP; ++p) az[p] = f2(0.f);
   double G[2 * RP];
 #pragma unroll
   for (int j = 0; j < 2 * RP; ++j) G[j] = 0.0;
   double csum = 0.0;
+  uint32_t mc0 = 0, mc1 = 0, mc2 = 0, mc3 = 0, mc4 = 0, mc5 = 0;
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -331,37 +330,89 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
   const int64_t i0 = blockIdx.x;
   if (tid == 0 && i0 < a.n_local) {
     mbar_expect_tx(&bar[0], sbytes);
-    tma_bulk_g2s(stage[0], a.ws.colrec + (size_t)i0 * Kp * CS, sbytes, &bar[0]);
+    tma_bulk_g2s(smem, a.ws.colrec + (size_t)i0 * Kp * CS, sbytes, &bar[0]);
   }
+  __shared__ int s_mode[2][8];
   int j = 0;
   for (int64_t i = i0; i < a.n_local; i += gridDim.x, ++j) {
     const int st = j & 1;
+    const float W2max = a.ws.gstat[i];
+    if (tid == 0) csum += a.ws.cvec[i];
+
+    // ---- re-centred row coefficients for this group (before the barrier, so
+    // the CTA-wide tile mode costs no extra synchronisation)
+    float u0[D];
+    float U0sq = 0.f;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      u0[r] = a.q_m[i * D + r] - mur[r];
+      U0sq = fmaf(u0[r], u0[r], U0sq);
+    }
+    const float wmax = sqrtf(W2max);
+    float2 al[RP], cc[RP][D];
+    float tb = 0.f;
+#pragma unroll
+    for (int p = 0; p < RP; ++p) {
+      float av[2], cv[2][D];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = kid[2 * p + h] >= 0 ? kid[2 * p + h] : 0;
+        const float* fc = a.ws.fwd_coef + (size_t)k * CW;
+        const float g = h ? ga[p].y : ga[p].x;
+        float ap = fmaf(g, U0sq, fc[0]);
+        float cn = 0.f;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          const float c = fc[2 + r];
+          ap = fmaf(c, u0[r], ap);
+          cv[h][r] = fmaf(2.f * g, u0[r], c);
+          cn = fmaf(cv[h][r], cv[h][r], cn);
+        }
+        av[h] = kid[2 * p + h] >= 0 ? ap : 0.f;
+        tb = fmaxf(tb, sqrtf(cn) * wmax + fabsf(g) * W2max);
+      }
+      al[p] = make_float2(av[0], av[1]);
+#pragma unroll
+      for (int r = 0; r < D; ++r) cc[p][r] = make_float2(cv[0][r], cv[1][r]);
+    }
+    // degree n of the expm1 Taylor polynomial such that its remainder at the
+    // bound, summed over all N groups, stays below 2e-6
+    int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
+    md = __reduce_max_sync(0xffffffffu, md);
+    if ((tid & 31) == 0) s_mode[st][tid >> 5] = md;
+
     // all warps are done with the other stage (group j-1): refill it with group j+1
     __syncthreads();
     const int64_t inext = i + gridDim.x;
     if (tid == 0 && inext < a.n_local) {
       mbar_expect_tx(&bar[st ^ 1], sbytes);
-      tma_bulk_g2s(stage[st ^ 1], a.ws.colrec + (size_t)inext * Kp * CS, sbytes, &bar[st ^ 1]);
+      tma_bulk_g2s(smem + (st ? 0 : sbytes), a.ws.colrec + (size_t)inext * Kp * CS, sbytes, &bar[st ^ 1]);
     }
-    const float U2max = a.ws.gstat[i];
-    if (tid == 0) csum += a.ws.cvec[i];
+    // CTA-uniform mode: every warp does the same work per group (no barrier skew)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) md = max(md, s_mode[st][w]);
+    mc0 += md == 0;
+    mc1 += md == 1;
+    mc2 += md == 2;
+    mc3 += md == 3;
+    mc4 += md == 4;
+    mc5 += md == 5;
     mbar_wait(&bar[st], (uint32_t)((j >> 1) & 1));
-    const float* col = stage[st];
+    const float* col = reinterpret_cast<const float*>(smem + (st ? sbytes : 0));
 
-    // ---- pair tile: dg_i(k) for the owned rows, warp-uniform mode
-    const float umax = sqrtf(U2max);
-    float tb = 0.f;
-#pragma unroll
-    for (int q = 0; q < 2 * RP; ++q) tb = fmaxf(tb, rb_a[q] + rb_g[q] * U2max + rb_c[q] * umax);
-    int md = tb <= 0.0625f ? 0 : (tb <= 0.5f ? 1 : 2);
-    md = __reduce_max_sync(0xffffffffu, md);
     float dgv[2 * RP];
-    if (md == 0)
-      tile_poly<D, RP, 5>(col, Kp, al, ga, cc, dgv);
-    else if (md == 1)
-      tile_poly<D, RP, 9>(col, Kp, al, ga, cc, dgv);
-    else
-      tile_online<D, RP>(col, Kp, al, ga, cc, dgv);
+    switch (md) {
+      case 0: tile_poly<D, RP, 3>(col, Kp, az, ga, cc, dgv); break;
+      case 1: tile_poly<D, RP, 4>(col, Kp, az, ga, cc, dgv); break;
+      case 2: tile_poly<D, RP, 5>(col, Kp, az, ga, cc, dgv); break;
+      case 3: tile_poly<D, RP, 7>(col, Kp, az, ga, cc, dgv); break;
+      case 4: tile_poly<D, RP, 9>(col, Kp, az, ga, cc, dgv); break;
+      default: tile_online<D, RP>(col, Kp, az, ga, cc, dgv); break;
+    }
+#pragma unroll
+    for (int p = 0; p < RP; ++p) {
+      dgv[2 * p] += al[p].x;
+      dgv[2 * p + 1] += al[p].y;
+    }
 #pragma unroll
     for (int q = 0; q < 2 * RP; ++q) {
       if (kid[q] >= 0) {
@@ -377,6 +428,13 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
   for (int q = 0; q < 2 * RP; ++q)
     if (kid[q] >= 0) part[kid[q]] = G[q];
   if (tid == 0) part[K] = csum;
+  if ((tid & 31) == 0)
+  {
+    const uint32_t mcs[6] = {mc0, mc1, mc2, mc3, mc4, mc5};
+#pragma unroll
+    for (int m = 0; m < 6; ++m)
+      if (mcs[m]) atomicAdd(&a.cnt->mode_hist[m], (unsigned long long)mcs[m]);
+  }
   __threadfence();
   __syncthreads();
   __shared__ uint32_t s_last;

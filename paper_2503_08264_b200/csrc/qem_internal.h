@@ -49,6 +49,7 @@ struct Counters {
   unsigned long long clamps;
   int32_t iter;        // current iteration t (graph mode)
   int32_t trace_base;  // t0 of the running qem_iterate
+  unsigned long long mode_hist[8];  // forward tile modes, counted per (warp, group)
 };
 
 }  // namespace qem

@@ -15,6 +15,7 @@
 // Root:  a(k) = f_root(k) + sum_i dg_i(k);  log Pe = sum_i c_i + lse(a) - log K.
 // Backward: w_i(k') = sum_k w_root(k) exp(ln P_i(k') + D_k(k') - dg_i(k)).
 #include <cstdio>
+#include <cstdlib>
 
 #include "qem_device.cuh"
 #include "qem_internal.h"
@@ -45,6 +46,7 @@ struct TLArgs {
   double* trace;
   int64_t trace_len;
   int t_host;
+  float thr[5];  // forward tile-mode bounds for expm1 degrees 3/4/5/7/9
   TwoLevelWs ws;
   Counters* cnt;
 };
@@ -255,12 +257,11 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RS = pad4(D + 3);
   const int K = a.K, tid = threadIdx.x, NT = blockDim.x;
+  constexpr int CW = D + 2;
   float* rows = reinterpret_cast<float*>(smem);          // [K][RS]
-  float* alpha0 = rows + (size_t)K * RS;                 // [K] (padded to even)
-  double* red = reinterpret_cast<double*>(alpha0 + ((K + 1) & ~1));  // [32][D]
+  float* spare = rows + (size_t)K * RS;                  // [K] (padded to even; unused)
+  double* red = reinterpret_cast<double*>(spare + ((K + 1) & ~1));  // [32][D]
   double* mom = red + 32 * D;                            // [D]
-  for (int e = tid; e < K * RS; e += NT) rows[e] = a.ws.bwd_table[e];
-  for (int k = tid; k < K; k += NT) alpha0[k] = a.ws.bwd_table[(size_t)k * RS];
   float mur[D];
 #pragma unroll
   for (int r = 0; r < D; ++r) mur[r] = a.ws.ref->mu_ref[r];
@@ -268,7 +269,32 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
 
   for (int64_t i = blockIdx.x; i < a.n_local; i += gridDim.x) {
     __syncthreads();
-    for (int k = tid; k < K; k += NT) rows[(size_t)k * RS] = alpha0[k] - a.ws.dg[(size_t)i * K + k] * kLog2e;
+    // row table re-centred on the group's Q mean (same algebra as the forward):
+    // alpha'' = (alpha + gamma |u0|^2 + c.u0 - dg) log2e, c'' = (c + 2 gamma u0) log2e
+    {
+      float u0[D];
+      float U0sq = 0.f;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        u0[r] = a.q_m[i * D + r] - mur[r];
+        U0sq = fmaf(u0[r], u0[r], U0sq);
+      }
+      for (int k = tid; k < K; k += NT) {
+        const float* fc = a.ws.fwd_coef + (size_t)k * CW;
+        const float g = fc[1];
+        float ap = fmaf(g, U0sq, fc[0]);
+        float* rw = rows + (size_t)k * RS;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          const float c = fc[2 + r];
+          ap = fmaf(c, u0[r], ap);
+          rw[2 + r] = fmaf(2.f * g, u0[r], c) * kLog2e;
+        }
+        rw[0] = (ap - a.ws.dg[(size_t)i * K + k]) * kLog2e;
+        rw[1] = g * kLog2e;
+        rw[2 + D] = a.w_root[k];
+      }
+    }
     float2 u[CP][D], U2[CP], Lc[CP];
     constexpr int CS = pad4(D + 3);
     const int Kp = FwdLayout<D>::kpad(K);
@@ -427,6 +453,15 @@ static TLArgs make_args(qem_ctx* c) {
   a.trace = c->in_iterate ? c->bufs.trace : nullptr;
   a.trace_len = c->bufs.trace_len;
   a.t_host = 0;
+  // |D'| bound below which the degree-n Taylor remainder |D'|^{n+1}/(n+1)!,
+  // accumulated over all N groups of the plate, stays under 2e-6
+  const int degs[5] = {3, 4, 5, 7, 9};
+  for (int q = 0; q < 5; ++q) {
+    double f = 1.0;
+    for (int m = 2; m <= degs[q] + 1; ++m) f *= m;
+    double t = pow(f * 2e-6 / (double)(d.n > 0 ? d.n : 1), 1.0 / (degs[q] + 1));
+    a.thr[q] = (float)(t < 0.5 ? t : 0.5);
+  }
   a.ws = c->tw;
   if (c->bufs.plate_sum) a.ws.red = c->bufs.plate_sum;
   a.cnt = c->cnt;
@@ -438,7 +473,14 @@ static int rows_threads(int K, int rp) {
   nt = (nt + 31) & ~31;
   return nt < 32 ? 32 : nt;
 }
-static int pick_rp(int K) { return K >= 512 ? 2 : 1; }
+static int pick_rp(int K) {
+  static const int forced = [] {
+    const char* e = getenv("QEM_RP");  // tuning override: 1 or 2 row pairs per thread
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2) return forced;
+  return K >= 512 ? 2 : 1;
+}
 
 template <int D>
 static size_t bwd_smem(int K) {

@@ -180,6 +180,12 @@ class QEM:
         check(lib().qem_read_flags(self.ctx, _stream(stream), ctypes.byref(f), ctypes.byref(c)), "qem_read_flags")
         return f.value, c.value
 
+    def mode_hist(self, stream=None):
+        """Forward tile-mode histogram since the last call (diagnostics)."""
+        h = (ctypes.c_uint64 * 6)()
+        check(lib().qem_read_mode_hist(self.ctx, _stream(stream), h), "qem_read_mode_hist")
+        return [int(v) for v in h]
+
     def kernel_launches(self) -> int:
         return int(lib().qem_kernel_launches(self.ctx))
 

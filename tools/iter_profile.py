@@ -42,11 +42,12 @@ def main():
         lp = g.log_pe.item()
         w = g.levels[0]["w"]
         ess = (1.0 / (w.double() ** 2).sum()).item()
+        hist = g.mode_hist() if m.family == 2 else []
         rows.append(dict(t=t, sample=ev[0].elapsed_time(ev[1]), fwd=ev[1].elapsed_time(ev[2]),
                          bwd=ev[2].elapsed_time(ev[3]), mstep=ev[3].elapsed_time(ev[4]), log_pe=lp, root_ess=ess))
         r = rows[-1]
         print(f"t={t:3d} sample {r['sample']:.3f} fwd {r['fwd']:.3f} bwd {r['bwd']:.3f} mstep {r['mstep']:.3f} ms"
-              f"  logPe {lp:.6e}  root ESS {ess:.2f}", flush=True)
+              f"  logPe {lp:.6e}  root ESS {ess:.2f}  modes {hist}", flush=True)
     print(json.dumps(dict(config=a.config, rows=rows)))
 
 
