@@ -106,6 +106,8 @@ size_t carve(qem_ctx* c, char* base) {
     c->tw.gstat = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local));
     c->tw.cvec = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->n_local));
     c->tw.perm = reinterpret_cast<int*>(take(sizeof(int) * K));
+    c->tw.alpha_d = reinterpret_cast<double*>(take(sizeof(double) * K));
+    c->tw.hmsg = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
   } else {
     const int64_t A = d.n, AB = d.n * d.n_sub, KK = (int64_t)K * K;
     c->th.f_root = reinterpret_cast<double*>(take(sizeof(double) * K));

@@ -349,29 +349,30 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
       U0sq = fmaf(u0[r], u0[r], U0sq);
     }
     const float wmax = sqrtf(W2max);
-    float2 al[RP], cc[RP][D];
+    // alpha'_k in fp64 (it can be large where D is large; the tile only sees D')
+    double ald[2 * RP];
+    float2 cc[RP][D];
     float tb = 0.f;
 #pragma unroll
     for (int p = 0; p < RP; ++p) {
-      float av[2], cv[2][D];
+      float cv[2][D];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int k = kid[2 * p + h] >= 0 ? kid[2 * p + h] : 0;
         const float* fc = a.ws.fwd_coef + (size_t)k * CW;
         const float g = h ? ga[p].y : ga[p].x;
-        float ap = fmaf(g, U0sq, fc[0]);
+        double ap = a.ws.alpha_d[k] + (double)g * (double)U0sq;
         float cn = 0.f;
 #pragma unroll
         for (int r = 0; r < D; ++r) {
           const float c = fc[2 + r];
-          ap = fmaf(c, u0[r], ap);
+          ap += (double)c * (double)u0[r];
           cv[h][r] = fmaf(2.f * g, u0[r], c);
           cn = fmaf(cv[h][r], cv[h][r], cn);
         }
-        av[h] = kid[2 * p + h] >= 0 ? ap : 0.f;
+        ald[2 * p + h] = ap;
         tb = fmaxf(tb, sqrtf(cn) * wmax + fabsf(g) * W2max);
       }
-      al[p] = make_float2(av[0], av[1]);
 #pragma unroll
       for (int r = 0; r < D; ++r) cc[p][r] = make_float2(cv[0][r], cv[1][r]);
     }
@@ -408,16 +409,15 @@ __global__ void __launch_bounds__(256) k_forward(TLArgs a) {
       case 4: tile_poly<D, RP, 9>(col, Kp, az, ga, cc, dgv); break;
       default: tile_online<D, RP>(col, Kp, az, ga, cc, dgv); break;
     }
-#pragma unroll
-    for (int p = 0; p < RP; ++p) {
-      dgv[2 * p] += al[p].x;
-      dgv[2 * p + 1] += al[p].y;
-    }
+    // h = log sum P exp(D') feeds the backward directly (no cancellation against
+    // alpha'); dg = alpha' + h in fp64 feeds the plate sum.
 #pragma unroll
     for (int q = 0; q < 2 * RP; ++q) {
       if (kid[q] >= 0) {
-        a.ws.dg[(size_t)i * K + kid[q]] = dgv[q];
-        G[q] += (double)dgv[q];
+        const double dgd = ald[q] + (double)dgv[q];
+        a.ws.hmsg[(size_t)i * K + kid[q]] = dgv[q];
+        a.ws.dg[(size_t)i * K + kid[q]] = (float)dgd;
+        G[q] += dgd;
       }
     }
   }

@@ -30,6 +30,8 @@ struct TwoLevelWs {
   float* gstat;       // [n_local]  max_k' |u|^2 (forward mode bound)
   double* cvec;       // [n_local]  c_i = g_i(k_ref)
   int* perm;          // [K]        forward row order (rows sorted by coefficient magnitude)
+  double* alpha_d;    // [K]        alpha_k in fp64
+  float* hmsg;        // [n_local][K] h_i(k) = dg_i(k) - alpha'_ik (re-centred message)
 };
 
 struct ThreeLevelWs {

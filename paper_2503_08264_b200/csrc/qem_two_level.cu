@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
     const double gamma = -0.5 * (ek - e_ref);
     fc[0] = (float)alpha;
     fc[1] = (float)gamma;
+    a.ws.alpha_d[k] = alpha;
     bt[0] = (float)(alpha * kLog2eD);
     bt[1] = (float)(gamma * kLog2eD);
     double f = 0.0;
@@ -282,15 +283,11 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
       for (int k = tid; k < K; k += NT) {
         const float* fc = a.ws.fwd_coef + (size_t)k * CW;
         const float g = fc[1];
-        float ap = fmaf(g, U0sq, fc[0]);
         float* rw = rows + (size_t)k * RS;
 #pragma unroll
-        for (int r = 0; r < D; ++r) {
-          const float c = fc[2 + r];
-          ap = fmaf(c, u0[r], ap);
-          rw[2 + r] = fmaf(2.f * g, u0[r], c) * kLog2e;
-        }
-        rw[0] = (ap - a.ws.dg[(size_t)i * K + k]) * kLog2e;
+        for (int r = 0; r < D; ++r) rw[2 + r] = fmaf(2.f * g, u0[r], fc[2 + r]) * kLog2e;
+        // alpha'_k - dg_i(k) = -h_i(k): the re-centred message, no cancellation
+        rw[0] = -a.ws.hmsg[(size_t)i * K + k] * kLog2e;
         rw[1] = g * kLog2e;
         rw[2 + D] = a.w_root[k];
       }
