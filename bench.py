@@ -162,23 +162,24 @@ def run_gpu(args):
     seed = 100 + args.config
     stream = torch.cuda.current_stream()
 
+    from paper_2503_08264_b200.dist import ShardedQEM
+    runner = ShardedQEM(g)
+
     def allreduce():
-        if world > 1:
-            dist.all_reduce(g.plate_sum, op=dist.ReduceOp.SUM)
+        runner.allreduce_plate_sum()
 
     def step(t, ev=None):
-        g.sample_q(seed=seed, iter=t)
+        # ev: [fwd kernel start, fwd kernel end, bwd kernel start, bwd kernel end, allreduce start, end]
         if ev:
-            ev[0].record(stream)
+            g.set_kernel_events(ev[:4])
+        g.sample_q(seed=seed, iter=t)
         g.estep_forward()
         if ev:
-            ev[1].record(stream)
+            ev[4].record(stream)
         allreduce()
         if ev:
-            ev[2].record(stream)
+            ev[5].record(stream)
         g.estep_backward()
-        if ev:
-            ev[3].record(stream)
         g.mstep(t)
 
     t = 1
@@ -187,7 +188,7 @@ def run_gpu(args):
         t += 1
     torch.cuda.synchronize()
     launches_per_step = 0
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -205,11 +206,13 @@ def run_gpu(args):
         dist.barrier()
     clk = clocks.stop()
     ms_total = start.elapsed_time(stop)
+    g.set_kernel_events(None)
+    # pair-tile kernels alone (events recorded by libqem around k_forward / k_backward)
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     bwd_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
-    comm_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    # launches: sample(1) + forward(root_prep, forward) + backward(root, backward) + mstep(1)
-    launches_per_step = 6
+    comm_ms = sum(e[4].elapsed_time(e[5]) for e in evs) / args.steps
+    # launches: sample(1) + forward(root_prep, colprep, forward) + backward(root, backward) + mstep(1)
+    launches_per_step = 7
     flags, clamps = g.read_flags()
     if world > 1:
         tt = torch.tensor([ms_total, fwd_ms, bwd_ms, comm_ms], dtype=torch.float64, device=dev)

@@ -209,6 +209,12 @@ qem_status qem_read_flags(qem_ctx* ctx, void* stream, uint32_t* flags, int64_t* 
    h_hist[6] and clears it.  Two-level only; diagnostics. */
 qem_status qem_read_mode_hist(qem_ctx* ctx, void* stream, uint64_t* h_hist);
 
+/* Optional cudaEvent_t handles (as void*, NULL = off) that the library
+   records on the launch stream immediately before/after the two-level
+   pair-tile kernels (forward K2b, backward K4) of every later E-step, so a
+   caller can time exactly those kernels.  The events are caller-owned. */
+qem_status qem_set_kernel_events(qem_ctx* ctx, void* fwd_start, void* fwd_end, void* bwd_start, void* bwd_end);
+
 /* Number of kernels the last qem_* call launched (for the bench's
    gpu_launches claim). */
 int64_t qem_kernel_launches(const qem_ctx* ctx);

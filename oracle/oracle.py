@@ -111,6 +111,38 @@ def estep(m, z, q, data):
                 m2=[m2r, m2t, m2s])
 
 
+def _data2(data):
+    xg = _f64(data.xg) if data.xg is not None else None
+    xb = np.ascontiguousarray(data.xb, np.uint8) if data.xb is not None else None
+    yb = np.ascontiguousarray(data.yb, np.uint8) if data.yb is not None else None
+    return xg, xb, yb
+
+
+def forward2(m, z, q, data):
+    """Two-level forward half: (f_root [K], g [n][K]) (plate messages g_i(k))."""
+    zs = [_f64(a) for a in z]
+    qs = [(_f64(a), _f64(b)) for a, b in q]
+    xg, xb, yb = _data2(data)
+    f_root, g = np.zeros(m.K), np.zeros((m.n, m.K))
+    mm = _m2(m)
+    lib().orc2_forward(ctypes.byref(mm), m.K, _p(zs[0]), _p(zs[1]), _p(qs[0][0]), _p(qs[0][1]), _p(qs[1][0]),
+                       _p(qs[1][1]), _p(xg), _p(xb), _p(yb), _p(f_root), _p(g))
+    return f_root, g
+
+
+def backward2(m, z, q, data, w_root, g):
+    """Two-level backward half given root weights: (w [n][K], m1 [n*d], m2 [n*d])."""
+    zs = [_f64(a) for a in z]
+    qs = [(_f64(a), _f64(b)) for a, b in q]
+    xg, xb, yb = _data2(data)
+    w, m1, m2 = np.zeros((m.n, m.K)), np.zeros(m.n * m.d), np.zeros(m.n * m.d)
+    mm = _m2(m)
+    wr, gg = _f64(w_root), _f64(g)
+    lib().orc2_backward(ctypes.byref(mm), m.K, _p(zs[0]), _p(zs[1]), _p(qs[1][0]), _p(qs[1][1]), _p(xg), _p(xb),
+                        _p(yb), _p(wr), _p(gg), _p(w), _p(m1), _p(m2))
+    return w, m1, m2
+
+
 def sample(q_mean, q_var, eps):
     """z = fmaf(sqrtf(v), eps, m) in fp32 (R22); eps [n][K] fp32 -> z [n][K] fp32."""
     L = lib()

@@ -125,28 +125,20 @@ static double group_loglik(const orc_model2* m, long i, const double* zi /*[d][K
 }
 
 /*
- * One MPIW E-step on a two-level model (Eq. 7a-c, PAPER.md:139-150).
- * Inputs (all arrays row-major, k fastest):
- *   z_root [R][K], z [n][d][K]       samples (fp32-representable values)
- *   qr_m, qr_v [R]; q_m, q_v [n][d]  factorised Gaussian Q (mean, variance)
- *   xg [n][J] (obs 1) or xb [n][J][d], yb [n][J] (obs 2)
- * Outputs:
- *   log_pe; w_root [K]; w [n][K]; g [n][K] (per-group messages
- *   g_i(k) = log (1/K) sum_k' exp(B_i(k,k') + A_i(k')), DESIGN.md);
- *   m1_root, m2_root [R]; m1, m2 [n][d]  (E z, E z^2).
- * Returns 0, or 1 if the evidence is degenerate (all terms -inf).
+ * Forward half of the two-level E-step: the root factor
+ *   f_root(k) = log p(root^k) - log q(root^k)
+ * and the per-group plate messages (elimination of each group's own index,
+ * PAPER.md:393)
+ *   g_i(k) = log (1/K) sum_k' exp(B_i(k,k') + A_i(k')),
+ *   B_i(k,k') = log p(z_i^k' | root^k),  A_i(k') = log p(x_i | z_i^k') - log q(z_i^k').
+ * Arrays as in orc2_estep.
  */
-int orc2_estep(const orc_model2* m, int K, const double* z_root, const double* z,
-               const double* qr_m, const double* qr_v, const double* q_m, const double* q_v,
-               const double* xg, const unsigned char* xb, const unsigned char* yb,
-               double* log_pe, double* w_root, double* w, double* g,
-               double* m1_root, double* m2_root, double* m1, double* m2) {
+void orc2_forward(const orc_model2* m, int K, const double* z_root, const double* z, const double* qr_m,
+                  const double* qr_v, const double* q_m, const double* q_v, const double* xg,
+                  const unsigned char* xb, const unsigned char* yb, double* f_root, double* g) {
   const int d = m->d, R = d + (m->scale_kind != 0);
   const long n = m->n;
   const double logK = log((double)K);
-
-  /* Root factor f_root(k) = log p(root^k) - log q(root^k). */
-  double* f_root = (double*)malloc(sizeof(double) * K);
   for (int k = 0; k < K; ++k) {
     double f = 0.0;
     for (int r = 0; r < R; ++r) {
@@ -155,8 +147,6 @@ int orc2_estep(const orc_model2* m, int K, const double* z_root, const double* z
     }
     f_root[k] = f;
   }
-
-  /* Forward: g_i(k) = lse_k' [ B_i(k,k') + A_i(k') ] - log K. */
 #pragma omp parallel for schedule(static)
   for (long i = 0; i < n; ++i) {
     const double* zi = z + (size_t)i * d * K;
@@ -179,31 +169,19 @@ int orc2_estep(const orc_model2* m, int K, const double* z_root, const double* z
     free(A);
     free(t);
   }
+}
 
-  /* Plate product and root: a(k) = f_root(k) + sum_i g_i(k) (index order). */
-  double* a = (double*)malloc(sizeof(double) * K);
-  for (int k = 0; k < K; ++k) {
-    double s = f_root[k];
-    for (long i = 0; i < n; ++i) s += g[(size_t)i * K + k];
-    a[k] = s;
-  }
-  double L = lse(a, K, 1);
-  *log_pe = L - logK;
-  int degenerate = (L == -INFINITY) || isnan(L);
-  for (int k = 0; k < K; ++k) w_root[k] = degenerate ? NAN : exp(a[k] - L);
-
-  for (int r = 0; r < R; ++r) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int k = 0; k < K; ++k) {
-      double v = z_root[(size_t)r * K + k];
-      s1 += w_root[k] * v;
-      s2 += w_root[k] * v * v;
-    }
-    m1_root[r] = s1;
-    m2_root[r] = s2;
-  }
-
-  /* Backward: w_i(k') = sum_k w_root(k) exp(B_i(k,k') + A_i(k') - log K - g_i(k)). */
+/*
+ * Backward half: each group's marginal weights given the root weights
+ *   w_i(k') = sum_k w_root(k) exp(B_i(k,k') + A_i(k') - log K - g_i(k))
+ * (Eq. 7a with m = indicator of z_i^k'), and their moments (E z, E z^2).
+ */
+void orc2_backward(const orc_model2* m, int K, const double* z_root, const double* z, const double* q_m,
+                   const double* q_v, const double* xg, const unsigned char* xb, const unsigned char* yb,
+                   const double* w_root, const double* g, double* w, double* m1, double* m2) {
+  const int d = m->d, R = d + (m->scale_kind != 0);
+  const long n = m->n;
+  const double logK = log((double)K);
 #pragma omp parallel for schedule(static)
   for (long i = 0; i < n; ++i) {
     const double* zi = z + (size_t)i * d * K;
@@ -235,6 +213,55 @@ int orc2_estep(const orc_model2* m, int K, const double* z_root, const double* z
     }
     free(A);
   }
+}
+
+/*
+ * One MPIW E-step on a two-level model (Eq. 7a-c, PAPER.md:139-150).
+ * Inputs (all arrays row-major, k fastest):
+ *   z_root [R][K], z [n][d][K]       samples (fp32-representable values)
+ *   qr_m, qr_v [R]; q_m, q_v [n][d]  factorised Gaussian Q (mean, variance)
+ *   xg [n][J] (obs 1) or xb [n][J][d], yb [n][J] (obs 2)
+ * Outputs:
+ *   log_pe; w_root [K]; w [n][K]; g [n][K] (per-group messages
+ *   g_i(k) = log (1/K) sum_k' exp(B_i(k,k') + A_i(k')), DESIGN.md);
+ *   m1_root, m2_root [R]; m1, m2 [n][d]  (E z, E z^2).
+ * Returns 0, or 1 if the evidence is degenerate (all terms -inf).
+ */
+int orc2_estep(const orc_model2* m, int K, const double* z_root, const double* z,
+               const double* qr_m, const double* qr_v, const double* q_m, const double* q_v,
+               const double* xg, const unsigned char* xb, const unsigned char* yb,
+               double* log_pe, double* w_root, double* w, double* g,
+               double* m1_root, double* m2_root, double* m1, double* m2) {
+  const int d = m->d, R = d + (m->scale_kind != 0);
+  const long n = m->n;
+  const double logK = log((double)K);
+  double* f_root = (double*)malloc(sizeof(double) * K);
+  orc2_forward(m, K, z_root, z, qr_m, qr_v, q_m, q_v, xg, xb, yb, f_root, g);
+
+  /* Plate product and root: a(k) = f_root(k) + sum_i g_i(k) (index order). */
+  double* a = (double*)malloc(sizeof(double) * K);
+  for (int k = 0; k < K; ++k) {
+    double s = f_root[k];
+    for (long i = 0; i < n; ++i) s += g[(size_t)i * K + k];
+    a[k] = s;
+  }
+  double L = lse(a, K, 1);
+  *log_pe = L - logK;
+  int degenerate = (L == -INFINITY) || isnan(L);
+  for (int k = 0; k < K; ++k) w_root[k] = degenerate ? NAN : exp(a[k] - L);
+
+  for (int r = 0; r < R; ++r) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      double v = z_root[(size_t)r * K + k];
+      s1 += w_root[k] * v;
+      s2 += w_root[k] * v * v;
+    }
+    m1_root[r] = s1;
+    m2_root[r] = s2;
+  }
+  (void)d;
+  orc2_backward(m, K, z_root, z, q_m, q_v, xg, xb, yb, w_root, g, w, m1, m2);
   free(a);
   free(f_root);
   return degenerate;

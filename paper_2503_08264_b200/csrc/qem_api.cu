@@ -367,6 +367,15 @@ qem_status qem_read_mode_hist(qem_ctx* c, void* stream, uint64_t* h) {
 
 int64_t qem_kernel_launches(const qem_ctx* c) { return c ? c->launches : 0; }
 
+qem_status qem_set_kernel_events(qem_ctx* c, void* fwd_start, void* fwd_end, void* bwd_start, void* bwd_end) {
+  if (!c) return fail(QEM_INVALID_ARGUMENT, "null context");
+  c->ev[0] = fwd_start;
+  c->ev[1] = fwd_end;
+  c->ev[2] = bwd_start;
+  c->ev[3] = bwd_end;
+  return QEM_OK;
+}
+
 qem_status qem_copy_messages(qem_ctx* c, float* d_dg, double* d_c, void* stream) {
   if (!c || !d_dg || !d_c) return fail(QEM_INVALID_ARGUMENT, "null argument");
   if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "messages are two-level only");

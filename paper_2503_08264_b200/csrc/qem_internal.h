@@ -75,6 +75,7 @@ struct qem_ctx {
   cudaGraphExec_t graph;
   int graph_valid;
   int in_iterate;
+  void* ev[4];  // optional caller events around the pair-tile kernels (fwd start/end, bwd start/end)
   uint64_t graph_seed_;
   int64_t graph_launches_;
 };

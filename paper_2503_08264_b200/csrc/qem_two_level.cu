@@ -538,7 +538,9 @@ static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st
   prep_fn<D>(c->desc.obs_kind)<<<c->grid_prep, prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, a.J), st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (c->ev[0]) cudaEventRecord((cudaEvent_t)c->ev[0], st);
   fwd_fn<D>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
+  if (c->ev[1]) cudaEventRecord((cudaEvent_t)c->ev[1], st);
   c->launches += 3;
   return cudaGetLastError();
 }
@@ -551,7 +553,9 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int cp = pick_rp(K);
+  if (c->ev[2]) cudaEventRecord((cudaEvent_t)c->ev[2], st);
   bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
+  if (c->ev[3]) cudaEventRecord((cudaEvent_t)c->ev[3], st);
   c->launches += 2;
   return cudaGetLastError();
 }

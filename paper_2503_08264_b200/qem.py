@@ -186,6 +186,17 @@ class QEM:
         check(lib().qem_read_mode_hist(self.ctx, _stream(stream), h), "qem_read_mode_hist")
         return [int(v) for v in h]
 
+    def set_kernel_events(self, events=None) -> None:
+        """Record 4 torch.cuda.Event (fwd start/end, bwd start/end) around the pair-tile kernels."""
+        if events is None:
+            handles = [None] * 4
+        else:
+            for e in events:  # torch creates the CUDA event lazily
+                e.record()
+            handles = [ctypes.c_void_p(e.cuda_event) for e in events]
+        self._events = events
+        check(lib().qem_set_kernel_events(self.ctx, *handles), "qem_set_kernel_events")
+
     def kernel_launches(self) -> int:
         return int(lib().qem_kernel_launches(self.ctx))
 
