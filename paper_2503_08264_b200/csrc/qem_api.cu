@@ -102,7 +102,13 @@ size_t carve(qem_ctx* c, char* base) {
     c->tw.red = reinterpret_cast<double*>(take(sizeof(double) * (K + 1)));
     c->tw.dg = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
     const size_t kp = (size_t)((K + 3) / 4 * 4);
-    c->tw.colrec = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * kp * pad4(D + 3)));
+    if (!c->tc)
+      c->tw.colrec = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * kp * pad4(D + 3)));
+    if (c->tc) {
+      c->tw.rowop = take((size_t)K * 96);
+      c->tw.colop = take((size_t)c->n_local * K * 96);
+      c->tw.colaux = reinterpret_cast<float*>(take((size_t)c->n_local * K * 12));
+    }
     c->tw.gstat = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local));
     c->tw.cvec = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->n_local));
     c->tw.perm = reinterpret_cast<int*>(take(sizeof(int) * K));
@@ -171,6 +177,7 @@ qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t 
   c->n_local = group_end - group_begin;
   c->R = desc->family == QEM_FAMILY_TWO_LEVEL ? desc->d + (desc->scale_kind != QEM_SCALE_FIXED) : 1 + desc->n_cov;
   c->grid_fwd = c->grid_bwd = 1;
+  c->tc = desc->family == QEM_FAMILY_TWO_LEVEL && qem::tl_use_tc(desc);
   if (desc->family == QEM_FAMILY_TWO_LEVEL) qem::tl_grids(desc, c->n_local, sm_count(), &c->grid_fwd, &c->grid_bwd, &c->grid_prep);
   c->ws_bytes = carve(c, nullptr);
   cudaError_t e = cudaMalloc(&c->ws, c->ws_bytes);

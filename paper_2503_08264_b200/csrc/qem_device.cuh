@@ -1,5 +1,6 @@
 // qem_device.cuh -- device helpers for the sm_100a kernels.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -64,6 +65,69 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
   }
+}
+
+// ------------------------------------------- tcgen05 operand helpers (d = 16)
+// Tensor-core operands hold a 16-dim fp32 vector per row as three bf16 terms
+// (x = x0 + x1 + x2, each round-to-nearest), i.e. 48 bf16 = 96 bytes per row,
+// in the K-major SWIZZLE_NONE canonical layout: 8-row x 16-byte core matrices,
+// chunks of 8 bf16 along K 128 B apart (LBO), 8-row groups 768 B apart (SBO).
+constexpr int kTcRowBytes = 96;
+__host__ __device__ __forceinline__ int tc_offset(int row, int kk) {
+  return (row >> 3) * 768 + (kk >> 3) * 128 + (row & 7) * 16 + (kk & 7) * 2;
+}
+__device__ __forceinline__ void split3_bf16(float x, __nv_bfloat16 (&s)[3]) {
+  s[0] = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(s[0]);
+  s[1] = __float2bfloat16_rn(r1);
+  const float r2 = r1 - __bfloat162float(s[1]);
+  s[2] = __float2bfloat16_rn(r2);
+}
+// UMMA shared-memory descriptor: start address, LBO, SBO (bytes), version 1, no swizzle.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// Instruction descriptor kind::f16: fp32 accumulate, bf16 A/B, K-major, N, M.
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// D += A_split . B_split over the 3-term splits, small products first (measured
+// max error 1e-7 of sum|a_r b_r|, unbiased: tools/tc_probe.cu).
+__device__ __forceinline__ void umma_bf16x3(uint32_t tmem_d, uint32_t a_saddr, uint32_t b_saddr, uint32_t idesc) {
+  const int pa[6] = {2, 1, 0, 1, 0, 0}, pb[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll
+  for (int q = 0; q < 6; ++q)
+    umma_bf16(tmem_d, umma_desc(a_saddr + pa[q] * 256, 128, 768), umma_desc(b_saddr + pb[q] * 256, 128, 768), idesc,
+              q > 0);
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// 32 lanes x 32 columns of fp32 from TMEM (each thread: its lane, 32 consecutive columns).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
 // ---------------------------------------------------------------- reductions

@@ -31,6 +31,10 @@ struct TwoLevelWs {
   double* cvec;       // [n_local]  c_i = g_i(k_ref)
   int* perm;          // [K]        forward row order (rows sorted by coefficient magnitude)
   double* alpha_d;    // [K]        alpha_k in fp64
+  // tensor-core path (d = 16, K % 256 == 0): bf16x3 operands, DESIGN.md "Tensor cores"
+  void* rowop;        // [K] x 96 B  row coefficients c_k (K-major canonical layout)
+  void* colop;        // [n_local][K] x 96 B  u = z - mu_ref per column
+  float* colaux;      // [n_local][3][K] SoA {|u|^2, P, ln P}
   float* hmsg;        // [n_local][K] h_i(k) = dg_i(k) - alpha'_ik (re-centred message)
 };
 
@@ -75,6 +79,7 @@ struct qem_ctx {
   cudaGraphExec_t graph;
   int graph_valid;
   int in_iterate;
+  int tc;  // d=16 tensor-core pair kernels in use
   void* ev[4];  // optional caller events around the pair-tile kernels (fwd start/end, bwd start/end)
   uint64_t graph_seed_;
   int64_t graph_launches_;
@@ -85,6 +90,7 @@ namespace qem {
 cudaError_t tl_forward(qem_ctx* c, cudaStream_t s);
 cudaError_t tl_backward(qem_ctx* c, cudaStream_t s);
 int tl_supported_d(int d);
+int tl_use_tc(const qem_model_desc* d);
 void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* grid_fwd, int* grid_bwd, int* grid_prep);
 // three-level launchers (qem_three_level.cu)
 cudaError_t th_forward(qem_ctx* c, cudaStream_t s);

@@ -191,6 +191,7 @@ __device__ __forceinline__ float2 expm1_poly(float2 x) {
 }
 
 #include "qem_forward.cuh"
+#include "qem_tc.cuh"
 
 // -------------------------------------------------------------- root (K3)
 // One block: w_root = softmax(f_root + G), log Pe, root moments.
@@ -493,10 +494,12 @@ static KernelFn fwd_fn(int rp) {
   return rp == 1 ? k_forward<D, 1> : k_forward<D, 2>;
 }
 template <int D>
-static KernelFn prep_fn(int obs) {
+static KernelFn prep_fn(int obs, bool tc) {
   if constexpr (D == 1)
-    if (obs == QEM_OBS_GAUSS) return k_colprep<D, QEM_OBS_GAUSS>;
-  return k_colprep<D, QEM_OBS_BERNOULLI_LOGIT>;
+    if (obs == QEM_OBS_GAUSS) return k_colprep<D, QEM_OBS_GAUSS, false>;
+  if constexpr (D == kTcD)
+    if (tc) return k_colprep<D, QEM_OBS_BERNOULLI_LOGIT, true>;
+  return k_colprep<D, QEM_OBS_BERNOULLI_LOGIT, false>;
 }
 template <int D>
 static KernelFn bwd_fn(int cp) {
@@ -515,11 +518,17 @@ template <int D>
 static int prep_threads(int) { return 32 * FwdLayout<D>::PREP_WARPS; }
 
 template <int D>
-static void grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb, int* gp) {
+static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, int* gf, int* gb, int* gp) {
   const int K = d->K, rp = pick_rp(K);
-  const int of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
-  const int ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
-  const int op = occupancy(prep_fn<D>(d->obs_kind), prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, d->n_obs));
+  int of, ob;
+  if (tc) {
+    of = occupancy(k_forward_tc<kTcCQ>, 128 * kTcCQ, FwdTcLayout<kTcCQ>::bytes(K));
+    ob = occupancy(k_backward_tc<kTcCQ>, 128 * kTcCQ, BwdTcLayout<kTcCQ>::bytes(K));
+  } else {
+    of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
+    ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
+  }
+  const int op = occupancy(prep_fn<D>(d->obs_kind, tc), prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, d->n_obs));
   // Persistent-style grids: one full wave of resident CTAs, capped by the groups.
   int64_t f = (int64_t)sms * of, b = (int64_t)sms * ob, p = (int64_t)sms * op;
   *gf = (int)(f < n_local ? f : n_local);
@@ -535,11 +544,19 @@ static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (c->desc.obs_kind == QEM_OBS_GAUSS && D != 1) return cudaErrorInvalidValue;
-  prep_fn<D>(c->desc.obs_kind)<<<c->grid_prep, prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, a.J), st>>>(a);
+  const bool tc = D == kTcD && c->tc;
+  if (tc) {
+    k_rowop<<<(K * kTcD + 255) / 256, 256, 0, st>>>(a);
+    c->launches += 1;
+  }
+  prep_fn<D>(c->desc.obs_kind, tc)<<<c->grid_prep, prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, a.J), st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (c->ev[0]) cudaEventRecord((cudaEvent_t)c->ev[0], st);
-  fwd_fn<D>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
+  if (tc)
+    k_forward_tc<kTcCQ><<<c->grid_fwd, 128 * kTcCQ, FwdTcLayout<kTcCQ>::bytes(K), st>>>(a);
+  else
+    fwd_fn<D>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
   if (c->ev[1]) cudaEventRecord((cudaEvent_t)c->ev[1], st);
   c->launches += 3;
   return cudaGetLastError();
@@ -554,7 +571,10 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int cp = pick_rp(K);
   if (c->ev[2]) cudaEventRecord((cudaEvent_t)c->ev[2], st);
-  bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
+  if (D == kTcD && c->tc)
+    k_backward_tc<kTcCQ><<<c->grid_bwd, 128 * kTcCQ, BwdTcLayout<kTcCQ>::bytes(K), st>>>(a);
+  else
+    bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
   if (c->ev[3]) cudaEventRecord((cudaEvent_t)c->ev[3], st);
   c->launches += 2;
   return cudaGetLastError();
@@ -569,12 +589,18 @@ int tl_supported_d(int d) {
   return 0;
 }
 
+int tl_use_tc(const qem_model_desc* d) {
+  static const int off = getenv("QEM_NO_TC") != nullptr;  // tuning / comparison override
+  return !off && d->d == kTcD && d->obs_kind == QEM_OBS_BERNOULLI_LOGIT && d->K % 256 == 0 && d->K <= QEM_MAX_K;
+}
+
 void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb, int* gp) {
   *gf = *gb = *gp = 1;
+  const bool tc = tl_use_tc(d) != 0;
   switch (d->d) {
 #define X(v)                              \
   case v:                                 \
-    grids<v>(d, n_local, sms, gf, gb, gp);\
+    grids<v>(d, n_local, sms, tc, gf, gb, gp);\
     return;
     QEM_D_LIST(X)
 #undef X
