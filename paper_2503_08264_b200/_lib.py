@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqem.so")
+LIB_PATH = os.environ.get("QEM_LIB_OVERRIDE") or os.path.join(HERE, "libqem.so")  # override: tuning experiments
 
 FAMILY_TWO_LEVEL, FAMILY_THREE_LEVEL = 2, 3
 OK, INVALID_ARGUMENT, INVALID_MODEL, UNSUPPORTED, CUDA_ERROR = 0, 1, 2, 3, 4

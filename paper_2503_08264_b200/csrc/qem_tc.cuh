@@ -50,66 +50,78 @@ __device__ __forceinline__ void lds16(const float* p, float (&o)[16]) {
   }
 }
 
-// Forward epilogue, online log-sum-exp over t' = tm + gamma |u|^2 + ln P (the
-// row constant kappa is added at the end): state (st0 = running max, st1 = sum).
-template <int NCH>
-__device__ __forceinline__ void fwd_epi_online(uint32_t taddr, const float* u2, const float* lp, float g, float& st0,
-                                               float& st1) {
-#pragma unroll 1
-  for (int ch = 0; ch < NCH; ++ch) {
-    float v[32];
-    tmem_ld32(taddr + ch * 32, v);
+// Walk NC16 chunks of 16 TMEM columns with the next chunk's tcgen05.ld in
+// flight while the current one is processed (two register buffers).
+template <int NC16, class F>
+__device__ __forceinline__ void tmem_pipeline16(uint32_t taddr, F&& f) {
+  uint32_t r0[16], r1[16];
+  tmem_ld16_async(taddr, r0);
+  tmem_wait16(r0);
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      float a[16], b[16];
-      lds16(u2 + ch * 32 + hh * 16, a);
-      lds16(lp + ch * 32 + hh * 16, b);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) v[hh * 16 + c] = fmaf(g, a[c], v[hh * 16 + c]) + b[c];
+  for (int c = 0; c < NC16; ++c) {
+    if (c & 1) {
+      if (c + 1 < NC16) tmem_ld16_async(taddr + (c + 1) * 16, r0);
+      f(c, r1);
+      if (c + 1 < NC16) tmem_wait16(r0);
+    } else {
+      if (c + 1 < NC16) tmem_ld16_async(taddr + (c + 1) * 16, r1);
+      f(c, r0);
+      if (c + 1 < NC16) tmem_wait16(r1);
     }
-    // tree max and 8 independent partial sums (short dependency chains)
-    float mx[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) mx[q] = fmaxf(fmaxf(v[q], v[q + 8]), fmaxf(v[q + 16], v[q + 24]));
-    const float cm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-    const float mn = fmaxf(st0, cm);
-    const float nm = -mn * kLog2e;
-    float ps[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) ps[q] = 0.f;
-#pragma unroll
-    for (int c = 0; c < 32; ++c) ps[c & 7] += ex2(fmaf(v[c], kLog2e, nm));
-    const float tot = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-    st1 = fmaf(st1, ex2((st0 - mn) * kLog2e), tot);
-    st0 = mn;
   }
 }
 
+// Forward epilogue, online log-sum-exp over t' = tm + gamma |u|^2 + ln P (the
+// row constant kappa is added at the end): state (st0 = running max, st1 = sum).
+template <int NC16>
+__device__ __forceinline__ void fwd_epi_online(uint32_t taddr, const float* u2, const float* lp, float g, float& st0,
+                                               float& st1) {
+  tmem_pipeline16<NC16>(taddr, [&](int c16, uint32_t(&r)[16]) {
+    float a[16], b[16], v[16];
+    lds16(u2 + c16 * 16, a);
+    lds16(lp + c16 * 16, b);
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) {
+      const float2 t = add2(fma2(f2(g), make_float2(a[c], a[c + 1]), make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1]))),
+                            make_float2(b[c], b[c + 1]));
+      v[c] = t.x;
+      v[c + 1] = t.y;
+    }
+    float mx[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mx[q] = fmaxf(fmaxf(v[q], v[q + 4]), fmaxf(v[q + 8], v[q + 12]));
+    const float mn = fmaxf(st0, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));
+    const float nm = -mn * kLog2e;
+    float2 ps[2] = {f2(0.f), f2(0.f)};
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) {
+      const float2 e = fma2(make_float2(v[c], v[c + 1]), f2(kLog2e), f2(nm));
+      ps[(c >> 1) & 1] = add2(ps[(c >> 1) & 1], make_float2(ex2(e.x), ex2(e.y)));
+    }
+    const float2 tot = add2(ps[0], ps[1]);
+    st1 = fmaf(st1, ex2((st0 - mn) * kLog2e), tot.x + tot.y);
+    st0 = mn;
+  });
+}
+
 // Forward epilogue, polynomial mode: st0 += sum P expm1_N(tm + gamma |u|^2 + kappa).
-template <int N, int NCH>
+template <int N, int NC16>
 __device__ __forceinline__ void fwd_epi_poly(uint32_t taddr, const float* u2, const float* pp, float g, float kap,
                                              float& st0) {
-  float2 acc[4];
+  float2 acc[2] = {f2(0.f), f2(0.f)};
+  tmem_pipeline16<NC16>(taddr, [&](int c16, uint32_t(&r)[16]) {
+    float a[16], b[16];
+    lds16(u2 + c16 * 16, a);
+    lds16(pp + c16 * 16, b);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) acc[q] = f2(0.f);
-#pragma unroll 1
-  for (int ch = 0; ch < NCH; ++ch) {
-    float v[32];
-    tmem_ld32(taddr + ch * 32, v);
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      float a[16], b[16];
-      lds16(u2 + ch * 32 + hh * 16, a);
-      lds16(pp + ch * 32 + hh * 16, b);
-#pragma unroll
-      for (int c = 0; c < 16; c += 2) {
-        const float2 dp = add2(fma2(f2(g), make_float2(a[c], a[c + 1]), make_float2(v[hh * 16 + c], v[hh * 16 + c + 1])),
-                               f2(kap));
-        acc[(c >> 1) & 3] = fma2(make_float2(b[c], b[c + 1]), expm1_poly<N>(dp), acc[(c >> 1) & 3]);
-      }
+    for (int c = 0; c < 16; c += 2) {
+      const float2 dp =
+          add2(fma2(f2(g), make_float2(a[c], a[c + 1]), make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1]))),
+               f2(kap));
+      acc[(c >> 1) & 1] = fma2(make_float2(b[c], b[c + 1]), expm1_poly<N>(dp), acc[(c >> 1) & 1]);
     }
-  }
-  const float2 t2 = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+  });
+  const float2 t2 = add2(acc[0], acc[1]);
   st0 += t2.x + t2.y;
 }
 
@@ -131,7 +143,7 @@ template <int CQ>
 __global__ void __launch_bounds__(128 * CQ, 1) k_forward_tc(TLArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   using L = FwdTcLayout<CQ>;
-  constexpr int NT = 128 * CQ, CW = 256 / CQ, NCH = CW / 32;
+  constexpr int NT = 128 * CQ, CW = 256 / CQ, NC16 = CW / 16;
   const int K = a.K, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, cq = warp >> 2;
   const int NB = K / 256, RB = K / 128, TPG = NB * RB;
@@ -263,12 +275,12 @@ __global__ void __launch_bounds__(128 * CQ, 1) k_forward_tc(TLArgs a) {
     const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * CW) + ((uint32_t)(quarter * 32) << 16);
     float st0 = s_st0[cq * K + k], st1 = s_st1[cq * K + k];
     switch (md) {
-      case 0: fwd_epi_poly<3, NCH>(taddr, axb, axb + K, g, kap, st0); break;
-      case 1: fwd_epi_poly<4, NCH>(taddr, axb, axb + K, g, kap, st0); break;
-      case 2: fwd_epi_poly<5, NCH>(taddr, axb, axb + K, g, kap, st0); break;
-      case 3: fwd_epi_poly<7, NCH>(taddr, axb, axb + K, g, kap, st0); break;
-      case 4: fwd_epi_poly<9, NCH>(taddr, axb, axb + K, g, kap, st0); break;
-      default: fwd_epi_online<NCH>(taddr, axb, axb + 2 * K, g, st0, st1); break;
+      case 0: fwd_epi_poly<3, NC16>(taddr, axb, axb + K, g, kap, st0); break;
+      case 1: fwd_epi_poly<4, NC16>(taddr, axb, axb + K, g, kap, st0); break;
+      case 2: fwd_epi_poly<5, NC16>(taddr, axb, axb + K, g, kap, st0); break;
+      case 3: fwd_epi_poly<7, NC16>(taddr, axb, axb + K, g, kap, st0); break;
+      case 4: fwd_epi_poly<9, NC16>(taddr, axb, axb + K, g, kap, st0); break;
+      default: fwd_epi_online<NC16>(taddr, axb, axb + 2 * K, g, st0, st1); break;
     }
     s_st0[cq * K + k] = st0;
     s_st1[cq * K + k] = st1;
@@ -297,7 +309,7 @@ __global__ void __launch_bounds__(128 * CQ, 1) k_forward_tc(TLArgs a) {
 #pragma unroll
         for (int r = 0; r < kTcD; ++r) ap += (double)fc[2 + r] * (double)s_u0[r];
         const double dgd = ap + (double)h;
-        a.ws.hmsg[(size_t)i * K + k] = h;
+        a.ws.hmsg[(size_t)i * K + k] = h - s_kappa[k];  // TC path: the backward's row constant is -(h - kappa)
         a.ws.dg[(size_t)i * K + k] = (float)dgd;
         s_g[k] += dgd;
       }
@@ -347,13 +359,13 @@ template <int CQ>
 __global__ void __launch_bounds__(128 * CQ, 1) k_backward_tc(TLArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   using L = BwdTcLayout<CQ>;
-  constexpr int NT = 128 * CQ, NW = NT / 32, CW = 256 / CQ, NCH = CW / 32;
+  constexpr int NT = 128 * CQ, NW = NT / 32, CW = 256 / CQ, NC16 = CW / 16;
   const int K = a.K, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, cq = warp >> 2;
   const int CB = K / 128, RB = K / 256, TPG = CB * RB;
   unsigned char* s_rowop = smem;
   unsigned char* s_colop = smem + L::colop(K);
-  float* s_rt = reinterpret_cast<float*>(smem + L::rowtab(K));  // SoA [3][K]: gamma log2e, (kappa-h) log2e, w_root
+  float* s_rt = reinterpret_cast<float*>(smem + L::rowtab(K));  // SoA [2][K]: gamma log2e, (kappa-h) log2e + log2 w_root
   float* s_w = reinterpret_cast<float*>(smem + L::wsm(K));
   float* s_wp = reinterpret_cast<float*>(smem + L::wpart(K));
   double* s_red = reinterpret_cast<double*>(smem + L::red(K));  // [NW][16]
@@ -416,24 +428,12 @@ __global__ void __launch_bounds__(128 * CQ, 1) k_backward_tc(TLArgs a) {
     const int64_t J = j * CB + cb;
     const int64_t i = blockIdx.x + j * gridDim.x;
     if (t == 0) {
-      // ---- group row table: {gamma log2e, (kappa - h) log2e, w_root, 0}
-      float u0[kTcD];
-      float U0sq = 0.f;
-#pragma unroll
-      for (int r = 0; r < kTcD; ++r) {
-        u0[r] = a.q_m[i * kTcD + r] - a.ws.ref->mu_ref[r];
-        U0sq = fmaf(u0[r], u0[r], U0sq);
-      }
+      // ---- group row table (SoA): gamma log2e | (kappa - h) log2e + log2 w_root
       for (int k = tid; k < K; k += NT) {
-        const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
-        const float g = fc[1];
-        float kap = g * U0sq;
-#pragma unroll
-        for (int r = 0; r < kTcD; ++r) kap = fmaf(fc[2 + r], u0[r], kap);
-        const float h = a.ws.hmsg[(size_t)i * K + k];
-        s_rt[k] = g * kLog2e;
-        s_rt[K + k] = (-kap - h) * kLog2e;
-        s_rt[2 * K + k] = a.w_root[k];
+        // the TC forward stored h - kappa (kappa = -(gamma |u0|^2 + c . u0), the re-centring constant)
+        const float hk = a.ws.hmsg[(size_t)i * K + k];
+        s_rt[k] = a.ws.fwd_coef[(size_t)k * (kTcD + 2) + 1] * kLog2e;
+        s_rt[K + k] = -hk * kLog2e + log2f(a.w_root[k]);  // w_root folded in (log2 0 = -inf)
       }
       __syncthreads();
     }
@@ -450,26 +450,25 @@ __global__ void __launch_bounds__(128 * CQ, 1) k_backward_tc(TLArgs a) {
     // ---- epilogue: column k', rows rb*256 + cq*CW .. +CW
     const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * CW) + ((uint32_t)(quarter * 32) << 16);
     const float* rt = s_rt + rb * 256 + cq * CW;
-    float wp[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-    for (int ch = 0; ch < NCH; ++ch) {
-      float v[32];
-      tmem_ld32(taddr + ch * 32, v);
+    // pairs of rows as float2 (FFMA2/FADD2); w_root is folded into the row
+    // constant as log2(w), so each pair costs 3 FMA-pipe lane-ops + 1 ex2 + 1 add
+    float2 wp[2] = {f2(0.f), f2(0.f)};
+    tmem_pipeline16<NC16>(taddr, [&](int c16, uint32_t(&r)[16]) {
+      float gg[16], rc[16];
+      lds16(rt + c16 * 16, gg);
+      lds16(rt + K + c16 * 16, rc);
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        float gg[16], rc[16], wr[16];
-        lds16(rt + ch * 32 + hh * 16, gg);
-        lds16(rt + K + ch * 32 + hh * 16, rc);
-        lds16(rt + 2 * K + ch * 32 + hh * 16, wr);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float x = fmaf(v[hh * 16 + c], kLog2e, rc[c]);
-          x = fmaf(gg[c], U2, x) + Lc;
-          wp[c & 3] = fmaf(wr[c], ex2(x), wp[c & 3]);  // 4 independent accumulation chains
-        }
+      for (int c = 0; c < 16; c += 2) {
+        float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), f2(kLog2e),
+                        make_float2(rc[c], rc[c + 1]));
+        x = add2(fma2(make_float2(gg[c], gg[c + 1]), f2(U2), x), f2(Lc));
+        wp[(c >> 1) & 1] = add2(wp[(c >> 1) & 1], make_float2(ex2(x.x), ex2(x.y)));
       }
+    });
+    {
+      const float2 t2 = add2(wp[0], wp[1]);
+      wacc += t2.x + t2.y;
     }
-    wacc += (wp[0] + wp[1]) + (wp[2] + wp[3]);
     if (rb == RB - 1) {
       s_wp[cq * 128 + r_in] = wacc;
       __syncthreads();
