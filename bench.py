@@ -39,13 +39,34 @@ SMS = 148
 SM_MAX_MHZ = 1965.0
 
 
-def pair_ceiling(d: int, mhz: float = SM_MAX_MHZ) -> dict:
-    """Pairs/s ceiling of ONE pass (forward or backward) from the binding pipe."""
+def pair_ceiling(d: int, tc: bool = False, mhz: float = SM_MAX_MHZ) -> dict:
+    """Pairs/s ceiling of ONE pass (forward or backward) from the binding pipe.
+
+    FFMA tiles (tc False): 1 exp (MUFU) + d+2 FP32 lane-ops per pair.
+    tcgen05 tiles (tc True, d = 16): the d-term contraction runs on the tensor
+    cores (bf16x3: 6 bf16 products = 12 d flops/pair, ceiling from the measured
+    bf16 peak), leaving 1 exp + 3 FP32 lane-ops per pair on the SM pipes."""
     f = mhz * 1e6 * SMS
     sfu = f * SFU_PER_SM_CLK / 1.0
-    fp32 = f * FP32_PER_SM_CLK / (d + 2.0)
-    return {"pairs_per_s": min(sfu, fp32), "pipe": "sfu" if sfu <= fp32 else "fp32",
-            "sfu_pairs_per_s": sfu, "fp32_pairs_per_s": fp32}
+    fp32 = f * FP32_PER_SM_CLK / (3.0 if tc else d + 2.0)
+    out = {"sfu_pairs_per_s": sfu, "fp32_pairs_per_s": fp32}
+    pipes = {"sfu": sfu, "fp32": fp32}
+    if tc:
+        out["tensor_pairs_per_s"] = pipes["tensor"] = BF16_TFLOPS * 1e12 / (12.0 * d)
+    pipe = min(pipes, key=pipes.get)
+    out.update(pairs_per_s=pipes[pipe], pipe=pipe)
+    return out
+
+
+def _measured_bf16() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 2250.0  # nominal dense bf16 (B200_PROFILING.md fallback)
+
+
+BF16_TFLOPS = _measured_bf16()
 
 
 class ClockSampler:
@@ -168,26 +189,31 @@ def run_gpu(args):
     def allreduce():
         runner.allreduce_plate_sum()
 
+    launched = [0]
+
     def step(t, ev=None):
         # ev: [fwd kernel start, fwd kernel end, bwd kernel start, bwd kernel end, allreduce start, end]
         if ev:
             g.set_kernel_events(ev[:4])
         g.sample_q(seed=seed, iter=t)
+        launched[0] += g.kernel_launches()
         g.estep_forward()
+        launched[0] += g.kernel_launches()
         if ev:
             ev[4].record(stream)
         allreduce()
         if ev:
             ev[5].record(stream)
         g.estep_backward()
+        launched[0] += g.kernel_launches()
         g.mstep(t)
+        launched[0] += g.kernel_launches()
 
     t = 1
     for _ in range(args.warmup):
         step(t)
         t += 1
     torch.cuda.synchronize()
-    launches_per_step = 0
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
@@ -196,6 +222,7 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    launched[0] = 0
     start.record(stream)
     for s in range(args.steps):
         step(t, evs[s])
@@ -211,8 +238,8 @@ def run_gpu(args):
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     bwd_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
     comm_ms = sum(e[4].elapsed_time(e[5]) for e in evs) / args.steps
-    # launches: sample(1) + forward(root_prep, colprep, forward) + backward(root, backward) + mstep(1)
-    launches_per_step = 7
+    # libqem kernels launched in the timed region (qem_kernel_launches after every call)
+    n_launched = launched[0]
     flags, clamps = g.read_flags()
     if world > 1:
         tt = torch.tensor([ms_total, fwd_ms, bwd_ms, comm_ms], dtype=torch.float64, device=dev)
@@ -230,14 +257,20 @@ def run_gpu(args):
     # ----------------------------------------------------------- roofline
     local_pairs = (ge - gb) * m.K * m.K
     dom, dom_ms = ("forward", fwd_ms) if fwd_ms >= bwd_ms else ("backward", bwd_ms)
-    ceil = pair_ceiling(m.d)
+    tc = g.pair_path() == 1
+    ceil = pair_ceiling(m.d, tc)
     achieved = local_pairs / (dom_ms * 1e-3)
-    roof = {"bound": "alu", "pipe": ceil["pipe"], "kernel": f"k_{dom}", "unit": "Gpair/s",
+    per_pair = ({"exp": 1, "fp32": 3, "tensor_bf16_flops": 12 * m.d} if tc else {"exp": 1, "fp32": m.d + 2})
+    roof = {"bound": "alu", "pipe": ceil["pipe"], "kernel": f"k_{dom}" + ("_tc" if tc else ""), "unit": "Gpair/s",
             "achieved": achieved / 1e9, "peak": ceil["pairs_per_s"] / 1e9,
             "frac": achieved / ceil["pairs_per_s"], "traffic": None,
-            "per_pair": {"exp": 1, "fp32": m.d + 2},
-            "peak_basis": f"{SMS} SMs x {SM_MAX_MHZ:.0f} MHz x min({SFU_PER_SM_CLK:.0f} MUFU.EX2/clk, "
-                          f"{FP32_PER_SM_CLK:.0f} FP32/clk / (d+2)) per pass (DESIGN.md Roofline)",
+            "per_pair": per_pair,
+            "pipe_ceilings_gpair_s": {k.replace("_pairs_per_s", ""): v / 1e9 for k, v in ceil.items()
+                                      if k.endswith("_pairs_per_s") and k != "pairs_per_s"},
+            "peak_basis": (f"{SMS} SMs x {SM_MAX_MHZ:.0f} MHz x {SFU_PER_SM_CLK:.0f} MUFU.EX2/clk (1 exp per pair "
+                           f"per pass); tensor and FP32 ceilings beside it (DESIGN.md Roofline)" if tc else
+                           f"{SMS} SMs x {SM_MAX_MHZ:.0f} MHz x min({SFU_PER_SM_CLK:.0f} MUFU.EX2/clk, "
+                           f"{FP32_PER_SM_CLK:.0f} FP32/clk / (d+2)) per pass (DESIGN.md Roofline)"),
             "kernels_ms": {"forward": fwd_ms, "backward": bwd_ms, "allreduce": comm_ms}}
     if rank != 0:
         if world > 1:
@@ -273,7 +306,7 @@ def run_gpu(args):
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": n_launched,
         "clocks": clk,
         "flags": {"device_flags": flags, "var_clamps": clamps},
     }

@@ -219,6 +219,14 @@ qem_status qem_set_kernel_events(qem_ctx* ctx, void* fwd_start, void* fwd_end, v
    gpu_launches claim). */
 int64_t qem_kernel_launches(const qem_ctx* ctx);
 
+/* Which pair-tile kernels this context runs (fixed at qem_create):
+   0 = FP32 FFMA/SFU tiles (k_forward / k_backward, every d);
+   1 = tcgen05 tensor-core tiles (k_forward_tc / k_backward_tc: d = 16,
+       Bernoulli-logit observations, K % 256 == 0; the K x K x d cross term
+       c_k . u_k' on the tensor cores in bf16x3).
+   The bench uses it to name the binding pipe of its roofline.  -1 on NULL. */
+int32_t qem_pair_path(const qem_ctx* ctx);
+
 /* Copy the per-group reference-differenced messages Delta g_i(k)
    (float [n_local][K]) and per-group constants c_i (double [n_local]) of the
    last forward pass into caller buffers (stream-ordered D2D copies):

@@ -19,7 +19,7 @@ FLAG_DEGENERATE, FLAG_NAN, FLAG_CLAMP = 1, 2, 4
 EXPORTS = [
     "qem_model_validate", "qem_shard_range", "qem_create", "qem_destroy", "qem_bind", "qem_sample_q",
     "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_mstep", "qem_iterate",
-    "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_copy_messages", "qem_status_str", "qem_last_error",
+    "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_pair_path", "qem_copy_messages", "qem_status_str", "qem_last_error",
     "qem_version",
 ]
 
@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
         L.qem_set_kernel_events.restype = i32
         L.qem_kernel_launches.argtypes = [vp]
         L.qem_kernel_launches.restype = i64
+        L.qem_pair_path.argtypes = [vp]
+        L.qem_pair_path.restype = i32
         L.qem_copy_messages.argtypes = [vp, vp, vp, vp]
         L.qem_status_str.argtypes = [i32]
         L.qem_status_str.restype = ctypes.c_char_p

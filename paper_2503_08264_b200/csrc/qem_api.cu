@@ -374,6 +374,8 @@ qem_status qem_read_mode_hist(qem_ctx* c, void* stream, uint64_t* h) {
 
 int64_t qem_kernel_launches(const qem_ctx* c) { return c ? c->launches : 0; }
 
+int32_t qem_pair_path(const qem_ctx* c) { return c ? (c->tc ? 1 : 0) : -1; }
+
 qem_status qem_set_kernel_events(qem_ctx* c, void* fwd_start, void* fwd_end, void* bwd_start, void* bwd_end) {
   if (!c) return fail(QEM_INVALID_ARGUMENT, "null context");
   c->ev[0] = fwd_start;

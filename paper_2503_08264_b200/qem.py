@@ -200,6 +200,10 @@ class QEM:
     def kernel_launches(self) -> int:
         return int(lib().qem_kernel_launches(self.ctx))
 
+    def pair_path(self) -> int:
+        """0 = FP32/SFU pair tiles, 1 = tcgen05 tensor-core pair tiles (d = 16)."""
+        return int(lib().qem_pair_path(self.ctx))
+
     def messages(self):
         """(Delta g [n_local][K] f32, c [n_local] f64) of the last forward (device tensors)."""
         dg = torch.empty(self.n_local, self.m.K, dtype=torch.float32, device=self.device)
