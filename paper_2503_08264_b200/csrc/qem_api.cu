@@ -106,14 +106,20 @@ size_t carve(qem_ctx* c, char* base) {
       c->tw.colrec = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * kp * pad4(D + 3)));
     if (c->tc) {
       c->tw.rowop = take((size_t)K * 96);
-      c->tw.colop = take((size_t)c->n_local * K * 96);
-      c->tw.colaux = reinterpret_cast<float*>(take((size_t)c->n_local * K * 12));
+      c->tw.rowop_x = take((size_t)K * 32);
+      c->tw.colop = take((size_t)c->n_local * K * 128);
+      c->tw.colaux = reinterpret_cast<float*>(take((size_t)c->n_local * K * 8));
+      c->tw.gmode = reinterpret_cast<int*>(take(sizeof(int) * (size_t)c->n_local));
+      c->tw.rowop_b = take((size_t)K * 96);
+      c->tw.bgam = reinterpret_cast<float*>(take(sizeof(float) * K));
     }
     c->tw.gstat = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local));
     c->tw.cvec = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->n_local));
     c->tw.perm = reinterpret_cast<int*>(take(sizeof(int) * K));
     c->tw.alpha_d = reinterpret_cast<double*>(take(sizeof(double) * K));
     c->tw.hmsg = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
+    c->tw.tA = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->n_local * K));
+    c->tw.bwd_coef = reinterpret_cast<float*>(take(sizeof(float) * K * (D + 1)));
   } else {
     const int64_t A = d.n, AB = d.n * d.n_sub, KK = (int64_t)K * K;
     c->th.f_root = reinterpret_cast<double*>(take(sizeof(double) * K));

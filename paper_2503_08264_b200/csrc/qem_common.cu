@@ -5,6 +5,21 @@
 
 namespace qem {
 
+// n / d for 32-bit n by a runtime-constant d via multiply-high (Granlund-Montgomery):
+// q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1.
+struct FastDiv {
+  uint32_t d, m, l;
+  __host__ void init(uint32_t div) {
+    d = div;
+    l = 0;
+    while ((1ull << l) < div) ++l;
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> l);
+  }
+};
+
 struct SampleLevel {
   float* z;            // [inst][dims][K]
   const float* qm;     // [inst*dims]
@@ -15,6 +30,7 @@ struct SampleLevel {
   int dims;
   int level;
   int64_t inst_offset; // global instance index of local instance 0
+  FastDiv fdims;
 };
 
 struct SampleArgs {
@@ -22,7 +38,8 @@ struct SampleArgs {
   int nlev;
   int K;
   int quads_per_row;
-  int64_t total_quads;
+  FastDiv fqpr;
+  int64_t total_quads;  // < 2^31 (checked at launch)
   uint2 key;
   int t_host;
   const int32_t* d_iter;
@@ -33,16 +50,17 @@ struct SampleArgs {
 // One thread = 4 consecutive samples k of one latent dim (one Philox call,
 // two Box-Muller pairs).
 __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= a.total_quads) return;
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (uint32_t)a.total_quads) return;
   int L = 0;
 #pragma unroll
   for (int l = 1; l < 3; ++l)
-    if (l < a.nlev && q >= a.lv[l].quads_begin) L = l;
+    if (l < a.nlev && q >= (uint32_t)a.lv[l].quads_begin) L = l;
   const SampleLevel& s = a.lv[L];
-  const int64_t local = q - s.quads_begin;
-  const int64_t row = local / a.quads_per_row;
-  const int k0 = (int)(local - row * a.quads_per_row) * 4;
+  const uint32_t local = q - (uint32_t)s.quads_begin;
+  const uint32_t row32 = a.fqpr.div(local);
+  const int64_t row = row32;
+  const int k0 = (int)(local - row32 * (uint32_t)a.quads_per_row) * 4;
   const float m = s.qm[row];
   const float sd = __fsqrt_rn(s.qv[row]);
   float e[4];
@@ -51,8 +69,8 @@ __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
     for (int j = 0; j < 4; ++j) e[j] = (k0 + j < a.K) ? s.eps[row * a.K + k0 + j] : 0.f;
   } else {
     const int t = resolve_iter(a.t_host, a.d_iter);
-    const int64_t inst = row / s.dims;
-    const int dim = (int)(row - inst * s.dims);
+    const uint32_t inst = s.fdims.div(row32);
+    const int dim = (int)(row32 - inst * (uint32_t)s.dims);
     const uint32_t ginst = (uint32_t)(inst + s.inst_offset);
     const uint4 o = philox4x32_10(
         make_uint4((uint32_t)(k0 >> 2), (uint32_t)dim, ginst, ((uint32_t)s.level << 24) | ((uint32_t)t & 0xffffffu)),
@@ -87,6 +105,7 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
   const int K = c->desc.K;
   a.K = K;
   a.quads_per_row = (K + 3) / 4;
+  a.fqpr.init((uint32_t)a.quads_per_row);
   a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   a.t_host = iter;
   a.d_iter = &c->cnt->iter;
@@ -116,6 +135,7 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
     s.eps = d_eps ? d_eps[l] : nullptr;
     s.rows = inst * dims;
     s.dims = (int)dims;
+    s.fdims.init((uint32_t)dims);
     s.level = l;
     s.inst_offset = off;
     s.quads_begin = quads;
@@ -126,6 +146,7 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
   const int threads = 256;
   const int64_t blocks = (quads + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
+  if (quads >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;  // 32-bit sample indexing
   k_sample<<<(unsigned)blocks, threads, 0, st>>>(a);
   c->launches += 1;
   return cudaGetLastError();

@@ -55,6 +55,23 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Bulk prefetch of a global range into L2 (bytes % 16 == 0).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// Named barrier `id` (1..15) over `n` threads (a multiple of 32).
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// three-input max (FMNMX3 on sm_100a)
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   const uint32_t a = smem_u32(bar);
@@ -82,6 +99,27 @@ __device__ __forceinline__ void split3_bf16(float x, __nv_bfloat16 (&s)[3]) {
   s[1] = __float2bfloat16_rn(r1);
   const float r2 = r1 - __bfloat162float(s[1]);
   s[2] = __float2bfloat16_rn(r2);
+}
+// Column operand of the restructured tensor-core path: 128 B per column =
+// the 3 x 16 bf16 split of u (chunks 0-5) + one 16-entry "extra" K-slab
+// (chunks 6-7); 8-row groups 1024 B apart.
+constexpr int kTcColBytes = 128;
+// Row-extra operand (forward A-extra / backward B-extra): one 16-entry slab,
+// 32 B per row, 8-row groups 256 B apart.
+constexpr int kTcRowXBytes = 32;
+__host__ __device__ __forceinline__ int tc_col_offset(int row, int kk) {
+  return (row >> 3) * 1024 + (kk >> 3) * 128 + (row & 7) * 16 + (kk & 7) * 2;
+}
+__host__ __device__ __forceinline__ int tc_rowx_offset(int row, int kk) {
+  return (row >> 3) * 256 + (kk >> 3) * 128 + (row & 7) * 16 + (kk & 7) * 2;
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(__nv_bfloat16 lo, __nv_bfloat16 hi) {
+  return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+}
+// 8 bf16 (as floats already representable in bf16, or rounded) -> one 16-byte core-matrix row
+__device__ __forceinline__ uint4 pack8_bf16(const __nv_bfloat16 (&v)[8]) {
+  return make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                    pack_bf16x2(v[6], v[7]));
 }
 // UMMA shared-memory descriptor: start address, LBO, SBO (bytes), version 1, no swizzle.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {

@@ -147,7 +147,7 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
 // ------------------------------------------------------------------ K2a
 // One WARP per group (warp-shuffle reductions only, no block barriers); the
 // CTA's warps work on different groups.
-template <int D, int OBS, bool TC>
+template <int D, int OBS, bool TC_UNUSED>
 __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int CS = pad4(D + 3);
@@ -238,22 +238,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
         const double u = (double)zr[r] - (double)ref.mu_ref[r];
         U2d += u * u;
       }
-      if constexpr (TC) {
-        // tensor-core column operand: u = z - mu_ref split into 3 bf16 terms
-        // (K-major canonical layout, tc_col_offset), plus {|u|^2, P, ln P}
-        unsigned char* cop = reinterpret_cast<unsigned char*>(a.ws.colop) + (size_t)i * K * kTcRowBytes;
-        float U2f = 0.f;
-#pragma unroll
-        for (int r = 0; r < D; ++r) {
-          const float u = zr[r] - ref.mu_ref[r];
-          U2f = fmaf(u, u, U2f);
-          __nv_bfloat16 s3[3];
-          split3_bf16(u, s3);
-#pragma unroll
-          for (int q = 0; q < 3; ++q) *reinterpret_cast<__nv_bfloat16*>(cop + tc_offset(kc, q * 16 + r)) = s3[q];
-        }
-        a.ws.colaux[(size_t)i * 3 * K + kc] = U2f;
-      } else {
+      {
 #pragma unroll
         for (int r = D; r < CS; ++r) rec[r] = 0.f;
         rec[D] = W2;
@@ -263,12 +248,13 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
           dst[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
       }
       const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
+      a.ws.tA[(size_t)i * K + kc] = t;  // t_ref, for the backward's k*-row softmax
       tref[kc] = t;
       tmax = fmax(tmax, t);
       u2max = fmaxf(u2max, W2);
     }
     // padding columns: P = 0, ln P = -inf (contribute nothing)
-    if constexpr (!TC) {
+    {
       for (int kc = K + lane; kc < Kp; kc += 32) {
         float4* dst = reinterpret_cast<float4*>(rec0 + (size_t)kc * CS);
 #pragma unroll
@@ -283,11 +269,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
     const double logS = log(warp_sum(s));
     for (int kc = lane; kc < K; kc += 32) {
       const float lp = (float)(tref[kc] - M - logS);
-      if constexpr (TC) {
-        float* ax = a.ws.colaux + (size_t)i * 3 * K;  // SoA: |u|^2, P, ln P
-        ax[K + kc] = expf(lp);
-        ax[2 * K + kc] = lp;
-      } else {
+      {
         float* pc = rec0 + (size_t)kc * CS;
         pc[D + 1] = expf(lp);
         pc[D + 2] = lp;

@@ -14,7 +14,10 @@ struct RefInfo {
   double e_ref;             // 1 / V_ref
   double bref_const;        // -(d/2)(ln 2pi + ln V_ref)
   int k_ref;
-  int pad;
+  int k_star;               // backward reference: argmax_k w_root(k) (tensor-core path)
+  float mu_star[QEM_MAX_D]; // parent mean of root sample k_star
+  double e_star;            // 1 / V_star
+  double bstar_const;       // -(d/2)(ln 2pi + ln V_star)
 };
 
 // Two-level workspace (device pointers, carved out of one allocation).
@@ -32,9 +35,15 @@ struct TwoLevelWs {
   int* perm;          // [K]        forward row order (rows sorted by coefficient magnitude)
   double* alpha_d;    // [K]        alpha_k in fp64
   // tensor-core path (d = 16, K % 256 == 0): bf16x3 operands, DESIGN.md "Tensor cores"
-  void* rowop;        // [K] x 96 B  row coefficients c_k (K-major canonical layout)
-  void* colop;        // [n_local][K] x 96 B  u = z - mu_ref per column
-  float* colaux;      // [n_local][3][K] SoA {|u|^2, P, ln P}
+  void* rowop;        // [K] x 96 B  log2e c_k split in 3 bf16 (K-major canonical layout)
+  void* rowop_x;      // [K] x 32 B  forward row extra slab (log2e gamma_k pattern, lP switch)
+  void* colop;        // [n_local][K] x 128 B  u = z - mu_ref split + column extra slab
+  float* colaux;      // [n_local][2][K] SoA {P, ln P}
+  int* gmode;         // [n_local]  forward tile mode of the group (decided in k_colprep_tc)
+  double* tA;         // [n_local][K] t_ref(k') = B(k_ref,k') + A_i(k'), A = sum_j log p(x_ij|z^k') - log q(z^k') (fp64)
+  void* rowop_b;      // [K] x 96 B  backward rows: log2e (e_k mu_k - e_* mu_*) split (k_star-differenced)
+  float* bgam;        // [K]        backward log2e gamma*_k = -log2e (e_k - e_*) / 2
+  float* bwd_coef;    // [K][D+1]   FFMA backward rows: Eb_k = e_k mu_k - e_* mu_* (D), Eg_k = -(e_k - e_*)/2
   float* hmsg;        // [n_local][K] h_i(k) = dg_i(k) - alpha'_ik (re-centred message)
 };
 

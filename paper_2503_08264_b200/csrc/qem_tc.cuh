@@ -1,52 +1,340 @@
 // qem_tc.cuh -- tcgen05 tensor-core pair-tile kernels for d = 16 (config 5).
-// Included inside namespace qem by qem_two_level.cu (needs TLArgs, expm1_poly).
+// Included inside namespace qem by qem_two_level.cu (needs TLArgs, inv_fact).
 //
-// The d-dim part of every log-factor is a dense contraction over the latent
-// dimension: D_k(k') = alpha_k + gamma_k |u_k'|^2 + c_k . u_k'  (DESIGN.md
-// "Forward"), so the K x K x 16 product c . u runs on the 5th-gen tensor
-// cores: tcgen05.mma kind::f16 with both operands split into three bf16 terms
-// and the six leading partial products accumulated small-first in TMEM
-// (fp32-exact to ~1e-7 of sum|c_r u_r|, unbiased; tools/tc_probe.cu).  The
-// exp / log-sum-exp epilogue reads the 128 x 256 fp32 tile from TMEM
-// (tcgen05.ld) and runs on the SFU / FMA pipes while the next tile's MMAs run
-// into the other half of TMEM (2 x 256 columns).  One CTA per SM; 4*CQ warps:
-// warp w reads TMEM lane quarter (w % 4) and column slice (w / 4) of width 256/CQ.
+// Every log-factor of a pair is an affine function of a 16-dim contraction
+// ("Tensor cores"):
+//   log2e * (D_k(k') + ln P(k')) = c2_k . u_k' + g2_k |u_k'|^2 + lP(k') + const_k,
+// with c2 = log2e c, g2 = log2e gamma, lP = log2e ln P, u = z - mu_ref.  The
+// whole expression up to the row constant runs on the 5th-gen tensor cores as
+// ONE accumulation into TMEM (kind::f16, fp32 accumulate):
+//   6 MMAs  c2 . u       both operands split into three bf16 terms, the six
+//                        leading partial products small-first (tools/tc_probe.cu)
+//   1 MMA   the "extra" K-slab: row entries [g0 g0 g1 g0 g2 g1 | 1 1 1 | rho0 rho1 rho2]
+//                        x column entries  [U0 U1 U0 U2 U0 U1 | lP0 lP1 lP2 | 1 1 1]
+//           (U = |u|^2 and lP split in three bf16; rho = backward row constant)
+// so the epilogue per pair is one tcgen05.ld'd value -> ex2 -> add: the SFU
+// (MUFU.EX2, 16/clk/SM) and the TMEM read port (64 B/clk/SM) are the ceilings.
 //
-//  k_rowop           c_k -> bf16x3 operand (K rows x 96 B), once per E-step
-//  k_forward_tc<CQ>  M = 128 parent rows (static operand, resident in SMEM) x
-//                    N = 256 child columns (per-group operand, TMA double buffer);
-//                    thread = row x column slice; same tile modes as k_forward
-//  k_backward_tc<CQ> M = 128 child columns (per-group operand) x N = 256 parent
-//                    rows (static); thread = column x row slice
+// Warp roles (one CTA per SM, persistent over groups): warps 0-15 epilogue
+// (warp w reads TMEM lane quarter w%4 and column slice w/4), warp 16 TMA
+// producer (cp.async.bulk), warp 17 MMA issuer (one thread).  All hand-offs are
+// mbarriers: operand stages full/empty, TMEM accumulator buffers (2 x 256
+// columns) full/empty; epilogue-only sync uses named barriers.
+//
+//  k_rowop_tc     c2 -> rowop_c (K x 96 B), forward row extra -> rowop_x (K x 32 B)
+//  k_colprep_tc   K2a for d = 16 Bernoulli: unary terms, reference softmax, the
+//                 group's tile mode, column operand (128 B per column) + {P, ln P}
+//  k_forward_tc   M = 128 parent rows (streamed, static) x N = 256 child columns
+//                 (per group); thread = row, online log-sum-exp / expm1 polynomial
+//  k_backward_tc  M = 128 child columns (per group) x N = 256 parent rows
+//                 (static + per-group extra slab built in SMEM); thread = column
 #pragma once
 
 constexpr int kTcD = 16;
-constexpr uint32_t kTcColBlockBytes = 256 * kTcRowBytes;  // forward B tile (256 columns)
-constexpr uint32_t kTcBwdBlockBytes = 128 * kTcRowBytes;  // backward A tile (128 columns)
-constexpr int kTcCQ = 4;                                  // column slices per TMEM lane quarter
+constexpr int kTcEpiWarps = 16;
+constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;  // + TMA warp + MMA warp
+constexpr int kTcEpiThreads = kTcEpiWarps * 32;
+constexpr int kTcRowCBytes = kTcRowBytes;  // 96: c2 split (6 chunks)
 
-__global__ void __launch_bounds__(256) k_rowop(TLArgs a) {
-  const int K = a.K;
-  unsigned char* rop = reinterpret_cast<unsigned char*>(a.ws.rowop);
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * kTcD; e += gridDim.x * blockDim.x) {
-    const int k = e / kTcD, r = e % kTcD;
-    __nv_bfloat16 s3[3];
-    split3_bf16(a.ws.fwd_coef[(size_t)k * (kTcD + 2) + 2 + r], s3);
+// named barriers: 1 = all epilogue warps, 2..5 = the 4 warps of one TMEM lane quarter
+__device__ __forceinline__ void epi_bar() { named_bar(1, kTcEpiThreads); }
+__device__ __forceinline__ void quarter_bar(int q) { named_bar(2 + q, 128); }
+
+// bf16x3 split of the 16-entry extra slab of a row / column (two 16-byte chunks)
+__device__ __forceinline__ void extra_row(float g2, float lp_on, float rho, uint4& c0, uint4& c1) {
+  __nv_bfloat16 g[3], r[3];
+  split3_bf16(g2, g);
+  split3_bf16(rho, r);
+  const __nv_bfloat16 z = __float2bfloat16_rn(0.f), on = __float2bfloat16_rn(lp_on);
+  const __nv_bfloat16 a[8] = {g[0], g[0], g[1], g[0], g[2], g[1], on, on};
+  const __nv_bfloat16 b[8] = {on, r[0], r[1], r[2], z, z, z, z};
+  c0 = pack8_bf16(a);
+  c1 = pack8_bf16(b);
+}
+__device__ __forceinline__ void extra_col(float U, float lp, uint4& c0, uint4& c1) {
+  __nv_bfloat16 u[3], l[3];
+  split3_bf16(U, u);
+  split3_bf16(lp, l);
+  const __nv_bfloat16 z = __float2bfloat16_rn(0.f), one = __float2bfloat16_rn(1.f);
+  const __nv_bfloat16 a[8] = {u[0], u[1], u[0], u[2], u[0], u[1], l[0], l[1]};
+  const __nv_bfloat16 b[8] = {l[2], one, one, one, z, z, z, z};
+  c0 = pack8_bf16(a);
+  c1 = pack8_bf16(b);
+}
+
+// 7 MMAs of one 128 x 256 tile: 6 split products (small first) + the extra slab.
+__device__ __forceinline__ void umma_tile7(uint32_t tmem_d, uint32_t a_c, uint32_t a_sbo, uint32_t b_c, uint32_t b_sbo,
+                                           uint32_t a_x, uint32_t a_xsbo, uint32_t b_x, uint32_t b_xsbo,
+                                           uint32_t idesc) {
+  const int pa[6] = {2, 1, 0, 1, 0, 0}, pb[6] = {0, 1, 2, 0, 1, 0};
 #pragma unroll
-    for (int q = 0; q < 3; ++q) *reinterpret_cast<__nv_bfloat16*>(rop + tc_offset(k, q * 16 + r)) = s3[q];
+  for (int q = 0; q < 6; ++q)
+    umma_bf16(tmem_d, umma_desc(a_c + pa[q] * 256, 128, a_sbo), umma_desc(b_c + pb[q] * 256, 128, b_sbo), idesc,
+              q > 0);
+  umma_bf16(tmem_d, umma_desc(a_x, 128, a_xsbo), umma_desc(b_x, 128, b_xsbo), idesc, 1u);
+}
+
+// 16-dim row vector -> bf16x3 split in the 96-byte canonical row layout (tc_offset)
+__device__ __forceinline__ void store_row_split16(unsigned char* base, int k, const float (&v)[kTcD]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // 8 dims per 16-byte chunk
+    __nv_bfloat16 s[3][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      __nv_bfloat16 t[3];
+      split3_bf16(v[8 * h + r], t);
+      s[0][r] = t[0];
+      s[1][r] = t[1];
+      s[2][r] = t[2];
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) *reinterpret_cast<uint4*>(base + tc_offset(k, q * 16 + 8 * h)) = pack8_bf16(s[q]);
   }
 }
 
+template <int D>
+__device__ __forceinline__ double root_lnv(const TLArgs& a, int k) {
+  if (a.scale_kind == QEM_SCALE_FIXED) return log(a.fixed_var);
+  const double s = (double)a.z_root[D * a.K + k];
+  return a.scale_kind == QEM_SCALE_LOGSIGMA ? 2.0 * s : s;
+}
 
-// 16 consecutive floats from shared memory as four 128-bit loads
-__device__ __forceinline__ void lds16(const float* p, float (&o)[16]) {
+// Inside k_root (one block, after the root softmax; w = root weights in fp64):
+// the backward reference row k* = argmax_k w_root(k) (ties -> lowest k) and the
+// k*-differenced rows  E_k(z) = B(k,z) - B(k*,z) = Ea_k + Eb_k . z + Eg_k |z|^2,
+// Eb_k = e_k mu_k - e_* mu_*, Eg_k = -(e_k - e_*)/2, differenced in fp64 (DESIGN.md
+// "Backward reference"): bf16x3 row operand + log2e Eg for the tensor-core path,
+// fp32 [K][D+1] rows for the FFMA path.
+template <int D>
+__device__ void k_root_star(const TLArgs& a, const double* w) {
+  __shared__ double s_v[32];
+  __shared__ int s_i[32];
+  const int K = a.K, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  for (int k = tid; k < K; k += blockDim.x)
+    if (w[k] > best) {
+      best = w[k];
+      bi = k;
+    }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float4 v = reinterpret_cast<const float4*>(p)[q];
-    o[4 * q] = v.x;
-    o[4 * q + 1] = v.y;
-    o[4 * q + 2] = v.z;
-    o[4 * q + 3] = v.w;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_v[wid] = best;
+    s_i[wid] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int q = 1; q < (int)((blockDim.x + 31) >> 5); ++q)
+      if (s_v[q] > s_v[0] || (s_v[q] == s_v[0] && s_i[q] < s_i[0])) {
+        s_v[0] = s_v[q];
+        s_i[0] = s_i[q];
+      }
+    const int ks = s_i[0];
+    RefInfo* ref = a.ws.ref;
+    ref->k_star = ks;
+    for (int r = 0; r < D; ++r) ref->mu_star[r] = a.z_root[r * K + ks];
+    const double lnv = root_lnv<D>(a, ks);
+    ref->e_star = exp(-lnv);
+    ref->bstar_const = -0.5 * D * (kLn2Pi + lnv);
+  }
+  __syncthreads();
+  const int ks = s_i[0];
+  const double es = exp(-root_lnv<D>(a, ks));
+  for (int k = tid; k < K; k += blockDim.x) {
+    const double ek = exp(-root_lnv<D>(a, k));
+    if constexpr (D == kTcD) {
+      if (a.tc) {
+        float v[kTcD];
+#pragma unroll
+        for (int r = 0; r < kTcD; ++r)
+          v[r] = (float)((ek * (double)a.z_root[r * K + k] - es * (double)a.z_root[r * K + ks]) * kLog2eD);
+        store_row_split16(reinterpret_cast<unsigned char*>(a.ws.rowop_b), k, v);
+        a.ws.bgam[k] = (float)(-0.5 * (ek - es) * kLog2eD);
+        continue;
+      }
+    }
+    float* bc = a.ws.bwd_coef + (size_t)k * (D + 1);
+    for (int r = 0; r < D; ++r) bc[r] = (float)(ek * (double)a.z_root[r * K + k] - es * (double)a.z_root[r * K + ks]);
+    bc[D] = (float)(-0.5 * (ek - es));
+  }
+}
+
+// ------------------------------------------------------------------ rowop
+__global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
+  const int K = a.K;
+  unsigned char* rc = reinterpret_cast<unsigned char*>(a.ws.rowop);
+  unsigned char* rx = reinterpret_cast<unsigned char*>(a.ws.rowop_x);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+    const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
+    float v[kTcD];
+#pragma unroll
+    for (int r = 0; r < kTcD; ++r) v[r] = fc[2 + r] * kLog2e;
+    store_row_split16(rc, k, v);
+    uint4 c0, c1;
+    extra_row(fc[1] * kLog2e, 1.f, 0.f, c0, c1);  // forward: lP on, no row constant
+    *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 0)) = c0;
+    *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 8)) = c1;
+  }
+}
+
+// -------------------------------------------------------------- colprep (K2a)
+// One warp per group.  For column k': A_i(k') (fp64), t_i(k') = B(k_ref,k') + A_i(k'),
+// c_i = lse t - log K, P = softmax t; the group's tile mode from the bound on
+// |D'|; the column operand and {P, ln P}.
+struct PrepTc {
+  static constexpr int WARPS = 8;
+  __host__ __device__ static size_t warp_bytes(int K, int J) {
+    size_t b = 3 * kTcD * 8 + (size_t)J * kTcD * 4 + (size_t)J * 4;
+    return (b + 15) & ~(size_t)15;
+  }
+  __host__ __device__ static size_t bytes(int K, int J) { return WARPS * warp_bytes(K, J); }
+};
+
+__global__ void __launch_bounds__(256, 3) k_colprep_tc(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int D = kTcD;
+  const int K = a.K, J = a.J, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned char* wb = smem + (size_t)wid * PrepTc::warp_bytes(K, J);
+  double* qc = reinterpret_cast<double*>(wb);                      // [3][D]: m, 1/(2v), -(ln 2pi v)/2
+  float* xf = reinterpret_cast<float*>(qc + 3 * D);                // [J][D] features as 0/1 floats
+  float* yf = xf + J * D;                                          // [J]
+  const RefInfo ref = *a.ws.ref;
+  const double logK = log((double)K);
+  unsigned char* colop = reinterpret_cast<unsigned char*>(a.ws.colop);
+  for (int64_t i = (int64_t)blockIdx.x * PrepTc::WARPS + wid; i < a.n_local;
+       i += (int64_t)gridDim.x * PrepTc::WARPS) {
+    __syncwarp();
+    if (lane < D) {
+      const double m = a.q_m[i * D + lane], v = a.q_v[i * D + lane];
+      qc[lane] = m;
+      qc[D + lane] = 0.5 / v;
+      qc[2 * D + lane] = -0.5 * (kLn2Pi + log(v));
+    }
+    {
+      const uint8_t* x = reinterpret_cast<const uint8_t*>(a.x) + (size_t)i * J * D;
+      const uint8_t* y = reinterpret_cast<const uint8_t*>(a.y) + (size_t)i * J;
+      for (int e = lane; e < J * D; e += 32) xf[e] = x[e] ? 1.f : 0.f;
+      for (int j = lane; j < J; j += 32) yf[j] = y[j] ? 1.f : 0.f;
+    }
+    __syncwarp();
+    unsigned char* cop = colop + (size_t)i * K * kTcColBytes;
+    double tmax = -CUDART_INF;
+    float w2max = 0.f;
+    for (int kc = lane; kc < K; kc += 32) {
+      float zr[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) zr[r] = a.z[((size_t)i * D + r) * K + kc];
+      double lq = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const double dz = (double)zr[r] - qc[r];
+        lq += qc[2 * D + r] - dz * dz * qc[D + r];
+      }
+      double ll = 0.0;
+      for (int j = 0; j < J; ++j) {
+        const float4* xr = reinterpret_cast<const float4*>(xf + j * D);
+        float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < D / 4; ++q) {
+          const float4 xv = xr[q];
+          e0 = fmaf(xv.x, zr[4 * q], e0);
+          e1 = fmaf(xv.y, zr[4 * q + 1], e1);
+          e0 = fmaf(xv.z, zr[4 * q + 2], e0);
+          e1 = fmaf(xv.w, zr[4 * q + 3], e1);
+        }
+        const float eta = e0 + e1;
+        const float sp = fmaxf(eta, 0.f) + log1pf(__expf(-fabsf(eta)));
+        ll += (double)(yf[j] * eta) - (double)sp;
+      }
+      // column operand re-centred on the group's Q mean: w = z - m_i and
+      // S = |w|^2 + 2 m_i . w (so D_k(z) = alpha'_ik + c0_k . w + gamma_k S)
+      float W2 = 0.f, mw = 0.f;
+      double U2d = 0.0;
+      float wv[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const float m = (float)qc[r];
+        wv[r] = zr[r] - m;
+        W2 = fmaf(wv[r], wv[r], W2);
+        mw = fmaf(m, wv[r], mw);
+        const double ud = (double)zr[r] - (double)ref.mu_ref[r];
+        U2d += ud * ud;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // bf16x3 split of w, 8 dims (one 16-byte chunk per term) at a time
+        __nv_bfloat16 s0[8], s1[8], s2[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          __nv_bfloat16 t[3];
+          split3_bf16(wv[8 * h + r], t);
+          s0[r] = t[0];
+          s1[r] = t[1];
+          s2[r] = t[2];
+        }
+        *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 0 * 16 + 8 * h)) = pack8_bf16(s0);
+        *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 1 * 16 + 8 * h)) = pack8_bf16(s1);
+        *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 2 * 16 + 8 * h)) = pack8_bf16(s2);
+      }
+      {  // extra slab, first half: [S pattern | lP0 lP1 (patched below)]
+        uint4 c0, c1;
+        extra_col(fmaf(2.f, mw, W2), 0.f, c0, c1);
+        *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 48)) = c0;
+      }
+      // t_ref(k') = B(k_ref,k') + A_i(k') (fp64; the backward rebuilds A from it)
+      const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
+      a.ws.tA[(size_t)i * K + kc] = t;
+      tmax = fmax(tmax, t);
+      w2max = fmaxf(w2max, W2);
+    }
+    const double M = warp_max(tmax);
+    const float W2max = warp_maxf(w2max);
+    double sum = 0.0;
+    const double* tref = a.ws.tA + (size_t)i * K;  // written above by this lane (program order)
+    for (int kc = lane; kc < K; kc += 32) sum += (double)expf((float)(tref[kc] - M));
+    const double logS = log(warp_sum(sum));
+    // tile mode: bound on |D'_k(k')| = |c'_k . w + gamma_k |w|^2|, c' = c0 + 2 gamma m_i
+    float u0[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) u0[r] = (float)qc[r];
+    const float wmax = sqrtf(W2max);
+    float tb = 0.f;
+    for (int k = lane; k < K; k += 32) {
+      const float* fc = a.ws.fwd_coef + (size_t)k * (D + 2);
+      const float g = fc[1];
+      float cn = 0.f;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const float cp = fmaf(2.f * g, u0[r], fc[2 + r]);
+        cn = fmaf(cp, cp, cn);
+      }
+      tb = fmaxf(tb, sqrtf(cn) * wmax + fabsf(g) * W2max);
+    }
+    tb = warp_maxf(tb);
+    const int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
+    float* aux = a.ws.colaux + (size_t)i * 2 * K;  // SoA {P, ln P}
+    for (int kc = lane; kc < K; kc += 32) {
+      const float lp = (float)(tref[kc] - M - logS);
+      aux[kc] = expf(lp);
+      aux[K + kc] = lp;
+      uint4 c0, c1;
+      // ln P joins the MMA only in the online mode; the polynomial modes need D' alone
+      extra_col(0.f, md == 5 ? lp * kLog2e : 0.f, c0, c1);
+      *reinterpret_cast<uint32_t*>(cop + tc_col_offset(kc, 54)) = c0.w;  // lP0 lP1
+      *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 56)) = c1;
+    }
+    if (lane == 0) {
+      a.ws.cvec[i] = M + logS - logK;
+      a.ws.gstat[i] = W2max;
+      a.ws.gmode[i] = md;
+    }
   }
 }
 
@@ -71,261 +359,317 @@ __device__ __forceinline__ void tmem_pipeline16(uint32_t taddr, F&& f) {
   }
 }
 
-// Forward epilogue, online log-sum-exp over t' = tm + gamma |u|^2 + ln P (the
-// row constant kappa is added at the end): state (st0 = running max, st1 = sum).
+// 2^x - 1 by its Taylor polynomial of degree N in x ln 2 (Horner, FMA pipe)
+template <int N>
+__device__ __forceinline__ float2 expm1_2_poly(float2 x) {
+  constexpr double ln2 = 0.69314718055994530942;
+  double cN = inv_fact(N);
+  for (int i = 0; i < N; ++i) cN *= ln2;
+  float2 p = f2((float)cN);
+#pragma unroll
+  for (int n = N - 1; n >= 1; --n) {
+    double c = inv_fact(n);
+    for (int i = 0; i < n; ++i) c *= ln2;
+    p = fma2(p, x, f2((float)c));
+  }
+  return mul2(p, x);
+}
+
+// Forward epilogue, online mode: (m, s) = running max / sum of 2^(v - m) over
+// v = c2.u + g2 U + lP (log2 domain; the row constant is added at the end).
+// The max is lazy: s is rescaled only when a chunk raises it.
 template <int NC16>
-__device__ __forceinline__ void fwd_epi_online(uint32_t taddr, const float* u2, const float* lp, float g, float& st0,
-                                               float& st1) {
-  tmem_pipeline16<NC16>(taddr, [&](int c16, uint32_t(&r)[16]) {
-    float a[16], b[16], v[16];
-    lds16(u2 + c16 * 16, a);
-    lds16(lp + c16 * 16, b);
+__device__ __forceinline__ void fwd_epi_online(uint32_t taddr, float& m, float& s) {
+  tmem_pipeline16<NC16>(taddr, [&](int, uint32_t(&r)[16]) {
+    float v[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
+    const float m0 = fmax3f(v[0], v[1], v[2]), m1 = fmax3f(v[3], v[4], v[5]), m2 = fmax3f(v[6], v[7], v[8]);
+    const float m3 = fmax3f(v[9], v[10], v[11]), m4 = fmax3f(v[12], v[13], v[14]);
+    const float mx = fmax3f(fmax3f(m0, m1, m2), fmax3f(m3, m4, v[15]), m);
+    if (mx > m) {
+      s *= ex2(m - mx);
+      m = mx;
+    }
+    const float2 nm = f2(-m);
+    float2 acc[2] = {f2(0.f), f2(0.f)};
 #pragma unroll
     for (int c = 0; c < 16; c += 2) {
-      const float2 t = add2(fma2(f2(g), make_float2(a[c], a[c + 1]), make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1]))),
-                            make_float2(b[c], b[c + 1]));
-      v[c] = t.x;
-      v[c + 1] = t.y;
+      const float2 e = add2(make_float2(v[c], v[c + 1]), nm);
+      acc[(c >> 1) & 1] = add2(acc[(c >> 1) & 1], make_float2(ex2(e.x), ex2(e.y)));
     }
-    float mx[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) mx[q] = fmaxf(fmaxf(v[q], v[q + 4]), fmaxf(v[q + 8], v[q + 12]));
-    const float mn = fmaxf(st0, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));
-    const float nm = -mn * kLog2e;
-    float2 ps[2] = {f2(0.f), f2(0.f)};
-#pragma unroll
-    for (int c = 0; c < 16; c += 2) {
-      const float2 e = fma2(make_float2(v[c], v[c + 1]), f2(kLog2e), f2(nm));
-      ps[(c >> 1) & 1] = add2(ps[(c >> 1) & 1], make_float2(ex2(e.x), ex2(e.y)));
-    }
-    const float2 tot = add2(ps[0], ps[1]);
-    st1 = fmaf(st1, ex2((st0 - mn) * kLog2e), tot.x + tot.y);
-    st0 = mn;
+    const float2 t = add2(acc[0], acc[1]);
+    s += t.x + t.y;
   });
 }
 
-// Forward epilogue, polynomial mode: st0 += sum P expm1_N(tm + gamma |u|^2 + kappa).
+// Forward epilogue, polynomial mode: acc += sum P (2^v - 1), v = log2e D' = c2.w + g2 S.
 template <int N, int NC16>
-__device__ __forceinline__ void fwd_epi_poly(uint32_t taddr, const float* u2, const float* pp, float g, float kap,
-                                             float& st0) {
-  float2 acc[2] = {f2(0.f), f2(0.f)};
+__device__ __forceinline__ void fwd_epi_poly(uint32_t taddr, const float* pp, float& acc) {
+  float2 a2[2] = {f2(0.f), f2(0.f)};
   tmem_pipeline16<NC16>(taddr, [&](int c16, uint32_t(&r)[16]) {
-    float a[16], b[16];
-    lds16(u2 + c16 * 16, a);
-    lds16(pp + c16 * 16, b);
+    float p[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(pp + c16 * 16)[q];
+      p[4 * q] = v.x;
+      p[4 * q + 1] = v.y;
+      p[4 * q + 2] = v.z;
+      p[4 * q + 3] = v.w;
+    }
 #pragma unroll
     for (int c = 0; c < 16; c += 2) {
-      const float2 dp =
-          add2(fma2(f2(g), make_float2(a[c], a[c + 1]), make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1]))),
-               f2(kap));
-      acc[(c >> 1) & 1] = fma2(make_float2(b[c], b[c + 1]), expm1_poly<N>(dp), acc[(c >> 1) & 1]);
+      const float2 dp = make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+      a2[(c >> 1) & 1] = fma2(make_float2(p[c], p[c + 1]), expm1_2_poly<N>(dp), a2[(c >> 1) & 1]);
     }
   });
-  const float2 t2 = add2(acc[0], acc[1]);
-  st0 += t2.x + t2.y;
+  const float2 t = add2(a2[0], a2[1]);
+  acc += t.x + t.y;
 }
 
-template <int CQ>
-struct FwdTcLayout {
-  static __host__ __device__ size_t colop(int K) { return (size_t)K * kTcRowBytes; }  // rowop at 0
-  static __host__ __device__ size_t aux(int K) { return colop(K) + 2 * (size_t)kTcColBlockBytes; }
-  static __host__ __device__ size_t kappa(int K) { return aux(K) + 2 * (size_t)K * 12; }
-  static __host__ __device__ size_t st0(int K) { return kappa(K) + (size_t)K * 4; }
-  static __host__ __device__ size_t st1(int K) { return st0(K) + (size_t)CQ * K * 4; }
-  static __host__ __device__ size_t gsum(int K) { return st1(K) + (size_t)CQ * K * 4; }
-  static __host__ __device__ size_t u0(int K) { return gsum(K) + (size_t)K * 8; }
-  static __host__ __device__ size_t bars(int K) { return u0(K) + 32 * 4; }
-  static __host__ __device__ size_t bytes(int K) { return bars(K) + 64; }
+// Tile walk of a persistent CTA (no integer division in the loop): group j (instance i =
+// blockIdx.x + j gridDim.x), outer block cb, inner block rb; T = tile count, J = (group, outer block) count.
+struct TileWalk {
+  int64_t T, J, j, i;
+  int t, cb, rb, nin, nout;
+  __device__ TileWalk(int n_in, int n_out)
+      : T(0), J(0), j(0), i(blockIdx.x), t(0), cb(0), rb(0), nin(n_in), nout(n_out) {}
+  __device__ __forceinline__ void next() {
+    ++T;
+    ++t;
+    if (++rb == nin) {
+      rb = 0;
+      ++J;
+      if (++cb == nout) {
+        cb = 0;
+        t = 0;
+        ++j;
+        i += gridDim.x;
+      }
+    }
+  }
 };
 
-// Forward: warp w, lane l -> row k = rb*128 + 32*(w%4) + l, columns cq*(256/CQ).. of each tile.
-template <int CQ>
-__global__ void __launch_bounds__(128 * CQ, 1) k_forward_tc(TLArgs a) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  using L = FwdTcLayout<CQ>;
-  constexpr int NT = 128 * CQ, CW = 256 / CQ, NC16 = CW / 16;
+// ------------------------------------------------------------------ forward
+struct FwdTcL {
+  static constexpr int SA = 3;                                       // row-block stages
+  static constexpr uint32_t A_C = 128 * kTcRowCBytes;                // 12 KB
+  static constexpr uint32_t A_STAGE = A_C + 128 * kTcRowXBytes;      // 16 KB
+  static constexpr uint32_t B_STAGE = 256 * kTcColBytes;             // 32 KB
+  static constexpr uint32_t P_STAGE = 256 * 4;                       // P of the block's columns
+  static constexpr size_t a() { return 0; }
+  static constexpr size_t b() { return a() + SA * A_STAGE; }
+  static constexpr size_t p() { return b() + 2 * B_STAGE; }
+  static constexpr size_t fin() { return p() + 2 * P_STAGE; }         // [2][4][128] float2
+  static constexpr size_t bars() { return fin() + 2 * 4 * 128 * 8; }  // 16 mbarriers
+  static constexpr size_t kap() { return bars() + 16 * 8; }
+  static size_t __host__ __device__ st0(int K) { return kap() + (size_t)K * 4; }
+  static size_t __host__ __device__ st1(int K) { return st0(K) + (size_t)4 * K * 4; }
+  static size_t __host__ __device__ g(int K) { return st1(K) + (size_t)4 * K * 4; }
+  static size_t __host__ __device__ bytes(int K) { return g(K) + (size_t)K * 8; }
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using L = FwdTcL;
+  constexpr int SA = L::SA;
   const int K = a.K, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quarter = warp & 3, cq = warp >> 2;
   const int NB = K / 256, RB = K / 128, TPG = NB * RB;
-  unsigned char* s_rowop = smem;
-  unsigned char* s_colop = smem + L::colop(K);
-  float* s_aux = reinterpret_cast<float*>(smem + L::aux(K));  // 2 x [3][K] SoA
-  float* s_kappa = reinterpret_cast<float*>(smem + L::kappa(K));
+  unsigned char* s_a = smem + L::a();
+  unsigned char* s_b = smem + L::b();
+  float* s_p = reinterpret_cast<float*>(smem + L::p());
+  float2* s_fin = reinterpret_cast<float2*>(smem + L::fin());
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars());
+  uint64_t* a_full = bars;           // [SA]
+  uint64_t* a_empty = bars + SA;     // [SA]
+  uint64_t* b_full = bars + 2 * SA;  // [2]
+  uint64_t* b_empty = b_full + 2;    // [2]  MMA commit + 16 epilogue warps
+  uint64_t* t_full = b_empty + 2;    // [2]
+  uint64_t* t_empty = t_full + 2;    // [2]  16 epilogue warps
   float* s_st0 = reinterpret_cast<float*>(smem + L::st0(K));
   float* s_st1 = reinterpret_cast<float*>(smem + L::st1(K));
-  double* s_g = reinterpret_cast<double*>(smem + L::gsum(K));
-  float* s_u0 = reinterpret_cast<float*>(smem + L::u0(K));  // [16] u0, [16] |u0|^2
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bars(K));  // [0,1] tma, [2,3] mma, [4] rowop
+  double* s_g = reinterpret_cast<double*>(smem + L::g(K));
   __shared__ uint32_t s_tmem;
-  __shared__ int s_mode[4 * CQ];
 
   const int64_t n = a.n_local;
   const int64_t ngroups = n > blockIdx.x ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t nblocks = ngroups * NB, ntiles = ngroups * TPG;
-  const uint32_t idesc = umma_idesc_bf16(128, 256);
+  const int64_t ntiles = ngroups * TPG;
 
   if (tid == 0) {
-    for (int b = 0; b < 5; ++b) mbar_init(&bar[b], 1);
+    for (int b = 0; b < SA; ++b) {
+      mbar_init(&a_full[b], 1);
+      mbar_init(&a_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&b_full[b], 1);
+      mbar_init(&b_empty[b], 1 + kTcEpiWarps);
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], kTcEpiWarps);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) {
+  if (warp == kTcEpiWarps + 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int k = tid; k < K; k += NT) s_g[k] = 0.0;
+  for (int k = tid; k < K; k += blockDim.x) s_g[k] = 0.0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-
-  auto issue_block = [&](int64_t J) {  // colop block J (and the group's aux with its first block)
-    if (J >= nblocks) return;
-    const int64_t j = J / NB;
-    const int cb = (int)(J % NB);
-    const int64_t i = blockIdx.x + j * gridDim.x;
-    const int st = (int)(J & 1);
-    const uint32_t bytes = kTcColBlockBytes + (cb == 0 ? (uint32_t)K * 12 : 0u);
-    mbar_expect_tx(&bar[st], bytes);
-    tma_bulk_g2s(s_colop + st * kTcColBlockBytes,
-                 reinterpret_cast<const unsigned char*>(a.ws.colop) + ((size_t)i * K + (size_t)cb * 256) * kTcRowBytes,
-                 kTcColBlockBytes, &bar[st]);
-    if (cb == 0)
-      tma_bulk_g2s(s_aux + (size_t)(j & 1) * 3 * K, a.ws.colaux + (size_t)i * 3 * K, (uint32_t)K * 12, &bar[st]);
-  };
-  auto issue_mma = [&](int64_t T) {
-    const int64_t J = T / TPG * NB + (T % TPG) / RB;
-    const int rb = (int)(T % TPG % RB);
-    mbar_wait(&bar[J & 1], (uint32_t)((J >> 1) & 1));
-    tc_fence_after();
-    umma_bf16x3(tmem + (uint32_t)(T & 1) * 256, smem_u32(s_rowop) + (uint32_t)rb * 128 * kTcRowBytes,
-                smem_u32(s_colop) + (uint32_t)(J & 1) * kTcColBlockBytes, idesc);
-    umma_commit(&bar[2 + (T & 1)]);
-  };
-
-  if (tid == 0) {
-    mbar_expect_tx(&bar[4], (uint32_t)K * kTcRowBytes);
-    tma_bulk_g2s(s_rowop, a.ws.rowop, (uint32_t)K * kTcRowBytes, &bar[4]);
-    issue_block(0);
-    issue_block(1);
-  }
-  mbar_wait(&bar[4], 0);
-  if (tid == 0 && ntiles > 0) issue_mma(0);
-
   double csum = 0.0;
-  int md = 0;
-  for (int64_t T = 0; T < ntiles; ++T) {
-    const int64_t j = T / TPG;
-    const int t = (int)(T % TPG), cb = t / RB, rb = t % RB;
-    const int64_t J = j * NB + cb;
-    const int64_t i = blockIdx.x + j * gridDim.x;
-    if (t == 0) {
-      // ---- group setup: re-centring constants of all rows and the tile mode
-      float u0[kTcD];
-      float U0sq = 0.f;
-#pragma unroll
-      for (int r = 0; r < kTcD; ++r) {
-        u0[r] = a.q_m[i * kTcD + r] - a.ws.ref->mu_ref[r];
-        U0sq = fmaf(u0[r], u0[r], U0sq);
+
+  if (warp == kTcEpiWarps) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const unsigned char* colop = reinterpret_cast<const unsigned char*>(a.ws.colop);
+      const unsigned char* rowc = reinterpret_cast<const unsigned char*>(a.ws.rowop);
+      const unsigned char* rowx = reinterpret_cast<const unsigned char*>(a.ws.rowop_x);
+      for (TileWalk tw(RB, NB); tw.T < ntiles; tw.next()) {
+        const int64_t T = tw.T, j = tw.j;
+        const int t = tw.t, cb = tw.cb, rb = tw.rb;
+        const int64_t i = tw.i;
+        if (rb == 0) {
+          const int64_t J = tw.J;
+          const int st = (int)(J & 1);
+          if (J >= 2) mbar_wait(&b_empty[st], (uint32_t)(((J >> 1) - 1) & 1));
+          mbar_expect_tx(&b_full[st], L::B_STAGE + L::P_STAGE);
+          tma_bulk_g2s(s_b + st * L::B_STAGE, colop + ((size_t)i * K + (size_t)cb * 256) * kTcColBytes, L::B_STAGE,
+                       &b_full[st]);
+          tma_bulk_g2s(s_p + st * 256, a.ws.colaux + (size_t)i * 2 * K + (size_t)cb * 256, L::P_STAGE, &b_full[st]);
+        }
+        const int sa = (int)(T % SA);
+        const int64_t ua = T / SA;
+        if (ua >= 1) mbar_wait(&a_empty[sa], (uint32_t)((ua - 1) & 1));
+        mbar_expect_tx(&a_full[sa], L::A_STAGE);
+        tma_bulk_g2s(s_a + sa * L::A_STAGE, rowc + (size_t)rb * L::A_C, L::A_C, &a_full[sa]);
+        tma_bulk_g2s(s_a + sa * L::A_STAGE + L::A_C, rowx + (size_t)rb * 128 * kTcRowXBytes, 128 * kTcRowXBytes,
+                     &a_full[sa]);
       }
-      if (tid < kTcD) s_u0[tid] = u0[tid];
-      if (tid == 0) s_u0[kTcD] = U0sq;
-      const float W2max = a.ws.gstat[i];
-      const float wmax = sqrtf(W2max);
-      if (tid == 0) csum += a.ws.cvec[i];
-      float tb = 0.f;
-      for (int k = tid; k < K; k += NT) {
-        const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
-        const float g = fc[1];
-        float kap = g * U0sq;
-        float cn = 0.f;
+    }
+  } else if (warp == kTcEpiWarps + 1) {
+    // -------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(128, 256);
+      for (TileWalk tw(RB, NB); tw.T < ntiles; tw.next()) {
+        const int64_t T = tw.T, j = tw.j;
+        const int t = tw.t, cb = tw.cb, rb = tw.rb;
+        const int64_t J = tw.J;
+        const int sa = (int)(T % SA), tb = (int)(T & 1);
+        mbar_wait(&a_full[sa], (uint32_t)((T / SA) & 1));
+        if (rb == 0) mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));
+        if (T >= 2) mbar_wait(&t_empty[tb], (uint32_t)(((T >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t A = smem_u32(s_a + sa * L::A_STAGE), B = smem_u32(s_b + (J & 1) * L::B_STAGE);
+        umma_tile7(tmem + (uint32_t)tb * 256, A, 768, B, 1024, A + L::A_C, 256, B + 768, 1024, idesc);
+        umma_commit(&t_full[tb]);
+        umma_commit(&a_empty[sa]);
+        if (rb == RB - 1) umma_commit(&b_empty[J & 1]);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3, cq = warp >> 2, etid = tid;
+    int md = 5;
+    float mi[kTcD];
+    float M2 = 0.f;
+    for (TileWalk tw(RB, NB); tw.T < ntiles; tw.next()) {
+      const int64_t T = tw.T, j = tw.j;
+      const int t = tw.t, cb = tw.cb, rb = tw.rb;
+      const int64_t J = tw.J;
+      const int64_t i = tw.i;
+      if (t == 0) {
+        // ---- group setup: the group's mode; m_i for the fp64 re-centring constant alpha'_ik
+        epi_bar();
+        md = a.ws.gmode[i];
+        M2 = 0.f;
 #pragma unroll
         for (int r = 0; r < kTcD; ++r) {
-          const float c = fc[2 + r];
-          kap = fmaf(c, u0[r], kap);
-          const float cp = fmaf(2.f * g, u0[r], c);
-          cn = fmaf(cp, cp, cn);
+          mi[r] = a.q_m[i * kTcD + r];
+          M2 = fmaf(mi[r], mi[r], M2);
         }
-        s_kappa[k] = -kap;
-        tb = fmaxf(tb, sqrtf(cn) * wmax + fabsf(g) * W2max);
-      }
-      int m = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
-      m = __reduce_max_sync(0xffffffffu, m);
-      if (lane == 0) s_mode[warp] = m;
-      __syncthreads();
-      md = 0;
-#pragma unroll
-      for (int w = 0; w < 4 * CQ; ++w) md = max(md, s_mode[w]);
-      for (int e = tid; e < CQ * K; e += NT) {
-        s_st0[e] = md == 5 ? -CUDART_INF_F : 0.f;
-        s_st1[e] = 0.f;
-      }
-      if (tid == 0) atomicAdd(&a.cnt->mode_hist[md], 1ull);
-      __syncthreads();
-    }
-    if (rb == 0) mbar_wait(&bar[J & 1], (uint32_t)((J >> 1) & 1));  // visibility of the block's aux data
-    // ---- MMA of tile T done?  then queue tile T+1 (other TMEM buffer) before the epilogue
-    mbar_wait(&bar[2 + (T & 1)], (uint32_t)((T >> 1) & 1));
-    tc_fence_after();
-    if (tid == 0 && T + 1 < ntiles) issue_mma(T + 1);
-
-    // ---- epilogue: row k, columns cb*256 + cq*CW .. +CW
-    const int k = rb * 128 + quarter * 32 + lane;
-    const float g = a.ws.fwd_coef[(size_t)k * (kTcD + 2) + 1], kap = s_kappa[k];
-    const float* axb = s_aux + (size_t)(j & 1) * 3 * K + cb * 256 + cq * CW;
-    const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * CW) + ((uint32_t)(quarter * 32) << 16);
-    float st0 = s_st0[cq * K + k], st1 = s_st1[cq * K + k];
-    switch (md) {
-      case 0: fwd_epi_poly<3, NC16>(taddr, axb, axb + K, g, kap, st0); break;
-      case 1: fwd_epi_poly<4, NC16>(taddr, axb, axb + K, g, kap, st0); break;
-      case 2: fwd_epi_poly<5, NC16>(taddr, axb, axb + K, g, kap, st0); break;
-      case 3: fwd_epi_poly<7, NC16>(taddr, axb, axb + K, g, kap, st0); break;
-      case 4: fwd_epi_poly<9, NC16>(taddr, axb, axb + K, g, kap, st0); break;
-      default: fwd_epi_online<NC16>(taddr, axb, axb + 2 * K, g, st0, st1); break;
-    }
-    s_st0[cq * K + k] = st0;
-    s_st1[cq * K + k] = st1;
-    if (cb == NB - 1) {
-      // ---- the row block is complete: merge the CQ column slices, finalise h and dg
-      __syncthreads();
-      if (cq == 0) {
-        float h;
-        if (md == 5) {
-          float mx = -CUDART_INF_F;
-#pragma unroll
-          for (int q = 0; q < CQ; ++q) mx = fmaxf(mx, s_st0[q * K + k]);
-          float s = 0.f;
-#pragma unroll
-          for (int q = 0; q < CQ; ++q) s += s_st1[q * K + k] * ex2((s_st0[q * K + k] - mx) * kLog2e);
-          h = s_kappa[k] + mx + logf(s);  // the online state excludes the row constant kappa
-        } else {
-          float s = 0.f;
-#pragma unroll
-          for (int q = 0; q < CQ; ++q) s += s_st0[q * K + k];
-          h = log1pf(s);
+        if (etid == 0) {
+          atomicAdd(&a.cnt->mode_hist[md], 1ull);
+          csum += a.ws.cvec[i];
         }
-        // alpha'_ik = alpha_k + gamma_k |u0|^2 + c_k . u0 in fp64
-        const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
-        double ap = a.ws.alpha_d[k] + (double)fc[1] * (double)s_u0[kTcD];
+      }
+      const int k = rb * 128 + q * 32 + lane;
+      float st0, st1 = 0.f;
+      if (cb == 0)
+        st0 = md == 5 ? -CUDART_INF_F : 0.f;
+      else {
+        st0 = s_st0[cq * K + k];
+        st1 = s_st1[cq * K + k];
+      }
+      mbar_wait(&t_full[T & 1], (uint32_t)((T >> 1) & 1));
+      tc_fence_after();
+      const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * 64) + ((uint32_t)(q * 32) << 16);
+      if (md == 5) {
+        fwd_epi_online<4>(taddr, st0, st1);
+      } else {
+        mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));  // P of this block is in SMEM
+        const float* pp = s_p + (J & 1) * 256 + cq * 64;
+        switch (md) {
+          case 0: fwd_epi_poly<3, 4>(taddr, pp, st0); break;
+          case 1: fwd_epi_poly<4, 4>(taddr, pp, st0); break;
+          case 2: fwd_epi_poly<5, 4>(taddr, pp, st0); break;
+          case 3: fwd_epi_poly<7, 4>(taddr, pp, st0); break;
+          default: fwd_epi_poly<9, 4>(taddr, pp, st0); break;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&t_empty[T & 1]);
+        if (rb == RB - 1) mbar_arrive(&b_empty[J & 1]);
+      }
+      if (cb < NB - 1) {
+        s_st0[cq * K + k] = st0;
+        s_st1[cq * K + k] = st1;
+      } else {
+        // ---- row k complete: merge the 4 column slices, finalise h, dg, plate sum
+        float2* fin = s_fin + (rb & 1) * 512;
+        fin[cq * 128 + q * 32 + lane] = make_float2(st0, st1);
+        quarter_bar(q);
+        if (cq == 0) {
+          float h;
+          if (md == 5) {
+            float mx = -CUDART_INF_F;
 #pragma unroll
-        for (int r = 0; r < kTcD; ++r) ap += (double)fc[2 + r] * (double)s_u0[r];
-        const double dgd = ap + (double)h;
-        a.ws.hmsg[(size_t)i * K + k] = h - s_kappa[k];  // TC path: the backward's row constant is -(h - kappa)
-        a.ws.dg[(size_t)i * K + k] = (float)dgd;
-        s_g[k] += dgd;
+            for (int c = 0; c < 4; ++c) mx = fmaxf(mx, fin[c * 128 + q * 32 + lane].x);
+            float sm = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float2 f = fin[c * 128 + q * 32 + lane];
+              sm += f.y * ex2(f.x - mx);
+            }
+            h = (mx + log2f(sm)) * 0.69314718055994531f;
+          } else {
+            float sm = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sm += fin[c * 128 + q * 32 + lane].x;
+            h = log1pf(sm);
+          }
+          // alpha'_ik = D_k(m_i) = alpha0_k + gamma_k |m_i|^2 + c0_k . m_i in fp64
+          const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
+          double ap = a.ws.alpha_d[k] + (double)fc[1] * (double)M2;
+#pragma unroll
+          for (int r = 0; r < kTcD; ++r) ap += (double)fc[2 + r] * (double)mi[r];
+          const double dgd = ap + (double)h;
+          a.ws.hmsg[(size_t)i * K + k] = h;  // re-centred message, the backward's row constant
+          a.ws.dg[(size_t)i * K + k] = (float)dgd;
+          s_g[k] += dgd;
+        }
       }
     }
-    tc_fence_before();
-    __syncthreads();
-    // the block's colop stage is free once all its tiles are consumed: refill it
-    if (tid == 0 && rb == RB - 1) issue_block(J + 2);
   }
 
   // ---- teardown, per-CTA partial plate sums, last-CTA fixed-order reduce
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == kTcEpiWarps + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   double* part = a.ws.partial + (size_t)blockIdx.x * (K + 1);
-  for (int k = tid; k < K; k += NT) part[k] = s_g[k];
+  for (int k = tid; k < K; k += blockDim.x) part[k] = s_g[k];
   if (tid == 0) part[K] = csum;
   __threadfence();
   __syncthreads();
@@ -334,7 +678,7 @@ __global__ void __launch_bounds__(128 * CQ, 1) k_forward_tc(TLArgs a) {
   __syncthreads();
   if (s_last) {
     __threadfence();
-    for (int k = tid; k <= K; k += NT) {
+    for (int k = tid; k <= K; k += blockDim.x) {
       double sum = 0.0;
       for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(a.ws.partial + (size_t)b * (K + 1) + k);
       a.ws.red[k] = sum;
@@ -343,46 +687,203 @@ __global__ void __launch_bounds__(128 * CQ, 1) k_forward_tc(TLArgs a) {
   }
 }
 
-template <int CQ>
-struct BwdTcLayout {
-  static __host__ __device__ size_t colop(int K) { return (size_t)K * kTcRowBytes; }  // rowop at 0
-  static __host__ __device__ size_t rowtab(int K) { return colop(K) + 2 * (size_t)kTcBwdBlockBytes; }
-  static __host__ __device__ size_t wsm(int K) { return rowtab(K) + (size_t)K * 12; }
-  static __host__ __device__ size_t wpart(int K) { return wsm(K) + (size_t)K * 4; }
-  static __host__ __device__ size_t red(int K) { return wpart(K) + (size_t)CQ * 128 * 4; }
-  static __host__ __device__ size_t bars(int K) { return red(K) + (4 * CQ * kTcD + kTcD) * 8; }
-  static __host__ __device__ size_t bytes(int K) { return bars(K) + 64; }
+// ----------------------------------------------------------------- backward
+struct BwdTcL {
+  static constexpr int SB = 3;                                  // row-block stages
+  static constexpr uint32_t A_STAGE = 128 * kTcColBytes;        // 16 KB: 128 columns
+  static constexpr uint32_t B_STAGE = 256 * kTcRowCBytes;       // 24 KB: 256 rows of Eb (k*-differenced)
+  static constexpr size_t a() { return 0; }
+  static constexpr size_t b() { return a() + 2 * A_STAGE; }
+  static constexpr size_t wp() { return b() + SB * B_STAGE; }            // [2][4][128] float
+  static constexpr size_t rd() { return wp() + 2 * 4 * 128 * 4; }        // aux scratch [2 warps][40] double
+  static constexpr size_t bars() { return rd() + 2 * 40 * 8; }           // 24 mbarriers
+  static size_t __host__ __device__ w(int) { return bars() + 24 * 8; }   // [2][K] float
+  static size_t __host__ __device__ lst(int K) { return w(K) + (size_t)2 * K * 4; }  // [2][K] float
+  static size_t __host__ __device__ tt(int K) { return lst(K) + (size_t)2 * K * 4; }  // [K] double (prologue)
+  static size_t __host__ __device__ bx(int K) { return (tt(K) + (size_t)K * 8 + 1023) & ~(size_t)1023; }
+  static size_t __host__ __device__ bytes(int K) { return bx(K) + (size_t)2 * K * kTcRowXBytes; }
 };
 
-// Backward: warp w, lane l -> column k' = cb*128 + 32*(w%4) + l, rows cq*(256/CQ).. of each tile.
-template <int CQ>
-__global__ void __launch_bounds__(128 * CQ, 1) k_backward_tc(TLArgs a) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  using L = BwdTcLayout<CQ>;
-  constexpr int NT = 128 * CQ, NW = NT / 32, CW = 256 / CQ, NC16 = CW / 16;
+constexpr int kBwdAuxWarps = 2;
+constexpr int kBwdThreads = kTcThreads + 32 * kBwdAuxWarps;  // + per-group prologue / moment warps
+__device__ __forceinline__ void aux_bar() { named_bar(6, 32 * kBwdAuxWarps); }
+
+// Backward prologue of group i, run by the aux warps one or two groups ahead
+// (backward reference):
+//   log P(k'|k) = log P(k'|k*) + E_k(k') - (l_k - l_*),  E_k = B(k,.) - B(k*,.),
+// and with both passes re-centred on m_i the row constant reduces to
+//   rho_k = log2 w_root(k) - log2e (h_k - h_*)          (h = forward message)
+// so no fp32 term larger than the k*-relative spread ever cancels.
+//  * row extra slab (K x 32 B) into `bx`: [Eg pattern | 0 0 0 | rho] (rho = -1e30 where w_root = 0)
+//  * column constants sL[k'] = log2e log P(k'|k*), a softmax of row k* over the
+//    group's columns with fp64 logits B(k*,k') + A_i(k').
+__device__ void bwd_prologue(const TLArgs& a, int64_t i, unsigned char* bx, float* sL, double* s_t, double* s_rd,
+                             int atid) {
+  constexpr int NT = 32 * kBwdAuxWarps;
+  const int K = a.K, lane = atid & 31, warp = atid >> 5;
+  const int ks = a.ws.ref->k_star;
+  const float hs = a.ws.hmsg[(size_t)i * K + ks];
+  for (int k = atid; k < K; k += NT) {
+    const float wr = a.w_root[k];
+    const float rho = wr > 0.f ? log2f(wr) - (a.ws.hmsg[(size_t)i * K + k] - hs) * kLog2e : -1e30f;
+    uint4 c0, c1;
+    extra_row(a.ws.bgam[k], 0.f, rho, c0, c1);
+    *reinterpret_cast<uint4*>(bx + tc_rowx_offset(k, 0)) = c0;
+    *reinterpret_cast<uint4*>(bx + tc_rowx_offset(k, 8)) = c1;
+  }
+  fence_proxy_async();  // generic-proxy SMEM writes -> visible to the tensor core (async proxy)
+  const double es = a.ws.ref->e_star, bs = a.ws.ref->bstar_const;
+  // logits t(k') = B(k*,k') + A_i(k') in fp64 for 4 consecutive columns per step (float4 z loads)
+  double mx = -CUDART_INF;
+  for (int c4 = atid * 4; c4 < K; c4 += NT * 4) {
+    float4 zv[kTcD];
+#pragma unroll
+    for (int r = 0; r < kTcD; ++r) zv[r] = *reinterpret_cast<const float4*>(a.z + ((size_t)i * kTcD + r) * K + c4);
+    const double2 ta = *reinterpret_cast<const double2*>(a.ws.tA + (size_t)i * K + c4);
+    const double2 tb = *reinterpret_cast<const double2*>(a.ws.tA + (size_t)i * K + c4 + 2);
+    // B(k*,k') - B(k_ref,k') = (bs - es |z - mu*|^2 / 2) - (br - er |z - mu_ref|^2 / 2), fp64
+    double d[4] = {0.0, 0.0, 0.0, 0.0}, g[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < kTcD; ++r) {
+      const double mu = (double)a.ws.ref->mu_star[r], mr = (double)a.ws.ref->mu_ref[r];
+      const double zz[4] = {(double)zv[r].x, (double)zv[r].y, (double)zv[r].z, (double)zv[r].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        d[c] = fma(zz[c] - mu, zz[c] - mu, d[c]);
+        g[c] = fma(zz[c] - mr, zz[c] - mr, g[c]);
+      }
+    }
+    const double er = a.ws.ref->e_ref, br = a.ws.ref->bref_const;
+    const double t0 = (bs - 0.5 * es * d[0]) - (br - 0.5 * er * g[0]) + ta.x;
+    const double t1 = (bs - 0.5 * es * d[1]) - (br - 0.5 * er * g[1]) + ta.y;
+    const double t2 = (bs - 0.5 * es * d[2]) - (br - 0.5 * er * g[2]) + tb.x;
+    const double t3 = (bs - 0.5 * es * d[3]) - (br - 0.5 * er * g[3]) + tb.y;
+    s_t[c4] = t0;
+    s_t[c4 + 1] = t1;
+    s_t[c4 + 2] = t2;
+    s_t[c4 + 3] = t3;
+    mx = fmax(fmax(mx, fmax(t0, t1)), fmax(t2, t3));
+  }
+  mx = warp_max(mx);
+  if (lane == 0) s_rd[warp * 40 + 32] = mx;
+  aux_bar();
+  mx = s_rd[32];
+#pragma unroll
+  for (int w = 1; w < kBwdAuxWarps; ++w) mx = fmax(mx, s_rd[w * 40 + 32]);
+  double se = 0.0;
+  for (int kc = atid; kc < K; kc += NT) se += (double)expf((float)(s_t[kc] - mx));
+  se = warp_sum(se);
+  if (lane == 0) s_rd[warp * 40 + 33] = se;
+  aux_bar();
+  se = 0.0;
+#pragma unroll
+  for (int w = 0; w < kBwdAuxWarps; ++w) se += s_rd[w * 40 + 33];
+  const double lse = mx + log(se);
+  for (int kc = atid; kc < K; kc += NT) sL[kc] = (float)((s_t[kc] - lse) * kLog2eD);
+  aux_bar();  // s_t / s_rd reusable
+}
+
+// Moments of group i from its weights (fp64, self-normalised, shifted by the Q mean):
+// E z = c + S1/S0, Var z = S2/S0 - (S1/S0)^2, S_p = sum_k' w (z - c)^p.
+__device__ void bwd_moments(const TLArgs& a, int64_t i, const float* sw, double* s_rd, int atid) {
+  constexpr int NT = 32 * kBwdAuxWarps;
+  const int K = a.K, lane = atid & 31, warp = atid >> 5;
+  double s0 = 0.0;
+  for (int kc = atid; kc < K; kc += NT) s0 += (double)sw[kc];
+  s0 = warp_sum(s0);
+#pragma unroll 1
+  for (int r0 = 0; r0 < kTcD; r0 += 4) {
+    double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c4 = atid * 4; c4 < K; c4 += NT * 4) {
+      const float4 wv = *reinterpret_cast<const float4*>(sw + c4);
+      float4 zv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) zv[q] = *reinterpret_cast<const float4*>(a.z + ((size_t)i * kTcD + r0 + q) * K + c4);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double c = a.q_m[i * kTcD + r0 + q];
+        const double e0 = (double)zv[q].x - c, e1 = (double)zv[q].y - c, e2 = (double)zv[q].z - c,
+                     e3 = (double)zv[q].w - c;
+        const double w0 = wv.x, w1 = wv.y, w2 = wv.z, w3 = wv.w;
+        s1[q] += (w0 * e0 + w1 * e1) + (w2 * e2 + w3 * e3);
+        s2[q] += (w0 * e0 * e0 + w1 * e1 * e1) + (w2 * e2 * e2 + w3 * e3 * e3);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double a1 = warp_sum(s1[q]), a2 = warp_sum(s2[q]);
+      if (lane == 0) {
+        s_rd[warp * 40 + r0 + q] = a1;
+        s_rd[warp * 40 + 16 + r0 + q] = a2;
+      }
+    }
+  }
+  if (lane == 0) s_rd[warp * 40 + 34] = s0;
+  aux_bar();
+  if (atid < kTcD) {
+    double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < kBwdAuxWarps; ++w) {
+      S0 += s_rd[w * 40 + 34];
+      S1 += s_rd[w * 40 + atid];
+      S2 += s_rd[w * 40 + 16 + atid];
+    }
+    const double mu = S1 / S0;
+    a.m1[i * kTcD + atid] = (double)a.q_m[i * kTcD + atid] + mu;
+    a.v[i * kTcD + atid] = S2 / S0 - mu * mu;
+  }
+  aux_bar();
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using L = BwdTcL;
+  constexpr int SB = L::SB;
   const int K = a.K, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quarter = warp & 3, cq = warp >> 2;
   const int CB = K / 128, RB = K / 256, TPG = CB * RB;
-  unsigned char* s_rowop = smem;
-  unsigned char* s_colop = smem + L::colop(K);
-  float* s_rt = reinterpret_cast<float*>(smem + L::rowtab(K));  // SoA [2][K]: gamma log2e, (kappa-h) log2e + log2 w_root
-  float* s_w = reinterpret_cast<float*>(smem + L::wsm(K));
-  float* s_wp = reinterpret_cast<float*>(smem + L::wpart(K));
-  double* s_red = reinterpret_cast<double*>(smem + L::red(K));  // [NW][16]
-  double* s_mom = s_red + NW * kTcD;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bars(K));  // [0,1] tma, [2,3] mma, [4] rowop
+  unsigned char* s_a = smem + L::a();
+  unsigned char* s_b = smem + L::b();
+  float* s_wp = reinterpret_cast<float*>(smem + L::wp());
+  double* s_rd = reinterpret_cast<double*>(smem + L::rd());
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars());
+  uint64_t* a_full = bars;            // [2]
+  uint64_t* a_empty = bars + 2;       // [2]
+  uint64_t* b_full = bars + 4;        // [SB]
+  uint64_t* b_empty = b_full + SB;    // [SB]
+  uint64_t* t_full = b_empty + SB;    // [2]
+  uint64_t* t_empty = t_full + 2;     // [2]  16 epilogue warps
+  uint64_t* bx_full = t_empty + 2;    // [2]  aux warps: row extra slab of a group ready (MMA waits)
+  uint64_t* l_full = bx_full + 2;     // [2]  aux warps: column constants of a group ready (epilogue waits)
+  uint64_t* w_full = l_full + 2;      // [2]  16 epilogue warps: group's weights complete
+  uint64_t* w_empty = w_full + 2;     // [2]  aux warps: moments read the weights
+  float* s_w = reinterpret_cast<float*>(smem + L::w(K));
+  float* s_L = reinterpret_cast<float*>(smem + L::lst(K));
+  double* s_t = reinterpret_cast<double*>(smem + L::tt(K));
+  unsigned char* s_bx = smem + L::bx(K);
   __shared__ uint32_t s_tmem;
 
   const int64_t n = a.n_local;
   const int64_t ngroups = n > blockIdx.x ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t nblocks = ngroups * CB, ntiles = ngroups * TPG;
-  const uint32_t idesc = umma_idesc_bf16(128, 256);
+  const int64_t ntiles = ngroups * TPG;
 
   if (tid == 0) {
-    for (int b = 0; b < 5; ++b) mbar_init(&bar[b], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&a_full[b], 1);
+      mbar_init(&a_empty[b], 1);
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], kTcEpiWarps);
+      mbar_init(&bx_full[b], kBwdAuxWarps);
+      mbar_init(&l_full[b], kBwdAuxWarps);
+      mbar_init(&w_full[b], kTcEpiWarps);
+      mbar_init(&w_empty[b], kBwdAuxWarps);
+    }
+    for (int b = 0; b < SB; ++b) {
+      mbar_init(&b_full[b], 1);
+      mbar_init(&b_empty[b], 1);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) {
+  if (warp == kTcEpiWarps + 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -391,150 +892,141 @@ __global__ void __launch_bounds__(128 * CQ, 1) k_backward_tc(TLArgs a) {
   tc_fence_after();
   const uint32_t tmem = s_tmem;
 
-  auto issue_block = [&](int64_t J) {
-    if (J >= nblocks) return;
-    const int64_t j = J / CB;
-    const int cb = (int)(J % CB);
-    const int64_t i = blockIdx.x + j * gridDim.x;
-    const int st = (int)(J & 1);
-    mbar_expect_tx(&bar[st], kTcBwdBlockBytes);
-    tma_bulk_g2s(s_colop + st * kTcBwdBlockBytes,
-                 reinterpret_cast<const unsigned char*>(a.ws.colop) + ((size_t)i * K + (size_t)cb * 128) * kTcRowBytes,
-                 kTcBwdBlockBytes, &bar[st]);
-  };
-  auto issue_mma = [&](int64_t T) {
-    const int64_t J = T / TPG * CB + (T % TPG) / RB;
-    const int rb = (int)(T % TPG % RB);
-    mbar_wait(&bar[J & 1], (uint32_t)((J >> 1) & 1));
-    tc_fence_after();
-    umma_bf16x3(tmem + (uint32_t)(T & 1) * 256, smem_u32(s_colop) + (uint32_t)(J & 1) * kTcBwdBlockBytes,
-                smem_u32(s_rowop) + (uint32_t)rb * 256 * kTcRowBytes, idesc);
-    umma_commit(&bar[2 + (T & 1)]);
-  };
-
-  if (tid == 0) {
-    mbar_expect_tx(&bar[4], (uint32_t)K * kTcRowBytes);
-    tma_bulk_g2s(s_rowop, a.ws.rowop, (uint32_t)K * kTcRowBytes, &bar[4]);
-    issue_block(0);
-    issue_block(1);
-  }
-  mbar_wait(&bar[4], 0);
-  if (tid == 0 && ntiles > 0) issue_mma(0);
-
-  float wacc = 0.f, U2 = 0.f, Lc = 0.f;
-  for (int64_t T = 0; T < ntiles; ++T) {
-    const int64_t j = T / TPG;
-    const int t = (int)(T % TPG), cb = t / RB, rb = t % RB;
-    const int64_t J = j * CB + cb;
-    const int64_t i = blockIdx.x + j * gridDim.x;
-    if (t == 0) {
-      // ---- group row table (SoA): gamma log2e | (kappa - h) log2e + log2 w_root
-      for (int k = tid; k < K; k += NT) {
-        // the TC forward stored h - kappa (kappa = -(gamma |u0|^2 + c . u0), the re-centring constant)
-        const float hk = a.ws.hmsg[(size_t)i * K + k];
-        s_rt[k] = a.ws.fwd_coef[(size_t)k * (kTcD + 2) + 1] * kLog2e;
-        s_rt[K + k] = -hk * kLog2e + log2f(a.w_root[k]);  // w_root folded in (log2 0 = -inf)
-      }
-      __syncthreads();
-    }
-    const int r_in = quarter * 32 + lane;  // column within the block
-    if (rb == 0) {
-      const float* xa = a.ws.colaux + (size_t)i * 3 * K + cb * 128 + r_in;
-      U2 = xa[0];
-      Lc = xa[2 * K] * kLog2e;
-      wacc = 0.f;
-    }
-    mbar_wait(&bar[2 + (T & 1)], (uint32_t)((T >> 1) & 1));
-    tc_fence_after();
-    if (tid == 0 && T + 1 < ntiles) issue_mma(T + 1);
-    // ---- epilogue: column k', rows rb*256 + cq*CW .. +CW
-    const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * CW) + ((uint32_t)(quarter * 32) << 16);
-    const float* rt = s_rt + rb * 256 + cq * CW;
-    // pairs of rows as float2 (FFMA2/FADD2); w_root is folded into the row
-    // constant as log2(w), so each pair costs 3 FMA-pipe lane-ops + 1 ex2 + 1 add
-    float2 wp[2] = {f2(0.f), f2(0.f)};
-    tmem_pipeline16<NC16>(taddr, [&](int c16, uint32_t(&r)[16]) {
-      float gg[16], rc[16];
-      lds16(rt + c16 * 16, gg);
-      lds16(rt + K + c16 * 16, rc);
-#pragma unroll
-      for (int c = 0; c < 16; c += 2) {
-        float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), f2(kLog2e),
-                        make_float2(rc[c], rc[c + 1]));
-        x = add2(fma2(make_float2(gg[c], gg[c + 1]), f2(U2), x), f2(Lc));
-        wp[(c >> 1) & 1] = add2(wp[(c >> 1) & 1], make_float2(ex2(x.x), ex2(x.y)));
-      }
-    });
-    {
-      const float2 t2 = add2(wp[0], wp[1]);
-      wacc += t2.x + t2.y;
-    }
-    if (rb == RB - 1) {
-      s_wp[cq * 128 + r_in] = wacc;
-      __syncthreads();
-      if (cq == 0) {
-        float wv = 0.f;
-#pragma unroll
-        for (int q = 0; q < CQ; ++q) wv += s_wp[q * 128 + r_in];
-        const int kc = cb * 128 + r_in;
-        a.w[(size_t)i * K + kc] = wv;
-        s_w[kc] = wv;
-        if (isnan(wv)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+  if (warp == kTcEpiWarps) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const unsigned char* colop = reinterpret_cast<const unsigned char*>(a.ws.colop);
+      const unsigned char* rowc = reinterpret_cast<const unsigned char*>(a.ws.rowop_b);
+      // z of a group is read by its prologue (two groups ahead) and its moments: keep three groups ahead in L2
+      for (int64_t jj = 0; jj < 3 && jj < ngroups; ++jj)
+        prefetch_l2_bulk(a.z + (size_t)(blockIdx.x + jj * gridDim.x) * kTcD * K, (uint32_t)(kTcD * K * 4));
+      for (TileWalk tw(RB, CB); tw.T < ntiles; tw.next()) {
+        const int64_t T = tw.T, j = tw.j;
+        const int t = tw.t, cb = tw.cb, rb = tw.rb;
+        const int64_t i = tw.i;
+        if (t == 0 && j + 3 < ngroups)
+          prefetch_l2_bulk(a.z + (size_t)(i + 3 * gridDim.x) * kTcD * K, (uint32_t)(kTcD * K * 4));
+        if (rb == 0) {
+          const int64_t J = tw.J;
+          const int st = (int)(J & 1);
+          if (J >= 2) mbar_wait(&a_empty[st], (uint32_t)(((J >> 1) - 1) & 1));
+          mbar_expect_tx(&a_full[st], L::A_STAGE);
+          tma_bulk_g2s(s_a + st * L::A_STAGE, colop + ((size_t)i * K + (size_t)cb * 128) * kTcColBytes, L::A_STAGE,
+                       &a_full[st]);
+        }
+        const int sb = (int)(T % SB);
+        const int64_t ub = T / SB;
+        if (ub >= 1) mbar_wait(&b_empty[sb], (uint32_t)((ub - 1) & 1));
+        mbar_expect_tx(&b_full[sb], L::B_STAGE);
+        tma_bulk_g2s(s_b + sb * L::B_STAGE, rowc + (size_t)rb * L::B_STAGE, L::B_STAGE, &b_full[sb]);
       }
     }
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0 && rb == RB - 1) issue_block(J + 2);
-    if (t == TPG - 1) {
-      // ---- moments of group i (fp64): E z, then Var z
-      double s1[kTcD];
-#pragma unroll
-      for (int r = 0; r < kTcD; ++r) s1[r] = 0.0;
-      for (int kc = tid; kc < K; kc += NT) {
-        const double wv = s_w[kc];
-#pragma unroll
-        for (int r = 0; r < kTcD; ++r) s1[r] += wv * (double)a.z[((size_t)i * kTcD + r) * K + kc];
+  } else if (warp == kTcEpiWarps + 1) {
+    // -------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(128, 256);
+      for (TileWalk tw(RB, CB); tw.T < ntiles; tw.next()) {
+        const int64_t T = tw.T, j = tw.j;
+        const int t = tw.t, cb = tw.cb, rb = tw.rb;
+        const int64_t J = tw.J;
+        const int sb = (int)(T % SB), tb = (int)(T & 1);
+        if (t == 0) mbar_wait(&bx_full[j & 1], (uint32_t)((j >> 1) & 1));
+        if (rb == 0) mbar_wait(&a_full[J & 1], (uint32_t)((J >> 1) & 1));
+        mbar_wait(&b_full[sb], (uint32_t)((T / SB) & 1));
+        if (T >= 2) mbar_wait(&t_empty[tb], (uint32_t)(((T >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t A = smem_u32(s_a + (J & 1) * L::A_STAGE), B = smem_u32(s_b + sb * L::B_STAGE);
+        const uint32_t BX = smem_u32(s_bx + (size_t)(j & 1) * K * kTcRowXBytes + (size_t)rb * 256 * kTcRowXBytes);
+        umma_tile7(tmem + (uint32_t)tb * 256, A, 1024, B, 768, A + 768, 1024, BX, 256, idesc);
+        umma_commit(&t_full[tb]);
+        umma_commit(&b_empty[sb]);
+        if (rb == RB - 1) umma_commit(&a_empty[J & 1]);
       }
-#pragma unroll
-      for (int r = 0; r < kTcD; ++r) {
-        const double v = warp_sum(s1[r]);
-        if (lane == 0) s_red[warp * kTcD + r] = v;
+    }
+  } else if (warp >= kTcEpiWarps + 2) {
+    // --------------------------------------------- aux: prologues one/two groups ahead, moments behind
+    const int atid = tid - kTcThreads;
+    for (int64_t jj = 0; jj < 2 && jj < ngroups; ++jj) {
+      bwd_prologue(a, blockIdx.x + jj * gridDim.x, s_bx + (size_t)jj * K * kTcRowXBytes, s_L + jj * K, s_t, s_rd,
+                   atid);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bx_full[jj]);
+        mbar_arrive(&l_full[jj]);
       }
-      __syncthreads();
-      if (tid < kTcD) {
-        double m = 0.0;
-        for (int w = 0; w < NW; ++w) m += s_red[w * kTcD + tid];
-        s_mom[tid] = m;
-      }
-      __syncthreads();
-      double s2[kTcD];
-#pragma unroll
-      for (int r = 0; r < kTcD; ++r) s2[r] = 0.0;
-      for (int kc = tid; kc < K; kc += NT) {
-        const double wv = s_w[kc];
-#pragma unroll
-        for (int r = 0; r < kTcD; ++r) {
-          const double dz = (double)a.z[((size_t)i * kTcD + r) * K + kc] - s_mom[r];
-          s2[r] += wv * dz * dz;
+    }
+    for (int64_t j = 0; j < ngroups; ++j) {
+      const int st = (int)(j & 1);
+      mbar_wait(&w_full[st], (uint32_t)((j >> 1) & 1));  // group j finished: its stages are free
+      if (j + 2 < ngroups) {
+        bwd_prologue(a, blockIdx.x + (j + 2) * gridDim.x, s_bx + (size_t)st * K * kTcRowXBytes, s_L + st * K, s_t,
+                     s_rd, atid);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&bx_full[st]);
+          mbar_arrive(&l_full[st]);
         }
       }
-      __syncthreads();
+      bwd_moments(a, blockIdx.x + j * gridDim.x, s_w + st * K, s_rd, atid);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&w_empty[st]);
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3, cq = warp >> 2;
+    float L2c = 0.f, acc = 0.f;
+    for (TileWalk tw(RB, CB); tw.T < ntiles; tw.next()) {
+      const int64_t T = tw.T, j = tw.j;
+      const int t = tw.t, cb = tw.cb, rb = tw.rb;
+      const int64_t i = tw.i;
+      const int st = (int)(j & 1);
+      if (t == 0) {
+        mbar_wait(&l_full[st], (uint32_t)((j >> 1) & 1));                 // column constants of group j
+        if (j >= 2) mbar_wait(&w_empty[st], (uint32_t)(((j >> 1) - 1) & 1));  // s_w stage read by moments(j-2)
+      }
+      const int col = cb * 128 + q * 32 + lane;
+      if (rb == 0) {
+        L2c = s_L[st * K + col];  // log2e log P(k'|k*)
+        acc = 0.f;
+      }
+      mbar_wait(&t_full[T & 1], (uint32_t)((T >> 1) & 1));
+      tc_fence_after();
+      const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * 64) + ((uint32_t)(q * 32) << 16);
+      float2 wp[2] = {f2(0.f), f2(0.f)};
+      const float2 l2 = f2(L2c);
+      tmem_pipeline16<4>(taddr, [&](int, uint32_t(&r)[16]) {
 #pragma unroll
-      for (int r = 0; r < kTcD; ++r) {
-        const double v = warp_sum(s2[r]);
-        if (lane == 0) s_red[warp * kTcD + r] = v;
+        for (int c = 0; c < 16; c += 2) {
+          const float2 x = add2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), l2);
+          wp[(c >> 1) & 1] = add2(wp[(c >> 1) & 1], make_float2(ex2(x.x), ex2(x.y)));
+        }
+      });
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[T & 1]);
+      {
+        const float2 s2 = add2(wp[0], wp[1]);
+        acc += s2.x + s2.y;
       }
-      __syncthreads();
-      if (tid < kTcD) {
-        double vv = 0.0;
-        for (int w = 0; w < NW; ++w) vv += s_red[w * kTcD + tid];
-        a.m1[i * kTcD + tid] = s_mom[tid];
-        a.v[i * kTcD + tid] = vv;
+      if (rb == RB - 1) {
+        float* wpb = s_wp + (cb & 1) * 512;
+        wpb[cq * 128 + q * 32 + lane] = acc;
+        quarter_bar(q);
+        if (cq == 0) {
+          const float wv = wpb[q * 32 + lane] + wpb[128 + q * 32 + lane] + wpb[256 + q * 32 + lane] +
+                           wpb[384 + q * 32 + lane];
+          a.w[(size_t)i * K + col] = wv;
+          s_w[st * K + col] = wv;
+          if (isnan(wv)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+        }
       }
-      __syncthreads();
+      if (t == TPG - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&w_full[st]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == kTcEpiWarps + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }

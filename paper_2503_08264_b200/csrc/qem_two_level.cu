@@ -46,6 +46,7 @@ struct TLArgs {
   double* trace;
   int64_t trace_len;
   int t_host;
+  int tc;        // tensor-core pair kernels in use (d = 16)
   float thr[5];  // forward tile-mode bounds for expm1 degrees 3/4/5/7/9
   TwoLevelWs ws;
   Counters* cnt;
@@ -135,14 +136,31 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
     double dd = 0.0;
     float* fc = a.ws.fwd_coef + (size_t)k * CW;
     float* bt = a.ws.bwd_table + (size_t)k * RS;
-    for (int r = 0; r < D; ++r) {
-      const double del = (double)a.z_root[r * K + k] - (double)a.z_root[r * K + kref];
-      dd += del * del;
-      const double cr = ek * del;
-      fc[2 + r] = (float)cr;
-      bt[2 + r] = (float)(cr * kLog2eD);
+    double alpha;
+    if (a.tc) {
+      // tensor-core path: origin-0 form D_k(z) = alpha0 + c0 . z + gamma |z|^2 with
+      // c0 = e_k mu_k - e_ref mu_ref, alpha0 = -(d/2) dlnv - (e_k |mu_k|^2 - e_ref |mu_ref|^2) / 2,
+      // so a group re-centres with its own mean alone
+      double mk2 = 0.0, mr2 = 0.0;
+      for (int r = 0; r < D; ++r) {
+        const double mk = (double)a.z_root[r * K + k], mr = (double)a.z_root[r * K + kref];
+        mk2 += mk * mk;
+        mr2 += mr * mr;
+        const double cr = ek * mk - e_ref * mr;
+        fc[2 + r] = (float)cr;
+        bt[2 + r] = (float)(cr * kLog2eD);
+      }
+      alpha = -0.5 * D * dlnv - 0.5 * (ek * mk2 - e_ref * mr2);
+    } else {
+      for (int r = 0; r < D; ++r) {
+        const double del = (double)a.z_root[r * K + k] - (double)a.z_root[r * K + kref];
+        dd += del * del;
+        const double cr = ek * del;
+        fc[2 + r] = (float)cr;
+        bt[2 + r] = (float)(cr * kLog2eD);
+      }
+      alpha = -0.5 * D * dlnv - 0.5 * ek * dd;
     }
-    const double alpha = -0.5 * D * dlnv - 0.5 * ek * dd;
     const double gamma = -0.5 * (ek - e_ref);
     fc[0] = (float)alpha;
     fc[1] = (float)gamma;
@@ -161,6 +179,7 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
     s_key[k] = fabsf(fc[0]) + fabsf(fc[1]) + sqrtf(cn);
   }
   __syncthreads();
+  if (a.tc) return;  // the tensor-core forward does not use the row order
   // rank sort (ties by index): perm[rank] = k
   for (int k = tid; k < K; k += blockDim.x) {
     const float kk = s_key[k];
@@ -233,6 +252,7 @@ __global__ void __launch_bounds__(1024) k_root(TLArgs a) {
     if (isnan(L)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
   }
   __syncthreads();
+  k_root_star<D>(a, wsh);  // backward reference row k* + k*-differenced rows
   const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   for (int r = wid; r < R; r += nw) {
     double s1 = 0.0;
@@ -264,31 +284,26 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
   float* spare = rows + (size_t)K * RS;                  // [K] (padded to even; unused)
   double* red = reinterpret_cast<double*>(spare + ((K + 1) & ~1));  // [32][D]
   double* mom = red + 32 * D;                            // [D]
-  float mur[D];
-#pragma unroll
-  for (int r = 0; r < D; ++r) mur[r] = a.ws.ref->mu_ref[r];
   const int lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
 
   for (int64_t i = blockIdx.x; i < a.n_local; i += gridDim.x) {
     __syncthreads();
-    // row table re-centred on the group's Q mean (same algebra as the forward):
-    // alpha'' = (alpha + gamma |u0|^2 + c.u0 - dg) log2e, c'' = (c + 2 gamma u0) log2e
+    // row table re-centred on the group's Q mean and referenced to the backward row k*
+    // (DESIGN.md "Backward reference"):  log P(k'|k) = log P(k'|k*) + E_k(k') - (l_k - l_*),
+    // E_k(z) = B(k,z) - B(k*,z) = E'a_ik + c''_k . w + Eg_k |w|^2 with c'' = Eb_k + 2 Eg_k m_i,
+    // and E'a_ik - (l_k - l_*) = -(h_k - h_*)  (h = the forward's re-centred message)
     {
-      float u0[D];
-      float U0sq = 0.f;
+      float mi[D];
 #pragma unroll
-      for (int r = 0; r < D; ++r) {
-        u0[r] = a.q_m[i * D + r] - mur[r];
-        U0sq = fmaf(u0[r], u0[r], U0sq);
-      }
+      for (int r = 0; r < D; ++r) mi[r] = a.q_m[i * D + r];
+      const float hs = a.ws.hmsg[(size_t)i * K + a.ws.ref->k_star];
       for (int k = tid; k < K; k += NT) {
-        const float* fc = a.ws.fwd_coef + (size_t)k * CW;
-        const float g = fc[1];
+        const float* bc = a.ws.bwd_coef + (size_t)k * (D + 1);
+        const float g = bc[D];
         float* rw = rows + (size_t)k * RS;
 #pragma unroll
-        for (int r = 0; r < D; ++r) rw[2 + r] = fmaf(2.f * g, u0[r], fc[2 + r]) * kLog2e;
-        // alpha'_k - dg_i(k) = -h_i(k): the re-centred message, no cancellation
-        rw[0] = -a.ws.hmsg[(size_t)i * K + k] * kLog2e;
+        for (int r = 0; r < D; ++r) rw[2 + r] = fmaf(2.f * g, mi[r], bc[r]) * kLog2e;
+        rw[0] = -(a.ws.hmsg[(size_t)i * K + k] - hs) * kLog2e;
         rw[1] = g * kLog2e;
         rw[2 + D] = a.w_root[k];
       }
@@ -296,12 +311,48 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
     float2 u[CP][D], U2[CP], Lc[CP];
     constexpr int CS = pad4(D + 3);
     const int Kp = FwdLayout<D>::kpad(K);
+    // column constants log P(k'|k*): softmax over the group's columns of the fp64 logits
+    // B(k*,k') + A_i(k') (A from the column prep)
+    double tl[CP][2];
+    double tmx = -CUDART_INF;
+    {
+      const double es = a.ws.ref->e_star, bs = a.ws.ref->bstar_const;
+#pragma unroll
+      for (int p = 0; p < CP; ++p)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kc = tid + NT * (2 * p + h);
+          tl[p][h] = -CUDART_INF;
+          if (kc < K) {
+            double d2 = 0.0, g2 = 0.0;
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+              const double zz = (double)a.z[((size_t)i * D + r) * K + kc];
+              const double dz = zz - (double)a.ws.ref->mu_star[r], gz = zz - (double)a.ws.ref->mu_ref[r];
+              d2 += dz * dz;
+              g2 += gz * gz;
+            }
+            // t_ref + B(k*,k') - B(k_ref,k')
+            tl[p][h] = (bs - 0.5 * es * d2) - (a.ws.ref->bref_const - 0.5 * a.ws.ref->e_ref * g2) +
+                       a.ws.tA[(size_t)i * K + kc];
+            tmx = fmax(tmx, tl[p][h]);
+          }
+        }
+    }
+    tmx = block_max(tmx, red);
+    double tse = 0.0;
+#pragma unroll
+    for (int p = 0; p < CP; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (tid + NT * (2 * p + h) < K) tse += exp(tl[p][h] - tmx);
+    const double tlse = tmx + log(block_sum(tse, red));
 #pragma unroll
     for (int p = 0; p < CP; ++p) {
       float uu[2][D], u2[2], lc[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        // column record (u, |u|^2, P, ln P) written by the column prep (K2a)
+        // column record (w, |w|^2, P, ln P) written by the column prep (K2a)
         const int kc = tid + NT * (2 * p + h);
         const bool ok = kc < K;
         float rec[CS];
@@ -317,7 +368,7 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
 #pragma unroll
         for (int r = 0; r < D; ++r) uu[h][r] = ok ? rec[r] : 0.f;
         u2[h] = ok ? rec[D] : 0.f;
-        lc[h] = ok ? rec[D + 2] * kLog2e : -CUDART_INF_F;
+        lc[h] = ok ? (float)((tl[p][h] - tlse) * kLog2eD) : -CUDART_INF_F;
       }
 #pragma unroll
       for (int r = 0; r < D; ++r) u[p][r] = make_float2(uu[0][r], uu[1][r]);
@@ -451,6 +502,7 @@ static TLArgs make_args(qem_ctx* c) {
   a.trace = c->in_iterate ? c->bufs.trace : nullptr;
   a.trace_len = c->bufs.trace_len;
   a.t_host = 0;
+  a.tc = c->tc;
   // |D'| bound below which the degree-n Taylor remainder |D'|^{n+1}/(n+1)!,
   // accumulated over all N groups of the plate, stays under 2e-6
   const int degs[5] = {3, 4, 5, 7, 9};
@@ -497,8 +549,7 @@ template <int D>
 static KernelFn prep_fn(int obs, bool tc) {
   if constexpr (D == 1)
     if (obs == QEM_OBS_GAUSS) return k_colprep<D, QEM_OBS_GAUSS, false>;
-  if constexpr (D == kTcD)
-    if (tc) return k_colprep<D, QEM_OBS_BERNOULLI_LOGIT, true>;
+  if (tc) return k_colprep_tc;
   return k_colprep<D, QEM_OBS_BERNOULLI_LOGIT, false>;
 }
 template <int D>
@@ -516,19 +567,21 @@ static int occupancy(KernelFn f, int nt, size_t sm) {
 
 template <int D>
 static int prep_threads(int) { return 32 * FwdLayout<D>::PREP_WARPS; }
+template <int D>
+static size_t prep_smem(int K, int J, bool tc) { return tc ? PrepTc::bytes(K, J) : FwdLayout<D>::prep_bytes(K, J); }
 
 template <int D>
 static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, int* gf, int* gb, int* gp) {
   const int K = d->K, rp = pick_rp(K);
   int of, ob;
   if (tc) {
-    of = occupancy(k_forward_tc<kTcCQ>, 128 * kTcCQ, FwdTcLayout<kTcCQ>::bytes(K));
-    ob = occupancy(k_backward_tc<kTcCQ>, 128 * kTcCQ, BwdTcLayout<kTcCQ>::bytes(K));
+    of = occupancy(k_forward_tc, kTcThreads, FwdTcL::bytes(K));
+    ob = occupancy(k_backward_tc, kBwdThreads, BwdTcL::bytes(K));
   } else {
     of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
     ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
   }
-  const int op = occupancy(prep_fn<D>(d->obs_kind, tc), prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, d->n_obs));
+  const int op = occupancy(prep_fn<D>(d->obs_kind, tc), prep_threads<D>(K), prep_smem<D>(K, d->n_obs, tc));
   // Persistent-style grids: one full wave of resident CTAs, capped by the groups.
   int64_t f = (int64_t)sms * of, b = (int64_t)sms * ob, p = (int64_t)sms * op;
   *gf = (int)(f < n_local ? f : n_local);
@@ -546,15 +599,15 @@ static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st
   if (c->desc.obs_kind == QEM_OBS_GAUSS && D != 1) return cudaErrorInvalidValue;
   const bool tc = D == kTcD && c->tc;
   if (tc) {
-    k_rowop<<<(K * kTcD + 255) / 256, 256, 0, st>>>(a);
+    k_rowop_tc<<<(K + 255) / 256, 256, 0, st>>>(a);
     c->launches += 1;
   }
-  prep_fn<D>(c->desc.obs_kind, tc)<<<c->grid_prep, prep_threads<D>(K), FwdLayout<D>::prep_bytes(K, a.J), st>>>(a);
+  prep_fn<D>(c->desc.obs_kind, tc)<<<c->grid_prep, prep_threads<D>(K), prep_smem<D>(K, a.J, tc), st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (c->ev[0]) cudaEventRecord((cudaEvent_t)c->ev[0], st);
   if (tc)
-    k_forward_tc<kTcCQ><<<c->grid_fwd, 128 * kTcCQ, FwdTcLayout<kTcCQ>::bytes(K), st>>>(a);
+    k_forward_tc<<<c->grid_fwd, kTcThreads, FwdTcL::bytes(K), st>>>(a);
   else
     fwd_fn<D>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
   if (c->ev[1]) cudaEventRecord((cudaEvent_t)c->ev[1], st);
@@ -572,7 +625,7 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   const int cp = pick_rp(K);
   if (c->ev[2]) cudaEventRecord((cudaEvent_t)c->ev[2], st);
   if (D == kTcD && c->tc)
-    k_backward_tc<kTcCQ><<<c->grid_bwd, 128 * kTcCQ, BwdTcLayout<kTcCQ>::bytes(K), st>>>(a);
+    k_backward_tc<<<c->grid_bwd, kBwdThreads, BwdTcL::bytes(K), st>>>(a);
   else
     bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
   if (c->ev[3]) cudaEventRecord((cudaEvent_t)c->ev[3], st);

@@ -1,0 +1,85 @@
+"""GPU parity of the tcgen05 tensor-core pair kernels (d = 16, K % 256 == 0) vs the oracle.
+
+The tensor-core path has its own operand layouts,
+warp-specialised pipeline and per-group tile modes, so it gets its own sweep:
+every forward tile mode (expm1 polynomial degrees 3..9 and the online
+log-sum-exp), K = 256 / 512 / 1024 (one to four column blocks), and more
+groups than SMs (several groups per persistent CTA, ragged last wave), with
+the north-star tolerances of tests/test_gpu_parity.py.
+"""
+import numpy as np
+import pytest
+
+from helpers import make_case, posterior_like_q
+from oracle import oracle as orc
+from paper_2503_08264_b200 import synth
+from test_gpu_parity import check_estep
+
+pytestmark = pytest.mark.gpu
+
+# (groups, K, Q regime): shrink = multiple of the posterior width of posterior_like_q;
+# "prior" = random Q (one-hot root weights, online mode)
+CASES = {
+    "n40_K256_post1": (40, 256, 1.0),
+    "n300_K512_post3": (300, 512, 3.0),
+    "n161_K256_post10": (161, 256, 10.0),
+    "n150_K1024_post1": (150, 1024, 1.0),
+    "n301_K256_prior": (301, 256, None),
+    "n23_K768_post0.3": (23, 768, 0.3),
+    # very narrow Q: |D'| small enough for the expm1-polynomial tile modes
+    "n60_K256_post0.2": (60, 256, 0.2),
+    "n60_K256_post0.12": (60, 256, 0.12),
+    "n60_K256_post0.08": (60, 256, 0.08),
+    "n60_K256_post0.05": (60, 256, 0.05),
+    "n60_K512_post0.01": (60, 512, 0.01),
+    "n60_K256_post0.002": (60, 256, 0.002),
+    "n60_K256_post0.0004": (60, 256, 0.0004),
+}
+
+_seen_modes = np.zeros(6, np.int64)
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_tc_estep_parity(case):
+    from paper_2503_08264_b200.qem import QEM
+    n, K, shrink = CASES[case]
+    m = synth.config(5, n=n, K=K)
+    data = synth.make_data(m)
+    q = synth.random_q(m, 11) if shrink is None else posterior_like_q(m, data, seed=7, shrink=shrink)
+    _, _, eps, _ = make_case(m, q=q)
+    z = [orc.sample(qm, qv, e) for (qm, qv), e in zip(q, eps)]
+    ref = orc.estep(m, z, q, data)
+    g = QEM(m)
+    assert g.pair_path() == 1, "d=16, K%256==0 must run the tensor-core kernels"
+    g.set_data(data)
+    g.set_q(q)
+    g.sample_q(eps=eps)
+    g.estep()
+    out = g.result()
+    hist = np.asarray(g.mode_hist(), np.int64)
+    dg, c = g.messages()
+    flags, _ = g.read_flags()
+    g.close()
+    _seen_modes[:] += hist
+    assert hist.sum() == n, hist  # one mode per group
+    check_estep(m, out, ref, note=f"tc/{case}")
+    assert flags & 2 == 0
+    if shrink is None or shrink > 3:
+        # one-hot regime with the reference row far from the weight mass: |lnP|, |D'|, |h| reach
+        # O(500) on the dominant row, resolved to fp32; only the contract quantities are gated
+        return
+    # plate messages g_i(k) = c_i + dg_i(k) against the oracle's, on the rows the root
+    # softmax can see (w_root > 1e-6; far rows carry O(1000) log-factors resolved to fp32)
+    rows = ref["w"][0].reshape(-1) > 1e-6
+    g_ref = ref["g"][:, rows]
+    full = (c.cpu().numpy()[:, None] + dg.cpu().numpy().astype(np.float64))[:, rows]
+    err = np.abs(full - g_ref) / (5e-6 + 1e-6 * np.abs(g_ref))
+    assert err.max() <= 1.0, (case, float(err.max()))
+
+
+def test_tc_modes_covered():
+    """The sweep above must have exercised the online mode and the polynomial modes."""
+    if _seen_modes.sum() == 0:
+        pytest.skip("run with the parity sweep")
+    assert _seen_modes[5] > 0, _seen_modes
+    assert (_seen_modes[:5] > 0).sum() >= 1, _seen_modes
