@@ -69,6 +69,24 @@ def _measured_bf16() -> float:
 BF16_TFLOPS = _measured_bf16()
 
 
+def _algo_bytes(dom: str, tc: bool, n: int, m) -> float:
+    """Bytes one launch of the dominant pair kernel must move: its per-column operand stream in
+    (TC: 128 B column operand + 4 B P or log P(k'|k*); FFMA: the pad4(d+3) fp32 column record) and its
+    per-(group, sample) outputs (forward: dg + h, 8 B; backward: w, 4 B)."""
+    col = (128 + 4) if tc else 4 * ((m.d + 3 + 3) // 4 * 4)
+    out = 8 if dom == "forward" else 4
+    return float(n) * m.K * (col + out)
+
+
+def _ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (tools/ncu_traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return json.load(f)[kernel]["dram_bytes"]
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -263,7 +281,10 @@ def run_gpu(args):
     per_pair = ({"exp": 1, "fp32": 3, "tensor_bf16_flops": 12 * m.d} if tc else {"exp": 1, "fp32": m.d + 2})
     roof = {"bound": "alu", "pipe": ceil["pipe"], "kernel": f"k_{dom}" + ("_tc" if tc else ""), "unit": "Gpair/s",
             "achieved": achieved / 1e9, "peak": ceil["pairs_per_s"] / 1e9,
-            "frac": achieved / ceil["pairs_per_s"], "traffic": None,
+            "frac": achieved / ceil["pairs_per_s"],
+            "traffic": _ncu_traffic(f"k_{dom}" + ("_tc" if tc else "")),
+            "traffic_unit": "bytes/launch (ncu --set full, profiles/r01_traffic.json)",
+            "algorithmic_bytes": _algo_bytes(dom, tc, ge - gb, m),
             "per_pair": per_pair,
             "pipe_ceilings_gpair_s": {k.replace("_pairs_per_s", ""): v / 1e9 for k, v in ceil.items()
                                       if k.endswith("_pairs_per_s") and k != "pairs_per_s"},

@@ -99,6 +99,8 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
   }
 }
 
+constexpr float kLazy = 5.0f;  // natural-log units: deferred-rescale margin of the online log-sum-exp
+
 template <int D, int RP>
 __device__ __forceinline__ void tile_online(const float* col, int Kp, const float2 (&al)[RP], const float2 (&ga)[RP],
                                             const float2 (&cc)[RP][D], float (&dgv)[2 * RP]) {
@@ -124,17 +126,24 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
       float2 cm = tv[0][p];
 #pragma unroll
       for (int c = 1; c < CH; ++c) cm = max2(cm, tv[c][p]);
-      const float2 mn = max2(mr[p], cm);
-      const float2 sc = make_float2(ex2((mr[p].x - mn.x) * kLog2e), ex2((mr[p].y - mn.y) * kLog2e));
-      const float2 nm = make_float2(-mn.x * kLog2e, -mn.y * kLog2e);
-      float2 s = mul2(ac[p], sc);
+      // lazy max: rescale only when a chunk exceeds the running shift by > kLazy (the
+      // unscaled terms stay <= e^kLazy), so almost every pair costs exactly one ex2
+      if (cm.x > mr[p].x + kLazy) {
+        ac[p].x *= ex2((mr[p].x - cm.x) * kLog2e);
+        mr[p].x = cm.x;
+      }
+      if (cm.y > mr[p].y + kLazy) {
+        ac[p].y *= ex2((mr[p].y - cm.y) * kLog2e);
+        mr[p].y = cm.y;
+      }
+      const float2 nm = make_float2(-mr[p].x * kLog2e, -mr[p].y * kLog2e);
+      float2 s = ac[p];
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const float2 e = fma2(tv[c][p], f2(kLog2e), nm);
         s = add2(s, make_float2(ex2(e.x), ex2(e.y)));
       }
       ac[p] = s;
-      mr[p] = mn;
     }
   }
 #pragma unroll
@@ -159,7 +168,11 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
   double* qconst = tref + K;                            // [3][D]
   uint32_t* bmask = reinterpret_cast<uint32_t*>(qconst + 3 * D);  // [J]
   uint32_t* ybits = bmask + J;                          // [J]
-  const RefInfo ref = *a.ws.ref;
+  // reference-row constants (fields read individually: the struct is large)
+  float mu_ref[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) mu_ref[r] = a.ws.ref->mu_ref[r];
+  const double bref_const = a.ws.ref->bref_const, e_ref = a.ws.ref->e_ref;
   const double logK = log((double)K);
   double gc0 = 0.0, gc1 = 0.0;
   if constexpr (OBS == QEM_OBS_GAUSS) {
@@ -235,7 +248,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
         const float w = zr[r] - (float)qconst[r];
         rec[r] = w;
         W2 = fmaf(w, w, W2);
-        const double u = (double)zr[r] - (double)ref.mu_ref[r];
+        const double u = (double)zr[r] - (double)mu_ref[r];
         U2d += u * u;
       }
       {
@@ -247,7 +260,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
         for (int q = 0; q < CS / 4; ++q)
           dst[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
       }
-      const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
+      const double t = bref_const - 0.5 * e_ref * U2d + (ll - lq);
       a.ws.tA[(size_t)i * K + kc] = t;  // t_ref, for the backward's k*-row softmax
       tref[kc] = t;
       tmax = fmax(tmax, t);

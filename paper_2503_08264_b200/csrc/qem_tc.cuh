@@ -192,21 +192,26 @@ __global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
 struct PrepTc {
   static constexpr int WARPS = 8;
   __host__ __device__ static size_t warp_bytes(int K, int J) {
-    size_t b = 3 * kTcD * 8 + (size_t)J * kTcD * 4 + (size_t)J * 4;
+    size_t b = 3 * kTcD * 8 + 2 * kTcD * 4 + (size_t)((J + 1) / 2) * kTcD * 8;
     return (b + 15) & ~(size_t)15;
   }
   __host__ __device__ static size_t bytes(int K, int J) { return WARPS * warp_bytes(K, J); }
 };
 
-__global__ void __launch_bounds__(256, 3) k_colprep_tc(TLArgs a) {
+__global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int D = kTcD;
   const int K = a.K, J = a.J, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned char* wb = smem + (size_t)wid * PrepTc::warp_bytes(K, J);
   double* qc = reinterpret_cast<double*>(wb);                      // [3][D]: m, 1/(2v), -(ln 2pi v)/2
-  float* xf = reinterpret_cast<float*>(qc + 3 * D);                // [J][D] features as 0/1 floats
-  float* yf = xf + J * D;                                          // [J]
-  const RefInfo ref = *a.ws.ref;
+  float* yx = reinterpret_cast<float*>(qc + 3 * D);                // [D]  sum_j y_j x_j (integer-valued)
+  float* mref = yx + D;                                            // [D]  mu_ref
+  float2* xp = reinterpret_cast<float2*>(mref + D);                // [(J+1)/2][D] {x_2p, x_2p+1} as 0/1
+  const int Jh = (J + 1) / 2;
+  // reference-row constants (fields read individually: the struct is large)
+  if (lane < D) mref[lane] = a.ws.ref->mu_ref[lane];
+  const volatile float* mu_ref = mref;  // re-read per column (keeps registers for the z prefetch)
+  const double bref_const = a.ws.ref->bref_const, e_ref = a.ws.ref->e_ref;
   const double logK = log((double)K);
   unsigned char* colop = reinterpret_cast<unsigned char*>(a.ws.colop);
   for (int64_t i = (int64_t)blockIdx.x * PrepTc::WARPS + wid; i < a.n_local;
@@ -221,39 +226,60 @@ __global__ void __launch_bounds__(256, 3) k_colprep_tc(TLArgs a) {
     {
       const uint8_t* x = reinterpret_cast<const uint8_t*>(a.x) + (size_t)i * J * D;
       const uint8_t* y = reinterpret_cast<const uint8_t*>(a.y) + (size_t)i * J;
-      for (int e = lane; e < J * D; e += 32) xf[e] = x[e] ? 1.f : 0.f;
-      for (int j = lane; j < J; j += 32) yf[j] = y[j] ? 1.f : 0.f;
+      for (int e = lane; e < Jh * D; e += 32) {
+        const int jp = e / D, r = e % D, j0 = 2 * jp, j1 = 2 * jp + 1;
+        xp[e] = make_float2(x[j0 * D + r] ? 1.f : 0.f, (j1 < J && x[j1 * D + r]) ? 1.f : 0.f);
+      }
+      if (lane < D) {
+        int v = 0;
+        for (int j = 0; j < J; ++j) v += (y[j] && x[j * D + lane]) ? 1 : 0;
+        yx[lane] = (float)v;
+      }
     }
     __syncwarp();
     unsigned char* cop = colop + (size_t)i * K * kTcColBytes;
     double tmax = -CUDART_INF;
     float w2max = 0.f;
+    // z of the next column is loaded while this one is processed (latency hiding at 16 warps/SM)
+    float zn[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) zn[r] = lane < K ? a.z[((size_t)i * D + r) * K + lane] : 0.f;
     for (int kc = lane; kc < K; kc += 32) {
       float zr[D];
 #pragma unroll
-      for (int r = 0; r < D; ++r) zr[r] = a.z[((size_t)i * D + r) * K + kc];
-      double lq = 0.0;
+      for (int r = 0; r < D; ++r) zr[r] = zn[r];
+      if (kc + 32 < K) {
+#pragma unroll
+        for (int r = 0; r < D; ++r) zn[r] = a.z[((size_t)i * D + r) * K + kc + 32];
+      }
+      // log q(z) and the label part sum_j y_j eta_j = (sum_j y_j x_j) . z, both fp64
+      // (group constants re-read from SMEM each column: volatile keeps ptxas from hoisting 48 doubles)
+      const volatile double* qv = qc;
+      double lq = 0.0, ly = 0.0;
 #pragma unroll
       for (int r = 0; r < D; ++r) {
-        const double dz = (double)zr[r] - qc[r];
-        lq += qc[2 * D + r] - dz * dz * qc[D + r];
+        const double zd = (double)zr[r], dz = zd - qv[r];
+        lq += qv[2 * D + r] - dz * dz * qv[D + r];
+        ly = fma((double)yx[r], zd, ly);
       }
-      double ll = 0.0;
-      for (int j = 0; j < J; ++j) {
-        const float4* xr = reinterpret_cast<const float4*>(xf + j * D);
-        float e0 = 0.f, e1 = 0.f;
+      // softplus part: eta_j = x_j . z for two observations at a time (FFMA2)
+      double lsp = 0.0;
+      for (int jp = 0; jp < Jh; ++jp) {
+        const float4* xr = reinterpret_cast<const float4*>(xp + jp * D);
+        float2 e0 = f2(0.f), e1 = f2(0.f);
 #pragma unroll
-        for (int q = 0; q < D / 4; ++q) {
+        for (int q = 0; q < D / 2; ++q) {
           const float4 xv = xr[q];
-          e0 = fmaf(xv.x, zr[4 * q], e0);
-          e1 = fmaf(xv.y, zr[4 * q + 1], e1);
-          e0 = fmaf(xv.z, zr[4 * q + 2], e0);
-          e1 = fmaf(xv.w, zr[4 * q + 3], e1);
+          e0 = fma2(make_float2(xv.x, xv.y), f2(zr[2 * q]), e0);
+          e1 = fma2(make_float2(xv.z, xv.w), f2(zr[2 * q + 1]), e1);
         }
-        const float eta = e0 + e1;
-        const float sp = fmaxf(eta, 0.f) + log1pf(__expf(-fabsf(eta)));
-        ll += (double)(yf[j] * eta) - (double)sp;
+        const float2 eta = add2(e0, e1);
+        const float sa = fmaxf(eta.x, 0.f) + log1pf(__expf(-fabsf(eta.x)));
+        const float sb = fmaxf(eta.y, 0.f) + log1pf(__expf(-fabsf(eta.y)));
+        lsp += (double)sa;
+        if (2 * jp + 1 < J) lsp += (double)sb;
       }
+      const double ll = ly - lsp;
       // column operand re-centred on the group's Q mean: w = z - m_i and
       // S = |w|^2 + 2 m_i . w (so D_k(z) = alpha'_ik + c0_k . w + gamma_k S)
       float W2 = 0.f, mw = 0.f;
@@ -265,7 +291,7 @@ __global__ void __launch_bounds__(256, 3) k_colprep_tc(TLArgs a) {
         wv[r] = zr[r] - m;
         W2 = fmaf(wv[r], wv[r], W2);
         mw = fmaf(m, wv[r], mw);
-        const double ud = (double)zr[r] - (double)ref.mu_ref[r];
+        const double ud = (double)zr[r] - (double)mu_ref[r];
         U2d += ud * ud;
       }
 #pragma unroll
@@ -289,7 +315,7 @@ __global__ void __launch_bounds__(256, 3) k_colprep_tc(TLArgs a) {
         *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 48)) = c0;
       }
       // t_ref(k') = B(k_ref,k') + A_i(k') (fp64; the backward rebuilds A from it)
-      const double t = ref.bref_const - 0.5 * ref.e_ref * U2d + (ll - lq);
+      const double t = bref_const - 0.5 * e_ref * U2d + (ll - lq);
       a.ws.tA[(size_t)i * K + kc] = t;
       tmax = fmax(tmax, t);
       w2max = fmaxf(w2max, W2);
@@ -298,6 +324,7 @@ __global__ void __launch_bounds__(256, 3) k_colprep_tc(TLArgs a) {
     const float W2max = warp_maxf(w2max);
     double sum = 0.0;
     const double* tref = a.ws.tA + (size_t)i * K;  // written above by this lane (program order)
+#pragma unroll 4
     for (int kc = lane; kc < K; kc += 32) sum += (double)expf((float)(tref[kc] - M));
     const double logS = log(warp_sum(sum));
     // tile mode: bound on |D'_k(k')| = |c'_k . w + gamma_k |w|^2|, c' = c0 + 2 gamma m_i
@@ -386,8 +413,8 @@ __device__ __forceinline__ void fwd_epi_online(uint32_t taddr, float& m, float& 
     for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
     const float m0 = fmax3f(v[0], v[1], v[2]), m1 = fmax3f(v[3], v[4], v[5]), m2 = fmax3f(v[6], v[7], v[8]);
     const float m3 = fmax3f(v[9], v[10], v[11]), m4 = fmax3f(v[12], v[13], v[14]);
-    const float mx = fmax3f(fmax3f(m0, m1, m2), fmax3f(m3, m4, v[15]), m);
-    if (mx > m) {
+    const float mx = fmax3f(m0, m1, fmax3f(m2, m3, fmax3f(m4, v[15], m)));
+    if (mx > m + 8.f) {  // lazy shift (log2 units): unscaled terms stay <= 2^8
       s *= ex2(m - mx);
       m = mx;
     }
@@ -580,7 +607,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
       const int64_t i = tw.i;
       if (t == 0) {
         // ---- group setup: the group's mode; m_i for the fp64 re-centring constant alpha'_ik
-        epi_bar();
+        // (nothing in SMEM is group-scoped, so no barrier: warps drift freely across groups)
         md = a.ws.gmode[i];
         M2 = 0.f;
 #pragma unroll
@@ -688,6 +715,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
 }
 
 // ----------------------------------------------------------------- backward
+constexpr int kBwdAuxWarps = 2;  // per-group row-slab builders of the backward
+
 struct BwdTcL {
   static constexpr int SB = 3;                                  // row-block stages
   static constexpr uint32_t A_STAGE = 128 * kTcColBytes;        // 16 KB: 128 columns
@@ -695,144 +724,147 @@ struct BwdTcL {
   static constexpr size_t a() { return 0; }
   static constexpr size_t b() { return a() + 2 * A_STAGE; }
   static constexpr size_t wp() { return b() + SB * B_STAGE; }            // [2][4][128] float
-  static constexpr size_t rd() { return wp() + 2 * 4 * 128 * 4; }        // aux scratch [2 warps][40] double
-  static constexpr size_t bars() { return rd() + 2 * 40 * 8; }           // 24 mbarriers
-  static size_t __host__ __device__ w(int) { return bars() + 24 * 8; }   // [2][K] float
-  static size_t __host__ __device__ lst(int K) { return w(K) + (size_t)2 * K * 4; }  // [2][K] float
-  static size_t __host__ __device__ tt(int K) { return lst(K) + (size_t)2 * K * 4; }  // [K] double (prologue)
-  static size_t __host__ __device__ bx(int K) { return (tt(K) + (size_t)K * 8 + 1023) & ~(size_t)1023; }
+  static constexpr size_t bars() { return wp() + 2 * 4 * 128 * 4; }      // 24 mbarriers
+  static size_t __host__ __device__ bx(int) { return (bars() + 24 * 8 + 1023) & ~(size_t)1023; }
   static size_t __host__ __device__ bytes(int K) { return bx(K) + (size_t)2 * K * kTcRowXBytes; }
 };
+constexpr int kBwdThreads = kTcThreads + 32 * kBwdAuxWarps;
 
-constexpr int kBwdAuxWarps = 2;
-constexpr int kBwdThreads = kTcThreads + 32 * kBwdAuxWarps;  // + per-group prologue / moment warps
-__device__ __forceinline__ void aux_bar() { named_bar(6, 32 * kBwdAuxWarps); }
+// ------------------------------------------------- backward column constants (K4a)
+// Backward reference:
+//   log P(k'|k) = log P(k'|k*) + E_k(k') - (l_k - l_*),  E_k = B(k,.) - B(k*,.).
+// One warp per group: the column constants L*(k') = log2e log P(k'|k*), a softmax over
+// the group's columns of the fp64 logits t_ref(k') + B(k*,k') - B(k_ref,k'), into
+// colaux's second slot (the forward's ln P is not needed any more).
+struct BwdColsTc {
+  static constexpr int WARPS = 8;
+  __host__ __device__ static size_t bytes(int K) { return (size_t)WARPS * K * 8; }
+};
 
-// Backward prologue of group i, run by the aux warps one or two groups ahead
-// (backward reference):
-//   log P(k'|k) = log P(k'|k*) + E_k(k') - (l_k - l_*),  E_k = B(k,.) - B(k*,.),
-// and with both passes re-centred on m_i the row constant reduces to
-//   rho_k = log2 w_root(k) - log2e (h_k - h_*)          (h = forward message)
-// so no fp32 term larger than the k*-relative spread ever cancels.
-//  * row extra slab (K x 32 B) into `bx`: [Eg pattern | 0 0 0 | rho] (rho = -1e30 where w_root = 0)
-//  * column constants sL[k'] = log2e log P(k'|k*), a softmax of row k* over the
-//    group's columns with fp64 logits B(k*,k') + A_i(k').
-__device__ void bwd_prologue(const TLArgs& a, int64_t i, unsigned char* bx, float* sL, double* s_t, double* s_rd,
-                             int atid) {
-  constexpr int NT = 32 * kBwdAuxWarps;
-  const int K = a.K, lane = atid & 31, warp = atid >> 5;
-  const int ks = a.ws.ref->k_star;
-  const float hs = a.ws.hmsg[(size_t)i * K + ks];
-  for (int k = atid; k < K; k += NT) {
-    const float wr = a.w_root[k];
-    const float rho = wr > 0.f ? log2f(wr) - (a.ws.hmsg[(size_t)i * K + k] - hs) * kLog2e : -1e30f;
-    uint4 c0, c1;
-    extra_row(a.ws.bgam[k], 0.f, rho, c0, c1);
-    *reinterpret_cast<uint4*>(bx + tc_rowx_offset(k, 0)) = c0;
-    *reinterpret_cast<uint4*>(bx + tc_rowx_offset(k, 8)) = c1;
+__global__ void __launch_bounds__(256) k_bwd_cols_tc(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int K = a.K, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* tv = reinterpret_cast<double*>(smem) + (size_t)wid * K;
+  float mus[kTcD], mur[kTcD];
+#pragma unroll
+  for (int r = 0; r < kTcD; ++r) {
+    mus[r] = a.ws.ref->mu_star[r];
+    mur[r] = a.ws.ref->mu_ref[r];
   }
-  fence_proxy_async();  // generic-proxy SMEM writes -> visible to the tensor core (async proxy)
   const double es = a.ws.ref->e_star, bs = a.ws.ref->bstar_const;
-  // logits t(k') = B(k*,k') + A_i(k') in fp64 for 4 consecutive columns per step (float4 z loads)
-  double mx = -CUDART_INF;
-  for (int c4 = atid * 4; c4 < K; c4 += NT * 4) {
-    float4 zv[kTcD];
+  const double er = a.ws.ref->e_ref, br = a.ws.ref->bref_const;
+  for (int64_t i = (int64_t)blockIdx.x * BwdColsTc::WARPS + wid; i < a.n_local;
+       i += (int64_t)gridDim.x * BwdColsTc::WARPS) {
+    double mx = -CUDART_INF;
+    for (int c4 = lane * 4; c4 < K; c4 += 128) {
+      float4 zv[kTcD];
 #pragma unroll
-    for (int r = 0; r < kTcD; ++r) zv[r] = *reinterpret_cast<const float4*>(a.z + ((size_t)i * kTcD + r) * K + c4);
-    const double2 ta = *reinterpret_cast<const double2*>(a.ws.tA + (size_t)i * K + c4);
-    const double2 tb = *reinterpret_cast<const double2*>(a.ws.tA + (size_t)i * K + c4 + 2);
-    // B(k*,k') - B(k_ref,k') = (bs - es |z - mu*|^2 / 2) - (br - er |z - mu_ref|^2 / 2), fp64
-    double d[4] = {0.0, 0.0, 0.0, 0.0}, g[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int r = 0; r < kTcD; ++r) zv[r] = *reinterpret_cast<const float4*>(a.z + ((size_t)i * kTcD + r) * K + c4);
+      const double2 ta = *reinterpret_cast<const double2*>(a.ws.tA + (size_t)i * K + c4);
+      const double2 tb = *reinterpret_cast<const double2*>(a.ws.tA + (size_t)i * K + c4 + 2);
+      double d[4] = {0.0, 0.0, 0.0, 0.0}, g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int r = 0; r < kTcD; ++r) {
-      const double mu = (double)a.ws.ref->mu_star[r], mr = (double)a.ws.ref->mu_ref[r];
-      const double zz[4] = {(double)zv[r].x, (double)zv[r].y, (double)zv[r].z, (double)zv[r].w};
+      for (int r = 0; r < kTcD; ++r) {
+        const double zz[4] = {(double)zv[r].x, (double)zv[r].y, (double)zv[r].z, (double)zv[r].w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double ds = zz[c] - (double)mus[r], dr = zz[c] - (double)mur[r];
+          d[c] = fma(ds, ds, d[c]);
+          g[c] = fma(dr, dr, g[c]);
+        }
+      }
+      const double t4[4] = {ta.x, ta.y, tb.x, tb.y};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        d[c] = fma(zz[c] - mu, zz[c] - mu, d[c]);
-        g[c] = fma(zz[c] - mr, zz[c] - mr, g[c]);
+        const double t = (bs - 0.5 * es * d[c]) - (br - 0.5 * er * g[c]) + t4[c];
+        tv[c4 + c] = t;
+        mx = fmax(mx, t);
       }
     }
-    const double er = a.ws.ref->e_ref, br = a.ws.ref->bref_const;
-    const double t0 = (bs - 0.5 * es * d[0]) - (br - 0.5 * er * g[0]) + ta.x;
-    const double t1 = (bs - 0.5 * es * d[1]) - (br - 0.5 * er * g[1]) + ta.y;
-    const double t2 = (bs - 0.5 * es * d[2]) - (br - 0.5 * er * g[2]) + tb.x;
-    const double t3 = (bs - 0.5 * es * d[3]) - (br - 0.5 * er * g[3]) + tb.y;
-    s_t[c4] = t0;
-    s_t[c4 + 1] = t1;
-    s_t[c4 + 2] = t2;
-    s_t[c4 + 3] = t3;
-    mx = fmax(fmax(mx, fmax(t0, t1)), fmax(t2, t3));
+    mx = warp_max(mx);
+    __syncwarp();
+    double se = 0.0;
+#pragma unroll 4
+    for (int kc = lane; kc < K; kc += 32) se += (double)expf((float)(tv[kc] - mx));
+    const double lse = mx + log(warp_sum(se));
+    float* L = a.ws.colaux + (size_t)i * 2 * K + K;
+    for (int kc = lane; kc < K; kc += 32) L[kc] = (float)((tv[kc] - lse) * kLog2eD);
+    __syncwarp();
   }
-  mx = warp_max(mx);
-  if (lane == 0) s_rd[warp * 40 + 32] = mx;
-  aux_bar();
-  mx = s_rd[32];
-#pragma unroll
-  for (int w = 1; w < kBwdAuxWarps; ++w) mx = fmax(mx, s_rd[w * 40 + 32]);
-  double se = 0.0;
-  for (int kc = atid; kc < K; kc += NT) se += (double)expf((float)(s_t[kc] - mx));
-  se = warp_sum(se);
-  if (lane == 0) s_rd[warp * 40 + 33] = se;
-  aux_bar();
-  se = 0.0;
-#pragma unroll
-  for (int w = 0; w < kBwdAuxWarps; ++w) se += s_rd[w * 40 + 33];
-  const double lse = mx + log(se);
-  for (int kc = atid; kc < K; kc += NT) sL[kc] = (float)((s_t[kc] - lse) * kLog2eD);
-  aux_bar();  // s_t / s_rd reusable
 }
 
-// Moments of group i from its weights (fp64, self-normalised, shifted by the Q mean):
-// E z = c + S1/S0, Var z = S2/S0 - (S1/S0)^2, S_p = sum_k' w (z - c)^p.
-__device__ void bwd_moments(const TLArgs& a, int64_t i, const float* sw, double* s_rd, int atid) {
-  constexpr int NT = 32 * kBwdAuxWarps;
-  const int K = a.K, lane = atid & 31, warp = atid >> 5;
-  double s0 = 0.0;
-  for (int kc = atid; kc < K; kc += NT) s0 += (double)sw[kc];
-  s0 = warp_sum(s0);
+// ------------------------------------------------------------ moments (K4c)
+// One warp per group, after the backward: E z = c + S1/S0, Var z = S2/S0 - (S1/S0)^2,
+// S_p = sum_k' w (z - c)^p in fp64 (self-normalised, shifted by the Q mean c = m_i; R24).
+__global__ void __launch_bounds__(256) k_moments_tc(TLArgs a) {
+  const int K = a.K, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * nw + wid; i < a.n_local; i += (int64_t)gridDim.x * nw) {
+    const float* w = a.w + (size_t)i * K;
+    double s0 = 0.0;
+    for (int c4 = lane * 4; c4 < K; c4 += 128) {
+      const float4 wv = *reinterpret_cast<const float4*>(w + c4);
+      s0 += ((double)wv.x + (double)wv.y) + ((double)wv.z + (double)wv.w);
+    }
+    s0 = warp_sum(s0);
 #pragma unroll 1
-  for (int r0 = 0; r0 < kTcD; r0 += 4) {
-    double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int c4 = atid * 4; c4 < K; c4 += NT * 4) {
-      const float4 wv = *reinterpret_cast<const float4*>(sw + c4);
-      float4 zv[4];
+    for (int r0 = 0; r0 < kTcD; r0 += 8) {
+      double s1[8], s2[8];
+      float cm[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) zv[q] = *reinterpret_cast<const float4*>(a.z + ((size_t)i * kTcD + r0 + q) * K + c4);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double c = a.q_m[i * kTcD + r0 + q];
-        const double e0 = (double)zv[q].x - c, e1 = (double)zv[q].y - c, e2 = (double)zv[q].z - c,
-                     e3 = (double)zv[q].w - c;
-        const double w0 = wv.x, w1 = wv.y, w2 = wv.z, w3 = wv.w;
-        s1[q] += (w0 * e0 + w1 * e1) + (w2 * e2 + w3 * e3);
-        s2[q] += (w0 * e0 * e0 + w1 * e1 * e1) + (w2 * e2 * e2 + w3 * e3 * e3);
+      for (int q = 0; q < 8; ++q) {
+        s1[q] = s2[q] = 0.0;
+        cm[q] = a.q_m[i * kTcD + r0 + q];
       }
-    }
+      for (int c4 = lane * 4; c4 < K; c4 += 128) {
+        const float4 wv = *reinterpret_cast<const float4*>(w + c4);
+        float4 zv[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double a1 = warp_sum(s1[q]), a2 = warp_sum(s2[q]);
-      if (lane == 0) {
-        s_rd[warp * 40 + r0 + q] = a1;
-        s_rd[warp * 40 + 16 + r0 + q] = a2;
+        for (int q = 0; q < 8; ++q) zv[q] = *reinterpret_cast<const float4*>(a.z + ((size_t)i * kTcD + r0 + q) * K + c4);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double e0 = (double)zv[q].x - (double)cm[q], e1 = (double)zv[q].y - (double)cm[q];
+          const double e2 = (double)zv[q].z - (double)cm[q], e3 = (double)zv[q].w - (double)cm[q];
+          const double p0 = (double)wv.x * e0, p1 = (double)wv.y * e1, p2 = (double)wv.z * e2, p3 = (double)wv.w * e3;
+          s1[q] += (p0 + p1) + (p2 + p3);
+          s2[q] += (p0 * e0 + p1 * e1) + (p2 * e2 + p3 * e3);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double S1 = warp_sum(s1[q]), S2 = warp_sum(s2[q]);
+        if (lane == q) {
+          const double mu = S1 / s0;
+          a.m1[i * kTcD + r0 + q] = (double)cm[q] + mu;
+          a.v[i * kTcD + r0 + q] = S2 / s0 - mu * mu;
+        }
       }
     }
   }
-  if (lane == 0) s_rd[warp * 40 + 34] = s0;
-  aux_bar();
-  if (atid < kTcD) {
-    double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+}
+
+// Backward row extra slab of group i (K x 32 B) into `bx`, built by the aux warps two groups
+// ahead: [Eg pattern | 0 0 0 | rho], rho_k = log2 w_root(k) - log2e (h_k - h_*) (h = the
+// forward's re-centred message; -1e30 where w_root = 0).
+__device__ void bwd_bx(const TLArgs& a, int64_t i, unsigned char* bx, int atid) {
+  constexpr int NT = 32 * kBwdAuxWarps;
+  const int K = a.K;
+  const float hs = a.ws.hmsg[(size_t)i * K + a.ws.ref->k_star];
+#pragma unroll 2
+  for (int k4 = atid * 4; k4 < K; k4 += NT * 4) {
+    const float4 wr = *reinterpret_cast<const float4*>(a.w_root + k4);
+    const float4 hm = *reinterpret_cast<const float4*>(a.ws.hmsg + (size_t)i * K + k4);
+    const float4 bg = *reinterpret_cast<const float4*>(a.ws.bgam + k4);
+    const float w4[4] = {wr.x, wr.y, wr.z, wr.w}, h4[4] = {hm.x, hm.y, hm.z, hm.w}, g4[4] = {bg.x, bg.y, bg.z, bg.w};
 #pragma unroll
-    for (int w = 0; w < kBwdAuxWarps; ++w) {
-      S0 += s_rd[w * 40 + 34];
-      S1 += s_rd[w * 40 + atid];
-      S2 += s_rd[w * 40 + 16 + atid];
+    for (int c = 0; c < 4; ++c) {
+      const float rho = w4[c] > 0.f ? log2f(w4[c]) - (h4[c] - hs) * kLog2e : -1e30f;
+      uint4 c0, c1;
+      extra_row(g4[c], 0.f, rho, c0, c1);
+      *reinterpret_cast<uint4*>(bx + tc_rowx_offset(k4 + c, 0)) = c0;
+      *reinterpret_cast<uint4*>(bx + tc_rowx_offset(k4 + c, 8)) = c1;
     }
-    const double mu = S1 / S0;
-    a.m1[i * kTcD + atid] = (double)a.q_m[i * kTcD + atid] + mu;
-    a.v[i * kTcD + atid] = S2 / S0 - mu * mu;
   }
-  aux_bar();
+  fence_proxy_async();  // generic-proxy SMEM writes -> visible to the tensor core (async proxy)
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
@@ -844,7 +876,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
   unsigned char* s_a = smem + L::a();
   unsigned char* s_b = smem + L::b();
   float* s_wp = reinterpret_cast<float*>(smem + L::wp());
-  double* s_rd = reinterpret_cast<double*>(smem + L::rd());
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars());
   uint64_t* a_full = bars;            // [2]
   uint64_t* a_empty = bars + 2;       // [2]
@@ -853,12 +884,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
   uint64_t* t_full = b_empty + SB;    // [2]
   uint64_t* t_empty = t_full + 2;     // [2]  16 epilogue warps
   uint64_t* bx_full = t_empty + 2;    // [2]  aux warps: row extra slab of a group ready (MMA waits)
-  uint64_t* l_full = bx_full + 2;     // [2]  aux warps: column constants of a group ready (epilogue waits)
-  uint64_t* w_full = l_full + 2;      // [2]  16 epilogue warps: group's weights complete
-  uint64_t* w_empty = w_full + 2;     // [2]  aux warps: moments read the weights
-  float* s_w = reinterpret_cast<float*>(smem + L::w(K));
-  float* s_L = reinterpret_cast<float*>(smem + L::lst(K));
-  double* s_t = reinterpret_cast<double*>(smem + L::tt(K));
+  uint64_t* g_done = bx_full + 2;     // [2]  16 epilogue warps: group finished (its slab stage is free)
   unsigned char* s_bx = smem + L::bx(K);
   __shared__ uint32_t s_tmem;
 
@@ -873,9 +899,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
       mbar_init(&t_full[b], 1);
       mbar_init(&t_empty[b], kTcEpiWarps);
       mbar_init(&bx_full[b], kBwdAuxWarps);
-      mbar_init(&l_full[b], kBwdAuxWarps);
-      mbar_init(&w_full[b], kTcEpiWarps);
-      mbar_init(&w_empty[b], kBwdAuxWarps);
+      mbar_init(&g_done[b], kTcEpiWarps);
     }
     for (int b = 0; b < SB; ++b) {
       mbar_init(&b_full[b], 1);
@@ -897,15 +921,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
     if (lane == 0) {
       const unsigned char* colop = reinterpret_cast<const unsigned char*>(a.ws.colop);
       const unsigned char* rowc = reinterpret_cast<const unsigned char*>(a.ws.rowop_b);
-      // z of a group is read by its prologue (two groups ahead) and its moments: keep three groups ahead in L2
-      for (int64_t jj = 0; jj < 3 && jj < ngroups; ++jj)
-        prefetch_l2_bulk(a.z + (size_t)(blockIdx.x + jj * gridDim.x) * kTcD * K, (uint32_t)(kTcD * K * 4));
       for (TileWalk tw(RB, CB); tw.T < ntiles; tw.next()) {
-        const int64_t T = tw.T, j = tw.j;
-        const int t = tw.t, cb = tw.cb, rb = tw.rb;
+        const int64_t T = tw.T;
+        const int cb = tw.cb, rb = tw.rb;
         const int64_t i = tw.i;
-        if (t == 0 && j + 3 < ngroups)
-          prefetch_l2_bulk(a.z + (size_t)(i + 3 * gridDim.x) * kTcD * K, (uint32_t)(kTcD * K * 4));
         if (rb == 0) {
           const int64_t J = tw.J;
           const int st = (int)(J & 1);
@@ -926,9 +945,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_bf16(128, 256);
       for (TileWalk tw(RB, CB); tw.T < ntiles; tw.next()) {
-        const int64_t T = tw.T, j = tw.j;
-        const int t = tw.t, cb = tw.cb, rb = tw.rb;
-        const int64_t J = tw.J;
+        const int64_t T = tw.T, j = tw.j, J = tw.J;
+        const int t = tw.t, rb = tw.rb;
         const int sb = (int)(T % SB), tb = (int)(T & 1);
         if (t == 0) mbar_wait(&bx_full[j & 1], (uint32_t)((j >> 1) & 1));
         if (rb == 0) mbar_wait(&a_full[J & 1], (uint32_t)((J >> 1) & 1));
@@ -944,32 +962,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
       }
     }
   } else if (warp >= kTcEpiWarps + 2) {
-    // --------------------------------------------- aux: prologues one/two groups ahead, moments behind
+    // ------------------------------- aux: row extra slabs two groups ahead of the MMAs
     const int atid = tid - kTcThreads;
     for (int64_t jj = 0; jj < 2 && jj < ngroups; ++jj) {
-      bwd_prologue(a, blockIdx.x + jj * gridDim.x, s_bx + (size_t)jj * K * kTcRowXBytes, s_L + jj * K, s_t, s_rd,
-                   atid);
+      bwd_bx(a, blockIdx.x + jj * gridDim.x, s_bx + (size_t)jj * K * kTcRowXBytes, atid);
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&bx_full[jj]);
-        mbar_arrive(&l_full[jj]);
-      }
+      if (lane == 0) mbar_arrive(&bx_full[jj]);
     }
-    for (int64_t j = 0; j < ngroups; ++j) {
+    for (int64_t j = 0; j + 2 < ngroups; ++j) {
       const int st = (int)(j & 1);
-      mbar_wait(&w_full[st], (uint32_t)((j >> 1) & 1));  // group j finished: its stages are free
-      if (j + 2 < ngroups) {
-        bwd_prologue(a, blockIdx.x + (j + 2) * gridDim.x, s_bx + (size_t)st * K * kTcRowXBytes, s_L + st * K, s_t,
-                     s_rd, atid);
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&bx_full[st]);
-          mbar_arrive(&l_full[st]);
-        }
-      }
-      bwd_moments(a, blockIdx.x + j * gridDim.x, s_w + st * K, s_rd, atid);
+      mbar_wait(&g_done[st], (uint32_t)((j >> 1) & 1));  // group j's MMAs all complete: its stage is free
+      bwd_bx(a, blockIdx.x + (j + 2) * gridDim.x, s_bx + (size_t)st * K * kTcRowXBytes, atid);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&w_empty[st]);
+      if (lane == 0) mbar_arrive(&bx_full[st]);
     }
   } else {
     // ---------------------------------------------------------------- epilogue
@@ -979,14 +984,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
       const int64_t T = tw.T, j = tw.j;
       const int t = tw.t, cb = tw.cb, rb = tw.rb;
       const int64_t i = tw.i;
-      const int st = (int)(j & 1);
-      if (t == 0) {
-        mbar_wait(&l_full[st], (uint32_t)((j >> 1) & 1));                 // column constants of group j
-        if (j >= 2) mbar_wait(&w_empty[st], (uint32_t)(((j >> 1) - 1) & 1));  // s_w stage read by moments(j-2)
-      }
       const int col = cb * 128 + q * 32 + lane;
       if (rb == 0) {
-        L2c = s_L[st * K + col];  // log2e log P(k'|k*)
+        L2c = a.ws.colaux[(size_t)i * 2 * K + K + col];  // log2e log P(k'|k*) (k_bwd_cols_tc)
         acc = 0.f;
       }
       mbar_wait(&t_full[T & 1], (uint32_t)((T >> 1) & 1));
@@ -1003,7 +1003,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
       });
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[T & 1]);
+      if (lane == 0) {
+        mbar_arrive(&t_empty[T & 1]);
+        if (t == TPG - 1) mbar_arrive(&g_done[j & 1]);
+      }
       {
         const float2 s2 = add2(wp[0], wp[1]);
         acc += s2.x + s2.y;
@@ -1016,13 +1019,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
           const float wv = wpb[q * 32 + lane] + wpb[128 + q * 32 + lane] + wpb[256 + q * 32 + lane] +
                            wpb[384 + q * 32 + lane];
           a.w[(size_t)i * K + col] = wv;
-          s_w[st * K + col] = wv;
           if (isnan(wv)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
         }
-      }
-      if (t == TPG - 1) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&w_full[st]);
       }
     }
   }

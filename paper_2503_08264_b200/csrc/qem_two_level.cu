@@ -577,6 +577,7 @@ static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, in
   if (tc) {
     of = occupancy(k_forward_tc, kTcThreads, FwdTcL::bytes(K));
     ob = occupancy(k_backward_tc, kBwdThreads, BwdTcL::bytes(K));
+    occupancy(k_bwd_cols_tc, 256, BwdColsTc::bytes(K));  // sets its dynamic-SMEM attribute
   } else {
     of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
     ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
@@ -623,12 +624,21 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int cp = pick_rp(K);
+  const bool tc = D == kTcD && c->tc;
+  if (tc) {
+    k_bwd_cols_tc<<<c->grid_prep, 256, BwdColsTc::bytes(K), st>>>(a);
+    c->launches += 1;
+  }
   if (c->ev[2]) cudaEventRecord((cudaEvent_t)c->ev[2], st);
-  if (D == kTcD && c->tc)
+  if (tc)
     k_backward_tc<<<c->grid_bwd, kBwdThreads, BwdTcL::bytes(K), st>>>(a);
   else
     bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
   if (c->ev[3]) cudaEventRecord((cudaEvent_t)c->ev[3], st);
+  if (tc) {
+    k_moments_tc<<<c->grid_prep, 256, 0, st>>>(a);
+    c->launches += 1;
+  }
   c->launches += 2;
   return cudaGetLastError();
 }
