@@ -185,6 +185,7 @@ qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t 
   c->grid_fwd = c->grid_bwd = 1;
   c->tc = desc->family == QEM_FAMILY_TWO_LEVEL && qem::tl_use_tc(desc);
   if (desc->family == QEM_FAMILY_TWO_LEVEL) qem::tl_grids(desc, c->n_local, sm_count(), &c->grid_fwd, &c->grid_bwd, &c->grid_prep);
+  c->grid_stage = (int)(c->n_local < sm_count() ? c->n_local : sm_count());
   c->ws_bytes = carve(c, nullptr);
   cudaError_t e = cudaMalloc(&c->ws, c->ws_bytes);
   if (e != cudaSuccess) {

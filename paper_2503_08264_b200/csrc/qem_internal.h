@@ -77,6 +77,7 @@ struct qem_ctx {
   int grid_fwd;
   int grid_bwd;
   int grid_prep;
+  int grid_stage;  // one CTA per SM, capped by the groups (TMA-staged per-group kernels)
   void* ws;
   size_t ws_bytes;
   qem::TwoLevelWs tw;

@@ -189,6 +189,17 @@ __global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
 // One warp per group.  For column k': A_i(k') (fp64), t_i(k') = B(k_ref,k') + A_i(k'),
 // c_i = lse t - log K, P = softmax t; the group's tile mode from the bound on
 // |D'|; the column operand and {P, ln P}.
+// softplus(eta) = max(eta, 0) + log1p(e^-|eta|) on the SFU: v = 2^(-|eta| log2e), u = 1 + v (rounded),
+// log1p(v) = ln2 lg2(u) + (v - (u - 1)) / u  (the second term restores the rounding of 1 + v).
+// Absolute error <= ~1.5e-7 per observation (lg2.approx; R26).
+__device__ __forceinline__ float softplus_mufu(float eta) {
+  const float v = ex2(-fabsf(eta) * kLog2e);
+  const float u = 1.f + v;
+  float l2;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u));
+  return fmaxf(eta, 0.f) + fmaf(l2, 0.69314718055994531f, __fdividef(v - (u - 1.f), u));
+}
+
 struct PrepTc {
   static constexpr int WARPS = 8;
   __host__ __device__ static size_t warp_bytes(int K, int J) {
@@ -274,8 +285,7 @@ __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
           e1 = fma2(make_float2(xv.z, xv.w), f2(zr[2 * q + 1]), e1);
         }
         const float2 eta = add2(e0, e1);
-        const float sa = fmaxf(eta.x, 0.f) + log1pf(__expf(-fabsf(eta.x)));
-        const float sb = fmaxf(eta.y, 0.f) + log1pf(__expf(-fabsf(eta.y)));
+        const float sa = softplus_mufu(eta.x), sb = softplus_mufu(eta.y);
         lsp += (double)sa;
         if (2 * jp + 1 < J) lsp += (double)sb;
       }
@@ -347,15 +357,23 @@ __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
     tb = warp_maxf(tb);
     const int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
     float* aux = a.ws.colaux + (size_t)i * 2 * K;  // SoA {P, ln P}
-    for (int kc = lane; kc < K; kc += 32) {
-      const float lp = (float)(tref[kc] - M - logS);
-      aux[kc] = expf(lp);
-      aux[K + kc] = lp;
-      uint4 c0, c1;
-      // ln P joins the MMA only in the online mode; the polynomial modes need D' alone
-      extra_col(0.f, md == 5 ? lp * kLog2e : 0.f, c0, c1);
-      *reinterpret_cast<uint32_t*>(cop + tc_col_offset(kc, 54)) = c0.w;  // lP0 lP1
-      *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 56)) = c1;
+    for (int kb = lane; kb < K; kb += 128) {  // 4 columns per lane per batch: their loads in flight together
+      double tb4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) tb4[u] = kb + 32 * u < K ? ldg_d(tref + kb + 32 * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kc = kb + 32 * u;
+        if (kc >= K) break;
+        const float lp = (float)(tb4[u] - M - logS);
+        aux[kc] = expf(lp);
+        aux[K + kc] = lp;
+        uint4 c0, c1;
+        // ln P joins the MMA only in the online mode; the polynomial modes need D' alone
+        extra_col(0.f, md == 5 ? lp * kLog2e : 0.f, c0, c1);
+        *reinterpret_cast<uint32_t*>(cop + tc_col_offset(kc, 54)) = c0.w;  // lP0 lP1
+        *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 56)) = c1;
+      }
     }
     if (lane == 0) {
       a.ws.cvec[i] = M + logS - logK;
@@ -488,15 +506,17 @@ struct FwdTcL {
   static constexpr size_t b() { return a() + SA * A_STAGE; }
   static constexpr size_t p() { return b() + 2 * B_STAGE; }
   static constexpr size_t fin() { return p() + 2 * P_STAGE; }         // [2][4][128] float2
-  static constexpr size_t bars() { return fin() + 2 * 4 * 128 * 8; }  // 16 mbarriers
-  static constexpr size_t kap() { return bars() + 16 * 8; }
-  static size_t __host__ __device__ st0(int K) { return kap() + (size_t)K * 4; }
+  static constexpr size_t bars() { return fin() + 2 * 4 * 128 * 8; }  // 20 mbarriers
+  static size_t __host__ __device__ st0(int) { return bars() + 20 * 8; }
   static size_t __host__ __device__ st1(int K) { return st0(K) + (size_t)4 * K * 4; }
   static size_t __host__ __device__ g(int K) { return st1(K) + (size_t)4 * K * 4; }
   static size_t __host__ __device__ bytes(int K) { return g(K) + (size_t)K * 8; }
 };
 
-__global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
+constexpr int kFwdAuxWarps = 2;  // row finalisers of the forward
+constexpr int kFwdThreads = kTcThreads + 32 * kFwdAuxWarps;
+
+__global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   using L = FwdTcL;
   constexpr int SA = L::SA;
@@ -513,6 +533,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
   uint64_t* b_empty = b_full + 2;    // [2]  MMA commit + 16 epilogue warps
   uint64_t* t_full = b_empty + 2;    // [2]
   uint64_t* t_empty = t_full + 2;    // [2]  16 epilogue warps
+  uint64_t* f_full = t_empty + 2;    // [2]  16 epilogue warps: a row block's slice states are in s_fin
+  uint64_t* f_empty = f_full + 2;    // [2]  aux warps: s_fin stage merged
   float* s_st0 = reinterpret_cast<float*>(smem + L::st0(K));
   float* s_st1 = reinterpret_cast<float*>(smem + L::st1(K));
   double* s_g = reinterpret_cast<double*>(smem + L::g(K));
@@ -532,6 +554,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
       mbar_init(&b_empty[b], 1 + kTcEpiWarps);
       mbar_init(&t_full[b], 1);
       mbar_init(&t_empty[b], kTcEpiWarps);
+      mbar_init(&f_full[b], kTcEpiWarps);
+      mbar_init(&f_empty[b], kFwdAuxWarps);
     }
     fence_mbar_init();
   }
@@ -594,20 +618,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
         if (rb == RB - 1) umma_commit(&b_empty[J & 1]);
       }
     }
-  } else {
-    // ---------------------------------------------------------------- epilogue
-    const int q = warp & 3, cq = warp >> 2, etid = tid;
+  } else if (warp >= kTcEpiWarps + 2) {
+    // ------------------------------------------- aux: merge the 4 column slices of each row, finalise
+    // h, dg = alpha' + h and the plate sum (one row block of 128 rows at a time, behind the epilogue)
+    const int atid = tid - kTcThreads;
+    constexpr int NTA = 32 * kFwdAuxWarps;
     int md = 5;
     float mi[kTcD];
     float M2 = 0.f;
-    for (TileWalk tw(RB, NB); tw.T < ntiles; tw.next()) {
-      const int64_t T = tw.T, j = tw.j;
-      const int t = tw.t, cb = tw.cb, rb = tw.rb;
-      const int64_t J = tw.J;
-      const int64_t i = tw.i;
-      if (t == 0) {
-        // ---- group setup: the group's mode; m_i for the fp64 re-centring constant alpha'_ik
-        // (nothing in SMEM is group-scoped, so no barrier: warps drift freely across groups)
+    int64_t j = 0, i = blockIdx.x;
+    int rb = 0;
+    for (int64_t u = 0; u < ngroups * RB; ++u) {
+      if (rb == 0) {
         md = a.ws.gmode[i];
         M2 = 0.f;
 #pragma unroll
@@ -615,11 +637,62 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
           mi[r] = a.q_m[i * kTcD + r];
           M2 = fmaf(mi[r], mi[r], M2);
         }
-        if (etid == 0) {
+        if (atid == 0) {
           atomicAdd(&a.cnt->mode_hist[md], 1ull);
           csum += a.ws.cvec[i];
         }
       }
+      const int st = (int)(u & 1);
+      mbar_wait(&f_full[st], (uint32_t)((u >> 1) & 1));
+      const float2* fin = s_fin + st * 512;
+      for (int rr = atid; rr < 128; rr += NTA) {
+        const int k = rb * 128 + rr;
+        float h;
+        if (md == 5) {
+          float mx = -CUDART_INF_F;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) mx = fmaxf(mx, fin[c * 128 + rr].x);
+          float sm = 0.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float2 f = fin[c * 128 + rr];
+            sm += f.y * ex2(f.x - mx);
+          }
+          h = (mx + log2f(sm)) * 0.69314718055994531f;
+        } else {
+          float sm = 0.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) sm += fin[c * 128 + rr].x;
+          h = log1pf(sm);
+        }
+        // alpha'_ik = D_k(m_i) = alpha0_k + gamma_k |m_i|^2 + c0_k . m_i in fp64
+        const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
+        double ap = a.ws.alpha_d[k] + (double)fc[1] * (double)M2;
+#pragma unroll
+        for (int r = 0; r < kTcD; ++r) ap += (double)fc[2 + r] * (double)mi[r];
+        const double dgd = ap + (double)h;
+        a.ws.hmsg[(size_t)i * K + k] = h;  // re-centred message, the backward's row constant
+        a.ws.dg[(size_t)i * K + k] = (float)dgd;
+        s_g[k] += dgd;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&f_empty[st]);
+      if (++rb == RB) {
+        rb = 0;
+        ++j;
+        i += gridDim.x;
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3, cq = warp >> 2;
+    int md = 5;
+    int64_t u = 0;  // finalised row blocks so far
+    for (TileWalk tw(RB, NB); tw.T < ntiles; tw.next()) {
+      const int64_t T = tw.T, J = tw.J;
+      const int t = tw.t, cb = tw.cb, rb = tw.rb;
+      const int64_t i = tw.i;
+      if (t == 0) md = a.ws.gmode[i];
       const int k = rb * 128 + q * 32 + lane;
       float st0, st1 = 0.f;
       if (cb == 0)
@@ -654,39 +727,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
         s_st0[cq * K + k] = st0;
         s_st1[cq * K + k] = st1;
       } else {
-        // ---- row k complete: merge the 4 column slices, finalise h, dg, plate sum
-        float2* fin = s_fin + (rb & 1) * 512;
-        fin[cq * 128 + q * 32 + lane] = make_float2(st0, st1);
-        quarter_bar(q);
-        if (cq == 0) {
-          float h;
-          if (md == 5) {
-            float mx = -CUDART_INF_F;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) mx = fmaxf(mx, fin[c * 128 + q * 32 + lane].x);
-            float sm = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const float2 f = fin[c * 128 + q * 32 + lane];
-              sm += f.y * ex2(f.x - mx);
-            }
-            h = (mx + log2f(sm)) * 0.69314718055994531f;
-          } else {
-            float sm = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) sm += fin[c * 128 + q * 32 + lane].x;
-            h = log1pf(sm);
-          }
-          // alpha'_ik = D_k(m_i) = alpha0_k + gamma_k |m_i|^2 + c0_k . m_i in fp64
-          const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
-          double ap = a.ws.alpha_d[k] + (double)fc[1] * (double)M2;
-#pragma unroll
-          for (int r = 0; r < kTcD; ++r) ap += (double)fc[2 + r] * (double)mi[r];
-          const double dgd = ap + (double)h;
-          a.ws.hmsg[(size_t)i * K + k] = h;  // re-centred message, the backward's row constant
-          a.ws.dg[(size_t)i * K + k] = (float)dgd;
-          s_g[k] += dgd;
-        }
+        // ---- row k complete in this slice: hand (max, sum) to the aux warps
+        const int fs = (int)(u & 1);
+        if (u >= 2) mbar_wait(&f_empty[fs], (uint32_t)(((u >> 1) - 1) & 1));
+        s_fin[fs * 512 + cq * 128 + q * 32 + lane] = make_float2(st0, st1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&f_full[fs]);
+        ++u;
       }
     }
   }
@@ -697,7 +744,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_forward_tc(TLArgs a) {
   if (warp == kTcEpiWarps + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   double* part = a.ws.partial + (size_t)blockIdx.x * (K + 1);
   for (int k = tid; k < K; k += blockDim.x) part[k] = s_g[k];
-  if (tid == 0) part[K] = csum;
+  if (tid == kTcThreads) part[K] = csum;  // the first aux thread accumulated sum_i c_i
   __threadfence();
   __syncthreads();
   __shared__ uint32_t s_last;
@@ -733,18 +780,63 @@ constexpr int kBwdThreads = kTcThreads + 32 * kBwdAuxWarps;
 // ------------------------------------------------- backward column constants (K4a)
 // Backward reference:
 //   log P(k'|k) = log P(k'|k*) + E_k(k') - (l_k - l_*),  E_k = B(k,.) - B(k*,.).
-// One warp per group: the column constants L*(k') = log2e log P(k'|k*), a softmax over
-// the group's columns of the fp64 logits t_ref(k') + B(k*,k') - B(k_ref,k'), into
-// colaux's second slot (the forward's ln P is not needed any more).
-struct BwdColsTc {
-  static constexpr int WARPS = 8;
-  __host__ __device__ static size_t bytes(int K) { return (size_t)WARPS * K * 8; }
+// Per group: the column constants L*(k') = log2e log P(k'|k*), a softmax over the group's
+// columns of the fp64 logits t_ref(k') + B(k*,k') - B(k_ref,k'), into colaux's second slot
+// (the forward's ln P is not needed any more).  One CTA per SM, persistent over groups;
+// each group's z (16 x K fp32, contiguous) and t_ref (K fp64) arrive in SMEM by one
+// cp.async.bulk each into a 2-stage ring, so HBM streams while the previous group computes.
+struct GroupStage {  // shared by k_bwd_cols_tc and k_moments_tc
+  static constexpr int THREADS = 256;
+  __host__ __device__ static size_t z_bytes(int K) { return (size_t)kTcD * K * 4; }
+  __host__ __device__ static size_t stage(int K) { return z_bytes(K) + (size_t)K * 8; }  // + t_ref or w
+  __host__ __device__ static size_t bytes(int K) { return 2 * stage(K) + 64 * 8 + 4 * 8; }
 };
 
-__global__ void __launch_bounds__(256) k_bwd_cols_tc(TLArgs a) {
+__device__ __forceinline__ double block_max256(double v, double* scr) {
+  v = warp_max(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scr[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double m = scr[0];
+#pragma unroll
+  for (int w = 1; w < GroupStage::THREADS / 32; ++w) m = fmax(m, scr[w]);
+  return m;
+}
+__device__ __forceinline__ double block_sum256(double v, double* scr) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scr[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double m = 0.0;
+#pragma unroll
+  for (int w = 0; w < GroupStage::THREADS / 32; ++w) m += scr[w];
+  return m;
+}
+
+__global__ void __launch_bounds__(GroupStage::THREADS, 1) k_bwd_cols_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int K = a.K, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* tv = reinterpret_cast<double*>(smem) + (size_t)wid * K;
+  const int K = a.K, tid = threadIdx.x;
+  const size_t SZ = GroupStage::stage(K);
+  double* scr = reinterpret_cast<double*>(smem + 2 * SZ);
+  uint64_t* full = reinterpret_cast<uint64_t*>(scr + 64);
+  const int64_t n = a.n_local;
+  const int64_t ngroups = n > blockIdx.x ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint32_t zb = (uint32_t)GroupStage::z_bytes(K), tb = (uint32_t)K * 8;
+  auto issue = [&](int64_t j) {
+    const int64_t i = blockIdx.x + j * gridDim.x;
+    unsigned char* st = smem + (size_t)(j & 1) * SZ;
+    mbar_expect_tx(&full[j & 1], zb + tb);
+    tma_bulk_g2s(st, a.z + (size_t)i * kTcD * K, zb, &full[j & 1]);
+    tma_bulk_g2s(st + zb, a.ws.tA + (size_t)i * K, tb, &full[j & 1]);
+  };
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int64_t j = 0; j < 2 && j < ngroups; ++j) issue(j);
   float mus[kTcD], mur[kTcD];
 #pragma unroll
   for (int r = 0; r < kTcD; ++r) {
@@ -753,19 +845,21 @@ __global__ void __launch_bounds__(256) k_bwd_cols_tc(TLArgs a) {
   }
   const double es = a.ws.ref->e_star, bs = a.ws.ref->bstar_const;
   const double er = a.ws.ref->e_ref, br = a.ws.ref->bref_const;
-  for (int64_t i = (int64_t)blockIdx.x * BwdColsTc::WARPS + wid; i < a.n_local;
-       i += (int64_t)gridDim.x * BwdColsTc::WARPS) {
+  const int c4 = tid * 4;
+  const bool act = c4 < K;
+  for (int64_t j = 0; j < ngroups; ++j) {
+    const int64_t i = blockIdx.x + j * gridDim.x;
+    const unsigned char* st = smem + (size_t)(j & 1) * SZ;
+    mbar_wait(&full[j & 1], (uint32_t)((j >> 1) & 1));
+    double t[4] = {-CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF};
     double mx = -CUDART_INF;
-    for (int c4 = lane * 4; c4 < K; c4 += 128) {
-      float4 zv[kTcD];
-#pragma unroll
-      for (int r = 0; r < kTcD; ++r) zv[r] = *reinterpret_cast<const float4*>(a.z + ((size_t)i * kTcD + r) * K + c4);
-      const double2 ta = *reinterpret_cast<const double2*>(a.ws.tA + (size_t)i * K + c4);
-      const double2 tb = *reinterpret_cast<const double2*>(a.ws.tA + (size_t)i * K + c4 + 2);
+    if (act) {
+      const float* zs = reinterpret_cast<const float*>(st);
       double d[4] = {0.0, 0.0, 0.0, 0.0}, g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int r = 0; r < kTcD; ++r) {
-        const double zz[4] = {(double)zv[r].x, (double)zv[r].y, (double)zv[r].z, (double)zv[r].w};
+        const float4 zv = *reinterpret_cast<const float4*>(zs + (size_t)r * K + c4);
+        const double zz[4] = {(double)zv.x, (double)zv.y, (double)zv.z, (double)zv.w};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const double ds = zz[c] - (double)mus[r], dr = zz[c] - (double)mur[r];
@@ -773,72 +867,97 @@ __global__ void __launch_bounds__(256) k_bwd_cols_tc(TLArgs a) {
           g[c] = fma(dr, dr, g[c]);
         }
       }
-      const double t4[4] = {ta.x, ta.y, tb.x, tb.y};
+      const double* tr = reinterpret_cast<const double*>(st + zb);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const double t = (bs - 0.5 * es * d[c]) - (br - 0.5 * er * g[c]) + t4[c];
-        tv[c4 + c] = t;
-        mx = fmax(mx, t);
+        t[c] = (bs - 0.5 * es * d[c]) - (br - 0.5 * er * g[c]) + tr[c4 + c];
+        mx = fmax(mx, t[c]);
       }
     }
-    mx = warp_max(mx);
-    __syncwarp();
+    mx = block_max256(mx, scr);
     double se = 0.0;
-#pragma unroll 4
-    for (int kc = lane; kc < K; kc += 32) se += (double)expf((float)(tv[kc] - mx));
-    const double lse = mx + log(warp_sum(se));
-    float* L = a.ws.colaux + (size_t)i * 2 * K + K;
-    for (int kc = lane; kc < K; kc += 32) L[kc] = (float)((tv[kc] - lse) * kLog2eD);
-    __syncwarp();
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) se += (double)expf((float)(t[c] - mx));
+    }
+    const double lse = mx + log(block_sum256(se, scr + 8));
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0 && j + 2 < ngroups) issue(j + 2);
+    if (act)
+      *reinterpret_cast<float4*>(a.ws.colaux + (size_t)i * 2 * K + K + c4) =
+          make_float4((float)((t[0] - lse) * kLog2eD), (float)((t[1] - lse) * kLog2eD),
+                      (float)((t[2] - lse) * kLog2eD), (float)((t[3] - lse) * kLog2eD));
   }
 }
 
 // ------------------------------------------------------------ moments (K4c)
-// One warp per group, after the backward: E z = c + S1/S0, Var z = S2/S0 - (S1/S0)^2,
-// S_p = sum_k' w (z - c)^p in fp64 (self-normalised, shifted by the Q mean c = m_i; R24).
-__global__ void __launch_bounds__(256) k_moments_tc(TLArgs a) {
-  const int K = a.K, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int64_t i = (int64_t)blockIdx.x * nw + wid; i < a.n_local; i += (int64_t)gridDim.x * nw) {
-    const float* w = a.w + (size_t)i * K;
-    double s0 = 0.0;
+// After the backward: E z = c + S1/S0, Var z = S2/S0 - (S1/S0)^2, S_p = sum_k' w (z - c)^p in
+// fp64 (self-normalised, shifted by the Q mean c = m_i; R24).  One CTA per SM over groups,
+// z and w of a group staged by cp.async.bulk (2-stage ring); warp q handles dims 2q, 2q+1.
+__global__ void __launch_bounds__(GroupStage::THREADS, 1) k_moments_tc(TLArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int K = a.K, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t SZ = GroupStage::stage(K);
+  double* scr = reinterpret_cast<double*>(smem + 2 * SZ);
+  uint64_t* full = reinterpret_cast<uint64_t*>(scr + 64);
+  const int64_t n = a.n_local;
+  const int64_t ngroups = n > blockIdx.x ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint32_t zb = (uint32_t)GroupStage::z_bytes(K), wb = (uint32_t)K * 4;
+  auto issue = [&](int64_t j) {
+    const int64_t i = blockIdx.x + j * gridDim.x;
+    unsigned char* st = smem + (size_t)(j & 1) * SZ;
+    mbar_expect_tx(&full[j & 1], zb + wb);
+    tma_bulk_g2s(st, a.z + (size_t)i * kTcD * K, zb, &full[j & 1]);
+    tma_bulk_g2s(st + zb, a.w + (size_t)i * K, wb, &full[j & 1]);
+  };
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int64_t j = 0; j < 2 && j < ngroups; ++j) issue(j);
+  for (int64_t j = 0; j < ngroups; ++j) {
+    const int64_t i = blockIdx.x + j * gridDim.x;
+    const unsigned char* st = smem + (size_t)(j & 1) * SZ;
+    mbar_wait(&full[j & 1], (uint32_t)((j >> 1) & 1));
+    const float* zs = reinterpret_cast<const float*>(st);
+    const float* ws = reinterpret_cast<const float*>(st + zb);
+    const int r0 = 2 * warp;  // 8 warps x 2 dims = 16
+    const double c0 = a.q_m[i * kTcD + r0], c1 = a.q_m[i * kTcD + r0 + 1];
+    double s0 = 0.0, a1 = 0.0, a2 = 0.0, b1 = 0.0, b2 = 0.0;
     for (int c4 = lane * 4; c4 < K; c4 += 128) {
-      const float4 wv = *reinterpret_cast<const float4*>(w + c4);
-      s0 += ((double)wv.x + (double)wv.y) + ((double)wv.z + (double)wv.w);
+      const float4 wv = *reinterpret_cast<const float4*>(ws + c4);
+      const float4 za = *reinterpret_cast<const float4*>(zs + (size_t)r0 * K + c4);
+      const float4 zb4 = *reinterpret_cast<const float4*>(zs + (size_t)(r0 + 1) * K + c4);
+      const double w4[4] = {wv.x, wv.y, wv.z, wv.w};
+      const double e4[4] = {za.x - c0, za.y - c0, za.z - c0, za.w - c0};
+      const double f4[4] = {zb4.x - c1, zb4.y - c1, zb4.z - c1, zb4.w - c1};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        s0 += w4[c];
+        const double pe = w4[c] * e4[c], pf = w4[c] * f4[c];
+        a1 += pe;
+        a2 = fma(pe, e4[c], a2);
+        b1 += pf;
+        b2 = fma(pf, f4[c], b2);
+      }
     }
     s0 = warp_sum(s0);
-#pragma unroll 1
-    for (int r0 = 0; r0 < kTcD; r0 += 8) {
-      double s1[8], s2[8];
-      float cm[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        s1[q] = s2[q] = 0.0;
-        cm[q] = a.q_m[i * kTcD + r0 + q];
-      }
-      for (int c4 = lane * 4; c4 < K; c4 += 128) {
-        const float4 wv = *reinterpret_cast<const float4*>(w + c4);
-        float4 zv[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) zv[q] = *reinterpret_cast<const float4*>(a.z + ((size_t)i * kTcD + r0 + q) * K + c4);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const double e0 = (double)zv[q].x - (double)cm[q], e1 = (double)zv[q].y - (double)cm[q];
-          const double e2 = (double)zv[q].z - (double)cm[q], e3 = (double)zv[q].w - (double)cm[q];
-          const double p0 = (double)wv.x * e0, p1 = (double)wv.y * e1, p2 = (double)wv.z * e2, p3 = (double)wv.w * e3;
-          s1[q] += (p0 + p1) + (p2 + p3);
-          s2[q] += (p0 * e0 + p1 * e1) + (p2 * e2 + p3 * e3);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double S1 = warp_sum(s1[q]), S2 = warp_sum(s2[q]);
-        if (lane == q) {
-          const double mu = S1 / s0;
-          a.m1[i * kTcD + r0 + q] = (double)cm[q] + mu;
-          a.v[i * kTcD + r0 + q] = S2 / s0 - mu * mu;
-        }
-      }
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    b1 = warp_sum(b1);
+    b2 = warp_sum(b2);
+    if (lane == 0) {
+      const double ma = a1 / s0, mb = b1 / s0;
+      a.m1[i * kTcD + r0] = c0 + ma;
+      a.v[i * kTcD + r0] = a2 / s0 - ma * ma;
+      a.m1[i * kTcD + r0 + 1] = c1 + mb;
+      a.v[i * kTcD + r0 + 1] = b2 / s0 - mb * mb;
     }
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0 && j + 2 < ngroups) issue(j + 2);
   }
 }
 

@@ -575,9 +575,10 @@ static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, in
   const int K = d->K, rp = pick_rp(K);
   int of, ob;
   if (tc) {
-    of = occupancy(k_forward_tc, kTcThreads, FwdTcL::bytes(K));
+    of = occupancy(k_forward_tc, kFwdThreads, FwdTcL::bytes(K));
     ob = occupancy(k_backward_tc, kBwdThreads, BwdTcL::bytes(K));
-    occupancy(k_bwd_cols_tc, 256, BwdColsTc::bytes(K));  // sets its dynamic-SMEM attribute
+    occupancy(k_bwd_cols_tc, GroupStage::THREADS, GroupStage::bytes(K));  // set the dynamic-SMEM attributes
+    occupancy(k_moments_tc, GroupStage::THREADS, GroupStage::bytes(K));
   } else {
     of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
     ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
@@ -608,7 +609,7 @@ static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st
   if (e != cudaSuccess) return e;
   if (c->ev[0]) cudaEventRecord((cudaEvent_t)c->ev[0], st);
   if (tc)
-    k_forward_tc<<<c->grid_fwd, kTcThreads, FwdTcL::bytes(K), st>>>(a);
+    k_forward_tc<<<c->grid_fwd, kFwdThreads, FwdTcL::bytes(K), st>>>(a);
   else
     fwd_fn<D>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
   if (c->ev[1]) cudaEventRecord((cudaEvent_t)c->ev[1], st);
@@ -626,7 +627,7 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   const int cp = pick_rp(K);
   const bool tc = D == kTcD && c->tc;
   if (tc) {
-    k_bwd_cols_tc<<<c->grid_prep, 256, BwdColsTc::bytes(K), st>>>(a);
+    k_bwd_cols_tc<<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K), st>>>(a);
     c->launches += 1;
   }
   if (c->ev[2]) cudaEventRecord((cudaEvent_t)c->ev[2], st);
@@ -636,7 +637,7 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
     bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
   if (c->ev[3]) cudaEventRecord((cudaEvent_t)c->ev[3], st);
   if (tc) {
-    k_moments_tc<<<c->grid_prep, 256, 0, st>>>(a);
+    k_moments_tc<<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K), st>>>(a);
     c->launches += 1;
   }
   c->launches += 2;
