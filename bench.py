@@ -39,18 +39,36 @@ SMS = 148
 SM_MAX_MHZ = 1965.0
 
 
-def pair_ceiling(d: int, tc: bool = False, mhz: float = SM_MAX_MHZ) -> dict:
-    """Pairs/s ceiling of ONE pass (forward or backward) from the binding pipe.
+# FMA-pipe lane-ops of one exponential evaluated in software (exp2_poly2: 3 FADD + 5 FFMA;
+# the 2 integer ops of the exponent insert run on the ALU pipe)
+FMA_PER_SOFT_EXP = 8.0
 
-    FFMA tiles (tc False): 1 exp (MUFU) + d+2 FP32 lane-ops per pair.
-    tcgen05 tiles (tc True, d = 16): the d-term contraction runs on the tensor
-    cores (bf16x3: 6 bf16 products = 12 d flops/pair, ceiling from the measured
-    bf16 peak), leaving 1 exp + 3 FP32 lane-ops per pair on the SM pipes."""
+
+def exp_capacity(fma_other: float, mhz: float = SM_MAX_MHZ) -> dict:
+    """Pairs/s ceiling of ONE pass when every pair needs one exponential plus `fma_other` FMA-pipe
+    lane-ops, and the exponentials may run on the SFU (16 MUFU.EX2/clk/SM) or in software on the
+    FMA pipe (128 lane-ops/clk/SM, FMA_PER_SOFT_EXP each): maximise P subject to
+    (1 - f) P <= 16 and P (fma_other + 8 f) <= 128 over the software fraction f."""
+    f = max(0.0, (FP32_PER_SM_CLK - SFU_PER_SM_CLK * fma_other) / (SFU_PER_SM_CLK * FMA_PER_SOFT_EXP + FP32_PER_SM_CLK))
+    p = min(SFU_PER_SM_CLK / (1.0 - f), FP32_PER_SM_CLK / (fma_other + FMA_PER_SOFT_EXP * f))
+    return {"pairs_per_clk_sm": p, "soft_exp_fraction": f, "pairs_per_s": p * mhz * 1e6 * SMS}
+
+
+def pair_ceiling(d: int, tc: bool = False, mhz: float = SM_MAX_MHZ) -> dict:
+    """Pairs/s ceiling of ONE pass (forward or backward) from the binding resources.
+
+    FFMA tiles (tc False): 1 exp + d+2 FP32 lane-ops per pair.
+    tcgen05 tiles (tc True, d = 16): the d-term contraction runs on the tensor cores (bf16x3:
+    6 bf16 products = 12 d flops/pair, ceiling from the measured bf16 peak), leaving 1 exp + 2
+    FMA-pipe lane-ops per pair (add the column constant, accumulate) for the SM.
+    Binding ceiling = the exp capacity of SFU + FMA pipe together (exp_capacity); the SFU-only
+    figure (16 pairs/clk/SM) is reported beside it."""
     f = mhz * 1e6 * SMS
-    sfu = f * SFU_PER_SM_CLK / 1.0
-    fp32 = f * FP32_PER_SM_CLK / (3.0 if tc else d + 2.0)
-    out = {"sfu_pairs_per_s": sfu, "fp32_pairs_per_s": fp32}
-    pipes = {"sfu": sfu, "fp32": fp32}
+    other = 2.0 if tc else d + 2.0
+    cap = exp_capacity(other, mhz)
+    out = {"sfu_only_pairs_per_s": f * SFU_PER_SM_CLK,
+           "exp_sfu_fma_pairs_per_s": cap["pairs_per_s"], "soft_exp_fraction_at_ceiling": cap["soft_exp_fraction"]}
+    pipes = {"sfu+fma": cap["pairs_per_s"]}
     if tc:
         out["tensor_pairs_per_s"] = pipes["tensor"] = BF16_TFLOPS * 1e12 / (12.0 * d)
     pipe = min(pipes, key=pipes.get)
@@ -278,20 +296,20 @@ def run_gpu(args):
     tc = g.pair_path() == 1
     ceil = pair_ceiling(m.d, tc)
     achieved = local_pairs / (dom_ms * 1e-3)
-    per_pair = ({"exp": 1, "fp32": 3, "tensor_bf16_flops": 12 * m.d} if tc else {"exp": 1, "fp32": m.d + 2})
+    per_pair = ({"exp": 1, "fma_pipe": 2, "tensor_bf16_flops": 12 * m.d} if tc else {"exp": 1, "fma_pipe": m.d + 2})
     roof = {"bound": "alu", "pipe": ceil["pipe"], "kernel": f"k_{dom}" + ("_tc" if tc else ""), "unit": "Gpair/s",
             "achieved": achieved / 1e9, "peak": ceil["pairs_per_s"] / 1e9,
             "frac": achieved / ceil["pairs_per_s"],
+            "frac_vs_sfu_only": achieved / ceil["sfu_only_pairs_per_s"],
             "traffic": _ncu_traffic(f"k_{dom}" + ("_tc" if tc else "")),
             "traffic_unit": "bytes/launch (ncu --set full, profiles/r01_traffic.json)",
             "algorithmic_bytes": _algo_bytes(dom, tc, ge - gb, m),
             "per_pair": per_pair,
-            "pipe_ceilings_gpair_s": {k.replace("_pairs_per_s", ""): v / 1e9 for k, v in ceil.items()
-                                      if k.endswith("_pairs_per_s") and k != "pairs_per_s"},
-            "peak_basis": (f"{SMS} SMs x {SM_MAX_MHZ:.0f} MHz x {SFU_PER_SM_CLK:.0f} MUFU.EX2/clk (1 exp per pair "
-                           f"per pass); tensor and FP32 ceilings beside it (DESIGN.md Roofline)" if tc else
-                           f"{SMS} SMs x {SM_MAX_MHZ:.0f} MHz x min({SFU_PER_SM_CLK:.0f} MUFU.EX2/clk, "
-                           f"{FP32_PER_SM_CLK:.0f} FP32/clk / (d+2)) per pass (DESIGN.md Roofline)"),
+            "ceilings_gpair_s": {k.replace("_pairs_per_s", ""): v / 1e9 for k, v in ceil.items()
+                                 if k.endswith("_pairs_per_s") and k != "pairs_per_s"},
+            "peak_basis": (f"{SMS} SMs x {SM_MAX_MHZ:.0f} MHz x exp capacity of SFU ({SFU_PER_SM_CLK:.0f} MUFU.EX2/clk) "
+                           f"+ FMA pipe ({FP32_PER_SM_CLK:.0f} lane-ops/clk, {FMA_PER_SOFT_EXP:.0f} per software exp2) "
+                           f"with {per_pair['fma_pipe']} other FMA-pipe lane-ops per pair (DESIGN.md Roofline)"),
             "kernels_ms": {"forward": fwd_ms, "backward": bwd_ms, "allreduce": comm_ms}}
     if rank != 0:
         if world > 1:

@@ -35,6 +35,16 @@ constexpr int kTcEpiWarps = 16;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;  // + TMA warp + MMA warp
 constexpr int kTcEpiThreads = kTcEpiWarps * 32;
 constexpr int kTcRowCBytes = kTcRowBytes;  // 96: c2 split (6 chunks)
+// Of every 16 exponentials an epilogue thread evaluates, kPolyExp{Fwd,Bwd} go to the FMA
+// pipe (exp2_poly2) and the rest to the SFU, so the two pipes share the binding exp load
+// (measured on config 5, profiles/r01_poly_exp_sweep.txt: forward best at 2, backward at 4).
+#ifndef QEM_POLY_EXP_FWD
+#define QEM_POLY_EXP_FWD 2
+#endif
+#ifndef QEM_POLY_EXP_BWD
+#define QEM_POLY_EXP_BWD 4
+#endif
+constexpr int kPolyExpFwd = QEM_POLY_EXP_FWD, kPolyExpBwd = QEM_POLY_EXP_BWD;
 
 // named barriers: 1 = all epilogue warps, 2..5 = the 4 warps of one TMEM lane quarter
 __device__ __forceinline__ void epi_bar() { named_bar(1, kTcEpiThreads); }
@@ -441,7 +451,8 @@ __device__ __forceinline__ void fwd_epi_online(uint32_t taddr, float& m, float& 
 #pragma unroll
     for (int c = 0; c < 16; c += 2) {
       const float2 e = add2(make_float2(v[c], v[c + 1]), nm);
-      acc[(c >> 1) & 1] = add2(acc[(c >> 1) & 1], make_float2(ex2(e.x), ex2(e.y)));
+      const float2 x = c >= 16 - kPolyExpFwd ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y));
+      acc[(c >> 1) & 1] = add2(acc[(c >> 1) & 1], x);
     }
     const float2 t = add2(acc[0], acc[1]);
     s += t.x + t.y;
@@ -1117,7 +1128,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
           const float2 x = add2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), l2);
-          wp[(c >> 1) & 1] = add2(wp[(c >> 1) & 1], make_float2(ex2(x.x), ex2(x.y)));
+          const float2 e = c >= 16 - kPolyExpBwd ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          wp[(c >> 1) & 1] = add2(wp[(c >> 1) & 1], e);
         }
       });
       tc_fence_before();

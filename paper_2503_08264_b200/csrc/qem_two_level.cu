@@ -569,6 +569,8 @@ template <int D>
 static int prep_threads(int) { return 32 * FwdLayout<D>::PREP_WARPS; }
 template <int D>
 static size_t prep_smem(int K, int J, bool tc) { return tc ? PrepTc::bytes(K, J) : FwdLayout<D>::prep_bytes(K, J); }
+template <int D>
+static int prep_threads_tc(int K, bool tc) { return tc ? 32 * PrepTc::WARPS : prep_threads<D>(K); }
 
 template <int D>
 static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, int* gf, int* gb, int* gp) {
@@ -583,7 +585,7 @@ static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, in
     of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
     ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
   }
-  const int op = occupancy(prep_fn<D>(d->obs_kind, tc), prep_threads<D>(K), prep_smem<D>(K, d->n_obs, tc));
+  const int op = occupancy(prep_fn<D>(d->obs_kind, tc), prep_threads_tc<D>(K, tc), prep_smem<D>(K, d->n_obs, tc));
   // Persistent-style grids: one full wave of resident CTAs, capped by the groups.
   int64_t f = (int64_t)sms * of, b = (int64_t)sms * ob, p = (int64_t)sms * op;
   *gf = (int)(f < n_local ? f : n_local);
@@ -604,7 +606,7 @@ static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st
     k_rowop_tc<<<(K + 255) / 256, 256, 0, st>>>(a);
     c->launches += 1;
   }
-  prep_fn<D>(c->desc.obs_kind, tc)<<<c->grid_prep, prep_threads<D>(K), prep_smem<D>(K, a.J, tc), st>>>(a);
+  prep_fn<D>(c->desc.obs_kind, tc)<<<c->grid_prep, prep_threads_tc<D>(K, tc), prep_smem<D>(K, a.J, tc), st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (c->ev[0]) cudaEventRecord((cudaEvent_t)c->ev[0], st);
