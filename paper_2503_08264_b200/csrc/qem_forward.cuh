@@ -99,7 +99,11 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
   }
 }
 
-constexpr float kLazy = 5.0f;  // natural-log units: deferred-rescale margin of the online log-sum-exp
+// Rescale margin of the online log-sum-exp (natural-log units).  0 = the shift is always the exact
+// running max, so the dominant term of every row is ex2(0) = 1 exactly: a positive margin saves
+// rescales but leaves ~1e-7 relative error on the dominant term, which the 1e5-group plate sum of
+// config 4 random-walks past the weight tolerance (tests/test_gpu_fullsize.py, intermediate regime).
+constexpr float kLazy = 0.0f;
 
 template <int D, int RP>
 __device__ __forceinline__ void tile_online(const float* col, int Kp, const float2 (&al)[RP], const float2 (&ga)[RP],
@@ -126,8 +130,7 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
       float2 cm = tv[0][p];
 #pragma unroll
       for (int c = 1; c < CH; ++c) cm = max2(cm, tv[c][p]);
-      // lazy max: rescale only when a chunk exceeds the running shift by > kLazy (the
-      // unscaled terms stay <= e^kLazy), so almost every pair costs exactly one ex2
+      // rescale only when a chunk raises the running max (rare after the first chunks)
       if (cm.x > mr[p].x + kLazy) {
         ac[p].x *= ex2((mr[p].x - cm.x) * kLog2e);
         mr[p].x = cm.x;
@@ -141,7 +144,7 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const float2 e = fma2(tv[c][p], f2(kLog2e), nm);
-        s = add2(s, make_float2(ex2(e.x), ex2(e.y)));
+        s = add2(s, kSoftExpFfma && c == CH - 1 ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y)));
       }
       ac[p] = s;
     }

@@ -442,7 +442,7 @@ __device__ __forceinline__ void fwd_epi_online(uint32_t taddr, float& m, float& 
     const float m0 = fmax3f(v[0], v[1], v[2]), m1 = fmax3f(v[3], v[4], v[5]), m2 = fmax3f(v[6], v[7], v[8]);
     const float m3 = fmax3f(v[9], v[10], v[11]), m4 = fmax3f(v[12], v[13], v[14]);
     const float mx = fmax3f(m0, m1, fmax3f(m2, m3, fmax3f(m4, v[15], m)));
-    if (mx > m + 8.f) {  // lazy shift (log2 units): unscaled terms stay <= 2^8
+    if (mx > m) {  // exact running max (see kLazy in qem_forward.cuh); rare after the first chunks
       s *= ex2(m - mx);
       m = mx;
     }

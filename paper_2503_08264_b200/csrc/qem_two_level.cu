@@ -209,6 +209,14 @@ __device__ __forceinline__ float2 expm1_poly(float2 x) {
   return mul2(p, x);
 }
 
+// FFMA-path tiles: 1 = evaluate 1 of every 4 exponentials on the FMA pipe (exp2_poly2) so the
+// FMA pipe and the SFU share the exp load; 0 = SFU only (default: on config 4 the software
+// exps cost more than they save, profiles/r01_poly_exp_sweep.txt).
+#ifndef QEM_SOFT_EXP_FFMA
+#define QEM_SOFT_EXP_FFMA 0
+#endif
+constexpr bool kSoftExpFfma = QEM_SOFT_EXP_FFMA != 0;
+
 #include "qem_forward.cuh"
 #include "qem_tc.cuh"
 
@@ -379,8 +387,8 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
     float2 acc[CP];
 #pragma unroll
     for (int p = 0; p < CP; ++p) acc[p] = f2(0.f);
-#pragma unroll 2
-    for (int k = 0; k < K; ++k) {
+    // one row of the pair tile; `soft` evaluates its exponentials on the FMA pipe (exp2_poly2)
+    auto row = [&](int k, bool soft) {
       const float* rp = rows + (size_t)k * RS;
       float rb[RS];
 #pragma unroll
@@ -402,9 +410,15 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
 #pragma unroll
           for (int r = 0; r < D; ++r) t = fma2(f2(rb[2 + r]), u[p][r], t);
         }
-        acc[p] = fma2(w2, make_float2(ex2(t.x), ex2(t.y)), acc[p]);
+        acc[p] = fma2(w2, soft ? exp2_poly2(t) : make_float2(ex2(t.x), ex2(t.y)), acc[p]);
       }
+    };
+    int k = 0;
+    for (; k + 4 <= K; k += 4) {  // every 4th row's exponentials on the FMA pipe (kSoftExpFfma)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) row(k + kk, kSoftExpFfma && kk == 3);
     }
+    for (; k < K; ++k) row(k, false);
     // ---- weights out + moments (fp64)
     double s1[D];
 #pragma unroll
