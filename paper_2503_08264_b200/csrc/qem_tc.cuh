@@ -160,12 +160,12 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
   const double es = exp(-root_lnv<D>(a, ks));
   for (int k = tid; k < K; k += blockDim.x) {
     const double ek = exp(-root_lnv<D>(a, k));
-    if constexpr (D == kTcD) {
+    if constexpr (D <= kTcD) {
       if (a.tc) {
         float v[kTcD];
 #pragma unroll
         for (int r = 0; r < kTcD; ++r)
-          v[r] = (float)((ek * (double)a.z_root[r * K + k] - es * (double)a.z_root[r * K + ks]) * kLog2eD);
+          v[r] = r < D ? (float)((ek * (double)a.z_root[r * K + k] - es * (double)a.z_root[r * K + ks]) * kLog2eD) : 0.f;
         store_row_split16(reinterpret_cast<unsigned char*>(a.ws.rowop_b), k, v);
         a.ws.bgam[k] = (float)(-0.5 * (ek - es) * kLog2eD);
         continue;
@@ -178,15 +178,16 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
 }
 
 // ------------------------------------------------------------------ rowop
+template <int D>
 __global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
   const int K = a.K;
   unsigned char* rc = reinterpret_cast<unsigned char*>(a.ws.rowop);
   unsigned char* rx = reinterpret_cast<unsigned char*>(a.ws.rowop_x);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
-    const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
-    float v[kTcD];
+    const float* fc = a.ws.fwd_coef + (size_t)k * (D + 2);
+    float v[kTcD];  // contraction zero-padded to 16 dims
 #pragma unroll
-    for (int r = 0; r < kTcD; ++r) v[r] = fc[2 + r] * kLog2e;
+    for (int r = 0; r < kTcD; ++r) v[r] = r < D ? fc[2 + r] * kLog2e : 0.f;
     store_row_split16(rc, k, v);
     uint4 c0, c1;
     extra_row(fc[1] * kLog2e, 1.f, 0.f, c0, c1);  // forward: lP on, no row constant
@@ -219,9 +220,12 @@ struct PrepTc {
   __host__ __device__ static size_t bytes(int K, int J) { return WARPS * warp_bytes(K, J); }
 };
 
+// 8 <= D <= 16 latent dims (the contraction is zero-padded to 16); Bernoulli-logit observations
+// (configs 2/5 shape; the OBS parameter keeps the Gaussian likelihood for d = 1 experiments).
+template <int D, int OBS>
 __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int D = kTcD;
+  static_assert(D <= kTcD, "tensor-core path: d <= 16");
   const int K = a.K, J = a.J, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned char* wb = smem + (size_t)wid * PrepTc::warp_bytes(K, J);
   double* qc = reinterpret_cast<double*>(wb);                      // [3][D]: m, 1/(2v), -(ln 2pi v)/2
@@ -234,6 +238,11 @@ __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
   const volatile float* mu_ref = mref;  // re-read per column (keeps registers for the z prefetch)
   const double bref_const = a.ws.ref->bref_const, e_ref = a.ws.ref->e_ref;
   const double logK = log((double)K);
+  double gc0 = 0.0, gc1 = 0.0;
+  if constexpr (OBS == QEM_OBS_GAUSS) {
+    gc0 = -0.5 * J * (kLn2Pi + log(a.obs_var));
+    gc1 = 0.5 / a.obs_var;
+  }
   unsigned char* colop = reinterpret_cast<unsigned char*>(a.ws.colop);
   for (int64_t i = (int64_t)blockIdx.x * PrepTc::WARPS + wid; i < a.n_local;
        i += (int64_t)gridDim.x * PrepTc::WARPS) {
@@ -244,7 +253,18 @@ __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
       qc[D + lane] = 0.5 / v;
       qc[2 * D + lane] = -0.5 * (kLn2Pi + log(v));
     }
-    {
+    double sx = 0.0, sxx = 0.0;
+    if constexpr (OBS == QEM_OBS_GAUSS) {
+      // sufficient statistics of the group's observations (d = 1)
+      const float* x = reinterpret_cast<const float*>(a.x) + i * J;
+      for (int jj = lane; jj < J; jj += 32) {
+        const double xv = x[jj];
+        sx += xv;
+        sxx += xv * xv;
+      }
+      sx = warp_sum(sx);
+      sxx = warp_sum(sxx);
+    } else {
       const uint8_t* x = reinterpret_cast<const uint8_t*>(a.x) + (size_t)i * J * D;
       const uint8_t* y = reinterpret_cast<const uint8_t*>(a.y) + (size_t)i * J;
       for (int e = lane; e < Jh * D; e += 32) {
@@ -273,49 +293,78 @@ __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
 #pragma unroll
         for (int r = 0; r < D; ++r) zn[r] = a.z[((size_t)i * D + r) * K + kc + 32];
       }
-      // log q(z) and the label part sum_j y_j eta_j = (sum_j y_j x_j) . z, both fp64
-      // (group constants re-read from SMEM each column: volatile keeps ptxas from hoisting 48 doubles)
+      // log q(z), fp64 (group constants re-read from SMEM each column: volatile keeps ptxas
+      // from hoisting them into registers)
       const volatile double* qv = qc;
-      double lq = 0.0, ly = 0.0;
+      double lq = 0.0;
 #pragma unroll
       for (int r = 0; r < D; ++r) {
-        const double zd = (double)zr[r], dz = zd - qv[r];
+        const double dz = (double)zr[r] - qv[r];
         lq += qv[2 * D + r] - dz * dz * qv[D + r];
-        ly = fma((double)yx[r], zd, ly);
       }
-      // softplus part: eta_j = x_j . z for two observations at a time (FFMA2)
-      double lsp = 0.0;
-      for (int jp = 0; jp < Jh; ++jp) {
-        const float4* xr = reinterpret_cast<const float4*>(xp + jp * D);
-        float2 e0 = f2(0.f), e1 = f2(0.f);
+      double ll;
+      if constexpr (OBS == QEM_OBS_GAUSS) {
+        const double zz = zr[0];
+        ll = gc0 - (sxx - 2.0 * zz * sx + (double)J * zz * zz) * gc1;
+      } else {
+        // label part sum_j y_j eta_j = (sum_j y_j x_j) . z in fp64; softplus part per
+        // observation, two observations at a time (FFMA2)
+        double ly = 0.0;
 #pragma unroll
-        for (int q = 0; q < D / 2; ++q) {
-          const float4 xv = xr[q];
-          e0 = fma2(make_float2(xv.x, xv.y), f2(zr[2 * q]), e0);
-          e1 = fma2(make_float2(xv.z, xv.w), f2(zr[2 * q + 1]), e1);
+        for (int r = 0; r < D; ++r) ly = fma((double)yx[r], (double)zr[r], ly);
+        double lsp = 0.0;
+        for (int jp = 0; jp < Jh; ++jp) {
+          const float2* xr = xp + jp * D;
+          float2 e0 = f2(0.f), e1 = f2(0.f);
+          if constexpr (D % 2 == 0) {
+#pragma unroll
+            for (int q = 0; q < D / 2; ++q) {  // 128-bit loads: features 2q, 2q+1 of both observations
+              const float4 xv = reinterpret_cast<const float4*>(xr)[q];
+              e0 = fma2(make_float2(xv.x, xv.y), f2(zr[2 * q]), e0);
+              e1 = fma2(make_float2(xv.z, xv.w), f2(zr[2 * q + 1]), e1);
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+              if (r & 1)
+                e1 = fma2(xr[r], f2(zr[r]), e1);
+              else
+                e0 = fma2(xr[r], f2(zr[r]), e0);
+            }
+          }
+          const float2 eta = add2(e0, e1);
+          const float sa = softplus_mufu(eta.x), sb = softplus_mufu(eta.y);
+          lsp += (double)sa;
+          if (2 * jp + 1 < J) lsp += (double)sb;
         }
-        const float2 eta = add2(e0, e1);
-        const float sa = softplus_mufu(eta.x), sb = softplus_mufu(eta.y);
-        lsp += (double)sa;
-        if (2 * jp + 1 < J) lsp += (double)sb;
+        ll = ly - lsp;
       }
-      const double ll = ly - lsp;
       // column operand re-centred on the group's Q mean: w = z - m_i and
       // S = |w|^2 + 2 m_i . w (so D_k(z) = alpha'_ik + c0_k . w + gamma_k S)
       float W2 = 0.f, mw = 0.f;
       double U2d = 0.0;
-      float wv[D];
+      float wv[kTcD];
 #pragma unroll
-      for (int r = 0; r < D; ++r) {
-        const float m = (float)qc[r];
-        wv[r] = zr[r] - m;
-        W2 = fmaf(wv[r], wv[r], W2);
-        mw = fmaf(m, wv[r], mw);
-        const double ud = (double)zr[r] - (double)mu_ref[r];
-        U2d += ud * ud;
+      for (int r = 0; r < kTcD; ++r) {
+        if (r < D) {
+          const float m = (float)qc[r];
+          wv[r] = zr[r] - m;
+          W2 = fmaf(wv[r], wv[r], W2);
+          mw = fmaf(m, wv[r], mw);
+          const double ud = (double)zr[r] - (double)mu_ref[r];
+          U2d += ud * ud;
+        } else {
+          wv[r] = 0.f;  // zero-padded contraction
+        }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {  // bf16x3 split of w, 8 dims (one 16-byte chunk per term) at a time
+        if (8 * h >= D) {
+          const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, q * 16 + 8 * h)) = zero;
+          continue;
+        }
         __nv_bfloat16 s0[8], s1[8], s2[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -527,6 +576,7 @@ struct FwdTcL {
 constexpr int kFwdAuxWarps = 2;  // row finalisers of the forward
 constexpr int kFwdThreads = kTcThreads + 32 * kFwdAuxWarps;
 
+template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   using L = FwdTcL;
@@ -635,7 +685,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
     const int atid = tid - kTcThreads;
     constexpr int NTA = 32 * kFwdAuxWarps;
     int md = 5;
-    float mi[kTcD];
+    float mi[D];
     float M2 = 0.f;
     int64_t j = 0, i = blockIdx.x;
     int rb = 0;
@@ -644,8 +694,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
         md = a.ws.gmode[i];
         M2 = 0.f;
 #pragma unroll
-        for (int r = 0; r < kTcD; ++r) {
-          mi[r] = a.q_m[i * kTcD + r];
+        for (int r = 0; r < D; ++r) {
+          mi[r] = a.q_m[i * D + r];
           M2 = fmaf(mi[r], mi[r], M2);
         }
         if (atid == 0) {
@@ -677,10 +727,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
           h = log1pf(sm);
         }
         // alpha'_ik = D_k(m_i) = alpha0_k + gamma_k |m_i|^2 + c0_k . m_i in fp64
-        const float* fc = a.ws.fwd_coef + (size_t)k * (kTcD + 2);
+        const float* fc = a.ws.fwd_coef + (size_t)k * (D + 2);
         double ap = a.ws.alpha_d[k] + (double)fc[1] * (double)M2;
 #pragma unroll
-        for (int r = 0; r < kTcD; ++r) ap += (double)fc[2 + r] * (double)mi[r];
+        for (int r = 0; r < D; ++r) ap += (double)fc[2 + r] * (double)mi[r];
         const double dgd = ap + (double)h;
         a.ws.hmsg[(size_t)i * K + k] = h;  // re-centred message, the backward's row constant
         a.ws.dg[(size_t)i * K + k] = (float)dgd;
@@ -796,11 +846,11 @@ constexpr int kBwdThreads = kTcThreads + 32 * kBwdAuxWarps;
 // (the forward's ln P is not needed any more).  One CTA per SM, persistent over groups;
 // each group's z (16 x K fp32, contiguous) and t_ref (K fp64) arrive in SMEM by one
 // cp.async.bulk each into a 2-stage ring, so HBM streams while the previous group computes.
-struct GroupStage {  // shared by k_bwd_cols_tc and k_moments_tc
+struct GroupStage {  // shared by k_bwd_cols_tc and k_moments_tc (z of D dims + t_ref or w)
   static constexpr int THREADS = 256;
-  __host__ __device__ static size_t z_bytes(int K) { return (size_t)kTcD * K * 4; }
-  __host__ __device__ static size_t stage(int K) { return z_bytes(K) + (size_t)K * 8; }  // + t_ref or w
-  __host__ __device__ static size_t bytes(int K) { return 2 * stage(K) + 64 * 8 + 4 * 8; }
+  __host__ __device__ static size_t z_bytes(int K, int D) { return (size_t)D * K * 4; }
+  __host__ __device__ static size_t stage(int K, int D) { return z_bytes(K, D) + (size_t)K * 8; }
+  __host__ __device__ static size_t bytes(int K, int D) { return 2 * stage(K, D) + 64 * 8 + 4 * 8; }
 };
 
 __device__ __forceinline__ double block_max256(double v, double* scr) {
@@ -824,20 +874,21 @@ __device__ __forceinline__ double block_sum256(double v, double* scr) {
   return m;
 }
 
+template <int D>
 __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_bwd_cols_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int K = a.K, tid = threadIdx.x;
-  const size_t SZ = GroupStage::stage(K);
+  const size_t SZ = GroupStage::stage(K, D);
   double* scr = reinterpret_cast<double*>(smem + 2 * SZ);
   uint64_t* full = reinterpret_cast<uint64_t*>(scr + 64);
   const int64_t n = a.n_local;
   const int64_t ngroups = n > blockIdx.x ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const uint32_t zb = (uint32_t)GroupStage::z_bytes(K), tb = (uint32_t)K * 8;
+  const uint32_t zb = (uint32_t)GroupStage::z_bytes(K, D), tb = (uint32_t)K * 8;
   auto issue = [&](int64_t j) {
     const int64_t i = blockIdx.x + j * gridDim.x;
     unsigned char* st = smem + (size_t)(j & 1) * SZ;
     mbar_expect_tx(&full[j & 1], zb + tb);
-    tma_bulk_g2s(st, a.z + (size_t)i * kTcD * K, zb, &full[j & 1]);
+    tma_bulk_g2s(st, a.z + (size_t)i * D * K, zb, &full[j & 1]);
     tma_bulk_g2s(st + zb, a.ws.tA + (size_t)i * K, tb, &full[j & 1]);
   };
   if (tid == 0) {
@@ -848,9 +899,9 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_bwd_cols_tc(TLArgs a
   __syncthreads();
   if (tid == 0)
     for (int64_t j = 0; j < 2 && j < ngroups; ++j) issue(j);
-  float mus[kTcD], mur[kTcD];
+  float mus[D], mur[D];
 #pragma unroll
-  for (int r = 0; r < kTcD; ++r) {
+  for (int r = 0; r < D; ++r) {
     mus[r] = a.ws.ref->mu_star[r];
     mur[r] = a.ws.ref->mu_ref[r];
   }
@@ -868,7 +919,7 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_bwd_cols_tc(TLArgs a
       const float* zs = reinterpret_cast<const float*>(st);
       double d[4] = {0.0, 0.0, 0.0, 0.0}, g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int r = 0; r < kTcD; ++r) {
+      for (int r = 0; r < D; ++r) {
         const float4 zv = *reinterpret_cast<const float4*>(zs + (size_t)r * K + c4);
         const double zz[4] = {(double)zv.x, (double)zv.y, (double)zv.z, (double)zv.w};
 #pragma unroll
@@ -905,20 +956,21 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_bwd_cols_tc(TLArgs a
 // After the backward: E z = c + S1/S0, Var z = S2/S0 - (S1/S0)^2, S_p = sum_k' w (z - c)^p in
 // fp64 (self-normalised, shifted by the Q mean c = m_i; R24).  One CTA per SM over groups,
 // z and w of a group staged by cp.async.bulk (2-stage ring); warp q handles dims 2q, 2q+1.
+template <int D>
 __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_moments_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int K = a.K, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t SZ = GroupStage::stage(K);
+  const size_t SZ = GroupStage::stage(K, D);
   double* scr = reinterpret_cast<double*>(smem + 2 * SZ);
   uint64_t* full = reinterpret_cast<uint64_t*>(scr + 64);
   const int64_t n = a.n_local;
   const int64_t ngroups = n > blockIdx.x ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const uint32_t zb = (uint32_t)GroupStage::z_bytes(K), wb = (uint32_t)K * 4;
+  const uint32_t zb = (uint32_t)GroupStage::z_bytes(K, D), wb = (uint32_t)K * 4;
   auto issue = [&](int64_t j) {
     const int64_t i = blockIdx.x + j * gridDim.x;
     unsigned char* st = smem + (size_t)(j & 1) * SZ;
     mbar_expect_tx(&full[j & 1], zb + wb);
-    tma_bulk_g2s(st, a.z + (size_t)i * kTcD * K, zb, &full[j & 1]);
+    tma_bulk_g2s(st, a.z + (size_t)i * D * K, zb, &full[j & 1]);
     tma_bulk_g2s(st + zb, a.w + (size_t)i * K, wb, &full[j & 1]);
   };
   if (tid == 0) {
@@ -935,13 +987,15 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_moments_tc(TLArgs a)
     mbar_wait(&full[j & 1], (uint32_t)((j >> 1) & 1));
     const float* zs = reinterpret_cast<const float*>(st);
     const float* ws = reinterpret_cast<const float*>(st + zb);
-    const int r0 = 2 * warp;  // 8 warps x 2 dims = 16
-    const double c0 = a.q_m[i * kTcD + r0], c1 = a.q_m[i * kTcD + r0 + 1];
+    const int r0 = 2 * warp;  // 8 warps x 2 dims (dims >= D: the warp idles)
+    const int r1 = r0 + 1 < D ? r0 + 1 : r0;
+    const bool act = r0 < D;
+    const double c0 = act ? a.q_m[i * D + r0] : 0.0, c1 = act ? a.q_m[i * D + r1] : 0.0;
     double s0 = 0.0, a1 = 0.0, a2 = 0.0, b1 = 0.0, b2 = 0.0;
-    for (int c4 = lane * 4; c4 < K; c4 += 128) {
+    for (int c4 = lane * 4; act && c4 < K; c4 += 128) {
       const float4 wv = *reinterpret_cast<const float4*>(ws + c4);
       const float4 za = *reinterpret_cast<const float4*>(zs + (size_t)r0 * K + c4);
-      const float4 zb4 = *reinterpret_cast<const float4*>(zs + (size_t)(r0 + 1) * K + c4);
+      const float4 zb4 = *reinterpret_cast<const float4*>(zs + (size_t)r1 * K + c4);
       const double w4[4] = {wv.x, wv.y, wv.z, wv.w};
       const double e4[4] = {za.x - c0, za.y - c0, za.z - c0, za.w - c0};
       const double f4[4] = {zb4.x - c1, zb4.y - c1, zb4.z - c1, zb4.w - c1};
@@ -960,12 +1014,14 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_moments_tc(TLArgs a)
     a2 = warp_sum(a2);
     b1 = warp_sum(b1);
     b2 = warp_sum(b2);
-    if (lane == 0) {
+    if (lane == 0 && act) {
       const double ma = a1 / s0, mb = b1 / s0;
-      a.m1[i * kTcD + r0] = c0 + ma;
-      a.v[i * kTcD + r0] = a2 / s0 - ma * ma;
-      a.m1[i * kTcD + r0 + 1] = c1 + mb;
-      a.v[i * kTcD + r0 + 1] = b2 / s0 - mb * mb;
+      a.m1[i * D + r0] = c0 + ma;
+      a.v[i * D + r0] = a2 / s0 - ma * ma;
+      if (r1 != r0) {
+        a.m1[i * D + r1] = c1 + mb;
+        a.v[i * D + r1] = b2 / s0 - mb * mb;
+      }
     }
     __syncthreads();  // every thread is done with this stage
     if (tid == 0 && j + 2 < ngroups) issue(j + 2);

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
   __shared__ double s_val[32];
   __shared__ int s_idx[32];
   __shared__ double s_lnv_ref;
+  __shared__ double s_qc[2 * (QEM_MAX_D + 1)];
   __shared__ float s_key[QEM_MAX_K];
   const int K = a.K, tid = threadIdx.x;
   const int R = D + (a.scale_kind != QEM_SCALE_FIXED);
@@ -113,6 +114,11 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
     s_lnv_ref = lnv;
     ref->e_ref = exp(-lnv);
     ref->bref_const = -0.5 * D * (kLn2Pi + lnv);
+  }
+  // per-dimension constants of f_root: -(ln prior_var - ln v_r)/2 and 1/v_r
+  for (int r = tid; r < R; r += blockDim.x) {
+    s_qc[r] = -0.5 * (log(a.prior_var) - log((double)a.qr_v[r]));
+    s_qc[QEM_MAX_D + 1 + r] = 1.0 / (double)a.qr_v[r];
   }
   __syncthreads();
   const int kref = a.ws.ref->k_ref;
@@ -167,10 +173,12 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
     a.ws.alpha_d[k] = alpha;
     bt[0] = (float)(alpha * kLog2eD);
     bt[1] = (float)(gamma * kLog2eD);
+    // f_root(k) = sum_r lnN(z_r; prior) - lnN(z_r; Q_root), the log-normalisers hoisted (s_qc)
     double f = 0.0;
     for (int r = 0; r < R; ++r) {
       const double v = (double)a.z_root[r * K + k];
-      f += lnN(v, a.prior_mean, a.prior_var) - lnN(v, (double)a.qr_m[r], (double)a.qr_v[r]);
+      const double dp = v - a.prior_mean, dq = v - (double)a.qr_m[r];
+      f += s_qc[r] - 0.5 * dp * dp / a.prior_var + 0.5 * dq * dq * s_qc[QEM_MAX_D + 1 + r];
     }
     a.ws.f_root[k] = f;
     // sort key: |D| bound at unit column scale
@@ -563,7 +571,9 @@ template <int D>
 static KernelFn prep_fn(int obs, bool tc) {
   if constexpr (D == 1)
     if (obs == QEM_OBS_GAUSS) return k_colprep<D, QEM_OBS_GAUSS, false>;
-  if (tc) return k_colprep_tc;
+  if constexpr (D >= 8 && D <= kTcD) {
+    if (tc) return k_colprep_tc<D, QEM_OBS_BERNOULLI_LOGIT>;
+  }
   return k_colprep<D, QEM_OBS_BERNOULLI_LOGIT, false>;
 }
 template <int D>
@@ -591,10 +601,14 @@ static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, in
   const int K = d->K, rp = pick_rp(K);
   int of, ob;
   if (tc) {
-    of = occupancy(k_forward_tc, kFwdThreads, FwdTcL::bytes(K));
-    ob = occupancy(k_backward_tc, kBwdThreads, BwdTcL::bytes(K));
-    occupancy(k_bwd_cols_tc, GroupStage::THREADS, GroupStage::bytes(K));  // set the dynamic-SMEM attributes
-    occupancy(k_moments_tc, GroupStage::THREADS, GroupStage::bytes(K));
+    if constexpr (D <= kTcD) {
+      of = occupancy(k_forward_tc<D>, kFwdThreads, FwdTcL::bytes(K));
+      ob = occupancy(k_backward_tc, kBwdThreads, BwdTcL::bytes(K));
+      occupancy(k_bwd_cols_tc<D>, GroupStage::THREADS, GroupStage::bytes(K, D));  // set the dynamic-SMEM attributes
+      occupancy(k_moments_tc<D>, GroupStage::THREADS, GroupStage::bytes(K, D));
+    } else {
+      of = ob = 1;
+    }
   } else {
     of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
     ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
@@ -615,9 +629,9 @@ static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (c->desc.obs_kind == QEM_OBS_GAUSS && D != 1) return cudaErrorInvalidValue;
-  const bool tc = D == kTcD && c->tc;
+  const bool tc = D <= kTcD && c->tc;
   if (tc) {
-    k_rowop_tc<<<(K + 255) / 256, 256, 0, st>>>(a);
+    k_rowop_tc<D><<<(K + 255) / 256, 256, 0, st>>>(a);
     c->launches += 1;
   }
   prep_fn<D>(c->desc.obs_kind, tc)<<<c->grid_prep, prep_threads_tc<D>(K, tc), prep_smem<D>(K, a.J, tc), st>>>(a);
@@ -625,7 +639,7 @@ static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st
   if (e != cudaSuccess) return e;
   if (c->ev[0]) cudaEventRecord((cudaEvent_t)c->ev[0], st);
   if (tc)
-    k_forward_tc<<<c->grid_fwd, kFwdThreads, FwdTcL::bytes(K), st>>>(a);
+    k_forward_tc<(D <= kTcD ? D : 1)><<<c->grid_fwd, kFwdThreads, FwdTcL::bytes(K), st>>>(a);
   else
     fwd_fn<D>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
   if (c->ev[1]) cudaEventRecord((cudaEvent_t)c->ev[1], st);
@@ -641,9 +655,10 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int cp = pick_rp(K);
-  const bool tc = D == kTcD && c->tc;
+  const bool tc = D <= kTcD && c->tc;
+  constexpr int DT = D <= kTcD ? D : 1;
   if (tc) {
-    k_bwd_cols_tc<<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K), st>>>(a);
+    k_bwd_cols_tc<DT><<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K, DT), st>>>(a);
     c->launches += 1;
   }
   if (c->ev[2]) cudaEventRecord((cudaEvent_t)c->ev[2], st);
@@ -653,7 +668,7 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
     bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
   if (c->ev[3]) cudaEventRecord((cudaEvent_t)c->ev[3], st);
   if (tc) {
-    k_moments_tc<<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K), st>>>(a);
+    k_moments_tc<DT><<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K, DT), st>>>(a);
     c->launches += 1;
   }
   c->launches += 2;
@@ -671,7 +686,12 @@ int tl_supported_d(int d) {
 
 int tl_use_tc(const qem_model_desc* d) {
   static const int off = getenv("QEM_NO_TC") != nullptr;  // tuning / comparison override
-  return !off && d->d == kTcD && d->obs_kind == QEM_OBS_BERNOULLI_LOGIT && d->K % 256 == 0 && d->K <= QEM_MAX_K;
+  // tensor-core pair kernels: 8 <= d <= 16 (contraction zero-padded to 16), K a multiple of 256,
+  // Bernoulli-logit observations.  Below d = 8 the FFMA tiles win: the 128-byte column operand
+  // would be mostly padding, and at config 4's K = 256 its HBM stream (3.3 GB per pass) would
+  // rival the pair work.
+  return !off && d->d >= 8 && d->d <= kTcD && tl_supported_d(d->d) && d->obs_kind == QEM_OBS_BERNOULLI_LOGIT &&
+         d->K % 256 == 0 && d->K <= QEM_MAX_K;
 }
 
 void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb, int* gp) {
