@@ -92,16 +92,28 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
   return d;
 }
+__device__ __forceinline__ uint32_t mbar_try_wait(uint32_t a, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return done;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait for the phase of `bar` with the given parity.  A wait longer than 10 s traps (a protocol
+// bug then fails the launch with an error instead of hanging the GPU).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
   const uint32_t a = smem_u32(bar);
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
+  if (mbar_try_wait(a, parity)) return;
+  const uint64_t t0 = global_ns();
+  while (!mbar_try_wait(a, parity))
+    if (global_ns() - t0 > 10000000000ull) __trap();
 }
 
 // ------------------------------------------- tcgen05 operand helpers (d = 16)
@@ -222,6 +234,27 @@ __device__ __forceinline__ double ldg_d(const double* p) {
   double v;
   asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Register-dependency fence: no use of `r` is scheduled before this point (pairs with a
+// preceding tcgen05.wait::ld, since volatile asm statements keep their relative order).
+__device__ __forceinline__ void reg_fence16(uint32_t (&r)[16]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
+// 32 lanes x 64 columns from TMEM in one go: four x16 loads in flight, one wait.
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[4][16]) {
+  tmem_ld16_async(taddr, r[0]);
+  tmem_ld16_async(taddr + 16, r[1]);
+  tmem_ld16_async(taddr + 32, r[2]);
+  tmem_ld16_async(taddr + 48, r[3]);
+  tmem_wait16(r[0]);
+  reg_fence16(r[1]);
+  reg_fence16(r[2]);
+  reg_fence16(r[3]);
 }
 
 // ---------------------------------------------------------------- reductions

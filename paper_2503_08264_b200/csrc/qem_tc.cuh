@@ -482,30 +482,30 @@ __device__ __forceinline__ float2 expm1_2_poly(float2 x) {
 // Forward epilogue, online mode: (m, s) = running max / sum of 2^(v - m) over
 // v = c2.u + g2 U + lP (log2 domain; the row constant is added at the end).
 // The max is lazy: s is rescaled only when a chunk raises it.
-template <int NC16>
 __device__ __forceinline__ void fwd_epi_online(uint32_t taddr, float& m, float& s) {
-  tmem_pipeline16<NC16>(taddr, [&](int, uint32_t(&r)[16]) {
-    float v[16];
+  uint32_t r[4][16];
+  tmem_ld64(taddr, r);  // the thread's 64 columns of this tile, one TMEM round trip
+  float mx = m;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
-    const float m0 = fmax3f(v[0], v[1], v[2]), m1 = fmax3f(v[3], v[4], v[5]), m2 = fmax3f(v[6], v[7], v[8]);
-    const float m3 = fmax3f(v[9], v[10], v[11]), m4 = fmax3f(v[12], v[13], v[14]);
-    const float mx = fmax3f(m0, m1, fmax3f(m2, m3, fmax3f(m4, v[15], m)));
-    if (mx > m) {  // exact running max (see kLazy in qem_forward.cuh); rare after the first chunks
-      s *= ex2(m - mx);
-      m = mx;
-    }
-    const float2 nm = f2(-m);
-    float2 acc[2] = {f2(0.f), f2(0.f)};
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) mx = fmax3f(mx, __uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1]));
+  if (mx > m) {  // exact running max (see kLazy in qem_forward.cuh)
+    s *= ex2(m - mx);
+    m = mx;
+  }
+  const float2 nm = f2(-m);
+  float2 acc[4] = {f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int c = 0; c < 16; c += 2) {
-      const float2 e = add2(make_float2(v[c], v[c + 1]), nm);
+      const float2 e = add2(make_float2(__uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1])), nm);
       const float2 x = c >= 16 - kPolyExpFwd ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y));
-      acc[(c >> 1) & 1] = add2(acc[(c >> 1) & 1], x);
+      acc[q] = add2(acc[q], x);
     }
-    const float2 t = add2(acc[0], acc[1]);
-    s += t.x + t.y;
-  });
+  const float2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+  s += t.x + t.y;
 }
 
 // Forward epilogue, polynomial mode: acc += sum P (2^v - 1), v = log2e D' = c2.w + g2 S.
@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
       tc_fence_after();
       const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * 64) + ((uint32_t)(q * 32) << 16);
       if (md == 5) {
-        fwd_epi_online<4>(taddr, st0, st1);
+        fwd_epi_online(taddr, st0, st1);
       } else {
         mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));  // P of this block is in SMEM
         const float* pp = s_p + (J & 1) * 256 + cq * 64;
@@ -832,7 +832,7 @@ struct BwdTcL {
   static constexpr size_t a() { return 0; }
   static constexpr size_t b() { return a() + 2 * A_STAGE; }
   static constexpr size_t wp() { return b() + SB * B_STAGE; }            // [2][4][128] float
-  static constexpr size_t bars() { return wp() + 2 * 4 * 128 * 4; }      // 24 mbarriers
+  static constexpr size_t bars() { return wp() + 2 * 4 * 128 * 4; }      // 24 mbarriers (20 used)
   static size_t __host__ __device__ bx(int) { return (bars() + 24 * 8 + 1023) & ~(size_t)1023; }
   static size_t __host__ __device__ bytes(int K) { return bx(K) + (size_t)2 * K * kTcRowXBytes; }
 };
@@ -1032,7 +1032,7 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_moments_tc(TLArgs a)
 // ahead: [Eg pattern | 0 0 0 | rho], rho_k = log2 w_root(k) - log2e (h_k - h_*) (h = the
 // forward's re-centred message; -1e30 where w_root = 0).
 __device__ void bwd_bx(const TLArgs& a, int64_t i, unsigned char* bx, int atid) {
-  constexpr int NT = 32 * kBwdAuxWarps;
+  constexpr int NT = 32;  // one aux warp builds the slabs
   const int K = a.K;
   const float hs = a.ws.hmsg[(size_t)i * K + a.ws.ref->k_star];
 #pragma unroll 2
@@ -1071,6 +1071,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
   uint64_t* t_empty = t_full + 2;     // [2]  16 epilogue warps
   uint64_t* bx_full = t_empty + 2;    // [2]  aux warps: row extra slab of a group ready (MMA waits)
   uint64_t* g_done = bx_full + 2;     // [2]  16 epilogue warps: group finished (its slab stage is free)
+  uint64_t* wp_full = g_done + 2;     // [2]  16 epilogue warps: a column block's 4 slice sums are in s_wp
+  uint64_t* wp_empty = wp_full + 2;   // [2]  merger warp: s_wp stage merged
   unsigned char* s_bx = smem + L::bx(K);
   __shared__ uint32_t s_tmem;
 
@@ -1084,8 +1086,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
       mbar_init(&a_empty[b], 1);
       mbar_init(&t_full[b], 1);
       mbar_init(&t_empty[b], kTcEpiWarps);
-      mbar_init(&bx_full[b], kBwdAuxWarps);
+      mbar_init(&bx_full[b], 1);  // the slab-builder warp
       mbar_init(&g_done[b], kTcEpiWarps);
+      mbar_init(&wp_full[b], kTcEpiWarps);
+      mbar_init(&wp_empty[b], 1);
     }
     for (int b = 0; b < SB; ++b) {
       mbar_init(&b_full[b], 1);
@@ -1147,9 +1151,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
         if (rb == RB - 1) umma_commit(&a_empty[J & 1]);
       }
     }
-  } else if (warp >= kTcEpiWarps + 2) {
-    // ------------------------------- aux: row extra slabs two groups ahead of the MMAs
-    const int atid = tid - kTcThreads;
+  } else if (warp == kTcEpiWarps + 2) {
+    // ------------------------------- aux 1: row extra slabs two groups ahead of the MMAs
+    const int atid = lane;
     for (int64_t jj = 0; jj < 2 && jj < ngroups; ++jj) {
       bwd_bx(a, blockIdx.x + jj * gridDim.x, s_bx + (size_t)jj * K * kTcRowXBytes, atid);
       __syncwarp();
@@ -1161,6 +1165,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
       bwd_bx(a, blockIdx.x + (j + 2) * gridDim.x, s_bx + (size_t)st * K * kTcRowXBytes, atid);
       __syncwarp();
       if (lane == 0) mbar_arrive(&bx_full[st]);
+    }
+  } else if (warp == kTcEpiWarps + 3) {
+    // ------------------------------- aux 2: merge the 4 row-slice sums of each column block -> w
+    int64_t i = blockIdx.x;
+    int cb = 0;
+    for (int64_t u = 0; u < ngroups * CB; ++u) {
+      const int st = (int)(u & 1);
+      mbar_wait(&wp_full[st], (uint32_t)((u >> 1) & 1));
+      const float* wpb = s_wp + st * 512;
+#pragma unroll
+      for (int c = lane; c < 128; c += 32) {
+        const float wv = wpb[c] + wpb[128 + c] + wpb[256 + c] + wpb[384 + c];
+        a.w[(size_t)i * K + cb * 128 + c] = wv;
+        if (isnan(wv)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wp_empty[st]);
+      if (++cb == CB) {
+        cb = 0;
+        i += gridDim.x;
+      }
     }
   } else {
     // ---------------------------------------------------------------- epilogue
@@ -1180,6 +1205,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
       const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * 64) + ((uint32_t)(q * 32) << 16);
       float2 wp[2] = {f2(0.f), f2(0.f)};
       const float2 l2 = f2(L2c);
+      // 16-column chunks with the next chunk's TMEM load in flight (measured faster here than one
+      // 64-column load: the SFU work of a chunk overlaps the next load)
       tmem_pipeline16<4>(taddr, [&](int, uint32_t(&r)[16]) {
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
@@ -1188,26 +1215,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
           wp[(c >> 1) & 1] = add2(wp[(c >> 1) & 1], e);
         }
       });
+      wp[0] = add2(wp[0], wp[1]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&t_empty[T & 1]);
         if (t == TPG - 1) mbar_arrive(&g_done[j & 1]);
       }
-      {
-        const float2 s2 = add2(wp[0], wp[1]);
-        acc += s2.x + s2.y;
-      }
+      acc += wp[0].x + wp[0].y;
       if (rb == RB - 1) {
-        float* wpb = s_wp + (cb & 1) * 512;
-        wpb[cq * 128 + q * 32 + lane] = acc;
-        quarter_bar(q);
-        if (cq == 0) {
-          const float wv = wpb[q * 32 + lane] + wpb[128 + q * 32 + lane] + wpb[256 + q * 32 + lane] +
-                           wpb[384 + q * 32 + lane];
-          a.w[(size_t)i * K + col] = wv;
-          if (isnan(wv)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
-        }
+        // hand the column block's slice sum to the merger warp (no epilogue barrier)
+        const int64_t u = tw.J;
+        const int st = (int)(u & 1);
+        if (u >= 2) mbar_wait(&wp_empty[st], (uint32_t)(((u >> 1) - 1) & 1));
+        s_wp[st * 512 + cq * 128 + q * 32 + lane] = acc;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wp_full[st]);
       }
     }
   }
