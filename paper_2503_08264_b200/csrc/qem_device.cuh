@@ -92,12 +92,14 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
   return d;
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware (woken when the phase
+// completes) instead of spinning and taking issue slots from the epilogue warps.
 __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t a, uint32_t parity) {
   uint32_t done;
   asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(done)
-      : "r"(a), "r"(parity)
+      : "r"(a), "r"(parity), "r"(1000000u)
       : "memory");
   return done;
 }

@@ -565,9 +565,11 @@ struct FwdTcL {
   static constexpr size_t a() { return 0; }
   static constexpr size_t b() { return a() + SA * A_STAGE; }
   static constexpr size_t p() { return b() + 2 * B_STAGE; }
-  static constexpr size_t fin() { return p() + 2 * P_STAGE; }         // [2][4][128] float2
-  static constexpr size_t bars() { return fin() + 2 * 4 * 128 * 8; }  // 20 mbarriers
-  static size_t __host__ __device__ st0(int) { return bars() + 20 * 8; }
+  static constexpr int FS = 8;                                        // row-block hand-over stages
+  static constexpr size_t fin() { return p() + 2 * P_STAGE; }         // [FS][4][128] float2
+  static constexpr size_t bars() { return fin() + FS * 4 * 128 * 8; }  // 2*SA + 8 + 2*FS mbarriers
+  static constexpr int NBARS = 2 * SA + 8 + 2 * FS;
+  static size_t __host__ __device__ st0(int) { return bars() + NBARS * 8; }
   static size_t __host__ __device__ st1(int K) { return st0(K) + (size_t)4 * K * 4; }
   static size_t __host__ __device__ g(int K) { return st1(K) + (size_t)4 * K * 4; }
   static size_t __host__ __device__ bytes(int K) { return g(K) + (size_t)K * 8; }
@@ -594,8 +596,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
   uint64_t* b_empty = b_full + 2;    // [2]  MMA commit + 16 epilogue warps
   uint64_t* t_full = b_empty + 2;    // [2]
   uint64_t* t_empty = t_full + 2;    // [2]  16 epilogue warps
-  uint64_t* f_full = t_empty + 2;    // [2]  16 epilogue warps: a row block's slice states are in s_fin
-  uint64_t* f_empty = f_full + 2;    // [2]  aux warps: s_fin stage merged
+  uint64_t* f_full = t_empty + 2;    // [FS] 16 epilogue warps: a row block's slice states are in s_fin
+  uint64_t* f_empty = f_full + L::FS;  // [FS] aux warps: s_fin stage merged
   float* s_st0 = reinterpret_cast<float*>(smem + L::st0(K));
   float* s_st1 = reinterpret_cast<float*>(smem + L::st1(K));
   double* s_g = reinterpret_cast<double*>(smem + L::g(K));
@@ -615,6 +617,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
       mbar_init(&b_empty[b], 1 + kTcEpiWarps);
       mbar_init(&t_full[b], 1);
       mbar_init(&t_empty[b], kTcEpiWarps);
+    }
+    for (int b = 0; b < L::FS; ++b) {
       mbar_init(&f_full[b], kTcEpiWarps);
       mbar_init(&f_empty[b], kFwdAuxWarps);
     }
@@ -703,8 +707,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
           csum += a.ws.cvec[i];
         }
       }
-      const int st = (int)(u & 1);
-      mbar_wait(&f_full[st], (uint32_t)((u >> 1) & 1));
+      const int st = (int)(u % L::FS);
+      mbar_wait(&f_full[st], (uint32_t)((u / L::FS) & 1));
       const float2* fin = s_fin + st * 512;
       for (int rr = atid; rr < 128; rr += NTA) {
         const int k = rb * 128 + rr;
@@ -789,8 +793,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
         s_st1[cq * K + k] = st1;
       } else {
         // ---- row k complete in this slice: hand (max, sum) to the aux warps
-        const int fs = (int)(u & 1);
-        if (u >= 2) mbar_wait(&f_empty[fs], (uint32_t)(((u >> 1) - 1) & 1));
+        const int fs = (int)(u % L::FS);
+        if (u >= L::FS) mbar_wait(&f_empty[fs], (uint32_t)(((u / L::FS) - 1) & 1));
         s_fin[fs * 512 + cq * 128 + q * 32 + lane] = make_float2(st0, st1);
         __syncwarp();
         if (lane == 0) mbar_arrive(&f_full[fs]);
