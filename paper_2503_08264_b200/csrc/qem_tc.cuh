@@ -211,6 +211,9 @@ __device__ __forceinline__ float softplus_mufu(float eta) {
   return fmaxf(eta, 0.f) + fmaf(l2, 0.69314718055994531f, __fdividef(v - (u - 1.f), u));
 }
 
+#ifndef QEM_COLPREP_MINB
+#define QEM_COLPREP_MINB 2  // resident CTAs per SM the column prep is compiled for (register budget)
+#endif
 struct PrepTc {
   static constexpr int WARPS = 8;
   __host__ __device__ static size_t warp_bytes(int K, int J) {
@@ -223,7 +226,7 @@ struct PrepTc {
 // 8 <= D <= 16 latent dims (the contraction is zero-padded to 16); Bernoulli-logit observations
 // (configs 2/5 shape; the OBS parameter keeps the Gaussian likelihood for d = 1 experiments).
 template <int D, int OBS>
-__global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
+__global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   static_assert(D <= kTcD, "tensor-core path: d <= 16");
   const int K = a.K, J = a.J, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -281,63 +284,15 @@ __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
     unsigned char* cop = colop + (size_t)i * K * kTcColBytes;
     double tmax = -CUDART_INF;
     float w2max = 0.f;
-    // z of the next column is loaded while this one is processed (latency hiding at 16 warps/SM)
-    float zn[D];
-#pragma unroll
-    for (int r = 0; r < D; ++r) zn[r] = lane < K ? a.z[((size_t)i * D + r) * K + lane] : 0.f;
-    for (int kc = lane; kc < K; kc += 32) {
-      float zr[D];
-#pragma unroll
-      for (int r = 0; r < D; ++r) zr[r] = zn[r];
-      if (kc + 32 < K) {
-#pragma unroll
-        for (int r = 0; r < D; ++r) zn[r] = a.z[((size_t)i * D + r) * K + kc + 32];
-      }
-      // log q(z), fp64 (group constants re-read from SMEM each column: volatile keeps ptxas
-      // from hoisting them into registers)
+    // the rest of a column once its likelihood is known: log q, the column operand, t_ref
+    auto finish = [&](int kc, const float (&zr)[D], double ll) {
+      // log q(z), fp64 (group constants re-read from SMEM: volatile keeps ptxas from hoisting them)
       const volatile double* qv = qc;
       double lq = 0.0;
 #pragma unroll
       for (int r = 0; r < D; ++r) {
         const double dz = (double)zr[r] - qv[r];
         lq += qv[2 * D + r] - dz * dz * qv[D + r];
-      }
-      double ll;
-      if constexpr (OBS == QEM_OBS_GAUSS) {
-        const double zz = zr[0];
-        ll = gc0 - (sxx - 2.0 * zz * sx + (double)J * zz * zz) * gc1;
-      } else {
-        // label part sum_j y_j eta_j = (sum_j y_j x_j) . z in fp64; softplus part per
-        // observation, two observations at a time (FFMA2)
-        double ly = 0.0;
-#pragma unroll
-        for (int r = 0; r < D; ++r) ly = fma((double)yx[r], (double)zr[r], ly);
-        double lsp = 0.0;
-        for (int jp = 0; jp < Jh; ++jp) {
-          const float2* xr = xp + jp * D;
-          float2 e0 = f2(0.f), e1 = f2(0.f);
-          if constexpr (D % 2 == 0) {
-#pragma unroll
-            for (int q = 0; q < D / 2; ++q) {  // 128-bit loads: features 2q, 2q+1 of both observations
-              const float4 xv = reinterpret_cast<const float4*>(xr)[q];
-              e0 = fma2(make_float2(xv.x, xv.y), f2(zr[2 * q]), e0);
-              e1 = fma2(make_float2(xv.z, xv.w), f2(zr[2 * q + 1]), e1);
-            }
-          } else {
-#pragma unroll
-            for (int r = 0; r < D; ++r) {
-              if (r & 1)
-                e1 = fma2(xr[r], f2(zr[r]), e1);
-              else
-                e0 = fma2(xr[r], f2(zr[r]), e0);
-            }
-          }
-          const float2 eta = add2(e0, e1);
-          const float sa = softplus_mufu(eta.x), sb = softplus_mufu(eta.y);
-          lsp += (double)sa;
-          if (2 * jp + 1 < J) lsp += (double)sb;
-        }
-        ll = ly - lsp;
       }
       // column operand re-centred on the group's Q mean: w = z - m_i and
       // S = |w|^2 + 2 m_i . w (so D_k(z) = alpha'_ik + c0_k . w + gamma_k S)
@@ -347,7 +302,7 @@ __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
 #pragma unroll
       for (int r = 0; r < kTcD; ++r) {
         if (r < D) {
-          const float m = (float)qc[r];
+          const float m = (float)qv[r];
           wv[r] = zr[r] - m;
           W2 = fmaf(wv[r], wv[r], W2);
           mw = fmaf(m, wv[r], mw);
@@ -388,6 +343,66 @@ __global__ void __launch_bounds__(256, 2) k_colprep_tc(TLArgs a) {
       a.ws.tA[(size_t)i * K + kc] = t;
       tmax = fmax(tmax, t);
       w2max = fmaxf(w2max, W2);
+    };
+    // Two columns per lane at a time (kc and kc + K/2): the per-observation feature loads are
+    // shared and the two likelihood chains hide each other's latency.
+    for (int kcA = lane; kcA < K / 2; kcA += 32) {
+      const int kcB = kcA + K / 2;
+      float zA[D], zB[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        zA[r] = a.z[((size_t)i * D + r) * K + kcA];
+        zB[r] = a.z[((size_t)i * D + r) * K + kcB];
+      }
+      double llA, llB;
+      if constexpr (OBS == QEM_OBS_GAUSS) {
+        const double za = zA[0], zb = zB[0];
+        llA = gc0 - (sxx - 2.0 * za * sx + (double)J * za * za) * gc1;
+        llB = gc0 - (sxx - 2.0 * zb * sx + (double)J * zb * zb) * gc1;
+      } else {
+        // label part sum_j y_j eta_j = (sum_j y_j x_j) . z in fp64; softplus part per
+        // observation, two observations at a time (FFMA2), for both columns
+        double lyA = 0.0, lyB = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          lyA = fma((double)yx[r], (double)zA[r], lyA);
+          lyB = fma((double)yx[r], (double)zB[r], lyB);
+        }
+        double lspA = 0.0, lspB = 0.0;
+        for (int jp = 0; jp < Jh; ++jp) {
+          const float2* xr = xp + jp * D;
+          float2 a0 = f2(0.f), a1 = f2(0.f), b0 = f2(0.f), b1 = f2(0.f);
+          if constexpr (D % 2 == 0) {
+#pragma unroll
+            for (int q = 0; q < D / 2; ++q) {  // 128-bit loads: features 2q, 2q+1 of both observations
+              const float4 xv = reinterpret_cast<const float4*>(xr)[q];
+              a0 = fma2(make_float2(xv.x, xv.y), f2(zA[2 * q]), a0);
+              a1 = fma2(make_float2(xv.z, xv.w), f2(zA[2 * q + 1]), a1);
+              b0 = fma2(make_float2(xv.x, xv.y), f2(zB[2 * q]), b0);
+              b1 = fma2(make_float2(xv.z, xv.w), f2(zB[2 * q + 1]), b1);
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+              if (r & 1) {
+                a1 = fma2(xr[r], f2(zA[r]), a1);
+                b1 = fma2(xr[r], f2(zB[r]), b1);
+              } else {
+                a0 = fma2(xr[r], f2(zA[r]), a0);
+                b0 = fma2(xr[r], f2(zB[r]), b0);
+              }
+            }
+          }
+          const float2 ea = add2(a0, a1), eb = add2(b0, b1);
+          const bool two = 2 * jp + 1 < J;
+          lspA += (double)softplus_mufu(ea.x) + (two ? (double)softplus_mufu(ea.y) : 0.0);
+          lspB += (double)softplus_mufu(eb.x) + (two ? (double)softplus_mufu(eb.y) : 0.0);
+        }
+        llA = lyA - lspA;
+        llB = lyB - lspB;
+      }
+      finish(kcA, zA, llA);
+      finish(kcB, zB, llB);
     }
     const double M = warp_max(tmax);
     const float W2max = warp_maxf(w2max);
