@@ -101,7 +101,7 @@ size_t carve(qem_ctx* c, char* base) {
     c->tw.partial = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->grid_fwd * (K + 1)));
     c->tw.red = reinterpret_cast<double*>(take(sizeof(double) * (K + 1)));
     c->tw.dg = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
-    const size_t kp = (size_t)((K + 3) / 4 * 4);
+    const size_t kp = (size_t)((K + 15) / 16 * 16);  // >= FwdLayout::kpad(K) for any column chunk <= 16
     if (!c->tc)
       c->tw.colrec = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * kp * pad4(D + 3)));
     if (c->tc) {

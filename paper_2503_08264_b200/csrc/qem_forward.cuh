@@ -20,10 +20,13 @@
 //   The mode is CTA-uniform (max over the CTA's rows) so warps stay in step.
 #pragma once
 
+#ifndef QEM_FWD_CH
+#define QEM_FWD_CH 16
+#endif
 template <int D>
 struct FwdLayout {
   static constexpr int CS = pad4(D + 3);  // u[D], U2, P, lnP
-  static constexpr int CH = 4;            // column chunk of the online log-sum-exp
+  static constexpr int CH = QEM_FWD_CH;   // column chunk of the online log-sum-exp (one max per chunk)
   __host__ __device__ static int kpad(int K) { return (K + CH - 1) / CH * CH; }
   __host__ __device__ static size_t stage_bytes(int K) { return (size_t)kpad(K) * CS * sizeof(float); }
   // k_forward: two stages + two mbarriers
