@@ -111,6 +111,12 @@ typedef struct {
   double new_weight; /* w in (0,1]: m_t = (1-w) m_{t-1} + w m_one  (history lambda = 1-w) */
   double schedule_p; /* if > 0: lambda_t = 1 - t^{-p} (Theorem 1) overrides new_weight   */
   double var_floor;  /* Gaussian M-step variance floor (> 0), default 1e-8              */
+  int32_t fresh_denominator; /* 1: fresh-sample denominator (R28):
+                                the one-step moments are sum_k r_k(z) m(z^k) / Pe(z_new) for an
+                                independent draw z_new, i.e. qem_mstep scales the self-normalised
+                                ones by Pe(z)/Pe(z_new) = exp(log_pe - log_pe_fresh).  Needs
+                                bufs.log_pe_fresh; two-level family only.  0 (default): Eq. 7a. */
+  int32_t reserved;
 } qem_opts;
 
 typedef struct {
@@ -136,6 +142,8 @@ typedef struct {
   int64_t trace_len;
   double* plate_sum;   /* [K+1] optional caller-owned plate-sum / all-reduce buffer;
                           NULL = the context's own (see qem_reduce_buffer)          */
+  double* log_pe_fresh; /* [1] log Pe(z_new) of the fresh-denominator pass (qem_estep_evidence);
+                          required when opts.fresh_denominator, else may be NULL    */
 } qem_buffers;
 
 typedef struct qem_ctx qem_ctx;
@@ -185,17 +193,29 @@ qem_status qem_reduce_buffer(qem_ctx* ctx, double** d_buf, int64_t* count);
    moments. */
 qem_status qem_estep_backward(qem_ctx* ctx, void* stream);
 
+/* Fresh-denominator evidence pass: forward + root evidence on the
+   currently bound samples (drawn independently of the E-step's: Philox with bit 23 of `iter`
+   set, or a second host eps draw), log Pe(z_new) -> bufs.log_pe_fresh.  Weights, moments and
+   bufs.log_pe are not touched.  world == 1; sharded runs call qem_estep_forward, all-reduce
+   the reduce buffer, then qem_evidence_root.  Two-level family only (else QEM_UNSUPPORTED). */
+qem_status qem_estep_evidence(qem_ctx* ctx, void* stream);
+qem_status qem_evidence_root(qem_ctx* ctx, void* stream);
+
 /* K5 -- EMA over mean parameters + Gaussian M-step for every bound level
    (Alg. 1 lines 3 and 6; Eq. 9): with lambda = history weight of iteration t,
      m1 <- lam m1 + (1-lam) m1_new
      v  <- lam v + (1-lam) v_new + lam (1-lam) (m1_old - m1_new)^2
    (exactly the EMA of (E z, E z^2), R19), then
-     q_mean = (float) m1,  q_var = (float) max(v, var_floor).            */
+     q_mean = (float) m1,  q_var = (float) max(v, var_floor).
+   With opts.fresh_denominator the one-step mean parameters (m1_new, v_new + m1_new^2) are
+   first multiplied by exp(log_pe - log_pe_fresh) (read on the device).                */
 qem_status qem_mstep(qem_ctx* ctx, int32_t t, void* stream);
 
 /* K6 -- T QEM iterations t = t0 .. t0+T-1 of sample (Philox, seed) ->
    E-step -> M-step, replayed from one captured CUDA graph (world == 1), or
-   issued eagerly when `use_graph` == 0.  log Pe of iteration t0+j goes to
+   issued eagerly when `use_graph` == 0.  With opts.fresh_denominator each
+   iteration first samples z_new (Philox iteration word t | 2^23) and runs the
+   evidence pass.  log Pe of iteration t0+j goes to
    bufs.trace[j] when bufs.trace != NULL. */
 qem_status qem_iterate(qem_ctx* ctx, int32_t t0, int32_t T, uint64_t seed, int32_t use_graph,
                        void* stream);

@@ -205,23 +205,36 @@ def initial_state(m):
     return [(np.zeros(n * dd), np.ones(n * dd)) for n, dd in synth.latent_shapes(m)]
 
 
-def qem_step(m, state, q_t, eps_t, t, new_weight=0.3, p=0.0, floor=1e-8, data=None):
+def qem_step(m, state, q_t, eps_t, t, new_weight=0.3, p=0.0, floor=1e-8, data=None, eps_new=None):
     """One iteration t of Algorithm 1 after its M-step.
 
     state: per level (m1, m2) = m_{t-1}; q_t: per level (mean f32, var f32) =
     set_exp_family_params(m_{t-1}); eps_t: per level [instances*dims][K] fp32.
-    Returns dict(z, est (E-step dict), state (m_t), q_next (Q_{t+1}), clamps)."""
+    eps_new (optional): a second, independent draw for the fresh-sample denominator
+    (PAPER.md:274-275): the one-step moments become sum_k r_k(z) m(z^k) / Pe(z_new), i.e.
+    the self-normalised moments times Pe(z) / Pe(z_new) (R28).
+    Returns dict(z, est (E-step dict), state (m_t), q_next (Q_{t+1}), clamps, ratio)."""
     z = [sample(qm, qv, e) for (qm, qv), e in zip(q_t, eps_t)]
     est = estep(m, z, q_t, data)
+    ratio, lp_new = 1.0, None
+    if eps_new is not None:
+        z_new = [sample(qm, qv, e) for (qm, qv), e in zip(q_t, eps_new)]
+        lp_new = estep(m, z_new, q_t, data)["log_pe"]
+        ratio = float(np.exp(est["log_pe"] - lp_new))
     lm = lam(t, new_weight, p)
     new_state, q_next, clamps = [], [], 0
     for (m1, m2), a, b in zip(state, est["m1"], est["m2"]):
-        s = ema(lm, m1, m2, a, b)
+        s = ema(lm, m1, m2, ratio * a, ratio * b)
         new_state.append(s)
         qm, qv, c = mstep(s[0], s[1], floor)
         q_next.append((qm, qv))
         clamps += c
-    return dict(z=z, est=est, state=new_state, q_next=q_next, clamps=clamps, lam=lm)
+    return dict(z=z, est=est, state=new_state, q_next=q_next, clamps=clamps, lam=lm, ratio=ratio,
+                log_pe_new=lp_new)
+
+
+# Offset of the seed of the fresh-sample (denominator) draw in host-eps mode.
+FRESH_SEED_OFFSET = 7919
 
 
 def eps_for_iteration(m, t, seed):
@@ -231,13 +244,15 @@ def eps_for_iteration(m, t, seed):
             for lvl, (n, dd) in enumerate(synth.latent_shapes(m))]
 
 
-def run_qem(m, data, T, seed, new_weight=0.3, p=0.0, floor=1e-8):
-    """Free-running QEM for T iterations from m_0 (Algorithm 1). Returns the per-step dicts."""
+def run_qem(m, data, T, seed, new_weight=0.3, p=0.0, floor=1e-8, fresh=False):
+    """Free-running QEM for T iterations from m_0 (Algorithm 1). Returns the per-step dicts.
+    fresh: use the fresh-sample denominator with eps from seed + FRESH_SEED_OFFSET."""
     state = initial_state(m)
     q = [mstep(a, b, floor)[:2] for a, b in state]
     out = []
     for t in range(1, T + 1):
-        r = qem_step(m, state, q, eps_for_iteration(m, t, seed), t, new_weight, p, floor, data)
+        eps_new = eps_for_iteration(m, t, seed + FRESH_SEED_OFFSET) if fresh else None
+        r = qem_step(m, state, q, eps_for_iteration(m, t, seed), t, new_weight, p, floor, data, eps_new=eps_new)
         out.append(r)
         state, q = r["state"], r["q_next"]
     return out

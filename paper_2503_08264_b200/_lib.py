@@ -18,7 +18,8 @@ FLAG_DEGENERATE, FLAG_NAN, FLAG_CLAMP = 1, 2, 4
 # Every symbol include/qem.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "qem_model_validate", "qem_shard_range", "qem_create", "qem_destroy", "qem_bind", "qem_sample_q",
-    "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_mstep", "qem_iterate",
+    "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_estep_evidence",
+    "qem_evidence_root", "qem_mstep", "qem_iterate",
     "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_pair_path", "qem_copy_messages", "qem_status_str", "qem_last_error",
     "qem_version",
 ]
@@ -33,7 +34,8 @@ class ModelDesc(ctypes.Structure):
 
 
 class Opts(ctypes.Structure):
-    _fields_ = [("new_weight", ctypes.c_double), ("schedule_p", ctypes.c_double), ("var_floor", ctypes.c_double)]
+    _fields_ = [("new_weight", ctypes.c_double), ("schedule_p", ctypes.c_double), ("var_floor", ctypes.c_double),
+                ("fresh_denominator", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class Level(ctypes.Structure):
@@ -45,7 +47,7 @@ class Level(ctypes.Structure):
 class Buffers(ctypes.Structure):
     _fields_ = [("level", Level * 3), ("x", ctypes.c_void_p), ("y", ctypes.c_void_p),
                 ("log_pe", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_len", ctypes.c_int64),
-                ("plate_sum", ctypes.c_void_p)]
+                ("plate_sum", ctypes.c_void_p), ("log_pe_fresh", ctypes.c_void_p)]
 
 
 class QemError(RuntimeError):
@@ -75,6 +77,8 @@ def lib() -> ctypes.CDLL:
         L.qem_estep_backward.argtypes = [vp, vp]
         L.qem_reduce_buffer.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i64)]
         L.qem_mstep.argtypes = [vp, i32, vp]
+        L.qem_estep_evidence.argtypes = [vp, vp]
+        L.qem_evidence_root.argtypes = [vp, vp]
         L.qem_iterate.argtypes = [vp, i32, i32, u64, i32, vp]
         L.qem_read_flags.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(i64)]
         L.qem_read_mode_hist.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
@@ -91,7 +95,8 @@ def lib() -> ctypes.CDLL:
         L.qem_version.restype = ctypes.c_char_p
         for name in ["qem_model_validate", "qem_shard_range", "qem_create", "qem_bind", "qem_sample_q", "qem_estep",
                      "qem_estep_forward", "qem_estep_backward", "qem_reduce_buffer", "qem_mstep", "qem_iterate",
-                     "qem_read_flags", "qem_read_mode_hist", "qem_copy_messages"]:
+                     "qem_read_flags", "qem_read_mode_hist", "qem_copy_messages", "qem_estep_evidence",
+                     "qem_evidence_root"]:
             getattr(L, name).restype = i32
         _lib = L
     return _lib

@@ -178,6 +178,10 @@ qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t 
     delete c;
     return fail(QEM_INVALID_ARGUMENT, "bad options (need 0<new_weight<=1, 0<=schedule_p<1, var_floor>0)");
   }
+  if (c->opts.fresh_denominator && desc->family != QEM_FAMILY_TWO_LEVEL) {
+    delete c;
+    return fail(QEM_UNSUPPORTED, "fresh denominator: two-level family only");
+  }
   c->g_begin = group_begin;
   c->g_end = group_end;
   c->n_local = group_end - group_begin;
@@ -218,6 +222,8 @@ qem_status qem_bind(qem_ctx* c, const qem_buffers* b) {
   if (!b->x || !b->log_pe) return fail(QEM_INVALID_ARGUMENT, "null observation or log_pe buffer");
   if ((c->desc.obs_kind == QEM_OBS_BERNOULLI_LOGIT || c->desc.obs_kind == QEM_OBS_POISSON_LOG) && !b->y)
     return fail(QEM_INVALID_ARGUMENT, "null label buffer y");
+  if (c->opts.fresh_denominator && !b->log_pe_fresh)
+    return fail(QEM_INVALID_ARGUMENT, "opts.fresh_denominator needs bufs.log_pe_fresh");
   c->bufs = *b;
   c->bound = 1;
   if (c->graph_valid) {
@@ -271,6 +277,36 @@ qem_status qem_estep(qem_ctx* c, void* stream) {
   return s;
 }
 
+static cudaError_t evidence_root(qem_ctx* c, cudaStream_t st) {
+  c->evidence_only = 1;
+  const cudaError_t e = qem::tl_backward(c, st);
+  c->evidence_only = 0;
+  return e;
+}
+
+qem_status qem_evidence_root(qem_ctx* c, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "fresh denominator: two-level family only");
+  if (!c->bufs.log_pe_fresh) return fail(QEM_INVALID_ARGUMENT, "bufs.log_pe_fresh is NULL");
+  c->launches = 0;
+  const cudaError_t e = evidence_root(c, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_evidence_root");
+}
+
+qem_status qem_estep_evidence(qem_ctx* c, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "fresh denominator: two-level family only");
+  if (!c->bufs.log_pe_fresh) return fail(QEM_INVALID_ARGUMENT, "bufs.log_pe_fresh is NULL");
+  s = qem_estep_forward(c, stream);
+  if (s) return s;
+  const int64_t l = c->launches;
+  s = qem_evidence_root(c, stream);
+  c->launches += l;
+  return s;
+}
+
 qem_status qem_mstep(qem_ctx* c, int32_t t, void* stream) {
   qem_status s = need_bound(c);
   if (s) return s;
@@ -286,7 +322,16 @@ static cudaError_t iterate_body(qem_ctx* c, uint64_t seed, cudaStream_t st) {
     ~Guard() { c->in_iterate = 0; }
   } guard{c};
   c->in_iterate = 1;
-  cudaError_t e = qem::launch_sample(c, seed, 0, nullptr, st);
+  cudaError_t e;
+  if (c->opts.fresh_denominator) {  // z_new from the independent Philox stream, its evidence first
+    e = qem::launch_sample(c, seed, 0, nullptr, st, 0x800000u);
+    if (e != cudaSuccess) return e;
+    e = qem::tl_forward(c, st);
+    if (e != cudaSuccess) return e;
+    e = evidence_root(c, st);
+    if (e != cudaSuccess) return e;
+  }
+  e = qem::launch_sample(c, seed, 0, nullptr, st);
   if (e != cudaSuccess) return e;
   e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_forward(c, st) : qem::th_forward(c, st);
   if (e != cudaSuccess) return e;

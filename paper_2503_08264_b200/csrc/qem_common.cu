@@ -42,6 +42,7 @@ struct SampleArgs {
   int64_t total_quads;  // < 2^31 (checked at launch)
   uint2 key;
   int t_host;
+  uint32_t iter_or;  // OR-ed into the iteration word (bit 23: the fresh-denominator stream)
   const int32_t* d_iter;
 };
 
@@ -113,7 +114,8 @@ __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
     const int dim = (int)(row32 - inst * (uint32_t)s.dims);
     const uint32_t ginst = (uint32_t)(inst + s.inst_offset);
     const uint4 o = philox4x32_10(
-        make_uint4((uint32_t)(k0 >> 2), (uint32_t)dim, ginst, ((uint32_t)s.level << 24) | ((uint32_t)t & 0xffffffu)),
+        make_uint4((uint32_t)(k0 >> 2), (uint32_t)dim, ginst,
+                   ((uint32_t)s.level << 24) | (((uint32_t)t | a.iter_or) & 0xffffffu)),
         a.key);
     // Box-Muller on u = ((x >> 9) + 0.5) * 2^-23: radius and angle evaluated
     // from the integer bits (bm_radius, bm_sincos2pi: ~3x fewer instructions than
@@ -138,8 +140,10 @@ __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
   }
 }
 
-cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps, cudaStream_t st) {
+cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps, cudaStream_t st,
+                          uint32_t iter_or) {
   SampleArgs a{};
+  a.iter_or = iter_or;
   const int K = c->desc.K;
   a.K = K;
   a.quads_per_row = (K + 3) / 4;
@@ -208,6 +212,8 @@ struct MstepArgs {
   int64_t total;
   double new_weight, p, floor_v;
   int t_host;
+  const double* log_pe;        // fresh denominator: ratio = exp(log_pe - log_pe_fresh)
+  const double* log_pe_fresh;  // nullptr: self-normalised moments (Eq. 7a)
   Counters* cnt;
 };
 
@@ -225,7 +231,15 @@ __global__ void __launch_bounds__(256) k_mstep(MstepArgs a) {
       if (l < a.nlev && e >= a.lv[l].begin) L = l;
     const MstepLevel& s = a.lv[L];
     const int64_t j = e - s.begin;
-    const double m1 = s.m1[j], v = s.v[j], a1 = s.m1n[j], av = s.vn[j];
+    const double m1 = s.m1[j], v = s.v[j];
+    double a1 = s.m1n[j], av = s.vn[j];
+    if (a.log_pe_fresh) {
+      // fresh-sample denominator: mean parameters (a1, av + a1^2) times
+      // r = Pe(z)/Pe(z_new); centred: a1' = r a1, av' = r av + r (1 - r) a1^2
+      const double r = exp(*a.log_pe - *a.log_pe_fresh);
+      av = r * av + r * (1.0 - r) * a1 * a1;
+      a1 = r * a1;
+    }
     const double d = m1 - a1;
     const double nm1 = lam * m1 + (1.0 - lam) * a1;
     const double nv = lam * v + (1.0 - lam) * av + lam * (1.0 - lam) * d * d;
@@ -281,6 +295,10 @@ cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t st) {
   a.floor_v = c->opts.var_floor;
   a.t_host = t;
   a.cnt = c->cnt;
+  if (c->opts.fresh_denominator) {
+    a.log_pe = c->bufs.log_pe;
+    a.log_pe_fresh = c->bufs.log_pe_fresh;
+  }
   const int threads = 256;
   const int64_t blocks = (tot + threads - 1) / threads;
   k_mstep<<<(unsigned)(blocks > 0 ? blocks : 1), threads, 0, st>>>(a);

@@ -90,6 +90,7 @@ struct qem_ctx {
   int graph_valid;
   int in_iterate;
   int tc;  // d=16 tensor-core pair kernels in use
+  int evidence_only;  // the next tl_backward runs the root evidence only (fresh-denominator pass)
   void* ev[4];  // optional caller events around the pair-tile kernels (fwd start/end, bwd start/end)
   uint64_t graph_seed_;
   int64_t graph_launches_;
@@ -107,6 +108,6 @@ cudaError_t th_forward(qem_ctx* c, cudaStream_t s);
 cudaError_t th_backward(qem_ctx* c, cudaStream_t s);
 // common (qem_common.cu)
 cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps,
-                          cudaStream_t s);
+                          cudaStream_t s, uint32_t iter_or = 0);
 cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t s);
 }  // namespace qem

@@ -147,6 +147,7 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
         s_v[0] = s_v[q];
         s_i[0] = s_i[q];
       }
+    if (s_i[0] >= K) s_i[0] = 0;  // all weights NaN (degenerate evidence, flagged by k_root): stay in range
     const int ks = s_i[0];
     RefInfo* ref = a.ws.ref;
     ref->k_star = ks;

@@ -47,6 +47,7 @@ struct TLArgs {
   int64_t trace_len;
   int t_host;
   int tc;        // tensor-core pair kernels in use (d = 16)
+  int evidence_only;  // k_root: log Pe only (fresh-denominator pass)
   float thr[5];  // forward tile-mode bounds for expm1 degrees 3/4/5/7/9
   TwoLevelWs ws;
   Counters* cnt;
@@ -250,6 +251,14 @@ __global__ void __launch_bounds__(1024) k_root(TLArgs a) {
   const double S = block_sum(s, scratch);
   const double L = M + log(S);
   const bool degenerate = !(L > -CUDART_INF) || isnan(L);
+  if (a.evidence_only) {  // fresh-denominator pass: log Pe(z_new) only
+    if (tid == 0) {
+      *a.log_pe = a.ws.red[K] + L - log((double)K);
+      if (degenerate) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_DEGENERATE);
+      if (isnan(L)) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+    }
+    return;
+  }
   for (int k = tid; k < K; k += blockDim.x) {
     const double w = exp(wsh[k] - L);
     wsh[k] = w;
@@ -525,6 +534,11 @@ static TLArgs make_args(qem_ctx* c) {
   a.trace_len = c->bufs.trace_len;
   a.t_host = 0;
   a.tc = c->tc;
+  a.evidence_only = c->evidence_only;
+  if (c->evidence_only) {
+    a.log_pe = c->bufs.log_pe_fresh;  // log Pe(z_new)
+    a.trace = nullptr;
+  }
   // |D'| bound below which the degree-n Taylor remainder |D'|^{n+1}/(n+1)!,
   // accumulated over all N groups of the plate, stays under 2e-6
   const int degs[5] = {3, 4, 5, 7, 9};
@@ -656,6 +670,10 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   k_root<D><<<1, nt, (size_t)(K + 32) * sizeof(double), st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (c->evidence_only) {  // fresh-denominator pass: the root evidence is all it needs
+    c->launches += 1;
+    return cudaSuccess;
+  }
   const int cp = pick_rp(K, D);
   const bool tc = D <= kTcD && c->tc;
   constexpr int DT = D <= kTcD ? D : 1;

@@ -49,8 +49,22 @@ class ShardedQEM:
         self.allreduce_plate_sum()
         self.b.estep_backward()
 
-    def step(self, t: int, seed: int, eps=None) -> None:
-        """Iteration t of Algorithm 1 with Q_t already set: z ~ Q_t, E-step, EMA/M-step."""
+    def evidence(self) -> None:
+        """Fresh-denominator evidence pass on the bound samples: local forward,
+        the same all-reduce, then log Pe(z_new) on every rank (no backward)."""
+        self.b.estep_forward()
+        self.allreduce_plate_sum()
+        self.b.evidence_root()
+
+    def step(self, t: int, seed: int, eps=None, eps_new=None, fresh: bool = False) -> None:
+        """Iteration t of Algorithm 1 with Q_t already set: z ~ Q_t, E-step, EMA/M-step.
+        fresh: first draw z_new (Philox stream bit 23, or eps_new) and run its evidence pass (R28)."""
+        if fresh:
+            if eps_new is None:
+                self.b.sample_q(seed=seed, iter=t | (1 << 23))
+            else:
+                self.b.sample_q(eps=eps_new)
+            self.evidence()
         if eps is None:
             self.b.sample_q(seed=seed, iter=t)
         else:

@@ -47,7 +47,7 @@ class QEM:
     """One context over LOCAL level-1 instances [group_begin, group_end)."""
 
     def __init__(self, m, *, new_weight=0.3, schedule_p=0.0, var_floor=1e-8, group_begin=0, group_end=None,
-                 device="cuda", trace_len=0):
+                 device="cuda", trace_len=0, fresh_denominator=False):
         if not torch.cuda.is_available():
             raise _lib.QemError("QEM needs a CUDA device (there is no CPU fallback)")
         self.m = m
@@ -57,7 +57,8 @@ class QEM:
         self.g_begin, self.g_end = int(group_begin), int(group_end)
         self.n_local = self.g_end - self.g_begin
         d = _desc(m)
-        o = _lib.Opts(new_weight, schedule_p, var_floor)
+        o = _lib.Opts(new_weight, schedule_p, var_floor, int(bool(fresh_denominator)), 0)
+        self.fresh = bool(fresh_denominator)
         ctx = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             check(lib().qem_create(ctypes.byref(d), ctypes.byref(o), self.g_begin, self.g_end, ctypes.byref(ctx)),
@@ -79,6 +80,7 @@ class QEM:
                       m1=torch.zeros(nl, **f64), v=torch.zeros(nl, **f64))
             self.levels.append(lv)
         self.log_pe = torch.zeros(1, **f64)
+        self.log_pe_fresh = torch.zeros(1, **f64)
         self.plate_sum = torch.zeros(K + 1, **f64)
         self.trace = torch.zeros(max(trace_len, 1), **f64)
         self.x = self.y = None
@@ -111,6 +113,7 @@ class QEM:
         b.trace = self.trace.data_ptr()
         b.trace_len = self.trace.numel()
         b.plate_sum = self.plate_sum.data_ptr()
+        b.log_pe_fresh = self.log_pe_fresh.data_ptr()
         check(lib().qem_bind(self.ctx, ctypes.byref(b)), "qem_bind")
         self._bound = True
 
@@ -165,6 +168,14 @@ class QEM:
 
     def estep_backward(self, stream=None) -> None:
         check(lib().qem_estep_backward(self.ctx, _stream(stream)), "qem_estep_backward")
+
+    def estep_evidence(self, stream=None) -> None:
+        """Fresh-denominator pass: log Pe of the bound samples -> log_pe_fresh."""
+        check(lib().qem_estep_evidence(self.ctx, _stream(stream)), "qem_estep_evidence")
+
+    def evidence_root(self, stream=None) -> None:
+        """Phase 2 of the sharded evidence pass (after estep_forward + the all-reduce)."""
+        check(lib().qem_evidence_root(self.ctx, _stream(stream)), "qem_evidence_root")
 
     def mstep(self, t: int, stream=None) -> None:
         check(lib().qem_mstep(self.ctx, t, _stream(stream)), "qem_mstep")

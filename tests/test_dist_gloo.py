@@ -60,6 +60,10 @@ class OracleShardBackend:
         self.w_root = torch.from_numpy(np.exp(a - L))
         self.w, self.m1, self.m2 = orc.backward2(self.m, self.z, self.q, self.data, self.w_root.numpy(), self.g)
 
+    def evidence_root(self):
+        a = self.f_root + self.plate_sum[: self.m.K].numpy()
+        self.log_pe_fresh = logsumexp(a) - np.log(self.m.K)
+
     def mstep(self, t):
         pass
 
@@ -116,6 +120,50 @@ def test_two_rank_sharded_estep_matches_single_process(cid, n, K):
         np.testing.assert_allclose(m1, ref["m1"][1][b * m.d:e * m.d], rtol=1e-11, atol=1e-14)
         np.testing.assert_allclose(m2, ref["m2"][1][b * m.d:e * m.d], rtol=1e-11, atol=1e-14)
     assert covered[0][0] == 0 and covered[-1][1] == n and covered[0][1] == covered[1][0]
+
+
+def _worker_evidence(rank, world, port, n, K, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from helpers import make_case
+        from paper_2503_08264_b200 import dist as qdist, synth
+        m = synth.config(4, n=n, K=K)
+        data, q, eps, z_new = make_case(m, eps_seed=99)
+        b, e = qdist.shard_range(m.n, rank, world)
+        be = OracleShardBackend(m, data, q, z_new, b, e)
+        qdist.ShardedQEM(be).evidence()
+        out_q.put((rank, be.log_pe_fresh))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_evidence_pass():
+    """Fresh-denominator evidence pass across 2 ranks: local forward, the same
+    all-reduce, log Pe(z_new) on every rank equal to the single-process oracle's."""
+    from helpers import make_case
+    from oracle import oracle as orc
+    from paper_2503_08264_b200 import synth
+    world, n, K = 2, 23, 16
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_evidence, args=(r, world, port, n, K, q_out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q_out.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = synth.config(4, n=n, K=K)
+    data, q, eps, z_new = make_case(m, eps_seed=99)
+    ref = orc.estep(m, z_new, q, data)["log_pe"]
+    for rank, lp in res:
+        assert abs(lp - ref) <= 1e-12 * abs(ref), (rank, lp, ref)
 
 
 def test_python_and_c_shard_ranges_agree():
