@@ -292,11 +292,15 @@ def run_gpu(args):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce)
+    tc = g.pair_path() == 1
+    fresh = None
+    if world == 1 and not args.no_variants:
+        g.close()  # free the first context's workspace before the variant's
+        fresh = run_fresh_variant(args, m, data, dev, seed)
 
     # ----------------------------------------------------------- roofline
     local_pairs = (ge - gb) * m.K * m.K
     dom, dom_ms = ("forward", fwd_ms) if fwd_ms >= bwd_ms else ("backward", bwd_ms)
-    tc = g.pair_path() == 1
     ceil = pair_ceiling(m.d, tc)
     achieved = local_pairs / (dom_ms * 1e-3)
     per_pair = ({"exp": 1, "fma_pipe": 2, "tensor_bf16_flops": 12 * m.d} if tc else {"exp": 1, "fma_pipe": m.d + 2})
@@ -353,6 +357,7 @@ def run_gpu(args):
         "gpu_launches": n_launched,
         "clocks": clk,
         "flags": {"device_flags": flags, "var_clamps": clamps},
+        "variants": {"fresh_denominator": fresh},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -411,6 +416,48 @@ def run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce):
             "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world}
 
 
+def run_fresh_variant(args, m, data, dev, seed):
+    """NEXT row f2: the same QEM iteration with the fresh-sample denominator
+     -- an independent draw z_new, its forward + root evidence, then the E-step
+    and the ratio-scaled M-step.  Device-timed like the main line, W warm-up + K steps."""
+    import torch
+    from paper_2503_08264_b200.qem import QEM
+    g = QEM(m, device=dev, fresh_denominator=True)
+    g.set_data(data)
+    stream = torch.cuda.current_stream()
+    # every timed step restarts from the same Q_t (device copies): the free-running estimator's
+    # ratio exp(log Pe(z) - log Pe(z_new)) overflows within a few iterations at this scale
+    # (DESIGN.md R28), and NaN states would not time the real work
+    q0 = [(lv["q_mean"].clone(), lv["q_var"].clone()) for lv in g.levels]
+
+    def one(t):
+        for lv, (qm, qv) in zip(g.levels, q0):
+            lv["q_mean"].copy_(qm)
+            lv["q_var"].copy_(qv)
+        g.sample_q(seed=seed, iter=t | (1 << 23))
+        g.estep_evidence()
+        g.sample_q(seed=seed, iter=t)
+        g.estep()
+        g.mstep(t)
+
+    t = 1
+    for _ in range(args.warmup):
+        one(t)
+        t += 1
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record(stream)
+    for _ in range(args.steps):
+        one(t)
+        t += 1
+    en.record(stream)
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / args.steps
+    g.close()
+    return {"ms_per_step": ms, "value": m.pairs / (ms * 1e-3), "unit": "factor-pairs/s (E-step pairs; the evidence "
+            "pass's forward pairs are extra work)", "qem_iters_per_s": 1e3 / ms}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
     world, rank, _ = dist_env()
@@ -454,6 +501,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
         bv = s_val[w];
         bi = s_idx[w];
       }
+    if (bi >= K) bi = 0;  // every distance NaN (degenerate Q, flagged by the M-step): stay in range
     RefInfo* ref = a.ws.ref;
     ref->k_ref = bi;
     for (int r = 0; r < D; ++r) ref->mu_ref[r] = a.z_root[r * K + bi];
