@@ -293,10 +293,11 @@ def run_gpu(args):
     if not args.no_e2e:
         e2e = run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce)
     tc = g.pair_path() == 1
-    fresh = None
+    fresh = mfam = None
     if world == 1 and not args.no_variants:
         g.close()  # free the first context's workspace before the variant's
         fresh = run_fresh_variant(args, m, data, dev, seed)
+        mfam = run_mstep_family_variant(dev)
 
     # ----------------------------------------------------------- roofline
     local_pairs = (ge - gb) * m.K * m.K
@@ -357,7 +358,7 @@ def run_gpu(args):
         "gpu_launches": n_launched,
         "clocks": clk,
         "flags": {"device_flags": flags, "var_clamps": clamps},
-        "variants": {"fresh_denominator": fresh},
+        "variants": {"fresh_denominator": fresh, "mstep_family": mfam},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -456,6 +457,33 @@ def run_fresh_variant(args, m, data, dev, seed):
     g.close()
     return {"ms_per_step": ms, "value": m.pairs / (ms * 1e-3), "unit": "factor-pairs/s (E-step pairs; the evidence "
             "pass's forward pairs are extra work)", "qem_iters_per_s": 1e3 / ms}
+
+
+def run_mstep_family_variant(dev, n=1_000_000, reps=10):
+    """NEXT row f1: EMA + M-step of the non-Gaussian Q families on 1e6 latent
+    instances each (Gamma / Beta Newton iterations in fp64, one thread per instance)."""
+    import torch
+    from paper_2503_08264_b200.qem import BETA, GAMMA, mstep_family
+    g = torch.Generator(device=dev).manual_seed(0)
+    out = {}
+    for name, fam in (("gamma", GAMMA), ("beta", BETA)):
+        a = torch.exp(torch.rand(n, 2, generator=g, device=dev, dtype=torch.float64) * 4 - 2)
+        if fam == GAMMA:  # mean parameters (k/th, psi(k) - ln th) of random (k, th)
+            m = torch.stack([a[:, 0] / a[:, 1], torch.special.digamma(a[:, 0]) - torch.log(a[:, 1])], 1)
+        else:
+            s = torch.special.digamma(a.sum(1))
+            m = torch.stack([torch.special.digamma(a[:, 0]) - s, torch.special.digamma(a[:, 1]) - s], 1)
+        ema = m.clone()
+        mstep_family(fam, 0.7, m, ema)  # warm-up
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for _ in range(reps):
+            mstep_family(fam, 0.7, m, ema)
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / reps
+        out[name] = {"instances": n, "ms": ms, "ns_per_instance": ms * 1e6 / n}
+    return out
 
 
 def run_reference(args):

@@ -80,6 +80,15 @@ typedef int32_t qem_status;
 #define QEM_FLAG_NAN 2u        /* a NaN reached a weight or moment          */
 #define QEM_FLAG_CLAMP 4u      /* an M-step variance hit the floor (R8)     */
 
+/* Q families of qem_mstep_family (NEXT row f1) and its per-instance status. */
+#define QEM_QFAMILY_GAMMA 1       /* mean params (E z, E ln z)          -> (shape k, rate th)   */
+#define QEM_QFAMILY_BETA 2        /* mean params (E ln z, E ln(1-z))    -> (a, b)               */
+#define QEM_QFAMILY_BERNOULLI 3   /* mean param  E z                    -> p                    */
+#define QEM_QFAMILY_CATEGORICAL 4 /* mean params E onehot(z) [C]        -> p [C] (normalised)   */
+#define QEM_EXPFAM_OK 0
+#define QEM_EXPFAM_INFEASIBLE 1      /* moments outside the family's mean-parameter space        */
+#define QEM_EXPFAM_NO_CONVERGENCE 2  /* the Newton iteration did not reach its tolerance          */
+
 #define QEM_MAX_K 1024
 #define QEM_MAX_D 32
 
@@ -210,6 +219,20 @@ qem_status qem_evidence_root(qem_ctx* ctx, void* stream);
    With opts.fresh_denominator the one-step mean parameters (m1_new, v_new + m1_new^2) are
    first multiplied by exp(log_pe - log_pe_fresh) (read on the device).                */
 qem_status qem_mstep(qem_ctx* ctx, int32_t t, void* stream);
+
+/* EMA over mean parameters + M-step for non-Gaussian Q families (Alg. 1 lines 3, 6; Eq. 9;
+   PAPER.md:218 "a Beta's parameters are recovered from expectations of log transformations",
+   PAPER.md:247).  Context-free, stream-ordered, one device thread per latent instance, fp64.
+   S = 2 (Gamma, Beta), 1 (Bernoulli), C (Categorical) mean parameters per instance:
+     d_m_new  [n][S]  one-step mean parameters (input)
+     d_m_ema  [n][S]  EMA state, updated in place: m <- lam m + (1 - lam) m_new
+     d_params [n][S]  conventional parameters of the updated state (output): Gamma (k, th) by
+                      Newton on psi(k) - ln k = m2 - ln m1, th = k/m1; Beta (a, b) by damped
+                      2-d Newton in (ln a, ln b); Bernoulli p; Categorical p normalised
+     d_status [n]     QEM_EXPFAM_* per instance (nullable)
+   Errors: QEM_INVALID_ARGUMENT for a bad family / n < 0 / C < 1 / null arrays. */
+qem_status qem_mstep_family(int32_t family, int64_t n, int32_t C, double lam, const double* d_m_new,
+                            double* d_m_ema, double* d_params, int32_t* d_status, void* stream);
 
 /* K6 -- T QEM iterations t = t0 .. t0+T-1 of sample (Philox, seed) ->
    E-step -> M-step, replayed from one captured CUDA graph (world == 1), or

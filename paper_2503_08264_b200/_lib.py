@@ -19,7 +19,7 @@ FLAG_DEGENERATE, FLAG_NAN, FLAG_CLAMP = 1, 2, 4
 EXPORTS = [
     "qem_model_validate", "qem_shard_range", "qem_create", "qem_destroy", "qem_bind", "qem_sample_q",
     "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_estep_evidence",
-    "qem_evidence_root", "qem_mstep", "qem_iterate",
+    "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_iterate",
     "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_pair_path", "qem_copy_messages", "qem_status_str", "qem_last_error",
     "qem_version",
 ]
@@ -77,6 +77,8 @@ def lib() -> ctypes.CDLL:
         L.qem_estep_backward.argtypes = [vp, vp]
         L.qem_reduce_buffer.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i64)]
         L.qem_mstep.argtypes = [vp, i32, vp]
+        L.qem_mstep_family.argtypes = [i32, i64, i32, ctypes.c_double, vp, vp, vp, vp, vp]
+        L.qem_mstep_family.restype = i32
         L.qem_estep_evidence.argtypes = [vp, vp]
         L.qem_evidence_root.argtypes = [vp, vp]
         L.qem_iterate.argtypes = [vp, i32, i32, u64, i32, vp]

@@ -110,4 +110,7 @@ cudaError_t th_backward(qem_ctx* c, cudaStream_t s);
 cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps,
                           cudaStream_t s, uint32_t iter_or = 0);
 cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t s);
+// non-Gaussian Q families (qem_expfam.cu)
+cudaError_t launch_mstep_family(int family, int64_t n, int C, double lam, const double* m_new, double* m_ema,
+                                double* params, int32_t* status, cudaStream_t st);
 }  // namespace qem

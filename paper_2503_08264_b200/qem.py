@@ -32,6 +32,22 @@ def model_validate(m) -> Optional[str]:
     return None if st == _lib.OK else buf.value.decode()
 
 
+GAMMA, BETA, BERNOULLI, CATEGORICAL = 1, 2, 3, 4
+
+
+def mstep_family(family: int, lam: float, m_new: torch.Tensor, m_ema: torch.Tensor, C: int = 1, stream=None):
+    """EMA over mean parameters + M-step of a non-Gaussian Q family (qem_mstep_family) on device
+    tensors: m_new, m_ema float64 [n][S] (m_ema updated in place).  Returns (params [n][S], status [n])."""
+    assert m_new.dtype == torch.float64 and m_ema.dtype == torch.float64 and m_new.is_cuda
+    n = m_new.shape[0]
+    params = torch.empty_like(m_ema)
+    status = torch.empty(n, dtype=torch.int32, device=m_new.device)
+    check(lib().qem_mstep_family(int(family), n, int(C), float(lam), ctypes.c_void_p(m_new.data_ptr()),
+                                 ctypes.c_void_p(m_ema.data_ptr()), ctypes.c_void_p(params.data_ptr()),
+                                 ctypes.c_void_p(status.data_ptr()), _stream(stream)), "qem_mstep_family")
+    return params, status
+
+
 def shard_range(n: int, rank: int, world: int):
     b, e = ctypes.c_int64(), ctypes.c_int64()
     check(lib().qem_shard_range(n, rank, world, ctypes.byref(b), ctypes.byref(e)), "qem_shard_range")
