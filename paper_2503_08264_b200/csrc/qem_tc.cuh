@@ -201,15 +201,30 @@ __global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
 // One warp per group.  For column k': A_i(k') (fp64), t_i(k') = B(k_ref,k') + A_i(k'),
 // c_i = lse t - log K, P = softmax t; the group's tile mode from the bound on
 // |D'|; the column operand and {P, ln P}.
-// softplus(eta) = max(eta, 0) + log1p(e^-|eta|) on the SFU: v = 2^(-|eta| log2e), u = 1 + v (rounded),
-// log1p(v) = ln2 lg2(u) + (v - (u - 1)) / u  (the second term restores the rounding of 1 + v).
-// Absolute error <= ~1.5e-7 per observation (lg2.approx; R26).
-__device__ __forceinline__ float softplus_mufu(float eta) {
-  const float v = ex2(-fabsf(eta) * kLog2e);
-  const float u = 1.f + v;
-  float l2;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u));
-  return fmaxf(eta, 0.f) + fmaf(l2, 0.69314718055994531f, __fdividef(v - (u - 1.f), u));
+// softplus(eta) = max(eta, 0) + log1p(e^-|eta|): v = 2^(-|eta| log2e) on the SFU, log1p(v) by a
+// polynomial on the FMA pipe; absolute error <= ~1.5e-7 per observation (R26).
+
+// log1p(v), v in [0, 1], two at a time on the FMA pipe: v p(v) with p of degree 8 (near-minimax
+// for the absolute error, 5e-9; <= 1.4e-7 evaluated in fp32)
+__device__ __forceinline__ float2 log1p01_poly2(float2 v) {
+  float2 p = f2(3.929332364e-03f);
+  p = fma2(p, v, f2(-2.385043912e-02f));
+  p = fma2(p, v, f2(6.807538122e-02f));
+  p = fma2(p, v, f2(-1.268995851e-01f));
+  p = fma2(p, v, f2(1.856928021e-01f));
+  p = fma2(p, v, f2(-2.467250526e-01f));
+  p = fma2(p, v, f2(3.328963518e-01f));
+  p = fma2(p, v, f2(-4.999709129e-01f));
+  p = fma2(p, v, f2(9.999993443e-01f));
+  return mul2(p, v);
+}
+
+// softplus of an observation pair {eta_2p, eta_2p+1} summed (the second dropped when it is the
+// zero padding of an odd J): max(eta, 0) + log1p(2^(-|eta| log2e)), one MUFU per observation
+__device__ __forceinline__ float softplus_pair(float2 eta, bool two) {
+  const float2 v = make_float2(ex2(-fabsf(eta.x) * kLog2e), two ? ex2(-fabsf(eta.y) * kLog2e) : 0.f);
+  const float2 l = log1p01_poly2(v);
+  return (fmaxf(eta.x, 0.f) + (two ? fmaxf(eta.y, 0.f) : 0.f)) + (l.x + l.y);
 }
 
 #ifndef QEM_COLPREP_MINB
@@ -217,8 +232,10 @@ __device__ __forceinline__ float softplus_mufu(float eta) {
 #endif
 struct PrepTc {
   static constexpr int WARPS = 8;
+  static constexpr int ZS_FLOATS = 2 * 2 * kTcD * 32;  // z ring: [stage][half][r][32 columns]
+  static constexpr size_t ZS_BYTES = ZS_FLOATS * 4;
   __host__ __device__ static size_t warp_bytes(int K, int J) {
-    size_t b = 3 * kTcD * 8 + 2 * kTcD * 4 + (size_t)((J + 1) / 2) * kTcD * 8;
+    size_t b = 3 * kTcD * 8 + kTcD * 4 + (size_t)((J + 1) / 2) * kTcD * 8 + ZS_BYTES;
     return (b + 15) & ~(size_t)15;
   }
   __host__ __device__ static size_t bytes(int K, int J) { return WARPS * warp_bytes(K, J); }
@@ -230,17 +247,35 @@ template <int D, int OBS>
 __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   static_assert(D <= kTcD, "tensor-core path: d <= 16");
+  static_assert(D % 2 == 0, "pairs of dims per 8-byte load");
   const int K = a.K, J = a.J, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned char* wb = smem + (size_t)wid * PrepTc::warp_bytes(K, J);
-  double* qc = reinterpret_cast<double*>(wb);                      // [3][D]: m, 1/(2v), -(ln 2pi v)/2
-  float* yx = reinterpret_cast<float*>(qc + 3 * D);                // [D]  sum_j y_j x_j (integer-valued)
-  float* mref = yx + D;                                            // [D]  mu_ref
-  float2* xp = reinterpret_cast<float2*>(mref + D);                // [(J+1)/2][D] {x_2p, x_2p+1} as 0/1
+  // per-group column quadratic (fp64): with w = z - m_i (exact in fp64),
+  //   B(k_ref, k') - ln q(z) + sum_j y_j eta_j = C_i + sum_r w_r (alpha_r w_r + beta_r),
+  //   alpha_r = 1/(2 v_r) - e_ref/2,  beta_r = (sum_j y_j x_jr) - e_ref (m_r - mu_ref,r),
+  //   C_i = bref_const - (e_ref/2) |m - mu_ref|^2 + sum_r (ln 2pi v_r)/2 + (sum_j y_j x_j) . m
+  // (the three terms of t_ref collected per dimension; oracle: separate fp64 sums)
+  double* qm = reinterpret_cast<double*>(wb);                      // [D]  m_i
+  double2* qab = reinterpret_cast<double2*>(qm + kTcD);            // [D]  {alpha_r, beta_r}
+  float* qmf = reinterpret_cast<float*>(qab + kTcD);               // [D]  m_i (fp32, exact: R22)
+  float2* xp = reinterpret_cast<float2*>(qmf + kTcD);              // [(J+1)/2][D] {x_2p, x_2p+1} as 0/1
   const int Jh = (J + 1) / 2;
-  // reference-row constants (fields read individually: the struct is large)
-  if (lane < D) mref[lane] = a.ws.ref->mu_ref[lane];
-  const volatile float* mu_ref = mref;  // re-read per column (keeps registers for the z prefetch)
+  float* zs = reinterpret_cast<float*>(xp + (size_t)Jh * kTcD);    // z ring (PrepTc::ZS_FLOATS)
+  // z of 32 column pairs {kc, kc + K/2} of group g into ring stage st: LDGSTS, so the loads of
+  // iteration it + 1 fly while iteration it computes (the column loop is latency-bound otherwise)
+  auto stage_z = [&](int64_t g, int it, int st) {
+    const float* zg = a.z + (size_t)g * D * K + it * 32;
+    float* dst = zs + st * (2 * kTcD * 32);
+#pragma unroll
+    for (int c = lane; c < 2 * D * 8; c += 32) {
+      const int h = c / (D * 8), r = (c / 8) % D, p = c % 8;
+      cp_async16(dst + (h * kTcD + r) * 32 + p * 4, zg + (size_t)r * K + h * (K / 2) + p * 4);
+    }
+    cp_async_commit();
+  };
+  const int NIT = K / 64;  // K % 256 == 0 on this path
   const double bref_const = a.ws.ref->bref_const, e_ref = a.ws.ref->e_ref;
+  const float mref_l = lane < D ? a.ws.ref->mu_ref[lane] : 0.f;
   const double logK = log((double)K);
   double gc0 = 0.0, gc1 = 0.0;
   if constexpr (OBS == QEM_OBS_GAUSS) {
@@ -248,16 +283,12 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     gc1 = 0.5 / a.obs_var;
   }
   unsigned char* colop = reinterpret_cast<unsigned char*>(a.ws.colop);
-  for (int64_t i = (int64_t)blockIdx.x * PrepTc::WARPS + wid; i < a.n_local;
-       i += (int64_t)gridDim.x * PrepTc::WARPS) {
+  const int64_t gstride = (int64_t)gridDim.x * PrepTc::WARPS;
+  if ((int64_t)blockIdx.x * PrepTc::WARPS + wid < a.n_local) stage_z((int64_t)blockIdx.x * PrepTc::WARPS + wid, 0, 0);
+  for (int64_t i = (int64_t)blockIdx.x * PrepTc::WARPS + wid; i < a.n_local; i += gstride) {
     __syncwarp();
-    if (lane < D) {
-      const double m = a.q_m[i * D + lane], v = a.q_v[i * D + lane];
-      qc[lane] = m;
-      qc[D + lane] = 0.5 / v;
-      qc[2 * D + lane] = -0.5 * (kLn2Pi + log(v));
-    }
     double sx = 0.0, sxx = 0.0;
+    int yxi = 0;  // sum_j y_j x_j,lane (integer)
     if constexpr (OBS == QEM_OBS_GAUSS) {
       // sufficient statistics of the group's observations (d = 1)
       const float* x = reinterpret_cast<const float*>(a.x) + i * J;
@@ -275,40 +306,44 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         const int jp = e / D, r = e % D, j0 = 2 * jp, j1 = 2 * jp + 1;
         xp[e] = make_float2(x[j0 * D + r] ? 1.f : 0.f, (j1 < J && x[j1 * D + r]) ? 1.f : 0.f);
       }
-      if (lane < D) {
-        int v = 0;
-        for (int j = 0; j < J; ++j) v += (y[j] && x[j * D + lane]) ? 1 : 0;
-        yx[lane] = (float)v;
-      }
+      if (lane < D)
+        for (int j = 0; j < J; ++j) yxi += (y[j] && x[j * D + lane]) ? 1 : 0;
     }
+    double ci = 0.0;
+    if (lane < D) {
+      const double m = a.q_m[i * D + lane], v = a.q_v[i * D + lane], dl = m - (double)mref_l;
+      qm[lane] = m;
+      qmf[lane] = (float)m;
+      qab[lane] = make_double2(0.5 / v - 0.5 * e_ref, (double)yxi - e_ref * dl);
+      ci = 0.5 * (kLn2Pi + log(v)) - 0.5 * e_ref * dl * dl + (double)yxi * m;
+    }
+    const double Ci = bref_const + warp_sum(ci);
     __syncwarp();
     unsigned char* cop = colop + (size_t)i * K * kTcColBytes;
-    double tmax = -CUDART_INF;
+    double tmax = -CUDART_INF, tsum = 0.0;  // the lane's online (max, sum of e^(t - max)) over its columns
     float w2max = 0.f;
     // the rest of a column once its likelihood is known: log q, the column operand, t_ref
     auto finish = [&](int kc, const float (&zr)[D], double ll) {
-      // log q(z), fp64 (group constants re-read from SMEM: volatile keeps ptxas from hoisting them)
-      const volatile double* qv = qc;
-      double lq = 0.0;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        const double dz = (double)zr[r] - qv[r];
-        lq += qv[2 * D + r] - dz * dz * qv[D + r];
-      }
+      // group constants re-read from SMEM (volatile keeps ptxas from hoisting them into registers)
+      const volatile double* qmv = qm;
+      const volatile double2* qabv = qab;
+      const volatile float* qmfv = qmf;
+      double quad = Ci;
       // column operand re-centred on the group's Q mean: w = z - m_i and
       // S = |w|^2 + 2 m_i . w (so D_k(z) = alpha'_ik + c0_k . w + gamma_k S)
       float W2 = 0.f, mw = 0.f;
-      double U2d = 0.0;
       float wv[kTcD];
 #pragma unroll
       for (int r = 0; r < kTcD; ++r) {
         if (r < D) {
-          const float m = (float)qv[r];
+          const double md = qmv[r];
+          const double2 ab = const_cast<const double2&>(qabv[r]);
+          const double wd = (double)zr[r] - md;
+          quad = fma(wd, fma(ab.x, wd, ab.y), quad);
+          const float m = qmfv[r];
           wv[r] = zr[r] - m;
           W2 = fmaf(wv[r], wv[r], W2);
           mw = fmaf(m, wv[r], mw);
-          const double ud = (double)zr[r] - (double)mu_ref[r];
-          U2d += ud * ud;
         } else {
           wv[r] = 0.f;  // zero-padded contraction
         }
@@ -340,20 +375,33 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 48)) = c0;
       }
       // t_ref(k') = B(k_ref,k') + A_i(k') (fp64; the backward rebuilds A from it)
-      const double t = bref_const - 0.5 * e_ref * U2d + (ll - lq);
+      const double t = quad + ll;
       a.ws.tA[(size_t)i * K + kc] = t;
-      tmax = fmax(tmax, t);
+      if (t > tmax) {
+        tsum = fma(tsum, (double)expf((float)(tmax - t)), 1.0);
+        tmax = t;
+      } else {
+        tsum += (double)expf((float)(t - tmax));
+      }
       w2max = fmaxf(w2max, W2);
     };
     // Two columns per lane at a time (kc and kc + K/2): the per-observation feature loads are
     // shared and the two likelihood chains hide each other's latency.
-    for (int kcA = lane; kcA < K / 2; kcA += 32) {
-      const int kcB = kcA + K / 2;
+    for (int it = 0; it < NIT; ++it) {
+      if (it + 1 < NIT) {
+        stage_z(i, it + 1, (it + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const float* zst = zs + (it & 1) * (2 * kTcD * 32);
+      const int kcA = it * 32 + lane, kcB = kcA + K / 2;
       float zA[D], zB[D];
 #pragma unroll
       for (int r = 0; r < D; ++r) {
-        zA[r] = a.z[((size_t)i * D + r) * K + kcA];
-        zB[r] = a.z[((size_t)i * D + r) * K + kcB];
+        zA[r] = zst[r * 32 + lane];
+        zB[r] = zst[(kTcD + r) * 32 + lane];
       }
       double llA, llB;
       if constexpr (OBS == QEM_OBS_GAUSS) {
@@ -361,14 +409,8 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         llA = gc0 - (sxx - 2.0 * za * sx + (double)J * za * za) * gc1;
         llB = gc0 - (sxx - 2.0 * zb * sx + (double)J * zb * zb) * gc1;
       } else {
-        // label part sum_j y_j eta_j = (sum_j y_j x_j) . z in fp64; softplus part per
+        // label part sum_j y_j eta_j is in the column quadratic (beta_r, C_i); softplus part per
         // observation, two observations at a time (FFMA2), for both columns
-        double lyA = 0.0, lyB = 0.0;
-#pragma unroll
-        for (int r = 0; r < D; ++r) {
-          lyA = fma((double)yx[r], (double)zA[r], lyA);
-          lyB = fma((double)yx[r], (double)zB[r], lyB);
-        }
         double lspA = 0.0, lspB = 0.0;
         for (int jp = 0; jp < Jh; ++jp) {
           const float2* xr = xp + jp * D;
@@ -396,48 +438,51 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
           }
           const float2 ea = add2(a0, a1), eb = add2(b0, b1);
           const bool two = 2 * jp + 1 < J;
-          lspA += (double)softplus_mufu(ea.x) + (two ? (double)softplus_mufu(ea.y) : 0.0);
-          lspB += (double)softplus_mufu(eb.x) + (two ? (double)softplus_mufu(eb.y) : 0.0);
+          lspA += (double)softplus_pair(ea, two);
+          lspB += (double)softplus_pair(eb, two);
         }
-        llA = lyA - lspA;
-        llB = lyB - lspB;
+        llA = -lspA;
+        llB = -lspB;
       }
       finish(kcA, zA, llA);
       finish(kcB, zB, llB);
+      __syncwarp();  // the stage is refilled two iterations on
     }
+    if (i + gstride < a.n_local) stage_z(i + gstride, 0, 0);  // next group's first stage, under the passes below
     const double M = warp_max(tmax);
     const float W2max = warp_maxf(w2max);
-    double sum = 0.0;
     const double* tref = a.ws.tA + (size_t)i * K;  // written above by this lane (program order)
-#pragma unroll 4
-    for (int kc = lane; kc < K; kc += 32) sum += (double)expf((float)(tref[kc] - M));
-    const double logS = log(warp_sum(sum));
+    const double logS = log(warp_sum(tsum * (double)expf((float)(tmax - M))));
     // tile mode: bound on |D'_k(k')| = |c'_k . w + gamma_k |w|^2|, c' = c0 + 2 gamma m_i
     float u0[D];
 #pragma unroll
-    for (int r = 0; r < D; ++r) u0[r] = (float)qc[r];
+    for (int r = 0; r < D; ++r) u0[r] = (float)qm[r];
     const float wmax = sqrtf(W2max);
     float tb = 0.f;
+#pragma unroll 4  // fwd_coef rows stream from L2: keep several rows' loads in flight
     for (int k = lane; k < K; k += 32) {
-      const float* fc = a.ws.fwd_coef + (size_t)k * (D + 2);
-      const float g = fc[1];
+      const float2* fc = reinterpret_cast<const float2*>(a.ws.fwd_coef + (size_t)k * (D + 2));  // D even
+      const float2 h = __ldg(fc);
+      const float g = h.y;
       float cn = 0.f;
 #pragma unroll
-      for (int r = 0; r < D; ++r) {
-        const float cp = fmaf(2.f * g, u0[r], fc[2 + r]);
-        cn = fmaf(cp, cp, cn);
+      for (int q = 0; q < D / 2; ++q) {
+        const float2 c = __ldg(fc + 1 + q);
+        const float cp0 = fmaf(2.f * g, u0[2 * q], c.x), cp1 = fmaf(2.f * g, u0[2 * q + 1], c.y);
+        cn = fmaf(cp0, cp0, cn);
+        cn = fmaf(cp1, cp1, cn);
       }
       tb = fmaxf(tb, sqrtf(cn) * wmax + fabsf(g) * W2max);
     }
     tb = warp_maxf(tb);
     const int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
     float* aux = a.ws.colaux + (size_t)i * 2 * K;  // SoA {P, ln P}
-    for (int kb = lane; kb < K; kb += 128) {  // 4 columns per lane per batch: their loads in flight together
-      double tb4[4];
+    for (int kb = lane; kb < K; kb += 256) {  // 8 columns per lane per batch: their loads in flight together
+      double tb4[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) tb4[u] = kb + 32 * u < K ? ldg_d(tref + kb + 32 * u) : 0.0;
+      for (int u = 0; u < 8; ++u) tb4[u] = kb + 32 * u < K ? tref[kb + 32 * u] : 0.0;  // coherent: written above
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int kc = kb + 32 * u;
         if (kc >= K) break;
         const float lp = (float)(tb4[u] - M - logS);
