@@ -172,6 +172,18 @@ qem_status qem_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begi
    qem_destroy.  opts may be NULL (w=0.3, no schedule, floor 1e-8). */
 qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin,
                       int64_t group_end, qem_ctx** out);
+/* Caller-owned workspace variant (serving deployments that pool device memory):
+   qem_workspace_bytes reports the bytes qem_create_in needs for the same
+   (desc, opts, group range) -- host-only arithmetic, no device call except the
+   SM-count query that sizes the per-CTA partial buffers; qem_create_in carves
+   the context's buffers from d_workspace (device memory, 256-byte aligned,
+   >= that many bytes, owned by the caller and not freed by qem_destroy; it
+   must outlive the context).  Errors: QEM_INVALID_ARGUMENT on a null pointer,
+   misalignment or a short workspace; otherwise as qem_create. */
+qem_status qem_workspace_bytes(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin,
+                               int64_t group_end, size_t* bytes);
+qem_status qem_create_in(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin,
+                         int64_t group_end, void* d_workspace, size_t ws_bytes, qem_ctx** out);
 void qem_destroy(qem_ctx* ctx);
 
 /* Bind the caller's device buffers.  Must precede every compute call; may be
@@ -219,6 +231,22 @@ qem_status qem_evidence_root(qem_ctx* ctx, void* stream);
    With opts.fresh_denominator the one-step mean parameters (m1_new, v_new + m1_new^2) are
    first multiplied by exp(log_pe - log_pe_fresh) (read on the device).                */
 qem_status qem_mstep(qem_ctx* ctx, int32_t t, void* stream);
+
+/* MPIW E-step on EXPLICIT log-factor tables (Eq. 7a-c; plate elimination,
+   PAPER.md:393) for a root with K samples and n plate instances below it:
+     d_f_root [K]        f_root(k)   = log p(root^k) - log q(root^k)
+     d_f      [n][K][K]  f_i(k, k')  = log p(z_i^k', x_i | root^k) - log q(z_i^k')  (k' fastest)
+   Outputs (device, fp64, caller-owned): d_g [n][K] messages g_i(k) = lse_k' f_i(k,k') - ln K;
+   d_log_pe [1] = lse_k (f_root(k) + sum_i g_i(k)) - ln K; d_w_root [K] root weights;
+   d_w [n][K] per-instance marginal weights w_i(k') (each row sums to 1).  Any factor kind the
+   caller can tabulate runs here (discrete latents, crossed effects); it also pins the reduction
+   of the fused kernels independently of their factor arithmetic.  Degenerate evidence (every
+   root sample at -inf) gives log Pe = -inf and NaN weights, as data.  n may be 0 (d_f, d_g, d_w
+   then unused).  Errors: QEM_INVALID_ARGUMENT for n < 0, K outside [1, QEM_TABLES_MAX_K] or a
+   null array.  Asynchronous on `stream`. */
+#define QEM_TABLES_MAX_K 8192
+qem_status qem_estep_tables(int64_t n, int32_t K, const double* d_f_root, const double* d_f, double* d_g,
+                            double* d_log_pe, double* d_w_root, double* d_w, void* stream);
 
 /* EMA over mean parameters + M-step for non-Gaussian Q families (Alg. 1 lines 3, 6; Eq. 9;
    PAPER.md:218 "a Beta's parameters are recovered from expectations of log transformations",

@@ -12,4 +12,6 @@ Modules:
   oracle.py      ctypes wrapper + the QEM step (Algorithm 1) around it.
   brute.py       literal K^n enumeration in numpy (pins qem_oracle.c).
   closed_form.py conjugate-Gaussian posterior and evidence (pins the K->inf limit).
+  expfam.py      Gamma/Beta/Bernoulli/Categorical M-steps from mean parameters (scipy).
+  tables.py      the E-step on explicit log-factor tables: elimination + enumeration (numpy).
 """

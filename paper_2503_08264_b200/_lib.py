@@ -17,9 +17,9 @@ FLAG_DEGENERATE, FLAG_NAN, FLAG_CLAMP = 1, 2, 4
 
 # Every symbol include/qem.h declares (checked by tests/test_abi.py).
 EXPORTS = [
-    "qem_model_validate", "qem_shard_range", "qem_create", "qem_destroy", "qem_bind", "qem_sample_q",
+    "qem_model_validate", "qem_shard_range", "qem_create", "qem_workspace_bytes", "qem_create_in", "qem_destroy", "qem_bind", "qem_sample_q",
     "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_estep_evidence",
-    "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_iterate",
+    "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_estep_tables", "qem_iterate",
     "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_pair_path", "qem_copy_messages", "qem_status_str", "qem_last_error",
     "qem_version",
 ]
@@ -68,6 +68,11 @@ def lib() -> ctypes.CDLL:
         L.qem_model_validate.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_char_p, ctypes.c_size_t]
         L.qem_shard_range.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.qem_create.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(Opts), i64, i64, ctypes.POINTER(vp)]
+        L.qem_workspace_bytes.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(Opts), i64, i64,
+                                          ctypes.POINTER(ctypes.c_size_t)]
+        L.qem_create_in.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(Opts), i64, i64, vp, ctypes.c_size_t,
+                                    ctypes.POINTER(vp)]
+        L.qem_estep_tables.argtypes = [i64, i32, vp, vp, vp, vp, vp, vp, vp]
         L.qem_destroy.argtypes = [vp]
         L.qem_destroy.restype = None
         L.qem_bind.argtypes = [vp, ctypes.POINTER(Buffers)]
@@ -98,7 +103,7 @@ def lib() -> ctypes.CDLL:
         for name in ["qem_model_validate", "qem_shard_range", "qem_create", "qem_bind", "qem_sample_q", "qem_estep",
                      "qem_estep_forward", "qem_estep_backward", "qem_reduce_buffer", "qem_mstep", "qem_iterate",
                      "qem_read_flags", "qem_read_mode_hist", "qem_copy_messages", "qem_estep_evidence",
-                     "qem_evidence_root"]:
+                     "qem_evidence_root", "qem_workspace_bytes", "qem_create_in", "qem_estep_tables"]:
             getattr(L, name).restype = i32
         _lib = L
     return _lib

@@ -155,10 +155,11 @@ qem_status qem_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begi
   return QEM_OK;
 }
 
-qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin, int64_t group_end,
-                      qem_ctx** out) {
-  if (!out) return fail(QEM_INVALID_ARGUMENT, "null output pointer");
-  *out = nullptr;
+// Shared by qem_create / qem_create_in / qem_workspace_bytes: validate, fill the context, size the
+// workspace; then (unless measure_only) carve it from `ws` (caller-owned) or a cudaMalloc.
+static qem_status create_impl(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin,
+                              int64_t group_end, void* ws, size_t ws_cap, size_t* bytes, qem_ctx** out) {
+  if (out) *out = nullptr;
   qem_status s = validate(desc, nullptr, 0);
   if (s != QEM_OK) return s;
   if (group_begin < 0 || group_end > desc->n || group_begin >= group_end)
@@ -191,15 +192,32 @@ qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t 
   if (desc->family == QEM_FAMILY_TWO_LEVEL) qem::tl_grids(desc, c->n_local, sm_count(), &c->grid_fwd, &c->grid_bwd, &c->grid_prep);
   c->grid_stage = (int)(c->n_local < sm_count() ? c->n_local : sm_count());
   c->ws_bytes = carve(c, nullptr);
-  cudaError_t e = cudaMalloc(&c->ws, c->ws_bytes);
-  if (e != cudaSuccess) {
+  if (bytes) *bytes = c->ws_bytes;
+  if (!out) {  // measure only
     delete c;
-    return cuda_fail(e, "cudaMalloc(workspace)");
+    return QEM_OK;
+  }
+  cudaError_t e = cudaSuccess;
+  if (ws) {
+    if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0 || ws_cap < c->ws_bytes) {
+      const size_t need = c->ws_bytes;
+      delete c;
+      return fail(QEM_INVALID_ARGUMENT, "caller workspace: need %zu bytes at 256-byte alignment (got %zu)", need, ws_cap);
+    }
+    c->ws = ws;
+    c->ws_owned = false;
+  } else {
+    e = cudaMalloc(&c->ws, c->ws_bytes);
+    if (e != cudaSuccess) {
+      delete c;
+      return cuda_fail(e, "cudaMalloc(workspace)");
+    }
+    c->ws_owned = true;
   }
   carve(c, reinterpret_cast<char*>(c->ws));
   e = cudaMemset(c->cnt, 0, sizeof(qem::Counters));
   if (e != cudaSuccess) {
-    cudaFree(c->ws);
+    if (c->ws_owned) cudaFree(c->ws);
     delete c;
     return cuda_fail(e, "cudaMemset");
   }
@@ -207,10 +225,28 @@ qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t 
   return QEM_OK;
 }
 
+qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin, int64_t group_end,
+                      qem_ctx** out) {
+  if (!out) return fail(QEM_INVALID_ARGUMENT, "null output pointer");
+  return create_impl(desc, opts, group_begin, group_end, nullptr, 0, nullptr, out);
+}
+
+qem_status qem_workspace_bytes(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin,
+                               int64_t group_end, size_t* bytes) {
+  if (!bytes) return fail(QEM_INVALID_ARGUMENT, "null output pointer");
+  return create_impl(desc, opts, group_begin, group_end, nullptr, 0, bytes, nullptr);
+}
+
+qem_status qem_create_in(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin, int64_t group_end,
+                         void* d_workspace, size_t ws_bytes, qem_ctx** out) {
+  if (!out || !d_workspace) return fail(QEM_INVALID_ARGUMENT, "null output or workspace pointer");
+  return create_impl(desc, opts, group_begin, group_end, d_workspace, ws_bytes, nullptr, out);
+}
+
 void qem_destroy(qem_ctx* c) {
   if (!c) return;
   if (c->graph_valid) cudaGraphExecDestroy(c->graph);
-  if (c->ws) cudaFree(c->ws);
+  if (c->ws && c->ws_owned) cudaFree(c->ws);
   delete c;
 }
 
@@ -317,6 +353,17 @@ qem_status qem_mstep_family(int32_t family, int64_t n, int32_t C, double lam, co
   const cudaError_t e =
       qem::launch_mstep_family(family, n, C, lam, d_m_new, d_m_ema, d_params, d_status, (cudaStream_t)stream);
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_mstep_family");
+}
+
+qem_status qem_estep_tables(int64_t n, int32_t K, const double* d_f_root, const double* d_f, double* d_g,
+                            double* d_log_pe, double* d_w_root, double* d_w, void* stream) {
+  if (n < 0 || K < 1 || K > QEM_TABLES_MAX_K) return fail(QEM_INVALID_ARGUMENT, "need n >= 0 and 1 <= K <= %d", QEM_TABLES_MAX_K);
+  if ((int64_t)n * K > ((int64_t)1 << 40)) return fail(QEM_INVALID_ARGUMENT, "tables too large");
+  if (!d_f_root || !d_log_pe || !d_w_root || (n > 0 && (!d_f || !d_g || !d_w)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e =
+      qem::launch_estep_tables(n, K, d_f_root, d_f, d_g, d_log_pe, d_w_root, d_w, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_tables");
 }
 
 qem_status qem_mstep(qem_ctx* c, int32_t t, void* stream) {

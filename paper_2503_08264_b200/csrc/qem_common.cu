@@ -90,9 +90,9 @@ __device__ __forceinline__ void bm_sincos2pi(uint32_t m, float& sn, float& cs) {
 // sampling, App. E; fp32 definition DESIGN.md R22).
 // One thread = 4 consecutive samples k of one latent dim (one Philox call,
 // two Box-Muller pairs).
-__global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= (uint32_t)a.total_quads) return;
+// One Philox4x32-10 call (4 samples) per quad; grid-stride over the quads (a few waves of
+// resident blocks: the per-thread start-up cost would otherwise rival the Philox rounds).
+__device__ __forceinline__ void sample_quad(const SampleArgs& a, uint32_t q, int t) {
   int L = 0;
 #pragma unroll
   for (int l = 1; l < 3; ++l)
@@ -109,7 +109,6 @@ __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) e[j] = (k0 + j < a.K) ? s.eps[row * a.K + k0 + j] : 0.f;
   } else {
-    const int t = resolve_iter(a.t_host, a.d_iter);
     const uint32_t inst = s.fdims.div(row32);
     const int dim = (int)(row32 - inst * (uint32_t)s.dims);
     const uint32_t ginst = (uint32_t)(inst + s.inst_offset);
@@ -138,6 +137,12 @@ __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
     for (int j = 0; j < 4; ++j)
       if (k0 + j < a.K) zr[j] = __fmaf_rn(sd, e[j], m);
   }
+}
+
+__global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
+  const int t = resolve_iter(a.t_host, a.d_iter);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)a.total_quads; q += stride) sample_quad(a, q, t);
 }
 
 cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps, cudaStream_t st,
@@ -186,9 +191,16 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
   a.nlev = nlev;
   a.total_quads = quads;
   const int threads = 256;
-  const int64_t blocks = (quads + threads - 1) / threads;
+  int64_t blocks = (quads + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
   if (quads >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;  // 32-bit sample indexing
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const int64_t cap = (int64_t)sms * 8 * 4;  // four waves of 8 resident 256-thread blocks per SM
+  if (blocks > cap) blocks = cap;
   k_sample<<<(unsigned)blocks, threads, 0, st>>>(a);
   c->launches += 1;
   return cudaGetLastError();

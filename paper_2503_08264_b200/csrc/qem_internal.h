@@ -80,6 +80,7 @@ struct qem_ctx {
   int grid_stage;  // one CTA per SM, capped by the groups (TMA-staged per-group kernels)
   void* ws;
   size_t ws_bytes;
+  bool ws_owned;  // false: caller-owned workspace (qem_create_in)
   qem::TwoLevelWs tw;
   qem::ThreeLevelWs th;
   qem::Counters* cnt;
@@ -111,6 +112,8 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
                           cudaStream_t s, uint32_t iter_or = 0);
 cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t s);
 // non-Gaussian Q families (qem_expfam.cu)
+cudaError_t launch_estep_tables(int64_t n, int K, const double* f_root, const double* f, double* g, double* log_pe,
+                                double* w_root, double* w, cudaStream_t st);
 cudaError_t launch_mstep_family(int family, int64_t n, int C, double lam, const double* m_new, double* m_ema,
                                 double* params, int32_t* status, cudaStream_t st);
 }  // namespace qem

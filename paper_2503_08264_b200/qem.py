@@ -48,6 +48,37 @@ def mstep_family(family: int, lam: float, m_new: torch.Tensor, m_ema: torch.Tens
     return params, status
 
 
+def estep_tables(f_root: torch.Tensor, f: torch.Tensor, stream=None):
+    """MPIW E-step on explicit log-factor tables (qem_estep_tables): f_root float64 [K], f float64
+    [n][K][K] (device).  Returns dict(log_pe [1], w_root [K], w [n][K], g [n][K])."""
+    assert f_root.dtype == torch.float64 and f.dtype == torch.float64 and f_root.is_cuda
+    K = f_root.shape[0]
+    n = f.shape[0] if f.numel() else 0
+    assert f.numel() == 0 or tuple(f.shape) == (n, K, K)
+    f_root, f = f_root.contiguous(), f.contiguous()
+    dev = f_root.device
+    out = dict(log_pe=torch.empty(1, dtype=torch.float64, device=dev),
+               w_root=torch.empty(K, dtype=torch.float64, device=dev),
+               w=torch.empty(n, K, dtype=torch.float64, device=dev),
+               g=torch.empty(n, K, dtype=torch.float64, device=dev))
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr() if t.numel() else None)  # noqa: E731
+    check(lib().qem_estep_tables(n, K, ptr(f_root), ptr(f), ptr(out["g"]), ptr(out["log_pe"]), ptr(out["w_root"]),
+                                 ptr(out["w"]), _stream(stream)), "qem_estep_tables")
+    return out
+
+
+def workspace_bytes(m, group_begin=0, group_end=None, *, new_weight=0.3, schedule_p=0.0, var_floor=1e-8,
+                    fresh_denominator=False) -> int:
+    """Device workspace a context over [group_begin, group_end) needs (qem_workspace_bytes)."""
+    d = _desc(m)
+    o = _lib.Opts(new_weight, schedule_p, var_floor, int(bool(fresh_denominator)), 0)
+    nb = ctypes.c_size_t()
+    check(lib().qem_workspace_bytes(ctypes.byref(d), ctypes.byref(o), int(group_begin),
+                                    int(m.n if group_end is None else group_end), ctypes.byref(nb)),
+          "qem_workspace_bytes")
+    return nb.value
+
+
 def shard_range(n: int, rank: int, world: int):
     b, e = ctypes.c_int64(), ctypes.c_int64()
     check(lib().qem_shard_range(n, rank, world, ctypes.byref(b), ctypes.byref(e)), "qem_shard_range")
@@ -63,7 +94,7 @@ class QEM:
     """One context over LOCAL level-1 instances [group_begin, group_end)."""
 
     def __init__(self, m, *, new_weight=0.3, schedule_p=0.0, var_floor=1e-8, group_begin=0, group_end=None,
-                 device="cuda", trace_len=0, fresh_denominator=False):
+                 device="cuda", trace_len=0, fresh_denominator=False, caller_workspace=False):
         if not torch.cuda.is_available():
             raise _lib.QemError("QEM needs a CUDA device (there is no CPU fallback)")
         self.m = m
@@ -76,9 +107,19 @@ class QEM:
         o = _lib.Opts(new_weight, schedule_p, var_floor, int(bool(fresh_denominator)), 0)
         self.fresh = bool(fresh_denominator)
         ctx = ctypes.c_void_p()
+        self._ws = None
         with torch.cuda.device(self.device):
-            check(lib().qem_create(ctypes.byref(d), ctypes.byref(o), self.g_begin, self.g_end, ctypes.byref(ctx)),
-                  "qem_create")
+            if caller_workspace:  # the context's buffers carved from a torch allocation (qem_create_in)
+                nb = ctypes.c_size_t()
+                check(lib().qem_workspace_bytes(ctypes.byref(d), ctypes.byref(o), self.g_begin, self.g_end,
+                                                ctypes.byref(nb)), "qem_workspace_bytes")
+                self._ws = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
+                check(lib().qem_create_in(ctypes.byref(d), ctypes.byref(o), self.g_begin, self.g_end,
+                                          ctypes.c_void_p(self._ws.data_ptr()), nb.value, ctypes.byref(ctx)),
+                      "qem_create_in")
+            else:
+                check(lib().qem_create(ctypes.byref(d), ctypes.byref(o), self.g_begin, self.g_end,
+                                       ctypes.byref(ctx)), "qem_create")
         self.ctx = ctx
         K = m.K
         f32 = dict(dtype=torch.float32, device=self.device)
@@ -251,6 +292,7 @@ class QEM:
         if getattr(self, "ctx", None):
             lib().qem_destroy(self.ctx)
             self.ctx = None
+            self._ws = None  # a caller workspace outlives the context
 
     def __del__(self):
         try:

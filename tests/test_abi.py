@@ -91,3 +91,46 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(^\s*(from|import)\s+oracle\b|liboracle|qem_oracle|orc_)", src, re.M), f
+
+
+@pytest.mark.gpu
+def test_caller_workspace_matches_own_workspace():
+    """qem_create_in on a caller allocation (sized by qem_workspace_bytes) computes exactly what
+    qem_create's own workspace does; a short or misaligned workspace is rejected."""
+    import numpy as np
+    import torch
+    from paper_2503_08264_b200 import _lib, synth
+    from paper_2503_08264_b200.qem import QEM, workspace_bytes
+    m = synth.config(5, n=40, K=256)
+    data = synth.make_data(m)
+    outs = []
+    for caller in (False, True):
+        g = QEM(m, caller_workspace=caller)
+        g.set_data(data)
+        g.set_q(synth.initial_q(m))
+        g.iterate(1, 2, seed=3)
+        outs.append(g.result())
+        if caller:
+            assert g._ws.numel() == workspace_bytes(m)
+        g.close()
+    for l in range(2):
+        np.testing.assert_array_equal(outs[0]["q_mean"][l], outs[1]["q_mean"][l])
+        np.testing.assert_array_equal(outs[0]["w"][l], outs[1]["w"][l])
+    L = _lib.lib()
+    d = _lib_desc(m)
+    o = _lib.Opts(0.3, 0.0, 1e-8, 0, 0)
+    nb = workspace_bytes(m)
+    buf = torch.empty(nb + 512, dtype=torch.uint8, device="cuda")
+    ctx = ctypes.c_void_p()
+    assert L.qem_create_in(ctypes.byref(d), ctypes.byref(o), 0, m.n, ctypes.c_void_p(buf.data_ptr()), nb - 256,
+                           ctypes.byref(ctx)) == _lib.INVALID_ARGUMENT
+    assert L.qem_create_in(ctypes.byref(d), ctypes.byref(o), 0, m.n, ctypes.c_void_p(buf.data_ptr() + 8), nb,
+                           ctypes.byref(ctx)) == _lib.INVALID_ARGUMENT
+    assert L.qem_create_in(ctypes.byref(d), ctypes.byref(o), 0, m.n, ctypes.c_void_p(buf.data_ptr()), nb,
+                           ctypes.byref(ctx)) == _lib.OK
+    L.qem_destroy(ctx)
+
+
+def _lib_desc(m):
+    from paper_2503_08264_b200.qem import _desc
+    return _desc(m)
