@@ -10,9 +10,9 @@ timeout 400 python bench.py > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.er
 timeout 400 python bench.py --config 4 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "bench4 rc=$?"
 timeout 400 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 cat gpurun_out/bench_c5.json gpurun_out/bench_c4.json gpurun_out/bench_ref.json
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c5.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c4.csv python bench.py --config 4 --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-B="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c5.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-variants > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c4.csv python bench.py --config 4 --steps 2 --warmup 3 --no-cpu --no-e2e --no-variants > /dev/null 2>&1
+B="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-variants"
 for k in k_backward_tc k_forward_tc k_colprep_tc k_sample; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 -o gpurun_out/ncu_c5_$k $B --config 5 > /dev/null 2>&1
 done
