@@ -293,11 +293,12 @@ def run_gpu(args):
     if not args.no_e2e:
         e2e = run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce)
     tc = g.pair_path() == 1
-    fresh = mfam = None
+    fresh = mfam = disc = None
     if world == 1 and not args.no_variants:
         g.close()  # free the first context's workspace before the variant's
         fresh = run_fresh_variant(args, m, data, dev, seed)
         mfam = run_mstep_family_variant(dev)
+        disc = run_discrete_variant(dev)
 
     # ----------------------------------------------------------- roofline
     local_pairs = (ge - gb) * m.K * m.K
@@ -358,7 +359,7 @@ def run_gpu(args):
         "gpu_launches": n_launched,
         "clocks": clk,
         "flags": {"device_flags": flags, "var_clamps": clamps},
-        "variants": {"fresh_denominator": fresh, "mstep_family": mfam},
+        "variants": {"fresh_denominator": fresh, "mstep_family": mfam, "discrete_occupancy": disc},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -457,6 +458,32 @@ def run_fresh_variant(args, m, data, dev, seed):
     g.close()
     return {"ms_per_step": ms, "value": m.pairs / (ms * 1e-3), "unit": "factor-pairs/s (E-step pairs; the evidence "
             "pass's forward pairs are extra work)", "qem_iters_per_s": 1e3 / ms}
+
+
+def run_discrete_variant(dev, steps=10):
+    """NEXT row f1, E-step side (R30): one QEM iteration of the Occupancy-shaped
+    discrete-latent model (14400 categorical sites under a 2-d Gaussian root, K = 64; device
+    Philox samples, explicit fp64 log-factor tables), timed with CUDA events after 3 warm-up
+    iterations."""
+    import torch
+    from paper_2503_08264_b200 import synth
+    from paper_2503_08264_b200.qem import CategoricalQEM
+    om = synth.occupancy()
+    g = CategoricalQEM(om, device=dev)
+    for t in range(1, 4):
+        g.step(t, 7)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    st.record()
+    for t in range(4, 4 + steps):
+        g.step(t, 7)
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / steps
+    pairs = om.n * om.K * om.K
+    return {"workload": f"occupancy n={om.n} C={om.C} R={om.R} d={om.d} K={om.K}", "ms_per_step": ms,
+            "value": pairs / (ms * 1e-3), "unit": "factor-pairs/s (tables path, fp64)",
+            "qem_iters_per_s": 1e3 / ms}
 
 
 def run_mstep_family_variant(dev, n=1_000_000, reps=10):

@@ -232,13 +232,65 @@ qem_status qem_evidence_root(qem_ctx* ctx, void* stream);
    first multiplied by exp(log_pe - log_pe_fresh) (read on the device).                */
 qem_status qem_mstep(qem_ctx* ctx, int32_t t, void* stream);
 
+/* ---- Discrete latents under a continuous root (NEXT row f1, E-step side; R30) ----
+   Occupancy-shaped model: root r in R^d, prior N(0, I), Q_root =
+   N(m, diag v); per instance i a categorical z_i in {0..C-1}, prior logits eta_ic(r) = x_ic . r,
+   Q_i = Categorical(p_i), observations through the per-state log-likelihood table
+   L_i(c) = log p(y_i | z_i = c).  One QEM iteration = qem_sample_normal (root) +
+   qem_sample_categorical + qem_tables_categorical + qem_estep_tables +
+   qem_moments_categorical + qem_mstep_categorical.  All arrays device-resident and caller-owned; calls are asynchronous on `stream`;
+   QEM_INVALID_ARGUMENT on bad sizes / null arrays. */
+#define QEM_CAT_MAX_C 8
+
+/* Gaussian samples z[row][k] = fmaf(sqrtf(var[row]), eps, mean[row]) (fp32, R22) for `rows`
+   latent rows: eps from d_eps [rows][K] when non-NULL, else Philox4x32-10 at counter
+   (k/4, 0, row, level << 24 | iter) + Box-Muller, as qem_sample_q.  iter >= 1, 0 <= level < 256. */
+qem_status qem_sample_normal(int64_t rows, int32_t K, int32_t level, uint64_t seed, int32_t iter,
+                             const float* d_mean, const float* d_var, const float* d_eps, float* d_z,
+                             void* stream);
+/* Categorical samples z[i][k] in [0, C): the smallest c with u < p_i(0) + ... + p_i(c) (fp64
+   sequential prefix; C-1 if none), u = ((w >> 8) + 1/2) 2^-24 from word k%4 of Philox4x32-10 at
+   counter (k/4, 0, i, 3 << 24 | iter), key = seed.  d_p [n][C] fp64 (rows summing to 1),
+   d_z [n][K] int32.  1 <= C <= QEM_CAT_MAX_C, iter >= 1. */
+qem_status qem_sample_categorical(int64_t n, int32_t C, int32_t K, uint64_t seed, int32_t iter,
+                                  const double* d_p, int32_t* d_z, void* stream);
+/* Log-factor tables of the model above (fp64):
+     d_f_root [K]      log N(r^k; 0, I) - log q(r^k)          (r^k = d_root_z[.][k], fp32 [d][K])
+     d_f [n][K][K]     log softmax_c(x_i . r^k)[z_i^k'] + L_i(z_i^k') - log p_i(z_i^k')
+   d_root_mean/var [d] fp32 (Q_root), d_x [n][C][d], d_loglik [n][C], d_p [n][C] fp64,
+   d_z [n][K] int32.  Feed d_f_root / d_f to qem_estep_tables. */
+qem_status qem_tables_categorical(int64_t n, int32_t C, int32_t K, int32_t d, const float* d_root_z,
+                                  const float* d_root_mean, const float* d_root_var, const double* d_x,
+                                  const double* d_loglik, const double* d_p, const int32_t* d_z,
+                                  double* d_f_root, double* d_f, void* stream);
+/* Moments (Eq. 7a) from qem_estep_tables' weights: d_root_m [d][2] = (E r_e, E r_e^2) under
+   d_w_root [K]; d_pm [n][C] = E onehot(z_i) = sum_k' w_i(k') [z_i^k' = c] under d_w [n][K]. */
+qem_status qem_moments_categorical(int64_t n, int32_t C, int32_t K, int32_t d, const double* d_w_root,
+                                   const float* d_root_z, const double* d_w, const int32_t* d_z,
+                                   double* d_root_m, double* d_pm, void* stream);
+/* EMA over mean parameters (history weight lam in [0, 1), Eq. 9 / DESIGN.md R5) + M-step:
+   root  d_root_ema [d][2] <- lam ema + (1-lam) d_root_m;  Q_root mean = E r, var =
+         max(E r^2 - (E r)^2, var_floor), written fp32 to d_root_mean / d_root_var (R22);
+   inst  d_p_ema [n][C] <- lam ema + (1-lam) d_pm;  d_p = d_p_ema / sum_c d_p_ema (fp64).
+   Variance-floor clamps are added to *d_clamps (int64, device) when non-NULL. */
+qem_status qem_mstep_categorical(int64_t n, int32_t C, int32_t d, double lam, double var_floor,
+                                 const double* d_root_m, double* d_root_ema, float* d_root_mean,
+                                 float* d_root_var, const double* d_pm, double* d_p_ema, double* d_p,
+                                 int64_t* d_clamps, void* stream);
+/* Per-state log-likelihood of R Bernoulli observations per instance (the data table L of
+   qem_tables_categorical): d_L[i][c] = sum_r y_ir l_irc - softplus(l_irc), softplus(l) =
+   max(l, 0) + log1p(exp(-|l|)) (fp64); d_y [n][R] uint8 in {0,1}, d_logit [n][R][C] fp64. */
+qem_status qem_loglik_bernoulli_states(int64_t n, int32_t C, int32_t R, const uint8_t* d_y,
+                                       const double* d_logit, double* d_L, void* stream);
+
 /* MPIW E-step on EXPLICIT log-factor tables (Eq. 7a-c; plate elimination,
    PAPER.md:393) for a root with K samples and n plate instances below it:
      d_f_root [K]        f_root(k)   = log p(root^k) - log q(root^k)
      d_f      [n][K][K]  f_i(k, k')  = log p(z_i^k', x_i | root^k) - log q(z_i^k')  (k' fastest)
    Outputs (device, fp64, caller-owned): d_g [n][K] messages g_i(k) = lse_k' f_i(k,k') - ln K;
    d_log_pe [1] = lse_k (f_root(k) + sum_i g_i(k)) - ln K; d_w_root [K] root weights;
-   d_w [n][K] per-instance marginal weights w_i(k') (each row sums to 1).  Any factor kind the
+   d_w [n][K] per-instance marginal weights w_i(k') (each row sums to 1; also the scratch of the plate
+   sum before the backward writes it).  Any factor kind the
    caller can tabulate runs here (discrete latents, crossed effects); it also pins the reduction
    of the fused kernels independently of their factor arithmetic.  Degenerate evidence (every
    root sample at -inf) gives log Pe = -inf and NaN weights, as data.  n may be 0 (d_f, d_g, d_w

@@ -19,7 +19,9 @@ FLAG_DEGENERATE, FLAG_NAN, FLAG_CLAMP = 1, 2, 4
 EXPORTS = [
     "qem_model_validate", "qem_shard_range", "qem_create", "qem_workspace_bytes", "qem_create_in", "qem_destroy", "qem_bind", "qem_sample_q",
     "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_estep_evidence",
-    "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_estep_tables", "qem_iterate",
+    "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_estep_tables", "qem_sample_normal",
+    "qem_sample_categorical", "qem_tables_categorical", "qem_moments_categorical", "qem_mstep_categorical",
+    "qem_loglik_bernoulli_states", "qem_iterate",
     "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_pair_path", "qem_copy_messages", "qem_status_str", "qem_last_error",
     "qem_version",
 ]
@@ -73,6 +75,12 @@ def lib() -> ctypes.CDLL:
         L.qem_create_in.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(Opts), i64, i64, vp, ctypes.c_size_t,
                                     ctypes.POINTER(vp)]
         L.qem_estep_tables.argtypes = [i64, i32, vp, vp, vp, vp, vp, vp, vp]
+        L.qem_sample_normal.argtypes = [i64, i32, i32, u64, i32, vp, vp, vp, vp, vp]
+        L.qem_sample_categorical.argtypes = [i64, i32, i32, u64, i32, vp, vp, vp]
+        L.qem_tables_categorical.argtypes = [i64, i32, i32, i32] + [vp] * 10
+        L.qem_moments_categorical.argtypes = [i64, i32, i32, i32] + [vp] * 7
+        L.qem_mstep_categorical.argtypes = [i64, i32, i32, ctypes.c_double, ctypes.c_double] + [vp] * 9
+        L.qem_loglik_bernoulli_states.argtypes = [i64, i32, i32, vp, vp, vp, vp]
         L.qem_destroy.argtypes = [vp]
         L.qem_destroy.restype = None
         L.qem_bind.argtypes = [vp, ctypes.POINTER(Buffers)]
@@ -103,7 +111,9 @@ def lib() -> ctypes.CDLL:
         for name in ["qem_model_validate", "qem_shard_range", "qem_create", "qem_bind", "qem_sample_q", "qem_estep",
                      "qem_estep_forward", "qem_estep_backward", "qem_reduce_buffer", "qem_mstep", "qem_iterate",
                      "qem_read_flags", "qem_read_mode_hist", "qem_copy_messages", "qem_estep_evidence",
-                     "qem_evidence_root", "qem_workspace_bytes", "qem_create_in", "qem_estep_tables"]:
+                     "qem_evidence_root", "qem_workspace_bytes", "qem_create_in", "qem_estep_tables",
+                     "qem_sample_normal", "qem_sample_categorical", "qem_tables_categorical",
+                     "qem_moments_categorical", "qem_mstep_categorical", "qem_loglik_bernoulli_states"]:
             getattr(L, name).restype = i32
         _lib = L
     return _lib

@@ -366,6 +366,69 @@ qem_status qem_estep_tables(int64_t n, int32_t K, const double* d_f_root, const 
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_tables");
 }
 
+qem_status qem_sample_normal(int64_t rows, int32_t K, int32_t level, uint64_t seed, int32_t iter,
+                             const float* d_mean, const float* d_var, const float* d_eps, float* d_z, void* stream) {
+  if (rows < 0 || K < 1 || iter < 1 || level < 0 || level > 255)
+    return fail(QEM_INVALID_ARGUMENT, "need rows >= 0, K >= 1, iter >= 1, 0 <= level < 256");
+  if (rows > 0 && (!d_mean || !d_var || !d_z)) return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e =
+      qem::launch_sample_rows(rows, K, level, seed, iter, d_mean, d_var, d_eps, d_z, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_sample_normal");
+}
+
+qem_status qem_sample_categorical(int64_t n, int32_t C, int32_t K, uint64_t seed, int32_t iter, const double* d_p,
+                                  int32_t* d_z, void* stream) {
+  if (n < 0 || n > 0xffffffffLL || C < 1 || C > QEM_CAT_MAX_C || K < 1 || iter < 1)
+    return fail(QEM_INVALID_ARGUMENT, "need 0 <= n < 2^32, 1 <= C <= %d, K >= 1, iter >= 1", QEM_CAT_MAX_C);
+  if (n > 0 && (!d_p || !d_z)) return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_cat_sample(n, C, K, seed, iter, d_p, d_z, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_sample_categorical");
+}
+
+qem_status qem_tables_categorical(int64_t n, int32_t C, int32_t K, int32_t d, const float* d_root_z,
+                                  const float* d_root_mean, const float* d_root_var, const double* d_x,
+                                  const double* d_loglik, const double* d_p, const int32_t* d_z, double* d_f_root,
+                                  double* d_f, void* stream) {
+  if (n < 0 || C < 1 || C > QEM_CAT_MAX_C || K < 1 || d < 1) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root ||
+      (n > 0 && (!d_x || !d_loglik || !d_p || !d_z || !d_f)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_cat_tables(n, C, K, d, d_root_z, d_root_mean, d_root_var, d_x, d_loglik, d_p,
+                                               d_z, d_f_root, d_f, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_tables_categorical");
+}
+
+qem_status qem_moments_categorical(int64_t n, int32_t C, int32_t K, int32_t d, const double* d_w_root,
+                                   const float* d_root_z, const double* d_w, const int32_t* d_z, double* d_root_m,
+                                   double* d_pm, void* stream) {
+  if (n < 0 || C < 1 || C > QEM_CAT_MAX_C || K < 1 || d < 1) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!d_w_root || !d_root_z || !d_root_m || (n > 0 && (!d_w || !d_z || !d_pm)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e =
+      qem::launch_cat_moments(n, C, K, d, d_w_root, d_root_z, d_w, d_z, d_root_m, d_pm, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_moments_categorical");
+}
+
+qem_status qem_mstep_categorical(int64_t n, int32_t C, int32_t d, double lam, double var_floor,
+                                 const double* d_root_m, double* d_root_ema, float* d_root_mean, float* d_root_var,
+                                 const double* d_pm, double* d_p_ema, double* d_p, int64_t* d_clamps, void* stream) {
+  if (n < 0 || C < 1 || C > QEM_CAT_MAX_C || d < 1) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!(lam >= 0.0 && lam < 1.0) || !(var_floor > 0.0)) return fail(QEM_INVALID_ARGUMENT, "need 0 <= lam < 1, var_floor > 0");
+  if (!d_root_m || !d_root_ema || !d_root_mean || !d_root_var || (n > 0 && (!d_pm || !d_p_ema || !d_p)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_cat_mstep(n, C, d, lam, var_floor, d_root_m, d_root_ema, d_root_mean, d_root_var,
+                                              d_pm, d_p_ema, d_p, d_clamps, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_mstep_categorical");
+}
+
+qem_status qem_loglik_bernoulli_states(int64_t n, int32_t C, int32_t R, const uint8_t* d_y, const double* d_logit,
+                                       double* d_L, void* stream) {
+  if (n < 0 || C < 1 || C > QEM_CAT_MAX_C || R < 0) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (n > 0 && (!d_L || (R > 0 && (!d_y || !d_logit)))) return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_cat_loglik(n, C, R, d_y, d_logit, d_L, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_loglik_bernoulli_states");
+}
+
 qem_status qem_mstep(qem_ctx* c, int32_t t, void* stream) {
   qem_status s = need_bound(c);
   if (s) return s;

@@ -145,6 +145,37 @@ __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)a.total_quads; q += stride) sample_quad(a, q, t);
 }
 
+// Context-free Gaussian sampler (qem_sample_normal): `rows` latent rows of K samples, one level
+// tag (the Philox counter's top byte) and global row index = instance with dims = 1.
+cudaError_t launch_sample_rows(int64_t rows, int K, int level, uint64_t seed, int32_t iter, const float* qm,
+                               const float* qv, const float* eps, float* z, cudaStream_t st) {
+  SampleArgs a{};
+  a.K = K;
+  a.quads_per_row = (K + 3) / 4;
+  a.fqpr.init((uint32_t)a.quads_per_row);
+  a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  a.t_host = iter;
+  a.d_iter = nullptr;
+  a.nlev = 1;
+  SampleLevel& s = a.lv[0];
+  s.z = z;
+  s.qm = qm;
+  s.qv = qv;
+  s.eps = eps;
+  s.rows = rows;
+  s.dims = 1;
+  s.fdims.init(1u);
+  s.level = level;
+  s.inst_offset = 0;
+  s.quads_begin = 0;
+  a.total_quads = rows * a.quads_per_row;
+  if (a.total_quads == 0) return cudaSuccess;
+  if (a.total_quads >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;
+  const int64_t blocks = (a.total_quads + 255) / 256;
+  k_sample<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps, cudaStream_t st,
                           uint32_t iter_or) {
   SampleArgs a{};

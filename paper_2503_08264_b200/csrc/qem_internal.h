@@ -114,6 +114,20 @@ cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t s);
 // non-Gaussian Q families (qem_expfam.cu)
 cudaError_t launch_estep_tables(int64_t n, int K, const double* f_root, const double* f, double* g, double* log_pe,
                                 double* w_root, double* w, cudaStream_t st);
+cudaError_t launch_sample_rows(int64_t rows, int K, int level, uint64_t seed, int32_t iter, const float* qm,
+                               const float* qv, const float* eps, float* z, cudaStream_t st);
+cudaError_t launch_cat_sample(int64_t n, int C, int K, uint64_t seed, int32_t iter, const double* p, int32_t* z,
+                              cudaStream_t st);
+cudaError_t launch_cat_tables(int64_t n, int C, int K, int d, const float* rz, const float* rm, const float* rv,
+                              const double* x, const double* L, const double* p, const int32_t* z, double* f_root,
+                              double* f, cudaStream_t st);
+cudaError_t launch_cat_mstep(int64_t n, int C, int d, double lam, double floor, const double* root_m, double* root_ema,
+                             float* root_mean, float* root_var, const double* pm, double* p_ema, double* p,
+                             int64_t* clamps, cudaStream_t st);
+cudaError_t launch_cat_loglik(int64_t n, int C, int R, const uint8_t* y, const double* logit, double* L,
+                              cudaStream_t st);
+cudaError_t launch_cat_moments(int64_t n, int C, int K, int d, const double* w_root, const float* rz, const double* w,
+                               const int32_t* z, double* root_m, double* pm, cudaStream_t st);
 cudaError_t launch_mstep_family(int family, int64_t n, int C, double lam, const double* m_new, double* m_ema,
                                 double* params, int32_t* status, cudaStream_t st);
 }  // namespace qem

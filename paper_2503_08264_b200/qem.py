@@ -85,6 +85,10 @@ def shard_range(n: int, rank: int, world: int):
     return b.value, e.value
 
 
+def _ptr(t: Optional[torch.Tensor]) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() else None)
+
+
 def _stream(stream=None) -> ctypes.c_void_p:
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
@@ -299,3 +303,69 @@ class QEM:
             self.close()
         except Exception:
             pass
+
+
+class CategoricalQEM:
+    """QEM for discrete (categorical) latents under a Gaussian root (NEXT row f1, R30):
+    one iteration = qem_sample_normal + qem_sample_categorical + qem_tables_categorical +
+    qem_estep_tables + qem_moments_categorical + qem_mstep_categorical, all on device; this class
+    only owns the buffers and sequences the calls (argument marshalling)."""
+
+    def __init__(self, om, *, new_weight=0.3, schedule_p=0.0, var_floor=1e-8, device="cuda"):
+        if not torch.cuda.is_available():
+            raise _lib.QemError("CategoricalQEM needs a CUDA device (there is no CPU fallback)")
+        self.om, self.device = om, torch.device(device)
+        self.new_weight, self.schedule_p, self.var_floor = new_weight, schedule_p, var_floor
+        n, C, R, d, K = om.n, om.C, om.R, om.d, om.K
+        f32 = dict(dtype=torch.float32, device=self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt)).to(self.device)  # noqa: E731
+        self.x, self.logit, self.y = up(om.x, np.float64), up(om.logit, np.float64), up(om.y, np.uint8)
+        self.L = torch.empty(n, C, **f64)
+        check(lib().qem_loglik_bernoulli_states(n, C, R, _ptr(self.y), _ptr(self.logit), _ptr(self.L), _stream()),
+              "qem_loglik_bernoulli_states")
+        self.root_mean, self.root_var = torch.zeros(d, **f32), torch.ones(d, **f32)
+        self.root_ema = torch.tensor([[0.0, 1.0]] * d, **f64)
+        self.p = torch.full((n, C), 1.0 / C, **f64)
+        self.p_ema = self.p.clone()
+        self.root_z, self.z = torch.empty(d, K, **f32), torch.empty(n, K, dtype=torch.int32, device=self.device)
+        self.f_root, self.f = torch.empty(K, **f64), torch.empty(n, K, K, **f64)
+        self.g, self.w = torch.empty(n, K, **f64), torch.empty(n, K, **f64)
+        self.w_root, self.log_pe = torch.empty(K, **f64), torch.empty(1, **f64)
+        self.root_m, self.pm = torch.empty(d, 2, **f64), torch.empty(n, C, **f64)
+        self.clamps = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def lam(self, t: int) -> float:
+        """History weight (R5): 1 - new_weight, or 1 - t^-p with a schedule."""
+        return 1.0 - (t ** -self.schedule_p if self.schedule_p > 0 else self.new_weight)
+
+    def estep(self, t: int, seed: int, root_eps: Optional[torch.Tensor] = None, stream=None) -> None:
+        om, L, s = self.om, lib(), _stream(stream)
+        n, C, d, K = om.n, om.C, om.d, om.K
+        eps = _ptr(root_eps) if root_eps is not None else None
+        check(L.qem_sample_normal(d, K, 0, seed, t, _ptr(self.root_mean), _ptr(self.root_var), eps, _ptr(self.root_z),
+                                  s), "qem_sample_normal")
+        check(L.qem_sample_categorical(n, C, K, seed, t, _ptr(self.p), _ptr(self.z), s), "qem_sample_categorical")
+        check(L.qem_tables_categorical(n, C, K, d, _ptr(self.root_z), _ptr(self.root_mean), _ptr(self.root_var),
+                                       _ptr(self.x), _ptr(self.L), _ptr(self.p), _ptr(self.z), _ptr(self.f_root),
+                                       _ptr(self.f), s), "qem_tables_categorical")
+        check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
+                                 _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        check(L.qem_moments_categorical(n, C, K, d, _ptr(self.w_root), _ptr(self.root_z), _ptr(self.w), _ptr(self.z),
+                                        _ptr(self.root_m), _ptr(self.pm), s), "qem_moments_categorical")
+
+    def mstep(self, t: int, stream=None) -> None:
+        om = self.om
+        check(lib().qem_mstep_categorical(om.n, om.C, om.d, self.lam(t), self.var_floor, _ptr(self.root_m),
+                                          _ptr(self.root_ema), _ptr(self.root_mean), _ptr(self.root_var),
+                                          _ptr(self.pm), _ptr(self.p_ema), _ptr(self.p), _ptr(self.clamps),
+                                          _stream(stream)), "qem_mstep_categorical")
+
+    def step(self, t: int, seed: int, root_eps=None, stream=None) -> None:
+        self.estep(t, seed, root_eps, stream)
+        self.mstep(t, stream)
+
+    def set_state(self, st: dict) -> None:
+        """Teacher forcing (parity tests): Q and EMA state from host arrays."""
+        for k in ("root_mean", "root_var", "root_ema", "p", "p_ema"):
+            getattr(self, k).copy_(torch.from_numpy(np.asarray(st[k])).to(getattr(self, k).dtype))

@@ -184,3 +184,56 @@ def random_q(m: Model, seed: int, spread: float = 1.0):
         out.append((mean, var))
     return out
 
+
+
+# ------------------------------------------------------------------ discrete latents (row f1)
+
+
+@dataclasses.dataclass
+class Occupancy:
+    """Occupancy-shaped discrete-latent model (R30): root r in R^d
+    ~ N(0, I); per site i a categorical z_i in {0..C-1} with prior logits x_ic . r; R repeated
+    Bernoulli detections y_ir with per-state logits l_irc.  Default shape: J=12 species x M=6
+    years x I=200 routes = 14400 sites, R=5 repeats, C=2 (absent / present),
+    d=2 (occupancy intercept, weather weight)."""
+    n: int
+    C: int
+    R: int
+    d: int
+    K: int
+    x: np.ndarray       # [n][C][d] float64 state covariates (state 0: zeros)
+    logit: np.ndarray   # [n][R][C] float64 detection logits
+    y: np.ndarray       # [n][R] uint8
+    r_true: np.ndarray  # [d] the root draw the data came from
+    z_true: np.ndarray  # [n] int
+
+
+def occupancy(n: int = 14400, R: int = 5, K: int = 64, C: int = 2, seed: int = 6) -> Occupancy:
+    """Ancestral draw from the prior (numpy PCG64, `seed`).  Covariates: weather_i ~ N(0, 1);
+    present-state covariates (1, weather_i) (further states: independent N(0, 1) covariates);
+    detection logits: absent -10 (the paper's false-positive logit), present
+    2 quality_ir - 0.5 with quality_ir ~ Bern(0.8) (the paper's quality covariate with its weight
+    fixed), further states N(0, 1)."""
+    rng = np.random.default_rng(seed)
+    d = 2
+    x = np.zeros((n, C, d))
+    weather = rng.normal(0.0, 1.0, n)
+    x[:, 1, 0] = 1.0
+    x[:, 1, 1] = weather
+    if C > 2:
+        x[:, 2:, :] = rng.normal(0.0, 1.0, (n, C - 2, d))
+    logit = np.zeros((n, R, C))
+    logit[:, :, 0] = -10.0
+    quality = rng.random((n, R)) < 0.8
+    logit[:, :, 1] = 2.0 * quality - 0.5
+    if C > 2:
+        logit[:, :, 2:] = rng.normal(0.0, 1.0, (n, R, C - 2))
+    r = rng.normal(0.0, 1.0, d)
+    eta = x @ r                                              # [n][C]
+    pz = np.exp(eta - eta.max(axis=1, keepdims=True))
+    pz /= pz.sum(axis=1, keepdims=True)
+    u = rng.random(n)
+    z = np.minimum((u[:, None] >= np.cumsum(pz, axis=1)).sum(axis=1), C - 1)
+    lz = logit[np.arange(n), :, z]                           # [n][R]
+    y = (rng.random((n, R)) < 1.0 / (1.0 + np.exp(-lz))).astype(np.uint8)
+    return Occupancy(n=n, C=C, R=R, d=d, K=K, x=x, logit=logit, y=y, r_true=r, z_true=z)
