@@ -293,12 +293,13 @@ def run_gpu(args):
     if not args.no_e2e:
         e2e = run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce)
     tc = g.pair_path() == 1
-    fresh = mfam = disc = None
+    fresh = mfam = disc = pred = None
     if world == 1 and not args.no_variants:
         g.close()  # free the first context's workspace before the variant's
         fresh = run_fresh_variant(args, m, data, dev, seed)
         mfam = run_mstep_family_variant(dev)
         disc = run_discrete_variant(dev)
+        pred = run_predictive_variant(m, data, dev, seed)
 
     # ----------------------------------------------------------- roofline
     local_pairs = (ge - gb) * m.K * m.K
@@ -359,7 +360,8 @@ def run_gpu(args):
         "gpu_launches": n_launched,
         "clocks": clk,
         "flags": {"device_flags": flags, "var_clamps": clamps},
-        "variants": {"fresh_denominator": fresh, "mstep_family": mfam, "discrete_occupancy": disc},
+        "variants": {"fresh_denominator": fresh, "mstep_family": mfam, "discrete_occupancy": disc,
+                     "predictive_loglik": pred},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -458,6 +460,39 @@ def run_fresh_variant(args, m, data, dev, seed):
     g.close()
     return {"ms_per_step": ms, "value": m.pairs / (ms * 1e-3), "unit": "factor-pairs/s (E-step pairs; the evidence "
             "pass's forward pairs are extra work)", "qem_iters_per_s": 1e3 / ms}
+
+
+def run_predictive_variant(m, data, dev, seed, S=100, reps=5):
+    """NEXT row f3 (R31): after an E-step of the bench workload, S = 100 backward index
+    resamples ("averaged over 100 predictive samples") + the predictive
+    log-likelihood of a held-out set of J observations per group; CUDA-event timed."""
+    import torch
+    from paper_2503_08264_b200 import synth
+    from paper_2503_08264_b200.qem import QEM
+    g = QEM(m, device=dev)
+    g.set_data(data)
+    g.set_q(synth.initial_q(m))
+    g.iterate(1, 4, seed=seed)
+    g.sample_q(seed=seed, iter=5)
+    g.estep()
+    test = synth.make_test_data(m, data)
+    ir, ix = g.backward_resample(S, 1)
+    g.predictive_loglik(ix, test)
+    torch.cuda.synchronize()
+    st, mid, en = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    st.record()
+    for r in range(reps):
+        ir, ix = g.backward_resample(S, 2 + r)
+    mid.record()
+    for r in range(reps):
+        pll, ll_s, _ = g.predictive_loglik(ix, test)
+    en.record()
+    torch.cuda.synchronize()
+    out = {"S": S, "resample_ms": st.elapsed_time(mid) / reps, "predict_ms": mid.elapsed_time(en) / reps,
+           "pll": float(pll.item()), "J_test": int(m.J),
+           "resampled_rows_per_s": S * m.n * m.K / (st.elapsed_time(mid) / reps * 1e-3)}
+    g.close()
+    return out
 
 
 def run_discrete_variant(dev, steps=10):

@@ -232,6 +232,29 @@ qem_status qem_evidence_root(qem_ctx* ctx, void* stream);
    first multiplied by exp(log_pe - log_pe_fresh) (read on the device).                */
 qem_status qem_mstep(qem_ctx* ctx, int32_t t, void* stream);
 
+/* ---- Predictive log-likelihood (NEXT row f3; R31) ----
+   qem_backward_resample: after qem_estep (or qem_estep_forward + the all-reduce + the root pass
+   of qem_estep_backward) on a two-level context, draw S index tuples from the MPIW posterior
+   over index tuples (r_k / sum r, Eq. 7a-c) by ancestral sampling in reverse elimination order:
+   k_root ~ w_root, then k_i ~ P_i(k' | k_root) = exp(B_i(k_root,k') + A_i(k') - ln K - g_i(k_root))
+   for every LOCAL instance i, by inverse CDF (fp64 prefix in k' order) on 24-bit Philox
+   uniforms: word 0 of Philox4x32-10 at counter (s, 0, 0, 5 << 24) for the root and
+   (s, 1 + global i, 0, 5 << 24) for instance i, key = seed -- identical across world sizes.
+   d_idx_root [S], d_idx [S][n_local] int32 (device, caller-owned).
+   qem_predictive_loglik: ll_part[s][i] = sum_j log p(x_test_ij | z_i^{idx[s][i]}) (fp64;
+   test data laid out as the training data: Gaussian float [n_local][J_test], Bernoulli
+   uint8 x [n_local][J_test][d] + y [n_local][J_test]), d_ll_s[s] = sum_i ll_part[s][i] (local
+   instances, fixed order) and, when d_pll != NULL, d_pll = log (1/S) sum_s exp(ll_s) -- valid
+   at world == 1; sharded runs SUM-all-reduce d_ll_s and call qem_logmeanexp.  Errors:
+   QEM_UNSUPPORTED for the three-level family, QEM_INVALID_ARGUMENT for S < 1 or null arrays. */
+qem_status qem_backward_resample(qem_ctx* ctx, int32_t S, uint64_t seed, int32_t* d_idx_root, int32_t* d_idx,
+                                 void* stream);
+qem_status qem_predictive_loglik(qem_ctx* ctx, int32_t S, const int32_t* d_idx, int32_t J_test,
+                                 const void* d_x_test, const uint8_t* d_y_test, double* d_ll_part,
+                                 double* d_ll_s, double* d_pll, void* stream);
+/* d_out[0] = log (1/n) sum_i exp(d_x[i]) (fp64, fixed order), n >= 1. */
+qem_status qem_logmeanexp(int64_t n, const double* d_x, double* d_out, void* stream);
+
 /* ---- Discrete latents under a continuous root (NEXT row f1, E-step side; R30) ----
    Occupancy-shaped model: root r in R^d, prior N(0, I), Q_root =
    N(m, diag v); per instance i a categorical z_i in {0..C-1}, prior logits eta_ic(r) = x_ic . r,

@@ -14,4 +14,6 @@ Modules:
   closed_form.py conjugate-Gaussian posterior and evidence (pins the K->inf limit).
   expfam.py      Gamma/Beta/Bernoulli/Categorical M-steps from mean parameters (scipy).
   tables.py      the E-step on explicit log-factor tables: elimination + enumeration (numpy).
+  discrete.py    discrete (categorical) latents under a Gaussian root (numpy).
+  predict.py     backward index resampling + predictive log-likelihood (numpy).
 """

@@ -46,8 +46,9 @@ def _finish(logr, zs_per_axis):
     return log_pe, ws, m1s, m2s
 
 
-def estep2(m, z, q, data):
-    """Enumerate a two-level model (axes: root, group 0..n-1). Same I/O as oracle.estep."""
+def estep2(m, z, q, data, joint=False):
+    """Enumerate a two-level model (axes: root, group 0..n-1). Same I/O as oracle.estep; with
+    joint=True also the normalised weight of every index tuple, [K]*(n+1) (root axis first)."""
     K, n, d, R = m.K, m.n, m.d, m.R
     assert K ** (n + 1) <= 2_000_000, "enumeration guard"
     zr = np.asarray(z[0], np.float64).reshape(R, K)
@@ -86,8 +87,11 @@ def estep2(m, z, q, data):
         logr = logr + _axis(u, [i + 1], N)
     zs = [zr] + [zg[i] for i in range(n)]
     log_pe, ws, m1s, m2s = _finish(logr, zs)
-    return dict(log_pe=log_pe, w=[ws[0][None, :], np.stack(ws[1:])],
-                m1=[m1s[0], np.concatenate(m1s[1:])], m2=[m2s[0], np.concatenate(m2s[1:])])
+    out = dict(log_pe=log_pe, w=[ws[0][None, :], np.stack(ws[1:])],
+               m1=[m1s[0], np.concatenate(m1s[1:])], m2=[m2s[0], np.concatenate(m2s[1:])])
+    if joint:
+        out["joint"] = np.exp(logr - logsumexp(logr))
+    return out
 
 
 def estep3(m, z, q, data):

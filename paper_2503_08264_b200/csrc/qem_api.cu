@@ -366,6 +366,36 @@ qem_status qem_estep_tables(int64_t n, int32_t K, const double* d_f_root, const 
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_tables");
 }
 
+qem_status qem_backward_resample(qem_ctx* c, int32_t S, uint64_t seed, int32_t* d_idx_root, int32_t* d_idx,
+                                 void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "backward resampling: two-level family only");
+  if (S < 1 || !d_idx_root || !d_idx) return fail(QEM_INVALID_ARGUMENT, "need S >= 1 and output arrays");
+  const cudaError_t e = qem::launch_resample(c, S, seed, d_idx_root, d_idx, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_backward_resample");
+}
+
+qem_status qem_predictive_loglik(qem_ctx* c, int32_t S, const int32_t* d_idx, int32_t J_test, const void* d_x_test,
+                                 const uint8_t* d_y_test, double* d_ll_part, double* d_ll_s, double* d_pll,
+                                 void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "predictive log-likelihood: two-level family only");
+  if (S < 1 || J_test < 0 || !d_idx || !d_ll_part || !d_ll_s || (J_test > 0 && !d_x_test) ||
+      (J_test > 0 && c->desc.obs_kind == QEM_OBS_BERNOULLI_LOGIT && !d_y_test))
+    return fail(QEM_INVALID_ARGUMENT, "need S >= 1, J_test >= 0 and the arrays");
+  const cudaError_t e = qem::launch_predict(c, S, d_idx, J_test, d_x_test, d_y_test, d_ll_part, d_ll_s, d_pll,
+                                            (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_predictive_loglik");
+}
+
+qem_status qem_logmeanexp(int64_t n, const double* d_x, double* d_out, void* stream) {
+  if (n < 1 || !d_x || !d_out) return fail(QEM_INVALID_ARGUMENT, "need n >= 1 and arrays");
+  const cudaError_t e = qem::launch_logmeanexp(n, d_x, d_out, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_logmeanexp");
+}
+
 qem_status qem_sample_normal(int64_t rows, int32_t K, int32_t level, uint64_t seed, int32_t iter,
                              const float* d_mean, const float* d_var, const float* d_eps, float* d_z, void* stream) {
   if (rows < 0 || K < 1 || iter < 1 || level < 0 || level > 255)

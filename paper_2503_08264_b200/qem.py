@@ -284,6 +284,34 @@ class QEM:
         return dg, c
 
     # ---------------------------------------------------------- readback
+    def backward_resample(self, S: int, seed: int, stream=None):
+        """S index tuples from the MPIW posterior after an E-step (qem_backward_resample):
+        (idx_root [S], idx [S][n_local]) int32 device tensors."""
+        idx_root = torch.empty(S, dtype=torch.int32, device=self.device)
+        idx = torch.empty(S, self.n_local, dtype=torch.int32, device=self.device)
+        check(lib().qem_backward_resample(self.ctx, int(S), int(seed), _ptr(idx_root), _ptr(idx), _stream(stream)),
+              "qem_backward_resample")
+        return idx_root, idx
+
+    def predictive_loglik(self, idx: torch.Tensor, test: "synth.Data", stream=None):
+        """Predictive log-likelihood of held-out observations of the local groups at the resampled
+        latents (qem_predictive_loglik): returns (pll [1], ll_s [S], ll_part [S][n_local])."""
+        m, b, e = self.m, self.g_begin, self.g_end
+        S = idx.shape[0]
+        if m.obs_kind == synth.OBS_GAUSS:
+            x = torch.from_numpy(np.ascontiguousarray(test.xg[b:e], np.float32)).to(self.device)
+            y = None
+        else:
+            x = torch.from_numpy(np.ascontiguousarray(test.xb[b:e], np.uint8)).to(self.device)
+            y = torch.from_numpy(np.ascontiguousarray(test.yb[b:e], np.uint8)).to(self.device)
+        J = x.shape[1]
+        f64 = dict(dtype=torch.float64, device=self.device)
+        ll_part, ll_s, pll = torch.empty(S, self.n_local, **f64), torch.empty(S, **f64), torch.empty(1, **f64)
+        check(lib().qem_predictive_loglik(self.ctx, int(S), _ptr(idx), int(J), _ptr(x), _ptr(y), _ptr(ll_part),
+                                          _ptr(ll_s), _ptr(pll), _stream(stream)), "qem_predictive_loglik")
+        self._test_keep = (x, y)  # alive until the stream has consumed them
+        return pll, ll_s, ll_part
+
     def result(self):
         """Host copies of the last E-step: log_pe, w / m1 / v per level, plus Q and EMA state."""
         torch.cuda.current_stream().synchronize()

@@ -156,6 +156,25 @@ def make_data(m: Model, seed: Optional[int] = None) -> Data:
     return Data(xp=x, yp=y, truth={"g": g, "beta": beta, "u": u, "v": v})
 
 
+def make_test_data(m: Model, data: Data, J_test: Optional[int] = None, seed: Optional[int] = None) -> Data:
+    """Held-out observations of the SAME groups (a separate 'test' set), drawn
+    from the likelihood at the training draw's true group latents (two-level family); seed
+    defaults to 1000 + config id, J_test to the training J."""
+    assert m.family == FAMILY_TWO_LEVEL
+    J = m.J if J_test is None else J_test
+    rng = np.random.Generator(np.random.PCG64(1000 + m.config_id if seed is None else seed))
+    z = data.truth["z"]
+    out = Data(truth=data.truth)
+    if m.obs_kind == OBS_GAUSS:
+        out.xg = (z[:, 0:1] + np.sqrt(m.obs_var) * rng.standard_normal((m.n, J))).astype(np.float32)
+    else:
+        xb = (rng.random((m.n, J, m.d)) < 0.2).astype(np.uint8)
+        eta = np.einsum("njd,nd->nj", xb.astype(np.float64), z)
+        out.xb = xb
+        out.yb = (rng.random((m.n, J)) < 1.0 / (1.0 + np.exp(-eta))).astype(np.uint8)
+    return out
+
+
 def eps_normal(shape, seed: int) -> np.ndarray:
     """Host standard-normal draws (fp32) for the sampler's parity mode."""
     rng = np.random.Generator(np.random.PCG64(seed))
