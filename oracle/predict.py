@@ -66,8 +66,9 @@ def log_conditionals(m, z, q, data, g, i):
     return B + A[None, :] - np.log(K) - np.asarray(g)[i][:, None]
 
 
-def resample(m, z, q, data, est, S, seed):
-    """S index tuples: idx_root [S], idx [S][n], and the CDF margins of every draw."""
+def resample(m, z, q, data, est, S, seed, g_begin=0):
+    """S index tuples: idx_root [S], idx [S][n], and the CDF margins of every draw.  g_begin: the
+    global index of local instance 0 (the uniforms are keyed by the global instance)."""
     w_root = np.asarray(est["w"][0]).reshape(-1)
     idx_root, mr = np.zeros(S, np.int32), np.zeros(S)
     idx, mg = np.zeros((S, m.n), np.int32), np.zeros((S, m.n))
@@ -76,7 +77,7 @@ def resample(m, z, q, data, est, S, seed):
         idx_root[s], mr[s] = _inverse_cdf(w_root, _uniform(s, 0, seed))
         for i in range(m.n):
             row = logp[i][idx_root[s]]
-            idx[s, i], mg[s, i] = _inverse_cdf(np.exp(row - row.max()), _uniform(s, 1 + i, seed))
+            idx[s, i], mg[s, i] = _inverse_cdf(np.exp(row - row.max()), _uniform(s, 1 + g_begin + i, seed))
     return dict(idx_root=idx_root, idx=idx, margin_root=mr, margin=mg)
 
 

@@ -73,6 +73,18 @@ class ShardedQEM:
         self.b.mstep(t)
 
 
+    def predictive_loglik(self, S: int, seed: int, test):
+        """Row f3 across ranks: every rank draws S index tuples for its local
+        groups (the root draws coincide: replicated root weights, the same Philox counters), sums
+        its groups' held-out log-likelihood per draw, SUM-all-reduces the [S] partials and takes
+        log mean exp.  Returns (pll, ll_s) on every rank."""
+        idx_root, idx = self.b.backward_resample(S, seed)
+        _, ll_s, _ = self.b.predictive_loglik(idx, test)
+        if self.world > 1:
+            dist.all_reduce(ll_s, op=dist.ReduceOp.SUM, group=self.group)
+        return self.b.logmeanexp(ll_s), ll_s
+
+
 def root_digest(root_weights: torch.Tensor) -> str:
     """Digest of this rank's root weights (must be identical on all ranks)."""
     return hashlib.sha256(root_weights.detach().cpu().numpy().tobytes()).hexdigest()

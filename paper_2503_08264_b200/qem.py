@@ -67,6 +67,14 @@ def estep_tables(f_root: torch.Tensor, f: torch.Tensor, stream=None):
     return out
 
 
+def logmeanexp(x: torch.Tensor, stream=None) -> torch.Tensor:
+    """log (1/n) sum exp(x) of a float64 device vector (qem_logmeanexp); returns a [1] tensor."""
+    assert x.dtype == torch.float64 and x.is_cuda
+    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    check(lib().qem_logmeanexp(x.numel(), _ptr(x.contiguous()), _ptr(out), _stream(stream)), "qem_logmeanexp")
+    return out
+
+
 def workspace_bytes(m, group_begin=0, group_end=None, *, new_weight=0.3, schedule_p=0.0, var_floor=1e-8,
                     fresh_denominator=False) -> int:
     """Device workspace a context over [group_begin, group_end) needs (qem_workspace_bytes)."""
@@ -284,6 +292,9 @@ class QEM:
         return dg, c
 
     # ---------------------------------------------------------- readback
+    def logmeanexp(self, x: torch.Tensor) -> torch.Tensor:
+        return logmeanexp(x)
+
     def backward_resample(self, S: int, seed: int, stream=None):
         """S index tuples from the MPIW posterior after an E-step (qem_backward_resample):
         (idx_root [S], idx [S][n_local]) int32 device tensors."""

@@ -42,6 +42,7 @@ class OracleShardBackend:
         else:
             self.data = synth.Data(xb=data.xb[begin:end], yb=data.yb[begin:end])
         self.plate_sum = torch.zeros(m.K + 1, dtype=torch.float64)
+        self.begin, self.end = begin, end
 
     def sample_q(self, seed=0, iter=1, eps=None):
         pass  # samples are given (host eps path)
@@ -66,6 +67,27 @@ class OracleShardBackend:
 
     def mstep(self, t):
         pass
+
+    def backward_resample(self, S, seed):
+        from oracle import predict as op
+        est = dict(w=[self.w_root.numpy()[None, :]], g=self.g)
+        r = op.resample(self.m, self.z, self.q, self.data, est, S, seed, g_begin=self.begin)
+        return torch.from_numpy(r["idx_root"]), torch.from_numpy(r["idx"])
+
+    def predictive_loglik(self, idx, test):
+        from oracle import predict as op
+        part = op.test_loglik(self.m, self.z, self._test_shard(test), idx.numpy())
+        return None, torch.from_numpy(part.sum(axis=1)), torch.from_numpy(part)
+
+    def _test_shard(self, test):
+        from paper_2503_08264_b200 import synth
+        b, e = self.begin, self.end
+        if test.xg is not None:
+            return synth.Data(xg=test.xg[b:e])
+        return synth.Data(xb=test.xb[b:e], yb=test.yb[b:e])
+
+    def logmeanexp(self, ll_s):
+        return float(logsumexp(ll_s.numpy()) - np.log(ll_s.numel()))
 
 
 def _worker(rank, world, port, cid, n, K, out_q):
@@ -173,3 +195,55 @@ def test_python_and_c_shard_ranges_agree():
         for world in (1, 2, 3, 4, 8):
             for r in range(world):
                 assert qdist.shard_range(n, r, world) == qem.shard_range(n, r, world)
+
+
+def _worker_predict(rank, world, port, n, K, S, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from helpers import make_case
+        from paper_2503_08264_b200 import dist as qdist, synth
+        m = synth.config(4, n=n, K=K)
+        data, q, eps, z = make_case(m)
+        test = synth.make_test_data(m, data)
+        b, e = qdist.shard_range(m.n, rank, world)
+        be = OracleShardBackend(m, data, q, z, b, e)
+        runner = qdist.ShardedQEM(be)
+        runner.estep()
+        pll, ll_s = runner.predictive_loglik(S, 13, test)
+        out_q.put((rank, pll, ll_s.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_predictive_loglik():
+    """Row f3 across 2 ranks: per-rank resampling of the local groups + the [S] all-reduce gives
+    the single-process predictive log-likelihood (same draws: global instance keys)."""
+    from helpers import make_case
+    from oracle import oracle as orc
+    from oracle import predict as op
+    from paper_2503_08264_b200 import synth
+    world, n, K, S = 2, 19, 16, 40
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_predict, args=(r, world, port, n, K, S, q_out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q_out.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = synth.config(4, n=n, K=K)
+    data, q, eps, z = make_case(m)
+    test = synth.make_test_data(m, data)
+    est = orc.estep(m, z, q, data)
+    r = op.resample(m, z, q, data, est, S, 13)
+    pll_ref, ll_ref = op.predictive_loglik(op.test_loglik(m, z, test, r["idx"]))
+    for rank, pll, ll_s in res:
+        np.testing.assert_allclose(ll_s, ll_ref, rtol=1e-12)
+        assert abs(pll - pll_ref) <= 1e-12 * abs(pll_ref), (rank, pll, pll_ref)
