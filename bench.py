@@ -498,27 +498,29 @@ def run_predictive_variant(m, data, dev, seed, S=100, reps=5):
 def run_discrete_variant(dev, steps=10):
     """NEXT row f1, E-step side (R30): one QEM iteration of the Occupancy-shaped
     discrete-latent model (14400 categorical sites under a 2-d Gaussian root, K = 64; device
-    Philox samples, explicit fp64 log-factor tables), timed with CUDA events after 3 warm-up
-    iterations."""
+    Philox samples), with the factorised E-step (O(n K C)) and with materialised fp64 log-factor
+    tables (O(n K^2)); CUDA events after 3 warm-up iterations."""
     import torch
     from paper_2503_08264_b200 import synth
     from paper_2503_08264_b200.qem import CategoricalQEM
     om = synth.occupancy()
-    g = CategoricalQEM(om, device=dev)
-    for t in range(1, 4):
-        g.step(t, 7)
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    st.record()
-    for t in range(4, 4 + steps):
-        g.step(t, 7)
-    en.record()
-    torch.cuda.synchronize()
-    ms = st.elapsed_time(en) / steps
-    pairs = om.n * om.K * om.K
-    return {"workload": f"occupancy n={om.n} C={om.C} R={om.R} d={om.d} K={om.K}", "ms_per_step": ms,
-            "value": pairs / (ms * 1e-3), "unit": "factor-pairs/s (tables path, fp64)",
-            "qem_iters_per_s": 1e3 / ms}
+    out = {"workload": f"occupancy n={om.n} C={om.C} R={om.R} d={om.d} K={om.K}"}
+    for name, tables in (("factorised", False), ("tables", True)):
+        g = CategoricalQEM(om, device=dev, tables=tables)
+        for t in range(1, 4):
+            g.step(t, 7)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        st.record()
+        for t in range(4, 4 + steps):
+            g.step(t, 7)
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / steps
+        out[name] = {"ms_per_step": ms, "qem_iters_per_s": 1e3 / ms,
+                     "factor_pairs_per_s": om.n * om.K * om.K / (ms * 1e-3)}
+        del g
+    return out
 
 
 def run_mstep_family_variant(dev, n=1_000_000, reps=10):

@@ -286,6 +286,17 @@ qem_status qem_tables_categorical(int64_t n, int32_t C, int32_t K, int32_t d, co
                                   const float* d_root_mean, const float* d_root_var, const double* d_x,
                                   const double* d_loglik, const double* d_p, const int32_t* d_z,
                                   double* d_f_root, double* d_f, void* stream);
+/* The same E-step without materialising the tables (O(n K C) instead of O(n K^2)): f_i(k,k')
+   depends on k' only through the state z_i^k', so with n_i(c) = #{k' : z_i^k' = c},
+   g_i(k) = log sum_c n_i(c) exp(h_i(k,c)) - ln K and w_i(k') = W_i(z_i^k'), W_i(c) =
+   sum_k w_root(k) exp(h_i(k,c) - ln K - g_i(k)), h_i(k,c) the table entry of state c.  Outputs
+   as qem_tables_categorical + qem_estep_tables (d_f_root [K], d_g [n][K], d_log_pe [1],
+   d_w_root [K], d_w [n][K]; d_w doubles as the plate-sum scratch).  K <= QEM_TABLES_MAX_K. */
+qem_status qem_estep_categorical(int64_t n, int32_t C, int32_t K, int32_t d, const float* d_root_z,
+                                 const float* d_root_mean, const float* d_root_var, const double* d_x,
+                                 const double* d_loglik, const double* d_p, const int32_t* d_z,
+                                 double* d_f_root, double* d_g, double* d_log_pe, double* d_w_root,
+                                 double* d_w, void* stream);
 /* Moments (Eq. 7a) from qem_estep_tables' weights: d_root_m [d][2] = (E r_e, E r_e^2) under
    d_w_root [K]; d_pm [n][C] = E onehot(z_i) = sum_k' w_i(k') [z_i^k' = c] under d_w [n][K]. */
 qem_status qem_moments_categorical(int64_t n, int32_t C, int32_t K, int32_t d, const double* d_w_root,

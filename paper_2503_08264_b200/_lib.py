@@ -20,7 +20,7 @@ EXPORTS = [
     "qem_model_validate", "qem_shard_range", "qem_create", "qem_workspace_bytes", "qem_create_in", "qem_destroy", "qem_bind", "qem_sample_q",
     "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_estep_evidence",
     "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_estep_tables", "qem_sample_normal",
-    "qem_sample_categorical", "qem_tables_categorical", "qem_moments_categorical", "qem_mstep_categorical",
+    "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical", "qem_moments_categorical", "qem_mstep_categorical",
     "qem_loglik_bernoulli_states", "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_iterate",
     "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_pair_path", "qem_copy_messages", "qem_status_str", "qem_last_error",
     "qem_version",
@@ -79,6 +79,7 @@ def lib() -> ctypes.CDLL:
         L.qem_sample_categorical.argtypes = [i64, i32, i32, u64, i32, vp, vp, vp]
         L.qem_tables_categorical.argtypes = [i64, i32, i32, i32] + [vp] * 10
         L.qem_moments_categorical.argtypes = [i64, i32, i32, i32] + [vp] * 7
+        L.qem_estep_categorical.argtypes = [i64, i32, i32, i32] + [vp] * 13
         L.qem_mstep_categorical.argtypes = [i64, i32, i32, ctypes.c_double, ctypes.c_double] + [vp] * 9
         L.qem_loglik_bernoulli_states.argtypes = [i64, i32, i32, vp, vp, vp, vp]
         L.qem_backward_resample.argtypes = [vp, i32, u64, vp, vp, vp]
@@ -115,7 +116,7 @@ def lib() -> ctypes.CDLL:
                      "qem_estep_forward", "qem_estep_backward", "qem_reduce_buffer", "qem_mstep", "qem_iterate",
                      "qem_read_flags", "qem_read_mode_hist", "qem_copy_messages", "qem_estep_evidence",
                      "qem_evidence_root", "qem_workspace_bytes", "qem_create_in", "qem_estep_tables",
-                     "qem_sample_normal", "qem_sample_categorical", "qem_tables_categorical",
+                     "qem_sample_normal", "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical",
                      "qem_moments_categorical", "qem_mstep_categorical", "qem_loglik_bernoulli_states",
                      "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp"]:
             getattr(L, name).restype = i32

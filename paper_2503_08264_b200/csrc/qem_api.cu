@@ -428,6 +428,20 @@ qem_status qem_tables_categorical(int64_t n, int32_t C, int32_t K, int32_t d, co
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_tables_categorical");
 }
 
+qem_status qem_estep_categorical(int64_t n, int32_t C, int32_t K, int32_t d, const float* d_root_z,
+                                 const float* d_root_mean, const float* d_root_var, const double* d_x,
+                                 const double* d_loglik, const double* d_p, const int32_t* d_z, double* d_f_root,
+                                 double* d_g, double* d_log_pe, double* d_w_root, double* d_w, void* stream) {
+  if (n < 0 || C < 1 || C > QEM_CAT_MAX_C || K < 1 || K > QEM_TABLES_MAX_K || d < 1)
+    return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root || !d_log_pe || !d_w_root ||
+      (n > 0 && (!d_x || !d_loglik || !d_p || !d_z || !d_g || !d_w)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_cat_estep(n, C, K, d, d_root_z, d_root_mean, d_root_var, d_x, d_loglik, d_p, d_z,
+                                              d_f_root, d_g, d_log_pe, d_w_root, d_w, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_categorical");
+}
+
 qem_status qem_moments_categorical(int64_t n, int32_t C, int32_t K, int32_t d, const double* d_w_root,
                                    const float* d_root_z, const double* d_w, const int32_t* d_z, double* d_root_m,
                                    double* d_pm, void* stream) {

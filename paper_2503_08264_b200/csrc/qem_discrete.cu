@@ -121,6 +121,140 @@ __global__ void __launch_bounds__(kCatTabThreads) k_cat_tables(int64_t n, int C,
   }
 }
 
+// ---- the factorised E-step (qem_estep_categorical): f_i(k, k') = h_i(k, z_i^k') depends on k'
+// only through the state, so with n_i(c) = #{k' : z_i^k' = c}
+//   g_i(k)  = log sum_c n_i(c) exp(h_i(k, c)) - ln K                      (states with n_i(c) > 0)
+//   w_i(k') = W_i(z_i^k'),  W_i(c) = sum_k w_root(k) exp(h_i(k, c) - ln K - g_i(k))
+// -- the explicit-table results (Eq. 7) in O(n K C) instead of O(n K^2).
+__device__ __forceinline__ void cat_h_row(int64_t i, int k, int C, int K, int d, const double* __restrict__ x,
+                                          const float* __restrict__ rz, const double* hc,
+                                          double (&h)[QEM_CAT_MAX_C]) {
+  double mx = -CUDART_INF;
+#pragma unroll
+  for (int c = 0; c < QEM_CAT_MAX_C; ++c) {
+    double eta = 0.0;
+    if (c < C)
+      for (int e = 0; e < d; ++e) eta += x[(i * C + c) * d + e] * (double)rz[(int64_t)e * K + k];
+    h[c] = eta;
+    if (c < C) mx = fmax(mx, eta);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < QEM_CAT_MAX_C; ++c)
+    if (c < C) s += exp(h[c] - mx);
+  const double lse = mx + log(s);
+#pragma unroll
+  for (int c = 0; c < QEM_CAT_MAX_C; ++c)
+    if (c < C) h[c] = (h[c] - lse) + hc[c];
+}
+
+// Warp-per-instance state: the counts n_i(c) by ballots over the instance's K samples and the
+// per-state constants L_i(c) - log p_i(c) (lane c computes, every lane receives) -- no block sync.
+__device__ __forceinline__ void cat_warp_setup(int64_t i, int C, int K, const double* L, const double* p,
+                                               const int32_t* z, int lane, double (&hc)[QEM_CAT_MAX_C],
+                                               int (&cnt)[QEM_CAT_MAX_C]) {
+  const double mine = lane < C ? L[i * C + lane] - log(p[i * C + lane]) : 0.0;
+#pragma unroll
+  for (int c = 0; c < QEM_CAT_MAX_C; ++c) {
+    hc[c] = __shfl_sync(0xffffffffu, mine, c);
+    cnt[c] = 0;
+  }
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    const int k = k0 + lane;
+    const int zc = k < K ? z[i * K + k] : -1;
+#pragma unroll
+    for (int c = 0; c < QEM_CAT_MAX_C; ++c) cnt[c] += __popc(__ballot_sync(0xffffffffu, zc == c));
+  }
+}
+
+constexpr int kCatWarps = 8;
+
+__global__ void __launch_bounds__(kCatWarps * 32) k_cat_fwd(int64_t n, int C, int K, int d,
+                                                            const float* __restrict__ rz,
+                                                            const float* __restrict__ rm,
+                                                            const float* __restrict__ rv,
+                                                            const double* __restrict__ x,
+                                                            const double* __restrict__ L,
+                                                            const double* __restrict__ p,
+                                                            const int32_t* __restrict__ z, double* __restrict__ f_root,
+                                                            double* __restrict__ g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kCatWarps + (threadIdx.x >> 5);
+  if (i > n) return;
+  if (i == n) {  // f_root as in k_cat_tables
+    for (int k = lane; k < K; k += 32) {
+      double s = 0.0;
+      for (int e = 0; e < d; ++e) {
+        const double r = rz[(int64_t)e * K + k], v = rv[e], dr = r - (double)rm[e];
+        s += -0.5 * r * r + 0.5 * log(v) + 0.5 * dr * dr / v;
+      }
+      f_root[k] = s;
+    }
+    return;
+  }
+  double hc[QEM_CAT_MAX_C];
+  int cnt[QEM_CAT_MAX_C];
+  cat_warp_setup(i, C, K, L, p, z, lane, hc, cnt);
+  double lcnt[QEM_CAT_MAX_C];
+#pragma unroll
+  for (int c = 0; c < QEM_CAT_MAX_C; ++c) lcnt[c] = c < C && cnt[c] > 0 ? log((double)cnt[c]) : -CUDART_INF;
+  const double lk = log((double)K);
+  for (int k = lane; k < K; k += 32) {
+    double h[QEM_CAT_MAX_C];
+    cat_h_row(i, k, C, K, d, x, rz, hc, h);
+    double mx = -CUDART_INF;
+#pragma unroll
+    for (int c = 0; c < QEM_CAT_MAX_C; ++c)
+      if (lcnt[c] > -CUDART_INF) mx = fmax(mx, h[c] + lcnt[c]);
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < QEM_CAT_MAX_C; ++c)
+      if (lcnt[c] > -CUDART_INF) s += exp(h[c] + lcnt[c] - mx);
+    g[i * K + k] = mx == -CUDART_INF ? -CUDART_INF : mx + log(s) - lk;
+  }
+}
+
+__global__ void __launch_bounds__(kCatWarps * 32) k_cat_bwd(int64_t n, int C, int K, int d,
+                                                            const float* __restrict__ rz,
+                                                            const double* __restrict__ x,
+                                                            const double* __restrict__ L,
+                                                            const double* __restrict__ p,
+                                                            const int32_t* __restrict__ z,
+                                                            const double* __restrict__ g,
+                                                            const double* __restrict__ w_root,
+                                                            double* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kCatWarps + (threadIdx.x >> 5);
+  if (i >= n) return;
+  double hc[QEM_CAT_MAX_C];
+  int cnt[QEM_CAT_MAX_C];
+  cat_warp_setup(i, C, K, L, p, z, lane, hc, cnt);
+  const double lk = log((double)K);
+  double acc[QEM_CAT_MAX_C];
+#pragma unroll
+  for (int c = 0; c < QEM_CAT_MAX_C; ++c) acc[c] = 0.0;
+  for (int k = lane; k < K; k += 32) {
+    const double wr = w_root[k];
+    if (wr == 0.0) continue;  // zero-weight root samples carry no tuples (g may be -inf)
+    double h[QEM_CAT_MAX_C];
+    cat_h_row(i, k, C, K, d, x, rz, hc, h);
+    const double gk = g[i * K + k];
+#pragma unroll
+    for (int c = 0; c < QEM_CAT_MAX_C; ++c)
+      if (c < C && cnt[c] > 0) acc[c] += wr * exp(h[c] - lk - gk);
+  }
+  double W[QEM_CAT_MAX_C];
+#pragma unroll
+  for (int c = 0; c < QEM_CAT_MAX_C; ++c) W[c] = warp_sum(acc[c]);  // fixed shuffle tree
+  for (int k = lane; k < K; k += 32) {
+    const int zc = z[i * K + k];
+    double v = W[0];
+#pragma unroll
+    for (int c = 1; c < QEM_CAT_MAX_C; ++c) v = zc == c ? W[c] : v;
+    w[i * K + k] = v;
+  }
+}
+
 // Moments (Eq. 7a): one warp per instance, E[onehot z_i](c) = sum_k' w_i(k') [z_i^k' = c];
 // block 0's first d warps also do the root's (E r_e, E r_e^2) under w_root.
 __global__ void __launch_bounds__(kCatThreads) k_cat_moments(int64_t n, int C, int K, int d,
@@ -222,6 +356,19 @@ cudaError_t launch_cat_loglik(int64_t n, int C, int R, const uint8_t* y, const d
                               cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   k_cat_loglik<<<(unsigned)((n * C + kCatThreads - 1) / kCatThreads), kCatThreads, 0, st>>>(n, C, R, y, logit, L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cat_estep(int64_t n, int C, int K, int d, const float* rz, const float* rm, const float* rv,
+                             const double* x, const double* L, const double* p, const int32_t* z, double* f_root,
+                             double* g, double* log_pe, double* w_root, double* w, cudaStream_t st) {
+  k_cat_fwd<<<(unsigned)((n + 1 + kCatWarps - 1) / kCatWarps), kCatWarps * 32, 0, st>>>(n, C, K, d, rz, rm, rv, x, L,
+                                                                                      p, z, f_root, g);
+  cudaError_t e = launch_plate_root(n, K, f_root, g, w, log_pe, w_root, st);
+  if (e != cudaSuccess) return e;
+  if (n > 0)
+    k_cat_bwd<<<(unsigned)((n + kCatWarps - 1) / kCatWarps), kCatWarps * 32, 0, st>>>(n, C, K, d, rz, x, L, p, z, g,
+                                                                                     w_root, w);
   return cudaGetLastError();
 }
 

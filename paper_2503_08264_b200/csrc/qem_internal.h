@@ -114,6 +114,11 @@ cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t s);
 // non-Gaussian Q families (qem_expfam.cu)
 cudaError_t launch_estep_tables(int64_t n, int K, const double* f_root, const double* f, double* g, double* log_pe,
                                 double* w_root, double* w, cudaStream_t st);
+cudaError_t launch_plate_root(int64_t n, int K, const double* f_root, const double* g, double* scratch,
+                              double* log_pe, double* w_root, cudaStream_t st);
+cudaError_t launch_cat_estep(int64_t n, int C, int K, int d, const float* rz, const float* rm, const float* rv,
+                             const double* x, const double* L, const double* p, const int32_t* z, double* f_root,
+                             double* g, double* log_pe, double* w_root, double* w, cudaStream_t st);
 cudaError_t launch_sample_rows(int64_t rows, int K, int level, uint64_t seed, int32_t iter, const float* qm,
                                const float* qv, const float* eps, float* z, cudaStream_t st);
 cudaError_t launch_cat_sample(int64_t n, int C, int K, uint64_t seed, int32_t iter, const double* p, int32_t* z,

@@ -108,6 +108,21 @@ __global__ void __launch_bounds__(kTabThreads) k_tab_bwd(int K, int kblocks, con
   w[i * K + kp] = acc;
 }
 
+// a(k) = f_root(k) + sum_i g_i(k) (fixed order, `scratch` >= min(n, 296) x K doubles), then
+// log Pe = lse a - ln K and w_root = softmax a.
+cudaError_t launch_plate_root(int64_t n, int K, const double* f_root, const double* g, double* scratch,
+                              double* log_pe, double* w_root, cudaStream_t st) {
+  const int64_t parts = n < 148 * 2 ? n : 148 * 2, chunk = parts ? (n + parts - 1) / parts : 0;
+  const int nparts = parts ? (int)((n + chunk - 1) / chunk) : 0;
+  if (nparts) k_tab_plate<<<nparts, 128, 0, st>>>(n, K, chunk, g, scratch);
+  const int nsub = K < 1024 ? 1024 / K : 1;
+  const size_t smem = (size_t)K * (1 + nsub) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_tab_root, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_tab_root<<<1, 1024, smem, st>>>(nparts, K, f_root, scratch, log_pe, w_root);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_estep_tables(int64_t n, int K, const double* f_root, const double* f, double* g, double* log_pe,
                                 double* w_root, double* w, cudaStream_t st) {
   if (n > 0) {
@@ -119,14 +134,8 @@ cudaError_t launch_estep_tables(int64_t n, int K, const double* f_root, const do
     }
   }
   // stage-1 parts live in w (n x K >= parts x K), which the backward overwrites afterwards
-  const int64_t parts = n < 148 * 2 ? n : 148 * 2, chunk = parts ? (n + parts - 1) / parts : 0;
-  const int nparts = parts ? (int)((n + chunk - 1) / chunk) : 0;
-  if (nparts) k_tab_plate<<<nparts, 128, 0, st>>>(n, K, chunk, g, w);
-  const int nsub = K < 1024 ? 1024 / K : 1;
-  const size_t smem = (size_t)K * (1 + nsub) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_tab_root, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = launch_plate_root(n, K, f_root, g, w, log_pe, w_root, st);
   if (e != cudaSuccess) return e;
-  k_tab_root<<<1, 1024, smem, st>>>(nparts, K, f_root, w, log_pe, w_root);
   if (n > 0) {
     const int threads = K >= kTabThreads ? kTabThreads : (K + 31) / 32 * 32;
     const int kblocks = (K + threads - 1) / threads;

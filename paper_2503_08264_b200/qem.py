@@ -346,14 +346,16 @@ class QEM:
 
 class CategoricalQEM:
     """QEM for discrete (categorical) latents under a Gaussian root (NEXT row f1, R30):
-    one iteration = qem_sample_normal + qem_sample_categorical + qem_tables_categorical +
-    qem_estep_tables + qem_moments_categorical + qem_mstep_categorical, all on device; this class
-    only owns the buffers and sequences the calls (argument marshalling)."""
+    one iteration = qem_sample_normal + qem_sample_categorical + qem_estep_categorical (or
+    qem_tables_categorical + qem_estep_tables) + qem_moments_categorical + qem_mstep_categorical,
+    all on device; this class only owns the buffers and sequences the calls (argument marshalling)."""
 
-    def __init__(self, om, *, new_weight=0.3, schedule_p=0.0, var_floor=1e-8, device="cuda"):
+    def __init__(self, om, *, new_weight=0.3, schedule_p=0.0, var_floor=1e-8, device="cuda", tables=False):
+        """tables=False: the factorised E-step (qem_estep_categorical, O(n K C)); True: the
+        materialised log-factor tables + qem_estep_tables (O(n K^2), the generic engine)."""
         if not torch.cuda.is_available():
             raise _lib.QemError("CategoricalQEM needs a CUDA device (there is no CPU fallback)")
-        self.om, self.device = om, torch.device(device)
+        self.om, self.device, self.tables = om, torch.device(device), bool(tables)
         self.new_weight, self.schedule_p, self.var_floor = new_weight, schedule_p, var_floor
         n, C, R, d, K = om.n, om.C, om.R, om.d, om.K
         f32 = dict(dtype=torch.float32, device=self.device)
@@ -368,7 +370,8 @@ class CategoricalQEM:
         self.p = torch.full((n, C), 1.0 / C, **f64)
         self.p_ema = self.p.clone()
         self.root_z, self.z = torch.empty(d, K, **f32), torch.empty(n, K, dtype=torch.int32, device=self.device)
-        self.f_root, self.f = torch.empty(K, **f64), torch.empty(n, K, K, **f64)
+        self.f_root = torch.empty(K, **f64)
+        self.f = torch.empty(n, K, K, **f64) if self.tables else None
         self.g, self.w = torch.empty(n, K, **f64), torch.empty(n, K, **f64)
         self.w_root, self.log_pe = torch.empty(K, **f64), torch.empty(1, **f64)
         self.root_m, self.pm = torch.empty(d, 2, **f64), torch.empty(n, C, **f64)
@@ -385,11 +388,17 @@ class CategoricalQEM:
         check(L.qem_sample_normal(d, K, 0, seed, t, _ptr(self.root_mean), _ptr(self.root_var), eps, _ptr(self.root_z),
                                   s), "qem_sample_normal")
         check(L.qem_sample_categorical(n, C, K, seed, t, _ptr(self.p), _ptr(self.z), s), "qem_sample_categorical")
-        check(L.qem_tables_categorical(n, C, K, d, _ptr(self.root_z), _ptr(self.root_mean), _ptr(self.root_var),
-                                       _ptr(self.x), _ptr(self.L), _ptr(self.p), _ptr(self.z), _ptr(self.f_root),
-                                       _ptr(self.f), s), "qem_tables_categorical")
-        check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
-                                 _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        if self.tables:
+            check(L.qem_tables_categorical(n, C, K, d, _ptr(self.root_z), _ptr(self.root_mean), _ptr(self.root_var),
+                                           _ptr(self.x), _ptr(self.L), _ptr(self.p), _ptr(self.z), _ptr(self.f_root),
+                                           _ptr(self.f), s), "qem_tables_categorical")
+            check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
+                                     _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        else:
+            check(L.qem_estep_categorical(n, C, K, d, _ptr(self.root_z), _ptr(self.root_mean), _ptr(self.root_var),
+                                          _ptr(self.x), _ptr(self.L), _ptr(self.p), _ptr(self.z), _ptr(self.f_root),
+                                          _ptr(self.g), _ptr(self.log_pe), _ptr(self.w_root), _ptr(self.w), s),
+                  "qem_estep_categorical")
         check(L.qem_moments_categorical(n, C, K, d, _ptr(self.w_root), _ptr(self.root_z), _ptr(self.w), _ptr(self.z),
                                         _ptr(self.root_m), _ptr(self.pm), s), "qem_moments_categorical")
 

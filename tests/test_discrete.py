@@ -102,7 +102,9 @@ def _check_step(g, ref, tag):
     np.testing.assert_array_equal(g.root_z.cpu().numpy(), ref["root_z"], err_msg=tag)
     np.testing.assert_array_equal(g.z.cpu().numpy(), ref["z"], err_msg=tag)
     np.testing.assert_allclose(g.f_root.cpu().numpy(), ref["f_root"], rtol=1e-12, atol=1e-12, err_msg=tag)
-    np.testing.assert_allclose(g.f.cpu().numpy(), ref["f"], rtol=1e-12, atol=1e-12, err_msg=tag)
+    if g.tables:
+        np.testing.assert_allclose(g.f.cpu().numpy(), ref["f"], rtol=1e-12, atol=1e-12, err_msg=tag)
+    np.testing.assert_allclose(g.g.cpu().numpy(), ref["est"]["g"], rtol=1e-11, atol=1e-11, err_msg=tag)
     lp = float(g.log_pe.item())
     assert abs(lp - ref["est"]["log_pe"]) <= 1e-11 * max(1.0, abs(ref["est"]["log_pe"])), (tag, lp)
     np.testing.assert_allclose(g.w_root.cpu().numpy(), ref["est"]["w_root"], rtol=1e-10, atol=1e-14, err_msg=tag)
@@ -112,12 +114,13 @@ def _check_step(g, ref, tag):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("tables", [False, True])
 @pytest.mark.parametrize("n,C,K,T", [(300, 2, 64, 4), (97, 3, 37, 3), (1, 8, 5, 2)])
-def test_device_discrete_qem_teacher_forced(n, C, K, T):
+def test_device_discrete_qem_teacher_forced(n, C, K, T, tables):
     from paper_2503_08264_b200.qem import CategoricalQEM
     om = synth.occupancy(n=n, K=K, C=C, seed=3)
     L = od.loglik(om.y, om.logit)
-    g = CategoricalQEM(om)
+    g = CategoricalQEM(om, tables=tables)
     np.testing.assert_allclose(g.L.cpu().numpy(), L, rtol=1e-13, atol=1e-13)
     import torch
     state = od.initial_state(om)
@@ -136,13 +139,14 @@ def test_device_discrete_qem_teacher_forced(n, C, K, T):
 
 
 @pytest.mark.gpu
-def test_device_discrete_full_size_iteration():
+@pytest.mark.parametrize("tables", [False, True])
+def test_device_discrete_full_size_iteration(tables):
     """The Occupancy-shaped default (14400 sites, K = 64): one iteration against the oracle."""
     import torch
     from paper_2503_08264_b200.qem import CategoricalQEM
     om = synth.occupancy()
     L = od.loglik(om.y, om.logit)
-    g = CategoricalQEM(om)
+    g = CategoricalQEM(om, tables=tables)
     state = od.initial_state(om)
     eps = _eps(om, 1, 5)
     ref = od.qem_step(om, state, 1, 5, eps, L=L)
