@@ -293,13 +293,14 @@ def run_gpu(args):
     if not args.no_e2e:
         e2e = run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce)
     tc = g.pair_path() == 1
-    fresh = mfam = disc = pred = None
+    fresh = mfam = disc = pred = gam = None
     if world == 1 and not args.no_variants:
         g.close()  # free the first context's workspace before the variant's
         fresh = run_fresh_variant(args, m, data, dev, seed)
         mfam = run_mstep_family_variant(dev)
         disc = run_discrete_variant(dev)
         pred = run_predictive_variant(m, data, dev, seed)
+        gam = run_gamma_variant(dev)
 
     # ----------------------------------------------------------- roofline
     local_pairs = (ge - gb) * m.K * m.K
@@ -361,7 +362,7 @@ def run_gpu(args):
         "clocks": clk,
         "flags": {"device_flags": flags, "var_clamps": clamps},
         "variants": {"fresh_denominator": fresh, "mstep_family": mfam, "discrete_occupancy": disc,
-                     "predictive_loglik": pred},
+                     "predictive_loglik": pred, "gamma_poisson": gam},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -475,9 +476,9 @@ def run_predictive_variant(m, data, dev, seed, S=100, reps=5):
     g.iterate(1, 4, seed=seed)
     g.sample_q(seed=seed, iter=5)
     g.estep()
-    test = synth.make_test_data(m, data)
+    g.set_test_data(synth.make_test_data(m, data))  # uploaded once, outside the timed region
     ir, ix = g.backward_resample(S, 1)
-    g.predictive_loglik(ix, test)
+    g.predictive_loglik(ix)
     torch.cuda.synchronize()
     st, mid, en = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     st.record()
@@ -485,7 +486,7 @@ def run_predictive_variant(m, data, dev, seed, S=100, reps=5):
         ir, ix = g.backward_resample(S, 2 + r)
     mid.record()
     for r in range(reps):
-        pll, ll_s, _ = g.predictive_loglik(ix, test)
+        pll, ll_s, _ = g.predictive_loglik(ix)
     en.record()
     torch.cuda.synchronize()
     out = {"S": S, "resample_ms": st.elapsed_time(mid) / reps, "predict_ms": mid.elapsed_time(en) / reps,
@@ -493,6 +494,28 @@ def run_predictive_variant(m, data, dev, seed, S=100, reps=5):
            "resampled_rows_per_s": S * m.n * m.K / (st.elapsed_time(mid) / reps * 1e-3)}
     g.close()
     return out
+
+
+def run_gamma_variant(dev, steps=10):
+    """NEXT row f1, Gamma Q (R32): one QEM iteration of the Gamma-Poisson hierarchy
+    (2000 groups, J = 8, K = 128; Marsaglia-Tsang Gamma draws, fp64 tables, Gamma M-step)."""
+    import torch
+    from paper_2503_08264_b200 import synth
+    from paper_2503_08264_b200.qem import GammaPoissonQEM
+    gp = synth.gamma_poisson()
+    g = GammaPoissonQEM(gp, device=dev)
+    for t in range(1, 4):
+        g.step(t, 3)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    st.record()
+    for t in range(4, 4 + steps):
+        g.step(t, 3)
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / steps
+    return {"workload": f"gamma-poisson n={gp.n} J={gp.J} K={gp.K}", "ms_per_step": ms,
+            "factor_pairs_per_s": gp.n * gp.K * gp.K / (ms * 1e-3), "qem_iters_per_s": 1e3 / ms}
 
 
 def run_discrete_variant(dev, steps=10):

@@ -232,6 +232,35 @@ qem_status qem_evidence_root(qem_ctx* ctx, void* stream);
    first multiplied by exp(log_pe - log_pe_fresh) (read on the device).                */
 qem_status qem_mstep(qem_ctx* ctx, int32_t t, void* stream);
 
+/* ---- Gamma approximate posteriors (NEXT row f1, E-step side; R32) ----
+   Gamma-Poisson hierarchy under a Gaussian root: mu ~ N(0, 1), Q_root = N(m, v) (1-dim root);
+   lambda_i | mu ~ Gamma(shape alpha, rate alpha e^-mu); y_ij | lambda_i ~ Poisson(lambda_i);
+   Q_i = Gamma(shape k_i, rate th_i).  One QEM iteration = qem_sample_normal (root) +
+   qem_sample_gamma + qem_tables_gamma_poisson + qem_estep_tables + qem_moments_gamma +
+   qem_mstep_family(QEM_QFAMILY_GAMMA) for the groups and qem_mstep_categorical(n = 0) for the
+   root.  Device arrays, caller-owned, asynchronous on `stream`; QEM_INVALID_ARGUMENT on bad
+   sizes / null arrays. */
+/* d_z [n][K] fp64 Gamma(shape, rate) draws, d_q [n][2] = Q_i's (shape, rate) (qem_mstep_family's
+   QEM_QFAMILY_GAMMA parameter layout): Marsaglia-Tsang (shape < 1: boosted), attempt
+   a of (i, k) from Philox4x32-10 at counter (k, a, i, 6 << 24 | iter), key = seed: normal
+   sqrt(-2 ln u0) cos(2 pi u1), acceptance u2, boost u3^(1/shape), u_j = (word_j + 1/2) 2^-32
+   (fp64); NaN after 64 rejected attempts.  iter >= 1. */
+qem_status qem_sample_gamma(int64_t n, int32_t K, uint64_t seed, int32_t iter, const double* d_q, double* d_z,
+                            void* stream);
+/* Log-factor tables (fp64): d_f_root [K] = log N(mu^k; 0, 1) - log N(mu^k; m, v) (mu^k =
+   d_root_z[k], fp32; d_root_mean/var [1] fp32); d_f [n][K][K] = log Gamma(l; alpha, alpha e^-mu^k)
+   + sum_j log Pois(y_ij; l) - log Gamma(l; k_i, th_i), l = d_z[i][k'] (d_y [n][J] int32 counts,
+   d_q [n][2] fp64 = Q_i's (shape, rate)).  Feed to qem_estep_tables. */
+qem_status qem_tables_gamma_poisson(int64_t n, int32_t K, int32_t J, double alpha, const float* d_root_z,
+                                    const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
+                                    const double* d_q, const double* d_z, double* d_f_root, double* d_f,
+                                    void* stream);
+/* Mean parameters under qem_estep_tables' weights: d_gm [n][2] = (E lambda_i, E ln lambda_i),
+   d_root_m [2] = (E mu, E mu^2). */
+qem_status qem_moments_gamma(int64_t n, int32_t K, const double* d_w_root, const float* d_root_z,
+                             const double* d_w, const double* d_z, double* d_root_m, double* d_gm,
+                             void* stream);
+
 /* ---- Predictive log-likelihood (NEXT row f3; R31) ----
    qem_backward_resample: after qem_estep (or qem_estep_forward + the all-reduce + the root pass
    of qem_estep_backward) on a two-level context, draw S index tuples from the MPIW posterior

@@ -119,6 +119,13 @@ cudaError_t launch_plate_root(int64_t n, int K, const double* f_root, const doub
 cudaError_t launch_cat_estep(int64_t n, int C, int K, int d, const float* rz, const float* rm, const float* rv,
                              const double* x, const double* L, const double* p, const int32_t* z, double* f_root,
                              double* g, double* log_pe, double* w_root, double* w, cudaStream_t st);
+cudaError_t launch_gamma_sample(int64_t n, int K, uint64_t seed, int32_t iter, const double* q, double* z,
+                                cudaStream_t st);
+cudaError_t launch_gamma_tables(int64_t n, int K, int J, double alpha, const float* mu, const float* rm, const float* rv,
+                                const int32_t* y, const double* q, const double* z, double* f_root, double* f,
+                                cudaStream_t st);
+cudaError_t launch_gamma_moments(int64_t n, int K, const double* w_root, const float* mu, const double* w,
+                                 const double* z, double* root_m, double* gm, cudaStream_t st);
 cudaError_t launch_sample_rows(int64_t rows, int K, int level, uint64_t seed, int32_t iter, const float* qm,
                                const float* qv, const float* eps, float* z, cudaStream_t st);
 cudaError_t launch_cat_sample(int64_t n, int C, int K, uint64_t seed, int32_t iter, const double* p, int32_t* z,

@@ -304,23 +304,30 @@ class QEM:
               "qem_backward_resample")
         return idx_root, idx
 
-    def predictive_loglik(self, idx: torch.Tensor, test: "synth.Data", stream=None):
-        """Predictive log-likelihood of held-out observations of the local groups at the resampled
-        latents (qem_predictive_loglik): returns (pll [1], ll_s [S], ll_part [S][n_local])."""
+    def set_test_data(self, test: "synth.Data") -> None:
+        """Upload the LOCAL shard of held-out observations once (row f3)."""
         m, b, e = self.m, self.g_begin, self.g_end
-        S = idx.shape[0]
         if m.obs_kind == synth.OBS_GAUSS:
             x = torch.from_numpy(np.ascontiguousarray(test.xg[b:e], np.float32)).to(self.device)
             y = None
         else:
             x = torch.from_numpy(np.ascontiguousarray(test.xb[b:e], np.uint8)).to(self.device)
             y = torch.from_numpy(np.ascontiguousarray(test.yb[b:e], np.uint8)).to(self.device)
+        self._test = (x, y)
+
+    def predictive_loglik(self, idx: torch.Tensor, test: Optional["synth.Data"] = None, stream=None):
+        """Predictive log-likelihood of held-out observations of the local groups at the resampled
+        latents (qem_predictive_loglik): returns (pll [1], ll_s [S], ll_part [S][n_local]).
+        `test` uploads (and keeps) a held-out set; else the one from set_test_data is used."""
+        if test is not None:
+            self.set_test_data(test)
+        x, y = self._test
+        S = idx.shape[0]
         J = x.shape[1]
         f64 = dict(dtype=torch.float64, device=self.device)
         ll_part, ll_s, pll = torch.empty(S, self.n_local, **f64), torch.empty(S, **f64), torch.empty(1, **f64)
         check(lib().qem_predictive_loglik(self.ctx, int(S), _ptr(idx), int(J), _ptr(x), _ptr(y), _ptr(ll_part),
                                           _ptr(ll_s), _ptr(pll), _stream(stream)), "qem_predictive_loglik")
-        self._test_keep = (x, y)  # alive until the stream has consumed them
         return pll, ll_s, ll_part
 
     def result(self):
@@ -417,3 +424,60 @@ class CategoricalQEM:
         """Teacher forcing (parity tests): Q and EMA state from host arrays."""
         for k in ("root_mean", "root_var", "root_ema", "p", "p_ema"):
             getattr(self, k).copy_(torch.from_numpy(np.asarray(st[k])).to(getattr(self, k).dtype))
+
+
+class GammaPoissonQEM:
+    """QEM with Gamma approximate posteriors (NEXT row f1, R32) on the Gamma-Poisson
+    hierarchy of synth.gamma_poisson: one iteration = qem_sample_normal (root) + qem_sample_gamma
+    + qem_tables_gamma_poisson + qem_estep_tables + qem_moments_gamma + qem_mstep_family (GAMMA)
+    + qem_mstep_categorical (root only, n = 0), all on device (argument marshalling only)."""
+
+    def __init__(self, gp, *, new_weight=0.3, var_floor=1e-8, device="cuda"):
+        if not torch.cuda.is_available():
+            raise _lib.QemError("GammaPoissonQEM needs a CUDA device (there is no CPU fallback)")
+        self.gp, self.device = gp, torch.device(device)
+        self.new_weight, self.var_floor = new_weight, var_floor
+        n, K = gp.n, gp.K
+        f32 = dict(dtype=torch.float32, device=self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.y = torch.from_numpy(np.ascontiguousarray(gp.y, np.int32)).to(self.device)
+        self.root_mean, self.root_var = torch.zeros(1, **f32), torch.ones(1, **f32)
+        self.root_ema = torch.tensor([[0.0, 1.0]], **f64)
+        self.q = torch.ones(n, 2, **f64)                                   # Gamma(1, 1)
+        self.g_ema = torch.tensor([[1.0, -0.5772156649015329]] * n, **f64)  # its (E l, E ln l)
+        self.mu, self.z = torch.empty(1, K, **f32), torch.empty(n, K, **f64)
+        self.f_root, self.f = torch.empty(K, **f64), torch.empty(n, K, K, **f64)
+        self.g, self.w = torch.empty(n, K, **f64), torch.empty(n, K, **f64)
+        self.w_root, self.log_pe = torch.empty(K, **f64), torch.empty(1, **f64)
+        self.root_m, self.gm = torch.empty(1, 2, **f64), torch.empty(n, 2, **f64)
+        self.status = torch.zeros(n, dtype=torch.int32, device=self.device)
+        self.clamps = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def step(self, t: int, seed: int, root_eps: Optional[torch.Tensor] = None, stream=None) -> None:
+        gp, L, s = self.gp, lib(), _stream(stream)
+        n, K = gp.n, gp.K
+        check(L.qem_sample_normal(1, K, 0, seed, t, _ptr(self.root_mean), _ptr(self.root_var),
+                                  _ptr(root_eps) if root_eps is not None else None, _ptr(self.mu), s),
+              "qem_sample_normal")
+        check(L.qem_sample_gamma(n, K, seed, t, _ptr(self.q), _ptr(self.z), s), "qem_sample_gamma")
+        check(L.qem_tables_gamma_poisson(n, K, gp.J, float(gp.alpha), _ptr(self.mu), _ptr(self.root_mean),
+                                         _ptr(self.root_var), _ptr(self.y), _ptr(self.q), _ptr(self.z),
+                                         _ptr(self.f_root), _ptr(self.f), s), "qem_tables_gamma_poisson")
+        check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
+                                 _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        check(L.qem_moments_gamma(n, K, _ptr(self.w_root), _ptr(self.mu), _ptr(self.w), _ptr(self.z),
+                                  _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_gamma")
+        lam = 1.0 - self.new_weight
+        check(L.qem_mstep_family(GAMMA, n, 1, lam, _ptr(self.gm), _ptr(self.g_ema), _ptr(self.q), _ptr(self.status),
+                                 s), "qem_mstep_family")
+        check(L.qem_mstep_categorical(0, 1, 1, lam, self.var_floor, _ptr(self.root_m), _ptr(self.root_ema),
+                                      _ptr(self.root_mean), _ptr(self.root_var), None, None, None, _ptr(self.clamps),
+                                      s), "qem_mstep_categorical")
+
+    def set_state(self, st: dict) -> None:
+        """Teacher forcing (parity tests): Q and EMA state from host arrays."""
+        self.root_mean.fill_(float(st["root_mean"]))
+        self.root_var.fill_(float(st["root_var"]))
+        self.root_ema.copy_(torch.from_numpy(np.asarray(st["root_ema"], np.float64).reshape(1, 2)))
+        self.q.copy_(torch.from_numpy(np.asarray(st["q"], np.float64)))
+        self.g_ema.copy_(torch.from_numpy(np.asarray(st["g_ema"], np.float64)))

@@ -256,3 +256,25 @@ def occupancy(n: int = 14400, R: int = 5, K: int = 64, C: int = 2, seed: int = 6
     lz = logit[np.arange(n), :, z]                           # [n][R]
     y = (rng.random((n, R)) < 1.0 / (1.0 + np.exp(-lz))).astype(np.uint8)
     return Occupancy(n=n, C=C, R=R, d=d, K=K, x=x, logit=logit, y=y, r_true=r, z_true=z)
+
+
+@dataclasses.dataclass
+class GammaPoisson:
+    """Gamma-Poisson hierarchy under a Gaussian root (row f1's Gamma Q; R32):
+    mu ~ N(0, 1); lambda_i | mu ~ Gamma(shape alpha, rate alpha e^-mu); y_ij ~ Poisson(lambda_i)."""
+    n: int
+    J: int
+    K: int
+    alpha: float
+    y: np.ndarray        # [n][J] int32
+    mu_true: float
+    lam_true: np.ndarray  # [n]
+
+
+def gamma_poisson(n: int = 2000, J: int = 8, K: int = 128, alpha: float = 2.0, seed: int = 7) -> GammaPoisson:
+    """Ancestral draw from the prior (numpy PCG64, `seed`)."""
+    rng = np.random.default_rng(seed)
+    mu = float(rng.normal())
+    lam = rng.gamma(alpha, np.exp(mu) / alpha, n)          # numpy: (shape, scale = 1 / rate)
+    y = rng.poisson(lam[:, None], (n, J)).astype(np.int32)
+    return GammaPoisson(n=n, J=J, K=K, alpha=alpha, y=y, mu_true=mu, lam_true=lam)
