@@ -514,8 +514,24 @@ def run_gamma_variant(dev, steps=10):
     en.record()
     torch.cuda.synchronize()
     ms = st.elapsed_time(en) / steps
-    return {"workload": f"gamma-poisson n={gp.n} J={gp.J} K={gp.K}", "ms_per_step": ms,
-            "factor_pairs_per_s": gp.n * gp.K * gp.K / (ms * 1e-3), "qem_iters_per_s": 1e3 / ms}
+    out = {"workload": f"gamma-poisson n={gp.n} J={gp.J} K={gp.K}", "ms_per_step": ms,
+           "factor_pairs_per_s": gp.n * gp.K * gp.K / (ms * 1e-3), "qem_iters_per_s": 1e3 / ms}
+    del g
+    from paper_2503_08264_b200.qem import BetaBinomialQEM
+    bb = synth.beta_binomial()
+    g = BetaBinomialQEM(bb, device=dev)
+    for t in range(1, 4):
+        g.step(t, 3)
+    torch.cuda.synchronize()
+    st.record()
+    for t in range(4, 4 + steps):
+        g.step(t, 3)
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / steps
+    out["beta_binomial"] = {"workload": f"beta-binomial n={bb.n} K={bb.K}", "ms_per_step": ms,
+                            "factor_pairs_per_s": bb.n * bb.K * bb.K / (ms * 1e-3), "qem_iters_per_s": 1e3 / ms}
+    return out
 
 
 def run_discrete_variant(dev, steps=10):

@@ -261,6 +261,28 @@ qem_status qem_moments_gamma(int64_t n, int32_t K, const double* d_w_root, const
                              const double* d_w, const double* d_z, double* d_root_m, double* d_gm,
                              void* stream);
 
+/* ---- Beta approximate posteriors (NEXT row f1, E-step side; R32) ----
+   Beta-Binomial hierarchy under a Gaussian root: mu ~ N(0, 1), Q_root = N(m, v); p_i | mu ~
+   Beta(kappa s, kappa (1 - s)), s = sigmoid(mu); y_i ~ Binomial(N_i, p_i); Q_i = Beta(a_i, b_i).
+   One QEM iteration = qem_sample_normal (root) + qem_sample_beta + qem_tables_beta_binomial +
+   qem_estep_tables + qem_moments_beta + qem_mstep_family(QEM_QFAMILY_BETA) +
+   qem_mstep_categorical(n = 0) for the root.  d_q [n][2] = (a, b) (fp64, the BETA parameter
+   layout of qem_mstep_family).
+   qem_sample_beta: z = X / (X + Y), X ~ Gamma(a), Y ~ Gamma(b) by Marsaglia-Tsang as
+   qem_sample_gamma on the Philox streams 7 << 24 (X) and 8 << 24 (Y).
+   qem_tables_beta_binomial: d_f_root [K] as qem_tables_gamma_poisson; d_f [n][K][K] =
+   log Beta(p; kappa s_k, kappa (1 - s_k)) + log Binomial(y_i; N_i, p) - log Beta(p; a_i, b_i),
+   p = d_z[i][k'], d_y / d_N [n] int32.
+   qem_moments_beta: d_gm [n][2] = (E ln p_i, E ln(1 - p_i)), d_root_m [2] = (E mu, E mu^2). */
+qem_status qem_sample_beta(int64_t n, int32_t K, uint64_t seed, int32_t iter, const double* d_q, double* d_z,
+                           void* stream);
+qem_status qem_tables_beta_binomial(int64_t n, int32_t K, double kappa, const float* d_root_z,
+                                    const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
+                                    const int32_t* d_N, const double* d_q, const double* d_z, double* d_f_root,
+                                    double* d_f, void* stream);
+qem_status qem_moments_beta(int64_t n, int32_t K, const double* d_w_root, const float* d_root_z,
+                            const double* d_w, const double* d_z, double* d_root_m, double* d_gm, void* stream);
+
 /* ---- Predictive log-likelihood (NEXT row f3; R31) ----
    qem_backward_resample: after qem_estep (or qem_estep_forward + the all-reduce + the root pass
    of qem_estep_backward) on a two-level context, draw S index tuples from the MPIW posterior

@@ -16,5 +16,5 @@ Modules:
   tables.py      the E-step on explicit log-factor tables: elimination + enumeration (numpy).
   discrete.py    discrete (categorical) latents under a Gaussian root (numpy).
   predict.py     backward index resampling + predictive log-likelihood (numpy).
-  gamma.py       Gamma-Q E-step on a Gamma-Poisson hierarchy (numpy/scipy).
+  gamma.py       Gamma- and Beta-Q E-steps (Gamma-Poisson, Beta-Binomial; numpy/scipy).
 """

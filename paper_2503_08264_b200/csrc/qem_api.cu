@@ -427,6 +427,37 @@ qem_status qem_moments_gamma(int64_t n, int32_t K, const double* d_w_root, const
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_moments_gamma");
 }
 
+qem_status qem_sample_beta(int64_t n, int32_t K, uint64_t seed, int32_t iter, const double* d_q, double* d_z,
+                           void* stream) {
+  if (n < 0 || n > 0xffffffffLL || K < 1 || iter < 1)
+    return fail(QEM_INVALID_ARGUMENT, "need 0 <= n < 2^32, K >= 1, iter >= 1");
+  if (n > 0 && (!d_q || !d_z)) return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_beta_sample(n, K, seed, iter, d_q, d_z, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_sample_beta");
+}
+
+qem_status qem_tables_beta_binomial(int64_t n, int32_t K, double kappa, const float* d_root_z,
+                                    const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
+                                    const int32_t* d_N, const double* d_q, const double* d_z, double* d_f_root,
+                                    double* d_f, void* stream) {
+  if (n < 0 || K < 1 || !(kappa > 0.0)) return fail(QEM_INVALID_ARGUMENT, "bad sizes or kappa");
+  if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root || (n > 0 && (!d_y || !d_N || !d_q || !d_z || !d_f)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_beta_tables(n, K, kappa, d_root_z, d_root_mean, d_root_var, d_y, d_N, d_q, d_z,
+                                                d_f_root, d_f, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_tables_beta_binomial");
+}
+
+qem_status qem_moments_beta(int64_t n, int32_t K, const double* d_w_root, const float* d_root_z, const double* d_w,
+                            const double* d_z, double* d_root_m, double* d_gm, void* stream) {
+  if (n < 0 || K < 1) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!d_w_root || !d_root_z || !d_root_m || (n > 0 && (!d_w || !d_z || !d_gm)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e =
+      qem::launch_beta_moments(n, K, d_w_root, d_root_z, d_w, d_z, d_root_m, d_gm, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_moments_beta");
+}
+
 qem_status qem_sample_normal(int64_t rows, int32_t K, int32_t level, uint64_t seed, int32_t iter,
                              const float* d_mean, const float* d_var, const float* d_eps, float* d_z, void* stream) {
   if (rows < 0 || K < 1 || iter < 1 || level < 0 || level > 255)

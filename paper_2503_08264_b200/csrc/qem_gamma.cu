@@ -1,6 +1,9 @@
-// qem_gamma.cu -- Gamma approximate posteriors on the E-step side (NEXT row f1, R32):
-// a Gamma-Poisson hierarchy under a Gaussian root, on the explicit-table engine (qem_tables.cu)
-// and the Gamma M-step of qem_expfam.cu.
+// qem_gamma.cu -- Gamma and Beta approximate posteriors on the E-step side (NEXT row f1,
+// DESIGN.md R32): a Gamma-Poisson and a Beta-Binomial hierarchy under a Gaussian root, on the
+// explicit-table engine (qem_tables.cu) and the Gamma / Beta M-steps of qem_expfam.cu.
+// Beta-Binomial: p_i | mu ~ Beta(kappa s, kappa (1 - s)), s = sigmoid(mu); y_i ~ Binomial(N_i, p_i);
+// Q_i = Beta(a_i, b_i), drawn as X / (X + Y) from two Marsaglia-Tsang Gammas on the Philox
+// streams 7 << 24 (X) and 8 << 24 (Y).
 //
 // Model: root mu ~ N(0, 1) (log mean rate), Q_root = N(m, v); per group i a rate
 // lambda_i | mu ~ Gamma(shape alpha, rate alpha e^-mu) and counts y_ij | lambda_i ~ Poisson(lambda_i),
@@ -28,15 +31,9 @@ constexpr int kGammaMaxAttempts = 64;
 
 __device__ __forceinline__ double u32d(uint32_t w) { return ((double)w + 0.5) * 2.3283064365386963e-10; }
 
-__global__ void __launch_bounds__(256) k_gamma_sample(int64_t n, int K, uint2 key, uint32_t iterword,
-                                                      const double* __restrict__ q, double* __restrict__ z) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * K) return;
-  const int64_t i = t / K;
-  const int k = (int)(t - i * K);
-  const double a = q[2 * i], b = q[2 * i + 1];  // Q_i = (shape, rate)
+// Gamma(a, rate 1) by Marsaglia-Tsang; attempt `att` uses Philox at (k, att, i, tag | iter).
+__device__ __forceinline__ double mt_gamma(double a, int k, int64_t i, uint32_t iterword, uint2 key) {
   const double d = (a < 1.0 ? a + 1.0 : a) - 1.0 / 3.0, c = 1.0 / sqrt(9.0 * d);
-  double out = CUDART_NAN;
   for (int att = 0; att < kGammaMaxAttempts; ++att) {
     const uint4 o = philox4x32_10(make_uint4((uint32_t)k, (uint32_t)att, (uint32_t)i, iterword), key);
     const double x = sqrt(-2.0 * log(u32d(o.x))) * cospi(2.0 * u32d(o.y));
@@ -46,11 +43,101 @@ __global__ void __launch_bounds__(256) k_gamma_sample(int64_t n, int K, uint2 ke
     if (log(u32d(o.z)) < 0.5 * x * x + d - d * v + d * log(v)) {
       double g = d * v;
       if (a < 1.0) g *= pow(u32d(o.w), 1.0 / a);
-      out = g / b;
-      break;
+      return g;
     }
   }
-  z[t] = out;
+  return CUDART_NAN;
+}
+
+__global__ void __launch_bounds__(256) k_gamma_sample(int64_t n, int K, uint2 key, uint32_t iterword,
+                                                      const double* __restrict__ q, double* __restrict__ z) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * K) return;
+  const int64_t i = t / K;
+  const int k = (int)(t - i * K);
+  z[t] = mt_gamma(q[2 * i], k, i, iterword, key) / q[2 * i + 1];  // Q_i = (shape, rate)
+}
+
+// Beta(a, b) = X / (X + Y), X ~ Gamma(a), Y ~ Gamma(b) on the streams 7 << 24 and 8 << 24.
+__global__ void __launch_bounds__(256) k_beta_sample(int64_t n, int K, uint2 key, uint32_t iter,
+                                                     const double* __restrict__ q, double* __restrict__ z) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * K) return;
+  const int64_t i = t / K;
+  const int k = (int)(t - i * K);
+  const double x = mt_gamma(q[2 * i], k, i, (7u << 24) | (iter & 0xffffffu), key);
+  const double y = mt_gamma(q[2 * i + 1], k, i, (8u << 24) | (iter & 0xffffffu), key);
+  z[t] = x / (x + y);
+}
+
+// Beta-Binomial tables (one warp per (i, k) row; row n*K: the root row):
+//   f_i(k, k') = log Beta(p; kappa s_k, kappa (1 - s_k)) + y_i ln p + (N_i - y_i) ln(1 - p)
+//                + ln C(N_i, y_i) - log Beta(p; a_i, b_i),   s_k = sigmoid(mu^k), p = z_i^k'
+__global__ void __launch_bounds__(256) k_beta_tables(int64_t n, int K, double kappa, const float* __restrict__ mu,
+                                                     const float* __restrict__ rm, const float* __restrict__ rv,
+                                                     const int32_t* __restrict__ y, const int32_t* __restrict__ N,
+                                                     const double* __restrict__ q, const double* __restrict__ z,
+                                                     double* __restrict__ f_root, double* __restrict__ f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row > n * K) return;
+  if (row == n * K) {
+    const double m = rm[0], v = rv[0];
+    for (int k = lane; k < K; k += 32) {
+      const double r = mu[k], dr = r - m;
+      f_root[k] = -0.5 * r * r + 0.5 * log(v) + 0.5 * dr * dr / v;
+    }
+    return;
+  }
+  const int64_t i = row / K;
+  const int k = (int)(row - i * K);
+  const double sk = 1.0 / (1.0 + exp(-(double)mu[k]));
+  const double pa = kappa * sk, pb = kappa * (1.0 - sk);
+  const double cp = lgamma(kappa) - lgamma(pa) - lgamma(pb);
+  const double yy = y[i], nn = N[i];
+  const double cb = lgamma(nn + 1.0) - lgamma(yy + 1.0) - lgamma(nn - yy + 1.0);
+  const double qa = q[2 * i], qb = q[2 * i + 1];
+  const double cq = lgamma(qa + qb) - lgamma(qa) - lgamma(qb);
+  const double* zi = z + i * K;
+  double* fr = f + row * K;
+  for (int kp = lane; kp < K; kp += 32) {
+    const double p = zi[kp], lp = log(p), l1 = log1p(-p);
+    const double prior = cp + (pa - 1.0) * lp + (pb - 1.0) * l1;
+    const double lik = cb + yy * lp + (nn - yy) * l1;
+    const double lq = cq + (qa - 1.0) * lp + (qb - 1.0) * l1;
+    fr[kp] = prior + lik - lq;
+  }
+}
+
+// Beta mean parameters (E ln p, E ln(1-p)) per group [n][2], root (E mu, E mu^2) [2].
+__global__ void __launch_bounds__(256) k_beta_moments(int64_t n, int K, const double* __restrict__ w_root,
+                                                      const float* __restrict__ mu, const double* __restrict__ w,
+                                                      const double* __restrict__ z, double* __restrict__ root_m,
+                                                      double* __restrict__ gm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (wid > n) return;
+  double s1 = 0.0, s2 = 0.0;
+  if (wid == n) {
+    for (int k = lane; k < K; k += 32) {
+      const double r = mu[k], wk = w_root[k];
+      s1 += wk * r;
+      s2 += wk * r * r;
+    }
+  } else {
+    for (int k = lane; k < K; k += 32) {
+      const double p = z[wid * K + k], wk = w[wid * K + k];
+      s1 += wk * log(p);
+      s2 += wk * log1p(-p);
+    }
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    double* o = wid == n ? root_m : gm + 2 * wid;
+    o[0] = s1;
+    o[1] = s2;
+  }
 }
 
 // One warp per (i, k) row (row n*K: the root row).  Per group the count sufficient statistics
@@ -135,6 +222,28 @@ cudaError_t launch_gamma_sample(int64_t n, int K, uint64_t seed, int32_t iter, c
   const uint32_t iterword = kGammaTag | ((uint32_t)iter & 0xffffffu);
   k_gamma_sample<<<(unsigned)((n * K + 255) / 256), 256, 0, st>>>(
       n, K, make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)), iterword, q, z);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_beta_sample(int64_t n, int K, uint64_t seed, int32_t iter, const double* q, double* z,
+                               cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_beta_sample<<<(unsigned)((n * K + 255) / 256), 256, 0, st>>>(n, K, make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)),
+                                                                 (uint32_t)iter, q, z);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_beta_tables(int64_t n, int K, double kappa, const float* mu, const float* rm, const float* rv,
+                               const int32_t* y, const int32_t* N, const double* q, const double* z, double* f_root,
+                               double* f, cudaStream_t st) {
+  const int64_t rows = n * K + 1;
+  k_beta_tables<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(n, K, kappa, mu, rm, rv, y, N, q, z, f_root, f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_beta_moments(int64_t n, int K, const double* w_root, const float* mu, const double* w,
+                                const double* z, double* root_m, double* gm, cudaStream_t st) {
+  k_beta_moments<<<(unsigned)((n + 1 + 7) / 8), 256, 0, st>>>(n, K, w_root, mu, w, z, root_m, gm);
   return cudaGetLastError();
 }
 

@@ -126,6 +126,13 @@ cudaError_t launch_gamma_tables(int64_t n, int K, int J, double alpha, const flo
                                 cudaStream_t st);
 cudaError_t launch_gamma_moments(int64_t n, int K, const double* w_root, const float* mu, const double* w,
                                  const double* z, double* root_m, double* gm, cudaStream_t st);
+cudaError_t launch_beta_sample(int64_t n, int K, uint64_t seed, int32_t iter, const double* q, double* z,
+                               cudaStream_t st);
+cudaError_t launch_beta_tables(int64_t n, int K, double kappa, const float* mu, const float* rm, const float* rv,
+                               const int32_t* y, const int32_t* N, const double* q, const double* z, double* f_root,
+                               double* f, cudaStream_t st);
+cudaError_t launch_beta_moments(int64_t n, int K, const double* w_root, const float* mu, const double* w,
+                                const double* z, double* root_m, double* gm, cudaStream_t st);
 cudaError_t launch_sample_rows(int64_t rows, int K, int level, uint64_t seed, int32_t iter, const float* qm,
                                const float* qv, const float* eps, float* z, cudaStream_t st);
 cudaError_t launch_cat_sample(int64_t n, int C, int K, uint64_t seed, int32_t iter, const double* p, int32_t* z,

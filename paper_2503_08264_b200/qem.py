@@ -481,3 +481,55 @@ class GammaPoissonQEM:
         self.root_ema.copy_(torch.from_numpy(np.asarray(st["root_ema"], np.float64).reshape(1, 2)))
         self.q.copy_(torch.from_numpy(np.asarray(st["q"], np.float64)))
         self.g_ema.copy_(torch.from_numpy(np.asarray(st["g_ema"], np.float64)))
+
+
+class BetaBinomialQEM:
+    """QEM with Beta approximate posteriors (NEXT row f1, R32) on the Beta-Binomial
+    hierarchy of synth.beta_binomial: qem_sample_normal (root) + qem_sample_beta +
+    qem_tables_beta_binomial + qem_estep_tables + qem_moments_beta + qem_mstep_family (BETA) +
+    qem_mstep_categorical (root only), all on device (argument marshalling only)."""
+
+    def __init__(self, bb, *, new_weight=0.3, var_floor=1e-8, device="cuda"):
+        if not torch.cuda.is_available():
+            raise _lib.QemError("BetaBinomialQEM needs a CUDA device (there is no CPU fallback)")
+        self.bb, self.device = bb, torch.device(device)
+        self.new_weight, self.var_floor = new_weight, var_floor
+        n, K = bb.n, bb.K
+        f32 = dict(dtype=torch.float32, device=self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.y = torch.from_numpy(np.ascontiguousarray(bb.y, np.int32)).to(self.device)
+        self.N = torch.from_numpy(np.ascontiguousarray(bb.N, np.int32)).to(self.device)
+        self.root_mean, self.root_var = torch.zeros(1, **f32), torch.ones(1, **f32)
+        self.root_ema = torch.tensor([[0.0, 1.0]], **f64)
+        self.q = torch.ones(n, 2, **f64)                                   # Beta(1, 1)
+        self.g_ema = torch.tensor([[-1.0, -1.0]] * n, **f64)               # its (E ln p, E ln(1-p))
+        self.mu, self.z = torch.empty(1, K, **f32), torch.empty(n, K, **f64)
+        self.f_root, self.f = torch.empty(K, **f64), torch.empty(n, K, K, **f64)
+        self.g, self.w = torch.empty(n, K, **f64), torch.empty(n, K, **f64)
+        self.w_root, self.log_pe = torch.empty(K, **f64), torch.empty(1, **f64)
+        self.root_m, self.gm = torch.empty(1, 2, **f64), torch.empty(n, 2, **f64)
+        self.status = torch.zeros(n, dtype=torch.int32, device=self.device)
+        self.clamps = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def step(self, t: int, seed: int, root_eps: Optional[torch.Tensor] = None, stream=None) -> None:
+        bb, L, s = self.bb, lib(), _stream(stream)
+        n, K = bb.n, bb.K
+        check(L.qem_sample_normal(1, K, 0, seed, t, _ptr(self.root_mean), _ptr(self.root_var),
+                                  _ptr(root_eps) if root_eps is not None else None, _ptr(self.mu), s),
+              "qem_sample_normal")
+        check(L.qem_sample_beta(n, K, seed, t, _ptr(self.q), _ptr(self.z), s), "qem_sample_beta")
+        check(L.qem_tables_beta_binomial(n, K, float(bb.kappa), _ptr(self.mu), _ptr(self.root_mean),
+                                         _ptr(self.root_var), _ptr(self.y), _ptr(self.N), _ptr(self.q), _ptr(self.z),
+                                         _ptr(self.f_root), _ptr(self.f), s), "qem_tables_beta_binomial")
+        check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
+                                 _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        check(L.qem_moments_beta(n, K, _ptr(self.w_root), _ptr(self.mu), _ptr(self.w), _ptr(self.z),
+                                 _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_beta")
+        lam = 1.0 - self.new_weight
+        check(L.qem_mstep_family(BETA, n, 1, lam, _ptr(self.gm), _ptr(self.g_ema), _ptr(self.q), _ptr(self.status),
+                                 s), "qem_mstep_family")
+        check(L.qem_mstep_categorical(0, 1, 1, lam, self.var_floor, _ptr(self.root_m), _ptr(self.root_ema),
+                                      _ptr(self.root_mean), _ptr(self.root_var), None, None, None, _ptr(self.clamps),
+                                      s), "qem_mstep_categorical")
+
+    set_state = GammaPoissonQEM.set_state

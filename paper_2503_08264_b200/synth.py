@@ -278,3 +278,27 @@ def gamma_poisson(n: int = 2000, J: int = 8, K: int = 128, alpha: float = 2.0, s
     lam = rng.gamma(alpha, np.exp(mu) / alpha, n)          # numpy: (shape, scale = 1 / rate)
     y = rng.poisson(lam[:, None], (n, J)).astype(np.int32)
     return GammaPoisson(n=n, J=J, K=K, alpha=alpha, y=y, mu_true=mu, lam_true=lam)
+
+
+@dataclasses.dataclass
+class BetaBinomial:
+    """Beta-Binomial hierarchy under a Gaussian root (row f1's Beta Q; R32):
+    mu ~ N(0, 1); p_i | mu ~ Beta(kappa s, kappa (1 - s)), s = sigmoid(mu); y_i ~ Binomial(N_i, p_i)."""
+    n: int
+    K: int
+    kappa: float
+    y: np.ndarray   # [n] int32
+    N: np.ndarray   # [n] int32 trials
+    mu_true: float
+    p_true: np.ndarray
+
+
+def beta_binomial(n: int = 2000, K: int = 128, kappa: float = 8.0, n_max: int = 30, seed: int = 8) -> BetaBinomial:
+    """Ancestral draw from the prior (numpy PCG64, `seed`); trials N_i uniform on 1..n_max."""
+    rng = np.random.default_rng(seed)
+    mu = float(rng.normal())
+    s = 1.0 / (1.0 + np.exp(-mu))
+    p = rng.beta(kappa * s, kappa * (1.0 - s), n)
+    N = rng.integers(1, n_max + 1, n).astype(np.int32)
+    y = rng.binomial(N, p).astype(np.int32)
+    return BetaBinomial(n=n, K=K, kappa=kappa, y=y, N=N, mu_true=mu, p_true=p)

@@ -1,5 +1,5 @@
-"""Gamma approximate posteriors, E-step side (NEXT row f1; R32) on the Gamma-Poisson
-hierarchy: the oracle pinned on CPU (Marsaglia-Tsang draws against the Gamma law, evidence
+"""Gamma and Beta approximate posteriors, E-step side (NEXT row f1; R32) on the
+Gamma-Poisson and Beta-Binomial hierarchies: the oracle pinned on CPU (Marsaglia-Tsang draws against the Gamma law, evidence
 unbiasedness against quadrature with the rates integrated out exactly), then the device calls
 against it on GPU."""
 import numpy as np
@@ -58,7 +58,67 @@ def test_evidence_estimate_is_unbiased():
     assert abs(vals.mean() - exact) <= 4.5 * se, (vals.mean(), exact, se)
 
 
+@pytest.mark.parametrize("a,b", [(0.5, 0.7), (2.0, 5.0), (30.0, 3.0)])
+def test_beta_sampler_follows_the_beta_law(a, b):
+    z = og.sample_beta(np.array([[a, b]]), 3000, seed=5, t=1)[0]
+    assert np.all((z > 0) & (z < 1))
+    assert stats.kstest(z, stats.beta(a, b).cdf).pvalue > 1e-3
+
+
+def _evidence_bb(bb):
+    """p(y) = int N(mu; 0, 1) prod_i BetaBinomial(y_i; N_i, kappa s, kappa (1 - s)) dmu."""
+    t, wt = hermegauss(120)
+    wt = wt / np.sqrt(2 * np.pi)
+    tot = np.array([stats.betabinom.logpmf(bb.y, bb.N, bb.kappa / (1 + np.exp(-mu)),
+                                           bb.kappa * (1 - 1 / (1 + np.exp(-mu)))).sum() for mu in t])
+    return float((wt * np.exp(tot)).sum())
+
+
+def test_beta_evidence_estimate_is_unbiased():
+    bb = synth.beta_binomial(n=3, K=4, seed=3, n_max=6)
+    exact = _evidence_bb(bb)
+    rng = np.random.default_rng(6)
+    q = np.array([[2.0, 1.5], [0.9, 0.6], [3.0, 4.0]])
+    vals = []
+    for s in range(2500):
+        mu = np.float32(-0.1) + np.sqrt(np.float32(1.2)) * rng.normal(size=bb.K).astype(np.float32)
+        z = og.sample_beta(q, bb.K, seed=900 + s, t=1)
+        fr, f = og.make_tables_beta(bb, mu, -0.1, 1.2, q, z)
+        vals.append(np.exp(tables.estep_tables(fr, f)["log_pe"]))
+    vals = np.array(vals)
+    se = vals.std() / np.sqrt(len(vals))
+    assert abs(vals.mean() - exact) <= 4.5 * se, (vals.mean(), exact, se)
+
+
 # ------------------------------------------------------------------ device path (GPU)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,K,T", [(150, 64, 3), (29, 17, 2)])
+def test_device_beta_qem_teacher_forced(n, K, T):
+    import torch
+    from paper_2503_08264_b200.qem import BetaBinomialQEM
+    bb = synth.beta_binomial(n=n, K=K, seed=4)
+    g = BetaBinomialQEM(bb)
+    state = og.initial_state_beta(bb)
+    seed = 19
+    for t in range(1, T + 1):
+        g.set_state(state)
+        eps = np.random.default_rng(10 + t).normal(size=K).astype(np.float32)
+        ref = og.qem_step_beta(bb, state, t, seed, eps)
+        g.step(t, seed, root_eps=torch.from_numpy(eps).cuda())
+        torch.cuda.synchronize()
+        tag = f"beta n{n} K{K} t={t}"
+        np.testing.assert_allclose(g.z.cpu().numpy(), ref["z"], rtol=1e-12, err_msg=tag)
+        np.testing.assert_allclose(g.f.cpu().numpy(), ref["f"], rtol=1e-11, atol=1e-10, err_msg=tag)
+        assert abs(float(g.log_pe.item()) - ref["est"]["log_pe"]) <= 1e-10 * abs(ref["est"]["log_pe"]), tag
+        np.testing.assert_allclose(g.w.cpu().numpy(), ref["est"]["w"], rtol=1e-9, atol=1e-13, err_msg=tag)
+        np.testing.assert_allclose(g.gm.cpu().numpy(), ref["gm"], rtol=1e-10, atol=1e-12, err_msg=tag)
+        nxt = ref["next"]
+        assert np.all(g.status.cpu().numpy() == 0), tag
+        np.testing.assert_allclose(g.q.cpu().numpy(), nxt["q"], rtol=1e-8, err_msg=tag)
+        state = nxt
+
 
 
 @pytest.mark.gpu
