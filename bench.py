@@ -293,7 +293,7 @@ def run_gpu(args):
     if not args.no_e2e:
         e2e = run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce)
     tc = g.pair_path() == 1
-    fresh = mfam = disc = pred = gam = None
+    fresh = mfam = disc = pred = gam = crossed = None
     if world == 1 and not args.no_variants:
         g.close()  # free the first context's workspace before the variant's
         fresh = run_fresh_variant(args, m, data, dev, seed)
@@ -301,6 +301,7 @@ def run_gpu(args):
         disc = run_discrete_variant(dev)
         pred = run_predictive_variant(m, data, dev, seed)
         gam = run_gamma_variant(dev)
+        crossed = run_crossed_variant(dev)
 
     # ----------------------------------------------------------- roofline
     local_pairs = (ge - gb) * m.K * m.K
@@ -362,7 +363,7 @@ def run_gpu(args):
         "clocks": clk,
         "flags": {"device_flags": flags, "var_clamps": clamps},
         "variants": {"fresh_denominator": fresh, "mstep_family": mfam, "discrete_occupancy": disc,
-                     "predictive_loglik": pred, "gamma_poisson": gam},
+                     "predictive_loglik": pred, "gamma_poisson": gam, "crossed_bus": crossed},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -494,6 +495,29 @@ def run_predictive_variant(m, data, dev, seed, S=100, reps=5):
            "resampled_rows_per_s": S * m.n * m.K / (st.elapsed_time(mid) / reps * 1e-3)}
     g.close()
     return out
+
+
+def run_crossed_variant(dev, steps=10):
+    """NEXT row f4 (R33): one QEM iteration of the Bus-shaped crossed-effects model (120
+    year-borough groups, 40 journeys each, 57 companies, 6 journey types, K = 64): the K x K x J
+    observation contraction per group into fp64 tables + the table E-step."""
+    import torch
+    from paper_2503_08264_b200 import synth
+    from paper_2503_08264_b200.qem import CrossedQEM
+    cm = synth.bus_crossed()
+    g = CrossedQEM(cm, device=dev)
+    for t in range(1, 4):
+        g.step(t, 3)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    st.record()
+    for t in range(4, 4 + steps):
+        g.step(t, 3)
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / steps
+    return {"workload": f"bus-crossed n={cm.n} J={cm.J} C={cm.C} T={cm.T} K={cm.K}", "ms_per_step": ms,
+            "pair_obs_terms_per_s": cm.n * cm.K * cm.K * cm.J / (ms * 1e-3), "qem_iters_per_s": 1e3 / ms}
 
 
 def run_gamma_variant(dev, steps=10):

@@ -283,6 +283,30 @@ qem_status qem_tables_beta_binomial(int64_t n, int32_t K, double kappa, const fl
 qem_status qem_moments_beta(int64_t n, int32_t K, const double* d_w_root, const float* d_root_z,
                             const double* d_w, const double* d_z, double* d_root_m, double* d_gm, void* stream);
 
+/* ---- Crossed effects (NEXT row f4; R33) ----
+   Bus-Breakdown-shaped: root group (shared index k) = (mu, C company weights, T journey-type
+   weights), all N(0, 1), samples d_root_z [R][K] fp32 with R = 1 + C + T and Q_root
+   d_root_mean / d_root_var [R]; n groups (year x borough) with w_i ~ N(mu, 1), Q_i =
+   N(d_q_mean[i], d_q_var[i]), samples d_z [n][K] fp32; J observations per group with company
+   index d_comp [n][J] in [0, C), journey type d_jtype [n][J] in [0, T) and label d_y [n][J] in
+   {0, 1}: delay ~ Bernoulli(sigmoid(w_i + cw_c + jw_t)).  One QEM iteration = qem_sample_normal
+   (root rows, level 0) + qem_sample_normal (group rows, level 1) + qem_tables_crossed +
+   qem_estep_tables + qem_moments_gaussian + qem_mstep_categorical(n = 0) for the root dims and
+   again for the group latents (as d = n Gaussian dims).
+   qem_tables_crossed: d_f_root [K] = sum_r log N(r^k; 0, 1) - log q(r^k); d_f [n][K][K] =
+   log N(w_i^k'; mu^k, 1) + sum_j [y eta - softplus(eta)] - log q_i(w_i^k'),
+   eta = w_i^k' + cw^k_{comp_ij} + jw^k_{jtype_ij} (fp64).  J <= 4096.
+   qem_moments_gaussian: d_root_m [R][2] = (E r, E r^2) under d_w_root; d_gm [n][2] = (E w_i,
+   E w_i^2) under d_w [n][K]. */
+qem_status qem_tables_crossed(int64_t n, int32_t K, int32_t J, int32_t C, int32_t T, const float* d_root_z,
+                              const float* d_root_mean, const float* d_root_var, const float* d_z,
+                              const float* d_q_mean, const float* d_q_var, const int32_t* d_comp,
+                              const int32_t* d_jtype, const uint8_t* d_y, double* d_f_root, double* d_f,
+                              void* stream);
+qem_status qem_moments_gaussian(int64_t n, int32_t K, int32_t R, const double* d_w_root, const float* d_root_z,
+                                const double* d_w, const float* d_z, double* d_root_m, double* d_gm,
+                                void* stream);
+
 /* ---- Predictive log-likelihood (NEXT row f3; R31) ----
    qem_backward_resample: after qem_estep (or qem_estep_forward + the all-reduce + the root pass
    of qem_estep_backward) on a two-level context, draw S index tuples from the MPIW posterior

@@ -17,4 +17,5 @@ Modules:
   discrete.py    discrete (categorical) latents under a Gaussian root (numpy).
   predict.py     backward index resampling + predictive log-likelihood (numpy).
   gamma.py       Gamma- and Beta-Q E-steps (Gamma-Poisson, Beta-Binomial; numpy/scipy).
+  crossed.py     crossed effects (Bus-shaped company / journey-type tables; numpy/scipy).
 """

@@ -23,7 +23,7 @@ EXPORTS = [
     "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical", "qem_moments_categorical", "qem_mstep_categorical",
     "qem_loglik_bernoulli_states", "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_sample_gamma",
     "qem_tables_gamma_poisson", "qem_moments_gamma", "qem_sample_beta", "qem_tables_beta_binomial",
-    "qem_moments_beta", "qem_iterate",
+    "qem_moments_beta", "qem_tables_crossed", "qem_moments_gaussian", "qem_iterate",
     "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_pair_path", "qem_copy_messages", "qem_status_str", "qem_last_error",
     "qem_version",
 ]
@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
         L.qem_sample_beta.argtypes = [i64, i32, u64, i32, vp, vp, vp]
         L.qem_tables_beta_binomial.argtypes = [i64, i32, ctypes.c_double] + [vp] * 10
         L.qem_moments_beta.argtypes = [i64, i32] + [vp] * 7
+        L.qem_tables_crossed.argtypes = [i64, i32, i32, i32, i32] + [vp] * 12
+        L.qem_moments_gaussian.argtypes = [i64, i32, i32] + [vp] * 7
         L.qem_destroy.argtypes = [vp]
         L.qem_destroy.restype = None
         L.qem_bind.argtypes = [vp, ctypes.POINTER(Buffers)]
@@ -128,7 +130,8 @@ def lib() -> ctypes.CDLL:
                      "qem_moments_categorical", "qem_mstep_categorical", "qem_loglik_bernoulli_states",
                      "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_sample_gamma",
                      "qem_tables_gamma_poisson", "qem_moments_gamma", "qem_sample_beta",
-                     "qem_tables_beta_binomial", "qem_moments_beta"]:
+                     "qem_tables_beta_binomial", "qem_moments_beta", "qem_tables_crossed",
+                     "qem_moments_gaussian"]:
             getattr(L, name).restype = i32
         _lib = L
     return _lib

@@ -458,6 +458,29 @@ qem_status qem_moments_beta(int64_t n, int32_t K, const double* d_w_root, const 
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_moments_beta");
 }
 
+qem_status qem_tables_crossed(int64_t n, int32_t K, int32_t J, int32_t C, int32_t T, const float* d_root_z,
+                              const float* d_root_mean, const float* d_root_var, const float* d_z, const float* d_q_mean,
+                              const float* d_q_var, const int32_t* d_comp, const int32_t* d_jtype, const uint8_t* d_y,
+                              double* d_f_root, double* d_f, void* stream) {
+  if (n < 0 || K < 1 || J < 0 || C < 1 || T < 1 || J > 4096) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root ||
+      (n > 0 && (!d_z || !d_q_mean || !d_q_var || !d_f || (J > 0 && (!d_comp || !d_jtype || !d_y)))))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_crossed_tables(n, K, J, C, T, d_root_z, d_root_mean, d_root_var, d_z, d_q_mean,
+                                                   d_q_var, d_comp, d_jtype, d_y, d_f_root, d_f, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_tables_crossed");
+}
+
+qem_status qem_moments_gaussian(int64_t n, int32_t K, int32_t R, const double* d_w_root, const float* d_root_z,
+                                const double* d_w, const float* d_z, double* d_root_m, double* d_gm, void* stream) {
+  if (n < 0 || K < 1 || R < 1) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!d_w_root || !d_root_z || !d_root_m || (n > 0 && (!d_w || !d_z || !d_gm)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e =
+      qem::launch_crossed_moments(n, K, R, d_w_root, d_root_z, d_w, d_z, d_root_m, d_gm, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_moments_gaussian");
+}
+
 qem_status qem_sample_normal(int64_t rows, int32_t K, int32_t level, uint64_t seed, int32_t iter,
                              const float* d_mean, const float* d_var, const float* d_eps, float* d_z, void* stream) {
   if (rows < 0 || K < 1 || iter < 1 || level < 0 || level > 255)

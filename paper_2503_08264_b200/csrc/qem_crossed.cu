@@ -1,0 +1,121 @@
+// qem_crossed.cu -- crossed effects (NEXT row f4, R33): observations whose factor has
+// several parents on different plates, Bus-Breakdown-shaped (a delay's logit is
+// YearBoroughWeight_yb + CompanyWeight_c(ybi) + JourneyTypeWeight_j(ybi), the company and journey
+// weights picked out by per-observation index tables).
+//
+// Reading (R33): the crossed weights are global latents, so they join the root group and share
+// its sample index k (R2); the plate below is the year-borough groups.  The group factor then
+// couples both indices through every observation:
+//   f_i(k, k') = log N(w_i^k'; mu^k, 1) + sum_j [y_ij eta - softplus(eta)] - log q_i(w_i^k'),
+//   eta = w_i^k' + cw^k_{c_ij} + jw^k_{t_ij}
+// -- a K x K x J contraction per group (the "rank-3 factor" of SURVEY.md §8(f)#4), written into
+// explicit fp64 tables for qem_estep_tables.  Root samples: [R][K] fp32 with R = 1 + C + T
+// (mu, the C company weights, the T journey-type weights), all N(0, 1) a priori.
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "qem_device.cuh"
+#include "qem_internal.h"
+
+namespace qem {
+
+constexpr int kCrossWarps = 8;
+
+// One warp per (i, k) row; the row's per-observation offsets o_j = cw^k_{c_ij} + jw^k_{t_ij} and
+// labels are staged in the warp's shared-memory slice, lanes run over k'.  Row n*K: f_root.
+__global__ void __launch_bounds__(kCrossWarps * 32) k_crossed_tables(int64_t n, int K, int J, int C, int T,
+                                                                     const float* __restrict__ rz,
+                                                                     const float* __restrict__ rm,
+                                                                     const float* __restrict__ rv,
+                                                                     const float* __restrict__ z,
+                                                                     const float* __restrict__ qm,
+                                                                     const float* __restrict__ qv,
+                                                                     const int32_t* __restrict__ comp,
+                                                                     const int32_t* __restrict__ jtype,
+                                                                     const uint8_t* __restrict__ y,
+                                                                     double* __restrict__ f_root,
+                                                                     double* __restrict__ f) {
+  extern __shared__ double so[];  // [kCrossWarps][J] offsets
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * kCrossWarps + wid;
+  if (row > n * K) return;
+  const int R = 1 + C + T;
+  if (row == n * K) {  // f_root(k) = sum_r log N(r; 0, 1) - log N(r; m_r, v_r)
+    for (int k = lane; k < K; k += 32) {
+      double s = 0.0;
+      for (int r = 0; r < R; ++r) {
+        const double x = rz[(int64_t)r * K + k], v = rv[r], dx = x - (double)rm[r];
+        s += -0.5 * x * x + 0.5 * log(v) + 0.5 * dx * dx / v;
+      }
+      f_root[k] = s;
+    }
+    return;
+  }
+  const int64_t i = row / K;
+  const int k = (int)(row - i * K);
+  double* o = so + (size_t)wid * J;
+  for (int j = lane; j < J; j += 32)
+    o[j] = (double)rz[(int64_t)(1 + comp[i * J + j]) * K + k] + (double)rz[(int64_t)(1 + C + jtype[i * J + j]) * K + k];
+  __syncwarp();
+  const double mu = rz[k], m = qm[i], v = qv[i];
+  const uint8_t* yi = y + i * J;
+  const float* zi = z + i * K;
+  double* fr = f + row * K;
+  for (int kp = lane; kp < K; kp += 32) {
+    const double w = zi[kp];
+    double lik = 0.0;
+    for (int j = 0; j < J; ++j) {
+      const double eta = w + o[j];
+      lik += (yi[j] ? eta : 0.0) - (fmax(eta, 0.0) + log1p(exp(-fabs(eta))));
+    }
+    const double dw = w - mu, dq = w - m;
+    // log N(w; mu, 1) - log N(w; m, v): the 2 pi terms cancel
+    fr[kp] = -0.5 * dw * dw + 0.5 * log(v) + 0.5 * dq * dq / v + lik;
+  }
+}
+
+// (E x, E x^2) under the weights: root dims [R][2] from w_root, groups [n][2] from w.
+__global__ void __launch_bounds__(256) k_crossed_moments(int64_t n, int K, int R, const double* __restrict__ w_root,
+                                                         const float* __restrict__ rz, const double* __restrict__ w,
+                                                         const float* __restrict__ z, double* __restrict__ root_m,
+                                                         double* __restrict__ gm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (wid >= n + R) return;
+  const bool root = wid >= n;
+  const int64_t r = wid - n;
+  double s1 = 0.0, s2 = 0.0;
+  for (int k = lane; k < K; k += 32) {
+    const double x = root ? rz[r * K + k] : z[wid * K + k];
+    const double wk = root ? w_root[k] : w[wid * K + k];
+    s1 += wk * x;
+    s2 += wk * x * x;
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    double* out = root ? root_m + 2 * r : gm + 2 * wid;
+    out[0] = s1;
+    out[1] = s2;
+  }
+}
+
+cudaError_t launch_crossed_tables(int64_t n, int K, int J, int C, int T, const float* rz, const float* rm,
+                                  const float* rv, const float* z, const float* qm, const float* qv, const int32_t* comp,
+                                  const int32_t* jtype, const uint8_t* y, double* f_root, double* f, cudaStream_t st) {
+  const int64_t rows = n * K + 1;
+  const size_t smem = (size_t)kCrossWarps * (J > 0 ? J : 1) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_crossed_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_crossed_tables<<<(unsigned)((rows + kCrossWarps - 1) / kCrossWarps), kCrossWarps * 32, smem, st>>>(
+      n, K, J, C, T, rz, rm, rv, z, qm, qv, comp, jtype, y, f_root, f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_crossed_moments(int64_t n, int K, int R, const double* w_root, const float* rz, const double* w,
+                                   const float* z, double* root_m, double* gm, cudaStream_t st) {
+  k_crossed_moments<<<(unsigned)((n + R + 7) / 8), 256, 0, st>>>(n, K, R, w_root, rz, w, z, root_m, gm);
+  return cudaGetLastError();
+}
+
+}  // namespace qem

@@ -533,3 +533,58 @@ class BetaBinomialQEM:
                                       s), "qem_mstep_categorical")
 
     set_state = GammaPoissonQEM.set_state
+
+
+class CrossedQEM:
+    """QEM with crossed effects (NEXT row f4, R33) on synth.bus_crossed: one iteration =
+    qem_sample_normal (root rows, level 0; group rows, level 1) + qem_tables_crossed +
+    qem_estep_tables + qem_moments_gaussian + qem_mstep_categorical (n = 0: the Gaussian EMA +
+    M-step of the root dims, then of the group latents), all on device."""
+
+    def __init__(self, cm, *, new_weight=0.3, var_floor=1e-8, device="cuda"):
+        if not torch.cuda.is_available():
+            raise _lib.QemError("CrossedQEM needs a CUDA device (there is no CPU fallback)")
+        self.cm, self.device = cm, torch.device(device)
+        self.new_weight, self.var_floor = new_weight, var_floor
+        n, K, R = cm.n, cm.K, cm.R
+        f32 = dict(dtype=torch.float32, device=self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt)).to(self.device)  # noqa: E731
+        self.comp, self.jtype, self.y = up(cm.comp, np.int32), up(cm.jtype, np.int32), up(cm.y, np.uint8)
+        self.root_mean, self.root_var = torch.zeros(R, **f32), torch.ones(R, **f32)
+        self.root_ema = torch.tensor([[0.0, 1.0]] * R, **f64)
+        self.q_mean, self.q_var = torch.zeros(n, **f32), torch.ones(n, **f32)
+        self.g_ema = torch.tensor([[0.0, 1.0]] * n, **f64)
+        self.rz, self.z = torch.empty(R, K, **f32), torch.empty(n, K, **f32)
+        self.f_root, self.f = torch.empty(K, **f64), torch.empty(n, K, K, **f64)
+        self.g, self.w = torch.empty(n, K, **f64), torch.empty(n, K, **f64)
+        self.w_root, self.log_pe = torch.empty(K, **f64), torch.empty(1, **f64)
+        self.root_m, self.gm = torch.empty(R, 2, **f64), torch.empty(n, 2, **f64)
+        self.clamps = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def step(self, t: int, seed: int, root_eps: Optional[torch.Tensor] = None, eps: Optional[torch.Tensor] = None,
+             stream=None) -> None:
+        cm, L, s = self.cm, lib(), _stream(stream)
+        n, K, R = cm.n, cm.K, cm.R
+        check(L.qem_sample_normal(R, K, 0, seed, t, _ptr(self.root_mean), _ptr(self.root_var),
+                                  _ptr(root_eps) if root_eps is not None else None, _ptr(self.rz), s),
+              "qem_sample_normal")
+        check(L.qem_sample_normal(n, K, 1, seed, t, _ptr(self.q_mean), _ptr(self.q_var),
+                                  _ptr(eps) if eps is not None else None, _ptr(self.z), s), "qem_sample_normal")
+        check(L.qem_tables_crossed(n, K, cm.J, cm.C, cm.T, _ptr(self.rz), _ptr(self.root_mean), _ptr(self.root_var),
+                                   _ptr(self.z), _ptr(self.q_mean), _ptr(self.q_var), _ptr(self.comp),
+                                   _ptr(self.jtype), _ptr(self.y), _ptr(self.f_root), _ptr(self.f), s),
+              "qem_tables_crossed")
+        check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
+                                 _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        check(L.qem_moments_gaussian(n, K, R, _ptr(self.w_root), _ptr(self.rz), _ptr(self.w), _ptr(self.z),
+                                     _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_gaussian")
+        lam = 1.0 - self.new_weight
+        for m_new, ema, mean, var, d in ((self.root_m, self.root_ema, self.root_mean, self.root_var, R),
+                                         (self.gm, self.g_ema, self.q_mean, self.q_var, n)):
+            check(L.qem_mstep_categorical(0, 1, d, lam, self.var_floor, _ptr(m_new), _ptr(ema), _ptr(mean), _ptr(var),
+                                          None, None, None, _ptr(self.clamps), s), "qem_mstep_categorical")
+
+    def set_state(self, st: dict) -> None:
+        for k in ("root_mean", "root_var", "root_ema", "q_mean", "q_var", "g_ema"):
+            getattr(self, k).copy_(torch.from_numpy(np.asarray(st[k])).to(getattr(self, k).dtype))

@@ -302,3 +302,39 @@ def beta_binomial(n: int = 2000, K: int = 128, kappa: float = 8.0, n_max: int = 
     N = rng.integers(1, n_max + 1, n).astype(np.int32)
     y = rng.binomial(N, p).astype(np.int32)
     return BetaBinomial(n=n, K=K, kappa=kappa, y=y, N=N, mu_true=mu, p_true=p)
+
+
+@dataclasses.dataclass
+class Crossed:
+    """Bus-Breakdown-shaped crossed effects (row f4; R33): root
+    (mu, C company weights, T journey-type weights) ~ N(0, I); n year-borough groups
+    w_i ~ N(mu, 1); J delays per group ~ Bernoulli(sigmoid(w_i + cw_comp + jw_type)) with
+    per-observation company / journey-type index tables."""
+    n: int
+    J: int
+    C: int
+    T: int
+    K: int
+    comp: np.ndarray    # [n][J] int32
+    jtype: np.ndarray   # [n][J] int32
+    y: np.ndarray       # [n][J] uint8
+    root_true: np.ndarray
+    w_true: np.ndarray
+
+    @property
+    def R(self) -> int:
+        return 1 + self.C + self.T
+
+
+def bus_crossed(n: int = 120, J: int = 40, C: int = 57, T: int = 6, K: int = 64, seed: int = 9) -> Crossed:
+    """Ancestral draw from the prior (numpy PCG64, `seed`).  Defaults: 57 companies and 6
+    journey types as in the paper's Bus data, 12 years x 10 boroughs = 120
+    year-borough groups, 40 recorded journeys each."""
+    rng = np.random.default_rng(seed)
+    root = rng.normal(0.0, 1.0, 1 + C + T)
+    w = root[0] + rng.normal(0.0, 1.0, n)
+    comp = rng.integers(0, C, (n, J)).astype(np.int32)
+    jtype = rng.integers(0, T, (n, J)).astype(np.int32)
+    eta = w[:, None] + root[1 + comp] + root[1 + C + jtype]
+    y = (rng.random((n, J)) < 1.0 / (1.0 + np.exp(-eta))).astype(np.uint8)
+    return Crossed(n=n, J=J, C=C, T=T, K=K, comp=comp, jtype=jtype, y=y, root_true=root, w_true=w)
