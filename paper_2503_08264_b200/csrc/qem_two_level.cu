@@ -57,8 +57,11 @@ struct TLArgs {
 // One block.  Chooses k_ref (root sample nearest Q_root's mean in the
 // Q-metric; ties -> lowest k), builds the differenced row coefficients
 // (fp64 -> fp32) and the root factor f_root(k) = log p(root^k) - log q(root^k).
+// phase 0: everything in one block (FFMA path: the rank sort needs every row key);
+// phase 1: k_ref and RefInfo only; phase 2: the rows, split over blocks (tensor-core path, after
+// phase 1 -- the row work is store-bound on one SM's LSU).
 template <int D>
-__global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
+__global__ void __launch_bounds__(1024) k_root_prep(TLArgs a, int phase) {
   __shared__ double s_val[32];
   __shared__ int s_idx[32];
   __shared__ double s_lnv_ref;
@@ -66,14 +69,33 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
   __shared__ float s_key[QEM_MAX_K];
   const int K = a.K, tid = threadIdx.x;
   const int R = D + (a.scale_kind != QEM_SCALE_FIXED);
+  if (phase == 2) {  // k_ref from phase 1
+    if (tid == 0) {
+      const int kr = a.ws.ref->k_ref;
+      s_lnv_ref = a.scale_kind == QEM_SCALE_FIXED    ? log(a.fixed_var)
+                  : a.scale_kind == QEM_SCALE_LOGSIGMA ? 2.0 * (double)a.z_root[D * K + kr]
+                                                       : (double)a.z_root[D * K + kr];
+    }
+  } else {
   // k_ref = argmin_k sum_r (z_r^k - m_r)^2 / v_r
   double best = CUDART_INF;
   int bidx = 0x7fffffff;
   for (int k = tid; k < K; k += blockDim.x) {
+    // all R loads in flight before the arithmetic (a dependent load per dimension costs ~1 us)
+    float zr[D + 1], qm[D + 1], qv[D + 1];
+#pragma unroll
+    for (int r = 0; r < D + 1; ++r) {
+      zr[r] = r < R ? a.z_root[r * K + k] : 0.f;
+      qm[r] = r < R ? a.qr_m[r] : 0.f;
+      qv[r] = r < R ? a.qr_v[r] : 1.f;
+    }
     double q = 0.0;
-    for (int r = 0; r < R; ++r) {
-      const double dz = (double)a.z_root[r * K + k] - (double)a.qr_m[r];
-      q += dz * dz / (double)a.qr_v[r];
+#pragma unroll
+    for (int r = 0; r < D + 1; ++r) {
+      if (r < R) {
+        const double dz = (double)zr[r] - (double)qm[r];
+        q += dz * dz / (double)qv[r];
+      }
     }
     if (q < best || (q == best && k < bidx)) {
       best = q;
@@ -117,6 +139,8 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
     ref->e_ref = exp(-lnv);
     ref->bref_const = -0.5 * D * (kLn2Pi + lnv);
   }
+  if (phase == 1) return;
+  }
   // per-dimension constants of f_root: -(ln prior_var - ln v_r)/2 and 1/v_r
   for (int r = tid; r < R; r += blockDim.x) {
     s_qc[r] = -0.5 * (log(a.prior_var) - log((double)a.qr_v[r]));
@@ -128,7 +152,7 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
   const double e_ref = exp(-lnv_ref);
   constexpr int CW = D + 2;
   constexpr int RS = pad4(D + 3);
-  for (int k = tid; k < K; k += blockDim.x) {
+  for (int k = blockIdx.x * blockDim.x + tid; k < K; k += gridDim.x * blockDim.x) {
     double lnv, dlnv;
     if (a.scale_kind == QEM_SCALE_FIXED) {
       lnv = lnv_ref;
@@ -177,10 +201,20 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
     bt[1] = (float)(gamma * kLog2eD);
     // f_root(k) = sum_r lnN(z_r; prior) - lnN(z_r; Q_root), the log-normalisers hoisted (s_qc)
     double f = 0.0;
-    for (int r = 0; r < R; ++r) {
-      const double v = (double)a.z_root[r * K + k];
-      const double dp = v - a.prior_mean, dq = v - (double)a.qr_m[r];
-      f += s_qc[r] - 0.5 * dp * dp / a.prior_var + 0.5 * dq * dq * s_qc[QEM_MAX_D + 1 + r];
+    float zk[D + 1], qmk[D + 1];
+#pragma unroll
+    for (int r = 0; r < D + 1; ++r) {
+      zk[r] = r < R ? a.z_root[r * K + k] : 0.f;
+      qmk[r] = r < R ? a.qr_m[r] : 0.f;
+    }
+    const double ipv = 1.0 / a.prior_var;
+#pragma unroll
+    for (int r = 0; r < D + 1; ++r) {
+      if (r < R) {
+        const double v = (double)zk[r];
+        const double dp = v - a.prior_mean, dq = v - (double)qmk[r];
+        f += s_qc[r] - 0.5 * dp * dp * ipv + 0.5 * dq * dq * s_qc[QEM_MAX_D + 1 + r];
+      }
     }
     a.ws.f_root[k] = f;
     // sort key: |D| bound at unit column scale
@@ -189,7 +223,7 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a) {
     s_key[k] = fabsf(fc[0]) + fabsf(fc[1]) + sqrtf(cn);
   }
   __syncthreads();
-  if (a.tc) return;  // the tensor-core forward does not use the row order
+  if (a.tc || phase != 0) return;  // the tensor-core forward does not use the row order
   // rank sort (ties by index): perm[rank] = k
   for (int k = tid; k < K; k += blockDim.x) {
     const float kk = s_key[k];
@@ -642,14 +676,19 @@ template <int D>
 static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   const int K = a.K, rp = pick_rp(K, D);
   int nt = (K + 31) & ~31;
-  k_root_prep<D><<<1, nt, 0, st>>>(a);
+  const bool tc = D <= kTcD && c->tc;
+  if (tc) {  // k_ref in one block, then the rows over K/128 blocks
+    k_root_prep<D><<<1, nt, 0, st>>>(a, 1);
+    k_root_prep<D><<<(K + 127) / 128, 128, 0, st>>>(a, 2);
+  } else {
+    k_root_prep<D><<<1, nt, 0, st>>>(a, 0);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (c->desc.obs_kind == QEM_OBS_GAUSS && D != 1) return cudaErrorInvalidValue;
-  const bool tc = D <= kTcD && c->tc;
   if (tc) {
     k_rowop_tc<D><<<(K + 255) / 256, 256, 0, st>>>(a);
-    c->launches += 1;
+    c->launches += 2;  // + the second root-prep phase
   }
   prep_fn<D>(c->desc.obs_kind, tc)<<<c->grid_prep, prep_threads_tc<D>(K, tc), prep_smem<D>(K, a.J, tc), st>>>(a);
   e = cudaGetLastError();
