@@ -38,7 +38,9 @@ struct SampleArgs {
   int nlev;
   int K;
   int quads_per_row;
+  int units_per_row;  // quads_per_row / QPT
   FastDiv fqpr;
+  FastDiv fupr;
   int64_t total_quads;  // < 2^31 (checked at launch)
   uint2 key;
   int t_host;
@@ -90,59 +92,83 @@ __device__ __forceinline__ void bm_sincos2pi(uint32_t m, float& sn, float& cs) {
 // sampling, App. E; fp32 definition DESIGN.md R22).
 // One thread = 4 consecutive samples k of one latent dim (one Philox call,
 // two Box-Muller pairs).
-// One Philox4x32-10 call (4 samples) per quad; grid-stride over the quads (a few waves of
-// resident blocks: the per-thread start-up cost would otherwise rival the Philox rounds).
-__device__ __forceinline__ void sample_quad(const SampleArgs& a, uint32_t q, int t) {
-  int L = 0;
-#pragma unroll
-  for (int l = 1; l < 3; ++l)
-    if (l < a.nlev && q >= (uint32_t)a.lv[l].quads_begin) L = l;
-  const SampleLevel& s = a.lv[L];
-  const uint32_t local = q - (uint32_t)s.quads_begin;
-  const uint32_t row32 = a.fqpr.div(local);
+// One Philox4x32-10 call per quad of 4 samples; a thread takes QPT consecutive quads of one row
+// (QPT = 2 when K % 8 == 0: the row's mean / sd loads, the index divisions and the counter
+// setup are shared), grid-stride over the units of each level in turn (the level's parameters
+// are hoisted out of the loop).
+template <int QPT>
+__device__ __forceinline__ void sample_unit(const SampleArgs& a, const SampleLevel& s, uint32_t local, int t) {
+  const uint32_t row32 = a.fupr.div(local);
   const int64_t row = row32;
-  const int k0 = (int)(local - row32 * (uint32_t)a.quads_per_row) * 4;
+  const int k0 = (int)(local - row32 * (uint32_t)a.units_per_row) * 4 * QPT;
   const float m = s.qm[row];
   const float sd = __fsqrt_rn(s.qv[row]);
-  float e[4];
+  float e[QPT][4];
   if (s.eps != nullptr) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) e[j] = (k0 + j < a.K) ? s.eps[row * a.K + k0 + j] : 0.f;
+    for (int u = 0; u < QPT; ++u)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) e[u][j] = (k0 + 4 * u + j < a.K) ? s.eps[row * a.K + k0 + 4 * u + j] : 0.f;
   } else {
     const uint32_t inst = s.fdims.div(row32);
     const int dim = (int)(row32 - inst * (uint32_t)s.dims);
     const uint32_t ginst = (uint32_t)(inst + s.inst_offset);
-    const uint4 o = philox4x32_10(
-        make_uint4((uint32_t)(k0 >> 2), (uint32_t)dim, ginst,
-                   ((uint32_t)s.level << 24) | (((uint32_t)t | a.iter_or) & 0xffffffu)),
-        a.key);
-    // Box-Muller on u = ((x >> 9) + 0.5) * 2^-23: radius and angle evaluated
-    // from the integer bits (bm_radius, bm_sincos2pi: ~3x fewer instructions than
-    // sqrtf(-2 logf(u)) and sincospif(2u); absolute error <= ~1e-6 on eps vs the fp64 transform).
-    const float r0 = bm_radius(o.x >> 9), r1 = bm_radius(o.z >> 9);
-    float s0, c0, s1, c1;
-    bm_sincos2pi(o.y >> 9, s0, c0);
-    bm_sincos2pi(o.w >> 9, s1, c1);
-    e[0] = r0 * c0;
-    e[1] = r0 * s0;
-    e[2] = r1 * c1;
-    e[3] = r1 * s1;
+    const uint32_t word = ((uint32_t)s.level << 24) | (((uint32_t)t | a.iter_or) & 0xffffffu);
+#pragma unroll
+    for (int u = 0; u < QPT; ++u) {
+      const uint4 o = philox4x32_10(make_uint4((uint32_t)(k0 >> 2) + u, (uint32_t)dim, ginst, word), a.key);
+      // Box-Muller on u = ((x >> 9) + 0.5) * 2^-23: radius and angle evaluated
+      // from the integer bits (bm_radius, bm_sincos2pi: ~3x fewer instructions than
+      // sqrtf(-2 logf(u)) and sincospif(2u); absolute error <= ~1e-6 on eps vs the fp64 transform).
+      const float r0 = bm_radius(o.x >> 9), r1 = bm_radius(o.z >> 9);
+      float s0, c0, s1, c1;
+      bm_sincos2pi(o.y >> 9, s0, c0);
+      bm_sincos2pi(o.w >> 9, s1, c1);
+      e[u][0] = r0 * c0;
+      e[u][1] = r0 * s0;
+      e[u][2] = r1 * c1;
+      e[u][3] = r1 * s1;
+    }
   }
   float* zr = s.z + row * a.K + k0;
-  if (k0 + 4 <= a.K && (a.K & 3) == 0) {
-    *reinterpret_cast<float4*>(zr) =
-        make_float4(__fmaf_rn(sd, e[0], m), __fmaf_rn(sd, e[1], m), __fmaf_rn(sd, e[2], m), __fmaf_rn(sd, e[3], m));
-  } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (k0 + j < a.K) zr[j] = __fmaf_rn(sd, e[j], m);
+  for (int u = 0; u < QPT; ++u) {
+    if (k0 + 4 * u + 4 <= a.K && (a.K & 3) == 0) {
+      *reinterpret_cast<float4*>(zr + 4 * u) = make_float4(__fmaf_rn(sd, e[u][0], m), __fmaf_rn(sd, e[u][1], m),
+                                                           __fmaf_rn(sd, e[u][2], m), __fmaf_rn(sd, e[u][3], m));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (k0 + 4 * u + j < a.K) zr[4 * u + j] = __fmaf_rn(sd, e[u][j], m);
+    }
   }
 }
 
+template <int QPT>
 __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
   const int t = resolve_iter(a.t_host, a.d_iter);
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)a.total_quads; q += stride) sample_quad(a, q, t);
+  for (int L = 0; L < a.nlev; ++L) {
+    const SampleLevel s = a.lv[L];
+    const uint32_t units = (uint32_t)s.rows * (uint32_t)a.units_per_row;
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < units; u += stride) sample_unit<QPT>(a, s, u, t);
+  }
+}
+
+static cudaError_t launch_k_sample(SampleArgs& a, int64_t cap_blocks, cudaStream_t st) {
+  const int qpt = (a.K % 8 == 0) ? 2 : 1;
+  a.units_per_row = a.quads_per_row / qpt;
+  a.fupr.init((uint32_t)a.units_per_row);
+  int64_t units = 0;
+  for (int l = 0; l < a.nlev; ++l) units += a.lv[l].rows * a.units_per_row;
+  int64_t blocks = (units + 255) / 256;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > cap_blocks) blocks = cap_blocks;
+  if (qpt == 2)
+    k_sample<2><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else
+    k_sample<1><<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 // Context-free Gaussian sampler (qem_sample_normal): `rows` latent rows of K samples, one level
@@ -171,9 +197,7 @@ cudaError_t launch_sample_rows(int64_t rows, int K, int level, uint64_t seed, in
   a.total_quads = rows * a.quads_per_row;
   if (a.total_quads == 0) return cudaSuccess;
   if (a.total_quads >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;
-  const int64_t blocks = (a.total_quads + 255) / 256;
-  k_sample<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k_sample(a, 148 * 32, st);
 }
 
 cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps, cudaStream_t st,
@@ -221,9 +245,7 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
   }
   a.nlev = nlev;
   a.total_quads = quads;
-  const int threads = 256;
-  int64_t blocks = (quads + threads - 1) / threads;
-  if (blocks == 0) return cudaSuccess;
+  if (quads == 0) return cudaSuccess;
   if (quads >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;  // 32-bit sample indexing
   static const int sms = [] {
     int dev = 0, n = 148;
@@ -231,8 +253,8 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
     return n;
   }();
   const int64_t cap = (int64_t)sms * 8 * 4;  // four waves of 8 resident 256-thread blocks per SM
-  if (blocks > cap) blocks = cap;
-  k_sample<<<(unsigned)blocks, threads, 0, st>>>(a);
+  const cudaError_t e = launch_k_sample(a, cap, st);
+  if (e != cudaSuccess) return e;
   c->launches += 1;
   return cudaGetLastError();
 }
