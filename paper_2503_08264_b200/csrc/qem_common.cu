@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
 }
 
 static cudaError_t launch_k_sample(SampleArgs& a, int64_t cap_blocks, cudaStream_t st) {
-  const int qpt = (a.K % 8 == 0) ? 2 : 1;
+  const int qpt = (a.K % 16 == 0) ? 4 : ((a.K % 8 == 0) ? 2 : 1);
   a.units_per_row = a.quads_per_row / qpt;
   a.fupr.init((uint32_t)a.units_per_row);
   int64_t units = 0;
@@ -164,7 +164,9 @@ static cudaError_t launch_k_sample(SampleArgs& a, int64_t cap_blocks, cudaStream
   int64_t blocks = (units + 255) / 256;
   if (blocks == 0) return cudaSuccess;
   if (blocks > cap_blocks) blocks = cap_blocks;
-  if (qpt == 2)
+  if (qpt == 4)
+    k_sample<4><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else if (qpt == 2)
     k_sample<2><<<(unsigned)blocks, 256, 0, st>>>(a);
   else
     k_sample<1><<<(unsigned)blocks, 256, 0, st>>>(a);
