@@ -85,6 +85,9 @@ typedef int32_t qem_status;
 #define QEM_QFAMILY_BETA 2        /* mean params (E ln z, E ln(1-z))    -> (a, b)               */
 #define QEM_QFAMILY_BERNOULLI 3   /* mean param  E z                    -> p                    */
 #define QEM_QFAMILY_CATEGORICAL 4 /* mean params E onehot(z) [C]        -> p [C] (normalised)   */
+#define QEM_QFAMILY_DIRICHLET 5   /* mean params E ln z [C]             -> a [C] (C <= 16)      */
+#define QEM_QFAMILY_BINOMIAL 6    /* mean param  E z, C = trials N      -> p = E z / N          */
+#define QEM_QFAMILY_MULTINOMIAL 7 /* mean params E z [C]                -> p [C] (normalised)   */
 #define QEM_EXPFAM_OK 0
 #define QEM_EXPFAM_INFEASIBLE 1      /* moments outside the family's mean-parameter space        */
 #define QEM_EXPFAM_NO_CONVERGENCE 2  /* the Newton iteration did not reach its tolerance          */
@@ -412,12 +415,14 @@ qem_status qem_estep_tables(int64_t n, int32_t K, const double* d_f_root, const 
 /* EMA over mean parameters + M-step for non-Gaussian Q families (Alg. 1 lines 3, 6; Eq. 9;
    PAPER.md:218 "a Beta's parameters are recovered from expectations of log transformations",
    PAPER.md:247).  Context-free, stream-ordered, one device thread per latent instance, fp64.
-   S = 2 (Gamma, Beta), 1 (Bernoulli), C (Categorical) mean parameters per instance:
+   S = 2 (Gamma, Beta), 1 (Bernoulli, Binomial with C = trials), C (Categorical, Dirichlet,
+   Multinomial) mean parameters per instance (PAPER.md:10's list of families):
      d_m_new  [n][S]  one-step mean parameters (input)
      d_m_ema  [n][S]  EMA state, updated in place: m <- lam m + (1 - lam) m_new
      d_params [n][S]  conventional parameters of the updated state (output): Gamma (k, th) by
                       Newton on psi(k) - ln k = m2 - ln m1, th = k/m1; Beta (a, b) by damped
-                      2-d Newton in (ln a, ln b); Bernoulli p; Categorical p normalised
+                      2-d Newton in (ln a, ln b); Dirichlet a by Newton with a Sherman-Morrison
+                      Hessian; Bernoulli p; Binomial p = m/N; Categorical / Multinomial p normalised
      d_status [n]     QEM_EXPFAM_* per instance (nullable)
    Errors: QEM_INVALID_ARGUMENT for a bad family / n < 0 / C < 1 / null arrays. */
 qem_status qem_mstep_family(int32_t family, int64_t n, int32_t C, double lam, const double* d_m_new,

@@ -7,6 +7,9 @@ PAPER.md:218).  Plain scipy, fp64, following the definitions:
 
   Gamma(k shape, th rate)  T(z) = (z, ln z)          m = (k/th, psi(k) - ln th)
   Beta(a, b)               T(z) = (ln z, ln(1-z))    m = (psi(a) - psi(a+b), psi(b) - psi(a+b))
+  Dirichlet(a_1..a_C)      T(z) = ln z               m = psi(a) - psi(sum a)
+  Binomial(N, p)           T(z) = z                  m = N p
+  Multinomial(N, p)        T(z) = z                  m = N p
   Bernoulli(p)             T(z) = z                  m = p
   Categorical(p_1..p_C)    T(z) = onehot(z)          m = p
 
@@ -21,7 +24,7 @@ import numpy as np
 from scipy import optimize
 from scipy.special import digamma
 
-GAMMA, BETA, BERNOULLI, CATEGORICAL = 1, 2, 3, 4
+GAMMA, BETA, BERNOULLI, CATEGORICAL, DIRICHLET, BINOMIAL, MULTINOMIAL = 1, 2, 3, 4, 5, 6, 7
 
 
 def gamma_mean(k, th):
@@ -59,7 +62,24 @@ def beta_params(m):
     return np.exp(r.x)
 
 
-def params_from_mean(family, m):
+def dirichlet_mean(a):
+    a = np.asarray(a, np.float64)
+    return digamma(a) - digamma(a.sum())
+
+
+def dirichlet_params(m):
+    """a with dirichlet_mean(a) = m; requires every m_c < 0 and sum exp(m) < 1."""
+    m = np.asarray(m, np.float64)
+    if not (np.all(m < 0) and np.exp(m).sum() < 1):
+        raise ValueError("infeasible Dirichlet moments")
+    f = lambda x: dirichlet_mean(np.exp(x)) - m  # noqa: E731
+    r = optimize.root(f, x0=np.zeros_like(m), method="hybr", tol=1e-15)
+    if not r.success or np.max(np.abs(f(r.x))) > 1e-10:
+        r = optimize.root(f, x0=np.full_like(m, -0.5), method="lm", tol=1e-15)
+    return np.exp(r.x)
+
+
+def params_from_mean(family, m, C=None):
     """Conventional parameters from mean parameters, row by row (m: [n][S])."""
     m = np.atleast_2d(np.asarray(m, np.float64))
     if family == GAMMA:
@@ -68,12 +88,16 @@ def params_from_mean(family, m):
         return np.array([beta_params(r) for r in m])
     if family == BERNOULLI:
         return m.copy()
-    if family == CATEGORICAL:
+    if family in (CATEGORICAL, MULTINOMIAL):
         return m / m.sum(axis=1, keepdims=True)
+    if family == DIRICHLET:
+        return np.array([dirichlet_params(r) for r in m])
+    if family == BINOMIAL:
+        return m / C
     raise ValueError(family)
 
 
-def ema_mstep(family, lam, m_ema, m_new):
+def ema_mstep(family, lam, m_ema, m_new, C=None):
     """EMA over mean parameters (Eq. 9, history weight lam, R5), then the M-step."""
     m = lam * np.asarray(m_ema, np.float64) + (1.0 - lam) * np.asarray(m_new, np.float64)
-    return m, params_from_mean(family, m)
+    return m, params_from_mean(family, m, C)

@@ -345,9 +345,12 @@ qem_status qem_estep_evidence(qem_ctx* c, void* stream) {
 
 qem_status qem_mstep_family(int32_t family, int64_t n, int32_t C, double lam, const double* d_m_new,
                             double* d_m_ema, double* d_params, int32_t* d_status, void* stream) {
-  if (family < QEM_QFAMILY_GAMMA || family > QEM_QFAMILY_CATEGORICAL)
+  if (family < QEM_QFAMILY_GAMMA || family > QEM_QFAMILY_MULTINOMIAL)
     return fail(QEM_INVALID_ARGUMENT, "unknown Q family %d", family);
-  if (n < 0 || (family == QEM_QFAMILY_CATEGORICAL && C < 1)) return fail(QEM_INVALID_ARGUMENT, "bad n or C");
+  const bool needs_c = family == QEM_QFAMILY_CATEGORICAL || family == QEM_QFAMILY_DIRICHLET ||
+                       family == QEM_QFAMILY_BINOMIAL || family == QEM_QFAMILY_MULTINOMIAL;
+  if (n < 0 || (needs_c && C < 1) || (family == QEM_QFAMILY_DIRICHLET && C > 16))
+    return fail(QEM_INVALID_ARGUMENT, "bad n or C");
   if (n > 0 && (!d_m_new || !d_m_ema || !d_params)) return fail(QEM_INVALID_ARGUMENT, "null array");
   if (!(lam >= 0.0 && lam < 1.0)) return fail(QEM_INVALID_ARGUMENT, "lam must be in [0, 1)");
   const cudaError_t e =

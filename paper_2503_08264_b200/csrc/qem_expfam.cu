@@ -7,6 +7,9 @@
 //                     solve psi(k) - ln k = m2 - ln m1 for ln k (Newton), th = k / m1
 //   Beta(a, b)        m = (E ln z, E ln(1-z)) = (psi(a) - psi(a+b), psi(b) - psi(a+b)):
 //                     damped 2-d Newton in (ln a, ln b)
+//   Dirichlet(a[C])   m = E ln z = psi(a) - psi(sum a): Newton with a Sherman-Morrison Hessian
+//   Binomial(N, p)    m = E z = N p  (N given as C)
+//   Multinomial(N, p) m = E z = N p  (p = m / sum m, as Categorical)
 //   Bernoulli(p)      m = p
 //   Categorical(p)    m = p (normalised)
 // One thread per latent instance, fp64 throughout (digamma / trigamma by recurrence to x >= 8
@@ -110,6 +113,50 @@ __device__ int beta_params(double m1, double m2, double& a, double& b) {
   return fmax(fabs(r1), fabs(r2)) < 1e-10 ? QEM_EXPFAM_OK : QEM_EXPFAM_NO_CONVERGENCE;
 }
 
+// Dirichlet (a_1..a_C) from m_c = E ln z_c = psi(a_c) - psi(a_0), a_0 = sum a: Newton in a with
+// the Hessian diag(psi'(a_c)) - psi'(a_0) 11^T inverted by Sherman-Morrison (O(C)), halving the
+// step until every a_c stays positive; start from a_0 = 1/(1 - sum e^m), a_c = a_0 e^m_c (Minka's
+// moment start).  C <= QEM_DIRICHLET_MAX_C.
+#define QEM_DIRICHLET_MAX_C 16
+__device__ int dirichlet_params(const double* m, int C, double* a) {
+  double se = 0.0;
+  for (int c = 0; c < C; ++c) {
+    if (!(m[c] < 0.0)) return QEM_EXPFAM_INFEASIBLE;
+    se += exp(m[c]);
+  }
+  if (!(se < 1.0) || C > QEM_DIRICHLET_MAX_C) return QEM_EXPFAM_INFEASIBLE;
+  double al[QEM_DIRICHLET_MAX_C], g[QEM_DIRICHLET_MAX_C], q[QEM_DIRICHLET_MAX_C];
+  const double a0i = 1.0 / (1.0 - se);
+  for (int c = 0; c < C; ++c) al[c] = a0i * exp(m[c]) + 1e-3;
+  for (int it = 0; it < 200; ++it) {
+    double a0 = 0.0;
+    for (int c = 0; c < C; ++c) a0 += al[c];
+    const double p0 = digamma_d(a0), z = -trigamma_d(a0);
+    double gmax = 0.0, sgq = 0.0, siq = 0.0;
+    for (int c = 0; c < C; ++c) {
+      g[c] = digamma_d(al[c]) - p0 - m[c];
+      q[c] = trigamma_d(al[c]);
+      gmax = fmax(gmax, fabs(g[c]));
+      sgq += g[c] / q[c];
+      siq += 1.0 / q[c];
+    }
+    if (gmax < 1e-13) {
+      for (int c = 0; c < C; ++c) a[c] = al[c];
+      return QEM_EXPFAM_OK;
+    }
+    const double b = sgq / (1.0 / z + siq);
+    double lamb = 1.0;
+    for (int h = 0; h < 60; ++h, lamb *= 0.5) {
+      bool ok = true;
+      for (int c = 0; c < C; ++c) ok = ok && al[c] - lamb * (g[c] - b) / q[c] > 0.0;
+      if (ok) break;
+    }
+    for (int c = 0; c < C; ++c) al[c] -= lamb * (g[c] - b) / q[c];
+  }
+  for (int c = 0; c < C; ++c) a[c] = al[c];
+  return QEM_EXPFAM_NO_CONVERGENCE;
+}
+
 struct FamArgs {
   int family, S, C;
   int64_t n;
@@ -140,7 +187,14 @@ __global__ void __launch_bounds__(128) k_mstep_family(FamArgs a) {
     } else if (a.family == QEM_QFAMILY_BERNOULLI) {
       st = (m[0] >= 0.0 && m[0] <= 1.0) ? QEM_EXPFAM_OK : QEM_EXPFAM_INFEASIBLE;
       p[0] = fmin(fmax(m[0], 0.0), 1.0);
-    } else {  // categorical
+    } else if (a.family == QEM_QFAMILY_DIRICHLET) {
+      st = dirichlet_params(m, a.C, p);
+      if (st == QEM_EXPFAM_INFEASIBLE)
+        for (int c = 0; c < a.C; ++c) p[c] = CUDART_NAN;
+    } else if (a.family == QEM_QFAMILY_BINOMIAL) {  // m = E z = N p, C = N trials
+      st = (m[0] >= 0.0 && m[0] <= a.C) ? QEM_EXPFAM_OK : QEM_EXPFAM_INFEASIBLE;
+      p[0] = fmin(fmax(m[0] / a.C, 0.0), 1.0);
+    } else {  // categorical / multinomial: m = E onehot(z) or E counts, p = m / sum m
       double tot = 0.0;
       for (int c = 0; c < a.C; ++c) tot += m[c];
       st = tot > 0.0 ? QEM_EXPFAM_OK : QEM_EXPFAM_INFEASIBLE;
@@ -154,7 +208,9 @@ cudaError_t launch_mstep_family(int family, int64_t n, int C, double lam, const 
                                 double* params, int32_t* status, cudaStream_t st) {
   FamArgs a{};
   a.family = family;
-  a.S = family == QEM_QFAMILY_GAMMA || family == QEM_QFAMILY_BETA ? 2 : (family == QEM_QFAMILY_BERNOULLI ? 1 : C);
+  a.S = family == QEM_QFAMILY_GAMMA || family == QEM_QFAMILY_BETA
+            ? 2
+            : (family == QEM_QFAMILY_BERNOULLI || family == QEM_QFAMILY_BINOMIAL ? 1 : C);
   a.C = C;
   a.n = n;
   a.lam = lam;

@@ -32,7 +32,7 @@ def model_validate(m) -> Optional[str]:
     return None if st == _lib.OK else buf.value.decode()
 
 
-GAMMA, BETA, BERNOULLI, CATEGORICAL = 1, 2, 3, 4
+GAMMA, BETA, BERNOULLI, CATEGORICAL, DIRICHLET, BINOMIAL, MULTINOMIAL = 1, 2, 3, 4, 5, 6, 7
 
 
 def mstep_family(family: int, lam: float, m_new: torch.Tensor, m_ema: torch.Tensor, C: int = 1, stream=None):

@@ -51,6 +51,27 @@ def test_round_trip(family):
         np.testing.assert_allclose(m2, m, rtol=1e-9, atol=1e-12)
 
 
+def test_dirichlet_round_trip_and_beta_special_case():
+    """Dirichlet: mean -> conventional -> mean over random a (C = 2..6); C = 2 is the Beta."""
+    rng = np.random.default_rng(21)
+    for C in (2, 3, 6):
+        for _ in range(40):
+            a = np.exp(rng.uniform(-1.5, 2.5, C))
+            q = expfam.dirichlet_params(expfam.dirichlet_mean(a))
+            np.testing.assert_allclose(q, a, rtol=1e-7)
+    a = np.array([2.5, 0.7])
+    np.testing.assert_allclose(expfam.dirichlet_mean(a), expfam.beta_mean(*a), rtol=1e-14)
+    np.testing.assert_allclose(expfam.dirichlet_params(expfam.beta_mean(*a)), expfam.beta_params(expfam.beta_mean(*a)),
+                               rtol=1e-8)
+
+
+def test_binomial_and_multinomial_mean_maps():
+    """E z = N p for Binomial(N, p) and Multinomial(N, p) (textbook means), so p = m / N."""
+    np.testing.assert_allclose(expfam.params_from_mean(expfam.BINOMIAL, [[6.0]], C=20), [[0.3]])
+    m = 12 * np.array([[0.2, 0.5, 0.3]])
+    np.testing.assert_allclose(expfam.params_from_mean(expfam.MULTINOMIAL, m), [[0.2, 0.5, 0.3]])
+
+
 def test_infeasible_moments_rejected():
     with pytest.raises(ValueError):
         expfam.gamma_params([1.0, 0.5])  # E[ln z] >= ln E[z] violates Jensen
@@ -71,7 +92,8 @@ def test_ema_fixed_point():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("family", [expfam.GAMMA, expfam.BETA, expfam.BERNOULLI, expfam.CATEGORICAL])
+@pytest.mark.parametrize("family", [expfam.GAMMA, expfam.BETA, expfam.BERNOULLI, expfam.CATEGORICAL,
+                                    expfam.DIRICHLET, expfam.BINOMIAL, expfam.MULTINOMIAL])
 def test_device_mstep_family_matches_oracle(family):
     import torch
     from paper_2503_08264_b200.qem import mstep_family
@@ -85,10 +107,19 @@ def test_device_mstep_family_matches_oracle(family):
         m_new = np.array([fwd(*p) for p in pb])
     elif family == expfam.BERNOULLI:
         m_ema, m_new = rng.uniform(0, 1, (n, 1)), rng.uniform(0, 1, (n, 1))
+    elif family == expfam.DIRICHLET:
+        n = 400  # the oracle's scipy root per instance is slow
+        m_ema = np.array([expfam.dirichlet_mean(a) for a in np.exp(rng.uniform(-1.0, 2.0, (n, C)))])
+        m_new = np.array([expfam.dirichlet_mean(a) for a in np.exp(rng.uniform(-1.0, 2.0, (n, C)))])
+    elif family == expfam.BINOMIAL:
+        C = 20  # trials
+        m_ema, m_new = rng.uniform(0, C, (n, 1)), rng.uniform(0, C, (n, 1))
+    elif family == expfam.MULTINOMIAL:
+        m_ema, m_new = 9 * rng.dirichlet(np.ones(C), n), 9 * rng.dirichlet(np.ones(C), n)
     else:
         m_ema, m_new = rng.dirichlet(np.ones(C), n), rng.dirichlet(np.ones(C), n)
     lam = 0.7
-    s_ref, p_ref = expfam.ema_mstep(family, lam, m_ema, m_new)
+    s_ref, p_ref = expfam.ema_mstep(family, lam, m_ema, m_new, C=C)
     dev = torch.device("cuda")
     te, tn = torch.tensor(m_ema, device=dev), torch.tensor(m_new, device=dev)
     params, status = mstep_family(family, lam, tn, te, C=C)
