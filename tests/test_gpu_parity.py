@@ -73,6 +73,9 @@ CASES = {
     "K1": dict(cid=4, n=9, K=1),
     "n1_K33": dict(cid=2, n=1, K=33, d=4),
     "d8_K512": dict(cid=5, n=11, K=512, d=8),
+    # maximum K (QEM_MAX_K) on the FFMA tiles: d = 18 (config 2's dimension) and d = 3, ragged n
+    "maxK_d18": dict(cid=2, n=29, K=1024),
+    "maxK_d3_ragged": dict(cid=5, n=151, K=1024, d=3, J=9),
 }
 
 
