@@ -117,6 +117,7 @@ size_t carve(qem_ctx* c, char* base) {
     c->tw.cvec = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->n_local));
     c->tw.perm = reinterpret_cast<int*>(take(sizeof(int) * K));
     c->tw.alpha_d = reinterpret_cast<double*>(take(sizeof(double) * K));
+    c->tw.coef_d = reinterpret_cast<double*>(take(sizeof(double) * K * (D + 1)));
     c->tw.hmsg = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
     c->tw.tA = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->n_local * K));
     c->tw.bwd_coef = reinterpret_cast<float*>(take(sizeof(float) * K * (D + 1)));

@@ -34,6 +34,8 @@ struct TwoLevelWs {
   double* cvec;       // [n_local]  c_i = g_i(k_ref)
   int* perm;          // [K]        forward row order (rows sorted by coefficient magnitude)
   double* alpha_d;    // [K]        alpha_k in fp64
+  double* coef_d;     // [K][D+1]   gamma_k, c_k[D]: the fp32 row coefficients held as fp64 (the TC
+                      //            forward's aux merge evaluates alpha'_ik without conversions)
   // tensor-core path (d = 16, K % 256 == 0): bf16x3 operands, DESIGN.md "Tensor cores"
   void* rowop;        // [K] x 96 B  log2e c_k split in 3 bf16 (K-major canonical layout)
   void* rowop_x;      // [K] x 32 B  forward row extra slab (log2e gamma_k pattern, lP switch)

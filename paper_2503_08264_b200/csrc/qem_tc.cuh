@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
     const int atid = tid - kTcThreads;
     constexpr int NTA = 32 * kFwdAuxWarps;
     int md = 5;
-    float mi[D];
+    double mi[D];  // the group's Q mean, converted once per group (not per row)
     float M2 = 0.f;
     int64_t j = 0, i = blockIdx.x;
     int rb = 0;
@@ -760,8 +760,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
         M2 = 0.f;
 #pragma unroll
         for (int r = 0; r < D; ++r) {
-          mi[r] = a.q_m[i * D + r];
-          M2 = fmaf(mi[r], mi[r], M2);
+          const float mf = a.q_m[i * D + r];
+          mi[r] = (double)mf;
+          M2 = fmaf(mf, mf, M2);
         }
         if (atid == 0) {
           atomicAdd(&a.cnt->mode_hist[md], 1ull);
@@ -792,10 +793,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
           h = log1pf(sm);
         }
         // alpha'_ik = D_k(m_i) = alpha0_k + gamma_k |m_i|^2 + c0_k . m_i in fp64
-        const float* fc = a.ws.fwd_coef + (size_t)k * (D + 2);
-        double ap = a.ws.alpha_d[k] + (double)fc[1] * (double)M2;
+        const double* cd = a.ws.coef_d + (size_t)k * (D + 1);  // (gamma, c0[D]) as fp64: no conversions
+        double ap = fma(cd[0], (double)M2, a.ws.alpha_d[k]);
 #pragma unroll
-        for (int r = 0; r < D; ++r) ap += (double)fc[2 + r] * (double)mi[r];
+        for (int r = 0; r < D; ++r) ap = fma(cd[1 + r], mi[r], ap);
         const double dgd = ap + (double)h;
         a.ws.hmsg[(size_t)i * K + k] = h;  // re-centred message, the backward's row constant
         a.ws.dg[(size_t)i * K + k] = (float)dgd;

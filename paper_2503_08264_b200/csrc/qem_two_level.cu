@@ -196,6 +196,12 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a, int phase) {
     const double gamma = -0.5 * (ek - e_ref);
     fc[0] = (float)alpha;
     fc[1] = (float)gamma;
+    if (a.tc) {  // the same fp32 values, held as fp64 for the forward's aux merge
+      double* cd = a.ws.coef_d + (size_t)k * (D + 1);
+      cd[0] = (double)fc[1];
+#pragma unroll
+      for (int r = 0; r < D; ++r) cd[1 + r] = (double)fc[2 + r];
+    }
     a.ws.alpha_d[k] = alpha;
     bt[0] = (float)(alpha * kLog2eD);
     bt[1] = (float)(gamma * kLog2eD);
