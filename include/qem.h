@@ -330,6 +330,14 @@ qem_status qem_backward_resample(qem_ctx* ctx, int32_t S, uint64_t seed, int32_t
 qem_status qem_predictive_loglik(qem_ctx* ctx, int32_t S, const int32_t* d_idx, int32_t J_test,
                                  const void* d_x_test, const uint8_t* d_y_test, double* d_ll_part,
                                  double* d_ll_s, double* d_pll, void* stream);
+/* Global importance weighting (App. A, Eq. glob_iw; the baseline MPIW improves
+   on): after qem_estep_forward on a world-1 two-level context, the K joint draws with every
+   latent at the same index k: d_diag [n][K] = B_i(k, z_i^k) + A_i(z_i^k) (fp64),
+   d_log_pe [1] = lse_k (f_root(k) + sum_i d_diag[i][k]) - ln K, d_w [K] = the normalised
+   weights, and (when d_m1 != NULL) d_m1 [n][d] = sum_k w_k z_i^k.  d_scratch: >= n*K doubles.
+   QEM_UNSUPPORTED for the three-level family or a sharded context. */
+qem_status qem_global_iw(qem_ctx* ctx, double* d_diag, double* d_scratch, double* d_log_pe, double* d_w,
+                         double* d_m1, void* stream);
 /* d_out[0] = log (1/n) sum_i exp(d_x[i]) (fp64, fixed order), n >= 1. */
 qem_status qem_logmeanexp(int64_t n, const double* d_x, double* d_out, void* stream);
 

@@ -100,3 +100,23 @@ def test_loglik(m, z, test, idx):
 def predictive_loglik(ll_part):
     ll_s = np.asarray(ll_part).sum(axis=1)
     return float(logsumexp(ll_s) - np.log(len(ll_s))), ll_s
+
+
+def global_iw(m, z, q, data, est):
+    """Global importance weighting (App. A, Eq. glob_iw): K joint draws with every
+    latent at index k.  log r_k = f_root(k) + sum_i [B_i(k, z_i^k) + A_i(z_i^k)] with B + A recovered
+    from the conditionals (log P + ln K + g); returns log_pe, weights w [K], group means m1 [n][d]."""
+    K, d, R = m.K, m.d, m.R
+    lk = np.log(K)
+    diag = np.zeros((m.n, K))
+    for i in range(m.n):
+        lp = log_conditionals(m, z, q, data, est["g"], i)
+        diag[i] = np.diag(lp) + lk + np.asarray(est["g"])[i]
+    zr = np.asarray(z[0], np.float64).reshape(R, K)
+    qrm, qrv = (np.asarray(a, np.float64) for a in q[0])
+    f_root = sum(_lnN(zr[r], m.prior_mean, m.prior_var) - _lnN(zr[r], qrm[r], qrv[r]) for r in range(R))
+    a = f_root + diag.sum(axis=0)
+    lse = logsumexp(a)
+    w = np.exp(a - lse)
+    zg = np.asarray(z[1], np.float64).reshape(m.n, d, K)
+    return dict(log_pe=lse - lk, w=w, m1=(zg * w[None, None, :]).sum(axis=2), diag=diag)

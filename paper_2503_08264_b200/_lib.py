@@ -21,7 +21,7 @@ EXPORTS = [
     "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_estep_evidence",
     "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_estep_tables", "qem_sample_normal",
     "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical", "qem_moments_categorical", "qem_mstep_categorical",
-    "qem_loglik_bernoulli_states", "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_sample_gamma",
+    "qem_loglik_bernoulli_states", "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_global_iw", "qem_sample_gamma",
     "qem_tables_gamma_poisson", "qem_moments_gamma", "qem_sample_beta", "qem_tables_beta_binomial",
     "qem_moments_beta", "qem_tables_crossed", "qem_moments_gaussian", "qem_iterate",
     "qem_read_flags", "qem_read_mode_hist", "qem_set_kernel_events", "qem_kernel_launches", "qem_pair_path", "qem_copy_messages", "qem_status_str", "qem_last_error",
@@ -87,6 +87,7 @@ def lib() -> ctypes.CDLL:
         L.qem_backward_resample.argtypes = [vp, i32, u64, vp, vp, vp]
         L.qem_predictive_loglik.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, vp, vp]
         L.qem_logmeanexp.argtypes = [i64, vp, vp, vp]
+        L.qem_global_iw.argtypes = [vp] + [vp] * 6
         L.qem_sample_gamma.argtypes = [i64, i32, u64, i32, vp, vp, vp]
         L.qem_tables_gamma_poisson.argtypes = [i64, i32, i32, ctypes.c_double] + [vp] * 9
         L.qem_moments_gamma.argtypes = [i64, i32] + [vp] * 7
@@ -128,7 +129,8 @@ def lib() -> ctypes.CDLL:
                      "qem_evidence_root", "qem_workspace_bytes", "qem_create_in", "qem_estep_tables",
                      "qem_sample_normal", "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical",
                      "qem_moments_categorical", "qem_mstep_categorical", "qem_loglik_bernoulli_states",
-                     "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_sample_gamma",
+                     "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_global_iw",
+                     "qem_sample_gamma",
                      "qem_tables_gamma_poisson", "qem_moments_gamma", "qem_sample_beta",
                      "qem_tables_beta_binomial", "qem_moments_beta", "qem_tables_crossed",
                      "qem_moments_gaussian"]:

@@ -394,6 +394,17 @@ qem_status qem_predictive_loglik(qem_ctx* c, int32_t S, const int32_t* d_idx, in
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_predictive_loglik");
 }
 
+qem_status qem_global_iw(qem_ctx* c, double* d_diag, double* d_scratch, double* d_log_pe, double* d_w,
+                         double* d_m1, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "global IW: two-level family only");
+  if (c->g_begin != 0 || c->g_end != c->desc.n) return fail(QEM_UNSUPPORTED, "global IW: world == 1 only");
+  if (!d_diag || !d_scratch || !d_log_pe || !d_w) return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_global_iw(c, d_diag, d_scratch, d_log_pe, d_w, d_m1, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_global_iw");
+}
+
 qem_status qem_logmeanexp(int64_t n, const double* d_x, double* d_out, void* stream) {
   if (n < 1 || !d_x || !d_out) return fail(QEM_INVALID_ARGUMENT, "need n >= 1 and arrays");
   const cudaError_t e = qem::launch_logmeanexp(n, d_x, d_out, (cudaStream_t)stream);

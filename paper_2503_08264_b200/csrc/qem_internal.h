@@ -157,6 +157,8 @@ cudaError_t launch_cat_moments(int64_t n, int C, int K, int d, const double* w_r
 cudaError_t launch_resample(qem_ctx* c, int S, uint64_t seed, int32_t* idx_root, int32_t* idx, cudaStream_t st);
 cudaError_t launch_predict(qem_ctx* c, int S, const int32_t* idx, int J, const void* x, const uint8_t* y,
                            double* ll_part, double* ll_s, double* pll, cudaStream_t st);
+cudaError_t launch_global_iw(qem_ctx* c, double* diag, double* scratch, double* log_pe, double* w, double* m1,
+                             cudaStream_t st);
 cudaError_t launch_logmeanexp(int64_t n, const double* x, double* out, cudaStream_t st);
 cudaError_t launch_mstep_family(int family, int64_t n, int C, double lam, const double* m_new, double* m_ema,
                                 double* params, int32_t* status, cudaStream_t st);

@@ -197,6 +197,74 @@ __global__ void __launch_bounds__(kResWarps * 32) k_resample_groups(ResampleArgs
   draw_row(a, t, mx, s, i, lane);
 }
 
+// ---- global importance weighting (App. A, Eq. glob_iw): K joint draws with
+// every latent at the same index k (no index mixing):
+//   log r_k = f_root(k) + sum_i [B_i(k, z_i^k) + A_i(z_i^k)],  log Pe_glob = lse_k log r_k - ln K,
+// weights softmax(log r).  The per-group diagonal is t_ref_i(k) + D_k(z_i^k) (fp64), then the
+// plate-root reduction of the table engine does the rest.
+template <int D>
+__global__ void __launch_bounds__(256) k_global_diag(ResampleArgs a, double* __restrict__ diag) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.n_local * a.K) return;
+  const int64_t i = t / a.K;
+  const int k = (int)(t - i * a.K);
+  double c[D], a0, gam;
+  row_coef<D>(a, k, a.ref->k_ref, c, a0, gam);
+  const float* zi = a.z + (size_t)i * D * a.K + k;
+  double dot = 0.0, zz = 0.0;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    const double zr = zi[(size_t)r * a.K];
+    dot = fma(c[r], zr, dot);
+    zz = fma(zr, zr, zz);
+  }
+  diag[t] = a.tA[t] + a0 + fma(gam, zz, dot);
+}
+
+// group means under the global weights: m1[i][r] = sum_k w_k z_i^{r,k} (one warp per (i, r))
+__global__ void __launch_bounds__(256) k_global_m1(int64_t rows, int K, const double* __restrict__ w,
+                                                   const float* __restrict__ z, double* __restrict__ m1) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  double s = 0.0;
+  for (int k = lane; k < K; k += 32) s += w[k] * (double)z[row * K + k];
+  s = warp_sum(s);
+  if (lane == 0) m1[row] = s;
+}
+
+cudaError_t launch_global_iw(qem_ctx* c, double* diag, double* scratch, double* log_pe, double* w, double* m1,
+                             cudaStream_t st) {
+  ResampleArgs a{};
+  a.K = c->desc.K;
+  a.D = c->desc.d;
+  a.scale_kind = c->desc.scale_kind;
+  a.n_local = c->n_local;
+  a.fixed_var = c->desc.fixed_var;
+  a.z_root = c->bufs.level[0].z;
+  a.z = c->bufs.level[1].z;
+  a.tA = c->tw.tA;
+  a.ref = c->tw.ref;
+  const int64_t t = a.n_local * a.K;
+  switch (a.D) {
+#define X(v)                                                                      \
+  case v:                                                                         \
+    k_global_diag<v><<<(unsigned)((t + 255) / 256), 256, 0, st>>>(a, diag);       \
+    break;
+    X(1) X(2) X(3) X(4) X(8) X(16) X(18)
+#undef X
+    default:
+      return cudaErrorInvalidValue;
+  }
+  cudaError_t e = launch_plate_root(a.n_local, a.K, c->tw.f_root, diag, scratch, log_pe, w, st);
+  if (e != cudaSuccess) return e;
+  if (m1) {
+    const int64_t rows = a.n_local * a.D;
+    k_global_m1<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(rows, a.K, w, a.z, m1);
+  }
+  return cudaGetLastError();
+}
+
 struct PredictArgs {
   int K, D, S, J, obs_kind;
   int64_t n_local;

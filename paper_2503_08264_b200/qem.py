@@ -292,6 +292,19 @@ class QEM:
         return dg, c
 
     # ---------------------------------------------------------- readback
+    def global_iw(self, stream=None):
+        """Global importance weighting (App. A) on the bound samples after estep_forward / estep:
+        returns dict(log_pe [1], w [K], m1 [n][d], diag [n][K])."""
+        K, n, d = self.m.K, self.n_local, self.m.d
+        f64 = dict(dtype=torch.float64, device=self.device)
+        out = dict(log_pe=torch.empty(1, **f64), w=torch.empty(K, **f64), m1=torch.empty(n, d, **f64),
+                   diag=torch.empty(n, K, **f64))
+        scratch = torch.empty(n, K, **f64)
+        check(lib().qem_global_iw(self.ctx, _ptr(out["diag"]), _ptr(scratch), _ptr(out["log_pe"]), _ptr(out["w"]),
+                                  _ptr(out["m1"]), _stream(stream)), "qem_global_iw")
+        self._gscratch = scratch
+        return out
+
     def logmeanexp(self, x: torch.Tensor) -> torch.Tensor:
         return logmeanexp(x)
 

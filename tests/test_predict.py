@@ -160,3 +160,55 @@ def test_device_resample_is_deterministic_and_seeded():
     np.testing.assert_array_equal(a["idx"], b["idx"])
     assert np.any(a["idx"] != c["idx"])
     assert a["idx"].min() >= 0 and a["idx"].max() < m.K
+
+
+# ------------------------------------------------------------------ global IW (App. A)
+
+
+def test_global_iw_is_unbiased_on_the_conjugate_model():
+    """E[exp(log Pe_glob)] = p(x) (an importance-sampling estimate with joint proposals, App. A;
+    p(x) from the marginal Gaussian, closed_form.log_evidence) on config 1."""
+    m = synth.config(1, K=64)
+    data = synth.make_data(m)
+    mean, cov = closed_form.posterior(data.xg, m.prior_var, m.fixed_var, m.obs_var)
+    sd = np.sqrt(np.diag(cov)) * 1.3
+    q = [(np.array([mean[0]], np.float32), np.array([sd[0] ** 2], np.float32)),
+         (mean[1:].astype(np.float32), (sd[1:] ** 2).astype(np.float32))]
+    exact = closed_form.log_evidence(data.xg, m.prior_var, m.fixed_var, m.obs_var)
+    vals = []
+    for s in range(1500):
+        eps = [synth.eps_normal((nn * dd, m.K), 10_000 + 7 * s + lvl) for lvl, (nn, dd) in enumerate(synth.latent_shapes(m))]
+        z = [orc.sample(qm, qv, e) for (qm, qv), e in zip(q, eps)]
+        est = orc.estep(m, z, q, data)
+        vals.append(np.exp(op.global_iw(m, z, q, data, est)["log_pe"] - exact))
+    vals = np.array(vals)
+    se = vals.std() / np.sqrt(len(vals))
+    assert abs(vals.mean() - 1.0) <= 4.5 * se, (vals.mean(), se)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cid,n,K", [(1, 4, 8), (4, 200, 64), (5, 30, 256)])
+def test_device_global_iw_matches_oracle(cid, n, K):
+    import torch
+    from paper_2503_08264_b200.qem import QEM
+    m = synth.config(cid, n=n, K=K)
+    data = synth.make_data(m)
+    q = posterior_like_q(m, data, seed=2, shrink=1.5)
+    _, _, eps, z = make_case(m, q=q)
+    est = orc.estep(m, z, q, data)
+    ref = op.global_iw(m, z, q, data, est)
+    g = QEM(m)
+    g.set_data(data)
+    g.set_q(q)
+    g.sample_q(eps=eps)
+    g.estep()
+    out = g.global_iw()
+    torch.cuda.synchronize()
+    g.close()
+    # north-star tolerances: the column prep's t_ref carries fp32 softplus sums on the Bernoulli
+    # configs (R26), so the diagonal log-factors agree to ~1e-5 there, to ~1e-12 on the Gaussian ones
+    np.testing.assert_allclose(out["diag"].cpu().numpy(), ref["diag"], rtol=1e-7, atol=5e-5)
+    assert abs(float(out["log_pe"].item()) - ref["log_pe"]) <= 1e-5 * abs(ref["log_pe"])
+    np.testing.assert_allclose(out["w"].cpu().numpy(), ref["w"], atol=1e-5)
+    scale = np.maximum(np.abs(ref["m1"]), 1e-2)
+    assert np.max(np.abs(out["m1"].cpu().numpy() - ref["m1"]) / scale) <= 1e-4
