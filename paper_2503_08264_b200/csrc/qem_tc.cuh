@@ -1011,10 +1011,19 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_bwd_cols_tc(TLArgs a
     const double lse = mx + log(block_sum256(se, scr + 8));
     __syncthreads();  // every thread is done with this stage
     if (tid == 0 && j + 2 < ngroups) issue(j + 2);
-    if (act)
-      *reinterpret_cast<float4*>(a.ws.colaux + (size_t)i * 2 * K + K + c4) =
-          make_float4((float)((t[0] - lse) * kLog2eD), (float)((t[1] - lse) * kLog2eD),
-                      (float)((t[2] - lse) * kLog2eD), (float)((t[3] - lse) * kLog2eD));
+    if (act) {
+      // L*(k') into the lP slots of the column operand's extra slab (the forward's ln P is no longer
+      // needed): the backward's MMA adds it to every tile element (row slab lP switch on), so the
+      // epilogue does not
+      unsigned char* cop = reinterpret_cast<unsigned char*>(a.ws.colop) + (size_t)i * K * kTcColBytes;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 x0, x1;
+        extra_col(0.f, (float)((t[c] - lse) * kLog2eD), x0, x1);
+        *reinterpret_cast<uint32_t*>(cop + tc_col_offset(c4 + c, 54)) = x0.w;  // lP0 lP1
+        *reinterpret_cast<uint4*>(cop + tc_col_offset(c4 + c, 56)) = x1;       // lP2 1 1 1 0...
+      }
+    }
   }
 }
 
@@ -1111,7 +1120,7 @@ __device__ void bwd_bx(const TLArgs& a, int64_t i, unsigned char* bx, int atid) 
     for (int c = 0; c < 4; ++c) {
       const float rho = w4[c] > 0.f ? log2f(w4[c]) - (h4[c] - hs) * kLog2e : -1e30f;
       uint4 c0, c1;
-      extra_row(g4[c], 0.f, rho, c0, c1);
+      extra_row(g4[c], 1.f, rho, c0, c1);  // lP switch on: the column slab holds L* (k_bwd_cols_tc)
       *reinterpret_cast<uint4*>(bx + tc_rowx_offset(k4 + c, 0)) = c0;
       *reinterpret_cast<uint4*>(bx + tc_rowx_offset(k4 + c, 8)) = c1;
     }
@@ -1256,27 +1265,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
   } else {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3, cq = warp >> 2;
-    float L2c = 0.f, acc = 0.f;
+    float acc = 0.f;
     for (TileWalk tw(RB, CB); tw.T < ntiles; tw.next()) {
       const int64_t T = tw.T, j = tw.j;
       const int t = tw.t, cb = tw.cb, rb = tw.rb;
-      const int64_t i = tw.i;
-      const int col = cb * 128 + q * 32 + lane;
-      if (rb == 0) {
-        L2c = a.ws.colaux[(size_t)i * 2 * K + K + col];  // log2e log P(k'|k*) (k_bwd_cols_tc)
-        acc = 0.f;
-      }
+      if (rb == 0) acc = 0.f;
       mbar_wait(&t_full[T & 1], (uint32_t)((T >> 1) & 1));
       tc_fence_after();
       const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * 64) + ((uint32_t)(q * 32) << 16);
       float2 wp[2] = {f2(0.f), f2(0.f)};
-      const float2 l2 = f2(L2c);
       // 16-column chunks with the next chunk's TMEM load in flight (measured faster here than one
       // 64-column load: the SFU work of a chunk overlaps the next load)
       tmem_pipeline16<4>(taddr, [&](int, uint32_t(&r)[16]) {
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
-          const float2 x = add2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), l2);
+          // v = rho_k + E_k(k') + L*(k') in log2 units, all from the MMA (extra slab)
+          const float2 x = make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1]));
           const float2 e = c >= 16 - kPolyExpBwd ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           wp[(c >> 1) & 1] = add2(wp[(c >> 1) & 1], e);
         }
