@@ -310,7 +310,10 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
 // so the column loop only sees the small within-group part and alpha'_k is
 // added back to dg at the end (exact algebra).
 template <int D, int RP>
-__global__ void __launch_bounds__(256) k_forward(TLArgs a) {
+#ifndef QEM_FWD_MINB
+#define QEM_FWD_MINB 2  // register budget hint (min blocks of 256 threads); 2 measured best on config 4
+#endif
+__global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int CS = pad4(D + 3);
   constexpr int CW = D + 2;
