@@ -60,7 +60,9 @@ def pair_ceiling(d: int, tc: bool = False, mhz: float = SM_MAX_MHZ) -> dict:
     FFMA tiles (tc False): 1 exp + d+2 FP32 lane-ops per pair.
     tcgen05 tiles (tc True, d = 16): the d-term contraction runs on the tensor cores (bf16x3:
     6 bf16 products = 12 d flops/pair, ceiling from the measured bf16 peak), leaving 1 exp + 2
-    FMA-pipe lane-ops per pair (add the column constant, accumulate) for the SM.
+    FMA-pipe lane-ops per pair for the SM (the forward: subtract the running max, accumulate; the
+    backward folds its column constant into the MMA and needs only the accumulate, so this is
+    the forward's -- the dominant kernel's -- ceiling).
     Binding ceiling = the exp capacity of SFU + FMA pipe together (exp_capacity); the SFU-only
     figure (16 pairs/clk/SM) is reported beside it."""
     f = mhz * 1e6 * SMS
