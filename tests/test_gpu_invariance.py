@@ -66,3 +66,29 @@ def test_permuting_group_samples_permutes_their_weights():
     np.testing.assert_allclose(b["m1"][1], a["m1"][1], rtol=1e-5, atol=1e-6)
     for lvl in range(2):
         np.testing.assert_allclose(b["w"][lvl].reshape(-1, m.K).sum(axis=1), 1.0, atol=1e-5)
+
+
+def test_tensor_core_path_permutation_equivariance():
+    """The same on the tcgen05 path (config 5's shape, d = 16, K = 1024, 2000 groups): permuting
+    one group's K samples (all 16 dims alike) permutes its weights and leaves log Pe, the root
+    weights and the other groups unchanged up to the fp32 tile rounding."""
+    from paper_2503_08264_b200.qem import QEM
+    m = synth.config(5, n=2000, K=1024)
+    data = synth.make_data(m)
+    q = synth.random_q(m, 5, 0.3)
+    eps = [synth.eps_normal((nn * dd, m.K), 70 + lvl) for lvl, (nn, dd) in enumerate(synth.latent_shapes(m))]
+    g = QEM(m)
+    assert g.pair_path() == 1
+    g.close()
+    a = _estep(m, data, q, eps)
+    perm = np.random.default_rng(2).permutation(m.K)
+    eps2 = [eps[0], eps[1].copy()]
+    rows = slice(11 * m.d, 12 * m.d)  # group 11's 16 dims
+    eps2[1][rows] = eps[1][rows][:, perm]
+    b = _estep(m, data, q, eps2)
+    assert abs(b["log_pe"] - a["log_pe"]) <= 1e-5 * abs(a["log_pe"])
+    np.testing.assert_allclose(b["w"][0], a["w"][0], atol=1e-5)
+    np.testing.assert_allclose(b["w"][1][11], a["w"][1][11][perm], atol=1e-5)
+    others = np.ones(m.n, bool)
+    others[11] = False
+    np.testing.assert_allclose(b["w"][1][others], a["w"][1][others], atol=1e-5)
