@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
   constexpr int CW = D + 2;
   float* rows = reinterpret_cast<float*>(smem);          // [K][RS]
   float* spare = rows + (size_t)K * RS;                  // [K] (padded to even; unused)
-  double* red = reinterpret_cast<double*>(spare + ((K + 1) & ~1));  // [32][D]
-  double* mom = red + 32 * D;                            // [D]
+  double* red = reinterpret_cast<double*>(spare + ((K + 1) & ~1));  // [32][D] + [32]
   const int lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
 
   for (int64_t i = blockIdx.x; i < a.n_local; i += gridDim.x) {
@@ -477,10 +476,17 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
       for (int kk = 0; kk < 4; ++kk) row(k + kk, kSoftExpFfma && kk == 3);
     }
     for (; k < K; ++k) row(k, false);
-    // ---- weights out + moments (fp64)
-    double s1[D];
+    // ---- weights out + moments (fp64), one pass shifted by the Q mean c = m_i:
+    // S0 = sum w, S1 = sum w (z - c), S2 = sum w (z - c)^2, then E z = c S0 + S1 and
+    // sum w (z - E z)^2 = S2 - 2 (E z - c) S1 + (E z - c)^2 S0 (exact algebra; one z conversion
+    // per column and dimension instead of two, and one block reduction instead of two)
+    double s0 = 0.0, s1[D], s2[D], cq[D];
 #pragma unroll
-    for (int r = 0; r < D; ++r) s1[r] = 0.0;
+    for (int r = 0; r < D; ++r) {
+      s1[r] = 0.0;
+      s2[r] = 0.0;
+      cq[r] = (double)a.q_m[i * D + r];
+    }
     bool bad = false;
 #pragma unroll
     for (int p = 0; p < CP; ++p)
@@ -488,55 +494,42 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
       for (int h = 0; h < 2; ++h) {
         const int kc = tid + NT * (2 * p + h);
         if (kc < K) {
-          const float wv = h ? acc[p].y : acc[p].x;
-          bad |= isnan(wv);
-          a.w[(size_t)i * K + kc] = wv;
-#pragma unroll
-          for (int r = 0; r < D; ++r) s1[r] += (double)wv * (double)a.z[((size_t)i * D + r) * K + kc];
-        }
-      }
-    if (bad) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-      const double v = warp_sum(s1[r]);
-      if (lane == 0) red[wid * D + r] = v;
-    }
-    __syncthreads();
-    if (tid < D) {
-      double t = 0.0;
-      for (int w = 0; w < nw; ++w) t += red[w * D + tid];
-      mom[tid] = t;
-    }
-    __syncthreads();
-    double s2[D];
-#pragma unroll
-    for (int r = 0; r < D; ++r) s2[r] = 0.0;
-#pragma unroll
-    for (int p = 0; p < CP; ++p)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int kc = tid + NT * (2 * p + h);
-        if (kc < K) {
-          const double wv = h ? acc[p].y : acc[p].x;
+          const float wf = h ? acc[p].y : acc[p].x;
+          bad |= isnan(wf);
+          a.w[(size_t)i * K + kc] = wf;
+          const double wv = wf;
+          s0 += wv;
 #pragma unroll
           for (int r = 0; r < D; ++r) {
-            const double dz = (double)a.z[((size_t)i * D + r) * K + kc] - mom[r];
-            s2[r] += wv * dz * dz;
+            const double e = (double)a.z[((size_t)i * D + r) * K + kc] - cq[r];
+            const double we = wv * e;
+            s1[r] += we;
+            s2[r] = fma(we, e, s2[r]);
           }
         }
       }
-    __syncthreads();
+    if (bad) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+    s0 = warp_sum(s0);
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-      const double v = warp_sum(s2[r]);
-      if (lane == 0) red[wid * D + r] = v;
+      const double v1 = warp_sum(s1[r]), v2 = warp_sum(s2[r]);
+      if (lane == 0) {
+        red[wid * D + r] = v1;
+        red[(nw + wid) * D + r] = v2;
+      }
     }
+    if (lane == 0) red[32 * D + wid] = s0;  // red: [32 D] (S1, S2: 2 nw D <= 32 D, nw <= 16) + [32] (S0)
     __syncthreads();
     if (tid < D) {
-      double t = 0.0;
-      for (int w = 0; w < nw; ++w) t += red[w * D + tid];
-      a.m1[i * D + tid] = mom[tid];
-      a.v[i * D + tid] = t;
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+      for (int w = 0; w < nw; ++w) {
+        t0 += red[32 * D + w];
+        t1 += red[w * D + tid];
+        t2 += red[(nw + w) * D + tid];
+      }
+      const double m1 = cq[tid] * t0 + t1, dm = m1 - cq[tid];
+      a.m1[i * D + tid] = m1;
+      a.v[i * D + tid] = t2 - 2.0 * dm * t1 + dm * dm * t0;
     }
   }
 }
@@ -614,7 +607,7 @@ static int pick_rp(int K, int D) {
 template <int D>
 static size_t bwd_smem(int K) {
   constexpr int RS = pad4(D + 3);
-  size_t sm = (size_t)K * RS * sizeof(float) + (size_t)((K + 1) & ~1) * sizeof(float) + (32 * D + D) * sizeof(double);
+  size_t sm = (size_t)K * RS * sizeof(float) + (size_t)((K + 1) & ~1) * sizeof(float) + (32 * D + 32) * sizeof(double);
   return (sm + 15) & ~(size_t)15;
 }
 
