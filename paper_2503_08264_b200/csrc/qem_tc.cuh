@@ -617,8 +617,14 @@ struct TileWalk {
 };
 
 // ------------------------------------------------------------------ forward
+#ifndef QEM_FWD_SA
+#define QEM_FWD_SA 3
+#endif
+#ifndef QEM_FWD_FS
+#define QEM_FWD_FS 8
+#endif
 struct FwdTcL {
-  static constexpr int SA = 3;                                       // row-block stages
+  static constexpr int SA = QEM_FWD_SA;                              // row-block stages
   static constexpr uint32_t A_C = 128 * kTcRowCBytes;                // 12 KB
   static constexpr uint32_t A_STAGE = A_C + 128 * kTcRowXBytes;      // 16 KB
   static constexpr uint32_t B_STAGE = 256 * kTcColBytes;             // 32 KB
@@ -626,7 +632,7 @@ struct FwdTcL {
   static constexpr size_t a() { return 0; }
   static constexpr size_t b() { return a() + SA * A_STAGE; }
   static constexpr size_t p() { return b() + 2 * B_STAGE; }
-  static constexpr int FS = 8;                                        // row-block hand-over stages
+  static constexpr int FS = QEM_FWD_FS;                               // row-block hand-over stages
   static constexpr size_t fin() { return p() + 2 * P_STAGE; }         // [FS][4][128] float2
   static constexpr size_t bars() { return fin() + FS * 4 * 128 * 8; }  // 2*SA + 8 + 2*FS mbarriers
   static constexpr int NBARS = 2 * SA + 8 + 2 * FS;
