@@ -9,8 +9,8 @@
 // ONE accumulation into TMEM (kind::f16, fp32 accumulate):
 //   6 MMAs  c2 . u       both operands split into three bf16 terms, the six
 //                        leading partial products small-first (tools/tc_probe.cu)
-//   1 MMA   the "extra" K-slab: row entries [g0 g0 g1 g0 g2 g1 | 1 1 1 | rho0 rho1 rho2]
-//                        x column entries  [U0 U1 U0 U2 U0 U1 | lP0 lP1 lP2 | 1 1 1]
+//   1 MMA   the "extra" K-slab: row entries [g0 g0 g1 g0 g2 g1 rho0 rho1 | rho2 1 1 1 0 0 0 0]
+//                        x column entries  [U0 U1 U0 U2 U0 U1 1 1       | 1 lP0 lP1 lP2 0 0 0 0]
 //           (U = |u|^2 and lP split in three bf16; rho = backward row constant)
 // so the epilogue per pair is one tcgen05.ld'd value -> ex2 -> add: the SFU
 // (MUFU.EX2, 16/clk/SM) and the TMEM read port (64 B/clk/SM) are the ceilings.
@@ -56,8 +56,10 @@ __device__ __forceinline__ void extra_row(float g2, float lp_on, float rho, uint
   split3_bf16(g2, g);
   split3_bf16(rho, r);
   const __nv_bfloat16 z = __float2bfloat16_rn(0.f), on = __float2bfloat16_rn(lp_on);
-  const __nv_bfloat16 a[8] = {g[0], g[0], g[1], g[0], g[2], g[1], on, on};
-  const __nv_bfloat16 b[8] = {on, r[0], r[1], r[2], z, z, z, z};
+  // chunk 6: the six gamma split terms + rho0 rho1; chunk 7: rho2 + the lP switch (x3) -- the
+  // column side keeps every lP entry in chunk 7, so patching lP rewrites one whole 16-byte chunk
+  const __nv_bfloat16 a[8] = {g[0], g[0], g[1], g[0], g[2], g[1], r[0], r[1]};
+  const __nv_bfloat16 b[8] = {r[2], on, on, on, z, z, z, z};
   c0 = pack8_bf16(a);
   c1 = pack8_bf16(b);
 }
@@ -66,8 +68,8 @@ __device__ __forceinline__ void extra_col(float U, float lp, uint4& c0, uint4& c
   split3_bf16(U, u);
   split3_bf16(lp, l);
   const __nv_bfloat16 z = __float2bfloat16_rn(0.f), one = __float2bfloat16_rn(1.f);
-  const __nv_bfloat16 a[8] = {u[0], u[1], u[0], u[2], u[0], u[1], l[0], l[1]};
-  const __nv_bfloat16 b[8] = {l[2], one, one, one, z, z, z, z};
+  const __nv_bfloat16 a[8] = {u[0], u[1], u[0], u[2], u[0], u[1], one, one};
+  const __nv_bfloat16 b[8] = {one, l[0], l[1], l[2], z, z, z, z};
   c0 = pack8_bf16(a);
   c1 = pack8_bf16(b);
 }
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 1 * 16 + 8 * h)) = pack8_bf16(s1);
         *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 2 * 16 + 8 * h)) = pack8_bf16(s2);
       }
-      {  // extra slab, first half: [S pattern | lP0 lP1 (patched below)]
+      {  // extra slab, first chunk: [S pattern | 1 1]; the second (1, lP) is written below
         uint4 c0, c1;
         extra_col(fmaf(2.f, mw, W2), 0.f, c0, c1);
         *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 48)) = c0;
@@ -491,8 +493,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         uint4 c0, c1;
         // ln P joins the MMA only in the online mode; the polynomial modes need D' alone
         extra_col(0.f, md == 5 ? lp * kLog2e : 0.f, c0, c1);
-        *reinterpret_cast<uint32_t*>(cop + tc_col_offset(kc, 54)) = c0.w;  // lP0 lP1
-        *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 56)) = c1;
+        *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 56)) = c1;  // chunk 7: 1 lP0 lP1 lP2 0...
       }
     }
     if (lane == 0) {
@@ -1026,8 +1027,7 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_bwd_cols_tc(TLArgs a
       for (int c = 0; c < 4; ++c) {
         uint4 x0, x1;
         extra_col(0.f, (float)((t[c] - lse) * kLog2eD), x0, x1);
-        *reinterpret_cast<uint32_t*>(cop + tc_col_offset(c4 + c, 54)) = x0.w;  // lP0 lP1
-        *reinterpret_cast<uint4*>(cop + tc_col_offset(c4 + c, 56)) = x1;       // lP2 1 1 1 0...
+        *reinterpret_cast<uint4*>(cop + tc_col_offset(c4 + c, 56)) = x1;  // chunk 7: 1 L*0 L*1 L*2 0...
       }
     }
   }
