@@ -15,13 +15,32 @@
  *   Eq. 9     (Sec. 4)    EMA over mean parameters
  *   PAPER.md:393-394 (Limitations)          elimination over the plate tree,
  *                                           grouping, chunking
- * Readings of ambiguous points (R1..R22) are listed in DESIGN.md.
+ * Readings of ambiguous points (R1..R33) are listed in DESIGN.md.
+ *
+ * ENTRY POINTS
+ *  - the hot path (context-based, two- and three-level Gaussian models):
+ *    qem_model_validate, qem_shard_range, qem_create / qem_workspace_bytes + qem_create_in,
+ *    qem_bind, qem_sample_q, qem_estep (= qem_estep_forward + [all-reduce of
+ *    qem_reduce_buffer] + qem_estep_backward), qem_mstep, qem_iterate (CUDA graph),
+ *    qem_read_flags, diagnostics (qem_read_mode_hist, qem_set_kernel_events,
+ *    qem_copy_messages, qem_kernel_launches, qem_pair_path);
+ *  - NEXT rows: qem_estep_evidence / qem_evidence_root (fresh-sample
+ *    denominator), qem_mstep_family (Gamma, Beta, Dirichlet, Bernoulli, Binomial,
+ *    Multinomial, Categorical M-steps), qem_estep_tables (the E-step on explicit log-factor
+ *    tables), discrete latents (qem_sample_categorical, qem_estep_categorical,
+ *    qem_tables_categorical, qem_moments_categorical, qem_mstep_categorical,
+ *    qem_loglik_bernoulli_states, qem_sample_normal), Gamma / Beta Q (qem_sample_gamma,
+ *    qem_tables_gamma_poisson, qem_moments_gamma, qem_sample_beta, qem_tables_beta_binomial,
+ *    qem_moments_beta), crossed effects (qem_tables_crossed, qem_moments_gaussian), the
+ *    predictive log-likelihood (qem_backward_resample, qem_predictive_loglik,
+ *    qem_logmeanexp) and the global-IW baseline (qem_global_iw).
  *
  * CONVENTIONS (all entry points)
  *  - Plain C types only.  Pointers named d_* are DEVICE pointers owned by the
  *    caller (e.g. torch tensors); h_* are host pointers.  The library never
  *    frees caller memory; it performs no cudaMalloc except inside
- *    qem_create (its own small device workspace, freed by qem_destroy).
+ *    qem_create (its own device workspace, freed by qem_destroy; qem_create_in
+ *    takes a caller-owned workspace instead).
  *  - `stream` is a cudaStream_t passed as void*; NULL = legacy default stream.
  *    All device work is stream-ordered; no call synchronises the host except
  *    qem_read_flags and the h_* readbacks documented below.
