@@ -547,11 +547,16 @@ __device__ __forceinline__ float2 expm1_2_poly(float2 x) {
 __device__ __forceinline__ void fwd_epi_online(uint32_t taddr, float& m, float& s) {
   uint32_t r[4][16];
   tmem_ld64(taddr, r);  // the thread's 64 columns of this tile, one TMEM round trip
-  float mx = m;
+  // four independent FMNMX3 chains (one per 16-column load), then combined: a dependency chain
+  // of 8 + 2 instead of 32
+  float mq[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < 4; ++q) {
+    mq[q] = fmaxf(__uint_as_float(r[q][0]), __uint_as_float(r[q][1]));
 #pragma unroll
-    for (int c = 0; c < 16; c += 2) mx = fmax3f(mx, __uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1]));
+    for (int c = 2; c < 16; c += 2) mq[q] = fmax3f(mq[q], __uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1]));
+  }
+  const float mx = fmax3f(m, fmax3f(mq[0], mq[1], mq[2]), mq[3]);
   if (mx > m) {  // exact running max (see kLazy in qem_forward.cuh)
     s *= ex2(m - mx);
     m = mx;
