@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     }
     tb = warp_maxf(tb);
     const int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
-    float* aux = a.ws.colaux + (size_t)i * 2 * K;  // SoA {P, ln P}
+    float* aux = a.ws.colaux + (size_t)i * 2 * K;  // P (the forward's poly modes), first K slots
     for (int kb = lane; kb < K; kb += 256) {  // 8 columns per lane per batch: their loads in flight together
       double tb4[8];
 #pragma unroll
@@ -488,8 +488,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         const int kc = kb + 32 * u;
         if (kc >= K) break;
         const float lp = (float)(tb4[u] - M - logS);
-        aux[kc] = expf(lp);
-        aux[K + kc] = lp;
+        aux[kc] = expf(lp);  // (ln P itself travels in the column operand's lP slots)
         uint4 c0, c1;
         // ln P joins the MMA only in the online mode; the polynomial modes need D' alone
         extra_col(0.f, md == 5 ? lp * kLog2e : 0.f, c0, c1);
