@@ -114,25 +114,28 @@ __global__ void k3_msub(THArgs a) {
   a.ws.Mab[ab * K * K + (int64_t)ka * K + kr] = mx + log(s) - log((double)K);
 }
 
-// T_a(kr, ka) and h_a(kr): one thread per (a, kr).
+// T_a(kr, ka) and h_a(kr): one warp per (a, kr), lanes over ka (the B sub-plate messages of a
+// column summed by its lane; max / sum by warp shuffles in a fixed order).
 __global__ void k3_top(THArgs a) {
-  const int K = a.K;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = a.K, lane = threadIdx.x & 31;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (e >= a.A * K) return;
   const int kr = e % K, aa = e / K;
   const double g = a.z_root[kr];
   double* T = a.ws.Ta + ((int64_t)aa * K + kr) * K;
   double mx = -CUDART_INF;
-  for (int ka = 0; ka < K; ++ka) {
+  for (int ka = lane; ka < K; ka += 32) {
     const double u = a.z_top[(int64_t)aa * K + ka];
     double t = lnN(u, g, a.top_var) - lnq(u, a.qt_m[aa], a.qt_v[aa]);
     for (int b = 0; b < a.B; ++b) t += a.ws.Mab[((int64_t)aa * a.B + b) * K * K + (int64_t)ka * K + kr];
     T[ka] = t;
     mx = fmax(mx, t);
   }
+  mx = warp_max(mx);
   double s = 0.0;
-  for (int ka = 0; ka < K; ++ka) s += exp(T[ka] - mx);
-  a.ws.ha[(int64_t)aa * K + kr] = mx + log(s) - log((double)K);
+  for (int ka = lane; ka < K; ka += 32) s += exp(T[ka] - mx);
+  s = warp_sum(s);
+  if (lane == 0) a.ws.ha[(int64_t)aa * K + kr] = mx + log(s) - log((double)K);
 }
 
 // Root: one block.
@@ -201,15 +204,18 @@ __global__ void k3_wtop(THArgs a) {
 
 // w_u_a(ka) = sum_kr W_a(kr,ka); w_v_ab(kab) = sum_{kr,ka} W_a(kr,ka) exp(F + L - log K - M).
 __global__ void k3_wlevels(THArgs a) {
-  const int K = a.K;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per output weight: top weights w_a(ka) = sum_kr W_a(kr, ka) (lanes over kr), sub
+  // weights w_ab(kab) = sum_{ka, kr} W_a(kr, ka) P_ab(kab | ka, kr) (lanes over ka, loop over kr)
+  const int K = a.K, lane = threadIdx.x & 31;
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t ntop = (int64_t)a.A * K;
   const int64_t nsub = (int64_t)a.A * a.B * K;
   if (e < ntop) {
     const int ka = (int)(e % K), aa = (int)(e / K);
     double s = 0.0;
-    for (int kr = 0; kr < K; ++kr) s += a.ws.Ta[((int64_t)aa * K + kr) * K + ka];
-    a.w_top[e] = (float)s;
+    for (int kr = lane; kr < K; kr += 32) s += a.ws.Ta[((int64_t)aa * K + kr) * K + ka];
+    s = warp_sum(s);
+    if (lane == 0) a.w_top[e] = (float)s;
     return;
   }
   const int64_t f = e - ntop;
@@ -221,14 +227,15 @@ __global__ void k3_wlevels(THArgs a) {
   const double lq = lnq(v, a.qs_m[ab], a.qs_v[ab]);
   const double logK = log((double)K);
   double s = 0.0;
-  for (int ka = 0; ka < K; ++ka) {
+  for (int ka = lane; ka < K; ka += 32) {
     const double F = lnN(v, (double)a.z_top[(int64_t)aa * K + ka], a.sub_var) - lq;
     for (int kr = 0; kr < K; ++kr) {
       const double W = a.ws.Ta[((int64_t)aa * K + kr) * K + ka];
       s += W * exp(F + a.ws.Lab[(ab * K + kab) * K + kr] - logK - a.ws.Mab[ab * K * K + (int64_t)ka * K + kr]);
     }
   }
-  a.w_sub[ab * K + kab] = (float)s;
+  s = warp_sum(s);
+  if (lane == 0) a.w_sub[ab * K + kab] = (float)s;
 }
 
 // Moments (E z, Var z) of the top and sub levels from their weights (fp64).
@@ -321,7 +328,7 @@ cudaError_t th_forward(qem_ctx* c, cudaStream_t st) {
   k3_root_prep<<<1, 256, 0, st>>>(a);
   k3_ltable<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
   k3_msub<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
-  k3_top<<<nblk((int64_t)a.A * a.K, 64), 64, 0, st>>>(a);
+  k3_top<<<nblk((int64_t)a.A * a.K * 32, 256), 256, 0, st>>>(a);
   c->launches += 4;
   return cudaGetLastError();
 }
@@ -333,7 +340,7 @@ cudaError_t th_backward(qem_ctx* c, cudaStream_t st) {
   if (nt < 32) nt = 32;
   k3_root<<<1, nt, (size_t)(a.K + 32) * sizeof(double), st>>>(a);
   k3_wtop<<<nblk((int64_t)a.A * KK, 128), 128, 0, st>>>(a);
-  k3_wlevels<<<nblk((int64_t)a.A * a.K + AB * a.K, 64), 64, 0, st>>>(a);
+  k3_wlevels<<<nblk(((int64_t)a.A * a.K + AB * a.K) * 32, 256), 256, 0, st>>>(a);
   k3_moments<<<nblk(a.A + AB, 64), 64, 0, st>>>(a);
   c->launches += 4;
   return cudaGetLastError();
