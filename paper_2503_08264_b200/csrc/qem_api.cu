@@ -126,6 +126,7 @@ size_t carve(qem_ctx* c, char* base) {
     c->th.f_root = reinterpret_cast<double*>(take(sizeof(double) * K));
     c->th.Lab = reinterpret_cast<double*>(take(sizeof(double) * AB * KK));
     c->th.Mab = reinterpret_cast<double*>(take(sizeof(double) * AB * KK));
+    c->th.Fab = reinterpret_cast<double*>(take(sizeof(double) * AB * KK));
     c->th.Ta = reinterpret_cast<double*>(take(sizeof(double) * A * KK));
     c->th.ha = reinterpret_cast<double*>(take(sizeof(double) * A * K));
     c->th.red = reinterpret_cast<double*>(take(sizeof(double) * (K + 1)));

@@ -53,6 +53,7 @@ struct ThreeLevelWs {
   double* f_root;  // [K]
   double* Lab;     // [AB][K kab][K kr]  Poisson table
   double* Mab;     // [AB][K ka][K kr]
+  double* Fab;     // [AB][K ka][K kab]  F_ab = lnN(v; u_a, sub_var) - log q(v)
   double* Ta;      // [A][K kr][K ka]
   double* ha;      // [A][K]
   double* red;     // [K+1]

@@ -88,6 +88,20 @@ __global__ void k3_ltable(THArgs a) {
 }
 
 // M_ab(ka, kr) = lse_kab [F_ab(ka,kab) + L_ab(kab,kr)] - log K.
+// F_ab(ka, kab) = lnN(v_ab^kab; u_a^ka, sub_var) - log q(v_ab^kab): one thread per entry (the
+// logarithms once, not once per root sample)
+__global__ void k3_ftable(THArgs a) {
+  const int K = a.K;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)a.A * a.B * K * K) return;
+  const int kab = (int)(e % K);
+  const int ka = (int)((e / K) % K);
+  const int64_t ab = e / ((int64_t)K * K);
+  const int aa = (int)(ab / a.B);
+  const double v = a.z_sub[ab * K + kab];
+  a.ws.Fab[e] = lnN(v, (double)a.z_top[(int64_t)aa * K + ka], a.sub_var) - lnq(v, a.qs_m[ab], a.qs_v[ab]);
+}
+
 __global__ void k3_msub(THArgs a) {
   const int K = a.K;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -96,21 +110,12 @@ __global__ void k3_msub(THArgs a) {
   const int kr = (int)(e % K);
   const int ka = (int)((e / K) % K);
   const int64_t ab = e / ((int64_t)K * K);
-  const int aa = (int)(ab / a.B);
-  const double u = a.z_top[(int64_t)aa * K + ka];
   const double* L = a.ws.Lab + ab * K * K;
+  const double* F = a.ws.Fab + (ab * K + ka) * K;
   double mx = -CUDART_INF;
-  for (int kab = 0; kab < K; ++kab) {
-    const double v = a.z_sub[ab * K + kab];
-    const double t = lnN(v, u, a.sub_var) - lnq(v, a.qs_m[ab], a.qs_v[ab]) + L[(int64_t)kab * K + kr];
-    mx = fmax(mx, t);
-  }
+  for (int kab = 0; kab < K; ++kab) mx = fmax(mx, F[kab] + L[(int64_t)kab * K + kr]);
   double s = 0.0;
-  for (int kab = 0; kab < K; ++kab) {
-    const double v = a.z_sub[ab * K + kab];
-    const double t = lnN(v, u, a.sub_var) - lnq(v, a.qs_m[ab], a.qs_v[ab]) + L[(int64_t)kab * K + kr];
-    s += exp(t - mx);
-  }
+  for (int kab = 0; kab < K; ++kab) s += exp(F[kab] + L[(int64_t)kab * K + kr] - mx);
   a.ws.Mab[ab * K * K + (int64_t)ka * K + kr] = mx + log(s) - log((double)K);
 }
 
@@ -327,9 +332,10 @@ cudaError_t th_forward(qem_ctx* c, cudaStream_t st) {
   const int64_t KK = (int64_t)a.K * a.K, AB = (int64_t)a.A * a.B;
   k3_root_prep<<<1, 256, 0, st>>>(a);
   k3_ltable<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
+  k3_ftable<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
   k3_msub<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
   k3_top<<<nblk((int64_t)a.A * a.K * 32, 256), 256, 0, st>>>(a);
-  c->launches += 4;
+  c->launches += 5;
   return cudaGetLastError();
 }
 
