@@ -3,10 +3,14 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
+  --gpus N > 1 without a torchrun environment re-launches itself under
+  `python -m torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL).
+
 Contract:
   * a step is one whole hot-path pass = one QEM iteration (Alg. 1):
     Philox sampler (K1) -> forward pair tiles (K2) -> [NCCL all-reduce of the
-    (K+1) fp64 plate sums when N > 1] -> root + backward weights/moments (K3, K4)
+    (K+1) fp64 plate sums when N > 1, run inside libqem: qem_estep_reduce] -> root +
+    backward weights/moments (K3, K4)
     -> EMA + M-step (K5), on BASELINE config C (default 5; config 4 with --config 4);
   * metric: E-step factor-pairs/s (N*K^2 per step over the whole iteration), plus
     QEM iterations/s; strong scaling (the config's M groups split over N ranks);
@@ -92,20 +96,12 @@ def _measured_bf16() -> float:
 BF16_TFLOPS = _measured_bf16()
 
 
-def _algo_bytes(dom: str, tc: bool, n: int, m) -> float:
-    """Bytes one launch of the dominant pair kernel must move: its per-column operand stream in
-    (TC: 128 B column operand + 4 B P or log P(k'|k*); FFMA: the pad4(d+3) fp32 column record) and its
-    per-(group, sample) outputs (forward: dg + h, 8 B; backward: w, 4 B)."""
-    col = (128 + 4) if tc else 4 * ((m.d + 3 + 3) // 4 * 4)
-    out = 8 if dom == "forward" else 4
-    return float(n) * m.K * (col + out)
-
-
-def _ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (tools/ncu_traffic.py)."""
+def _ncu_traffic(kernel: str, cfg: int):
+    """DRAM bytes per launch of `kernel` on config `cfg` from the committed ncu --set full capture
+    (tools/ncu_traffic.py -> profiles/r02_traffic.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            return json.load(f)[kernel]["dram_bytes"]
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
+            return json.load(f)[f"config{cfg}"][kernel]["dram_bytes"]
     except Exception:
         return None
 
@@ -167,15 +163,15 @@ def dist_env():
 
 
 def oracle_sample(cfg: int, budget_s: float = 15.0, threads: int | None = None):
-    """Time the fp64 oracle E-step + EMA on a bounded sample of groups of config ``cfg``.
+    """Time the fp64 oracle E-step + EMA (as it stands) on a bounded sample of groups of config ``cfg``
+    with `threads` OpenMP threads (default: all host cores).
 
-    Returns (pairs/s, iters/s extrapolated to the full config, cores, description)."""
-    import numpy as np
+    Returns (pairs/s, iters/s extrapolated to the full config, threads, description)."""
     from oracle import oracle as orc
     from paper_2503_08264_b200 import synth
     full = synth.config(cfg)
     cores = threads or os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    orc.set_num_threads(cores)
     n = max(1, min(full.n, cores))
     spent, done_pairs, n_runs = 0.0, 0, 0
     while True:
@@ -197,39 +193,39 @@ def oracle_sample(cfg: int, budget_s: float = 15.0, threads: int | None = None):
     pairs_per_s = done_pairs / spent
     iters_per_s = pairs_per_s / full.pairs
     desc = (f"oracle fp64 E-step+EMA of config {cfg} on {n} of {full.n} groups (K={full.K}), "
-            f"{n_runs} run(s), {spent:.1f} s, OMP threads={os.environ.get('OMP_NUM_THREADS')}")
-    return pairs_per_s, iters_per_s, int(os.environ.get("OMP_NUM_THREADS", cores)), desc
+            f"{n_runs} run(s), {spent:.1f} s, OpenMP threads={orc.num_threads()}; iters/s extrapolated "
+            f"to all {full.n} groups")
+    return pairs_per_s, iters_per_s, orc.num_threads(), desc
 
 
 # ---------------------------------------------------------------- GPU bench
 
 
-def run_gpu(args):
-    import numpy as np
+def _algo_bytes_method(dom: str, n: int, m) -> float:
+    """The METHOD's bytes for one launch of the dominant pair kernel (SURVEY.md §8(d) "Bytes per
+    E-step": samples read, the unary term, messages / weights written), independent of how the
+    kernel lays out its operands: per (group, sample) the d fp32 sample coordinates + the fp32
+    unary log-term (P or ln P) in, and the pass's output out (forward: the message g; backward:
+    the weight w), 4 B each."""
+    return float(n) * m.K * (4.0 * m.d + 4.0 + 4.0)
+
+
+def measure_step(m, args, world, rank, dev, in_library, seed):
+    """Device-timed QEM iterations of model `m` (groups sharded over `world` ranks): W warm-up
+    steps, then K steps bracketed by barrier + synchronize; CUDA events on the launch stream;
+    per-kernel events around the two pair kernels (recorded by libqem); max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_2503_08264_b200 import synth
+    from paper_2503_08264_b200.dist import ShardedQEM
     from paper_2503_08264_b200.qem import QEM, shard_range
 
-    world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    m = synth.config(args.config)
     data = synth.make_data(m)
     gb, ge = shard_range(m.n, rank, world)
     g = QEM(m, group_begin=gb, group_end=ge, device=dev)
     g.set_data(data)
-    seed = 100 + args.config
     stream = torch.cuda.current_stream()
-
-    from paper_2503_08264_b200.dist import ShardedQEM
-    runner = ShardedQEM(g)
-
-    def allreduce():
-        runner.allreduce_plate_sum()
-
+    runner = ShardedQEM(g, in_library=in_library)
     launched = [0]
 
     def step(t, ev=None):
@@ -242,7 +238,7 @@ def run_gpu(args):
         launched[0] += g.kernel_launches()
         if ev:
             ev[4].record(stream)
-        allreduce()
+        runner.allreduce_plate_sum()
         if ev:
             ev[5].record(stream)
         g.estep_backward()
@@ -257,6 +253,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    local = dev.index or 0
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -275,74 +272,111 @@ def run_gpu(args):
     clk = clocks.stop()
     ms_total = start.elapsed_time(stop)
     g.set_kernel_events(None)
-    # pair-tile kernels alone (events recorded by libqem around k_forward / k_backward)
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     bwd_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
     comm_ms = sum(e[4].elapsed_time(e[5]) for e in evs) / args.steps
-    # libqem kernels launched in the timed region (qem_kernel_launches after every call)
-    n_launched = launched[0]
     flags, clamps = g.read_flags()
     if world > 1:
         tt = torch.tensor([ms_total, fwd_ms, bwd_ms, comm_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total, fwd_ms, bwd_ms, comm_ms = tt.tolist()
     ms_step = ms_total / args.steps
-    pairs_step = m.pairs  # whole job
-    value = pairs_step / (ms_step * 1e-3)
-
-    # ------------------------------------------------------------- e2e leg
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce)
     tc = g.pair_path() == 1
-    fresh = mfam = disc = pred = gam = crossed = None
-    if world == 1 and not args.no_variants:
-        g.close()  # free the first context's workspace before the variant's
-        fresh = run_fresh_variant(args, m, data, dev, seed)
-        mfam = run_mstep_family_variant(dev)
-        disc = run_discrete_variant(dev)
-        pred = run_predictive_variant(m, data, dev, seed)
-        gam = run_gamma_variant(dev)
-        crossed = run_crossed_variant(dev)
-
-    # ----------------------------------------------------------- roofline
     local_pairs = (ge - gb) * m.K * m.K
     dom, dom_ms = ("forward", fwd_ms) if fwd_ms >= bwd_ms else ("backward", bwd_ms)
+    kname = f"k_{dom}" + ("_tc" if tc else "")
     ceil = pair_ceiling(m.d, tc)
     achieved = local_pairs / (dom_ms * 1e-3)
     per_pair = ({"exp": 1, "fma_pipe": 2, "tensor_bf16_flops": 12 * m.d} if tc else {"exp": 1, "fma_pipe": m.d + 2})
-    roof = {"bound": "alu", "pipe": ceil["pipe"], "kernel": f"k_{dom}" + ("_tc" if tc else ""), "unit": "Gpair/s",
+    algo = _algo_bytes_method(dom, ge - gb, m)
+    traffic = _ncu_traffic(kname, args.config if m.config_id == args.config else m.config_id)
+    roof = {"bound": "alu", "pipe": ceil["pipe"], "kernel": kname, "unit": "Gpair/s",
             "achieved": achieved / 1e9, "peak": ceil["pairs_per_s"] / 1e9,
             "frac": achieved / ceil["pairs_per_s"],
             "frac_vs_exp_sfu_plus_fma": achieved / ceil["exp_sfu_plus_fma_pairs_per_s"],
-            "traffic": _ncu_traffic(f"k_{dom}" + ("_tc" if tc else "")),
-            "traffic_unit": "bytes/launch (ncu --set full, profiles/r01_traffic.json)",
-            "algorithmic_bytes": _algo_bytes(dom, tc, ge - gb, m),
+            "traffic": traffic,
+            "traffic_unit": "DRAM bytes/launch (ncu --set full, profiles/r02_traffic.json)",
+            "algorithmic_bytes": algo,
+            "algorithmic_bytes_basis": "SURVEY.md §8(d): per (group, sample) d fp32 coordinates + the fp32 unary "
+                                       "term in, the pass's fp32 output out",
+            "traffic_over_algorithmic": (traffic / algo) if traffic else None,
+            "achieved_gbs_algorithmic": algo / (dom_ms * 1e-3) / 1e9,
             "per_pair": per_pair,
             "ceilings_gpair_s": {k.replace("_pairs_per_s", ""): v / 1e9 for k, v in ceil.items()
                                  if k.endswith("_pairs_per_s") and k != "pairs_per_s"},
             "peak_basis": (f"{SMS} SMs x {SM_MAX_MHZ:.0f} MHz x min({SFU_PER_SM_CLK:.0f} MUFU.EX2/clk per exp, "
                            f"{FP32_PER_SM_CLK:.0f} FP32 lane-ops/clk / {per_pair['fma_pipe']} per pair) = the north-star "
-                           f"roofline (slower of SFU and FP32 ops at peak); frac_vs_exp_sfu_plus_fma is against the "
-                           f"stricter ceiling that also counts exps evaluated in software on the FMA pipe "
-                           f"({FMA_PER_SOFT_EXP:.0f} lane-ops each) (DESIGN.md Roofline)"),
+                           f"roofline (slower of SFU and FP32 ops at peak, guide peak rates); "
+                           f"frac_vs_exp_sfu_plus_fma is against the stricter ceiling that also counts exps "
+                           f"evaluated in software on the FMA pipe ({FMA_PER_SOFT_EXP:.0f} lane-ops each)"),
             "kernels_ms": {"forward": fwd_ms, "backward": bwd_ms, "allreduce": comm_ms}}
+    out = dict(g=g, data=data, gb=gb, ge=ge, ms_step=ms_step, value=m.pairs / (ms_step * 1e-3),
+               launched=launched[0], flags=flags, clamps=clamps, clocks=clk, roofline=roof, tc=tc, t=t,
+               allreduce=runner.allreduce_plate_sum, nccl=g.nccl_info() if in_library else None)
+    return out
+
+
+def _summary(meas, m):
+    """The JSON-able part of a measure_step result."""
+    return {"workload": f"config{m.config_id}:{m.name}", "M_groups": m.n, "K": m.K, "d": m.d, "J": m.J,
+            "pairs_per_step": m.pairs, "ms_per_step": meas["ms_step"], "value": meas["value"],
+            "unit": "factor-pairs/s", "qem_iters_per_s": 1e3 / meas["ms_step"], "roofline": meas["roofline"],
+            "gpu_launches": meas["launched"], "flags": {"device_flags": meas["flags"], "var_clamps": meas["clamps"]},
+            "clocks": meas["clocks"]}
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2503_08264_b200 import synth
+
+    world, rank, local = dist_env()
+    if world > 1 and torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    m = synth.config(args.config)
+    seed = 100 + args.config
+    main_m = measure_step(m, args, world, rank, dev, in_library=world > 1, seed=seed)
+    g = main_m["g"]
+
+    # ------------------------------------------------------------- e2e leg
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, g, m, main_m["data"], world, rank, dev, seed, main_m["t"], main_m["allreduce"])
+    nccl = main_m["nccl"]
+    g.close()
+    variants = {}
+    if not args.no_variants:
+        # config 4 (the other gated config, SURVEY.md §8(d)) at the same world size, sharded the same way
+        other = 4 if args.config == 5 else (5 if args.config == 4 else None)
+        if other is not None:
+            mo = synth.config(other)
+            meas = measure_step(mo, args, world, rank, dev, in_library=world > 1, seed=100 + other)
+            meas["g"].close()
+            variants[f"config{other}"] = _summary(meas, mo)
+        if world == 1:
+            variants["converged_regime"] = run_converged_variant(args, dev)
+            variants["iterate_graph"] = run_iterate_variant(dev)
+            variants["fresh_denominator"] = run_fresh_variant(args, m, main_m["data"], dev, seed)
+            variants["mstep_family"] = run_mstep_family_variant(dev)
+            variants["discrete_occupancy"] = run_discrete_variant(dev)
+            variants["predictive_loglik"] = run_predictive_variant(m, main_m["data"], dev, seed)
+            variants["gamma_poisson"] = run_gamma_variant(dev)
+            variants["crossed_bus"] = run_crossed_variant(dev)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     cpu = None
     if world == 1 and not args.no_cpu:
-        try:
-            pps, ips, cores, desc = oracle_sample(args.config, budget_s=args.cpu_budget)
-            cpu = {"value": pps, "unit": "factor-pairs/s", "cores": cores, "kind": "oracle", "sample": desc,
-                   "qem_iters_per_s": ips}
-        except Exception as exc:  # the baseline must not sink the bench line
-            cpu = {"value": None, "unit": "factor-pairs/s", "cores": os.cpu_count(), "kind": "oracle",
-                   "sample": f"failed: {exc}"}
+        cpu = cpu_baseline(args.config, args.cpu_budget)
+    ms_step = main_m["ms_step"]
     line = {
         "metric": "E-step factor-pairs/sec (N*K^2) and QEM iters/sec",
-        "value": value,
+        "value": main_m["value"],
         "unit": "factor-pairs/s",
         "n_gpus": world,
         "steps": args.steps,
@@ -351,25 +385,47 @@ def run_gpu(args):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32 pair tiles, f64 unary/plate sums",
+        "dtype": DTYPE_TC if main_m["tc"] else DTYPE_FFMA,
         "data": "synthetic (ancestral draw from the config's prior, numpy PCG64 seed = config id)",
         "qem_iters_per_s": 1e3 / ms_step,
         "config": {"workload": f"config{args.config}:{m.name}", "M_groups": m.n, "K": m.K, "d": m.d,
-                   "J": m.J, "pairs_per_step": pairs_step, "parallelism": f"groups sharded over {world} rank(s)",
+                   "J": m.J, "pairs_per_step": m.pairs, "parallelism": f"groups sharded over {world} rank(s)",
+                   "allreduce": ("in-library ncclAllReduce of K+1 fp64 (qem_estep_reduce)" if world > 1 else "none (1 rank)"),
+                   "nccl": ({"rank": nccl[0], "nranks": nccl[1], "version": nccl[2]} if nccl else None),
                    "l2": "inputs larger than L2 (samples + per-group messages > 126 MB)",
-                   "sampler": "device Philox4x32-10"},
-        "roofline": roof,
+                   "sampler": "device Philox4x32-10",
+                   "regime": "early run from Q = N(0,1): timed from iteration W+1 (converged regime in variants)"},
+        "roofline": main_m["roofline"],
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": n_launched,
-        "clocks": clk,
-        "flags": {"device_flags": flags, "var_clamps": clamps},
-        "variants": {"fresh_denominator": fresh, "mstep_family": mfam, "discrete_occupancy": disc,
-                     "predictive_loglik": pred, "gamma_poisson": gam, "crossed_bus": crossed},
+        "gpu_launches": main_m["launched"],
+        "clocks": main_m["clocks"],
+        "flags": {"device_flags": main_m["flags"], "var_clamps": main_m["clamps"]},
+        "variants": variants,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+DTYPE_TC = ("f32 (config-5 log-factor contraction: bf16x3 split on tcgen05, fp32 TMEM accumulation; "
+            "exp fp32: SFU ex2.approx + 2/16 fwd, 4/16 bwd degree-5 polynomial; f64 unary terms, plate sums, moments)")
+DTYPE_FFMA = "f32 pair tiles (FFMA + SFU ex2.approx), f64 unary terms, plate sums, moments"
+
+
+def cpu_baseline(cfg, budget):
+    """The fp64 oracle as it stands, on a bounded sample of the workload, at all host cores and at 1 thread."""
+    try:
+        cores = os.cpu_count() or 1
+        pps, ips, used, desc = oracle_sample(cfg, budget_s=budget, threads=cores)
+        out = {"value": pps, "unit": "factor-pairs/s", "cores": used, "kind": "oracle", "sample": desc,
+               "qem_iters_per_s": ips}
+        p1, i1, _, d1 = oracle_sample(cfg, budget_s=max(4.0, budget / 3), threads=1)
+        out["one_thread"] = {"value": p1, "unit": "factor-pairs/s", "cores": 1, "sample": d1, "qem_iters_per_s": i1}
+        return out
+    except Exception as exc:  # the baseline must not sink the bench line
+        return {"value": None, "unit": "factor-pairs/s", "cores": os.cpu_count(), "kind": "oracle",
+                "sample": f"failed: {exc}"}
 
 
 def run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce):
@@ -649,15 +705,49 @@ def run_mstep_family_variant(dev, n=1_000_000, reps=10):
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
+    """--impl reference: the CPU oracle (this tier's reference arm) as it stands, rank 0 only.
+
+    Each step is one oracle QEM iteration (E-step + EMA + M-step, Alg. 1) on a bounded sample of
+    n_s groups of the workload, n_s sized from a probe so the W + K steps end within ~budget
+    seconds; W untimed, K timed (wall clock, host)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    budget = max(5.0, min(60.0, args.cpu_budget))
-    pps, ips, cores, desc = oracle_sample(args.config, budget_s=budget)
-    ms_step = 1e3 / ips
+    from oracle import oracle as orc
     from paper_2503_08264_b200 import synth
-    m = synth.config(args.config)
+    full = synth.config(args.config)
+    cores = os.cpu_count() or 1
+    orc.set_num_threads(cores)
+    budget = max(10.0, min(120.0, args.cpu_budget * 4))
+    # probe: one step on `cores` groups sizes the per-step sample
+    n_s = max(1, min(full.n, cores))
+    m = synth.config(args.config, n=n_s)
+    data, seed = synth.make_data(m), 100 + args.config
+    state = orc.initial_state(m)
+    q = [orc.mstep(a, b)[:2] for a, b in state]
+    t0 = time.perf_counter()
+    orc.qem_step(m, state, q, orc.eps_for_iteration(m, 1, seed), 1, data=data)
+    probe = time.perf_counter() - t0
+    per_step = budget / (args.steps + args.warmup)
+    n_s = int(max(1, min(full.n, n_s * per_step / max(probe, 1e-4))))
+    m = synth.config(args.config, n=n_s)
+    data = synth.make_data(m)
+    state = orc.initial_state(m)
+    q = [orc.mstep(a, b)[:2] for a, b in state]
+    times = []
+    for t in range(1, args.warmup + args.steps + 1):
+        eps = orc.eps_for_iteration(m, t, seed)
+        t0 = time.perf_counter()
+        r = orc.qem_step(m, state, q, eps, t, data=data)
+        dt = time.perf_counter() - t0
+        state, q = r["state"], r["q_next"]
+        if t > args.warmup:
+            times.append(dt)
+    ms_step = 1e3 * sum(times) / len(times)
+    pps = m.pairs / (ms_step * 1e-3)
+    desc = (f"oracle fp64 QEM iterations (E-step + EMA + M-step) of config {args.config} on a sample of {n_s} of "
+            f"{full.n} groups (K={full.K}), {args.warmup} warm-up + {args.steps} timed steps, OpenMP threads="
+            f"{orc.num_threads()}")
     line = {
         "impl": "reference",
         "metric": "E-step factor-pairs/sec (N*K^2) and QEM iters/sec",
@@ -667,18 +757,142 @@ def run_reference(args):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_step,
+        "ms_per_step_basis": f"one step = the sampled {n_s}-group iteration (measured, not extrapolated)",
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (ancestral draw from the config's prior, numpy PCG64 seed = config id)",
-        "qem_iters_per_s": ips,
-        "config": {"workload": f"config{args.config}:{m.name}", "M_groups": m.n, "K": m.K, "d": m.d, "J": m.J,
-                   "pairs_per_step": m.pairs, "parallelism": "CPU oracle, OpenMP over groups"},
-        "cpu_baseline": {"value": pps, "unit": "factor-pairs/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "qem_iters_per_s_full_workload_extrapolated": pps / full.pairs,
+        "config": {"workload": f"config{args.config}:{full.name}", "M_groups": full.n, "K": full.K, "d": full.d,
+                   "J": full.J, "pairs_per_step": full.pairs, "sample_groups_per_step": n_s,
+                   "sample_pairs_per_step": m.pairs, "parallelism": "CPU oracle, OpenMP over groups"},
+        "cpu_baseline": {"value": pps, "unit": "factor-pairs/s", "cores": orc.num_threads(), "kind": "oracle",
+                         "sample": desc},
         "e2e": {"value": pps, "unit": "factor-pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_converged_variant(args, dev, steps=5):
+    """Converged-regime timing (the expm1-polynomial forward tile modes, DESIGN.md "Forward
+    numerics"): configs 4 and 5 with Q near the posterior (synth.posterior_like_q); every timed step
+    restarts from that Q (a device copy) so the regime holds, then sample -> E-step -> M-step.
+    Reports the forward mode histogram and the forward's rate against the FMA-pipe roofline of
+    the modes it ran (per pair: the d-term (FFMA) or tcgen05 contraction, the degree-n Horner
+    expm1, the P-weighted accumulate; online-lse mode: one exp on the SFU)."""
+    import torch
+    from paper_2503_08264_b200 import synth
+    from paper_2503_08264_b200.qem import QEM
+    out = {}
+    degs = [3, 4, 5, 7, 9]
+    for cid in (4, 5):
+        m = synth.config(cid)
+        data = synth.make_data(m)
+        g = QEM(m, device=dev)
+        g.set_data(data)
+        g.set_q(synth.posterior_like_q(m, data, seed=5, shrink=1.0))
+        q0 = [(lv["q_mean"].clone(), lv["q_var"].clone()) for lv in g.levels]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+        def one(t):
+            for lv, (qm, qv) in zip(g.levels, q0):
+                lv["q_mean"].copy_(qm)
+                lv["q_var"].copy_(qv)
+            g.sample_q(seed=100 + cid, iter=t)
+            g.estep()
+            g.mstep(t)
+
+        for t in range(1, 4):
+            one(t)
+        torch.cuda.synchronize()
+        g.mode_hist()
+        fwd = 0.0
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for t in range(4, 4 + steps):
+            g.set_kernel_events(ev)
+            one(t)
+            torch.cuda.synchronize()
+            fwd += ev[0].elapsed_time(ev[1])
+        en.record()
+        torch.cuda.synchronize()
+        g.set_kernel_events(None)
+        hist = g.mode_hist()
+        fwd /= steps
+        # step time without the per-step syncs: a second pass, device-timed back to back
+        st.record()
+        for t in range(4 + steps, 4 + 2 * steps):
+            one(t)
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / steps
+        tot = max(1, sum(hist))
+        tc = g.pair_path() == 1
+        base = 2.0 if tc else m.d + 2.0   # the log-factor (FFMA path) or the TMEM value (TC) per pair
+        # clocks per pair per SM from the mode mix: poly mode n: (base + n + 2) FMA lane-ops / 128;
+        # online mode: 1 exp / 16 (SFU) vs base + 2 FMA lane-ops
+        cyc = 0.0
+        for md, c in enumerate(hist):
+            frac = c / tot
+            if md < 5:
+                cyc += frac * (base + degs[md] + 2.0) / FP32_PER_SM_CLK
+            else:
+                cyc += frac * max(1.0 / SFU_PER_SM_CLK, (base + 2.0) / FP32_PER_SM_CLK)
+        ceiling = SMS * SM_MAX_MHZ * 1e6 / cyc
+        achieved = m.pairs / (fwd * 1e-3)
+        out[f"config{cid}"] = {"ms_per_step": ms, "qem_iters_per_s": 1e3 / ms, "value": m.pairs / (ms * 1e-3),
+                               "unit": "factor-pairs/s", "forward_ms": fwd,
+                               "forward_mode_hist": {"expm1_deg3": hist[0], "deg4": hist[1], "deg5": hist[2],
+                                                     "deg7": hist[3], "deg9": hist[4], "online_lse": hist[5]},
+                               "forward_roofline": {"bound": "alu", "pipe": "fma (mode mix)",
+                                                    "achieved": achieved / 1e9, "peak": ceiling / 1e9,
+                                                    "unit": "Gpair/s", "frac": achieved / ceiling}}
+        g.close()
+    return out
+
+
+def run_iterate_variant(dev):
+    """QEM iterations/s of every config through qem_iterate's captured CUDA graph (the library's own
+    loop: Philox sampler -> E-step -> EMA/M-step), device-timed after 5 warm-up iterations."""
+    import torch
+    from paper_2503_08264_b200 import synth
+    from paper_2503_08264_b200.qem import QEM
+    out = {}
+    for cid in (1, 2, 3, 4, 5):
+        m = synth.config(cid)
+        T = 200 if cid <= 3 else 10
+        g = QEM(m, device=dev, trace_len=T)
+        g.set_data(synth.make_data(m))
+        g.set_q(synth.initial_q(m))
+        g.iterate(1, 5, seed=100 + cid, use_graph=True)
+        torch.cuda.synchronize()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        g.iterate(6, T, seed=100 + cid, use_graph=True)
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / T
+        out[f"config{cid}"] = {"us_per_iteration": ms * 1e3, "qem_iters_per_s": 1e3 / ms,
+                               "factor_pairs_per_s": m.pairs / (ms * 1e-3), "iterations": f"6..{5 + T}",
+                               "kernels_per_iteration": g.kernel_launches() // T}
+        g.close()
+    return out
+
+
+def _relaunch_torchrun(n: int) -> int:
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run, one rank per GPU."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init log (nranks, transport) stays on
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -695,6 +909,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_relaunch_torchrun(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -20,8 +20,9 @@
  * ENTRY POINTS
  *  - the hot path (context-based, two- and three-level Gaussian models):
  *    qem_model_validate, qem_shard_range, qem_create / qem_workspace_bytes + qem_create_in,
- *    qem_bind, qem_sample_q, qem_estep (= qem_estep_forward + [all-reduce of
- *    qem_reduce_buffer] + qem_estep_backward), qem_mstep, qem_iterate (CUDA graph),
+ *    qem_bind, qem_sample_q, qem_estep (= qem_estep_forward + qem_estep_reduce (the NCCL
+ *    all-reduce of qem_reduce_buffer) + qem_estep_backward), qem_mstep, qem_iterate (CUDA graph),
+ *    the communicator (qem_nccl_unique_id, qem_nccl_init, qem_set_nccl_comm, qem_nccl_info),
  *    qem_read_flags, diagnostics (qem_read_mode_hist, qem_set_kernel_events,
  *    qem_copy_messages, qem_kernel_launches, qem_pair_path);
  *  - NEXT rows: qem_estep_evidence / qem_evidence_root (fresh-sample
@@ -84,6 +85,7 @@ typedef int32_t qem_status;
 #define QEM_INVALID_MODEL 2    /* model description fails validation */
 #define QEM_UNSUPPORTED 3      /* valid but not implemented (e.g. world>1 on three-level) */
 #define QEM_CUDA_ERROR 4       /* a CUDA call failed; see qem_last_error() */
+#define QEM_NCCL_ERROR 5       /* an NCCL call failed or NCCL cannot be loaded; see qem_last_error() */
 
 #define QEM_FAMILY_TWO_LEVEL 2
 #define QEM_FAMILY_THREE_LEVEL 3
@@ -221,17 +223,52 @@ qem_status qem_bind(qem_ctx* ctx, const qem_buffers* bufs);
 qem_status qem_sample_q(qem_ctx* ctx, uint64_t seed, int32_t iter, const float* const* d_eps,
                         void* stream);
 
+/* ---- Group sharding over ranks (PAPER.md:393-394 plate-wise elimination) ----
+   One process per GPU; rank r's context owns groups qem_shard_range(n, r, world).  The only
+   exchange of a QEM iteration is a SUM all-reduce of the (K+1) fp64 plate sums
+   [G_r(0..K-1), sum_i c_i] the local forward leaves in the reduce buffer (qem_reduce_buffer):
+   log-sum-exp-safe because the plate product is a plain sum of centred log-messages (Eq. 7c,
+   PAPER.md:148), so nothing is exponentiated before the reduction.  Every rank then computes the
+   root weights redundantly from the identical reduced bytes (root samples come from Philox keyed
+   by global indices: no broadcast).  The library runs that all-reduce itself (ncclAllReduce,
+   fp64 SUM, in place, on the call's stream, so qem_iterate captures it in its CUDA graph) once a
+   communicator is attached.  NCCL is loaded at run time (the process's libnccl.so.2, e.g. torch's,
+   else QEM_NCCL_LIB); processes that attach none never load it.  Two-level family only
+   (QEM_UNSUPPORTED for three-level contexts, which run as replicas).
+
+   qem_nccl_unique_id: writes a fresh ncclUniqueId (QEM_NCCL_ID_BYTES bytes) to h_id (host); rank 0
+     calls it and the caller distributes the bytes (e.g. over torch.distributed).
+   qem_nccl_init: COLLECTIVE over the `world` ranks: ncclCommInitRank(world, id, rank) plus one
+     warm-up all-reduce (NCCL connects on its first collective, which must not be captured).  The
+     context owns the communicator (destroyed by qem_destroy or a later attach).  Errors:
+     QEM_INVALID_ARGUMENT if qem_shard_range(n, rank, world) is not the context's group block;
+     QEM_NCCL_ERROR if NCCL fails or cannot be loaded.
+   qem_set_nccl_comm: attach a caller-owned ncclComm_t (passed as void*; NULL detaches); its
+     (ncclCommUserRank, ncclCommCount) must own the context's group block (else
+     QEM_INVALID_ARGUMENT).  Attaching invalidates a captured qem_iterate graph.
+   qem_nccl_info: the attached communicator's rank / world (0 / 1 without one) and NCCL version
+     (ncclGetVersion code, 0 without one); any output pointer may be NULL.
+   qem_estep_reduce: the all-reduce between qem_estep_forward and qem_estep_backward (a no-op on an
+     unsharded context without a communicator; QEM_UNSUPPORTED on a sharded one without). */
+#define QEM_NCCL_ID_BYTES 128
+qem_status qem_nccl_unique_id(void* h_id);
+qem_status qem_nccl_init(qem_ctx* ctx, const void* h_id, int32_t rank, int32_t world);
+qem_status qem_set_nccl_comm(qem_ctx* ctx, void* nccl_comm);
+qem_status qem_nccl_info(const qem_ctx* ctx, int32_t* rank, int32_t* world, int32_t* version);
+
 /* K2..K4 -- one MPIW E-step on the bound samples (Eq. 7a-c):
    log Pe -> bufs.log_pe, weights -> level[*].w, moments (E z, Var z) ->
-   level[*].m1 / .v.  For world > 1 use the two phases below instead, with a
-   SUM all-reduce of the (K+1) doubles returned by qem_reduce_buffer between
-   them; qem_estep == forward + backward when world == 1. */
+   level[*].m1 / .v.  = qem_estep_forward + qem_estep_reduce + qem_estep_backward.  A sharded
+   context needs a communicator (QEM_UNSUPPORTED otherwise); callers that reduce the plate sums
+   themselves use the phases with their own all-reduce of qem_reduce_buffer in between. */
 qem_status qem_estep(qem_ctx* ctx, void* stream);
 /* Phase 1: sample prep, unary terms, pair-tile forward log-sum-exp; leaves the
    local plate sum [G(0..K-1), sum_i c_i] (fp64) in the reduce buffer. */
 qem_status qem_estep_forward(qem_ctx* ctx, void* stream);
 /* Device pointer + count of the plate-sum buffer (fp64, K+1 entries). */
 qem_status qem_reduce_buffer(qem_ctx* ctx, double** d_buf, int64_t* count);
+/* SUM all-reduce of that buffer over the attached communicator (see "Group sharding" above). */
+qem_status qem_estep_reduce(qem_ctx* ctx, void* stream);
 /* Phase 2: root softmax + log Pe (from the reduced buffer), backward weights,
    moments. */
 qem_status qem_estep_backward(qem_ctx* ctx, void* stream);
@@ -456,8 +493,10 @@ qem_status qem_mstep_family(int32_t family, int64_t n, int32_t C, double lam, co
                             double* d_m_ema, double* d_params, int32_t* d_status, void* stream);
 
 /* K6 -- T QEM iterations t = t0 .. t0+T-1 of sample (Philox, seed) ->
-   E-step -> M-step, replayed from one captured CUDA graph (world == 1), or
-   issued eagerly when `use_graph` == 0.  With opts.fresh_denominator each
+   E-step (forward, all-reduce over the attached communicator, backward) -> M-step, replayed
+   from one captured CUDA graph, or issued eagerly when `use_graph` == 0.  A sharded context
+   needs a communicator (QEM_UNSUPPORTED otherwise) and every rank calls qem_iterate with the
+   same (t0, T, seed, use_graph): each iteration is one collective.  With opts.fresh_denominator each
    iteration first samples z_new (Philox iteration word t | 2^23) and runs the
    evidence pass.  log Pe of iteration t0+j goes to
    bufs.trace[j] when bufs.trace != NULL. */
@@ -476,7 +515,8 @@ qem_status qem_read_mode_hist(qem_ctx* ctx, void* stream, uint64_t* h_hist);
 /* Optional cudaEvent_t handles (as void*, NULL = off) that the library
    records on the launch stream immediately before/after the two-level
    pair-tile kernels (forward K2b, backward K4) of every later E-step, so a
-   caller can time exactly those kernels.  The events are caller-owned. */
+   caller can time exactly those kernels.  The events are caller-owned.  A captured qem_iterate
+   graph is discarded (it recorded the previous events). */
 qem_status qem_set_kernel_events(qem_ctx* ctx, void* fwd_start, void* fwd_end, void* bwd_start, void* bwd_end);
 
 /* Number of kernels the last qem_* call launched (for the bench's

@@ -196,6 +196,11 @@ def num_threads():
     return lib().orc_num_threads()
 
 
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the group loops (timing only; results are thread-count independent)."""
+    lib().orc_set_num_threads(int(n))
+
+
 # ------------------------------------------------------------------ QEM loop
 
 

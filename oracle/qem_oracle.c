@@ -556,3 +556,13 @@ int orc_num_threads(void) {
   return 1;
 #endif
 }
+
+/* Thread count of the OpenMP loops over groups (timing only: results do not depend on it --
+   every group's sums are computed by one thread and combined in index order). */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}

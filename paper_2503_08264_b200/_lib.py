@@ -12,13 +12,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("QEM_LIB_OVERRIDE") or os.path.join(HERE, "libqem.so")  # override: tuning experiments
 
 FAMILY_TWO_LEVEL, FAMILY_THREE_LEVEL = 2, 3
-OK, INVALID_ARGUMENT, INVALID_MODEL, UNSUPPORTED, CUDA_ERROR = 0, 1, 2, 3, 4
+OK, INVALID_ARGUMENT, INVALID_MODEL, UNSUPPORTED, CUDA_ERROR, NCCL_ERROR = 0, 1, 2, 3, 4, 5
+NCCL_ID_BYTES = 128
 FLAG_DEGENERATE, FLAG_NAN, FLAG_CLAMP = 1, 2, 4
 
 # Every symbol include/qem.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "qem_model_validate", "qem_shard_range", "qem_create", "qem_workspace_bytes", "qem_create_in", "qem_destroy", "qem_bind", "qem_sample_q",
-    "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_backward", "qem_estep_evidence",
+    "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_reduce", "qem_estep_backward", "qem_estep_evidence",
+    "qem_nccl_unique_id", "qem_nccl_init", "qem_set_nccl_comm", "qem_nccl_info",
     "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_estep_tables", "qem_sample_normal",
     "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical", "qem_moments_categorical", "qem_mstep_categorical",
     "qem_loglik_bernoulli_states", "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_global_iw", "qem_sample_gamma",
@@ -104,6 +106,11 @@ def lib() -> ctypes.CDLL:
         L.qem_estep_forward.argtypes = [vp, vp]
         L.qem_estep_backward.argtypes = [vp, vp]
         L.qem_reduce_buffer.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i64)]
+        L.qem_estep_reduce.argtypes = [vp, vp]
+        L.qem_nccl_unique_id.argtypes = [vp]
+        L.qem_nccl_init.argtypes = [vp, vp, i32, i32]
+        L.qem_set_nccl_comm.argtypes = [vp, vp]
+        L.qem_nccl_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
         L.qem_mstep.argtypes = [vp, i32, vp]
         L.qem_mstep_family.argtypes = [i32, i64, i32, ctypes.c_double, vp, vp, vp, vp, vp]
         L.qem_mstep_family.restype = i32
@@ -125,6 +132,7 @@ def lib() -> ctypes.CDLL:
         L.qem_version.restype = ctypes.c_char_p
         for name in ["qem_model_validate", "qem_shard_range", "qem_create", "qem_bind", "qem_sample_q", "qem_estep",
                      "qem_estep_forward", "qem_estep_backward", "qem_reduce_buffer", "qem_mstep", "qem_iterate",
+                     "qem_estep_reduce", "qem_nccl_unique_id", "qem_nccl_init", "qem_set_nccl_comm", "qem_nccl_info",
                      "qem_read_flags", "qem_read_mode_hist", "qem_copy_messages", "qem_estep_evidence",
                      "qem_evidence_root", "qem_workspace_bytes", "qem_create_in", "qem_estep_tables",
                      "qem_sample_normal", "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical",

@@ -11,12 +11,29 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["qem_api.cu", "qem_common.cu", "qem_two_level.cu", "qem_three_level.cu", "qem_expfam.cu", "qem_tables.cu", "qem_discrete.cu", "qem_predict.cu", "qem_gamma.cu", "qem_crossed.cu"]
+SOURCES = ["qem_api.cu", "qem_common.cu", "qem_two_level.cu", "qem_three_level.cu", "qem_expfam.cu", "qem_tables.cu", "qem_discrete.cu", "qem_predict.cu", "qem_gamma.cu", "qem_crossed.cu", "qem_nccl.cu"]
 HEADERS = ["qem_internal.h", "qem_device.cuh", "qem_forward.cuh", "qem_tc.cuh", os.path.join("..", "..", "include", "qem.h")]
 LIB = os.path.join(HERE, "libqem.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_include() -> str:
+    """nccl.h for the types and constants only (NCCL itself is dlopen'ed at run time, qem_nccl.cu):
+    the header of the NCCL torch ships (the copy the process will have loaded), else the system one."""
+    try:
+        import nvidia.nccl
+        for base in list(getattr(nvidia.nccl, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return "/usr/include"
+
+
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+         "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
+         "-I", _nccl_include()]
 
 
 def _stale() -> bool:
@@ -52,7 +69,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
             sys.stderr.write(out.decode())
     tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "--cudart", "static",
-                           "-o", tmp, *objs])
+                           "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, lib)
     return lib
 

@@ -26,6 +26,12 @@ qem_status cuda_fail(cudaError_t e, const char* where) {
   return fail(QEM_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
 }
 
+bool sharded(const qem_ctx* c) { return c->g_begin != 0 || c->g_end != c->desc.n; }
+
+qem_status nccl_fail(int r, const char* where) {
+  return fail(QEM_NCCL_ERROR, "%s: %s", where, qem::nccl_error_string(r));
+}
+
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int pad4(int x) { return (x + 3) & ~3; }
@@ -248,8 +254,95 @@ qem_status qem_create_in(const qem_model_desc* desc, const qem_opts* opts, int64
 void qem_destroy(qem_ctx* c) {
   if (!c) return;
   if (c->graph_valid) cudaGraphExecDestroy(c->graph);
+  if (c->nccl_owned) qem::nccl_comm_destroy(c->nccl_comm);
   if (c->ws && c->ws_owned) cudaFree(c->ws);
   delete c;
+}
+
+// ---- communicator (SURVEY.md §8(b) qem_set_nccl_comm, §8(e)) ----
+
+qem_status qem_nccl_unique_id(void* h_id) {
+  if (!h_id) return fail(QEM_INVALID_ARGUMENT, "null id buffer");
+  const int r = qem::nccl_unique_id(h_id);
+  return r == 0 ? QEM_OK : nccl_fail(r, "ncclGetUniqueId");
+}
+
+// The communicator's (rank, world) must own exactly this context's group block.
+static qem_status adopt_comm(qem_ctx* c, void* comm, int owned) {
+  int rank = -1, world = 0;
+  const int r = qem::nccl_comm_shape(comm, &rank, &world);
+  if (r != 0) return nccl_fail(r, "ncclCommCount / ncclCommUserRank");
+  int64_t b = 0, e = 0;
+  qem_shard_range(c->desc.n, rank, world, &b, &e);
+  if (b != c->g_begin || e != c->g_end)
+    return fail(QEM_INVALID_ARGUMENT, "communicator rank %d of %d owns groups [%lld, %lld), the context [%lld, %lld)",
+                rank, world, (long long)b, (long long)e, (long long)c->g_begin, (long long)c->g_end);
+  if (c->nccl_owned) qem::nccl_comm_destroy(c->nccl_comm);
+  c->nccl_comm = comm;
+  c->nccl_owned = owned;
+  c->nccl_rank = rank;
+  c->nccl_world = world;
+  c->nccl_warm = 0;
+  if (c->graph_valid) {  // a captured loop without (or with another) all-reduce is stale
+    cudaGraphExecDestroy(c->graph);
+    c->graph_valid = 0;
+  }
+  return QEM_OK;
+}
+
+qem_status qem_nccl_init(qem_ctx* c, const void* h_id, int32_t rank, int32_t world) {
+  if (!c || !h_id) return fail(QEM_INVALID_ARGUMENT, "null argument");
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "three-level models run as replicas only");
+  if (world < 1 || rank < 0 || rank >= world) return fail(QEM_INVALID_ARGUMENT, "bad rank %d of %d", rank, world);
+  int64_t b = 0, e = 0;
+  qem_shard_range(c->desc.n, rank, world, &b, &e);
+  if (b != c->g_begin || e != c->g_end)
+    return fail(QEM_INVALID_ARGUMENT, "rank %d of %d owns groups [%lld, %lld), the context [%lld, %lld)", rank, world,
+                (long long)b, (long long)e, (long long)c->g_begin, (long long)c->g_end);
+  void* comm = nullptr;
+  int r = qem::nccl_comm_init(&comm, h_id, rank, world);
+  if (r != 0) return nccl_fail(r, "ncclCommInitRank");
+  qem_status s = adopt_comm(c, comm, 1);
+  if (s != QEM_OK) {
+    qem::nccl_comm_destroy(comm);
+    return s;
+  }
+  cudaStream_t st;
+  cudaError_t ce = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (ce != cudaSuccess) return cuda_fail(ce, "qem_nccl_init: stream");
+  r = qem::nccl_warmup(c, st);  // connect now (collective, like the init), so later captures see a live comm
+  ce = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (r != 0) return nccl_fail(r, "qem_nccl_init: warm-up all-reduce");
+  if (ce != cudaSuccess) return cuda_fail(ce, "qem_nccl_init: warm-up sync");
+  c->nccl_warm = 1;
+  return QEM_OK;
+}
+
+qem_status qem_set_nccl_comm(qem_ctx* c, void* nccl_comm) {
+  if (!c) return fail(QEM_INVALID_ARGUMENT, "null context");
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "three-level models run as replicas only");
+  if (!nccl_comm) {  // detach
+    if (c->nccl_owned) qem::nccl_comm_destroy(c->nccl_comm);
+    c->nccl_comm = nullptr;
+    c->nccl_owned = 0;
+    c->nccl_rank = 0;
+    c->nccl_world = 1;
+    if (c->graph_valid) {
+      cudaGraphExecDestroy(c->graph);
+      c->graph_valid = 0;
+    }
+    return QEM_OK;
+  }
+  return adopt_comm(c, nccl_comm, 0);
+}
+
+qem_status qem_nccl_info(const qem_ctx* c, int32_t* rank, int32_t* world, int32_t* version) {
+  if (!c) return fail(QEM_INVALID_ARGUMENT, "null context");
+  if (rank) *rank = c->nccl_comm ? c->nccl_rank : 0;
+  if (world) *world = c->nccl_comm ? c->nccl_world : 1;
+  if (version) *version = c->nccl_comm ? qem::nccl_version() : 0;
+  return QEM_OK;
 }
 
 qem_status qem_bind(qem_ctx* c, const qem_buffers* b) {
@@ -306,10 +399,31 @@ qem_status qem_estep_backward(qem_ctx* c, void* stream) {
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_backward");
 }
 
+qem_status qem_estep_reduce(qem_ctx* c, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "three-level has no sharded reduction");
+  if (!c->nccl_comm) {
+    if (sharded(c)) return fail(QEM_UNSUPPORTED, "sharded context without a communicator (qem_nccl_init / qem_set_nccl_comm)");
+    return QEM_OK;  // single rank: the local plate sum is the global one
+  }
+  const int r = qem::ctx_allreduce(c, (cudaStream_t)stream);
+  return r == 0 ? QEM_OK : nccl_fail(r, "qem_estep_reduce");
+}
+
 qem_status qem_estep(qem_ctx* c, void* stream) {
-  qem_status s = qem_estep_forward(c, stream);
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (sharded(c) && !c->nccl_comm)
+    return fail(QEM_UNSUPPORTED, "qem_estep on a sharded context needs a communicator (qem_nccl_init / "
+                                 "qem_set_nccl_comm), or the phase calls with a caller all-reduce");
+  s = qem_estep_forward(c, stream);
   if (s) return s;
   const int64_t l = c->launches;
+  if (c->nccl_comm) {
+    s = qem_estep_reduce(c, stream);
+    if (s) return s;
+  }
   s = qem_estep_backward(c, stream);
   c->launches += l;
   return s;
@@ -337,9 +451,15 @@ qem_status qem_estep_evidence(qem_ctx* c, void* stream) {
   if (s) return s;
   if (c->desc.family != QEM_FAMILY_TWO_LEVEL) return fail(QEM_UNSUPPORTED, "fresh denominator: two-level family only");
   if (!c->bufs.log_pe_fresh) return fail(QEM_INVALID_ARGUMENT, "bufs.log_pe_fresh is NULL");
+  if (sharded(c) && !c->nccl_comm)
+    return fail(QEM_UNSUPPORTED, "qem_estep_evidence on a sharded context needs a communicator");
   s = qem_estep_forward(c, stream);
   if (s) return s;
   const int64_t l = c->launches;
+  if (c->nccl_comm) {
+    s = qem_estep_reduce(c, stream);
+    if (s) return s;
+  }
   s = qem_evidence_root(c, stream);
   c->launches += l;
   return s;
@@ -595,6 +715,11 @@ static cudaError_t iterate_body(qem_ctx* c, uint64_t seed, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     e = qem::tl_forward(c, st);
     if (e != cudaSuccess) return e;
+    const int nr = qem::ctx_allreduce(c, st);
+    if (nr != 0) {
+      c->nccl_last = nr;
+      return cudaErrorUnknown;
+    }
     e = evidence_root(c, st);
     if (e != cudaSuccess) return e;
   }
@@ -602,6 +727,12 @@ static cudaError_t iterate_body(qem_ctx* c, uint64_t seed, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_forward(c, st) : qem::th_forward(c, st);
   if (e != cudaSuccess) return e;
+  // the only exchange of a sharded iteration: SUM of the (K+1) fp64 plate sums (no-op at one rank)
+  const int nr = qem::ctx_allreduce(c, st);
+  if (nr != 0) {
+    c->nccl_last = nr;
+    return cudaErrorUnknown;
+  }
   e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_backward(c, st) : qem::th_backward(c, st);
   if (e != cudaSuccess) return e;
   return qem::launch_mstep(c, 0, st);
@@ -611,8 +742,14 @@ qem_status qem_iterate(qem_ctx* c, int32_t t0, int32_t T, uint64_t seed, int32_t
   qem_status s = need_bound(c);
   if (s) return s;
   if (t0 < 1 || T < 0) return fail(QEM_INVALID_ARGUMENT, "need t0 >= 1 and T >= 0");
-  if (c->g_begin != 0 || c->g_end != c->desc.n)
-    return fail(QEM_UNSUPPORTED, "qem_iterate drives a single-rank context; sharded runs use the phase calls");
+  if (sharded(c) && !c->nccl_comm)
+    return fail(QEM_UNSUPPORTED, "qem_iterate on a sharded context needs a communicator (qem_nccl_init / "
+                                 "qem_set_nccl_comm)");
+  if (c->nccl_comm && !c->nccl_warm) {  // NCCL connects lazily: one eager collective before any capture
+    const int r = qem::nccl_warmup(c, (cudaStream_t)stream);
+    if (r != 0) return nccl_fail(r, "qem_iterate: NCCL warm-up");
+    c->nccl_warm = 1;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   // device iteration counter and trace base
   int32_t hdr[2] = {t0, t0};
@@ -624,7 +761,9 @@ qem_status qem_iterate(qem_ctx* c, int32_t t0, int32_t T, uint64_t seed, int32_t
   if (!use_graph) {
     for (int j = 0; j < T; ++j) {
       c->launches = 0;
+      c->nccl_last = 0;
       e = iterate_body(c, seed, st);
+      if (c->nccl_last) return nccl_fail(c->nccl_last, "qem_iterate (eager): all-reduce");
       if (e != cudaSuccess) return cuda_fail(e, "qem_iterate (eager)");
       per_iter = c->launches;
     }
@@ -643,9 +782,15 @@ qem_status qem_iterate(qem_ctx* c, int32_t t0, int32_t T, uint64_t seed, int32_t
     e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
       c->launches = 0;
+      c->nccl_last = 0;
       cudaError_t eb = iterate_body(c, seed, cap);
       e = cudaStreamEndCapture(cap, &g);
       if (eb != cudaSuccess) e = eb;
+      if (c->nccl_last) {
+        if (e == cudaSuccess) cudaGraphDestroy(g);
+        cudaStreamDestroy(cap);
+        return nccl_fail(c->nccl_last, "qem_iterate: graph capture of the all-reduce");
+      }
     }
     if (e == cudaSuccess) {
       e = cudaGraphInstantiate(&c->graph, g, 0);
@@ -697,6 +842,10 @@ int32_t qem_pair_path(const qem_ctx* c) { return c ? (c->tc ? 1 : 0) : -1; }
 
 qem_status qem_set_kernel_events(qem_ctx* c, void* fwd_start, void* fwd_end, void* bwd_start, void* bwd_end) {
   if (!c) return fail(QEM_INVALID_ARGUMENT, "null context");
+  if (c->graph_valid) {  // the captured loop baked the previous events in
+    cudaGraphExecDestroy(c->graph);
+    c->graph_valid = 0;
+  }
   c->ev[0] = fwd_start;
   c->ev[1] = fwd_end;
   c->ev[2] = bwd_start;
@@ -721,6 +870,7 @@ const char* qem_status_str(qem_status s) {
     case QEM_INVALID_MODEL: return "QEM_INVALID_MODEL";
     case QEM_UNSUPPORTED: return "QEM_UNSUPPORTED";
     case QEM_CUDA_ERROR: return "QEM_CUDA_ERROR";
+    case QEM_NCCL_ERROR: return "QEM_NCCL_ERROR";
   }
   return "QEM_UNKNOWN_STATUS";
 }

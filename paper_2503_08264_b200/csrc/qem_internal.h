@@ -98,6 +98,12 @@ struct qem_ctx {
   void* ev[4];  // optional caller events around the pair-tile kernels (fwd start/end, bwd start/end)
   uint64_t graph_seed_;
   int64_t graph_launches_;
+  // in-library plate-sum all-reduce (qem_nccl.cu): ncclComm_t, NULL = single rank
+  void* nccl_comm;
+  int nccl_owned;  // created by qem_nccl_init (destroyed with the context)
+  int nccl_rank, nccl_world;
+  int nccl_warm;   // one eager collective has run on the communicator
+  int nccl_last;   // ncclResult_t of a failed all-reduce inside iterate_body
 };
 
 namespace qem {
@@ -114,6 +120,15 @@ cudaError_t th_backward(qem_ctx* c, cudaStream_t s);
 cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps,
                           cudaStream_t s, uint32_t iter_or = 0);
 cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t s);
+// NCCL, resolved at run time (qem_nccl.cu); int results are ncclResult_t (0 = success)
+int ctx_allreduce(qem_ctx* c, cudaStream_t st);
+int nccl_warmup(qem_ctx* c, cudaStream_t st);
+int nccl_unique_id(void* out128);
+int nccl_comm_init(void** comm, const void* id128, int rank, int world);
+int nccl_comm_shape(void* comm, int* rank, int* world);
+void nccl_comm_destroy(void* comm);
+const char* nccl_error_string(int r);
+int nccl_version();
 // non-Gaussian Q families (qem_expfam.cu)
 cudaError_t launch_estep_tables(int64_t n, int K, const double* f_root, const double* f, double* g, double* log_pe,
                                 double* w_root, double* w, cudaStream_t st);

@@ -14,7 +14,11 @@ indices, so no sample broadcast is needed either.
 
 The compute backend is any object with the ``QEM`` phase API
 (``sample_q / estep_forward / estep_backward / mstep`` and a ``plate_sum``
-tensor); the product uses ``paper_2503_08264_b200.qem.QEM``.
+tensor); the product uses ``paper_2503_08264_b200.qem.QEM``.  A backend with
+``estep_reduce`` and a library-owned communicator (``QEM.nccl_init``) runs the
+all-reduce inside libqem (``ncclAllReduce`` on the compute stream, capturable
+by ``qem_iterate``'s CUDA graph); otherwise the plate sums go through
+``torch.distributed.all_reduce`` (e.g. gloo on CPU).
 """
 from __future__ import annotations
 
@@ -35,14 +39,27 @@ def shard_range(n: int, rank: int, world: int):
 class ShardedQEM:
     """Drives one QEM iteration across ranks: local forward -> all-reduce -> local backward -> M-step."""
 
-    def __init__(self, backend, group: Optional[dist.ProcessGroup] = None):
+    def __init__(self, backend, group: Optional[dist.ProcessGroup] = None, in_library: bool = False):
+        """in_library: attach a libqem-owned NCCL communicator to the backend (QEM.nccl_init) and
+        let the library run the all-reduce (qem_estep_reduce); else torch.distributed does."""
         self.b = backend
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.in_library = bool(in_library)
+        if self.in_library:
+            backend.nccl_init(group)
 
     def allreduce_plate_sum(self) -> None:
-        if self.world > 1:
-            dist.all_reduce(self.b.plate_sum, op=dist.ReduceOp.SUM, group=self.group)
+        if self.in_library:
+            self.b.estep_reduce()
+        elif self.world > 1:
+            t = self.b.plate_sum
+            if t.is_cuda and dist.get_backend(self.group) == "gloo":  # gloo reduces host tensors
+                h = t.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
     def estep(self) -> None:
         self.b.estep_forward()

@@ -235,6 +235,42 @@ class QEM:
     def estep_forward(self, stream=None) -> None:
         check(lib().qem_estep_forward(self.ctx, _stream(stream)), "qem_estep_forward")
 
+    def estep_reduce(self, stream=None) -> None:
+        """The SUM all-reduce of the (K+1) plate sums over the attached communicator (qem_estep_reduce)."""
+        check(lib().qem_estep_reduce(self.ctx, _stream(stream)), "qem_estep_reduce")
+
+    # ------------------------------------------------------- communicator
+    def nccl_init(self, group=None) -> None:
+        """Attach a library-owned NCCL communicator over the ranks of `group` (torch.distributed,
+        any backend; None = the default group, or a 1-rank communicator when torch.distributed is
+        not initialised).  Collective: rank 0 draws the ncclUniqueId (qem_nccl_unique_id), the
+        bytes travel over torch.distributed, every rank calls qem_nccl_init."""
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            rank, world = 0, 1
+        uid = (ctypes.c_char * _lib.NCCL_ID_BYTES)()
+        if rank == 0:
+            check(lib().qem_nccl_unique_id(uid), "qem_nccl_unique_id")
+        if world > 1:
+            box = [bytes(uid)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(box, src=src, group=group)
+            ctypes.memmove(uid, box[0], _lib.NCCL_ID_BYTES)
+        with torch.cuda.device(self.device):
+            check(lib().qem_nccl_init(self.ctx, uid, int(rank), int(world)), "qem_nccl_init")
+
+    def set_nccl_comm(self, comm_ptr) -> None:
+        """Attach a caller-owned ncclComm_t (an integer handle; None detaches)."""
+        check(lib().qem_set_nccl_comm(self.ctx, ctypes.c_void_p(comm_ptr)), "qem_set_nccl_comm")
+
+    def nccl_info(self):
+        """(rank, world, NCCL version code) of the attached communicator ((0, 1, 0) without one)."""
+        r, w, v = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        check(lib().qem_nccl_info(self.ctx, ctypes.byref(r), ctypes.byref(w), ctypes.byref(v)), "qem_nccl_info")
+        return r.value, w.value, v.value
+
     def estep_backward(self, stream=None) -> None:
         check(lib().qem_estep_backward(self.ctx, _stream(stream)), "qem_estep_backward")
 

@@ -338,3 +338,28 @@ def bus_crossed(n: int = 120, J: int = 40, C: int = 57, T: int = 6, K: int = 64,
     eta = w[:, None] + root[1 + comp] + root[1 + C + jtype]
     y = (rng.random((n, J)) < 1.0 / (1.0 + np.exp(-eta))).astype(np.uint8)
     return Crossed(n=n, J=J, C=C, T=T, K=K, comp=comp, jtype=jtype, y=y, root_true=root, w_true=w)
+
+
+def posterior_like_q(m: Model, data: Data, seed: int = 5, shrink: float = 1.0):
+    """A Q centred near the data-generating truth with roughly posterior widths:
+    the converged regime of QEM, where the root weights are spread (H1)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    t = data.truth
+    if m.family == FAMILY_TWO_LEVEL:
+        rm = list(t["mu"]) + ([t["s"]] if m.scale_kind != SCALE_FIXED else [])
+        rsd = shrink * 1.0 / np.sqrt(max(m.n, 1))
+        root_m = np.asarray(rm) + rsd * rng.standard_normal(m.R)
+        root_v = np.full(m.R, rsd ** 2)
+        z = np.asarray(t["z"]).reshape(-1)
+        gsd = shrink * 1.0 / np.sqrt(max(m.J, 1) * 0.25 + 1.0)
+        gm = z + gsd * rng.standard_normal(z.size)
+        gv = np.full(z.size, gsd ** 2)
+        return [(root_m.astype(np.float32), root_v.astype(np.float32)),
+                (gm.astype(np.float32), gv.astype(np.float32))]
+    rm = [t["g"]] + list(t["beta"])
+    rsd = shrink * 0.01
+    root_m = np.asarray(rm) + rsd * rng.standard_normal(m.R)
+    u, v = np.asarray(t["u"]), np.asarray(t["v"])
+    return [(root_m.astype(np.float32), np.full(m.R, rsd ** 2, np.float32)),
+            ((u + 0.3 * rng.standard_normal(u.size)).astype(np.float32), np.full(u.size, 0.09, np.float32)),
+            ((v + 0.01 * rng.standard_normal(v.size)).astype(np.float32), np.full(v.size, 1e-4, np.float32))]

@@ -76,7 +76,21 @@ def test_config4_full_size(regime):
                               float(np.abs(out["dg"] - dref).max()), float(np.abs(dref).max()))
 
 
-def test_config5_full_size_sampled():
+def _check_messages(m, out, ref, z, q, note):
+    """Every group's plate message g_i(k) = c_i + dg_i(k) vs the oracle's."""
+    kref = k_ref_of(m, z[0], q[0])
+    g_ref = ref["g"]
+    np.testing.assert_allclose(out["c"], g_ref[:, kref], rtol=2e-7, atol=1e-6, err_msg=note)
+    dref = g_ref - g_ref[:, kref:kref + 1]
+    err = np.abs(out["dg"] - dref) / (5e-6 + 1e-6 * np.abs(dref))
+    assert err.max() <= 1.0, (note, err.max(), np.unravel_index(err.argmax(), err.shape),
+                              float(np.abs(out["dg"] - dref).max()), float(np.abs(dref).max()))
+
+
+def test_config5_full_size():
+    """All 1e4 groups of config 5 (K = 1024, d = 16, the tcgen05 pair tiles) in the spread-root-weight
+    regime: log Pe, every weight (1.0e7 group weights + the root's), every moment and every group's
+    plate message against the fp64 oracle (~2 min of OpenMP oracle time on the GPU box's host)."""
     m = synth.config(5)
     data = synth.make_data(m)
     q = posterior_like_q(m, data, seed=3, shrink=3.0)
@@ -84,27 +98,35 @@ def test_config5_full_size_sampled():
     z = [orc.sample(qm, qv, e) for (qm, qv), e in zip(q, eps)]
     out = _gpu_estep(m, data, q, eps)
     assert out["flags"] & 2 == 0
-    K, d = m.K, m.d
-    # properties at full size
-    np.testing.assert_allclose(out["w"][0].sum(), 1.0, atol=1e-5)
-    np.testing.assert_allclose(out["w"][1].sum(axis=-1), 1.0, atol=2e-5)
-    # root softmax identity from the device's own plate messages
-    zr = np.asarray(z[0], np.float64).reshape(m.R, K)
-    f_root = sum(-0.5 * np.log(2 * np.pi) - 0.5 * zr[r] ** 2
-                 + 0.5 * np.log(2 * np.pi * float(q[0][1][r])) + 0.5 * (zr[r] - float(q[0][0][r])) ** 2 / float(q[0][1][r])
-                 for r in range(m.R))
-    a = f_root + out["dg"].astype(np.float64).sum(axis=0)
-    w_root = np.exp(a - logsumexp(a))
-    np.testing.assert_allclose(out["w"][0].reshape(-1), w_root, atol=1e-5)
-    # sampled groups: the oracle computes each group's message g_i(k) exactly
-    kref = k_ref_of(m, z[0], q[0])
-    rng = np.random.default_rng(0)
-    for i in sorted(rng.choice(m.n, 6, replace=False)):
-        mi = synth.config(5, n=1)
-        di = synth.Data(xb=data.xb[i:i + 1], yb=data.yb[i:i + 1])
-        zi = [z[0], z[1][i * d:(i + 1) * d]]
-        qi = [q[0], (q[1][0][i * d:(i + 1) * d], q[1][1][i * d:(i + 1) * d])]
-        gi = orc.estep(mi, zi, qi, di)["g"][0]
-        assert abs(out["c"][i] - gi[kref]) <= 2e-7 * abs(gi[kref]) + 1e-6, (i, out["c"][i], gi[kref])
-        err = np.abs(out["dg"][i] - (gi - gi[kref])).max()
-        assert err <= 5e-6, (i, err)
+    ref = orc.estep(m, z, q, data)
+    check_estep(m, out, ref, note="config5 full")
+    _check_messages(m, out, ref, z, q, "config5 full")
+
+
+@pytest.mark.parametrize("cid", [4, 5])
+def test_teacher_forced_full_size_first_iterations(cid):
+    """SURVEY.md §8(d) parity protocol for the large configs: the first 3 QEM iterations at full size
+    (Alg. 1; R21), each from the oracle's state m_{t-1} and Q_t with the
+    same host eps: E-step outputs, EMA state and the next Q at the contract tolerances."""
+    from paper_2503_08264_b200.qem import QEM
+    from test_gpu_qem import check_step
+    m = synth.config(cid)
+    data = synth.make_data(m)
+    seed = 100 + cid
+    g = QEM(m)
+    g.set_data(data)
+    state = orc.initial_state(m)
+    q = [orc.mstep(a, b)[:2] for a, b in state]
+    for t in range(1, 4):
+        eps = orc.eps_for_iteration(m, t, seed)
+        g.set_state([(a, b - a * a) for a, b in state])
+        g.set_q(q)
+        g.sample_q(eps=eps)
+        g.estep()
+        g.mstep(t)
+        out = g.result()
+        ref = orc.qem_step(m, state, q, eps, t, data=data)
+        check_step(m, out, ref, note=f"config{cid} full t={t}")
+        state, q = ref["state"], ref["q_next"]
+    assert g.read_flags()[0] & 2 == 0
+    g.close()

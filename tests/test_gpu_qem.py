@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 CASES = {
     "c1_T20": (dict(cid=1), 20),
     "c2_T100": (dict(cid=2), 100),
-    "c3_T30": (dict(cid=3), 30),
+    "c3_T100": (dict(cid=3), 100),
     "c4_n1000_T50": (dict(cid=4, n=1000), 50),
     "c5_n12_T10": (dict(cid=5, n=12), 10),
 }
@@ -33,6 +33,26 @@ def _model(spec):
 
 def _rel(a, b, scale):
     return float(np.max(np.abs(np.asarray(a) - np.asarray(b)) / scale)) if np.size(a) else 0.0
+
+
+def check_step(m, out, ref, note=""):
+    """One teacher-forced iteration (gpu result() vs orc.qem_step): the E-step at the contract
+    tolerances, then the EMA state m_t and the next Q (1e-4 relative).  Returns the worst errors."""
+    check_estep(m, out, ref["est"], note=note)
+    est = ref["est"]
+    worst = dict(log_pe=abs(out["log_pe"] - est["log_pe"]) / abs(est["log_pe"]), w=0.0, m=0.0, q=0.0)
+    for lvl, ((m1r, m2r), (qm, qv)) in enumerate(zip(ref["state"], ref["q_next"])):
+        vr = m2r - m1r * m1r
+        sd = np.sqrt(np.maximum(vr, 0))
+        e1 = _rel(out["ema_m1"][lvl], m1r, np.maximum(np.abs(m1r), sd))
+        e2 = _rel(out["ema_v"][lvl] + out["ema_m1"][lvl] ** 2, m2r, np.abs(m2r))
+        eq1 = _rel(out["q_mean"][lvl], qm, np.maximum(np.abs(qm), np.sqrt(qv)))
+        eq2 = _rel(out["q_var"][lvl], qv, np.abs(qv))
+        assert max(e1, e2) <= 1e-4, f"{note} level {lvl} EMA state rel err {max(e1, e2):.3g}"
+        assert max(eq1, eq2) <= 1e-4, f"{note} level {lvl} M-step params rel err {max(eq1, eq2):.3g}"
+        worst["m"] = max(worst["m"], e1, e2)
+        worst["q"] = max(worst["q"], eq1, eq2)
+    return worst
 
 
 @pytest.mark.parametrize("case", sorted(CASES))
@@ -57,20 +77,9 @@ def test_teacher_forced_trajectory(case):
         g.estep()
         g.mstep(t)
         out = g.result()
-        check_estep(m, out, ref["est"], note=f"{case} t={t}")
-        est = ref["est"]
-        worst["log_pe"] = max(worst["log_pe"], abs(out["log_pe"] - est["log_pe"]) / abs(est["log_pe"]))
-        for lvl, ((m1r, m2r), (qm, qv)) in enumerate(zip(ref["state"], ref["q_next"])):
-            vr = m2r - m1r * m1r
-            sd = np.sqrt(np.maximum(vr, 0))
-            e1 = _rel(out["ema_m1"][lvl], m1r, np.maximum(np.abs(m1r), sd))
-            e2 = _rel(out["ema_v"][lvl] + out["ema_m1"][lvl] ** 2, m2r, np.abs(m2r))
-            eq1 = _rel(out["q_mean"][lvl], qm, np.maximum(np.abs(qm), np.sqrt(qv)))
-            eq2 = _rel(out["q_var"][lvl], qv, np.abs(qv))
-            assert max(e1, e2) <= 1e-4, f"{case} t={t} level {lvl} EMA state rel err {max(e1, e2):.3g}"
-            assert max(eq1, eq2) <= 1e-4, f"{case} t={t} level {lvl} M-step params rel err {max(eq1, eq2):.3g}"
-            worst["m"] = max(worst["m"], e1, e2)
-            worst["q"] = max(worst["q"], eq1, eq2)
+        errs = check_step(m, out, ref, note=f"{case} t={t}")
+        for k in worst:
+            worst[k] = max(worst[k], errs[k])
         state, q = ref["state"], ref["q_next"]
     flags, _ = g.read_flags()
     assert flags & 2 == 0
@@ -105,3 +114,59 @@ def test_free_running_drift_reported(case):
     g.close()
     print(f"\n{case}: free-running root-mean drift by iteration: " + " ".join(f"{d:.1e}" for d in drift))
     assert max(drift) < 0.05
+
+
+def philox_eps(m, seed, t):
+    """The oracle's own draw of the device sampler's Philox stream for iteration t (fp64 Box-Muller
+    of the same counters, SURVEY.md §8(b) Determinism), rounded to fp32: one array per level."""
+    out = []
+    for lvl, (n, dd) in enumerate(synth.latent_shapes(m)):
+        e = np.concatenate([orc.normal_eps(seed, t, lvl, i, dd, m.K) for i in range(n)], axis=0)
+        out.append(e.astype(np.float32))
+    return out
+
+
+ITER_CASES = {
+    "c1_T20": (dict(cid=1), 20),
+    "c2_T20": (dict(cid=2), 20),
+    "c3_T20": (dict(cid=3), 20),
+    "c4_n500_T5": (dict(cid=4, n=500), 5),
+    "c5_n8_T5": (dict(cid=5, n=8), 5),
+}
+
+
+@pytest.mark.parametrize("use_graph", [True, False], ids=["graph", "eager"])
+@pytest.mark.parametrize("case", sorted(ITER_CASES))
+def test_qem_iterate_teacher_forced(case, use_graph):
+    """qem_iterate -- the library's own loop (Philox sampler -> E-step -> EMA + M-step, captured in a
+    CUDA graph or issued eagerly; Alg. 1) -- one iteration at a time from the
+    oracle's state m_{t-1} and Q_t.  The oracle draws the same Philox counters itself (fp64
+    Box-Muller); the device's fp32 transform is within 2e-6 of it (R27), and the step's
+    outputs (trace log Pe, weights, moments, EMA state, next Q) meet the contract tolerances."""
+    from paper_2503_08264_b200.qem import QEM
+    spec, T = ITER_CASES[case]
+    m = _model(spec)
+    data = synth.make_data(m)
+    seed = 0x5EED0000 + m.config_id
+    g = QEM(m, trace_len=1)
+    g.set_data(data)
+    state = orc.initial_state(m)
+    q = [orc.mstep(a, b)[:2] for a, b in state]
+    for t in range(1, T + 1):
+        g.set_state([(a, b - a * a) for a, b in state])
+        g.set_q(q)
+        g.iterate(t, 1, seed=seed, use_graph=use_graph)
+        out = g.result()
+        trace = float(g.trace[0].item())
+        eps = philox_eps(m, seed, t)
+        ref = orc.qem_step(m, state, q, eps, t, data=data)
+        for lvl, zr in enumerate(ref["z"]):
+            zg = out["z"][lvl].reshape(zr.shape).astype(np.float64)
+            sd = np.sqrt(np.asarray(q[lvl][1], np.float64))[:, None]
+            tol = 2e-6 * sd + 2.0 * np.spacing(np.abs(zr).astype(np.float32)).astype(np.float64)  # + fp32 rounding of z
+            assert np.all(np.abs(zg - zr) <= tol), f"{case} t={t} level {lvl} samples"
+        assert trace == out["log_pe"]
+        check_step(m, out, ref, note=f"{case} t={t} {'graph' if use_graph else 'eager'}")
+        state, q = ref["state"], ref["q_next"]
+    assert g.read_flags()[0] & 2 == 0
+    g.close()
