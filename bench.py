@@ -718,7 +718,7 @@ def run_reference(args):
     full = synth.config(args.config)
     cores = os.cpu_count() or 1
     orc.set_num_threads(cores)
-    budget = max(10.0, min(120.0, args.cpu_budget * 4))
+    budget = max(2.0, min(120.0, args.cpu_budget * 4))
     # probe: one step on `cores` groups sizes the per-step sample
     n_s = max(1, min(full.n, cores))
     m = synth.config(args.config, n=n_s)

@@ -3,6 +3,8 @@
 // M=128 N=256 K=16, 3-way bf16 split with 6 partial products (~fp32-exact
 // dot products), TMEM alloc / tcgen05.ld.32x32b / commit-to-mbarrier.
 // D[m][n] = sum_r A[m][r] * B[n][r], r < 16, compared with fp64 on the host.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 tools/tc_probe.cu -o tools/tc_probe
+//        (add -DTC_PROBE_SMALL_FIRST for the partial-product order the library uses).
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cstdio>
@@ -78,7 +80,11 @@ __global__ void probe(const float* A, const float* B, float* D, int split) {
   if (tid == 0) {
     const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
     // (split_a, split_b) products: 00 01 10 02 11 20 (or only 00 when split == 0)
+#ifdef TC_PROBE_SMALL_FIRST  // the order the library uses (qem_tc.cuh umma_tile7): smallest products first
+    const int pa[6] = {2, 1, 0, 1, 0, 0}, pb[6] = {0, 1, 2, 0, 1, 0};
+#else
     const int pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {0, 1, 0, 2, 1, 0};
+#endif
     const int np = split ? 6 : 1;
     for (int q = 0; q < np; ++q) {
       uint64_t ad = make_desc(a0 + pa[q] * 256, 128, 768);
