@@ -177,6 +177,11 @@ typedef struct {
                           NULL = the context's own (see qem_reduce_buffer)          */
   double* log_pe_fresh; /* [1] log Pe(z_new) of the fresh-denominator pass (qem_estep_evidence);
                           required when opts.fresh_denominator, else may be NULL    */
+  const float* eps_bank[3]; /* optional parity mode of qem_iterate: per bound level, host-generated
+                          N(0,1) draws [eps_bank_len][instances*dims][K] (fp32, device); iteration
+                          t0+j samples with slice j instead of Philox (the fresh-denominator z_new
+                          still comes from Philox).  eps_bank[0] == NULL: Philox (default). */
+  int64_t eps_bank_len;
 } qem_buffers;
 
 typedef struct qem_ctx qem_ctx;
@@ -496,7 +501,8 @@ qem_status qem_mstep_family(int32_t family, int64_t n, int32_t C, double lam, co
    E-step (forward, all-reduce over the attached communicator, backward) -> M-step, replayed
    from one captured CUDA graph, or issued eagerly when `use_graph` == 0.  A sharded context
    needs a communicator (QEM_UNSUPPORTED otherwise) and every rank calls qem_iterate with the
-   same (t0, T, seed, use_graph): each iteration is one collective.  With opts.fresh_denominator each
+   same (t0, T, seed, use_graph): each iteration is one collective.  With bufs.eps_bank bound the
+   samples come from the bank (QEM_INVALID_ARGUMENT if T > bufs.eps_bank_len).  With opts.fresh_denominator each
    iteration first samples z_new (Philox iteration word t | 2^23) and runs the
    evidence pass.  log Pe of iteration t0+j goes to
    bufs.trace[j] when bufs.trace != NULL. */

@@ -53,7 +53,8 @@ class Level(ctypes.Structure):
 class Buffers(ctypes.Structure):
     _fields_ = [("level", Level * 3), ("x", ctypes.c_void_p), ("y", ctypes.c_void_p),
                 ("log_pe", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_len", ctypes.c_int64),
-                ("plate_sum", ctypes.c_void_p), ("log_pe_fresh", ctypes.c_void_p)]
+                ("plate_sum", ctypes.c_void_p), ("log_pe_fresh", ctypes.c_void_p),
+                ("eps_bank", ctypes.c_void_p * 3), ("eps_bank_len", ctypes.c_int64)]
 
 
 class QemError(RuntimeError):

@@ -113,7 +113,7 @@ size_t carve(qem_ctx* c, char* base) {
     if (c->tc) {
       c->tw.rowop = take((size_t)K * 96);
       c->tw.rowop_x = take((size_t)K * 32);
-      c->tw.colop = take((size_t)c->n_local * K * 128);
+      c->tw.colop = take((size_t)c->n_local * K * (D == 1 ? 64 : 128));  // TcGeo<D>::COL
       c->tw.colaux = reinterpret_cast<float*>(take((size_t)c->n_local * K * 8));
       c->tw.gmode = reinterpret_cast<int*>(take(sizeof(int) * (size_t)c->n_local));
       c->tw.rowop_b = take((size_t)K * 96);
@@ -355,6 +355,11 @@ qem_status qem_bind(qem_ctx* c, const qem_buffers* b) {
     return fail(QEM_INVALID_ARGUMENT, "null label buffer y");
   if (c->opts.fresh_denominator && !b->log_pe_fresh)
     return fail(QEM_INVALID_ARGUMENT, "opts.fresh_denominator needs bufs.log_pe_fresh");
+  if (b->eps_bank[0]) {
+    for (int l = 1; l < nlev; ++l)
+      if (!b->eps_bank[l]) return fail(QEM_INVALID_ARGUMENT, "eps_bank: level %d is NULL", l);
+    if (b->eps_bank_len < 1) return fail(QEM_INVALID_ARGUMENT, "eps_bank_len must be >= 1");
+  }
   c->bufs = *b;
   c->bound = 1;
   if (c->graph_valid) {
@@ -742,6 +747,9 @@ qem_status qem_iterate(qem_ctx* c, int32_t t0, int32_t T, uint64_t seed, int32_t
   qem_status s = need_bound(c);
   if (s) return s;
   if (t0 < 1 || T < 0) return fail(QEM_INVALID_ARGUMENT, "need t0 >= 1 and T >= 0");
+  if (c->bufs.eps_bank[0] && T > c->bufs.eps_bank_len)
+    return fail(QEM_INVALID_ARGUMENT, "T=%d exceeds the bound eps bank (%lld iterations)", T,
+                (long long)c->bufs.eps_bank_len);
   if (sharded(c) && !c->nccl_comm)
     return fail(QEM_UNSUPPORTED, "qem_iterate on a sharded context needs a communicator (qem_nccl_init / "
                                  "qem_set_nccl_comm)");

@@ -46,6 +46,7 @@ struct SampleArgs {
   int t_host;
   uint32_t iter_or;  // OR-ed into the iteration word (bit 23: the fresh-denominator stream)
   const int32_t* d_iter;
+  const int32_t* d_base;  // eps bank mode (qem_iterate parity mode): slice (t - *d_base) of every level's eps
 };
 
 // r = sqrt(-2 ln u), u = (m + 1/2) 2^-23, m a 23-bit integer.  Near u = 1 (v = 1 - u < 2^-5,
@@ -148,8 +149,10 @@ template <int QPT>
 __global__ void __launch_bounds__(256) k_sample(SampleArgs a) {
   const int t = resolve_iter(a.t_host, a.d_iter);
   const uint32_t stride = gridDim.x * blockDim.x;
+  const int64_t bj = a.d_base ? (int64_t)(t - *a.d_base) : 0;  // eps bank slice of iteration t
   for (int L = 0; L < a.nlev; ++L) {
-    const SampleLevel s = a.lv[L];
+    SampleLevel s = a.lv[L];
+    if (s.eps) s.eps += bj * s.rows * a.K;
     const uint32_t units = (uint32_t)s.rows * (uint32_t)a.units_per_row;
     for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < units; u += stride) sample_unit<QPT>(a, s, u, t);
   }
@@ -206,6 +209,10 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
                           uint32_t iter_or) {
   SampleArgs a{};
   a.iter_or = iter_or;
+  if (!d_eps && iter == 0 && iter_or == 0 && c->bufs.eps_bank[0]) {  // qem_iterate in eps bank mode
+    d_eps = c->bufs.eps_bank;
+    a.d_base = &c->cnt->trace_base;
+  }
   const int K = c->desc.K;
   a.K = K;
   a.quads_per_row = (K + 3) / 4;

@@ -156,6 +156,10 @@ __host__ __device__ __forceinline__ int tc_col_offset(int row, int kk) {
 __host__ __device__ __forceinline__ int tc_rowx_offset(int row, int kk) {
   return (row >> 3) * 256 + (kk >> 3) * 128 + (row & 7) * 16 + (kk & 7) * 2;
 }
+// Any K-major no-swizzle operand of `rb` bytes per row (8-row groups 8 rb apart).
+__host__ __device__ __forceinline__ int tc_off(int row, int kk, int rb) {
+  return (row >> 3) * (8 * rb) + (kk >> 3) * 128 + (row & 7) * 16 + (kk & 7) * 2;
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(__nv_bfloat16 lo, __nv_bfloat16 hi) {
   return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
 }

@@ -46,6 +46,46 @@ constexpr int kTcRowCBytes = kTcRowBytes;  // 96: c2 split (6 chunks)
 #endif
 constexpr int kPolyExpFwd = QEM_POLY_EXP_FWD, kPolyExpBwd = QEM_POLY_EXP_BWD;
 
+// Operand geometry per latent dimension:
+//  D = 8..16 ("split"): the c-region of a row / column is the bf16x3 split of the 16-dim
+//    (zero-padded) contraction, 96 B, contracted by 6 MMAs (the six leading partial products);
+//    the 16-entry extra slab carries gamma |w|^2 (its S pattern), the row constant and ln P.
+//  D = 1 ("compact", config 4): the c-region is ONE 16-entry slab holding the six leading partial
+//    products of c w AND of gamma S explicitly -- row [c2 c1 c0 c1 c0 c0 g0 g0 | g1 g0 g2 g1 0 0 0 0],
+//    column [w0 w1 w2 w0 w1 w0 S0 S1 | S0 S2 S0 S1 0 0 0 0] -- 32 B and one MMA; the extra slab
+//    carries only the row constant and ln P (its gamma / S entries are zero).  A column is 64 B.
+template <int D>
+struct TcGeo {
+  static constexpr bool COMPACT = D == 1;
+  static constexpr int CB = COMPACT ? 32 : 96;   // c-region bytes per row / column
+  static constexpr int COL = CB + kTcRowXBytes;  // column operand bytes (c-region + extra slab)
+  static constexpr int XKK = CB / 2;             // bf16 index where a column's extra slab starts
+  __host__ __device__ static int col_off(int row, int kk) { return tc_off(row, kk, COL); }
+  __host__ __device__ static int row_off(int row, int kk) { return tc_off(row, kk, CB); }
+};
+
+// compact c-region (D = 1) of a row (c = log2e c_k, g = log2e gamma_k) and of a column (w, S)
+__device__ __forceinline__ void compact_row(float c, float g, uint4& c0, uint4& c1) {
+  __nv_bfloat16 cs[3], gs[3];
+  split3_bf16(c, cs);
+  split3_bf16(g, gs);
+  const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
+  const __nv_bfloat16 a[8] = {cs[2], cs[1], cs[0], cs[1], cs[0], cs[0], gs[0], gs[0]};
+  const __nv_bfloat16 b[8] = {gs[1], gs[0], gs[2], gs[1], z, z, z, z};
+  c0 = pack8_bf16(a);
+  c1 = pack8_bf16(b);
+}
+__device__ __forceinline__ void compact_col(float w, float S, uint4& c0, uint4& c1) {
+  __nv_bfloat16 ws[3], ss[3];
+  split3_bf16(w, ws);
+  split3_bf16(S, ss);
+  const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
+  const __nv_bfloat16 a[8] = {ws[0], ws[1], ws[2], ws[0], ws[1], ws[0], ss[0], ss[1]};
+  const __nv_bfloat16 b[8] = {ss[0], ss[2], ss[0], ss[1], z, z, z, z};
+  c0 = pack8_bf16(a);
+  c1 = pack8_bf16(b);
+}
+
 // named barriers: 1 = all epilogue warps, 2..5 = the 4 warps of one TMEM lane quarter
 __device__ __forceinline__ void epi_bar() { named_bar(1, kTcEpiThreads); }
 __device__ __forceinline__ void quarter_bar(int q) { named_bar(2 + q, 128); }
@@ -84,6 +124,18 @@ __device__ __forceinline__ void umma_tile7(uint32_t tmem_d, uint32_t a_c, uint32
     umma_bf16(tmem_d, umma_desc(a_c + pa[q] * 256, 128, a_sbo), umma_desc(b_c + pb[q] * 256, 128, b_sbo), idesc,
               q > 0);
   umma_bf16(tmem_d, umma_desc(a_x, 128, a_xsbo), umma_desc(b_x, 128, b_xsbo), idesc, 1u);
+}
+
+// One tile: the c-region MMAs (6 split products, or the compact slab) + the extra slab.
+template <int D>
+__device__ __forceinline__ void umma_tile(uint32_t tmem_d, uint32_t a_c, uint32_t a_sbo, uint32_t b_c, uint32_t b_sbo,
+                                          uint32_t a_x, uint32_t a_xsbo, uint32_t b_x, uint32_t b_xsbo, uint32_t idesc) {
+  if constexpr (TcGeo<D>::COMPACT) {
+    umma_bf16(tmem_d, umma_desc(a_c, 128, a_sbo), umma_desc(b_c, 128, b_sbo), idesc, 0u);
+    umma_bf16(tmem_d, umma_desc(a_x, 128, a_xsbo), umma_desc(b_x, 128, b_xsbo), idesc, 1u);
+  } else {
+    umma_tile7(tmem_d, a_c, a_sbo, b_c, b_sbo, a_x, a_xsbo, b_x, b_xsbo, idesc);
+  }
 }
 
 // 16-dim row vector -> bf16x3 split in the 96-byte canonical row layout (tc_offset)
@@ -163,7 +215,18 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
   const double es = exp(-root_lnv<D>(a, ks));
   for (int k = tid; k < K; k += blockDim.x) {
     const double ek = exp(-root_lnv<D>(a, k));
-    if constexpr (D <= kTcD) {
+    if constexpr (TcGeo<D>::COMPACT) {
+      if (a.tc) {  // Eb and Eg both in the compact c-region; the per-group slab's gamma stays 0
+        uint4 c0, c1;
+        compact_row((float)((ek * (double)a.z_root[k] - es * (double)a.z_root[ks]) * kLog2eD),
+                    (float)(-0.5 * (ek - es) * kLog2eD), c0, c1);
+        unsigned char* rb = reinterpret_cast<unsigned char*>(a.ws.rowop_b);
+        *reinterpret_cast<uint4*>(rb + TcGeo<D>::row_off(k, 0)) = c0;
+        *reinterpret_cast<uint4*>(rb + TcGeo<D>::row_off(k, 8)) = c1;
+        a.ws.bgam[k] = 0.f;
+        continue;
+      }
+    } else if constexpr (D <= kTcD) {
       if (a.tc) {
         float v[kTcD];
 #pragma unroll
@@ -188,6 +251,16 @@ __global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
   unsigned char* rx = reinterpret_cast<unsigned char*>(a.ws.rowop_x);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
     const float* fc = a.ws.fwd_coef + (size_t)k * (D + 2);
+    if constexpr (TcGeo<D>::COMPACT) {
+      uint4 c0, c1;
+      compact_row(fc[2] * kLog2e, fc[1] * kLog2e, c0, c1);
+      *reinterpret_cast<uint4*>(rc + TcGeo<D>::row_off(k, 0)) = c0;
+      *reinterpret_cast<uint4*>(rc + TcGeo<D>::row_off(k, 8)) = c1;
+      extra_row(0.f, 1.f, 0.f, c0, c1);  // forward: lP on, no row constant, gamma in the c-region
+      *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 0)) = c0;
+      *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 8)) = c1;
+      continue;
+    }
     float v[kTcD];  // contraction zero-padded to 16 dims
 #pragma unroll
     for (int r = 0; r < kTcD; ++r) v[r] = r < D ? fc[2 + r] * kLog2e : 0.f;
@@ -503,6 +576,160 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
   }
 }
 
+// -------------------------------------------- colprep, compact path (K2a, D = 1, config 4)
+// One warp per group (persistent over groups), lanes over the group's columns.  Per column k':
+//   t_ref(k') = B(k_ref,k') + A_i(k') = bref - (e_ref/2)(z - mu_ref)^2 + ll(z) - ln q(z)   (fp64;
+//   ll = the Gaussian likelihood through the group's sufficient statistics, as k_colprep),
+//   w = z - m_i, S = w^2 + 2 m_i w (fp32)  -> the compact c-region + extra chunk 0 [0 .. 0 1 1];
+// then P = softmax t_ref from the lanes' online (max, sum), the group's tile mode from the bound on
+// |D'_k(k')| = |c'_k w + gamma_k w^2| (c' = c0 + 2 gamma m_i), P -> colaux, and ln P into the extra
+// slab's second chunk (online mode only).  No shared memory: t_ref is re-read from L1/L2.
+template <int OBS>
+__global__ void __launch_bounds__(256) k_colprep_tc1(TLArgs a) {
+  using G = TcGeo<1>;
+  static_assert(OBS == QEM_OBS_GAUSS, "compact tensor-core path: Gaussian observations");
+  const int K = a.K, J = a.J, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const double bref = a.ws.ref->bref_const, e_ref = a.ws.ref->e_ref;
+  const double mref = (double)a.ws.ref->mu_ref[0];
+  const double logK = log((double)K);
+  const double gc0 = -0.5 * J * (kLn2Pi + log(a.obs_var)), gc1 = 0.5 / a.obs_var;
+  unsigned char* colop = reinterpret_cast<unsigned char*>(a.ws.colop);
+  for (int64_t i = (int64_t)blockIdx.x * nw + wid; i < a.n_local; i += (int64_t)gridDim.x * nw) {
+    const float* x = reinterpret_cast<const float*>(a.x) + i * J;
+    double sx = 0.0, sxx = 0.0;
+    for (int j = lane; j < J; j += 32) {
+      const double xv = x[j];
+      sx += xv;
+      sxx += xv * xv;
+    }
+    sx = warp_sum(sx);
+    sxx = warp_sum(sxx);
+    const float mf = a.q_m[i];
+    const double m = mf, v = a.q_v[i];
+    const double lqc = -0.5 * (kLn2Pi + log(v)), iv2 = 0.5 / v;
+    unsigned char* cop = colop + (size_t)i * K * G::COL;
+    const float* zi = a.z + (size_t)i * K;
+    double* tref = a.ws.tA + (size_t)i * K;
+    double tmax = -CUDART_INF, tsum = 0.0;
+    float w2max = 0.f;
+#pragma unroll 4
+    for (int kc = lane; kc < K; kc += 32) {
+      const float zf = zi[kc];
+      const double z = zf, dz = z - m, u = z - mref;
+      const double lq = lqc - dz * dz * iv2;
+      const double ll = gc0 - (sxx - 2.0 * z * sx + (double)J * z * z) * gc1;
+      const double t = bref - 0.5 * e_ref * u * u + (ll - lq);
+      tref[kc] = t;
+      if (t > tmax) {
+        tsum = fma(tsum, (double)expf((float)(tmax - t)), 1.0);
+        tmax = t;
+      } else {
+        tsum += (double)expf((float)(t - tmax));
+      }
+      const float w = zf - mf, W2 = w * w;
+      uint4 c0, c1;
+      compact_col(w, fmaf(2.f, mf * w, W2), c0, c1);
+      *reinterpret_cast<uint4*>(cop + G::col_off(kc, 0)) = c0;
+      *reinterpret_cast<uint4*>(cop + G::col_off(kc, 8)) = c1;
+      extra_col(0.f, 0.f, c0, c1);  // chunk 0: [0 0 0 0 0 0 1 1]; chunk 1 (1, lP) below
+      *reinterpret_cast<uint4*>(cop + G::col_off(kc, G::XKK)) = c0;
+      w2max = fmaxf(w2max, W2);
+    }
+    const double M = warp_max(tmax);
+    const float W2max = warp_maxf(w2max);
+    const double logS = log(warp_sum(tsum * (double)expf((float)(tmax - M))));
+    const float wmax = sqrtf(W2max);
+    float tb = 0.f;
+    for (int k = lane; k < K; k += 32) {
+      const float g = a.ws.fwd_coef[(size_t)k * 3 + 1], c = a.ws.fwd_coef[(size_t)k * 3 + 2];
+      tb = fmaxf(tb, fabsf(fmaf(2.f * g, mf, c)) * wmax + fabsf(g) * W2max);
+    }
+    tb = warp_maxf(tb);
+    const int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
+    float* aux = a.ws.colaux + (size_t)i * 2 * K;
+    __syncwarp();
+#pragma unroll 4
+    for (int kc = lane; kc < K; kc += 32) {
+      const float lp = (float)(tref[kc] - M - logS);  // this lane's own store above
+      aux[kc] = expf(lp);
+      uint4 c0, c1;
+      extra_col(0.f, md == 5 ? lp * kLog2e : 0.f, c0, c1);
+      *reinterpret_cast<uint4*>(cop + G::col_off(kc, G::XKK + 8)) = c1;
+    }
+    if (lane == 0) {
+      a.ws.cvec[i] = M + logS - logK;
+      a.ws.gstat[i] = W2max;
+      a.ws.gmode[i] = md;
+    }
+  }
+}
+
+// ------------------------------- backward column constants, compact path (K4a, D = 1)
+// As k_bwd_cols_tc, one warp per group: L*(k') = log2e log P(k'|k*), the softmax over the group's
+// columns of t_ref(k') + B(k*,k') - B(k_ref,k') (fp64), into the extra slab's lP slots.  Three
+// passes over the columns (max, sum, write); the re-reads of z / t_ref hit L1.
+template <int D>
+__global__ void __launch_bounds__(256) k_bwd_cols_warp(TLArgs a) {
+  static_assert(TcGeo<D>::COMPACT, "warp-per-group column constants: compact path");
+  using G = TcGeo<D>;
+  const int K = a.K, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double mus = (double)a.ws.ref->mu_star[0], mur = (double)a.ws.ref->mu_ref[0];
+  const double es = a.ws.ref->e_star, bs = a.ws.ref->bstar_const;
+  const double er = a.ws.ref->e_ref, br = a.ws.ref->bref_const;
+  for (int64_t i = (int64_t)blockIdx.x * nw + wid; i < a.n_local; i += (int64_t)gridDim.x * nw) {
+    const float* zi = a.z + (size_t)i * K;
+    const double* tr = a.ws.tA + (size_t)i * K;
+    auto tcol = [&](int kc) {
+      const double z = zi[kc], ds = z - mus, dr = z - mur;
+      return (bs - 0.5 * es * ds * ds) - (br - 0.5 * er * dr * dr) + tr[kc];
+    };
+    double mx = -CUDART_INF;
+    for (int kc = lane; kc < K; kc += 32) mx = fmax(mx, tcol(kc));
+    mx = warp_max(mx);
+    double se = 0.0;
+    for (int kc = lane; kc < K; kc += 32) se += (double)expf((float)(tcol(kc) - mx));
+    const double lse = mx + log(warp_sum(se));
+    unsigned char* cop = reinterpret_cast<unsigned char*>(a.ws.colop) + (size_t)i * K * G::COL;
+    for (int kc = lane; kc < K; kc += 32) {
+      uint4 x0, x1;
+      extra_col(0.f, (float)((tcol(kc) - lse) * kLog2eD), x0, x1);
+      *reinterpret_cast<uint4*>(cop + G::col_off(kc, G::XKK + 8)) = x1;
+    }
+  }
+}
+
+// ------------------------------------------------- moments, warp per group (K4c, small D)
+// E z = c + S1/S0, Var z = S2/S0 - (S1/S0)^2, S_p = sum_k' w (z - c)^p (fp64, shifted by the Q mean
+// c = m_i, self-normalised: R24), one warp per (group, dim).
+template <int D>
+__global__ void __launch_bounds__(256) k_moments_warp(TLArgs a) {
+  const int K = a.K, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t rows = a.n_local * D;
+  for (int64_t rr = (int64_t)blockIdx.x * nw + wid; rr < rows; rr += (int64_t)gridDim.x * nw) {
+    const int64_t i = rr / D;
+    const float* zr = a.z + (size_t)rr * K;
+    const float* wi = a.w + (size_t)i * K;
+    const double c = a.q_m[rr];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll 4
+    for (int kc = lane; kc < K; kc += 32) {
+      const double w = wi[kc], e = (double)zr[kc] - c, pe = w * e;
+      s0 += w;
+      s1 += pe;
+      s2 = fma(pe, e, s2);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      const double mm = s1 / s0;
+      a.m1[rr] = c + mm;
+      a.v[rr] = s2 / s0 - mm * mm;
+    }
+  }
+}
+
 // Walk NC16 chunks of 16 TMEM columns with the next chunk's tcgen05.ld in
 // flight while the current one is processed (two register buffers).
 template <int NC16, class F>
@@ -628,11 +855,12 @@ struct TileWalk {
 #ifndef QEM_FWD_FS
 #define QEM_FWD_FS 8
 #endif
+template <int D>
 struct FwdTcL {
   static constexpr int SA = QEM_FWD_SA;                              // row-block stages
-  static constexpr uint32_t A_C = 128 * kTcRowCBytes;                // 12 KB
-  static constexpr uint32_t A_STAGE = A_C + 128 * kTcRowXBytes;      // 16 KB
-  static constexpr uint32_t B_STAGE = 256 * kTcColBytes;             // 32 KB
+  static constexpr uint32_t A_C = 128 * TcGeo<D>::CB;                // 12 KB (split) / 4 KB (compact)
+  static constexpr uint32_t A_STAGE = A_C + 128 * kTcRowXBytes;      // 16 KB / 8 KB
+  static constexpr uint32_t B_STAGE = 256 * TcGeo<D>::COL;           // 32 KB / 16 KB
   static constexpr uint32_t P_STAGE = 256 * 4;                       // P of the block's columns
   static constexpr size_t a() { return 0; }
   static constexpr size_t b() { return a() + SA * A_STAGE; }
@@ -653,7 +881,8 @@ constexpr int kFwdThreads = kTcThreads + 32 * kFwdAuxWarps;
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  using L = FwdTcL;
+  using L = FwdTcL<D>;
+  using G = TcGeo<D>;
   constexpr int SA = L::SA;
   const int K = a.K, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NB = K / 256, RB = K / 128, TPG = NB * RB;
@@ -722,7 +951,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
           const int st = (int)(J & 1);
           if (J >= 2) mbar_wait(&b_empty[st], (uint32_t)(((J >> 1) - 1) & 1));
           mbar_expect_tx(&b_full[st], L::B_STAGE + L::P_STAGE);
-          tma_bulk_g2s(s_b + st * L::B_STAGE, colop + ((size_t)i * K + (size_t)cb * 256) * kTcColBytes, L::B_STAGE,
+          tma_bulk_g2s(s_b + st * L::B_STAGE, colop + ((size_t)i * K + (size_t)cb * 256) * G::COL, L::B_STAGE,
                        &b_full[st]);
           tma_bulk_g2s(s_p + st * 256, a.ws.colaux + (size_t)i * 2 * K + (size_t)cb * 256, L::P_STAGE, &b_full[st]);
         }
@@ -749,7 +978,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
         if (T >= 2) mbar_wait(&t_empty[tb], (uint32_t)(((T >> 1) - 1) & 1));
         tc_fence_after();
         const uint32_t A = smem_u32(s_a + sa * L::A_STAGE), B = smem_u32(s_b + (J & 1) * L::B_STAGE);
-        umma_tile7(tmem + (uint32_t)tb * 256, A, 768, B, 1024, A + L::A_C, 256, B + 768, 1024, idesc);
+        umma_tile<D>(tmem + (uint32_t)tb * 256, A, 8 * G::CB, B, 8 * G::COL, A + L::A_C, 256, B + 8 * G::CB,
+                     8 * G::COL, idesc);
         umma_commit(&t_full[tb]);
         umma_commit(&a_empty[sa]);
         if (rb == RB - 1) umma_commit(&b_empty[J & 1]);
@@ -902,10 +1132,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
 // ----------------------------------------------------------------- backward
 constexpr int kBwdAuxWarps = 2;  // per-group row-slab builders of the backward
 
+template <int D>
 struct BwdTcL {
   static constexpr int SB = 3;                                  // row-block stages
-  static constexpr uint32_t A_STAGE = 128 * kTcColBytes;        // 16 KB: 128 columns
-  static constexpr uint32_t B_STAGE = 256 * kTcRowCBytes;       // 24 KB: 256 rows of Eb (k*-differenced)
+  static constexpr uint32_t A_STAGE = 128 * TcGeo<D>::COL;      // 16 KB / 8 KB: 128 columns
+  static constexpr uint32_t B_STAGE = 256 * TcGeo<D>::CB;       // 24 KB / 8 KB: 256 rows of Eb (k*-differenced)
   static constexpr size_t a() { return 0; }
   static constexpr size_t b() { return a() + 2 * A_STAGE; }
   static constexpr size_t wp() { return b() + SB * B_STAGE; }            // [2][4][128] float
@@ -1138,9 +1369,11 @@ __device__ void bwd_bx(const TLArgs& a, int64_t i, unsigned char* bx, int atid) 
   fence_proxy_async();  // generic-proxy SMEM writes -> visible to the tensor core (async proxy)
 }
 
+template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  using L = BwdTcL;
+  using L = BwdTcL<D>;
+  using G = TcGeo<D>;
   constexpr int SB = L::SB;
   const int K = a.K, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int CB = K / 128, RB = K / 256, TPG = CB * RB;
@@ -1205,7 +1438,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
           const int st = (int)(J & 1);
           if (J >= 2) mbar_wait(&a_empty[st], (uint32_t)(((J >> 1) - 1) & 1));
           mbar_expect_tx(&a_full[st], L::A_STAGE);
-          tma_bulk_g2s(s_a + st * L::A_STAGE, colop + ((size_t)i * K + (size_t)cb * 128) * kTcColBytes, L::A_STAGE,
+          tma_bulk_g2s(s_a + st * L::A_STAGE, colop + ((size_t)i * K + (size_t)cb * 128) * G::COL, L::A_STAGE,
                        &a_full[st]);
         }
         const int sb = (int)(T % SB);
@@ -1230,7 +1463,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_backward_tc(TLArgs a) {
         tc_fence_after();
         const uint32_t A = smem_u32(s_a + (J & 1) * L::A_STAGE), B = smem_u32(s_b + sb * L::B_STAGE);
         const uint32_t BX = smem_u32(s_bx + (size_t)(j & 1) * K * kTcRowXBytes + (size_t)rb * 256 * kTcRowXBytes);
-        umma_tile7(tmem + (uint32_t)tb * 256, A, 1024, B, 768, A + 768, 1024, BX, 256, idesc);
+        umma_tile<D>(tmem + (uint32_t)tb * 256, A, 8 * G::COL, B, 8 * G::CB, A + 8 * G::CB, 8 * G::COL, BX, 256,
+                     idesc);
         umma_commit(&t_full[tb]);
         umma_commit(&b_empty[sb]);
         if (rb == RB - 1) umma_commit(&a_empty[J & 1]);

@@ -619,8 +619,9 @@ static KernelFn fwd_fn(int rp) {
 }
 template <int D>
 static KernelFn prep_fn(int obs, bool tc) {
-  if constexpr (D == 1)
-    if (obs == QEM_OBS_GAUSS) return k_colprep<D, QEM_OBS_GAUSS, false>;
+  if constexpr (D == 1) {
+    if (obs == QEM_OBS_GAUSS) return tc ? k_colprep_tc1<QEM_OBS_GAUSS> : k_colprep<D, QEM_OBS_GAUSS, false>;
+  }
   if constexpr (D >= 8 && D <= kTcD) {
     if (tc) return k_colprep_tc<D, QEM_OBS_BERNOULLI_LOGIT>;
   }
@@ -642,7 +643,9 @@ static int occupancy(KernelFn f, int nt, size_t sm) {
 template <int D>
 static int prep_threads(int) { return 32 * FwdLayout<D>::PREP_WARPS; }
 template <int D>
-static size_t prep_smem(int K, int J, bool tc) { return tc ? PrepTc::bytes(K, J) : FwdLayout<D>::prep_bytes(K, J); }
+static size_t prep_smem(int K, int J, bool tc) {
+  return tc ? (TcGeo<D <= kTcD ? D : 16>::COMPACT ? 0 : PrepTc::bytes(K, J)) : FwdLayout<D>::prep_bytes(K, J);
+}
 template <int D>
 static int prep_threads_tc(int K, bool tc) { return tc ? 32 * PrepTc::WARPS : prep_threads<D>(K); }
 
@@ -652,10 +655,12 @@ static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, in
   int of, ob;
   if (tc) {
     if constexpr (D <= kTcD) {
-      of = occupancy(k_forward_tc<D>, kFwdThreads, FwdTcL::bytes(K));
-      ob = occupancy(k_backward_tc, kBwdThreads, BwdTcL::bytes(K));
-      occupancy(k_bwd_cols_tc<D>, GroupStage::THREADS, GroupStage::bytes(K, D));  // set the dynamic-SMEM attributes
-      occupancy(k_moments_tc<D>, GroupStage::THREADS, GroupStage::bytes(K, D));
+      of = occupancy(k_forward_tc<D>, kFwdThreads, FwdTcL<D>::bytes(K));
+      ob = occupancy(k_backward_tc<D>, kBwdThreads, BwdTcL<D>::bytes(K));
+      if constexpr (!TcGeo<D>::COMPACT) {  // set the dynamic-SMEM attributes of the TMA-staged group kernels
+        occupancy(k_bwd_cols_tc<D>, GroupStage::THREADS, GroupStage::bytes(K, D));
+        occupancy(k_moments_tc<D>, GroupStage::THREADS, GroupStage::bytes(K, D));
+      }
     } else {
       of = ob = 1;
     }
@@ -694,7 +699,7 @@ static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st
   if (e != cudaSuccess) return e;
   if (c->ev[0]) cudaEventRecord((cudaEvent_t)c->ev[0], st);
   if (tc)
-    k_forward_tc<(D <= kTcD ? D : 1)><<<c->grid_fwd, kFwdThreads, FwdTcL::bytes(K), st>>>(a);
+    k_forward_tc<(D <= kTcD ? D : 1)><<<c->grid_fwd, kFwdThreads, FwdTcL<(D <= kTcD ? D : 1)>::bytes(K), st>>>(a);
   else
     fwd_fn<D>(rp)<<<c->grid_fwd, rows_threads(K, rp), FwdLayout<D>::bytes(K, a.J), st>>>(a);
   if (c->ev[1]) cudaEventRecord((cudaEvent_t)c->ev[1], st);
@@ -717,17 +722,23 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   const bool tc = D <= kTcD && c->tc;
   constexpr int DT = D <= kTcD ? D : 1;
   if (tc) {
-    k_bwd_cols_tc<DT><<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K, DT), st>>>(a);
+    if constexpr (TcGeo<DT>::COMPACT)
+      k_bwd_cols_warp<DT><<<c->grid_prep, 256, 0, st>>>(a);
+    else
+      k_bwd_cols_tc<DT><<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K, DT), st>>>(a);
     c->launches += 1;
   }
   if (c->ev[2]) cudaEventRecord((cudaEvent_t)c->ev[2], st);
   if (tc)
-    k_backward_tc<<<c->grid_bwd, kBwdThreads, BwdTcL::bytes(K), st>>>(a);
+    k_backward_tc<DT><<<c->grid_bwd, kBwdThreads, BwdTcL<DT>::bytes(K), st>>>(a);
   else
     bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
   if (c->ev[3]) cudaEventRecord((cudaEvent_t)c->ev[3], st);
   if (tc) {
-    k_moments_tc<DT><<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K, DT), st>>>(a);
+    if constexpr (TcGeo<DT>::COMPACT)
+      k_moments_warp<DT><<<c->grid_prep, 256, 0, st>>>(a);
+    else
+      k_moments_tc<DT><<<c->grid_stage, GroupStage::THREADS, GroupStage::bytes(K, DT), st>>>(a);
     c->launches += 1;
   }
   c->launches += 2;
@@ -745,12 +756,16 @@ int tl_supported_d(int d) {
 
 int tl_use_tc(const qem_model_desc* d) {
   static const int off = getenv("QEM_NO_TC") != nullptr;  // tuning / comparison override
-  // tensor-core pair kernels: 8 <= d <= 16 (contraction zero-padded to 16), K a multiple of 256,
-  // Bernoulli-logit observations.  Below d = 8 the FFMA tiles win: the 128-byte column operand
-  // would be mostly padding, and at config 4's K = 256 its HBM stream (3.3 GB per pass) would
-  // rival the pair work.
-  return !off && d->d >= 8 && d->d <= kTcD && tl_supported_d(d->d) && d->obs_kind == QEM_OBS_BERNOULLI_LOGIT &&
-         d->K % 256 == 0 && d->K <= QEM_MAX_K;
+  // tensor-core pair kernels, K a multiple of 256: 8 <= d <= 16 with Bernoulli-logit observations
+  // (split layout, contraction zero-padded to 16), or d = 1 with Gaussian ones (compact layout).
+  // For 2 <= d < 8 the FFMA tiles stay: the split layout's 128-byte column operand would be mostly
+  // padding.
+  static const int off1 = getenv("QEM_NO_TC1") != nullptr;  // the compact (d = 1) path only
+  if (off || d->K % 256 != 0 || d->K > QEM_MAX_K) return 0;
+  // d = 1 with Gaussian observations (config 4): the compact layout, one c-region MMA + the extra
+  // slab per tile and a 64-byte column operand (compact path)
+  if (d->d == 1) return !off1 && d->obs_kind == QEM_OBS_GAUSS;
+  return d->d >= 8 && d->d <= kTcD && tl_supported_d(d->d) && d->obs_kind == QEM_OBS_BERNOULLI_LOGIT;
 }
 
 void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb, int* gp) {

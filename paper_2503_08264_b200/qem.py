@@ -183,6 +183,11 @@ class QEM:
         b.trace_len = self.trace.numel()
         b.plate_sum = self.plate_sum.data_ptr()
         b.log_pe_fresh = self.log_pe_fresh.data_ptr()
+        bank = getattr(self, "_eps_bank", None)
+        if bank is not None:
+            for l, t in enumerate(bank):
+                b.eps_bank[l] = t.data_ptr()
+            b.eps_bank_len = bank[0].shape[0]
         check(lib().qem_bind(self.ctx, ctypes.byref(b)), "qem_bind")
         self._bound = True
 
@@ -202,6 +207,13 @@ class QEM:
         """Samples per level [inst*dims][K] fp32 host arrays (bypasses the sampler)."""
         for lv, zz in zip(self.levels, self._local(z)):
             lv["z"].copy_(torch.as_tensor(np.asarray(zz, np.float32)).reshape(lv["z"].shape))
+
+    def _bank_slices(self, nlev):
+        """Row slices of each level's eps arrays that belong to this context's shard."""
+        out = [slice(None)] * nlev
+        if self.m.family == synth.FAMILY_TWO_LEVEL and nlev > 1:
+            out[1] = slice(self.g_begin * self.m.d, self.g_end * self.m.d)
+        return out
 
     def _local(self, per_level):
         out = list(per_level)
@@ -285,9 +297,22 @@ class QEM:
     def mstep(self, t: int, stream=None) -> None:
         check(lib().qem_mstep(self.ctx, t, _stream(stream)), "qem_mstep")
 
-    def iterate(self, t0: int, T: int, seed: int, use_graph: bool = True, stream=None) -> None:
+    def iterate(self, t0: int, T: int, seed: int, use_graph: bool = True, stream=None, eps_bank=None) -> None:
+        """qem_iterate: T QEM iterations from t0.  eps_bank (parity mode): per level a host array
+        [T][instances*dims][K] of N(0,1) draws (this context's shard for level 1) used instead of
+        Philox; None restores Philox sampling."""
+        rebind = False
         if T > self.trace.numel():
             self.trace = torch.zeros(T, dtype=torch.float64, device=self.device)
+            rebind = True
+        if eps_bank is not None:
+            self._eps_bank = [torch.as_tensor(np.ascontiguousarray(np.asarray(e, np.float32)[:, sl])).to(self.device)
+                              for e, sl in zip(eps_bank, self._bank_slices(len(eps_bank)))]
+            rebind = True
+        elif getattr(self, "_eps_bank", None) is not None:
+            self._eps_bank = None
+            rebind = True
+        if rebind:
             self.bind()
         check(lib().qem_iterate(self.ctx, t0, T, seed, int(use_graph), _stream(stream)), "qem_iterate")
 

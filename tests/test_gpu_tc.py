@@ -1,4 +1,6 @@
-"""GPU parity of the tcgen05 tensor-core pair kernels (d = 16, K % 256 == 0) vs the oracle.
+"""GPU parity of the tcgen05 tensor-core pair kernels (K % 256 == 0) vs the oracle: the split layout
+(d = 16, Bernoulli observations, config 5's shape) and the compact layout (d = 1, Gaussian
+observations, config 4's shape).
 
 The tensor-core path has its own operand layouts,
 warp-specialised pipeline and per-group tile modes, so it gets its own sweep:
@@ -36,21 +38,22 @@ CASES = {
     "n60_K256_post0.0004": (60, 256, 0.0004),
 }
 
-_seen_modes = np.zeros(6, np.int64)
+_seen_modes = {4: np.zeros(6, np.int64), 5: np.zeros(6, np.int64)}
 
 
 @pytest.mark.parametrize("case", list(CASES))
-def test_tc_estep_parity(case):
+@pytest.mark.parametrize("cid", [5, 4], ids=["split_d16", "compact_d1"])
+def test_tc_estep_parity(cid, case):
     from paper_2503_08264_b200.qem import QEM
     n, K, shrink = CASES[case]
-    m = synth.config(5, n=n, K=K)
+    m = synth.config(cid, n=n, K=K)
     data = synth.make_data(m)
     q = synth.random_q(m, 11) if shrink is None else posterior_like_q(m, data, seed=7, shrink=shrink)
     _, _, eps, _ = make_case(m, q=q)
     z = [orc.sample(qm, qv, e) for (qm, qv), e in zip(q, eps)]
     ref = orc.estep(m, z, q, data)
     g = QEM(m)
-    assert g.pair_path() == 1, "d=16, K%256==0 must run the tensor-core kernels"
+    assert g.pair_path() == 1, "d=16 / d=1 with K%256==0 must run the tensor-core kernels"
     g.set_data(data)
     g.set_q(q)
     g.sample_q(eps=eps)
@@ -60,7 +63,7 @@ def test_tc_estep_parity(case):
     dg, c = g.messages()
     flags, _ = g.read_flags()
     g.close()
-    _seen_modes[:] += hist
+    _seen_modes[cid][:] += hist
     assert hist.sum() == n, hist  # one mode per group
     check_estep(m, out, ref, note=f"tc/{case}")
     assert flags & 2 == 0
@@ -77,9 +80,37 @@ def test_tc_estep_parity(case):
     assert err.max() <= 1.0, (case, float(err.max()))
 
 
-def test_tc_modes_covered():
+@pytest.mark.parametrize("cid", [5, 4])
+def test_tc_modes_covered(cid):
     """The sweep above must have exercised the online mode and the polynomial modes."""
-    if _seen_modes.sum() == 0:
+    seen = _seen_modes[cid]
+    if seen.sum() == 0:
         pytest.skip("run with the parity sweep")
-    assert _seen_modes[5] > 0, _seen_modes
-    assert (_seen_modes[:5] > 0).sum() >= 1, _seen_modes
+    assert seen[5] > 0, seen
+    assert (seen[:5] > 0).sum() >= 1, seen
+
+
+def test_ffma_path_d1_K256_still_matches():
+    """QEM_NO_TC1=1 keeps config 4's shape on the FFMA tiles (K = 256, d = 1): parity in a fresh
+    process (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from helpers import make_case, posterior_like_q\n"
+        "from oracle import oracle as orc\n"
+        "from paper_2503_08264_b200 import synth\n"
+        "from paper_2503_08264_b200.qem import QEM\n"
+        "from test_gpu_parity import check_estep\n"
+        "m = synth.config(4, n=700, K=256); data = synth.make_data(m)\n"
+        "for q in (synth.random_q(m, 11), posterior_like_q(m, data, seed=7, shrink=1.0)):\n"
+        "    _, _, eps, z = make_case(m, q=q)\n"
+        "    g = QEM(m); assert g.pair_path() == 0\n"
+        "    g.set_data(data); g.set_q(q); g.sample_q(eps=eps); g.estep(); out = g.result(); g.close()\n"
+        "    check_estep(m, out, orc.estep(m, z, q, data), note='ffma d1 K256')\n"
+        "print('FFMA_OK')\n" % (os.path.dirname(here), here))
+    env = dict(os.environ, QEM_NO_TC1="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert "FFMA_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
