@@ -10,11 +10,16 @@ namespace qem {
 constexpr double kLn2Pi = 1.8378770664093454835606594728112;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kLog2eD = 1.4426950408889634074;
+constexpr double kLn2D = 0.69314718055994530942;
 
 __device__ __forceinline__ float ex2(float x) {
+#ifdef QEM_EXACT_EX2  // diagnostics: the libm 2^x instead of the SFU's ex2.approx
+  return exp2f(x);
+#else
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+#endif
 }
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }

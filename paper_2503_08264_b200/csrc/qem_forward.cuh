@@ -83,7 +83,7 @@ __device__ __forceinline__ float2 max2(float2 a, float2 b) { return make_float2(
 
 template <int D, int RP, int N>
 __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2 (&al)[RP], const float2 (&ga)[RP],
-                                          const float2 (&cc)[RP][D], float (&dgv)[2 * RP]) {
+                                          const float2 (&cc)[RP][D], double (&dgv)[2 * RP]) {
   constexpr int CS = pad4(D + 3);
   float2 acc[RP];
 #pragma unroll
@@ -97,8 +97,8 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
   }
 #pragma unroll
   for (int p = 0; p < RP; ++p) {
-    dgv[2 * p] = log1pf(acc[p].x);
-    dgv[2 * p + 1] = log1pf(acc[p].y);
+    dgv[2 * p] = log1p((double)acc[p].x);  // fp64 logs: the fp32 ones' ~1-ulp errors are not zero-mean,
+    dgv[2 * p + 1] = log1p((double)acc[p].y);  // and they add up coherently over the groups' plate sum
   }
 }
 
@@ -110,7 +110,7 @@ constexpr float kLazy = 0.0f;
 
 template <int D, int RP>
 __device__ __forceinline__ void tile_online(const float* col, int Kp, const float2 (&al)[RP], const float2 (&ga)[RP],
-                                            const float2 (&cc)[RP][D], float (&dgv)[2 * RP]) {
+                                            const float2 (&cc)[RP][D], double (&dgv)[2 * RP]) {
   constexpr int CS = pad4(D + 3);
   constexpr int CH = FwdLayout<D>::CH;
   float2 mr[RP], ac[RP];
@@ -154,8 +154,8 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
   }
 #pragma unroll
   for (int p = 0; p < RP; ++p) {
-    dgv[2 * p] = mr[p].x + logf(ac[p].x);
-    dgv[2 * p + 1] = mr[p].y + logf(ac[p].y);
+    dgv[2 * p] = (double)mr[p].x + log((double)ac[p].x);
+    dgv[2 * p + 1] = (double)mr[p].y + log((double)ac[p].y);
   }
 }
 
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
     mbar_wait(&bar[st], (uint32_t)((j >> 1) & 1));
     const float* col = reinterpret_cast<const float*>(smem + (st ? sbytes : 0));
 
-    float dgv[2 * RP];
+    double dgv[2 * RP];
     switch (md) {
       case 0: tile_poly<D, RP, 3>(col, Kp, az, ga, cc, dgv); break;
       case 1: tile_poly<D, RP, 4>(col, Kp, az, ga, cc, dgv); break;
@@ -443,8 +443,8 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
 #pragma unroll
     for (int q = 0; q < 2 * RP; ++q) {
       if (kid[q] >= 0) {
-        const double dgd = ald[q] + (double)dgv[q];
-        a.ws.hmsg[(size_t)i * K + kid[q]] = dgv[q];
+        const double dgd = ald[q] + dgv[q];
+        a.ws.hmsg[(size_t)i * K + kid[q]] = (float)dgv[q];
         a.ws.dg[(size_t)i * K + kid[q]] = (float)dgd;
         G[q] += dgd;
       }

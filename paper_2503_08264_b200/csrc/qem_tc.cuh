@@ -218,7 +218,8 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
     if constexpr (TcGeo<D>::COMPACT) {
       if (a.tc) {  // Eb and Eg both in the compact c-region; the per-group slab's gamma stays 0
         uint4 c0, c1;
-        compact_row((float)((ek * (double)a.z_root[k] - es * (double)a.z_root[ks]) * kLog2eD),
+        const double zr0 = a.ws.ref->mu_ref[0];
+        compact_row((float)((ek * ((double)a.z_root[k] - zr0) - es * ((double)a.z_root[ks] - zr0)) * kLog2eD),
                     (float)(-0.5 * (ek - es) * kLog2eD), c0, c1);
         unsigned char* rb = reinterpret_cast<unsigned char*>(a.ws.rowop_b);
         *reinterpret_cast<uint4*>(rb + TcGeo<D>::row_off(k, 0)) = c0;
@@ -231,7 +232,9 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
         float v[kTcD];
 #pragma unroll
         for (int r = 0; r < kTcD; ++r)
-          v[r] = r < D ? (float)((ek * (double)a.z_root[r * K + k] - es * (double)a.z_root[r * K + ks]) * kLog2eD) : 0.f;
+          v[r] = r < D ? (float)((ek * ((double)a.z_root[r * K + k] - (double)a.ws.ref->mu_ref[r]) -
+                                  es * ((double)a.z_root[r * K + ks] - (double)a.ws.ref->mu_ref[r])) * kLog2eD)
+                       : 0.f;
         store_row_split16(reinterpret_cast<unsigned char*>(a.ws.rowop_b), k, v);
         a.ws.bgam[k] = (float)(-0.5 * (ek - es) * kLog2eD);
         continue;
@@ -249,24 +252,27 @@ __global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
   const int K = a.K;
   unsigned char* rc = reinterpret_cast<unsigned char*>(a.ws.rowop);
   unsigned char* rx = reinterpret_cast<unsigned char*>(a.ws.rowop_x);
+  constexpr int RS = pad4(D + 3);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
-    const float* fc = a.ws.fwd_coef + (size_t)k * (D + 2);
+    // log2e c_k, log2e gamma_k rounded once from fp64 (k_root_prep's bwd_table row; coef_d holds the
+    // same values in natural units for the aux merge)
+    const float* bt = a.ws.bwd_table + (size_t)k * RS;
     if constexpr (TcGeo<D>::COMPACT) {
       uint4 c0, c1;
-      compact_row(fc[2] * kLog2e, fc[1] * kLog2e, c0, c1);
+      compact_row(bt[2], bt[1], c0, c1);
       *reinterpret_cast<uint4*>(rc + TcGeo<D>::row_off(k, 0)) = c0;
       *reinterpret_cast<uint4*>(rc + TcGeo<D>::row_off(k, 8)) = c1;
-      extra_row(0.f, 1.f, 0.f, c0, c1);  // forward: lP on, no row constant, gamma in the c-region
+      extra_row(0.f, 0.f, 0.f, c0, c1);  // forward: no row constant, lP off (added by the epilogue), gamma in the c-region
       *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 0)) = c0;
       *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 8)) = c1;
       continue;
     }
     float v[kTcD];  // contraction zero-padded to 16 dims
 #pragma unroll
-    for (int r = 0; r < kTcD; ++r) v[r] = r < D ? fc[2 + r] * kLog2e : 0.f;
+    for (int r = 0; r < kTcD; ++r) v[r] = r < D ? bt[2 + r] : 0.f;
     store_row_split16(rc, k, v);
     uint4 c0, c1;
-    extra_row(fc[1] * kLog2e, 1.f, 0.f, c0, c1);  // forward: lP on, no row constant
+    extra_row(bt[1], 0.f, 0.f, c0, c1);  // forward: no row constant, lP off (added by the epilogue)
     *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 0)) = c0;
     *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 8)) = c1;
   }
@@ -310,7 +316,7 @@ struct PrepTc {
   static constexpr int ZS_FLOATS = 2 * 2 * kTcD * 32;  // z ring: [stage][half][r][32 columns]
   static constexpr size_t ZS_BYTES = ZS_FLOATS * 4;
   __host__ __device__ static size_t warp_bytes(int K, int J) {
-    size_t b = 3 * kTcD * 8 + kTcD * 4 + (size_t)((J + 1) / 2) * kTcD * 8 + ZS_BYTES;
+    size_t b = 3 * kTcD * 8 + 2 * kTcD * 4 + (size_t)((J + 1) / 2) * kTcD * 8 + ZS_BYTES;
     return (b + 15) & ~(size_t)15;
   }
   __host__ __device__ static size_t bytes(int K, int J) { return WARPS * warp_bytes(K, J); }
@@ -333,7 +339,8 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
   double* qm = reinterpret_cast<double*>(wb);                      // [D]  m_i
   double2* qab = reinterpret_cast<double2*>(qm + kTcD);            // [D]  {alpha_r, beta_r}
   float* qmf = reinterpret_cast<float*>(qab + kTcD);               // [D]  m_i (fp32, exact: R22)
-  float2* xp = reinterpret_cast<float2*>(qmf + kTcD);              // [(J+1)/2][D] {x_2p, x_2p+1} as 0/1
+  float* u0f = qmf + kTcD;                                         // [D]  u0_i = m_i - mu_ref (fp32)
+  float2* xp = reinterpret_cast<float2*>(u0f + kTcD);              // [(J+1)/2][D] {x_2p, x_2p+1} as 0/1
   const int Jh = (J + 1) / 2;
   float* zs = reinterpret_cast<float*>(xp + (size_t)Jh * kTcD);    // z ring (PrepTc::ZS_FLOATS)
   // z of 32 column pairs {kc, kc + K/2} of group g into ring stage st: LDGSTS, so the loads of
@@ -389,6 +396,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
       const double m = a.q_m[i * D + lane], v = a.q_v[i * D + lane], dl = m - (double)mref_l;
       qm[lane] = m;
       qmf[lane] = (float)m;
+      u0f[lane] = (float)m - mref_l;
       qab[lane] = make_double2(0.5 / v - 0.5 * e_ref, (double)yxi - e_ref * dl);
       ci = 0.5 * (kLn2Pi + log(v)) - 0.5 * e_ref * dl * dl + (double)yxi * m;
     }
@@ -403,9 +411,10 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
       const volatile double* qmv = qm;
       const volatile double2* qabv = qab;
       const volatile float* qmfv = qmf;
+      const volatile float* u0fv = u0f;
       double quad = Ci;
       // column operand re-centred on the group's Q mean: w = z - m_i and
-      // S = |w|^2 + 2 m_i . w (so D_k(z) = alpha'_ik + c0_k . w + gamma_k S)
+      // S = |w|^2 + 2 u0_i . w, u0_i = m_i - mu_ref (so D_k(z) = alpha'_ik + c_k . w + gamma_k S)
       float W2 = 0.f, mw = 0.f;
       float wv[kTcD];
 #pragma unroll
@@ -418,7 +427,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
           const float m = qmfv[r];
           wv[r] = zr[r] - m;
           W2 = fmaf(wv[r], wv[r], W2);
-          mw = fmaf(m, wv[r], mw);
+          mw = fmaf(u0fv[r], wv[r], mw);
         } else {
           wv[r] = 0.f;  // zero-padded contraction
         }
@@ -531,7 +540,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     // tile mode: bound on |D'_k(k')| = |c'_k . w + gamma_k |w|^2|, c' = c0 + 2 gamma m_i
     float u0[D];
 #pragma unroll
-    for (int r = 0; r < D; ++r) u0[r] = (float)qm[r];
+    for (int r = 0; r < D; ++r) u0[r] = u0f[r];
     const float wmax = sqrtf(W2max);
     float tb = 0.f;
 #pragma unroll 4  // fwd_coef rows stream from L2: keep several rows' loads in flight
@@ -560,11 +569,15 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
       for (int u = 0; u < 8; ++u) {
         const int kc = kb + 32 * u;
         if (kc >= K) break;
-        const float lp = (float)(tb4[u] - M - logS);
-        aux[kc] = expf(lp);  // (ln P itself travels in the column operand's lP slots)
+        const double lpd = tb4[u] - M - logS;
+        // the forward's per-column weight: P (polynomial modes) or log2e ln P (online mode), which the
+        // epilogue ADDS to the MMA's D' in fp32 (round to nearest).  Inside the MMA the tensor core's
+        // accumulation (aligned to the largest product, truncated) would bias every pair by ~3e-8 |lP|
+        // toward zero -- upward, coherently over the groups' plate sum (tools/tc_bias.cu).  log2e ln P
+        // is rounded once from fp64 (the fp32 log2e would scale it by 1 - 1.3e-8: the same kind of bias).
+        aux[kc] = md == 5 ? (float)(lpd * kLog2eD) : expf((float)lpd);
         uint4 c0, c1;
-        // ln P joins the MMA only in the online mode; the polynomial modes need D' alone
-        extra_col(0.f, md == 5 ? lp * kLog2e : 0.f, c0, c1);
+        extra_col(0.f, 0.f, c0, c1);  // lP slots zero in the forward (the backward writes L* there)
         *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 56)) = c1;  // chunk 7: 1 lP0 lP1 lP2 0...
       }
     }
@@ -606,6 +619,7 @@ __global__ void __launch_bounds__(256) k_colprep_tc1(TLArgs a) {
     sx = warp_sum(sx);
     sxx = warp_sum(sxx);
     const float mf = a.q_m[i];
+    const float u0f = mf - (float)mref;  // u0_i = m_i - mu_ref (the columns' S = w^2 + 2 u0 w)
     const double m = mf, v = a.q_v[i];
     const double lqc = -0.5 * (kLn2Pi + log(v)), iv2 = 0.5 / v;
     unsigned char* cop = colop + (size_t)i * K * G::COL;
@@ -629,7 +643,7 @@ __global__ void __launch_bounds__(256) k_colprep_tc1(TLArgs a) {
       }
       const float w = zf - mf, W2 = w * w;
       uint4 c0, c1;
-      compact_col(w, fmaf(2.f, mf * w, W2), c0, c1);
+      compact_col(w, fmaf(2.f, u0f * w, W2), c0, c1);
       *reinterpret_cast<uint4*>(cop + G::col_off(kc, 0)) = c0;
       *reinterpret_cast<uint4*>(cop + G::col_off(kc, 8)) = c1;
       extra_col(0.f, 0.f, c0, c1);  // chunk 0: [0 0 0 0 0 0 1 1]; chunk 1 (1, lP) below
@@ -643,7 +657,7 @@ __global__ void __launch_bounds__(256) k_colprep_tc1(TLArgs a) {
     float tb = 0.f;
     for (int k = lane; k < K; k += 32) {
       const float g = a.ws.fwd_coef[(size_t)k * 3 + 1], c = a.ws.fwd_coef[(size_t)k * 3 + 2];
-      tb = fmaxf(tb, fabsf(fmaf(2.f * g, mf, c)) * wmax + fabsf(g) * W2max);
+      tb = fmaxf(tb, fabsf(fmaf(2.f * g, u0f, c)) * wmax + fabsf(g) * W2max);
     }
     tb = warp_maxf(tb);
     const int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
@@ -651,10 +665,10 @@ __global__ void __launch_bounds__(256) k_colprep_tc1(TLArgs a) {
     __syncwarp();
 #pragma unroll 4
     for (int kc = lane; kc < K; kc += 32) {
-      const float lp = (float)(tref[kc] - M - logS);  // this lane's own store above
-      aux[kc] = expf(lp);
+      const double lpd = tref[kc] - M - logS;  // this lane's own store above
+      aux[kc] = md == 5 ? (float)(lpd * kLog2eD) : expf((float)lpd);  // P or log2e ln P (see k_colprep_tc)
       uint4 c0, c1;
-      extra_col(0.f, md == 5 ? lp * kLog2e : 0.f, c0, c1);
+      extra_col(0.f, 0.f, c0, c1);  // lP slots zero in the forward (the backward writes L* there)
       *reinterpret_cast<uint4*>(cop + G::col_off(kc, G::XKK + 8)) = c1;
     }
     if (lane == 0) {
@@ -770,9 +784,21 @@ __device__ __forceinline__ float2 expm1_2_poly(float2 x) {
 // Forward epilogue, online mode: (m, s) = running max / sum of 2^(v - m) over
 // v = c2.u + g2 U + lP (log2 domain; the row constant is added at the end).
 // The max is lazy: s is rescaled only when a chunk raises it.
-__device__ __forceinline__ void fwd_epi_online(uint32_t taddr, float& m, float& s) {
+__device__ __forceinline__ void fwd_epi_online(uint32_t taddr, const float* lpp, float& m, float& s) {
   uint32_t r[4][16];
   tmem_ld64(taddr, r);  // the thread's 64 columns of this tile, one TMEM round trip
+  // + log2e ln P of the columns (SMEM broadcast: every lane of the warp reads the same columns), in
+  // fp32 round to nearest (not inside the MMA: see k_colprep_tc)
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const float4 l = reinterpret_cast<const float4*>(lpp + q * 16)[c4];
+      r[q][4 * c4] = __float_as_uint(__uint_as_float(r[q][4 * c4]) + l.x);
+      r[q][4 * c4 + 1] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 1]) + l.y);
+      r[q][4 * c4 + 2] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 2]) + l.z);
+      r[q][4 * c4 + 3] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 3]) + l.w);
+    }
   // four independent FMNMX3 chains (one per 16-column load), then combined: a dependency chain
   // of 8 + 2 instead of 32
   float mq[4];
@@ -991,19 +1017,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
     const int atid = tid - kTcThreads;
     constexpr int NTA = 32 * kFwdAuxWarps;
     int md = 5;
-    double mi[D];  // the group's Q mean, converted once per group (not per row)
-    float M2 = 0.f;
+    double mi[D];  // u0_i = m_i - mu_ref of the group, formed once per group (not per row)
+    double M2 = 0.0;
     int64_t j = 0, i = blockIdx.x;
     int rb = 0;
     for (int64_t u = 0; u < ngroups * RB; ++u) {
       if (rb == 0) {
         md = a.ws.gmode[i];
-        M2 = 0.f;
+        M2 = 0.0;
 #pragma unroll
-        for (int r = 0; r < D; ++r) {
-          const float mf = a.q_m[i * D + r];
-          mi[r] = (double)mf;
-          M2 = fmaf(mf, mf, M2);
+        for (int r = 0; r < D; ++r) {  // u0_i = m_i - mu_ref, exact in fp64
+          mi[r] = (double)a.q_m[i * D + r] - (double)a.ws.ref->mu_ref[r];
+          M2 = fma(mi[r], mi[r], M2);
         }
         if (atid == 0) {
           atomicAdd(&a.cnt->mode_hist[md], 1ull);
@@ -1015,7 +1040,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
       const float2* fin = s_fin + st * 512;
       for (int rr = atid; rr < 128; rr += NTA) {
         const int k = rb * 128 + rr;
-        float h;
+        double h;
         if (md == 5) {
           float mx = -CUDART_INF_F;
 #pragma unroll
@@ -1026,20 +1051,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
             const float2 f = fin[c * 128 + rr];
             sm += f.y * ex2(f.x - mx);
           }
-          h = (mx + log2f(sm)) * 0.69314718055994531f;
+          // log2 -> natural units in fp64: the fp32 ln 2 (relative error 2.8e-9) times an h of tens
+          // would be a bias of ~1e-7 per group on every row but k_ref (whose h is 0), coherent over the
+          // plate sum (1e-4 in the root log-weights at 1000 groups)
+          h = ((double)mx + log2((double)sm)) * kLn2D;  // fp64 log: log2f's ~1-ulp error is not zero-mean
         } else {
           float sm = 0.f;
 #pragma unroll
           for (int c = 0; c < 4; ++c) sm += fin[c * 128 + rr].x;
-          h = log1pf(sm);
+          h = log1p((double)sm);
         }
-        // alpha'_ik = D_k(m_i) = alpha0_k + gamma_k |m_i|^2 + c0_k . m_i in fp64
-        const double* cd = a.ws.coef_d + (size_t)k * (D + 1);  // (gamma, c0[D]) as fp64: no conversions
-        double ap = fma(cd[0], (double)M2, a.ws.alpha_d[k]);
+        // alpha'_ik = D_k(m_i) = alpha_k + gamma_k |u0_i|^2 + c_k . u0_i in fp64 (u = z - mu_ref rows)
+        const double* cd = a.ws.coef_d + (size_t)k * (D + 1);  // (gamma, c[D]) as fp64: no conversions
+        double ap = fma(cd[0], M2, a.ws.alpha_d[k]);
 #pragma unroll
         for (int r = 0; r < D; ++r) ap = fma(cd[1 + r], mi[r], ap);
-        const double dgd = ap + (double)h;
-        a.ws.hmsg[(size_t)i * K + k] = h;  // re-centred message, the backward's row constant
+        const double dgd = ap + h;
+        a.ws.hmsg[(size_t)i * K + k] = (float)h;  // re-centred message, the backward's row constant
         a.ws.dg[(size_t)i * K + k] = (float)dgd;
         s_g[k] += dgd;
       }
@@ -1072,11 +1100,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
       mbar_wait(&t_full[T & 1], (uint32_t)((T >> 1) & 1));
       tc_fence_after();
       const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * 64) + ((uint32_t)(q * 32) << 16);
+      mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));  // P / log2e ln P of this block is in SMEM
+      const float* pp = s_p + (J & 1) * 256 + cq * 64;
       if (md == 5) {
-        fwd_epi_online(taddr, st0, st1);
+        fwd_epi_online(taddr, pp, st0, st1);
       } else {
-        mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));  // P of this block is in SMEM
-        const float* pp = s_p + (J & 1) * 256 + cq * 64;
         switch (md) {
           case 0: fwd_epi_poly<3, 4>(taddr, pp, st0); break;
           case 1: fwd_epi_poly<4, 4>(taddr, pp, st0); break;

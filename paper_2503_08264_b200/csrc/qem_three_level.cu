@@ -66,40 +66,36 @@ __global__ void k3_root_prep(THArgs a) {
   }
 }
 
-// L_ab(kab, kr): one thread per (ab, kab, kr).
-__global__ void k3_ltable(THArgs a) {
+// The two [ab][K][K] fp64 tables of the sub-plate contraction, one thread per entry e of each:
+//   L_ab(kab, kr)  (e = (ab K + kab) K + kr): the Poisson observation term;
+//   F_ab(ka, kab)  (e = (ab K + ka) K + kab): lnN(v_ab^kab; u_a^ka, sub_var) - log q(v_ab^kab)
+// (the logarithms once per entry, not once per root sample; read by k3_msub AND k3_wlevels, so the
+// backward's P_ab(kab | ka, kr) is built from the same operand as M_ab).
+__global__ void k3_tables(THArgs a) {
   const int K = a.K;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t tot = (int64_t)a.A * a.B * K * K;
   if (e >= tot) return;
-  const int kr = (int)(e % K);
-  const int kab = (int)((e / K) % K);
+  const int lo = (int)(e % K);
+  const int mid = (int)((e / K) % K);
   const int64_t ab = e / ((int64_t)K * K);
-  const double v = a.z_sub[ab * K + kab];
-  double ll = 0.0;
-  for (int j = 0; j < a.J; ++j) {
-    double eta = v;
-    const float* xj = a.x + (ab * a.J + j) * a.P;
-    for (int p = 0; p < a.P; ++p) eta += (double)a.z_root[(1 + p) * K + kr] * (double)xj[p];
-    const double y = (double)a.y[ab * a.J + j];
-    ll += log_pois(y, eta, lgamma(y + 1.0));
+  {  // L: kab = mid, kr = lo
+    const double v = a.z_sub[ab * K + mid];
+    double ll = 0.0;
+    for (int j = 0; j < a.J; ++j) {
+      double eta = v;
+      const float* xj = a.x + (ab * a.J + j) * a.P;
+      for (int p = 0; p < a.P; ++p) eta += (double)a.z_root[(1 + p) * K + lo] * (double)xj[p];
+      const double y = (double)a.y[ab * a.J + j];
+      ll += log_pois(y, eta, lgamma(y + 1.0));
+    }
+    a.ws.Lab[e] = ll;
   }
-  a.ws.Lab[e] = ll;
-}
-
-// M_ab(ka, kr) = lse_kab [F_ab(ka,kab) + L_ab(kab,kr)] - log K.
-// F_ab(ka, kab) = lnN(v_ab^kab; u_a^ka, sub_var) - log q(v_ab^kab): one thread per entry (the
-// logarithms once, not once per root sample)
-__global__ void k3_ftable(THArgs a) {
-  const int K = a.K;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)a.A * a.B * K * K) return;
-  const int kab = (int)(e % K);
-  const int ka = (int)((e / K) % K);
-  const int64_t ab = e / ((int64_t)K * K);
-  const int aa = (int)(ab / a.B);
-  const double v = a.z_sub[ab * K + kab];
-  a.ws.Fab[e] = lnN(v, (double)a.z_top[(int64_t)aa * K + ka], a.sub_var) - lnq(v, a.qs_m[ab], a.qs_v[ab]);
+  {  // F: ka = mid, kab = lo
+    const int aa = (int)(ab / a.B);
+    const double v = a.z_sub[ab * K + lo];
+    a.ws.Fab[e] = lnN(v, (double)a.z_top[(int64_t)aa * K + mid], a.sub_var) - lnq(v, a.qs_m[ab], a.qs_v[ab]);
+  }
 }
 
 __global__ void k3_msub(THArgs a) {
@@ -228,12 +224,10 @@ __global__ void k3_wlevels(THArgs a) {
   const int kab = (int)(f % K);
   const int64_t ab = f / K;
   const int aa = (int)(ab / a.B);
-  const double v = a.z_sub[ab * K + kab];
-  const double lq = lnq(v, a.qs_m[ab], a.qs_v[ab]);
   const double logK = log((double)K);
   double s = 0.0;
   for (int ka = lane; ka < K; ka += 32) {
-    const double F = lnN(v, (double)a.z_top[(int64_t)aa * K + ka], a.sub_var) - lq;
+    const double F = a.ws.Fab[(ab * K + ka) * K + kab];  // the operand M_ab was built from (k3_tables)
     for (int kr = 0; kr < K; ++kr) {
       const double W = a.ws.Ta[((int64_t)aa * K + kr) * K + ka];
       s += W * exp(F + a.ws.Lab[(ab * K + kab) * K + kr] - logK - a.ws.Mab[ab * K * K + (int64_t)ka * K + kr]);
@@ -331,11 +325,10 @@ cudaError_t th_forward(qem_ctx* c, cudaStream_t st) {
   THArgs a = make_args3(c);
   const int64_t KK = (int64_t)a.K * a.K, AB = (int64_t)a.A * a.B;
   k3_root_prep<<<1, 256, 0, st>>>(a);
-  k3_ltable<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
-  k3_ftable<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
+  k3_tables<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
   k3_msub<<<nblk(AB * KK, 128), 128, 0, st>>>(a);
   k3_top<<<nblk((int64_t)a.A * a.K * 32, 256), 256, 0, st>>>(a);
-  c->launches += 5;
+  c->launches += 4;
   return cudaGetLastError();
 }
 

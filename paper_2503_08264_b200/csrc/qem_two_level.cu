@@ -169,42 +169,33 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a, int phase) {
     float* fc = a.ws.fwd_coef + (size_t)k * CW;
     float* bt = a.ws.bwd_table + (size_t)k * RS;
     double alpha;
-    if (a.tc) {
-      // tensor-core path: origin-0 form D_k(z) = alpha0 + c0 . z + gamma |z|^2 with
-      // c0 = e_k mu_k - e_ref mu_ref, alpha0 = -(d/2) dlnv - (e_k |mu_k|^2 - e_ref |mu_ref|^2) / 2,
-      // so a group re-centres with its own mean alone
-      double mk2 = 0.0, mr2 = 0.0;
-      for (int r = 0; r < D; ++r) {
-        const double mk = (double)a.z_root[r * K + k], mr = (double)a.z_root[r * K + kref];
-        mk2 += mk * mk;
-        mr2 += mr * mr;
-        const double cr = ek * mk - e_ref * mr;
-        fc[2 + r] = (float)cr;
-        bt[2 + r] = (float)(cr * kLog2eD);
-      }
-      alpha = -0.5 * D * dlnv - 0.5 * (ek * mk2 - e_ref * mr2);
-    } else {
-      for (int r = 0; r < D; ++r) {
-        const double del = (double)a.z_root[r * K + k] - (double)a.z_root[r * K + kref];
-        dd += del * del;
-        const double cr = ek * del;
-        fc[2 + r] = (float)cr;
-        bt[2 + r] = (float)(cr * kLog2eD);
-      }
-      alpha = -0.5 * D * dlnv - 0.5 * ek * dd;
+    // u = z - mu_ref differenced rows D_k = alpha_k + gamma_k |u|^2 + c_k . u (both pair paths; the
+    // tensor-core columns carry S = |w|^2 + 2 u0_i . w with u0_i = m_i - mu_ref, so the fp32 rounding
+    // of c_k multiplies u, not z: it averages out over the groups instead of adding up coherently)
+    for (int r = 0; r < D; ++r) {
+      const double del = (double)a.z_root[r * K + k] - (double)a.z_root[r * K + kref];
+      dd += del * del;
+      const double cr = ek * del;
+      fc[2 + r] = (float)cr;
+      bt[2 + r] = (float)(cr * kLog2eD);
     }
+    alpha = -0.5 * D * dlnv - 0.5 * ek * dd;
     const double gamma = -0.5 * (ek - e_ref);
     fc[0] = (float)alpha;
     fc[1] = (float)gamma;
-    if (a.tc) {  // the same fp32 values, held as fp64 for the forward's aux merge
-      double* cd = a.ws.coef_d + (size_t)k * (D + 1);
-      cd[0] = (double)fc[1];
-#pragma unroll
-      for (int r = 0; r < D; ++r) cd[1 + r] = (double)fc[2 + r];
-    }
     a.ws.alpha_d[k] = alpha;
     bt[0] = (float)(alpha * kLog2eD);
     bt[1] = (float)(gamma * kLog2eD);
+    if (a.tc) {
+      // the tensor-core rows are these log2e-scaled fp32 values (one rounding from fp64, k_rowop_tc);
+      // the aux merge's alpha'_ik uses exactly the same coefficients back in natural units (fp64), so
+      // the MMA and the merge see one row function: a mismatch here (a second rounding of c log2e)
+      // would be a fixed per-row error times the group's E_P[w] -- coherent over the groups
+      double* cd = a.ws.coef_d + (size_t)k * (D + 1);
+      cd[0] = (double)bt[1] * kLn2D;
+#pragma unroll
+      for (int r = 0; r < D; ++r) cd[1 + r] = (double)bt[2 + r] * kLn2D;
+    }
     // f_root(k) = sum_r lnN(z_r; prior) - lnN(z_r; Q_root), the log-normalisers hoisted (s_qc)
     double f = 0.0;
     float zk[D + 1], qmk[D + 1];
