@@ -45,6 +45,13 @@ constexpr int kTcRowCBytes = kTcRowBytes;  // 96: c2 split (6 chunks)
 #define QEM_POLY_EXP_BWD 4
 #endif
 constexpr int kPolyExpFwd = QEM_POLY_EXP_FWD, kPolyExpBwd = QEM_POLY_EXP_BWD;
+// Where the forward's online mode adds log2e ln P(k'): 1 = the epilogue (fp32, round to nearest), 0 =
+// inside the MMA through the extra slab (the tensor core's truncating accumulation biases it by
+// ~3e-8 |lP| toward zero, tools/tc_bias.cu; measured cost and accuracy in DESIGN.md "Forward numerics")
+#ifndef QEM_LP_EPI
+#define QEM_LP_EPI 0
+#endif
+constexpr bool kLpEpi = QEM_LP_EPI != 0;
 
 // Operand geometry per latent dimension:
 //  D = 8..16 ("split"): the c-region of a row / column is the bf16x3 split of the 16-dim
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
       compact_row(bt[2], bt[1], c0, c1);
       *reinterpret_cast<uint4*>(rc + TcGeo<D>::row_off(k, 0)) = c0;
       *reinterpret_cast<uint4*>(rc + TcGeo<D>::row_off(k, 8)) = c1;
-      extra_row(0.f, 0.f, 0.f, c0, c1);  // forward: no row constant, lP off (added by the epilogue), gamma in the c-region
+      extra_row(0.f, kLpEpi ? 0.f : 1.f, 0.f, c0, c1);  // forward: no row constant, gamma in the c-region
       *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 0)) = c0;
       *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 8)) = c1;
       continue;
@@ -272,7 +279,7 @@ __global__ void __launch_bounds__(256) k_rowop_tc(TLArgs a) {
     for (int r = 0; r < kTcD; ++r) v[r] = r < D ? bt[2 + r] : 0.f;
     store_row_split16(rc, k, v);
     uint4 c0, c1;
-    extra_row(bt[1], 0.f, 0.f, c0, c1);  // forward: no row constant, lP off (added by the epilogue)
+    extra_row(bt[1], kLpEpi ? 0.f : 1.f, 0.f, c0, c1);  // forward: no row constant; lP switch
     *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 0)) = c0;
     *reinterpret_cast<uint4*>(rx + tc_rowx_offset(k, 8)) = c1;
   }
@@ -575,9 +582,10 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         // accumulation (aligned to the largest product, truncated) would bias every pair by ~3e-8 |lP|
         // toward zero -- upward, coherently over the groups' plate sum (tools/tc_bias.cu).  log2e ln P
         // is rounded once from fp64 (the fp32 log2e would scale it by 1 - 1.3e-8: the same kind of bias).
-        aux[kc] = md == 5 ? (float)(lpd * kLog2eD) : expf((float)lpd);
+        const float lp2 = (float)(lpd * kLog2eD);
+        aux[kc] = (md == 5 && kLpEpi) ? lp2 : expf((float)lpd);
         uint4 c0, c1;
-        extra_col(0.f, 0.f, c0, c1);  // lP slots zero in the forward (the backward writes L* there)
+        extra_col(0.f, (md == 5 && !kLpEpi) ? lp2 : 0.f, c0, c1);  // (the backward writes L* there)
         *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 56)) = c1;  // chunk 7: 1 lP0 lP1 lP2 0...
       }
     }
@@ -666,9 +674,10 @@ __global__ void __launch_bounds__(256) k_colprep_tc1(TLArgs a) {
 #pragma unroll 4
     for (int kc = lane; kc < K; kc += 32) {
       const double lpd = tref[kc] - M - logS;  // this lane's own store above
-      aux[kc] = md == 5 ? (float)(lpd * kLog2eD) : expf((float)lpd);  // P or log2e ln P (see k_colprep_tc)
+      const float lp2 = (float)(lpd * kLog2eD);
+      aux[kc] = (md == 5 && kLpEpi) ? lp2 : expf((float)lpd);  // P or log2e ln P (see k_colprep_tc)
       uint4 c0, c1;
-      extra_col(0.f, 0.f, c0, c1);  // lP slots zero in the forward (the backward writes L* there)
+      extra_col(0.f, (md == 5 && !kLpEpi) ? lp2 : 0.f, c0, c1);
       *reinterpret_cast<uint4*>(cop + G::col_off(kc, G::XKK + 8)) = c1;
     }
     if (lane == 0) {
@@ -788,9 +797,9 @@ __device__ __forceinline__ void fwd_epi_online(uint32_t taddr, const float* lpp,
   uint32_t r[4][16];
   tmem_ld64(taddr, r);  // the thread's 64 columns of this tile, one TMEM round trip
   // + log2e ln P of the columns (SMEM broadcast: every lane of the warp reads the same columns), in
-  // fp32 round to nearest (not inside the MMA: see k_colprep_tc)
+  // fp32 round to nearest (QEM_LP_EPI; else the MMA added it)
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < 4 && kLpEpi; ++q)
 #pragma unroll
     for (int c4 = 0; c4 < 4; ++c4) {
       const float4 l = reinterpret_cast<const float4*>(lpp + q * 16)[c4];
@@ -1100,8 +1109,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
       mbar_wait(&t_full[T & 1], (uint32_t)((T >> 1) & 1));
       tc_fence_after();
       const uint32_t taddr = tmem + (uint32_t)(T & 1) * 256 + (uint32_t)(cq * 64) + ((uint32_t)(q * 32) << 16);
-      mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));  // P / log2e ln P of this block is in SMEM
       const float* pp = s_p + (J & 1) * 256 + cq * 64;
+      if (md != 5 || kLpEpi) mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));  // P / lP of this block in SMEM
       if (md == 5) {
         fwd_epi_online(taddr, pp, st0, st1);
       } else {

@@ -751,11 +751,13 @@ int tl_use_tc(const qem_model_desc* d) {
   // (split layout, contraction zero-padded to 16), or d = 1 with Gaussian ones (compact layout).
   // For 2 <= d < 8 the FFMA tiles stay: the split layout's 128-byte column operand would be mostly
   // padding.
-  static const int off1 = getenv("QEM_NO_TC1") != nullptr;  // the compact (d = 1) path only
+  // d = 1 with Gaussian observations (config 4): the compact layout, one c-region MMA + the extra slab
+  // per tile and a 64-byte column operand (compact path) -- opt-in
+  // (QEM_TC1=1): on config 4 its forward is faster than the FFMA tiles but the step is not, and the
+  // online mode's ln P inside the MMA is biased by the truncating accumulation
+  static const int on1 = getenv("QEM_TC1") != nullptr && atoi(getenv("QEM_TC1")) != 0;
   if (off || d->K % 256 != 0 || d->K > QEM_MAX_K) return 0;
-  // d = 1 with Gaussian observations (config 4): the compact layout, one c-region MMA + the extra
-  // slab per tile and a 64-byte column operand (compact path)
-  if (d->d == 1) return !off1 && d->obs_kind == QEM_OBS_GAUSS;
+  if (d->d == 1) return on1 && d->obs_kind == QEM_OBS_GAUSS;
   return d->d >= 8 && d->d <= kTcD && tl_supported_d(d->d) && d->obs_kind == QEM_OBS_BERNOULLI_LOGIT;
 }
 

@@ -34,7 +34,7 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = {
     "tc_d16_K256": dict(cid=5, n=37, K=256),          # tcgen05 pair tiles
-    "ffma_d1_K256": dict(cid=4, n=301, K=256),        # FFMA tiles, scalar latents
+    "ffma_d1_K256": dict(cid=4, n=301, K=256),        # FFMA tiles, scalar latents (config 4's shape)
     "ffma_d18_K30": dict(cid=2, n=50),                # FFMA tiles, config 2's shape
 }
 

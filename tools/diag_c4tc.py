@@ -1,5 +1,5 @@
 """Diagnostic (not a test): per-iteration root-weight and plate-message errors of config 4's shape on the
-current pair path (set QEM_NO_TC1=1 for the FFMA tiles), teacher-forced from the oracle's trajectory.
+current pair path (FFMA tiles; QEM_TC1=1 for the compact tensor-core path), teacher-forced from the oracle's trajectory.
     python tools/diag_c4tc.py [n] [T]"""
 import os
 import sys
@@ -20,7 +20,7 @@ seed = 104
 ref_run = orc.run_qem(m, data, T, seed)
 g = QEM(m)
 g.set_data(data)
-print("pair path", g.pair_path(), "QEM_NO_TC1" in os.environ)
+print("pair path", g.pair_path())
 state = orc.initial_state(m)
 q = [orc.mstep(a, b)[:2] for a, b in state]
 for t in range(1, T + 1):
