@@ -175,6 +175,16 @@ static qem_status create_impl(const qem_model_desc* desc, const qem_opts* opts, 
                 (long long)group_end, (long long)desc->n);
   if (desc->family == QEM_FAMILY_THREE_LEVEL && (group_begin != 0 || group_end != desc->n))
     return fail(QEM_UNSUPPORTED, "three-level models run as replicas only (no group sharding)");
+  if (desc->family == QEM_FAMILY_TWO_LEVEL) {  // shared memory that grows with K and J
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && optin > 0) {
+      const size_t need = qem::tl_max_smem(desc);
+      if (need > (size_t)optin)
+        return fail(QEM_INVALID_MODEL, "K=%d, J=%d needs %zu bytes of shared memory per block (device limit %d)",
+                    desc->K, desc->n_obs, need, optin);
+    }
+  }
   qem_ctx* c = new (std::nothrow) qem_ctx();
   if (!c) return fail(QEM_INVALID_ARGUMENT, "out of host memory");
   c->desc = *desc;
@@ -604,6 +614,14 @@ qem_status qem_tables_crossed(int64_t n, int32_t K, int32_t J, int32_t C, int32_
                               const float* d_q_var, const int32_t* d_comp, const int32_t* d_jtype, const uint8_t* d_y,
                               double* d_f_root, double* d_f, void* stream) {
   if (n < 0 || K < 1 || J < 0 || C < 1 || T < 1 || J > 4096) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  {  // the crossed-table kernel stages 8 warps x J offsets (fp64) in shared memory
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && optin > 0 &&
+        (size_t)8 * J * sizeof(double) > (size_t)optin)
+      return fail(QEM_INVALID_ARGUMENT, "J=%d needs %zu bytes of shared memory per block (device limit %d)", J,
+                  (size_t)8 * J * sizeof(double), optin);
+  }
   if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root ||
       (n > 0 && (!d_z || !d_q_mean || !d_q_var || !d_f || (J > 0 && (!d_comp || !d_jtype || !d_y)))))
     return fail(QEM_INVALID_ARGUMENT, "null array");

@@ -112,6 +112,7 @@ cudaError_t tl_forward(qem_ctx* c, cudaStream_t s);
 cudaError_t tl_backward(qem_ctx* c, cudaStream_t s);
 int tl_supported_d(int d);
 int tl_use_tc(const qem_model_desc* d);
+size_t tl_max_smem(const qem_model_desc* d);
 void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* grid_fwd, int* grid_bwd, int* grid_prep);
 // three-level launchers (qem_three_level.cu)
 cudaError_t th_forward(qem_ctx* c, cudaStream_t s);

@@ -761,6 +761,43 @@ int tl_use_tc(const qem_model_desc* d) {
   return d->d >= 8 && d->d <= kTcD && tl_supported_d(d->d) && d->obs_kind == QEM_OBS_BERNOULLI_LOGIT;
 }
 
+// Largest dynamic shared memory any two-level kernel of this model's path asks for (bytes): checked
+// against the device's opt-in limit at context creation, so an oversized K / J is a model error up
+// front instead of a failed launch inside a captured graph.
+template <int D>
+static size_t max_smem(const qem_model_desc* d, bool tc) {
+  const int K = d->K, J = d->n_obs;
+  size_t m = 0;
+  auto up = [&](size_t v) { m = v > m ? v : m; };
+  if (tc) {
+    if constexpr (D <= kTcD) {
+      up(FwdTcL<D>::bytes(K));
+      up(BwdTcL<D>::bytes(K));
+      if constexpr (!TcGeo<D>::COMPACT) {
+        up(PrepTc::bytes(K, J));
+        up(GroupStage::bytes(K, D));
+      }
+    }
+  } else {
+    up(FwdLayout<D>::prep_bytes(K, J));
+    up(FwdLayout<D>::bytes(K, J));
+    up(bwd_smem<D>(K));
+  }
+  return m;
+}
+
+size_t tl_max_smem(const qem_model_desc* d) {
+  const bool tc = tl_use_tc(d) != 0;
+  switch (d->d) {
+#define X(v) \
+  case v:    \
+    return max_smem<v>(d, tc);
+    QEM_D_LIST(X)
+#undef X
+  }
+  return 0;
+}
+
 void tl_grids(const qem_model_desc* d, int64_t n_local, int sms, int* gf, int* gb, int* gp) {
   *gf = *gb = *gp = 1;
   const bool tc = tl_use_tc(d) != 0;
