@@ -837,7 +837,7 @@ def run_converged_variant(args, dev, steps=5):
             frac = c / tot
             if md < 5:
                 cyc += frac * (base + degs[md] + 2.0) / FP32_PER_SM_CLK
-            else:
+            elif md == 5:
                 cyc += frac * max(1.0 / SFU_PER_SM_CLK, (base + 2.0) / FP32_PER_SM_CLK)
         ceiling = SMS * SM_MAX_MHZ * 1e6 / cyc
         achieved = m.pairs / (fwd * 1e-3)

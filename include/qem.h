@@ -514,8 +514,9 @@ qem_status qem_iterate(qem_ctx* ctx, int32_t t0, int32_t T, uint64_t seed, int32
 qem_status qem_read_flags(qem_ctx* ctx, void* stream, uint32_t* flags, int64_t* clamps);
 
 /* Synchronises `stream`, copies the forward tile-mode histogram (counts of
-   (CTA-warp, group) tiles evaluated in mode 0..5) into
-   h_hist[6] and clears it.  Two-level only; diagnostics. */
+   (CTA-warp, group) tiles evaluated in mode 0..6: 0-4 expm1 polynomial of
+   degree 3/4/5/7/9, 5 online log-sum-exp; slot 6 is reserved and reads 0) into h_hist[7] and
+   clears it.  Two-level only; diagnostics. */
 qem_status qem_read_mode_hist(qem_ctx* ctx, void* stream, uint64_t* h_hist);
 
 /* Optional cudaEvent_t handles (as void*, NULL = off) that the library

@@ -1,7 +1,8 @@
 """Write profiles/<name>.json: per-kernel DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
 from one `ncu --set full` capture per kernel, for bench.py's roofline "traffic" field.
 
-    python tools/ncu_traffic.py profiles/r01_traffic.json gpurun_out/ncu_bwd4.ncu-rep [...]
+    python tools/ncu_traffic.py profiles/r02_traffic.json [--config N] gpurun_out/ncu_bwd4.ncu-rep [...]
+(with --config N the entries go under "configN", the layout bench.py reads)
 """
 import csv, json, subprocess, sys
 
@@ -24,12 +25,16 @@ def kernel_bytes(rep):
 
 if __name__ == "__main__":
     dst = sys.argv[1]
+    args = sys.argv[2:]
+    cfg = None
+    if args and args[0] == "--config":
+        cfg, args = "config" + args[1], args[2:]
     try:
         data = json.load(open(dst))
     except Exception:
         data = {}
-    for rep in sys.argv[2:]:
+    for rep in args:
         n, d = kernel_bytes(rep)
-        data[n] = d
-        print(n, d)
+        (data.setdefault(cfg, {}) if cfg else data)[n] = d
+        print(cfg, n, d)
     json.dump(data, open(dst, "w"), indent=1)
