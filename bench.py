@@ -612,40 +612,35 @@ def run_crossed_variant(dev, steps=10):
 
 
 def run_gamma_variant(dev, steps=10):
-    """NEXT row f1, Gamma Q (R32): one QEM iteration of the Gamma-Poisson hierarchy
-    (2000 groups, J = 8, K = 128; Marsaglia-Tsang Gamma draws, fp64 tables, Gamma M-step)."""
+    """NEXT row f1, Gamma / Beta Q (R32, R37): one QEM iteration of the Gamma-Poisson
+    (2000 groups, J = 8, K = 128) and Beta-Binomial (2000 groups, K = 128) hierarchies, with the
+    separable factors evaluated on chip (default) and through materialised fp64 tables."""
     import torch
     from paper_2503_08264_b200 import synth
-    from paper_2503_08264_b200.qem import GammaPoissonQEM
-    gp = synth.gamma_poisson()
-    g = GammaPoissonQEM(gp, device=dev)
-    for t in range(1, 4):
-        g.step(t, 3)
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    st.record()
-    for t in range(4, 4 + steps):
-        g.step(t, 3)
-    en.record()
-    torch.cuda.synchronize()
-    ms = st.elapsed_time(en) / steps
-    out = {"workload": f"gamma-poisson n={gp.n} J={gp.J} K={gp.K}", "ms_per_step": ms,
-           "factor_pairs_per_s": gp.n * gp.K * gp.K / (ms * 1e-3), "qem_iters_per_s": 1e3 / ms}
-    del g
-    from paper_2503_08264_b200.qem import BetaBinomialQEM
-    bb = synth.beta_binomial()
-    g = BetaBinomialQEM(bb, device=dev)
-    for t in range(1, 4):
-        g.step(t, 3)
-    torch.cuda.synchronize()
-    st.record()
-    for t in range(4, 4 + steps):
-        g.step(t, 3)
-    en.record()
-    torch.cuda.synchronize()
-    ms = st.elapsed_time(en) / steps
-    out["beta_binomial"] = {"workload": f"beta-binomial n={bb.n} K={bb.K}", "ms_per_step": ms,
-                            "factor_pairs_per_s": bb.n * bb.K * bb.K / (ms * 1e-3), "qem_iters_per_s": 1e3 / ms}
+    from paper_2503_08264_b200.qem import BetaBinomialQEM, GammaPoissonQEM
+
+    def timed(make):
+        g = make()
+        for t in range(1, 4):
+            g.step(t, 3)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        st.record()
+        for t in range(4, 4 + steps):
+            g.step(t, 3)
+        en.record()
+        torch.cuda.synchronize()
+        return st.elapsed_time(en) / steps
+
+    gp, bb = synth.gamma_poisson(), synth.beta_binomial()
+    out = {}
+    for name, model, cls in (("gamma_poisson", gp, GammaPoissonQEM), ("beta_binomial", bb, BetaBinomialQEM)):
+        res = {"workload": f"{name.replace('_', '-')} n={model.n} K={model.K}"}
+        for path, tables in (("separable", False), ("tables", True)):
+            ms = timed(lambda: cls(model, device=dev, tables=tables))
+            res[path] = {"ms_per_step": ms, "factor_pairs_per_s": model.n * model.K * model.K / (ms * 1e-3),
+                         "qem_iters_per_s": 1e3 / ms}
+        out[name] = res
     return out
 
 

@@ -481,6 +481,30 @@ qem_status qem_loglik_bernoulli_states(int64_t n, int32_t C, int32_t R, const ui
 qem_status qem_estep_tables(int64_t n, int32_t K, const double* d_f_root, const double* d_f, double* d_g,
                             double* d_log_pe, double* d_w_root, double* d_w, void* stream);
 
+/* The same E-step for SEPARABLE log-factors, without the n x K x K table (north star: the N K^2
+   tensor is never materialised in HBM; NEXT rows f1 / f4, R37):
+     f_i(k, k') = a_k + sum_{r<R} b_k[r] phi_i(k')[r] + psi_i(k'),   0 <= R <= 3
+     d_rows [K][1 + R]   (a_k, b_k[0..R-1])                     fp64, device
+     d_cols [n][K][R + 1] (phi_i(k')[0..R-1], psi_i(k'))         fp64, device
+   Each group's columns are staged in shared memory and every pair is evaluated on chip (fp64),
+   once for the forward and once for the backward.  Outputs, scratch use and degenerate-evidence
+   behaviour as qem_estep_tables.  Errors: QEM_INVALID_ARGUMENT for n < 0, K outside [1, QEM_MAX_K],
+   R outside [0, 3] or a null array. */
+qem_status qem_estep_separable(int64_t n, int32_t K, int32_t R, const double* d_f_root, const double* d_rows,
+                               const double* d_cols, double* d_g, double* d_log_pe, double* d_w_root, double* d_w,
+                               void* stream);
+/* Separable factors of the Gamma-Poisson model (R = 1: rows [K][2], columns [n][K][2]; the same
+   densities as qem_tables_gamma_poisson) and of the Beta-Binomial model (R = 2: rows [K][3],
+   columns [n][K][3]; as qem_tables_beta_binomial), plus d_f_root [K]. */
+qem_status qem_cols_gamma_poisson(int64_t n, int32_t K, int32_t J, double alpha, const float* d_root_z,
+                                  const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
+                                  const double* d_q, const double* d_z, double* d_f_root, double* d_rows,
+                                  double* d_cols, void* stream);
+qem_status qem_cols_beta_binomial(int64_t n, int32_t K, double kappa, const float* d_root_z,
+                                  const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
+                                  const int32_t* d_N, const double* d_q, const double* d_z, double* d_f_root,
+                                  double* d_rows, double* d_cols, void* stream);
+
 /* EMA over mean parameters + M-step for non-Gaussian Q families (Alg. 1 lines 3, 6; Eq. 9;
    PAPER.md:218 "a Beta's parameters are recovered from expectations of log transformations",
    PAPER.md:247).  Context-free, stream-ordered, one device thread per latent instance, fp64.

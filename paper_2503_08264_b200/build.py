@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["qem_api.cu", "qem_common.cu", "qem_two_level.cu", "qem_three_level.cu", "qem_expfam.cu", "qem_tables.cu", "qem_discrete.cu", "qem_predict.cu", "qem_gamma.cu", "qem_crossed.cu", "qem_nccl.cu"]
+SOURCES = ["qem_api.cu", "qem_common.cu", "qem_two_level.cu", "qem_three_level.cu", "qem_expfam.cu", "qem_tables.cu", "qem_discrete.cu", "qem_predict.cu", "qem_gamma.cu", "qem_crossed.cu", "qem_nccl.cu", "qem_separable.cu"]
 HEADERS = ["qem_internal.h", "qem_device.cuh", "qem_forward.cuh", "qem_tc.cuh", os.path.join("..", "..", "include", "qem.h")]
 LIB = os.path.join(HERE, "libqem.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -506,6 +506,44 @@ qem_status qem_estep_tables(int64_t n, int32_t K, const double* d_f_root, const 
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_tables");
 }
 
+qem_status qem_estep_separable(int64_t n, int32_t K, int32_t R, const double* d_f_root, const double* d_rows,
+                               const double* d_cols, double* d_g, double* d_log_pe, double* d_w_root, double* d_w,
+                               void* stream) {
+  if (n < 0 || K < 1 || K > QEM_MAX_K || R < 0 || R > 3)
+    return fail(QEM_INVALID_ARGUMENT, "need n >= 0, 1 <= K <= %d, 0 <= R <= 3", QEM_MAX_K);
+  if (!d_f_root || !d_rows || !d_log_pe || !d_w_root || (n > 0 && (!d_cols || !d_g || !d_w)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_estep_separable(n, K, R, d_f_root, d_rows, d_cols, d_g, d_log_pe, d_w_root, d_w,
+                                                    (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_separable");
+}
+
+qem_status qem_cols_gamma_poisson(int64_t n, int32_t K, int32_t J, double alpha, const float* d_root_z,
+                                  const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
+                                  const double* d_q, const double* d_z, double* d_f_root, double* d_rows,
+                                  double* d_cols, void* stream) {
+  if (n < 0 || K < 1 || J < 0 || !(alpha > 0.0)) return fail(QEM_INVALID_ARGUMENT, "bad sizes or alpha");
+  if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root || !d_rows ||
+      (n > 0 && (!d_q || !d_z || !d_cols || (J > 0 && !d_y))))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_gamma_cols(n, K, J, alpha, d_root_z, d_root_mean, d_root_var, d_y, d_q, d_z,
+                                               d_f_root, d_rows, d_cols, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_cols_gamma_poisson");
+}
+
+qem_status qem_cols_beta_binomial(int64_t n, int32_t K, double kappa, const float* d_root_z,
+                                  const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
+                                  const int32_t* d_N, const double* d_q, const double* d_z, double* d_f_root,
+                                  double* d_rows, double* d_cols, void* stream) {
+  if (n < 0 || K < 1 || !(kappa > 0.0)) return fail(QEM_INVALID_ARGUMENT, "bad sizes or kappa");
+  if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root || !d_rows ||
+      (n > 0 && (!d_y || !d_N || !d_q || !d_z || !d_cols)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_beta_cols(n, K, kappa, d_root_z, d_root_mean, d_root_var, d_y, d_N, d_q, d_z,
+                                              d_f_root, d_rows, d_cols, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_cols_beta_binomial");
+}
+
 qem_status qem_backward_resample(qem_ctx* c, int32_t S, uint64_t seed, int32_t* d_idx_root, int32_t* d_idx,
                                  void* stream) {
   qem_status s = need_bound(c);

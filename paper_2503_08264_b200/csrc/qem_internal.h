@@ -133,6 +133,15 @@ int nccl_version();
 // non-Gaussian Q families (qem_expfam.cu)
 cudaError_t launch_estep_tables(int64_t n, int K, const double* f_root, const double* f, double* g, double* log_pe,
                                 double* w_root, double* w, cudaStream_t st);
+cudaError_t launch_estep_separable(int64_t n, int K, int R, const double* f_root, const double* rows,
+                                   const double* cols, double* g, double* log_pe, double* w_root, double* w,
+                                   cudaStream_t st);
+cudaError_t launch_gamma_cols(int64_t n, int K, int J, double alpha, const float* mu, const float* rm, const float* rv,
+                              const int32_t* y, const double* q, const double* z, double* f_root, double* rows,
+                              double* cols, cudaStream_t st);
+cudaError_t launch_beta_cols(int64_t n, int K, double kappa, const float* mu, const float* rm, const float* rv,
+                             const int32_t* y, const int32_t* N, const double* q, const double* z, double* f_root,
+                             double* rows, double* cols, cudaStream_t st);
 cudaError_t launch_plate_root(int64_t n, int K, const double* f_root, const double* g, double* scratch,
                               double* log_pe, double* w_root, cudaStream_t st);
 cudaError_t launch_cat_estep(int64_t n, int C, int K, int d, const float* rz, const float* rm, const float* rv,

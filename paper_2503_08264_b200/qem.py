@@ -67,6 +67,25 @@ def estep_tables(f_root: torch.Tensor, f: torch.Tensor, stream=None):
     return out
 
 
+def estep_separable(f_root: torch.Tensor, rows: torch.Tensor, cols: torch.Tensor, stream=None):
+    """MPIW E-step on separable log-factors (qem_estep_separable): f_root [K], rows [K][1+R], cols
+    [n][K][R+1] (float64 device).  Returns dict(log_pe [1], w_root [K], w [n][K], g [n][K])."""
+    assert f_root.dtype == rows.dtype == cols.dtype == torch.float64 and f_root.is_cuda
+    K, R = f_root.shape[0], rows.shape[1] - 1
+    n = cols.shape[0] if cols.numel() else 0
+    assert tuple(rows.shape) == (K, R + 1) and (n == 0 or tuple(cols.shape) == (n, K, R + 1))
+    f_root, rows, cols = f_root.contiguous(), rows.contiguous(), cols.contiguous()
+    dev = f_root.device
+    out = dict(log_pe=torch.empty(1, dtype=torch.float64, device=dev),
+               w_root=torch.empty(K, dtype=torch.float64, device=dev),
+               w=torch.empty(n, K, dtype=torch.float64, device=dev),
+               g=torch.empty(n, K, dtype=torch.float64, device=dev))
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr() if t.numel() else None)  # noqa: E731
+    check(lib().qem_estep_separable(n, K, R, ptr(f_root), ptr(rows), ptr(cols), ptr(out["g"]), ptr(out["log_pe"]),
+                                    ptr(out["w_root"]), ptr(out["w"]), _stream(stream)), "qem_estep_separable")
+    return out
+
+
 def logmeanexp(x: torch.Tensor, stream=None) -> torch.Tensor:
     """log (1/n) sum exp(x) of a float64 device vector (qem_logmeanexp); returns a [1] tensor."""
     assert x.dtype == torch.float64 and x.is_cuda
@@ -506,10 +525,13 @@ class GammaPoissonQEM:
     + qem_tables_gamma_poisson + qem_estep_tables + qem_moments_gamma + qem_mstep_family (GAMMA)
     + qem_mstep_categorical (root only, n = 0), all on device (argument marshalling only)."""
 
-    def __init__(self, gp, *, new_weight=0.3, var_floor=1e-8, device="cuda"):
+    def __init__(self, gp, *, new_weight=0.3, var_floor=1e-8, device="cuda", tables=False):
+        """tables=False (default): separable factors evaluated on chip (qem_cols_gamma_poisson +
+        qem_estep_separable, no n x K x K array); True: the materialised fp64 tables
+        (qem_tables_gamma_poisson + qem_estep_tables), kept for comparison."""
         if not torch.cuda.is_available():
             raise _lib.QemError("GammaPoissonQEM needs a CUDA device (there is no CPU fallback)")
-        self.gp, self.device = gp, torch.device(device)
+        self.gp, self.device, self.tables = gp, torch.device(device), bool(tables)
         self.new_weight, self.var_floor = new_weight, var_floor
         n, K = gp.n, gp.K
         f32 = dict(dtype=torch.float32, device=self.device)
@@ -520,7 +542,11 @@ class GammaPoissonQEM:
         self.q = torch.ones(n, 2, **f64)                                   # Gamma(1, 1)
         self.g_ema = torch.tensor([[1.0, -0.5772156649015329]] * n, **f64)  # its (E l, E ln l)
         self.mu, self.z = torch.empty(1, K, **f32), torch.empty(n, K, **f64)
-        self.f_root, self.f = torch.empty(K, **f64), torch.empty(n, K, K, **f64)
+        self.f_root = torch.empty(K, **f64)
+        if self.tables:
+            self.f = torch.empty(n, K, K, **f64)
+        else:
+            self.rows, self.cols = torch.empty(K, 2, **f64), torch.empty(n, K, 2, **f64)
         self.g, self.w = torch.empty(n, K, **f64), torch.empty(n, K, **f64)
         self.w_root, self.log_pe = torch.empty(K, **f64), torch.empty(1, **f64)
         self.root_m, self.gm = torch.empty(1, 2, **f64), torch.empty(n, 2, **f64)
@@ -534,11 +560,19 @@ class GammaPoissonQEM:
                                   _ptr(root_eps) if root_eps is not None else None, _ptr(self.mu), s),
               "qem_sample_normal")
         check(L.qem_sample_gamma(n, K, seed, t, _ptr(self.q), _ptr(self.z), s), "qem_sample_gamma")
-        check(L.qem_tables_gamma_poisson(n, K, gp.J, float(gp.alpha), _ptr(self.mu), _ptr(self.root_mean),
-                                         _ptr(self.root_var), _ptr(self.y), _ptr(self.q), _ptr(self.z),
-                                         _ptr(self.f_root), _ptr(self.f), s), "qem_tables_gamma_poisson")
-        check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
-                                 _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        if self.tables:
+            check(L.qem_tables_gamma_poisson(n, K, gp.J, float(gp.alpha), _ptr(self.mu), _ptr(self.root_mean),
+                                             _ptr(self.root_var), _ptr(self.y), _ptr(self.q), _ptr(self.z),
+                                             _ptr(self.f_root), _ptr(self.f), s), "qem_tables_gamma_poisson")
+            check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
+                                     _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        else:
+            check(L.qem_cols_gamma_poisson(n, K, gp.J, float(gp.alpha), _ptr(self.mu), _ptr(self.root_mean),
+                                           _ptr(self.root_var), _ptr(self.y), _ptr(self.q), _ptr(self.z),
+                                           _ptr(self.f_root), _ptr(self.rows), _ptr(self.cols), s),
+                  "qem_cols_gamma_poisson")
+            check(L.qem_estep_separable(n, K, 1, _ptr(self.f_root), _ptr(self.rows), _ptr(self.cols), _ptr(self.g),
+                                        _ptr(self.log_pe), _ptr(self.w_root), _ptr(self.w), s), "qem_estep_separable")
         check(L.qem_moments_gamma(n, K, _ptr(self.w_root), _ptr(self.mu), _ptr(self.w), _ptr(self.z),
                                   _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_gamma")
         lam = 1.0 - self.new_weight
@@ -563,10 +597,11 @@ class BetaBinomialQEM:
     qem_tables_beta_binomial + qem_estep_tables + qem_moments_beta + qem_mstep_family (BETA) +
     qem_mstep_categorical (root only), all on device (argument marshalling only)."""
 
-    def __init__(self, bb, *, new_weight=0.3, var_floor=1e-8, device="cuda"):
+    def __init__(self, bb, *, new_weight=0.3, var_floor=1e-8, device="cuda", tables=False):
+        """tables: as GammaPoissonQEM (False: qem_cols_beta_binomial + qem_estep_separable)."""
         if not torch.cuda.is_available():
             raise _lib.QemError("BetaBinomialQEM needs a CUDA device (there is no CPU fallback)")
-        self.bb, self.device = bb, torch.device(device)
+        self.bb, self.device, self.tables = bb, torch.device(device), bool(tables)
         self.new_weight, self.var_floor = new_weight, var_floor
         n, K = bb.n, bb.K
         f32 = dict(dtype=torch.float32, device=self.device)
@@ -578,7 +613,11 @@ class BetaBinomialQEM:
         self.q = torch.ones(n, 2, **f64)                                   # Beta(1, 1)
         self.g_ema = torch.tensor([[-1.0, -1.0]] * n, **f64)               # its (E ln p, E ln(1-p))
         self.mu, self.z = torch.empty(1, K, **f32), torch.empty(n, K, **f64)
-        self.f_root, self.f = torch.empty(K, **f64), torch.empty(n, K, K, **f64)
+        self.f_root = torch.empty(K, **f64)
+        if self.tables:
+            self.f = torch.empty(n, K, K, **f64)
+        else:
+            self.rows, self.cols = torch.empty(K, 3, **f64), torch.empty(n, K, 3, **f64)
         self.g, self.w = torch.empty(n, K, **f64), torch.empty(n, K, **f64)
         self.w_root, self.log_pe = torch.empty(K, **f64), torch.empty(1, **f64)
         self.root_m, self.gm = torch.empty(1, 2, **f64), torch.empty(n, 2, **f64)
@@ -592,11 +631,20 @@ class BetaBinomialQEM:
                                   _ptr(root_eps) if root_eps is not None else None, _ptr(self.mu), s),
               "qem_sample_normal")
         check(L.qem_sample_beta(n, K, seed, t, _ptr(self.q), _ptr(self.z), s), "qem_sample_beta")
-        check(L.qem_tables_beta_binomial(n, K, float(bb.kappa), _ptr(self.mu), _ptr(self.root_mean),
-                                         _ptr(self.root_var), _ptr(self.y), _ptr(self.N), _ptr(self.q), _ptr(self.z),
-                                         _ptr(self.f_root), _ptr(self.f), s), "qem_tables_beta_binomial")
-        check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
-                                 _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        if self.tables:
+            check(L.qem_tables_beta_binomial(n, K, float(bb.kappa), _ptr(self.mu), _ptr(self.root_mean),
+                                             _ptr(self.root_var), _ptr(self.y), _ptr(self.N), _ptr(self.q),
+                                             _ptr(self.z), _ptr(self.f_root), _ptr(self.f), s),
+                  "qem_tables_beta_binomial")
+            check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
+                                     _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        else:
+            check(L.qem_cols_beta_binomial(n, K, float(bb.kappa), _ptr(self.mu), _ptr(self.root_mean),
+                                           _ptr(self.root_var), _ptr(self.y), _ptr(self.N), _ptr(self.q), _ptr(self.z),
+                                           _ptr(self.f_root), _ptr(self.rows), _ptr(self.cols), s),
+                  "qem_cols_beta_binomial")
+            check(L.qem_estep_separable(n, K, 2, _ptr(self.f_root), _ptr(self.rows), _ptr(self.cols), _ptr(self.g),
+                                        _ptr(self.log_pe), _ptr(self.w_root), _ptr(self.w), s), "qem_estep_separable")
         check(L.qem_moments_beta(n, K, _ptr(self.w_root), _ptr(self.mu), _ptr(self.w), _ptr(self.z),
                                  _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_beta")
         lam = 1.0 - self.new_weight

@@ -93,13 +93,27 @@ def test_beta_evidence_estimate_is_unbiased():
 # ------------------------------------------------------------------ device path (GPU)
 
 
+def _factors(g):
+    """The device's log-factor table: stored (tables path) or rebuilt from the separable rows and
+    columns, f[i][k][k'] = a_k + sum_r b_k[r] phi_i(k')[r] + psi_i(k') (qem_estep_separable)."""
+    if g.tables:
+        return g.f.cpu().numpy()
+    rows, cols = g.rows.cpu().numpy(), g.cols.cpu().numpy()
+    R = rows.shape[1] - 1
+    f = rows[None, :, 0, None] + cols[:, None, :, R]
+    for r in range(R):
+        f = f + rows[None, :, 1 + r, None] * cols[:, None, :, r]
+    return f
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("use_tables", [False, True], ids=["separable", "tables"])
 @pytest.mark.parametrize("n,K,T", [(150, 64, 3), (29, 17, 2)])
-def test_device_beta_qem_teacher_forced(n, K, T):
+def test_device_beta_qem_teacher_forced(n, K, T, use_tables):
     import torch
     from paper_2503_08264_b200.qem import BetaBinomialQEM
     bb = synth.beta_binomial(n=n, K=K, seed=4)
-    g = BetaBinomialQEM(bb)
+    g = BetaBinomialQEM(bb, tables=use_tables)
     state = og.initial_state_beta(bb)
     seed = 19
     for t in range(1, T + 1):
@@ -110,7 +124,7 @@ def test_device_beta_qem_teacher_forced(n, K, T):
         torch.cuda.synchronize()
         tag = f"beta n{n} K{K} t={t}"
         np.testing.assert_allclose(g.z.cpu().numpy(), ref["z"], rtol=1e-12, err_msg=tag)
-        np.testing.assert_allclose(g.f.cpu().numpy(), ref["f"], rtol=1e-11, atol=1e-10, err_msg=tag)
+        np.testing.assert_allclose(_factors(g), ref["f"], rtol=1e-11, atol=1e-10, err_msg=tag)
         assert abs(float(g.log_pe.item()) - ref["est"]["log_pe"]) <= 1e-10 * abs(ref["est"]["log_pe"]), tag
         np.testing.assert_allclose(g.w.cpu().numpy(), ref["est"]["w"], rtol=1e-9, atol=1e-13, err_msg=tag)
         np.testing.assert_allclose(g.gm.cpu().numpy(), ref["gm"], rtol=1e-10, atol=1e-12, err_msg=tag)
@@ -122,12 +136,13 @@ def test_device_beta_qem_teacher_forced(n, K, T):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("use_tables", [False, True], ids=["separable", "tables"])
 @pytest.mark.parametrize("n,K,T", [(200, 64, 3), (37, 33, 2)])
-def test_device_gamma_qem_teacher_forced(n, K, T):
+def test_device_gamma_qem_teacher_forced(n, K, T, use_tables):
     import torch
     from paper_2503_08264_b200.qem import GammaPoissonQEM
     gp = synth.gamma_poisson(n=n, K=K, seed=3)
-    g = GammaPoissonQEM(gp)
+    g = GammaPoissonQEM(gp, tables=use_tables)
     state = og.initial_state(gp)
     seed = 17
     for t in range(1, T + 1):
@@ -139,7 +154,7 @@ def test_device_gamma_qem_teacher_forced(n, K, T):
         tag = f"n{n} K{K} t={t}"
         np.testing.assert_array_equal(g.mu.cpu().numpy()[0], ref["mu"], err_msg=tag)
         np.testing.assert_allclose(g.z.cpu().numpy(), ref["z"], rtol=1e-13, err_msg=tag)
-        np.testing.assert_allclose(g.f.cpu().numpy(), ref["f"], rtol=1e-11, atol=1e-10, err_msg=tag)
+        np.testing.assert_allclose(_factors(g), ref["f"], rtol=1e-11, atol=1e-10, err_msg=tag)
         assert abs(float(g.log_pe.item()) - ref["est"]["log_pe"]) <= 1e-10 * abs(ref["est"]["log_pe"]), tag
         np.testing.assert_allclose(g.w.cpu().numpy(), ref["est"]["w"], rtol=1e-9, atol=1e-13, err_msg=tag)
         np.testing.assert_allclose(g.gm.cpu().numpy(), ref["gm"], rtol=1e-10, atol=1e-12, err_msg=tag)
