@@ -300,9 +300,9 @@ qem_status qem_mstep(qem_ctx* ctx, int32_t t, void* stream);
    Gamma-Poisson hierarchy under a Gaussian root: mu ~ N(0, 1), Q_root = N(m, v) (1-dim root);
    lambda_i | mu ~ Gamma(shape alpha, rate alpha e^-mu); y_ij | lambda_i ~ Poisson(lambda_i);
    Q_i = Gamma(shape k_i, rate th_i).  One QEM iteration = qem_sample_normal (root) +
-   qem_sample_gamma + qem_tables_gamma_poisson + qem_estep_tables + qem_moments_gamma +
-   qem_mstep_family(QEM_QFAMILY_GAMMA) for the groups and qem_mstep_categorical(n = 0) for the
-   root.  Device arrays, caller-owned, asynchronous on `stream`; QEM_INVALID_ARGUMENT on bad
+   qem_sample_gamma + qem_cols_gamma_poisson + qem_estep_separable (or qem_tables_gamma_poisson +
+   qem_estep_tables) + qem_moments_gamma + qem_mstep_family(QEM_QFAMILY_GAMMA) for the groups and
+   qem_mstep_gaussian for the root.  Device arrays, caller-owned, asynchronous on `stream`; QEM_INVALID_ARGUMENT on bad
    sizes / null arrays. */
 /* d_z [n][K] fp64 Gamma(shape, rate) draws, d_q [n][2] = Q_i's (shape, rate) (qem_mstep_family's
    QEM_QFAMILY_GAMMA parameter layout): Marsaglia-Tsang (shape < 1: boosted), attempt
@@ -355,8 +355,8 @@ qem_status qem_moments_beta(int64_t n, int32_t K, const double* d_w_root, const 
    index d_comp [n][J] in [0, C), journey type d_jtype [n][J] in [0, T) and label d_y [n][J] in
    {0, 1}: delay ~ Bernoulli(sigmoid(w_i + cw_c + jw_t)).  One QEM iteration = qem_sample_normal
    (root rows, level 0) + qem_sample_normal (group rows, level 1) + qem_tables_crossed +
-   qem_estep_tables + qem_moments_gaussian + qem_mstep_categorical(n = 0) for the root dims and
-   again for the group latents (as d = n Gaussian dims).
+   qem_estep_tables + qem_moments_gaussian + qem_mstep_gaussian for the root dims and again for the
+   group latents.
    qem_tables_crossed: d_f_root [K] = sum_r log N(r^k; 0, 1) - log q(r^k); d_f [n][K][K] =
    log N(w_i^k'; mu^k, 1) + sum_j [y eta - softplus(eta)] - log q_i(w_i^k'),
    eta = w_i^k' + cw^k_{comp_ij} + jw^k_{jtype_ij} (fp64).  J <= 4096.
@@ -458,6 +458,17 @@ qem_status qem_mstep_categorical(int64_t n, int32_t C, int32_t d, double lam, do
                                  const double* d_root_m, double* d_root_ema, float* d_root_mean,
                                  float* d_root_var, const double* d_pm, double* d_p_ema, double* d_p,
                                  int64_t* d_clamps, void* stream);
+/* EMA + Gaussian M-step of `rows` Gaussian latent dimensions (the root groups of the NEXT-row models,
+   the crossed effects' group latents): d_ema [rows][2] <- lam d_ema + (1 - lam) d_m, both holding the
+   mean parameters (E z, E z^2) (Eq. 9); then mean = E z, var = max(E z^2 - (E z)^2, var_floor) written
+   fp32 to d_mean / d_var (R22); variance-floor clamps added to *d_clamps when non-NULL.  The same
+   kernel as qem_mstep_categorical's root part, under its own name. */
+qem_status qem_mstep_gaussian(int64_t rows, double lam, double var_floor, const double* d_m, double* d_ema,
+                              float* d_mean, float* d_var, int64_t* d_clamps, void* stream);
+/* History weight lambda of iteration t (R5): 1 - new_weight, or 1 - t^-p when
+   schedule_p > 0 (Theorem 1) -- the value k_mstep uses; host arithmetic. */
+double qem_history_weight(int32_t t, double new_weight, double schedule_p);
+
 /* Per-state log-likelihood of R Bernoulli observations per instance (the data table L of
    qem_tables_categorical): d_L[i][c] = sum_r y_ir l_irc - softplus(l_irc), softplus(l) =
    max(l, 0) + log1p(exp(-|l|)) (fp64); d_y [n][R] uint8 in {0,1}, d_logit [n][R][C] fp64. */

@@ -747,6 +747,21 @@ qem_status qem_mstep_categorical(int64_t n, int32_t C, int32_t d, double lam, do
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_mstep_categorical");
 }
 
+qem_status qem_mstep_gaussian(int64_t rows, double lam, double var_floor, const double* d_m, double* d_ema,
+                              float* d_mean, float* d_var, int64_t* d_clamps, void* stream) {
+  if (rows < 0 || rows > 0x7fffffffLL) return fail(QEM_INVALID_ARGUMENT, "bad rows");
+  if (!(lam >= 0.0 && lam < 1.0) || !(var_floor > 0.0)) return fail(QEM_INVALID_ARGUMENT, "need 0 <= lam < 1, var_floor > 0");
+  if (rows == 0) return QEM_OK;
+  if (!d_m || !d_ema || !d_mean || !d_var) return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_cat_mstep(0, 1, (int)rows, lam, var_floor, d_m, d_ema, d_mean, d_var, nullptr,
+                                              nullptr, nullptr, d_clamps, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_mstep_gaussian");
+}
+
+double qem_history_weight(int32_t t, double new_weight, double schedule_p) {
+  return schedule_p > 0.0 ? 1.0 - pow((double)(t < 1 ? 1 : t), -schedule_p) : 1.0 - new_weight;
+}
+
 qem_status qem_loglik_bernoulli_states(int64_t n, int32_t C, int32_t R, const uint8_t* d_y, const double* d_logit,
                                        double* d_L, void* stream) {
   if (n < 0 || C < 1 || C > QEM_CAT_MAX_C || R < 0) return fail(QEM_INVALID_ARGUMENT, "bad sizes");

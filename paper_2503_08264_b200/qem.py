@@ -478,8 +478,8 @@ class CategoricalQEM:
         self.clamps = torch.zeros(1, dtype=torch.int64, device=self.device)
 
     def lam(self, t: int) -> float:
-        """History weight (R5): 1 - new_weight, or 1 - t^-p with a schedule."""
-        return 1.0 - (t ** -self.schedule_p if self.schedule_p > 0 else self.new_weight)
+        """History weight (R5; qem_history_weight): 1 - new_weight, or 1 - t^-p with a schedule."""
+        return float(lib().qem_history_weight(int(t), float(self.new_weight), float(self.schedule_p)))
 
     def estep(self, t: int, seed: int, root_eps: Optional[torch.Tensor] = None, stream=None) -> None:
         om, L, s = self.om, lib(), _stream(stream)
@@ -575,12 +575,12 @@ class GammaPoissonQEM:
                                         _ptr(self.log_pe), _ptr(self.w_root), _ptr(self.w), s), "qem_estep_separable")
         check(L.qem_moments_gamma(n, K, _ptr(self.w_root), _ptr(self.mu), _ptr(self.w), _ptr(self.z),
                                   _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_gamma")
-        lam = 1.0 - self.new_weight
+        lam = L.qem_history_weight(int(t), float(self.new_weight), 0.0)
         check(L.qem_mstep_family(GAMMA, n, 1, lam, _ptr(self.gm), _ptr(self.g_ema), _ptr(self.q), _ptr(self.status),
                                  s), "qem_mstep_family")
-        check(L.qem_mstep_categorical(0, 1, 1, lam, self.var_floor, _ptr(self.root_m), _ptr(self.root_ema),
-                                      _ptr(self.root_mean), _ptr(self.root_var), None, None, None, _ptr(self.clamps),
-                                      s), "qem_mstep_categorical")
+        check(L.qem_mstep_gaussian(1, lam, self.var_floor, _ptr(self.root_m), _ptr(self.root_ema),
+                                   _ptr(self.root_mean), _ptr(self.root_var), _ptr(self.clamps), s),
+              "qem_mstep_gaussian")
 
     def set_state(self, st: dict) -> None:
         """Teacher forcing (parity tests): Q and EMA state from host arrays."""
@@ -647,12 +647,12 @@ class BetaBinomialQEM:
                                         _ptr(self.log_pe), _ptr(self.w_root), _ptr(self.w), s), "qem_estep_separable")
         check(L.qem_moments_beta(n, K, _ptr(self.w_root), _ptr(self.mu), _ptr(self.w), _ptr(self.z),
                                  _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_beta")
-        lam = 1.0 - self.new_weight
+        lam = L.qem_history_weight(int(t), float(self.new_weight), 0.0)
         check(L.qem_mstep_family(BETA, n, 1, lam, _ptr(self.gm), _ptr(self.g_ema), _ptr(self.q), _ptr(self.status),
                                  s), "qem_mstep_family")
-        check(L.qem_mstep_categorical(0, 1, 1, lam, self.var_floor, _ptr(self.root_m), _ptr(self.root_ema),
-                                      _ptr(self.root_mean), _ptr(self.root_var), None, None, None, _ptr(self.clamps),
-                                      s), "qem_mstep_categorical")
+        check(L.qem_mstep_gaussian(1, lam, self.var_floor, _ptr(self.root_m), _ptr(self.root_ema),
+                                   _ptr(self.root_mean), _ptr(self.root_var), _ptr(self.clamps), s),
+              "qem_mstep_gaussian")
 
     set_state = GammaPoissonQEM.set_state
 
@@ -701,11 +701,11 @@ class CrossedQEM:
                                  _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
         check(L.qem_moments_gaussian(n, K, R, _ptr(self.w_root), _ptr(self.rz), _ptr(self.w), _ptr(self.z),
                                      _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_gaussian")
-        lam = 1.0 - self.new_weight
+        lam = L.qem_history_weight(int(t), float(self.new_weight), 0.0)
         for m_new, ema, mean, var, d in ((self.root_m, self.root_ema, self.root_mean, self.root_var, R),
                                          (self.gm, self.g_ema, self.q_mean, self.q_var, n)):
-            check(L.qem_mstep_categorical(0, 1, d, lam, self.var_floor, _ptr(m_new), _ptr(ema), _ptr(mean), _ptr(var),
-                                          None, None, None, _ptr(self.clamps), s), "qem_mstep_categorical")
+            check(L.qem_mstep_gaussian(d, lam, self.var_floor, _ptr(m_new), _ptr(ema), _ptr(mean), _ptr(var),
+                                       _ptr(self.clamps), s), "qem_mstep_gaussian")
 
     def set_state(self, st: dict) -> None:
         for k in ("root_mean", "root_var", "root_ema", "q_mean", "q_var", "g_ema"):

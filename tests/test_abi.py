@@ -134,3 +134,14 @@ def test_caller_workspace_matches_own_workspace():
 def _lib_desc(m):
     from paper_2503_08264_b200.qem import _desc
     return _desc(m)
+
+
+def test_history_weight_matches_the_oracle_schedule():
+    """qem_history_weight (host arithmetic, no GPU): lambda = 1 - w, or 1 - t^-p with a schedule
+    (R5; Theorem 1), equal to the oracle's."""
+    from oracle import oracle as orc
+    from paper_2503_08264_b200 import _lib
+    L = _lib.lib()
+    for t in (1, 2, 7, 100):
+        for w, p in ((0.3, 0.0), (0.05, 0.0), (0.3, 0.5), (0.3, 0.75)):
+            assert abs(L.qem_history_weight(t, w, p) - orc.lam(t, w, p)) <= 1e-15
