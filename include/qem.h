@@ -115,6 +115,10 @@ typedef int32_t qem_status;
 
 #define QEM_MAX_K 1024
 #define QEM_MAX_D 32
+/* The two-level family's latent dimensions d with compiled kernels (one translation unit each):
+   1-8, 10, 12, 14, 16, 18, 20, 24, 32 (= QEM_MAX_D); any other d is QEM_INVALID_MODEL.  Shared
+   memory that grows with d, K and J is checked against the device at context creation. */
+#define QEM_D_MENU_STR "1,2,3,4,5,6,7,8,10,12,14,16,18,20,24,32"
 
 /*
  * Plate-structured model description (a fixed menu).

@@ -11,8 +11,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["qem_api.cu", "qem_common.cu", "qem_two_level.cu", "qem_three_level.cu", "qem_expfam.cu", "qem_tables.cu", "qem_discrete.cu", "qem_predict.cu", "qem_gamma.cu", "qem_crossed.cu", "qem_nccl.cu", "qem_separable.cu"]
-HEADERS = ["qem_internal.h", "qem_device.cuh", "qem_forward.cuh", "qem_tc.cuh", os.path.join("..", "..", "include", "qem.h")]
+D_MENU = [1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 14, 16, 18, 20, 24, 32]  # qem_two_level.cu's QEM_D_LIST
+SOURCES = ["qem_api.cu", "qem_common.cu", "qem_two_level.cu"] + [f"qem_tl_d{d}.cu" for d in D_MENU] + [ "qem_three_level.cu", "qem_expfam.cu", "qem_tables.cu", "qem_discrete.cu", "qem_predict.cu", "qem_gamma.cu", "qem_crossed.cu", "qem_nccl.cu", "qem_separable.cu"]
+HEADERS = ["qem_internal.h", "qem_device.cuh", "qem_forward.cuh", "qem_tc.cuh", "qem_two_level.cuh", os.path.join("..", "..", "include", "qem.h")]
 LIB = os.path.join(HERE, "libqem.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -52,21 +53,33 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(objdir, exist_ok=True)
     objs = []
-    procs = []
+    cmds = []
     for s in SOURCES:
         o = os.path.join(objdir, s.replace(".cu", ".o"))
         cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+        cmds.append(cmd)
         objs.append(o)
-    for cmd, p in procs:
+    # at most one nvcc per core in flight (the per-D translation units are heavy)
+    jobs = max(1, int(os.environ.get("QEM_BUILD_JOBS", os.cpu_count() or 4)))
+    running = []
+    pending = list(cmds)
+
+    def reap(cmd, p):
         out, _ = p.communicate()
         if p.returncode != 0:
             sys.stderr.write(out.decode())
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
         if verbose:
             sys.stderr.write(out.decode())
+
+    while pending or running:
+        while pending and len(running) < jobs:
+            cmd = pending.pop(0)
+            running.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+        cmd, p = running.pop(0)
+        reap(cmd, p)
     tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "--cudart", "static",
                            "-o", tmp, *objs, "-ldl"])

@@ -58,7 +58,7 @@ qem_status validate(const qem_model_desc* d, char* msg, size_t cap) {
   if (!(d->prior_var > 0)) BAD("prior_var must be > 0");
   if (d->family == QEM_FAMILY_TWO_LEVEL) {
     if (d->d < 1 || d->d > QEM_MAX_D) BAD("d=%d out of range [1, %d]", d->d, QEM_MAX_D);
-    if (!qem::tl_supported_d(d->d)) BAD("d=%d has no compiled kernel (supported: 1,2,3,4,8,16,18)", d->d);
+    if (!qem::tl_supported_d(d->d)) BAD("d=%d has no compiled kernel (QEM_D_MENU: 1-8, 10, 12, 14, 16, 18, 20, 24, 32)", d->d);
     if (d->scale_kind < QEM_SCALE_FIXED || d->scale_kind > QEM_SCALE_LOGVAR) BAD("unknown scale_kind %d", d->scale_kind);
     if (d->scale_kind == QEM_SCALE_FIXED && !(d->fixed_var > 0)) BAD("fixed_var must be > 0");
     if (d->obs_kind == QEM_OBS_GAUSS) {

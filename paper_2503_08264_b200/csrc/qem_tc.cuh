@@ -1384,7 +1384,7 @@ __global__ void __launch_bounds__(GroupStage::THREADS, 1) k_moments_tc(TLArgs a)
 // Backward row extra slab of group i (K x 32 B) into `bx`, built by the aux warps two groups
 // ahead: [Eg pattern | 0 0 0 | rho], rho_k = log2 w_root(k) - log2e (h_k - h_*) (h = the
 // forward's re-centred message; -1e30 where w_root = 0).
-__device__ void bwd_bx(const TLArgs& a, int64_t i, unsigned char* bx, int atid) {
+__device__ __forceinline__ void bwd_bx(const TLArgs& a, int64_t i, unsigned char* bx, int atid) {
   constexpr int NT = 32;  // one aux warp builds the slabs
   const int K = a.K;
   const float hs = a.ws.hmsg[(size_t)i * K + a.ws.ref->k_star];

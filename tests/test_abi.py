@@ -55,8 +55,9 @@ def test_validate_and_shard_range(lib):
     bad = synth.config(1)
     bad.d = 5
     assert "d=5" in qem.model_validate(bad) or "OBS_GAUSS" in qem.model_validate(bad)
-    bad = synth.config(2, d=5)
-    assert "no compiled kernel" in qem.model_validate(bad)
+    assert qem.model_validate(synth.config(2, d=5)) is None  # d = 5 is on the compiled menu
+    bad = synth.config(2, d=11)
+    assert "no compiled kernel" in qem.model_validate(bad) and "QEM_D_MENU" in qem.model_validate(bad)
     # shards tile [0, n) exactly, contiguous, balanced within 1
     for n in (1, 7, 100_000, 10_000):
         for world in (1, 2, 3, 8):

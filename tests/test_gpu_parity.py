@@ -76,6 +76,11 @@ CASES = {
     # maximum K (QEM_MAX_K) on the FFMA tiles: d = 18 (config 2's dimension) and d = 3, ragged n
     "maxK_d18": dict(cid=2, n=29, K=1024),
     "maxK_d3_ragged": dict(cid=5, n=151, K=1024, d=3, J=9),
+    # the rest of the compiled d menu (QEM_D_MENU): FFMA tiles at d = 5, 20, 32, tensor cores at d = 12
+    "d5_K96": dict(cid=5, n=13, K=96, d=5, J=6),
+    "d12_tc_K256": dict(cid=5, n=17, K=256, d=12, J=9),
+    "d20_K64": dict(cid=2, n=7, K=64, d=20),
+    "d32_K40": dict(cid=5, n=5, K=40, d=32, J=4),
 }
 
 
@@ -173,3 +178,15 @@ def test_mstep_parity():
         np.testing.assert_allclose(out["q_var"][l], qv, rtol=2e-7)
     assert clamps >= 1 and (flags & 4)
     g.close()
+
+
+def test_d_menu_validation():
+    """d outside the compiled menu (QEM_D_MENU) is a model error, with the menu in the message; a
+    K / d combination whose shared memory exceeds the device limit is rejected at creation."""
+    from paper_2503_08264_b200 import _lib
+    from paper_2503_08264_b200.qem import QEM, model_validate
+    assert model_validate(synth.config(5, n=4, K=64, d=11)) and "QEM_D_MENU" in model_validate(synth.config(5, n=4, K=64, d=11))
+    for d in (1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 14, 16, 18, 20, 24, 32):
+        assert model_validate(synth.config(5 if d > 1 else 4, n=4, K=64, d=d)) is None, d
+    with pytest.raises(_lib.QemError, match="shared memory"):
+        QEM(synth.config(5, n=4, K=1024, d=32, J=5))
