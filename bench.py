@@ -589,26 +589,29 @@ def run_predictive_variant(m, data, dev, seed, S=100, reps=5):
 
 
 def run_crossed_variant(dev, steps=10):
-    """NEXT row f4 (R33): one QEM iteration of the Bus-shaped crossed-effects model (120
+    """NEXT row f4 (R33, R37): one QEM iteration of the Bus-shaped crossed-effects model (120
     year-borough groups, 40 journeys each, 57 companies, 6 journey types, K = 64): the K x K x J
-    observation contraction per group into fp64 tables + the table E-step."""
+    factor evaluated on chip (default) and through materialised fp64 tables."""
     import torch
     from paper_2503_08264_b200 import synth
     from paper_2503_08264_b200.qem import CrossedQEM
     cm = synth.bus_crossed()
-    g = CrossedQEM(cm, device=dev)
-    for t in range(1, 4):
-        g.step(t, 3)
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    st.record()
-    for t in range(4, 4 + steps):
-        g.step(t, 3)
-    en.record()
-    torch.cuda.synchronize()
-    ms = st.elapsed_time(en) / steps
-    return {"workload": f"bus-crossed n={cm.n} J={cm.J} C={cm.C} T={cm.T} K={cm.K}", "ms_per_step": ms,
-            "pair_obs_terms_per_s": cm.n * cm.K * cm.K * cm.J / (ms * 1e-3), "qem_iters_per_s": 1e3 / ms}
+    out = {"workload": f"bus-crossed n={cm.n} J={cm.J} C={cm.C} T={cm.T} K={cm.K}"}
+    for path, tables in (("on_chip", False), ("tables", True)):
+        g = CrossedQEM(cm, device=dev, tables=tables)
+        for t in range(1, 4):
+            g.step(t, 3)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        st.record()
+        for t in range(4, 4 + steps):
+            g.step(t, 3)
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / steps
+        out[path] = {"ms_per_step": ms, "pair_obs_terms_per_s": cm.n * cm.K * cm.K * cm.J / (ms * 1e-3),
+                     "qem_iters_per_s": 1e3 / ms}
+    return out
 
 
 def run_gamma_variant(dev, steps=10):

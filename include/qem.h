@@ -371,6 +371,16 @@ qem_status qem_tables_crossed(int64_t n, int32_t K, int32_t J, int32_t C, int32_
                               const float* d_q_mean, const float* d_q_var, const int32_t* d_comp,
                               const int32_t* d_jtype, const uint8_t* d_y, double* d_f_root, double* d_f,
                               void* stream);
+/* The crossed-effects E-step on chip (no n x K x K table; R37): the factor above is
+   evaluated per pair inside the forward (one block per group, online log-sum-exp over k') and again
+   inside the backward, fp64 as qem_tables_crossed + qem_estep_tables, same outputs (d_f_root [K],
+   d_g [n][K], d_log_pe [1], d_w_root [K], d_w [n][K]).  K <= QEM_MAX_K; K x J row offsets must fit in
+   shared memory (else QEM_INVALID_ARGUMENT). */
+qem_status qem_estep_crossed(int64_t n, int32_t K, int32_t J, int32_t C, int32_t T, const float* d_root_z,
+                             const float* d_root_mean, const float* d_root_var, const float* d_z, const float* d_q_mean,
+                             const float* d_q_var, const int32_t* d_comp, const int32_t* d_jtype, const uint8_t* d_y,
+                             double* d_f_root, double* d_g, double* d_log_pe, double* d_w_root, double* d_w,
+                             void* stream);
 qem_status qem_moments_gaussian(int64_t n, int32_t K, int32_t R, const double* d_w_root, const float* d_root_z,
                                 const double* d_w, const float* d_z, double* d_root_m, double* d_gm,
                                 void* stream);

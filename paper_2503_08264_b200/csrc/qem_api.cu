@@ -668,6 +668,30 @@ qem_status qem_tables_crossed(int64_t n, int32_t K, int32_t J, int32_t C, int32_
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_tables_crossed");
 }
 
+qem_status qem_estep_crossed(int64_t n, int32_t K, int32_t J, int32_t C, int32_t T, const float* d_root_z,
+                             const float* d_root_mean, const float* d_root_var, const float* d_z, const float* d_q_mean,
+                             const float* d_q_var, const int32_t* d_comp, const int32_t* d_jtype, const uint8_t* d_y,
+                             double* d_f_root, double* d_g, double* d_log_pe, double* d_w_root, double* d_w,
+                             void* stream) {
+  if (n < 0 || K < 1 || K > QEM_MAX_K || J < 0 || C < 1 || T < 1) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root || !d_log_pe || !d_w_root ||
+      (n > 0 && (!d_z || !d_q_mean || !d_q_var || !d_g || !d_w || (J > 0 && (!d_comp || !d_jtype || !d_y)))))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  {  // the backward stages K x J row offsets (fp64) per group in shared memory
+    int dev = 0, optin = 0;
+    const size_t need = (size_t)(2 * K + (size_t)K * J) * sizeof(double) + J + 8;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && optin > 0 &&
+        need > (size_t)optin)
+      return fail(QEM_INVALID_ARGUMENT, "K=%d, J=%d needs %zu bytes of shared memory per block (device limit %d)", K, J,
+                  need, optin);
+  }
+  const cudaError_t e = qem::launch_crossed_estep(n, K, J, C, T, d_root_z, d_root_mean, d_root_var, d_z, d_q_mean,
+                                                  d_q_var, d_comp, d_jtype, d_y, d_f_root, d_g, d_log_pe, d_w_root, d_w,
+                                                  (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_estep_crossed");
+}
+
 qem_status qem_moments_gaussian(int64_t n, int32_t K, int32_t R, const double* d_w_root, const float* d_root_z,
                                 const double* d_w, const float* d_z, double* d_root_m, double* d_gm, void* stream) {
   if (n < 0 || K < 1 || R < 1) return fail(QEM_INVALID_ARGUMENT, "bad sizes");

@@ -100,6 +100,138 @@ __global__ void __launch_bounds__(256) k_crossed_moments(int64_t n, int K, int R
   }
 }
 
+// ---- the same E-step on chip (no n x K x K table): the pair factor is evaluated where it is used.
+// Per group (one block): the group's samples, labels and the crossed root weights' index tables in
+// shared memory; the forward's thread per row k keeps its J offsets o_j = cw^k_{c_j} + jw^k_{t_j}
+// in shared memory and takes an online (max, sum) over k'; the backward's thread per column k'
+// recomputes the pair against every row.  fp64, the arithmetic of k_crossed_tables.
+struct CrossedArgs {
+  int64_t n;
+  int K, J, C, T;
+  const float *rz, *z, *qm, *qv;
+  const int32_t *comp, *jtype;
+  const uint8_t* y;
+};
+
+__device__ __forceinline__ double crossed_pair(double w, double mu, const double* o, const uint8_t* yi, int J,
+                                               double colterm) {
+  double lik = 0.0;
+  for (int j = 0; j < J; ++j) {
+    const double eta = w + o[j];
+    lik += (yi[j] ? eta : 0.0) - (fmax(eta, 0.0) + log1p(exp(-fabs(eta))));
+  }
+  const double dw = w - mu;
+  return -0.5 * dw * dw + colterm + lik;
+}
+
+// shared memory: [K] w, [K] column terms, [J] labels (bytes), [blockDim][J] row offsets
+__global__ void __launch_bounds__(256) k_crossed_fwd(CrossedArgs a, double* __restrict__ g) {
+  extern __shared__ double sm[];
+  const int K = a.K, J = a.J;
+  const int64_t i = blockIdx.x;
+  double* sw = sm;
+  double* sc = sw + K;
+  double* so = sc + K;                                   // [blockDim][J]
+  uint8_t* sy = reinterpret_cast<uint8_t*>(so + (size_t)blockDim.x * J);
+  const double m = a.qm[i], v = a.qv[i];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const double w = a.z[i * K + k], dq = w - m;
+    sw[k] = w;
+    sc[k] = 0.5 * log(v) + 0.5 * dq * dq / v;  // - log N(w; m, v) + the cancelled 2 pi
+  }
+  for (int j = threadIdx.x; j < J; j += blockDim.x) sy[j] = a.y[i * J + j];
+  __syncthreads();
+  const double lk = log((double)K);
+  double* o = so + (size_t)threadIdx.x * J;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    for (int j = 0; j < J; ++j)
+      o[j] = (double)a.rz[(int64_t)(1 + a.comp[i * J + j]) * K + k] + (double)a.rz[(int64_t)(1 + a.C + a.jtype[i * J + j]) * K + k];
+    const double mu = a.rz[k];
+    double mx = -CUDART_INF, s = 0.0;
+    for (int kp = 0; kp < K; ++kp) {
+      const double t = crossed_pair(sw[kp], mu, o, sy, J, sc[kp]);
+      if (t > mx) {
+        s = (mx == -CUDART_INF ? 0.0 : s * exp(mx - t)) + 1.0;
+        mx = t;
+      } else {
+        s += exp(t - mx);
+      }
+    }
+    g[i * K + k] = mx == -CUDART_INF ? -CUDART_INF : mx + log(s) - lk;
+  }
+}
+
+// shared memory: [K] c_k = ln w_root(k) - ln K - g_i(k), [K] mu^k, [K][J] row offsets, [J] labels
+__global__ void __launch_bounds__(256) k_crossed_bwd(CrossedArgs a, const double* __restrict__ g,
+                                                     const double* __restrict__ w_root, double* __restrict__ w) {
+  extern __shared__ double sm[];
+  const int K = a.K, J = a.J;
+  const int64_t i = blockIdx.x;
+  double* sc = sm;
+  double* smu = sc + K;
+  double* so = smu + K;  // [K][J]
+  uint8_t* sy = reinterpret_cast<uint8_t*>(so + (size_t)K * J);
+  const double lk = log((double)K);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const double wr = w_root[k];
+    sc[k] = wr > 0.0 ? log(wr) - lk - g[i * K + k] : -CUDART_INF;  // zero-weight rows drop out
+    smu[k] = a.rz[k];
+  }
+  for (int e = threadIdx.x; e < K * J; e += blockDim.x) {
+    const int k = e / J, j = e - k * J;
+    so[e] = (double)a.rz[(int64_t)(1 + a.comp[i * J + j]) * K + k] + (double)a.rz[(int64_t)(1 + a.C + a.jtype[i * J + j]) * K + k];
+  }
+  for (int j = threadIdx.x; j < J; j += blockDim.x) sy[j] = a.y[i * J + j];
+  __syncthreads();
+  const double m = a.qm[i], v = a.qv[i];
+  for (int kp = threadIdx.x; kp < K; kp += blockDim.x) {
+    const double wv = a.z[i * K + kp], dq = wv - m;
+    const double col = 0.5 * log(v) + 0.5 * dq * dq / v;
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double c = sc[k];
+      if (c > -CUDART_INF) acc += exp(crossed_pair(wv, smu[k], so + (size_t)k * J, sy, J, col) + c);
+    }
+    w[i * K + kp] = acc;
+  }
+}
+
+__global__ void k_crossed_root(int K, int R, const float* __restrict__ rz, const float* __restrict__ rm,
+                               const float* __restrict__ rv, double* __restrict__ f_root) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < R; ++r) {
+      const double x = rz[(int64_t)r * K + k], v = rv[r], dx = x - (double)rm[r];
+      s += -0.5 * x * x + 0.5 * log(v) + 0.5 * dx * dx / v;
+    }
+    f_root[k] = s;
+  }
+}
+
+cudaError_t launch_crossed_estep(int64_t n, int K, int J, int C, int T, const float* rz, const float* rm,
+                                 const float* rv, const float* z, const float* qm, const float* qv,
+                                 const int32_t* comp, const int32_t* jtype, const uint8_t* y, double* f_root,
+                                 double* g, double* log_pe, double* w_root, double* w, cudaStream_t st) {
+  CrossedArgs a{n, K, J, C, T, rz, z, qm, qv, comp, jtype, y};
+  k_crossed_root<<<(K + 127) / 128, 128, 0, st>>>(K, 1 + C + T, rz, rm, rv, f_root);
+  const int threads = K >= 128 ? 128 : (K + 31) / 32 * 32;
+  if (n > 0) {
+    const size_t sf = (size_t)(2 * K + (size_t)threads * J) * sizeof(double) + J + 8;
+    cudaError_t e = cudaFuncSetAttribute(k_crossed_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
+    if (e != cudaSuccess) return e;
+    k_crossed_fwd<<<(unsigned)n, threads, sf, st>>>(a, g);
+  }
+  cudaError_t e = launch_plate_root(n, K, f_root, g, w, log_pe, w_root, st);
+  if (e != cudaSuccess) return e;
+  if (n > 0) {
+    const size_t sb = (size_t)(2 * K + (size_t)K * J) * sizeof(double) + J + 8;
+    e = cudaFuncSetAttribute(k_crossed_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    if (e != cudaSuccess) return e;
+    k_crossed_bwd<<<(unsigned)n, threads, sb, st>>>(a, g, w_root, w);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_crossed_tables(int64_t n, int K, int J, int C, int T, const float* rz, const float* rm,
                                   const float* rv, const float* z, const float* qm, const float* qv, const int32_t* comp,
                                   const int32_t* jtype, const uint8_t* y, double* f_root, double* f, cudaStream_t st) {

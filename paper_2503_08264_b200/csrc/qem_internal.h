@@ -164,6 +164,10 @@ cudaError_t launch_beta_moments(int64_t n, int K, const double* w_root, const fl
 cudaError_t launch_crossed_tables(int64_t n, int K, int J, int C, int T, const float* rz, const float* rm,
                                   const float* rv, const float* z, const float* qm, const float* qv, const int32_t* comp,
                                   const int32_t* jtype, const uint8_t* y, double* f_root, double* f, cudaStream_t st);
+cudaError_t launch_crossed_estep(int64_t n, int K, int J, int C, int T, const float* rz, const float* rm,
+                                 const float* rv, const float* z, const float* qm, const float* qv,
+                                 const int32_t* comp, const int32_t* jtype, const uint8_t* y, double* f_root,
+                                 double* g, double* log_pe, double* w_root, double* w, cudaStream_t st);
 cudaError_t launch_crossed_moments(int64_t n, int K, int R, const double* w_root, const float* rz, const double* w,
                                    const float* z, double* root_m, double* gm, cudaStream_t st);
 cudaError_t launch_sample_rows(int64_t rows, int K, int level, uint64_t seed, int32_t iter, const float* qm,

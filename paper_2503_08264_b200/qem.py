@@ -663,10 +663,12 @@ class CrossedQEM:
     qem_estep_tables + qem_moments_gaussian + qem_mstep_categorical (n = 0: the Gaussian EMA +
     M-step of the root dims, then of the group latents), all on device."""
 
-    def __init__(self, cm, *, new_weight=0.3, var_floor=1e-8, device="cuda"):
+    def __init__(self, cm, *, new_weight=0.3, var_floor=1e-8, device="cuda", tables=False):
+        """tables=False (default): qem_estep_crossed evaluates the K x K x J factor on chip; True: the
+        materialised fp64 tables (qem_tables_crossed + qem_estep_tables)."""
         if not torch.cuda.is_available():
             raise _lib.QemError("CrossedQEM needs a CUDA device (there is no CPU fallback)")
-        self.cm, self.device = cm, torch.device(device)
+        self.cm, self.device, self.tables = cm, torch.device(device), bool(tables)
         self.new_weight, self.var_floor = new_weight, var_floor
         n, K, R = cm.n, cm.K, cm.R
         f32 = dict(dtype=torch.float32, device=self.device)
@@ -678,7 +680,8 @@ class CrossedQEM:
         self.q_mean, self.q_var = torch.zeros(n, **f32), torch.ones(n, **f32)
         self.g_ema = torch.tensor([[0.0, 1.0]] * n, **f64)
         self.rz, self.z = torch.empty(R, K, **f32), torch.empty(n, K, **f32)
-        self.f_root, self.f = torch.empty(K, **f64), torch.empty(n, K, K, **f64)
+        self.f_root = torch.empty(K, **f64)
+        self.f = torch.empty(n, K, K, **f64) if self.tables else None
         self.g, self.w = torch.empty(n, K, **f64), torch.empty(n, K, **f64)
         self.w_root, self.log_pe = torch.empty(K, **f64), torch.empty(1, **f64)
         self.root_m, self.gm = torch.empty(R, 2, **f64), torch.empty(n, 2, **f64)
@@ -693,12 +696,18 @@ class CrossedQEM:
               "qem_sample_normal")
         check(L.qem_sample_normal(n, K, 1, seed, t, _ptr(self.q_mean), _ptr(self.q_var),
                                   _ptr(eps) if eps is not None else None, _ptr(self.z), s), "qem_sample_normal")
-        check(L.qem_tables_crossed(n, K, cm.J, cm.C, cm.T, _ptr(self.rz), _ptr(self.root_mean), _ptr(self.root_var),
-                                   _ptr(self.z), _ptr(self.q_mean), _ptr(self.q_var), _ptr(self.comp),
-                                   _ptr(self.jtype), _ptr(self.y), _ptr(self.f_root), _ptr(self.f), s),
-              "qem_tables_crossed")
-        check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
-                                 _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        if self.tables:
+            check(L.qem_tables_crossed(n, K, cm.J, cm.C, cm.T, _ptr(self.rz), _ptr(self.root_mean),
+                                       _ptr(self.root_var), _ptr(self.z), _ptr(self.q_mean), _ptr(self.q_var),
+                                       _ptr(self.comp), _ptr(self.jtype), _ptr(self.y), _ptr(self.f_root),
+                                       _ptr(self.f), s), "qem_tables_crossed")
+            check(L.qem_estep_tables(n, K, _ptr(self.f_root), _ptr(self.f), _ptr(self.g), _ptr(self.log_pe),
+                                     _ptr(self.w_root), _ptr(self.w), s), "qem_estep_tables")
+        else:
+            check(L.qem_estep_crossed(n, K, cm.J, cm.C, cm.T, _ptr(self.rz), _ptr(self.root_mean), _ptr(self.root_var),
+                                      _ptr(self.z), _ptr(self.q_mean), _ptr(self.q_var), _ptr(self.comp),
+                                      _ptr(self.jtype), _ptr(self.y), _ptr(self.f_root), _ptr(self.g),
+                                      _ptr(self.log_pe), _ptr(self.w_root), _ptr(self.w), s), "qem_estep_crossed")
         check(L.qem_moments_gaussian(n, K, R, _ptr(self.w_root), _ptr(self.rz), _ptr(self.w), _ptr(self.z),
                                      _ptr(self.root_m), _ptr(self.gm), s), "qem_moments_gaussian")
         lam = L.qem_history_weight(int(t), float(self.new_weight), 0.0)

@@ -46,12 +46,13 @@ def test_evidence_estimate_is_unbiased():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("use_tables", [False, True], ids=["on_chip", "tables"])
 @pytest.mark.parametrize("n,J,C,T,K,steps", [(40, 12, 7, 3, 32, 3), (120, 40, 57, 6, 64, 2), (3, 1, 1, 1, 5, 2)])
-def test_device_crossed_qem_teacher_forced(n, J, C, T, K, steps):
+def test_device_crossed_qem_teacher_forced(n, J, C, T, K, steps, use_tables):
     import torch
     from paper_2503_08264_b200.qem import CrossedQEM
     cm = synth.bus_crossed(n=n, J=J, C=C, T=T, K=K, seed=4)
-    g = CrossedQEM(cm)
+    g = CrossedQEM(cm, tables=use_tables)
     state = oc.initial_state(cm)
     for t in range(1, steps + 1):
         g.set_state(state)
@@ -64,7 +65,10 @@ def test_device_crossed_qem_teacher_forced(n, J, C, T, K, steps):
         tag = f"crossed n{n} K{K} t={t}"
         np.testing.assert_array_equal(g.rz.cpu().numpy(), ref["rz"], err_msg=tag)
         np.testing.assert_array_equal(g.z.cpu().numpy(), ref["z"], err_msg=tag)
-        np.testing.assert_allclose(g.f.cpu().numpy(), ref["f"], rtol=1e-11, atol=1e-10, err_msg=tag)
+        if use_tables:
+            np.testing.assert_allclose(g.f.cpu().numpy(), ref["f"], rtol=1e-11, atol=1e-10, err_msg=tag)
+        else:  # no table: the plate messages g_i(k) = lse_k' f_i(k, k') - ln K of the oracle's tables
+            np.testing.assert_allclose(g.g.cpu().numpy(), ref["est"]["g"], rtol=1e-11, atol=1e-10, err_msg=tag)
         assert abs(float(g.log_pe.item()) - ref["est"]["log_pe"]) <= 1e-10 * abs(ref["est"]["log_pe"]), tag
         np.testing.assert_allclose(g.w_root.cpu().numpy(), ref["est"]["w_root"], rtol=1e-9, atol=1e-13, err_msg=tag)
         np.testing.assert_allclose(g.w.cpu().numpy(), ref["est"]["w"], rtol=1e-9, atol=1e-13, err_msg=tag)
