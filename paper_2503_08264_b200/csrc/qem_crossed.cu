@@ -124,40 +124,59 @@ __device__ __forceinline__ double crossed_pair(double w, double mu, const double
   return -0.5 * dw * dw + colterm + lik;
 }
 
-// shared memory: [K] w, [K] column terms, [J] labels (bytes), [blockDim][J] row offsets
+// Four threads per row (forward) / per column (backward), each over every 4th partner index, their
+// partial (max, sum) / sums combined by shuffles: the fp64 softplus chains are long, so the block
+// needs the threads for latency (one group per block).
+constexpr int kCrossSplit = 4;
+
+// shared memory: [K] w, [K] column terms, [blockDim / 4][J] row offsets, [J] labels (bytes)
 __global__ void __launch_bounds__(256) k_crossed_fwd(CrossedArgs a, double* __restrict__ g) {
   extern __shared__ double sm[];
-  const int K = a.K, J = a.J;
+  const int K = a.K, J = a.J, tid = threadIdx.x, part = tid % kCrossSplit;
+  const int rows_per_pass = blockDim.x / kCrossSplit, rr = tid / kCrossSplit;
   const int64_t i = blockIdx.x;
   double* sw = sm;
   double* sc = sw + K;
-  double* so = sc + K;                                   // [blockDim][J]
-  uint8_t* sy = reinterpret_cast<uint8_t*>(so + (size_t)blockDim.x * J);
+  double* so = sc + K;  // [rows_per_pass][J]
+  uint8_t* sy = reinterpret_cast<uint8_t*>(so + (size_t)rows_per_pass * J);
   const double m = a.qm[i], v = a.qv[i];
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+  for (int k = tid; k < K; k += blockDim.x) {
     const double w = a.z[i * K + k], dq = w - m;
     sw[k] = w;
     sc[k] = 0.5 * log(v) + 0.5 * dq * dq / v;  // - log N(w; m, v) + the cancelled 2 pi
   }
-  for (int j = threadIdx.x; j < J; j += blockDim.x) sy[j] = a.y[i * J + j];
-  __syncthreads();
+  for (int j = tid; j < J; j += blockDim.x) sy[j] = a.y[i * J + j];
   const double lk = log((double)K);
-  double* o = so + (size_t)threadIdx.x * J;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    for (int j = 0; j < J; ++j)
-      o[j] = (double)a.rz[(int64_t)(1 + a.comp[i * J + j]) * K + k] + (double)a.rz[(int64_t)(1 + a.C + a.jtype[i * J + j]) * K + k];
-    const double mu = a.rz[k];
+  for (int k0 = 0; k0 < K; k0 += rows_per_pass) {
+    __syncthreads();  // (first pass: the column data; later: the previous rows' offsets are consumed)
+    const int k = k0 + rr;
+    double* o = so + (size_t)rr * J;
+    if (k < K)
+      for (int j = part; j < J; j += kCrossSplit)
+        o[j] = (double)a.rz[(int64_t)(1 + a.comp[i * J + j]) * K + k] +
+               (double)a.rz[(int64_t)(1 + a.C + a.jtype[i * J + j]) * K + k];
+    __syncthreads();
     double mx = -CUDART_INF, s = 0.0;
-    for (int kp = 0; kp < K; ++kp) {
-      const double t = crossed_pair(sw[kp], mu, o, sy, J, sc[kp]);
-      if (t > mx) {
-        s = (mx == -CUDART_INF ? 0.0 : s * exp(mx - t)) + 1.0;
-        mx = t;
-      } else {
-        s += exp(t - mx);
+    if (k < K) {
+      const double mu = a.rz[k];
+      for (int kp = part; kp < K; kp += kCrossSplit) {
+        const double t = crossed_pair(sw[kp], mu, o, sy, J, sc[kp]);
+        if (t > mx) {
+          s = (mx == -CUDART_INF ? 0.0 : s * exp(mx - t)) + 1.0;
+          mx = t;
+        } else {
+          s += exp(t - mx);
+        }
       }
     }
-    g[i * K + k] = mx == -CUDART_INF ? -CUDART_INF : mx + log(s) - lk;
+#pragma unroll
+    for (int off = 1; off < kCrossSplit; off <<= 1) {  // combine the row's partial (max, sum)
+      const double om = __shfl_xor_sync(0xffffffffu, mx, off), os = __shfl_xor_sync(0xffffffffu, s, off);
+      const double nm = fmax(mx, om);
+      s = (mx == -CUDART_INF ? 0.0 : s * exp(mx - nm)) + (om == -CUDART_INF ? 0.0 : os * exp(om - nm));
+      mx = nm;
+    }
+    if (k < K && part == 0) g[i * K + k] = mx == -CUDART_INF ? -CUDART_INF : mx + log(s) - lk;
   }
 }
 
@@ -165,34 +184,40 @@ __global__ void __launch_bounds__(256) k_crossed_fwd(CrossedArgs a, double* __re
 __global__ void __launch_bounds__(256) k_crossed_bwd(CrossedArgs a, const double* __restrict__ g,
                                                      const double* __restrict__ w_root, double* __restrict__ w) {
   extern __shared__ double sm[];
-  const int K = a.K, J = a.J;
+  const int K = a.K, J = a.J, tid = threadIdx.x, part = tid % kCrossSplit;
+  const int cols_per_pass = blockDim.x / kCrossSplit;
   const int64_t i = blockIdx.x;
   double* sc = sm;
   double* smu = sc + K;
   double* so = smu + K;  // [K][J]
   uint8_t* sy = reinterpret_cast<uint8_t*>(so + (size_t)K * J);
   const double lk = log((double)K);
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+  for (int k = tid; k < K; k += blockDim.x) {
     const double wr = w_root[k];
     sc[k] = wr > 0.0 ? log(wr) - lk - g[i * K + k] : -CUDART_INF;  // zero-weight rows drop out
     smu[k] = a.rz[k];
   }
-  for (int e = threadIdx.x; e < K * J; e += blockDim.x) {
+  for (int e = tid; e < K * J; e += blockDim.x) {
     const int k = e / J, j = e - k * J;
     so[e] = (double)a.rz[(int64_t)(1 + a.comp[i * J + j]) * K + k] + (double)a.rz[(int64_t)(1 + a.C + a.jtype[i * J + j]) * K + k];
   }
-  for (int j = threadIdx.x; j < J; j += blockDim.x) sy[j] = a.y[i * J + j];
+  for (int j = tid; j < J; j += blockDim.x) sy[j] = a.y[i * J + j];
   __syncthreads();
   const double m = a.qm[i], v = a.qv[i];
-  for (int kp = threadIdx.x; kp < K; kp += blockDim.x) {
-    const double wv = a.z[i * K + kp], dq = wv - m;
-    const double col = 0.5 * log(v) + 0.5 * dq * dq / v;
+  for (int kp0 = 0; kp0 < K; kp0 += cols_per_pass) {
+    const int kp = kp0 + tid / kCrossSplit;
     double acc = 0.0;
-    for (int k = 0; k < K; ++k) {
-      const double c = sc[k];
-      if (c > -CUDART_INF) acc += exp(crossed_pair(wv, smu[k], so + (size_t)k * J, sy, J, col) + c);
+    if (kp < K) {
+      const double wv = a.z[i * K + kp], dq = wv - m;
+      const double col = 0.5 * log(v) + 0.5 * dq * dq / v;
+      for (int k = part; k < K; k += kCrossSplit) {
+        const double c = sc[k];
+        if (c > -CUDART_INF) acc += exp(crossed_pair(wv, smu[k], so + (size_t)k * J, sy, J, col) + c);
+      }
     }
-    w[i * K + kp] = acc;
+#pragma unroll
+    for (int off = 1; off < kCrossSplit; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (kp < K && part == 0) w[i * K + kp] = acc;
   }
 }
 
@@ -214,9 +239,9 @@ cudaError_t launch_crossed_estep(int64_t n, int K, int J, int C, int T, const fl
                                  double* g, double* log_pe, double* w_root, double* w, cudaStream_t st) {
   CrossedArgs a{n, K, J, C, T, rz, z, qm, qv, comp, jtype, y};
   k_crossed_root<<<(K + 127) / 128, 128, 0, st>>>(K, 1 + C + T, rz, rm, rv, f_root);
-  const int threads = K >= 128 ? 128 : (K + 31) / 32 * 32;
+  const int threads = 256;  // kCrossSplit threads per row / column, 64 rows / columns per pass
   if (n > 0) {
-    const size_t sf = (size_t)(2 * K + (size_t)threads * J) * sizeof(double) + J + 8;
+    const size_t sf = (size_t)(2 * K + (size_t)(threads / kCrossSplit) * J) * sizeof(double) + J + 8;
     cudaError_t e = cudaFuncSetAttribute(k_crossed_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
     if (e != cudaSuccess) return e;
     k_crossed_fwd<<<(unsigned)n, threads, sf, st>>>(a, g);

@@ -351,9 +351,11 @@ class QEM:
         if events is None:
             handles = [None] * 4
         else:
+            events = list(events) + [None] * (4 - len(events))
             for e in events:  # torch creates the CUDA event lazily
-                e.record()
-            handles = [ctypes.c_void_p(e.cuda_event) for e in events]
+                if e is not None:
+                    e.record()
+            handles = [ctypes.c_void_p(e.cuda_event) if e is not None else None for e in events]
         self._events = events
         check(lib().qem_set_kernel_events(self.ctx, *handles), "qem_set_kernel_events")
 
@@ -663,9 +665,11 @@ class CrossedQEM:
     qem_estep_tables + qem_moments_gaussian + qem_mstep_categorical (n = 0: the Gaussian EMA +
     M-step of the root dims, then of the group latents), all on device."""
 
-    def __init__(self, cm, *, new_weight=0.3, var_floor=1e-8, device="cuda", tables=False):
-        """tables=False (default): qem_estep_crossed evaluates the K x K x J factor on chip; True: the
-        materialised fp64 tables (qem_tables_crossed + qem_estep_tables)."""
+    def __init__(self, cm, *, new_weight=0.3, var_floor=1e-8, device="cuda", tables=True):
+        """tables=True (default): the materialised fp64 tables (qem_tables_crossed + qem_estep_tables;
+        n K^2 = 4 MB on the Bus shape, each pair's J-term sum evaluated once); False: qem_estep_crossed
+        evaluates the K x K x J factor on chip, twice per pair (forward, backward) -- 3x the time here
+        (R37)."""
         if not torch.cuda.is_available():
             raise _lib.QemError("CrossedQEM needs a CUDA device (there is no CPU fallback)")
         self.cm, self.device, self.tables = cm, torch.device(device), bool(tables)
