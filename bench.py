@@ -432,10 +432,10 @@ def run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce):
     """Same iteration through the public API with host buffers: every step's observations go H2D
     from pinned memory and its log Pe and new Q (M-step result) come back D2H.  The copies run on
     a second stream, pipelined with the compute (B200 rule: overlap copies with compute): step
-    t+1's observations upload while step t's backward runs (the column prep is their only
-    reader), and step t's results download while step t+1 samples and runs its forward.  Every
-    step's copies lie inside the timed region (the first upload starts after the start event,
-    the end event waits for the last download)."""
+    t+1's observations upload while step t's pair kernels run (the column prep is their only
+    reader), and step t's results -- snapshotted on the device after its M-step -- download while
+    step t+1 runs.  Every step's copies lie inside the timed region (the first upload starts after
+    the start event, the end event waits for the last download)."""
     import torch
     import torch.distributed as dist
     stream = torch.cuda.current_stream()
@@ -458,12 +458,23 @@ def run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce):
         e.record(cs)
         return e
 
+    # the step's results are snapshotted on the device (D2D, in stream order) and downloaded from the
+    # snapshot, so the next step's M-step never waits for the PCIe copy of this one
+    stage_lp = torch.empty_like(g.log_pe)
+    stage_q = [(torch.empty_like(lv["q_mean"]), torch.empty_like(lv["q_var"])) for lv in g.levels]
+
+    def snapshot():
+        stage_lp.copy_(g.log_pe)
+        for (sm, sv), lv in zip(stage_q, g.levels):
+            sm.copy_(lv["q_mean"])
+            sv.copy_(lv["q_var"])
+
     def download():
         with torch.cuda.stream(cs):
-            lp_host.copy_(g.log_pe, non_blocking=True)
-            for o, ov, lv in zip(outs, outv, g.levels):
-                o.copy_(lv["q_mean"], non_blocking=True)
-                ov.copy_(lv["q_var"], non_blocking=True)
+            lp_host.copy_(stage_lp, non_blocking=True)
+            for o, ov, (sm, sv) in zip(outs, outv, stage_q):
+                o.copy_(sm, non_blocking=True)
+                ov.copy_(sv, non_blocking=True)
         e = ev()
         e.record(cs)
         return e
@@ -473,49 +484,81 @@ def run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce):
     prep_done = torch.cuda.Event()
     g.set_kernel_events([prep_done])
 
-    def run(n, t):
-        x_ready, d2h_done = upload(), None
+    def run(n, t, copies=True):
+        if not copies:  # control: the same issue order and events, without the host copies
+            x_ready, d2h_done = ev(), None
+            x_ready.record(cs)
+        else:
+            x_ready, d2h_done = upload(), None
         for s in range(n):
             g.sample_q(seed=seed, iter=t)
             stream.wait_event(x_ready)           # this step's observations are on the device
             g.estep_forward()
-            if s + 1 < n:                        # next step's upload overlaps this step's pair kernels
+            if s + 1 < n:                        # next step's upload overlaps this step's forward pair kernel
                 cs.wait_event(prep_done)
-                x_ready = upload()
+                if copies:
+                    x_ready = upload()
+                else:
+                    x_ready = ev()
+                    x_ready.record(cs)
+                # ... and is done before the backward: an H2D copy running under config 4's FFMA backward
+                # measured 0.5 ms of slowdown, under the forward none (tools/e2e_diag.py)
+                stream.wait_event(x_ready)
             allreduce()
-            if d2h_done is not None:
-                stream.wait_event(d2h_done)      # the previous step's results have left the device
             g.estep_backward()
             g.mstep(t)
+            if d2h_done is not None:
+                stream.wait_event(d2h_done)      # the previous snapshot has left the device (a step ago)
+            snapshot()
             done = ev()
             done.record(stream)
             cs.wait_event(done)
-            d2h_done = download()
+            if copies:
+                d2h_done = download()
+            else:
+                d2h_done = ev()
+                d2h_done.record(cs)
             t += 1
         stream.wait_event(d2h_done)
         return t
 
-    t = run(2, t)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st.record(stream)
-    cs.wait_event(st)
-    t = run(args.steps, t)
-    en.record(stream)
-    torch.cuda.synchronize()
+    from paper_2503_08264_b200 import synth
+
+    def restart():
+        """Back to the main measurement's start (Q = N(0,1), m_0 = (0, 1), t = 1): the per-step cost
+        depends on the regime of the run (the forward's tile modes), so the e2e loop times the same
+        iterations W+1 .. W+K as the device-timed line."""
+        g.set_q(synth.initial_q(m))
+        g.set_state([(q, v) for q, v in synth.initial_q(m)])
+        return 1
+
+    def timed(copies):
+        t = run(args.warmup, restart(), copies)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record(stream)
+        cs.wait_event(st)
+        run(args.steps, t, copies)
+        en.record(stream)
+        torch.cuda.synchronize()
+        return st.elapsed_time(en)
+
+    ms = timed(True)
+    ms_ctrl = timed(False)  # control: the same loop and iterations without the copies
     g.set_kernel_events(None)
-    ms = st.elapsed_time(en)
     if world > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = tt.item()
     ms_step = ms / args.steps
     return {"value": m.pairs / (ms_step * 1e-3), "unit": "factor-pairs/s", "ms_per_step": ms_step,
+            "ms_per_step_same_loop_without_copies": ms_ctrl / args.steps,
             "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-            "overlap": "copies on a second stream: step t+1's upload under step t's pair kernels (after the column "
-                       "prep, the observations' only reader), step t's download under step t+1's sampler and forward"}
+            "overlap": "copies on a second stream: step t+1's upload under step t's forward pair kernel (after the "
+                       "column prep, the observations' only reader; done before the backward); step t's results "
+                       "snapshotted on the device (D2D) and downloaded under step t+1"}
 
 
 def run_fresh_variant(args, m, data, dev, seed):
