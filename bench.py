@@ -8,7 +8,8 @@
 
 Contract:
   * a step is one whole hot-path pass = one QEM iteration (Alg. 1):
-    Philox sampler (K1) -> forward pair tiles (K2) -> [NCCL all-reduce of the
+    Philox sampler (K1; fused into the column prep on the tensor-core path) -> forward pair
+    tiles (K2) -> [NCCL all-reduce of the
     (K+1) fp64 plate sums when N > 1, run inside libqem: qem_estep_reduce] -> root +
     backward weights/moments (K3, K4)
     -> EMA + M-step (K5), on BASELINE config C (default 5; config 4 with --config 4);
@@ -232,9 +233,7 @@ def measure_step(m, args, world, rank, dev, in_library, seed):
         # ev: [fwd kernel start, fwd kernel end, bwd kernel start, bwd kernel end, allreduce start, end]
         if ev:
             g.set_kernel_events(ev[:4])
-        g.sample_q(seed=seed, iter=t)
-        launched[0] += g.kernel_launches()
-        g.estep_forward()
+        g.sample_estep_forward(seed, t)  # sampler + forward (the draws fused into the column prep on the TC path)
         launched[0] += g.kernel_launches()
         if ev:
             ev[4].record(stream)
@@ -491,9 +490,8 @@ def run_e2e(args, g, m, data, world, rank, dev, seed, t, allreduce):
         else:
             x_ready, d2h_done = upload(), None
         for s in range(n):
-            g.sample_q(seed=seed, iter=t)
             stream.wait_event(x_ready)           # this step's observations are on the device
-            g.estep_forward()
+            g.sample_estep_forward(seed, t)
             if s + 1 < n:                        # next step's upload overlaps this step's forward pair kernel
                 cs.wait_event(prep_done)
                 if copies:

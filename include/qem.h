@@ -274,6 +274,11 @@ qem_status qem_estep(qem_ctx* ctx, void* stream);
 /* Phase 1: sample prep, unary terms, pair-tile forward log-sum-exp; leaves the
    local plate sum [G(0..K-1), sum_i c_i] (fp64) in the reduce buffer. */
 qem_status qem_estep_forward(qem_ctx* ctx, void* stream);
+/* qem_sample_q (Philox mode, iter >= 1) + qem_estep_forward in one call: on the tensor-core path the
+   level-1 draws are made inside the column prep (the same Philox counters and transform as the
+   sampler, so the bound z is bit-identical to qem_sample_q's), saving the prep's read of z; other
+   paths run the two calls.  qem_iterate uses it unless an eps bank is bound. */
+qem_status qem_sample_estep_forward(qem_ctx* ctx, uint64_t seed, int32_t iter, void* stream);
 /* Device pointer + count of the plate-sum buffer (fp64, K+1 entries). */
 qem_status qem_reduce_buffer(qem_ctx* ctx, double** d_buf, int64_t* count);
 /* SUM all-reduce of that buffer over the attached communicator (see "Group sharding" above). */

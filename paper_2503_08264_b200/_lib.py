@@ -22,7 +22,7 @@ EXPORTS = [
     "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_reduce", "qem_estep_backward", "qem_estep_evidence",
     "qem_nccl_unique_id", "qem_nccl_init", "qem_set_nccl_comm", "qem_nccl_info",
     "qem_estep_separable", "qem_cols_gamma_poisson", "qem_cols_beta_binomial", "qem_mstep_gaussian",
-    "qem_history_weight", "qem_estep_crossed",
+    "qem_history_weight", "qem_estep_crossed", "qem_sample_estep_forward",
     "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_estep_tables", "qem_sample_normal",
     "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical", "qem_moments_categorical", "qem_mstep_categorical",
     "qem_loglik_bernoulli_states", "qem_backward_resample", "qem_predictive_loglik", "qem_logmeanexp", "qem_global_iw", "qem_sample_gamma",
@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
                                     ctypes.POINTER(vp)]
         L.qem_estep_tables.argtypes = [i64, i32, vp, vp, vp, vp, vp, vp, vp]
         L.qem_estep_separable.argtypes = [i64, i32, i32] + [vp] * 8
+        L.qem_sample_estep_forward.argtypes = [vp, u64, i32, vp]
         L.qem_estep_crossed.argtypes = [i64, i32, i32, i32, i32] + [vp] * 15
         L.qem_mstep_gaussian.argtypes = [i64, ctypes.c_double, ctypes.c_double] + [vp] * 6
         L.qem_history_weight.argtypes = [i32, ctypes.c_double, ctypes.c_double]
@@ -152,7 +153,8 @@ def lib() -> ctypes.CDLL:
                      "qem_tables_gamma_poisson", "qem_moments_gamma", "qem_sample_beta",
                      "qem_tables_beta_binomial", "qem_moments_beta", "qem_tables_crossed",
                      "qem_moments_gaussian", "qem_estep_separable", "qem_cols_gamma_poisson",
-                     "qem_cols_beta_binomial", "qem_mstep_gaussian", "qem_estep_crossed"]:
+                     "qem_cols_beta_binomial", "qem_mstep_gaussian", "qem_estep_crossed",
+                     "qem_sample_estep_forward"]:
             getattr(L, name).restype = i32
         _lib = L
     return _lib

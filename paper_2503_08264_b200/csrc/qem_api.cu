@@ -388,6 +388,34 @@ qem_status qem_sample_q(qem_ctx* c, uint64_t seed, int32_t iter, const float* co
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_sample_q");
 }
 
+// Sampler + forward; on the tensor-core path the level-1 draws are fused into the column prep
+// (k_colprep_tc: the same Philox counters and transform as k_sample, bit-identical samples), so z is
+// written once and never re-read by the prep.  iter 0 = the device iteration counter (graph mode).
+static cudaError_t sample_forward(qem_ctx* c, uint64_t seed, int32_t iter, cudaStream_t st) {
+  if (!(c->tc && c->desc.family == QEM_FAMILY_TWO_LEVEL)) {
+    cudaError_t e = qem::launch_sample(c, seed, iter, nullptr, st);
+    if (e != cudaSuccess) return e;
+    return c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_forward(c, st) : qem::th_forward(c, st);
+  }
+  cudaError_t e = qem::launch_sample(c, seed, iter, nullptr, st, 0, /*root_only=*/1);
+  if (e != cudaSuccess) return e;
+  c->fuse_sample = 1;
+  c->fuse_iter = iter;
+  c->fuse_seed = seed;
+  e = qem::tl_forward(c, st);
+  c->fuse_sample = 0;
+  return e;
+}
+
+qem_status qem_sample_estep_forward(qem_ctx* c, uint64_t seed, int32_t iter, void* stream) {
+  qem_status s = need_bound(c);
+  if (s) return s;
+  if (iter < 1) return fail(QEM_INVALID_ARGUMENT, "iter must be >= 1");
+  c->launches = 0;
+  const cudaError_t e = sample_forward(c, seed, iter, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_sample_estep_forward");
+}
+
 qem_status qem_estep_forward(qem_ctx* c, void* stream) {
   qem_status s = need_bound(c);
   if (s) return s;
@@ -823,9 +851,13 @@ static cudaError_t iterate_body(qem_ctx* c, uint64_t seed, cudaStream_t st) {
     e = evidence_root(c, st);
     if (e != cudaSuccess) return e;
   }
-  e = qem::launch_sample(c, seed, 0, nullptr, st);
-  if (e != cudaSuccess) return e;
-  e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_forward(c, st) : qem::th_forward(c, st);
+  if (c->bufs.eps_bank[0]) {  // parity mode: the bank's draws, then the forward
+    e = qem::launch_sample(c, seed, 0, nullptr, st);
+    if (e != cudaSuccess) return e;
+    e = c->desc.family == QEM_FAMILY_TWO_LEVEL ? qem::tl_forward(c, st) : qem::th_forward(c, st);
+  } else {
+    e = sample_forward(c, seed, 0, st);
+  }
   if (e != cudaSuccess) return e;
   // the only exchange of a sharded iteration: SUM of the (K+1) fp64 plate sums (no-op at one rank)
   const int nr = qem::ctx_allreduce(c, st);

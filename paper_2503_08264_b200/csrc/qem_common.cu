@@ -49,46 +49,6 @@ struct SampleArgs {
   const int32_t* d_base;  // eps bank mode (qem_iterate parity mode): slice (t - *d_base) of every level's eps
 };
 
-// r = sqrt(-2 ln u), u = (m + 1/2) 2^-23, m a 23-bit integer.  Near u = 1 (v = 1 - u < 2^-5,
-// exact in fp32) -ln u = v + v^2/2 + ... + v^6/6 (error < v^7/7 < 1e-11); elsewhere
-// ln u = ln2 lg2.approx(u) (absolute error ~1.7e-7, i.e. <= 7e-7 on r >= 0.25 there).
-__device__ __forceinline__ float bm_radius(uint32_t m) {
-  const float u = ((float)m + 0.5f) * 1.1920928955078125e-07f;
-  float nl;
-  if (m >= 8126464u) {  // u > 1 - 2^-5
-    const float v = ((float)(8388607u - m) + 0.5f) * 1.1920928955078125e-07f;
-    nl = v * fmaf(v, fmaf(v, fmaf(v, fmaf(v, fmaf(v, 1.f / 6.f, 0.2f), 0.25f), 1.f / 3.f), 0.5f), 1.f);
-  } else {
-    float l2;
-    asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(u));
-    nl = -0.69314718055994531f * l2;
-  }
-  const float x = 2.f * nl;
-  float rs;
-  asm("rsqrt.approx.f32 %0, %1;" : "=f"(rs) : "f"(x));
-  return x * rs;
-}
-// (sin, cos) of 2 pi u, u = (m + 1/2) 2^-23: quadrant from the top two bits, reflection to
-// [0, pi/4] exact in fp32, Taylor polynomials (sin to x^9, cos to x^10; error < 3e-8).
-__device__ __forceinline__ void bm_sincos2pi(uint32_t m, float& sn, float& cs) {
-  const uint32_t q = m >> 21;                                          // quadrant
-  float f = ((float)(m & 0x1FFFFFu) + 0.5f) * 4.76837158203125e-07f;  // in (0, 1): angle f pi/2
-  const bool hi = f > 0.5f;
-  if (hi) f = 1.f - f;  // exact (Sterbenz)
-  const float x = f * 1.5707963267948966f, x2 = x * x;
-  const float sa = x * fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, 2.7557319e-6f, -1.9841270e-4f), 8.3333333e-3f),
-                                     -1.6666667e-1f), 1.f);
-  const float ca = fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, -2.7557319e-7f, 2.4801587e-5f), -1.3888889e-3f),
-                                           4.1666667e-2f), -0.5f), 1.f);
-  const float s1 = hi ? ca : sa, c1 = hi ? sa : ca;  // sin, cos of the in-quadrant angle
-  switch (q) {
-    case 0: sn = s1; cs = c1; break;
-    case 1: sn = c1; cs = -s1; break;
-    case 2: sn = -s1; cs = -c1; break;
-    default: sn = -c1; cs = s1; break;
-  }
-}
-
 // K1: z = fmaf(sqrtf(v), eps, m)  (Alg. 1 line 4; location-scale
 // sampling, App. E; fp32 definition DESIGN.md R22).
 // One thread = 4 consecutive samples k of one latent dim (one Philox call,
@@ -117,18 +77,11 @@ __device__ __forceinline__ void sample_unit(const SampleArgs& a, const SampleLev
     const uint32_t word = ((uint32_t)s.level << 24) | (((uint32_t)t | a.iter_or) & 0xffffffu);
 #pragma unroll
     for (int u = 0; u < QPT; ++u) {
-      const uint4 o = philox4x32_10(make_uint4((uint32_t)(k0 >> 2) + u, (uint32_t)dim, ginst, word), a.key);
-      // Box-Muller on u = ((x >> 9) + 0.5) * 2^-23: radius and angle evaluated
-      // from the integer bits (bm_radius, bm_sincos2pi: ~3x fewer instructions than
-      // sqrtf(-2 logf(u)) and sincospif(2u); absolute error <= ~1e-6 on eps vs the fp64 transform).
-      const float r0 = bm_radius(o.x >> 9), r1 = bm_radius(o.z >> 9);
-      float s0, c0, s1, c1;
-      bm_sincos2pi(o.y >> 9, s0, c0);
-      bm_sincos2pi(o.w >> 9, s1, c1);
-      e[u][0] = r0 * c0;
-      e[u][1] = r0 * s0;
-      e[u][2] = r1 * c1;
-      e[u][3] = r1 * s1;
+      const float4 n4 = philox_normal4(make_uint4((uint32_t)(k0 >> 2) + u, (uint32_t)dim, ginst, word), a.key);
+      e[u][0] = n4.x;
+      e[u][1] = n4.y;
+      e[u][2] = n4.z;
+      e[u][3] = n4.w;
     }
   }
   float* zr = s.z + row * a.K + k0;
@@ -206,7 +159,7 @@ cudaError_t launch_sample_rows(int64_t rows, int K, int level, uint64_t seed, in
 }
 
 cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps, cudaStream_t st,
-                          uint32_t iter_or) {
+                          uint32_t iter_or, int root_only) {
   SampleArgs a{};
   a.iter_or = iter_or;
   if (!d_eps && iter == 0 && iter_or == 0 && c->bufs.eps_bank[0]) {  // qem_iterate in eps bank mode
@@ -220,7 +173,7 @@ cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* 
   a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   a.t_host = iter;
   a.d_iter = &c->cnt->iter;
-  int nlev = c->desc.family == QEM_FAMILY_TWO_LEVEL ? 2 : 3;
+  int nlev = root_only ? 1 : (c->desc.family == QEM_FAMILY_TWO_LEVEL ? 2 : 3);
   int64_t quads = 0;
   for (int l = 0; l < nlev; ++l) {
     SampleLevel& s = a.lv[l];

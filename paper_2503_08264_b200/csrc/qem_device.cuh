@@ -61,6 +61,60 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
+// r = sqrt(-2 ln u), u = (m + 1/2) 2^-23, m a 23-bit integer.  Near u = 1 (v = 1 - u < 2^-5,
+// exact in fp32) -ln u = v + v^2/2 + ... + v^6/6 (error < v^7/7 < 1e-11); elsewhere
+// ln u = ln2 lg2.approx(u) (absolute error ~1.7e-7, i.e. <= 7e-7 on r >= 0.25 there).
+__device__ __forceinline__ float bm_radius(uint32_t m) {
+  const float u = ((float)m + 0.5f) * 1.1920928955078125e-07f;
+  float nl;
+  if (m >= 8126464u) {  // u > 1 - 2^-5
+    const float v = ((float)(8388607u - m) + 0.5f) * 1.1920928955078125e-07f;
+    nl = v * fmaf(v, fmaf(v, fmaf(v, fmaf(v, fmaf(v, 1.f / 6.f, 0.2f), 0.25f), 1.f / 3.f), 0.5f), 1.f);
+  } else {
+    float l2;
+    asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(u));
+    nl = -0.69314718055994531f * l2;
+  }
+  const float x = 2.f * nl;
+  float rs;
+  asm("rsqrt.approx.f32 %0, %1;" : "=f"(rs) : "f"(x));
+  return x * rs;
+}
+// (sin, cos) of 2 pi u, u = (m + 1/2) 2^-23: quadrant from the top two bits, reflection to
+// [0, pi/4] exact in fp32, Taylor polynomials (sin to x^9, cos to x^10; error < 3e-8).
+__device__ __forceinline__ void bm_sincos2pi(uint32_t m, float& sn, float& cs) {
+  const uint32_t q = m >> 21;                                          // quadrant
+  float f = ((float)(m & 0x1FFFFFu) + 0.5f) * 4.76837158203125e-07f;  // in (0, 1): angle f pi/2
+  const bool hi = f > 0.5f;
+  if (hi) f = 1.f - f;  // exact (Sterbenz)
+  const float x = f * 1.5707963267948966f, x2 = x * x;
+  const float sa = x * fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, 2.7557319e-6f, -1.9841270e-4f), 8.3333333e-3f),
+                                     -1.6666667e-1f), 1.f);
+  const float ca = fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, -2.7557319e-7f, 2.4801587e-5f), -1.3888889e-3f),
+                                           4.1666667e-2f), -0.5f), 1.f);
+  const float s1 = hi ? ca : sa, c1 = hi ? sa : ca;  // sin, cos of the in-quadrant angle
+  switch (q) {
+    case 0: sn = s1; cs = c1; break;
+    case 1: sn = c1; cs = -s1; break;
+    case 2: sn = -s1; cs = -c1; break;
+    default: sn = -c1; cs = s1; break;
+  }
+}
+
+// Four N(0,1) draws of one Philox4x32-10 call: Box-Muller on
+// u = ((x >> 9) + 0.5) 2^-23, radius and angle evaluated from the integer bits (bm_radius,
+// bm_sincos2pi: ~3x fewer instructions than sqrtf(-2 logf(u)) and sincospif(2u); absolute error
+// <= ~1e-6 on eps vs the fp64 transform).  The sampler (k_sample) and the fused column prep
+// (k_colprep_tc) both draw through this, so their samples are bit-identical.
+__device__ __forceinline__ float4 philox_normal4(uint4 ctr, uint2 key) {
+  const uint4 o = philox4x32_10(ctr, key);
+  const float r0 = bm_radius(o.x >> 9), r1 = bm_radius(o.z >> 9);
+  float s0, c0, s1, c1;
+  bm_sincos2pi(o.y >> 9, s0, c0);
+  bm_sincos2pi(o.w >> 9, s1, c1);
+  return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+}
+
 // ------------------------------------------------- TMA bulk copy + mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

@@ -102,6 +102,9 @@ struct qem_ctx {
   void* nccl_comm;
   int nccl_owned;  // created by qem_nccl_init (destroyed with the context)
   int nccl_rank, nccl_world;
+  int fuse_sample;     // the next tl_forward's column prep draws the level-1 samples (tensor-core path)
+  int fuse_iter;       // ... for this iteration (0: the device counter)
+  uint64_t fuse_seed;  // ... with this Philox key
   int nccl_warm;   // one eager collective has run on the communicator
   int nccl_last;   // ncclResult_t of a failed all-reduce inside iterate_body
 };
@@ -119,7 +122,7 @@ cudaError_t th_forward(qem_ctx* c, cudaStream_t s);
 cudaError_t th_backward(qem_ctx* c, cudaStream_t s);
 // common (qem_common.cu)
 cudaError_t launch_sample(qem_ctx* c, uint64_t seed, int32_t iter, const float* const* d_eps,
-                          cudaStream_t s, uint32_t iter_or = 0);
+                          cudaStream_t s, uint32_t iter_or = 0, int root_only = 0);
 cudaError_t launch_mstep(qem_ctx* c, int32_t t, cudaStream_t s);
 // NCCL, resolved at run time (qem_nccl.cu); int results are ncclResult_t (0 = success)
 int ctx_allreduce(qem_ctx* c, cudaStream_t st);

@@ -323,7 +323,7 @@ struct PrepTc {
   static constexpr int ZS_FLOATS = 2 * 2 * kTcD * 32;  // z ring: [stage][half][r][32 columns]
   static constexpr size_t ZS_BYTES = ZS_FLOATS * 4;
   __host__ __device__ static size_t warp_bytes(int K, int J) {
-    size_t b = 3 * kTcD * 8 + 2 * kTcD * 4 + (size_t)((J + 1) / 2) * kTcD * 8 + ZS_BYTES;
+    size_t b = 3 * kTcD * 8 + 3 * kTcD * 4 + (size_t)((J + 1) / 2) * kTcD * 8 + ZS_BYTES;
     return (b + 15) & ~(size_t)15;
   }
   __host__ __device__ static size_t bytes(int K, int J) { return WARPS * warp_bytes(K, J); }
@@ -347,7 +347,8 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
   double2* qab = reinterpret_cast<double2*>(qm + kTcD);            // [D]  {alpha_r, beta_r}
   float* qmf = reinterpret_cast<float*>(qab + kTcD);               // [D]  m_i (fp32, exact: R22)
   float* u0f = qmf + kTcD;                                         // [D]  u0_i = m_i - mu_ref (fp32)
-  float2* xp = reinterpret_cast<float2*>(u0f + kTcD);              // [(J+1)/2][D] {x_2p, x_2p+1} as 0/1
+  float* sdf = u0f + kTcD;                                         // [D]  sqrt(v_i) (fp32, the sampler's)
+  float2* xp = reinterpret_cast<float2*>(sdf + kTcD);              // [(J+1)/2][D] {x_2p, x_2p+1} as 0/1
   const int Jh = (J + 1) / 2;
   float* zs = reinterpret_cast<float*>(xp + (size_t)Jh * kTcD);    // z ring (PrepTc::ZS_FLOATS)
   // z of 32 column pairs {kc, kc + K/2} of group g into ring stage st: LDGSTS, so the loads of
@@ -362,6 +363,28 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     }
     cp_async_commit();
   };
+  // Fused sampler (qem_sample_estep_forward / qem_iterate): instead of loading z, draw it -- the
+  // same Philox counters and Box-Muller as k_sample (philox_normal4), z = fmaf(sqrt(v), eps, m) in
+  // fp32 (R22), so the samples are bit-identical -- write it to the bound z (the backward's column
+  // constants and the moments read it) and into the stage.  Lane: one quad of 4 columns x one dim.
+  const bool fuse = a.fuse_sample != 0;
+  const uint32_t zword = (1u << 24) | ((uint32_t)resolve_iter(a.t_sample, &a.cnt->iter) & 0xffffffu);
+  float* zout = const_cast<float*>(a.z);
+  auto gen_z = [&](int64_t g, int it, int st) {
+    float* dst = zs + st * (2 * kTcD * 32);
+    const uint32_t ginst = (uint32_t)(a.g_begin + g);
+#pragma unroll
+    for (int c = lane; c < 2 * D * 8; c += 32) {
+      const int h = c / (D * 8), r = (c / 8) % D, p = c % 8;
+      const int k0 = h * (K / 2) + it * 32 + p * 4;
+      const float4 e = philox_normal4(make_uint4((uint32_t)(k0 >> 2), (uint32_t)r, ginst, zword), a.skey);
+      const float m = qmf[r], sd = sdf[r];
+      const float4 zz = make_float4(__fmaf_rn(sd, e.x, m), __fmaf_rn(sd, e.y, m), __fmaf_rn(sd, e.z, m),
+                                    __fmaf_rn(sd, e.w, m));
+      *reinterpret_cast<float4*>(dst + (h * kTcD + r) * 32 + p * 4) = zz;
+      *reinterpret_cast<float4*>(zout + ((size_t)g * D + r) * K + k0) = zz;
+    }
+  };
   const int NIT = K / 64;  // K % 256 == 0 on this path
   const double bref_const = a.ws.ref->bref_const, e_ref = a.ws.ref->e_ref;
   const float mref_l = lane < D ? a.ws.ref->mu_ref[lane] : 0.f;
@@ -373,7 +396,8 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
   }
   unsigned char* colop = reinterpret_cast<unsigned char*>(a.ws.colop);
   const int64_t gstride = (int64_t)gridDim.x * PrepTc::WARPS;
-  if ((int64_t)blockIdx.x * PrepTc::WARPS + wid < a.n_local) stage_z((int64_t)blockIdx.x * PrepTc::WARPS + wid, 0, 0);
+  if (!fuse && (int64_t)blockIdx.x * PrepTc::WARPS + wid < a.n_local)
+    stage_z((int64_t)blockIdx.x * PrepTc::WARPS + wid, 0, 0);
   for (int64_t i = (int64_t)blockIdx.x * PrepTc::WARPS + wid; i < a.n_local; i += gstride) {
     __syncwarp();
     double sx = 0.0, sxx = 0.0;
@@ -404,6 +428,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
       qm[lane] = m;
       qmf[lane] = (float)m;
       u0f[lane] = (float)m - mref_l;
+      sdf[lane] = __fsqrt_rn(a.q_v[i * D + lane]);  // as k_sample
       qab[lane] = make_double2(0.5 / v - 0.5 * e_ref, (double)yxi - e_ref * dl);
       ci = 0.5 * (kLn2Pi + log(v)) - 0.5 * e_ref * dl * dl + (double)yxi * m;
     }
@@ -479,7 +504,9 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     // Two columns per lane at a time (kc and kc + K/2): the per-observation feature loads are
     // shared and the two likelihood chains hide each other's latency.
     for (int it = 0; it < NIT; ++it) {
-      if (it + 1 < NIT) {
+      if (fuse) {
+        gen_z(i, it, it & 1);
+      } else if (it + 1 < NIT) {
         stage_z(i, it + 1, (it + 1) & 1);
         cp_async_wait<1>();
       } else {
@@ -539,7 +566,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
       finish(kcB, zB, llB);
       __syncwarp();  // the stage is refilled two iterations on
     }
-    if (i + gstride < a.n_local) stage_z(i + gstride, 0, 0);  // next group's first stage, under the passes below
+    if (!fuse && i + gstride < a.n_local) stage_z(i + gstride, 0, 0);  // next group's first stage, under the passes below
     const double M = warp_max(tmax);
     const float W2max = warp_maxf(w2max);
     const double* tref = a.ws.tA + (size_t)i * K;  // written above by this lane (program order)

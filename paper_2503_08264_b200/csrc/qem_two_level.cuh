@@ -51,6 +51,10 @@ struct TLArgs {
   int t_host;
   int tc;        // tensor-core pair kernels in use (d = 16)
   int evidence_only;  // k_root: log Pe only (fresh-denominator pass)
+  int fuse_sample;    // k_colprep_tc draws the level-1 samples itself (qem_sample_estep_forward, qem_iterate)
+  int t_sample;       // its iteration (0: the device counter, graph mode)
+  uint2 skey;         // its Philox key (the seed)
+  int64_t g_begin;    // global index of local group 0 (the Philox counters)
   float thr[5];  // forward tile-mode bounds for expm1 degrees 3/4/5/7/9
   TwoLevelWs ws;
   Counters* cnt;
@@ -563,6 +567,10 @@ inline TLArgs make_args(qem_ctx* c) {
   a.t_host = 0;
   a.tc = c->tc;
   a.evidence_only = c->evidence_only;
+  a.fuse_sample = c->fuse_sample;
+  a.t_sample = c->fuse_iter;
+  a.skey = make_uint2((uint32_t)c->fuse_seed, (uint32_t)(c->fuse_seed >> 32));
+  a.g_begin = c->g_begin;
   if (c->evidence_only) {
     a.log_pe = c->bufs.log_pe_fresh;  // log Pe(z_new)
     a.trace = nullptr;

@@ -263,6 +263,10 @@ class QEM:
     def estep(self, stream=None) -> None:
         check(lib().qem_estep(self.ctx, _stream(stream)), "qem_estep")
 
+    def sample_estep_forward(self, seed: int, iter: int, stream=None) -> None:
+        """qem_sample_estep_forward: Philox samples + forward phase (fused on the tensor-core path)."""
+        check(lib().qem_sample_estep_forward(self.ctx, seed, iter, _stream(stream)), "qem_sample_estep_forward")
+
     def estep_forward(self, stream=None) -> None:
         check(lib().qem_estep_forward(self.ctx, _stream(stream)), "qem_estep_forward")
 

@@ -124,3 +124,44 @@ def test_compact_tc_path_d1_opt_in():
     env = dict(os.environ, QEM_TC1="1")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
     assert "COMPACT_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("n,K", [(37, 256), (9, 1024)])
+def test_fused_sampler_is_bit_identical(n, K):
+    """qem_sample_estep_forward draws the level-1 samples inside the column prep: the bound z, the
+    messages, log Pe, weights and moments equal qem_sample_q + qem_estep_forward's bit for bit
+    (same Philox counters, same transform), on a sharded block too (global counters)."""
+    from paper_2503_08264_b200.qem import QEM, shard_range
+    m = synth.config(5, n=n, K=K)
+    data = synth.make_data(m)
+    q = synth.random_q(m, 5)
+    for b, e in ((0, n), shard_range(n, 1, 2)):
+        outs = []
+        for fused in (False, True):
+            g = QEM(m, group_begin=b, group_end=e)
+            g.set_data(data)
+            g.set_q(q)
+            if fused:
+                g.sample_estep_forward(91, 4)
+            else:
+                g.sample_q(seed=91, iter=4)
+                g.estep_forward()
+            dg, c = [x.cpu().numpy() for x in g.messages()]
+            ps = g.plate_sum.cpu().numpy()
+            if (b, e) == (0, n):
+                g.estep_backward()
+            r = g.result()
+            r["dg"], r["c"], r["ps"] = dg, c, ps
+            outs.append(r)
+            g.close()
+        a, f = outs
+        for l in range(2):
+            np.testing.assert_array_equal(a["z"][l], f["z"][l])
+        np.testing.assert_array_equal(a["dg"], f["dg"])
+        np.testing.assert_array_equal(a["c"], f["c"])
+        np.testing.assert_array_equal(a["ps"], f["ps"])
+        if (b, e) == (0, n):
+            assert a["log_pe"] == f["log_pe"]
+            for l in range(2):
+                np.testing.assert_array_equal(a["w"][l], f["w"][l])
+                np.testing.assert_array_equal(a["m1"][l], f["m1"][l])
