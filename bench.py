@@ -932,8 +932,9 @@ def _relaunch_torchrun(n: int) -> int:
     port = s.getsockname()[1]
     s.close()
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init log (nranks, transport) stays on
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init log (nranks, transport) stays on ...
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr: stdout carries the one JSON line
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd, env=env)
