@@ -260,6 +260,7 @@ def measure_step(m, args, world, rank, dev, in_library, seed):
         dist.barrier()
     torch.cuda.synchronize()
     launched[0] = 0
+    g.mode_hist()  # read-and-reset: the timed steps' forward tile modes only
     start.record(stream)
     for s in range(args.steps):
         step(t, evs[s])
@@ -269,6 +270,7 @@ def measure_step(m, args, world, rank, dev, in_library, seed):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    hist = g.mode_hist()
     ms_total = start.elapsed_time(stop)
     g.set_kernel_events(None)
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
@@ -308,7 +310,9 @@ def measure_step(m, args, world, rank, dev, in_library, seed):
                            f"roofline (slower of SFU and FP32 ops at peak, guide peak rates); "
                            f"frac_vs_exp_sfu_plus_fma is against the stricter ceiling that also counts exps "
                            f"evaluated in software on the FMA pipe ({FMA_PER_SOFT_EXP:.0f} lane-ops each)"),
-            "kernels_ms": {"forward": fwd_ms, "backward": bwd_ms, "allreduce": comm_ms}}
+            "kernels_ms": {"forward": fwd_ms, "backward": bwd_ms, "allreduce": comm_ms},
+            "forward_mode_hist": dict(zip(["expm1_deg3", "deg4", "deg5", "deg7", "deg9", "online_lse"],
+                                          [int(x) for x in hist[:6]]))}
     out = dict(g=g, data=data, gb=gb, ge=ge, ms_step=ms_step, value=m.pairs / (ms_step * 1e-3),
                launched=launched[0], flags=flags, clamps=clamps, clocks=clk, roofline=roof, tc=tc, t=t,
                allreduce=runner.allreduce_plate_sum, nccl=g.nccl_info() if in_library else None)

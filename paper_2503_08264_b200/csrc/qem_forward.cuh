@@ -25,7 +25,9 @@
 #endif
 template <int D>
 struct FwdLayout {
-  static constexpr int CS = pad4(D + 3);  // u[D], U2, P, lnP
+  static constexpr int CS = pad4(D + 3);  // u[D], U2, P, lnP (d = 1: u, lnP, U2, P)
+  // record slots: for d = 1 ln P sits next to u, so the online tile's two fields are one 8-byte load
+  static constexpr int IU2 = D == 1 ? 2 : D, IP = D == 1 ? 3 : D + 1, ILP = D == 1 ? 1 : D + 2;
   static constexpr int CH = QEM_FWD_CH;   // column chunk of the online log-sum-exp (one max per chunk)
   __host__ __device__ static int kpad(int K) { return (K + CH - 1) / CH * CH; }
   __host__ __device__ static size_t stage_bytes(int K) { return (size_t)kpad(K) * CS * sizeof(float); }
@@ -40,14 +42,16 @@ struct FwdLayout {
   __host__ __device__ static size_t prep_bytes(int K, int J) { return PREP_WARPS * prep_warp_bytes(K, J); }
 };
 
+// D'_k(k') + base: the column term `base` (0, or ln P in the online tile) rides in the contraction's
+// first FMA instead of a separate add
 template <int D, int RP>
-__device__ __forceinline__ float2 pair_D(const float2 (&al)[RP], const float2 (&ga)[RP], const float2 (&cc)[RP][D],
+__device__ __forceinline__ float2 pair_D(float2 base, const float2 (&ga)[RP], const float2 (&cc)[RP][D],
                                          int p, const float* u, float U2) {
   if constexpr (D == 1) {
-    return fma2(fma2(ga[p], f2(u[0]), cc[p][0]), f2(u[0]), al[p]);
+    return fma2(fma2(ga[p], f2(u[0]), cc[p][0]), f2(u[0]), base);
   } else {
     // two accumulators halve the dependent FMA chain
-    float2 a0 = fma2(ga[p], f2(U2), al[p]);
+    float2 a0 = fma2(ga[p], f2(U2), base);
     float2 a1 = mul2(cc[p][0], f2(u[0]));
 #pragma unroll
     for (int r = 1; r < D; ++r) {
@@ -74,15 +78,15 @@ __device__ __forceinline__ void load_col(const float* cr, float (&u)[D], float& 
   }
 #pragma unroll
   for (int r = 0; r < D; ++r) u[r] = buf[r];
-  U2 = buf[D];
-  P = buf[D + 1];
-  lnP = buf[D + 2];
+  U2 = buf[FwdLayout<D>::IU2];
+  P = buf[FwdLayout<D>::IP];
+  lnP = buf[FwdLayout<D>::ILP];
 }
 
 __device__ __forceinline__ float2 max2(float2 a, float2 b) { return make_float2(fmaxf(a.x, b.x), fmaxf(a.y, b.y)); }
 
 template <int D, int RP, int N>
-__device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2 (&al)[RP], const float2 (&ga)[RP],
+__device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2 (&ga)[RP],
                                           const float2 (&cc)[RP][D], double (&dgv)[2 * RP]) {
   constexpr int CS = pad4(D + 3);
   float2 acc[RP];
@@ -93,7 +97,7 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
     float u[D], U2, P, lnP;
     load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
 #pragma unroll
-    for (int p = 0; p < RP; ++p) acc[p] = fma2(f2(P), expm1_poly<N>(pair_D<D, RP>(al, ga, cc, p, u, U2)), acc[p]);
+    for (int p = 0; p < RP; ++p) acc[p] = fma2(f2(P), expm1_poly<N>(pair_D<D, RP>(f2(0.f), ga, cc, p, u, U2)), acc[p]);
   }
 #pragma unroll
   for (int p = 0; p < RP; ++p) {
@@ -102,6 +106,13 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
   }
 }
 
+// Exponentials per online chunk (the last kFwdSoft of its QEM_FWD_CH columns) evaluated on the FMA
+// pipe (exp2_poly2) instead of the SFU.
+#ifndef QEM_FWD_SOFT
+#define QEM_FWD_SOFT 0
+#endif
+constexpr int kFwdSoft = QEM_FWD_SOFT;
+
 // Rescale margin of the online log-sum-exp (natural-log units).  0 = the shift is always the exact
 // running max, so the dominant term of every row is ex2(0) = 1 exactly: a positive margin saves
 // rescales but leaves ~1e-7 relative error on the dominant term, which the 1e5-group plate sum of
@@ -109,7 +120,7 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
 constexpr float kLazy = 0.0f;
 
 template <int D, int RP>
-__device__ __forceinline__ void tile_online(const float* col, int Kp, const float2 (&al)[RP], const float2 (&ga)[RP],
+__device__ __forceinline__ void tile_online(const float* col, int Kp, const float2 (&ga)[RP],
                                             const float2 (&cc)[RP][D], double (&dgv)[2 * RP]) {
   constexpr int CS = pad4(D + 3);
   constexpr int CH = FwdLayout<D>::CH;
@@ -126,7 +137,7 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
       float u[D], U2, P, lnP;
       load_col<D>(col + (size_t)(kc0 + c) * CS, u, U2, P, lnP);
 #pragma unroll
-      for (int p = 0; p < RP; ++p) tv[c][p] = add2(pair_D<D, RP>(al, ga, cc, p, u, U2), f2(lnP));
+      for (int p = 0; p < RP; ++p) tv[c][p] = pair_D<D, RP>(f2(lnP), ga, cc, p, u, U2);
     }
 #pragma unroll
     for (int p = 0; p < RP; ++p) {
@@ -147,7 +158,7 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const float2 e = fma2(tv[c][p], f2(kLog2e), nm);
-        s = add2(s, kSoftExpFfma && c == CH - 1 ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y)));
+        s = add2(s, c >= CH - kFwdSoft ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y)));
       }
       ac[p] = s;
     }
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
       {
 #pragma unroll
         for (int r = D; r < CS; ++r) rec[r] = 0.f;
-        rec[D] = W2;
+        rec[FwdLayout<D>::IU2] = W2;
         float4* dst = reinterpret_cast<float4*>(rec0 + (size_t)kc * CS);
 #pragma unroll
         for (int q = 0; q < CS / 4; ++q)
@@ -278,7 +289,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
         float4* dst = reinterpret_cast<float4*>(rec0 + (size_t)kc * CS);
 #pragma unroll
         for (int q = 0; q < CS / 4; ++q) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        rec0[(size_t)kc * CS + D + 2] = -CUDART_INF_F;
+        rec0[(size_t)kc * CS + FwdLayout<D>::ILP] = -CUDART_INF_F;
       }
     }
     const double M = warp_max(tmax);
@@ -290,8 +301,8 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
       const float lp = (float)(tref[kc] - M - logS);
       {
         float* pc = rec0 + (size_t)kc * CS;
-        pc[D + 1] = expf(lp);
-        pc[D + 2] = lp;
+        pc[FwdLayout<D>::IP] = expf(lp);
+        pc[FwdLayout<D>::ILP] = lp;
       }
     }
     if (lane == 0) {
@@ -341,9 +352,6 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
     }
     ga[p] = make_float2(gv[0], gv[1]);
   }
-  float2 az[RP];
-#pragma unroll
-  for (int p = 0; p < RP; ++p) az[p] = f2(0.f);
   double G[2 * RP];
 #pragma unroll
   for (int j = 0; j < 2 * RP; ++j) G[j] = 0.0;
@@ -362,9 +370,13 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
     tma_bulk_g2s(smem, a.ws.colrec + (size_t)i0 * Kp * CS, sbytes, &bar[0]);
   }
   __shared__ int s_mode[2][8];
+  // Groups past the first wave come from a device-wide queue (one atomic per group): per-group cost
+  // depends on the tile mode, so a static stride leaves CTAs idle at the end of the launch.
+  __shared__ int64_t s_next[2];
   int j = 0;
-  for (int64_t i = i0; i < a.n_local; i += gridDim.x, ++j) {
+  for (int64_t i = i0; i < a.n_local; ++j) {
     const int st = j & 1;
+    if (tid == 0) s_next[st] = (int64_t)gridDim.x + atomicAdd(&a.cnt->claim_fwd, 1u);
     const float W2max = a.ws.gstat[i];
     if (tid == 0) csum += a.ws.cvec[i];
 
@@ -413,7 +425,7 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
 
     // all warps are done with the other stage (group j-1): refill it with group j+1
     __syncthreads();
-    const int64_t inext = i + gridDim.x;
+    const int64_t inext = s_next[st];
     if (tid == 0 && inext < a.n_local) {
       mbar_expect_tx(&bar[st ^ 1], sbytes);
       tma_bulk_g2s(smem + (st ? 0 : sbytes), a.ws.colrec + (size_t)inext * Kp * CS, sbytes, &bar[st ^ 1]);
@@ -431,12 +443,12 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
 
     double dgv[2 * RP];
     switch (md) {
-      case 0: tile_poly<D, RP, 3>(col, Kp, az, ga, cc, dgv); break;
-      case 1: tile_poly<D, RP, 4>(col, Kp, az, ga, cc, dgv); break;
-      case 2: tile_poly<D, RP, 5>(col, Kp, az, ga, cc, dgv); break;
-      case 3: tile_poly<D, RP, 7>(col, Kp, az, ga, cc, dgv); break;
-      case 4: tile_poly<D, RP, 9>(col, Kp, az, ga, cc, dgv); break;
-      default: tile_online<D, RP>(col, Kp, az, ga, cc, dgv); break;
+      case 0: tile_poly<D, RP, 3>(col, Kp, ga, cc, dgv); break;
+      case 1: tile_poly<D, RP, 4>(col, Kp, ga, cc, dgv); break;
+      case 2: tile_poly<D, RP, 5>(col, Kp, ga, cc, dgv); break;
+      case 3: tile_poly<D, RP, 7>(col, Kp, ga, cc, dgv); break;
+      case 4: tile_poly<D, RP, 9>(col, Kp, ga, cc, dgv); break;
+      default: tile_online<D, RP>(col, Kp, ga, cc, dgv); break;
     }
     // h = log sum P exp(D') feeds the backward directly (no cancellation against
     // alpha'); dg = alpha' + h in fp64 feeds the plate sum.
@@ -449,6 +461,7 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
         G[q] += dgd;
       }
     }
+    i = inext;
   }
 
   // ---- per-CTA partial plate sums, then the last CTA reduces them in order.
@@ -476,6 +489,9 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
       for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(a.ws.partial + (size_t)b * (K + 1) + k);
       a.ws.red[k] = sum;
     }
-    if (tid == 0) a.cnt->ticket_fwd = 0;
+    if (tid == 0) {
+      a.cnt->ticket_fwd = 0;
+      a.cnt->claim_fwd = 0;
+    }
   }
 }

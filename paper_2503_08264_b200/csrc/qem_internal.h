@@ -68,6 +68,8 @@ struct Counters {
   int32_t iter;        // current iteration t (graph mode)
   int32_t trace_base;  // t0 of the running qem_iterate
   unsigned long long mode_hist[8];  // forward tile modes, counted per (warp, group)
+  uint32_t claim_fwd;  // k_forward's dynamic group queue (groups past the first wave); reset by its last CTA
+  uint32_t claim_pad;
 };
 
 }  // namespace qem

@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
         }
 #pragma unroll
         for (int r = 0; r < D; ++r) uu[h][r] = ok ? rec[r] : 0.f;
-        u2[h] = ok ? rec[D] : 0.f;
+        u2[h] = ok ? rec[FwdLayout<D>::IU2] : 0.f;
         lc[h] = ok ? (float)((tl[p][h] - tlse) * kLog2eD) : -CUDART_INF_F;
       }
 #pragma unroll
