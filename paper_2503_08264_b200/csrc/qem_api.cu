@@ -109,7 +109,8 @@ size_t carve(qem_ctx* c, char* base) {
     c->tw.dg = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
     const size_t kp = (size_t)((K + 15) / 16 * 16);  // >= FwdLayout::kpad(K) for any column chunk <= 16
     if (!c->tc)
-      c->tw.colrec = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * kp * pad4(D + 3)));
+      c->tw.colrec =  // per group: the column records + a trailer of 4 + pad4(D) floats (FwdLayout::GH)
+          reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * (kp * pad4(D + 3) + 4 + pad4(D))));
     if (c->tc) {
       c->tw.rowop = take((size_t)K * 96);
       c->tw.rowop_x = take((size_t)K * 32);

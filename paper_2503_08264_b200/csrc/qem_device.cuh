@@ -32,6 +32,36 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a
 // 1.5*2^23 shifter, 2^f by a degree-5 polynomial fitted on [-1/2, 1/2] (max relative error
 // 2.3e-7 in fp32, vs ~1.7e-7 for ex2.approx), 2^n added into the exponent field.
 // Inputs below -127 are clamped (2^-127: negligible wherever it is used).
+// ln x in fp64 for a positive normal fp32 x, branch-free: x = 2^e m with m in [sqrt(1/2), sqrt(2)),
+// ln m = 2 atanh(s), s = (m - 1)/(m + 1) (|s| <= 0.1716), the atanh series to s^21 (next term
+// < 3e-17); 1/(m + 1) from the fp32 reciprocal and two fp64 Newton steps.  Absolute error
+// <= 2e-15 for x up to 2^24 (checked against math.log on 2e5 points).  The fp64 logs of the
+// pair tiles' sums go through this instead of the library log (a third of the instructions).
+__device__ __forceinline__ double log_pos_f32(float x) {
+  const int ix = __float_as_int(x);
+  int e = ((ix >> 23) & 0xff) - 127;
+  int mi = (ix & 0x7fffff) | 0x3f800000;
+  if (mi > 0x3fb504f3) {
+    mi -= 0x00800000;
+    e += 1;
+  }
+  const double f = (double)__int_as_float(mi) - 1.0;  // exact
+  const double d = 2.0 + f;
+  double r;
+  {
+    float rf;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)d));
+    r = rf;
+  }
+  r = r * fma(-d, r, 2.0);
+  r = r * fma(-d, r, 2.0);
+  const double s = f * r, s2 = s * s;
+  double p = 1.0 / 21;
+#pragma unroll
+  for (int k = 19; k >= 1; k -= 2) p = fma(p, s2, 1.0 / k);
+  return fma((double)e, 0.69314718055994530942, 2.0 * s * p);
+}
+
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   x = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
   const float2 t = add2(x, f2(12582912.f));

@@ -30,7 +30,12 @@ struct FwdLayout {
   static constexpr int IU2 = D == 1 ? 2 : D, IP = D == 1 ? 3 : D + 1, ILP = D == 1 ? 1 : D + 2;
   static constexpr int CH = QEM_FWD_CH;   // column chunk of the online log-sum-exp (one max per chunk)
   __host__ __device__ static int kpad(int K) { return (K + CH - 1) / CH * CH; }
-  __host__ __device__ static size_t stage_bytes(int K) { return (size_t)kpad(K) * CS * sizeof(float); }
+  // group trailer after the Kp column records: [0] max |w|^2, [2..3] c_i (fp64), [4..4+D) Q mean m_i
+  // (fp32), so the forward's per-group scalars arrive with the group's TMA copy instead of as
+  // dependent global loads at the top of every group
+  static constexpr int GH = 4 + pad4(D);
+  __host__ __device__ static size_t group_floats(int K) { return (size_t)kpad(K) * CS + GH; }
+  __host__ __device__ static size_t stage_bytes(int K) { return group_floats(K) * sizeof(float); }
   // k_forward: two stages + two mbarriers
   __host__ __device__ static size_t bytes(int K, int /*J*/) { return 2 * stage_bytes(K) + 16; }
   // k_colprep, per warp: tref[K] + qconst[3][D] + bern masks/labels [2J]
@@ -165,8 +170,9 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
   }
 #pragma unroll
   for (int p = 0; p < RP; ++p) {
-    dgv[2 * p] = (double)mr[p].x + log((double)ac[p].x);
-    dgv[2 * p + 1] = (double)mr[p].y + log((double)ac[p].y);
+    // the row's dominant term is ex2(0) = 1, so ac >= 1 (finite unless the inputs were not)
+    dgv[2 * p] = (double)mr[p].x + (isfinite(ac[p].x) ? log_pos_f32(ac[p].x) : log((double)ac[p].x));
+    dgv[2 * p + 1] = (double)mr[p].y + (isfinite(ac[p].y) ? log_pos_f32(ac[p].y) : log((double)ac[p].y));
   }
 }
 
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
       }
     }
     __syncwarp();
-    float* rec0 = a.ws.colrec + (size_t)i * Kp * CS;
+    float* rec0 = a.ws.colrec + (size_t)i * FwdLayout<D>::group_floats(K);
     double tmax = -CUDART_INF;
     float u2max = 0.f;
     for (int kc = lane; kc < K; kc += 32) {
@@ -306,9 +312,15 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
       }
     }
     if (lane == 0) {
-      a.ws.cvec[i] = M + logS - logK;
+      const double cv = M + logS - logK;
+      a.ws.cvec[i] = cv;
       a.ws.gstat[i] = U2max;
+      float* gh = rec0 + (size_t)Kp * CS;
+      gh[0] = U2max;
+      gh[1] = 0.f;
+      *reinterpret_cast<double*>(gh + 2) = cv;
     }
+    if (lane < D) rec0[(size_t)Kp * CS + 4 + lane] = a.q_m[i * D + lane];
   }
 }
 
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
   const int64_t i0 = blockIdx.x;
   if (tid == 0 && i0 < a.n_local) {
     mbar_expect_tx(&bar[0], sbytes);
-    tma_bulk_g2s(smem, a.ws.colrec + (size_t)i0 * Kp * CS, sbytes, &bar[0]);
+    tma_bulk_g2s(smem, a.ws.colrec + (size_t)i0 * FwdLayout<D>::group_floats(K), sbytes, &bar[0]);
   }
   __shared__ int s_mode[2][8];
   // Groups past the first wave come from a device-wide queue (one atomic per group): per-group cost
@@ -377,8 +389,12 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
   for (int64_t i = i0; i < a.n_local; ++j) {
     const int st = j & 1;
     if (tid == 0) s_next[st] = (int64_t)gridDim.x + atomicAdd(&a.cnt->claim_fwd, 1u);
-    const float W2max = a.ws.gstat[i];
-    if (tid == 0) csum += a.ws.cvec[i];
+    // the group's records (issued one group ago) carry its scalars in the trailer
+    mbar_wait(&bar[st], (uint32_t)((j >> 1) & 1));
+    const float* col = reinterpret_cast<const float*>(smem + (st ? sbytes : 0));
+    const float* gh = col + (size_t)Kp * CS;
+    const float W2max = gh[0];
+    if (tid == 0) csum += *reinterpret_cast<const double*>(gh + 2);
 
     // ---- re-centred row coefficients for this group (before the barrier, so
     // the CTA-wide tile mode costs no extra synchronisation)
@@ -386,7 +402,7 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
     float U0sq = 0.f;
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-      u0[r] = a.q_m[i * D + r] - mur[r];
+      u0[r] = gh[4 + r] - mur[r];
       U0sq = fmaf(u0[r], u0[r], U0sq);
     }
     const float wmax = sqrtf(W2max);
@@ -428,7 +444,8 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
     const int64_t inext = s_next[st];
     if (tid == 0 && inext < a.n_local) {
       mbar_expect_tx(&bar[st ^ 1], sbytes);
-      tma_bulk_g2s(smem + (st ? 0 : sbytes), a.ws.colrec + (size_t)inext * Kp * CS, sbytes, &bar[st ^ 1]);
+      tma_bulk_g2s(smem + (st ? 0 : sbytes), a.ws.colrec + (size_t)inext * FwdLayout<D>::group_floats(K), sbytes,
+                   &bar[st ^ 1]);
     }
     // CTA-uniform mode: every warp does the same work per group (no barrier skew)
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) md = max(md, s_mode[st][w]);
@@ -438,9 +455,6 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
     mc3 += md == 3;
     mc4 += md == 4;
     mc5 += md == 5;
-    mbar_wait(&bar[st], (uint32_t)((j >> 1) & 1));
-    const float* col = reinterpret_cast<const float*>(smem + (st ? sbytes : 0));
-
     double dgv[2 * RP];
     switch (md) {
       case 0: tile_poly<D, RP, 3>(col, Kp, ga, cc, dgv); break;

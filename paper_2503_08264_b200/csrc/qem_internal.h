@@ -69,7 +69,7 @@ struct Counters {
   int32_t trace_base;  // t0 of the running qem_iterate
   unsigned long long mode_hist[8];  // forward tile modes, counted per (warp, group)
   uint32_t claim_fwd;  // k_forward's dynamic group queue (groups past the first wave); reset by its last CTA
-  uint32_t claim_pad;
+  uint32_t claim_bwd;  // k_backward's dynamic group queue; reset by k_root (which always runs just before it)
 };
 
 }  // namespace qem

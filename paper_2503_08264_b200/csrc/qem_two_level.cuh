@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(1024) k_root(TLArgs a) {
   const int K = a.K, tid = threadIdx.x;
   const int R = D + (a.scale_kind != QEM_SCALE_FIXED);
   constexpr int RS = pad4(D + 3);
+  if (tid == 0) a.cnt->claim_bwd = 0;  // the FFMA backward's group queue (stream-ordered before it)
   double mx = -CUDART_INF;
   for (int k = tid; k < K; k += blockDim.x) {
     const double av = a.ws.f_root[k] + a.ws.red[k];
@@ -348,9 +349,13 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
   float* spare = rows + (size_t)K * RS;                  // [K] (padded to even; unused)
   double* red = reinterpret_cast<double*>(spare + ((K + 1) & ~1));  // [32][D] + [32]
   const int lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
+  // groups past the first wave from a device-wide queue (claimed one group ahead; the block
+  // reductions below order the claim before every thread's read of s_next)
+  __shared__ int64_t s_next;
 
-  for (int64_t i = blockIdx.x; i < a.n_local; i += gridDim.x) {
+  for (int64_t i = blockIdx.x; i < a.n_local;) {
     __syncthreads();
+    if (tid == 0) s_next = (int64_t)gridDim.x + atomicAdd(&a.cnt->claim_bwd, 1u);
     // row table re-centred on the group's Q mean and referenced to the backward row k*
     // (DESIGN.md "Backward reference"):  log P(k'|k) = log P(k'|k*) + E_k(k') - (l_k - l_*),
     // E_k(z) = B(k,z) - B(k*,z) = E'a_ik + c''_k . w + Eg_k |w|^2 with c'' = Eb_k + 2 Eg_k m_i,
@@ -419,7 +424,8 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
         const int kc = tid + NT * (2 * p + h);
         const bool ok = kc < K;
         float rec[CS];
-        const float4* src = reinterpret_cast<const float4*>(a.ws.colrec + ((size_t)i * Kp + (ok ? kc : 0)) * CS);
+        const float4* src = reinterpret_cast<const float4*>(a.ws.colrec + (size_t)i * FwdLayout<D>::group_floats(K) +
+                                                            (size_t)(ok ? kc : 0) * CS);
 #pragma unroll
         for (int q = 0; q < CS / 4; ++q) {
           const float4 v = src[q];
@@ -529,6 +535,7 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
       a.m1[i * D + tid] = m1;
       a.v[i * D + tid] = t2 - 2.0 * dm * t1 + dm * dm * t0;
     }
+    i = s_next;
   }
 }
 
