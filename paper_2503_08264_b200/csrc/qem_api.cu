@@ -104,7 +104,8 @@ size_t carve(qem_ctx* c, char* base) {
     c->tw.bwd_table = reinterpret_cast<float*>(take(sizeof(float) * K * pad4(D + 3)));
     c->tw.f_root = reinterpret_cast<double*>(take(sizeof(double) * K));
     c->tw.ref = reinterpret_cast<qem::RefInfo*>(take(sizeof(qem::RefInfo)));
-    c->tw.partial = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->grid_fwd * (K + 1)));
+    // per-CTA plate-sum partials: fp64 (tensor-core forward) or 16-byte split sums (FFMA forward, Fx2)
+    c->tw.partial = reinterpret_cast<double*>(take(2 * sizeof(double) * (size_t)c->grid_fwd * (K + 1)));
     c->tw.red = reinterpret_cast<double*>(take(sizeof(double) * (K + 1)));
     c->tw.dg = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local * K));
     const size_t kp = (size_t)((K + 15) / 16 * 16);  // >= FwdLayout::kpad(K) for any column chunk <= 16

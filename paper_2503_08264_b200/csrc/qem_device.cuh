@@ -32,6 +32,29 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a
 // 1.5*2^23 shifter, 2^f by a degree-5 polynomial fitted on [-1/2, 1/2] (max relative error
 // 2.3e-7 in fp32, vs ~1.7e-7 for ex2.approx), 2^n added into the exponent field.
 // Inputs below -127 are clamped (2^-127: negligible wherever it is used).
+// Order-independent sum of fp64 terms (the FFMA forward's plate sums: which CTA adds which group
+// differs from launch to launch with its dynamic group queue).  Each term x is split, with two
+// round-to-grid steps (add and subtract a power-of-two-scaled 1.5), into h = x on the 2^-20 grid and
+// m = (x - h) on the 2^-57 grid (the rest, < 2^-58, is dropped); sums of h are exact while |sum h| <
+// 2^33 and sums of m while fewer than 2^17 terms meet (|m| <= 2^-21), so the totals do not depend
+// on the order.  Only DADDs (FP64 pipe): nothing lands on the XU pipe the pair tiles' ex2 saturate.
+// Past those bounds the sums stay fp64-accurate but order-dependent in the last bits.
+struct Fx2 {
+  double h = 0.0, m = 0.0;
+  __device__ __forceinline__ void add(Fx2 t) {
+    h += t.h;
+    m += t.m;
+  }
+  __device__ __forceinline__ void add(double x) {
+    const double th = __dsub_rn(__dadd_rn(x, 0x1.8p32), 0x1.8p32);  // x on the 2^-20 grid
+    const double r = __dsub_rn(x, th);                                // exact
+    const double tm = __dsub_rn(__dadd_rn(r, 0x1.8p-5), 0x1.8p-5);    // r on the 2^-57 grid
+    h += th;
+    m += tm;
+  }
+  __device__ __forceinline__ double value() const { return h + m; }
+};
+
 // ln x in fp64 for a positive normal fp32 x, branch-free: x = 2^e m with m in [sqrt(1/2), sqrt(2)),
 // ln m = 2 atanh(s), s = (m - 1)/(m + 1) (|s| <= 0.1716), the atanh series to s^21 (next term
 // < 3e-17); 1/(m + 1) from the fp32 reciprocal and two fp64 Newton steps.  Absolute error

@@ -36,8 +36,8 @@ struct FwdLayout {
   static constexpr int GH = 4 + pad4(D);
   __host__ __device__ static size_t group_floats(int K) { return (size_t)kpad(K) * CS + GH; }
   __host__ __device__ static size_t stage_bytes(int K) { return group_floats(K) * sizeof(float); }
-  // k_forward: two stages + two mbarriers
-  __host__ __device__ static size_t bytes(int K, int /*J*/) { return 2 * stage_bytes(K) + 16; }
+  // k_forward: two stages + two mbarriers + the CTA's plate-sum accumulators (K + 1 Fx2: per row, + c_i)
+  __host__ __device__ static size_t bytes(int K, int /*J*/) { return 2 * stage_bytes(K) + 16 + (size_t)(K + 1) * 16; }
   // k_colprep, per warp: tref[K] + qconst[3][D] + bern masks/labels [2J]
   __host__ __device__ static size_t prep_warp_bytes(int K, int J) {
     size_t b = (size_t)K * sizeof(double) + 3 * D * sizeof(double) + (size_t)2 * J * sizeof(uint32_t);
@@ -111,12 +111,18 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
   }
 }
 
-// Exponentials per online chunk (the last kFwdSoft of its QEM_FWD_CH columns) evaluated on the FMA
-// pipe (exp2_poly2) instead of the SFU.
-#ifndef QEM_FWD_SOFT
-#define QEM_FWD_SOFT 0
+// Exponentials per online chunk (the last fwd_soft<D>() of its QEM_FWD_CH columns) evaluated on the FMA
+// pipe (exp2_poly2) instead of the SFU.  Narrow latents (d <= 4: the contraction leaves the FMA pipe
+// half idle next to the SFU) take 2 of 16 (config 4, interleaved A/B: 0 1.886, 2 1.796, 3 1.816,
+// 4 1.847, 6 2.052 ms per forward); wide ones none.  QEM_FWD_SOFT overrides.
+template <int D>
+__host__ __device__ constexpr int fwd_soft() {
+#ifdef QEM_FWD_SOFT
+  return QEM_FWD_SOFT;
+#else
+  return D <= 4 ? 2 : 0;
 #endif
-constexpr int kFwdSoft = QEM_FWD_SOFT;
+}
 
 // Rescale margin of the online log-sum-exp (natural-log units).  0 = the shift is always the exact
 // running max, so the dominant term of every row is ex2(0) = 1 exactly: a positive margin saves
@@ -142,7 +148,12 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
       float u[D], U2, P, lnP;
       load_col<D>(col + (size_t)(kc0 + c) * CS, u, U2, P, lnP);
 #pragma unroll
-      for (int p = 0; p < RP; ++p) tv[c][p] = pair_D<D, RP>(f2(lnP), ga, cc, p, u, U2);
+      for (int p = 0; p < RP; ++p) {  // d = 1: ln P rides in the contraction's last FMA
+        if constexpr (D == 1)
+          tv[c][p] = pair_D<D, RP>(f2(lnP), ga, cc, p, u, U2);
+        else
+          tv[c][p] = add2(pair_D<D, RP>(f2(0.f), ga, cc, p, u, U2), f2(lnP));
+      }
     }
 #pragma unroll
     for (int p = 0; p < RP; ++p) {
@@ -163,7 +174,7 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const float2 e = fma2(tv[c][p], f2(kLog2e), nm);
-        s = add2(s, c >= CH - kFwdSoft ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y)));
+        s = add2(s, c >= CH - fwd_soft<D>() ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y)));
       }
       ac[p] = s;
     }
@@ -333,10 +344,14 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
 // so the column loop only sees the small within-group part and alpha'_k is
 // added back to dg at the end (exact algebra).
 template <int D, int RP>
-#ifndef QEM_FWD_MINB
-#define QEM_FWD_MINB 2  // register budget hint (min blocks of 256 threads); 2 measured best on config 4
-#endif
+// Register budget (min resident blocks of 256 threads): d <= 4 runs 2 rows per thread in <= 64
+// registers (config 4: 16 CTAs of 128 threads per SM; 4 rows in 124 registers at 8 CTAs measured
+// 1.998 ms against 1.886), wider latents keep the 128-register budget.  QEM_FWD_MINB overrides.
+#ifdef QEM_FWD_MINB
 __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
+#else
+__global__ void __launch_bounds__(256, (D <= 4 && RP == 1) ? 4 : 2) k_forward(TLArgs a) {
+#endif
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int CS = pad4(D + 3);
   constexpr int CW = D + 2;
@@ -364,10 +379,13 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
     }
     ga[p] = make_float2(gv[0], gv[1]);
   }
-  double G[2 * RP];
+  // plate-sum accumulators in shared memory (a thread owns its rows' entries; registers are the
+  // tile's): G[k] for row k, G[K] for sum_i c_i
+  Fx2* G = reinterpret_cast<Fx2*>(smem + 2 * sbytes + 16);
 #pragma unroll
-  for (int j = 0; j < 2 * RP; ++j) G[j] = 0.0;
-  double csum = 0.0;
+  for (int q = 0; q < 2 * RP; ++q)
+    if (kid[q] >= 0) G[kid[q]] = Fx2{};
+  if (tid == 0) G[K] = Fx2{};
   uint32_t mc0 = 0, mc1 = 0, mc2 = 0, mc3 = 0, mc4 = 0, mc5 = 0;
 
   if (tid == 0) {
@@ -394,7 +412,7 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
     const float* col = reinterpret_cast<const float*>(smem + (st ? sbytes : 0));
     const float* gh = col + (size_t)Kp * CS;
     const float W2max = gh[0];
-    if (tid == 0) csum += *reinterpret_cast<const double*>(gh + 2);
+    if (tid == 0) G[K].add(*reinterpret_cast<const double*>(gh + 2));
 
     // ---- re-centred row coefficients for this group (before the barrier, so
     // the CTA-wide tile mode costs no extra synchronisation)
@@ -472,18 +490,19 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
         const double dgd = ald[q] + dgv[q];
         a.ws.hmsg[(size_t)i * K + kid[q]] = (float)dgv[q];
         a.ws.dg[(size_t)i * K + kid[q]] = (float)dgd;
-        G[q] += dgd;
+        G[kid[q]].add(dgd);
       }
     }
     i = inext;
   }
 
-  // ---- per-CTA partial plate sums, then the last CTA reduces them in order.
-  double* part = a.ws.partial + (size_t)blockIdx.x * (K + 1);
+  // ---- per-CTA partial plate sums (split on fixed grids, Fx2: the groups a CTA drew from the queue
+  // vary from run to run, the sums do not), then the last CTA adds them up and rounds once to fp64.
+  Fx2* part = reinterpret_cast<Fx2*>(a.ws.partial) + (size_t)blockIdx.x * (K + 1);
 #pragma unroll
   for (int q = 0; q < 2 * RP; ++q)
-    if (kid[q] >= 0) part[kid[q]] = G[q];
-  if (tid == 0) part[K] = csum;
+    if (kid[q] >= 0) part[kid[q]] = G[kid[q]];
+  if (tid == 0) part[K] = G[K];
   if ((tid & 31) == 0)
   {
     const uint32_t mcs[6] = {mc0, mc1, mc2, mc3, mc4, mc5};
@@ -498,10 +517,14 @@ __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {
   __syncthreads();
   if (s_last) {
     __threadfence();
+    const Fx2* parts = reinterpret_cast<const Fx2*>(a.ws.partial);
     for (int k = tid; k <= K; k += blockDim.x) {
-      double sum = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(a.ws.partial + (size_t)b * (K + 1) + k);
-      a.ws.red[k] = sum;
+      Fx2 sum;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        const Fx2* pb = parts + (size_t)b * (K + 1) + k;
+        sum.add(Fx2{__ldcg(&pb->h), __ldcg(&pb->m)});
+      }
+      a.ws.red[k] = sum.value();
     }
     if (tid == 0) {
       a.cnt->ticket_fwd = 0;

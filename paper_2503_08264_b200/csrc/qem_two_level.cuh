@@ -622,6 +622,17 @@ static size_t bwd_smem(int K) {
 
 using KernelFn = void (*)(TLArgs);
 
+// The forward's rows per thread: d <= 4 keeps 2 (one row pair, the 64-register budget of k_forward)
+// up to K = 512, wider latents and larger K as the backward
+static int pick_rp_fwd(int K, int D) {
+  static const int forced = [] {
+    const char* e = getenv("QEM_RP");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2) return forced;
+  return (D <= 4 && K <= 512) ? 1 : pick_rp(K, D);  // k_forward's blocks stay <= 256 threads
+}
+
 template <int D>
 static KernelFn fwd_fn(int rp) {
   return rp == 1 ? k_forward<D, 1> : k_forward<D, 2>;
@@ -674,7 +685,8 @@ static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, in
       of = ob = 1;
     }
   } else {
-    of = occupancy(fwd_fn<D>(rp), rows_threads(K, rp), FwdLayout<D>::bytes(K, d->n_obs));
+    const int rpf = pick_rp_fwd(K, D);
+    of = occupancy(fwd_fn<D>(rpf), rows_threads(K, rpf), FwdLayout<D>::bytes(K, d->n_obs));
     ob = occupancy(bwd_fn<D>(rp), rows_threads(K, rp), bwd_smem<D>(K));
   }
   const int op = occupancy(prep_fn<D>(d->obs_kind, tc), prep_threads_tc<D>(K, tc), prep_smem<D>(K, d->n_obs, tc));
@@ -687,7 +699,7 @@ static void grids(const qem_model_desc* d, int64_t n_local, int sms, bool tc, in
 
 template <int D>
 static cudaError_t fwd_dispatch_obs(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
-  const int K = a.K, rp = pick_rp(K, D);
+  const int K = a.K, rp = pick_rp_fwd(K, D);
   int nt = (K + 31) & ~31;
   const bool tc = D <= kTcD && c->tc;
   if (tc) {  // k_ref in one block, then the rows over K/128 blocks

@@ -130,3 +130,30 @@ def test_teacher_forced_full_size_first_iterations(cid):
         state, q = ref["state"], ref["q_next"]
     assert g.read_flags()[0] & 2 == 0
     g.close()
+
+
+def test_config4_full_size_bitwise_reproducible():
+    """The FFMA pair kernels hand groups out from a device-wide queue (which CTA works which group
+    differs from launch to launch); the plate sums are order-independent split sums (Fx2), so repeated
+    E-steps -- in the same context and in a fresh one -- agree bit for bit at full size."""
+    from paper_2503_08264_b200.qem import QEM
+    m = synth.config(4)
+    data = synth.make_data(m)
+    q = posterior_like_q(m, data, seed=9, shrink=8.0)
+    outs = []
+    for rep in range(3):
+        if rep != 1:
+            g = QEM(m)
+            g.set_data(data)
+        g.set_q(q)
+        g.sample_q(seed=77, iter=1)
+        g.estep()
+        outs.append(g.result())
+        if rep != 0:
+            g.close()
+    for o in outs[1:]:
+        assert o["log_pe"] == outs[0]["log_pe"]
+        for lvl in range(2):
+            np.testing.assert_array_equal(o["w"][lvl], outs[0]["w"][lvl])
+            np.testing.assert_array_equal(o["m1"][lvl], outs[0]["m1"][lvl])
+            np.testing.assert_array_equal(o["v"][lvl], outs[0]["v"][lvl])
