@@ -257,13 +257,22 @@ __device__ __forceinline__ float2 expm1_poly(float2 x) {
   return mul2(p, x);
 }
 
-// FFMA-path tiles: 1 = evaluate 1 of every 4 exponentials on the FMA pipe (exp2_poly2) so the
-// FMA pipe and the SFU share the exp load; 0 = SFU only (default: on config 4 the software
-// exps cost more than they save, profiles/r01_poly_exp_sweep.txt).
-#ifndef QEM_SOFT_EXP_FFMA
-#define QEM_SOFT_EXP_FFMA 0
+// FFMA backward: rows of every kBwdUnroll whose exponentials run on the FMA pipe (exp2_poly2) instead
+// of the SFU.  Narrow latents (d <= 4) take 1 of 8 (config 4, interleaved A/B: 0 1.567, 1/8 1.467,
+// 2/8 1.623, 1/16 1.498, 3/16 1.529, 1/12 1.485 ms per backward); wide ones none.  QEM_BWD_SOFT
+// overrides.
+#ifndef QEM_BWD_UNROLL
+#define QEM_BWD_UNROLL 8
 #endif
-constexpr bool kSoftExpFfma = QEM_SOFT_EXP_FFMA != 0;
+constexpr int kBwdUnroll = QEM_BWD_UNROLL;
+template <int D>
+__host__ __device__ constexpr int bwd_soft() {
+#ifdef QEM_BWD_SOFT
+  return QEM_BWD_SOFT;
+#else
+  return D <= 4 ? 1 : 0;
+#endif
+}
 
 #include "qem_forward.cuh"
 #include "qem_tc.cuh"
@@ -475,9 +484,9 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
       }
     };
     int k = 0;
-    for (; k + 4 <= K; k += 4) {  // every 4th row's exponentials on the FMA pipe (kSoftExpFfma)
+    for (; k + kBwdUnroll <= K; k += kBwdUnroll) {  // the last kBwdSoft rows of each block: FMA-pipe exps
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) row(k + kk, kSoftExpFfma && kk == 3);
+      for (int kk = 0; kk < kBwdUnroll; ++kk) row(k + kk, kk >= kBwdUnroll - bwd_soft<D>());
     }
     for (; k < K; ++k) row(k, false);
     // ---- weights out + moments (fp64), one pass shifted by the Q mean c = m_i:
