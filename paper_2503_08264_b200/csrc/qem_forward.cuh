@@ -37,7 +37,12 @@ struct FwdLayout {
   __host__ __device__ static size_t group_floats(int K) { return (size_t)kpad(K) * CS + GH; }
   __host__ __device__ static size_t stage_bytes(int K) { return group_floats(K) * sizeof(float); }
   // k_forward: two stages + two mbarriers + the CTA's plate-sum accumulators (K + 1 Fx2: per row, + c_i)
-  __host__ __device__ static size_t bytes(int K, int /*J*/) { return 2 * stage_bytes(K) + 16 + (size_t)(K + 1) * 16; }
+  // (+ for d = 1 the moment tiles' per-warp partial moments, [warps <= K/64][2 NMAX])
+  static constexpr int NMAX = 9;  // highest Taylor degree of the polynomial modes
+  __host__ __device__ static size_t mom_bytes(int K) { return D == 1 ? (size_t)((K + 63) / 64) * 2 * NMAX * 8 : 0; }
+  __host__ __device__ static size_t bytes(int K, int /*J*/) {
+    return 2 * stage_bytes(K) + 16 + (size_t)(K + 1) * 16 + mom_bytes(K);
+  }
   // k_colprep, per warp: tref[K] + qconst[3][D] + bern masks/labels [2J]
   __host__ __device__ static size_t prep_warp_bytes(int K, int J) {
     size_t b = (size_t)K * sizeof(double) + 3 * D * sizeof(double) + (size_t)2 * J * sizeof(uint32_t);
@@ -109,6 +114,90 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
     dgv[2 * p] = log1p((double)acc[p].x);  // fp64 logs: the fp32 ones' ~1-ulp errors are not zero-mean,
     dgv[2 * p + 1] = log1p((double)acc[p].y);  // and they add up coherently over the groups' plate sum
   }
+}
+
+// Polynomial modes for d = 1 through the group's column moments.  With D'_k(k') = g_k w^2 + c_k w
+// (w = w(k'), the row's re-centred coefficients), the degree-N Taylor sum of tile_poly is
+//   sum_k' P(k') expm1_N(D'_k(k')) = sum_{n=1..N} (1/n!) sum_{j=0..n} C(n,j) g_k^j c_k^(n-j) mu_{n+j},
+//   mu_p = sum_k' P(k') w(k')^p   (p = 1 .. 2N, the same for every row of the group),
+// the same polynomial rearranged (exact algebra): O(K N) moments + O(N^2) per row instead of O(N) per
+// pair, all in fp64.  No cancellation beyond the Taylor terms' own size: the mode's bound tb >=
+// |c_k| max|w| + |g_k| max w^2 bounds every expanded term by tb^n.  The moments are reduced in a
+// fixed order (warp butterflies, then warps in index order), so the result is deterministic.
+template <int N>
+__device__ __forceinline__ double poly_from_moments(double g, double c, const double* mu) {
+  double gp[N + 1], cp[N + 1];
+  gp[0] = 1.0;
+  cp[0] = 1.0;
+#pragma unroll
+  for (int j = 1; j <= N; ++j) {
+    gp[j] = gp[j - 1] * g;
+    cp[j] = cp[j - 1] * c;
+  }
+  double acc = 0.0, fact = 1.0;
+#pragma unroll
+  for (int n = 1; n <= N; ++n) {
+    fact *= n;
+    double sn = 0.0, bin = 1.0;  // C(n, j)
+#pragma unroll
+    for (int j = 0; j <= n; ++j) {
+      sn = fma(bin * gp[j] * cp[n - j], mu[n + j - 1], sn);
+      bin = bin * (n - j) / (j + 1);
+    }
+    acc = fma(sn, 1.0 / fact, acc);
+  }
+  return acc;
+}
+
+template <int RP, int N>
+__device__ __forceinline__ void tile_moments1(const float* col, int K, const float2 (&ga)[RP], const float2 (&cc)[RP][1],
+                                              double (&dgv)[2 * RP], double* s_mom) {
+  constexpr int CS = pad4(4), NM = 2 * N;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  double m[NM];
+#pragma unroll
+  for (int p = 0; p < NM; ++p) m[p] = 0.0;
+  for (int kc = tid; kc < K; kc += blockDim.x) {
+    const double w = col[(size_t)kc * CS], P = col[(size_t)kc * CS + FwdLayout<1>::IP];
+    double pw = P;
+#pragma unroll
+    for (int p = 0; p < NM; ++p) {
+      pw *= w;
+      m[p] += pw;
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < NM; ++p) m[p] = warp_sum(m[p]);
+  if (lane == 0)
+#pragma unroll
+    for (int p = 0; p < NM; ++p) s_mom[wid * NM + p] = m[p];
+  __syncthreads();
+  double mu[NM];
+#pragma unroll
+  for (int p = 0; p < NM; ++p) mu[p] = 0.0;
+  for (int w = 0; w < nw; ++w)
+#pragma unroll
+    for (int p = 0; p < NM; ++p) mu[p] += s_mom[w * NM + p];
+#pragma unroll
+  for (int p = 0; p < RP; ++p) {
+    dgv[2 * p] = log1p(poly_from_moments<N>((double)ga[p].x, (double)cc[p][0].x, mu));
+    dgv[2 * p + 1] = log1p(poly_from_moments<N>((double)ga[p].y, (double)cc[p][0].y, mu));
+  }
+}
+
+// 1 = d = 1 polynomial modes through the column moments (tile_moments1), 0 = per pair (tile_poly)
+#ifndef QEM_MOMENT_TILES
+#define QEM_MOMENT_TILES 1
+#endif
+constexpr bool kMomentTiles = QEM_MOMENT_TILES != 0;
+
+template <int D, int RP, int N>
+__device__ __forceinline__ void tile_poly_mode(const float* col, int K, int Kp, const float2 (&ga)[RP],
+                                               const float2 (&cc)[RP][D], double (&dgv)[2 * RP], double* s_mom) {
+  if constexpr (D == 1 && kMomentTiles)
+    tile_moments1<RP, N>(col, K, ga, cc, dgv, s_mom);
+  else
+    tile_poly<D, RP, N>(col, Kp, ga, cc, dgv);
 }
 
 // Exponentials per online chunk (the last fwd_soft<D>() of its QEM_FWD_CH columns) evaluated on the FMA
@@ -382,6 +471,7 @@ __global__ void __launch_bounds__(256, (D <= 4 && RP == 1) ? 4 : 2) k_forward(TL
   // plate-sum accumulators in shared memory (a thread owns its rows' entries; registers are the
   // tile's): G[k] for row k, G[K] for sum_i c_i
   Fx2* G = reinterpret_cast<Fx2*>(smem + 2 * sbytes + 16);
+  double* s_mom = reinterpret_cast<double*>(smem + 2 * sbytes + 16 + (size_t)(K + 1) * 16);  // d = 1 moment tiles
 #pragma unroll
   for (int q = 0; q < 2 * RP; ++q)
     if (kid[q] >= 0) G[kid[q]] = Fx2{};
@@ -475,11 +565,11 @@ __global__ void __launch_bounds__(256, (D <= 4 && RP == 1) ? 4 : 2) k_forward(TL
     mc5 += md == 5;
     double dgv[2 * RP];
     switch (md) {
-      case 0: tile_poly<D, RP, 3>(col, Kp, ga, cc, dgv); break;
-      case 1: tile_poly<D, RP, 4>(col, Kp, ga, cc, dgv); break;
-      case 2: tile_poly<D, RP, 5>(col, Kp, ga, cc, dgv); break;
-      case 3: tile_poly<D, RP, 7>(col, Kp, ga, cc, dgv); break;
-      case 4: tile_poly<D, RP, 9>(col, Kp, ga, cc, dgv); break;
+      case 0: tile_poly_mode<D, RP, 3>(col, K, Kp, ga, cc, dgv, s_mom); break;
+      case 1: tile_poly_mode<D, RP, 4>(col, K, Kp, ga, cc, dgv, s_mom); break;
+      case 2: tile_poly_mode<D, RP, 5>(col, K, Kp, ga, cc, dgv, s_mom); break;
+      case 3: tile_poly_mode<D, RP, 7>(col, K, Kp, ga, cc, dgv, s_mom); break;
+      case 4: tile_poly_mode<D, RP, 9>(col, K, Kp, ga, cc, dgv, s_mom); break;
       default: tile_online<D, RP>(col, Kp, ga, cc, dgv); break;
     }
     // h = log sum P exp(D') feeds the backward directly (no cancellation against
