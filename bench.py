@@ -312,7 +312,8 @@ def measure_step(m, args, world, rank, dev, in_library, seed):
                            f"evaluated in software on the FMA pipe ({FMA_PER_SOFT_EXP:.0f} lane-ops each)"),
             "kernels_ms": {"forward": fwd_ms, "backward": bwd_ms, "allreduce": comm_ms},
             "forward_mode_hist": dict(zip(["expm1_deg3", "deg4", "deg5", "deg7", "deg9", "online_lse"],
-                                          [int(x) for x in hist[:6]]))}
+                                          [int(x) for x in hist[:6]])),
+            "backward_moment_groups": int(hist[6])}
     out = dict(g=g, data=data, gb=gb, ge=ge, ms_step=ms_step, value=m.pairs / (ms_step * 1e-3),
                launched=launched[0], flags=flags, clamps=clamps, clocks=clk, roofline=roof, tc=tc, t=t,
                allreduce=runner.allreduce_plate_sum, nccl=g.nccl_info() if in_library else None)
@@ -893,6 +894,7 @@ def run_converged_variant(args, dev, steps=5):
                                "unit": "factor-pairs/s", "forward_ms": fwd,
                                "forward_mode_hist": {"expm1_deg3": hist[0], "deg4": hist[1], "deg5": hist[2],
                                                      "deg7": hist[3], "deg9": hist[4], "online_lse": hist[5]},
+                               "backward_moment_groups": hist[6],
                                "forward_roofline": {"bound": "alu", "pipe": "fma (mode mix)",
                                                     "achieved": achieved / 1e9, "peak": ceiling / 1e9,
                                                     "unit": "Gpair/s", "frac": achieved / ceiling}}

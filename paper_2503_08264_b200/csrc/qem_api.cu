@@ -117,11 +117,12 @@ size_t carve(qem_ctx* c, char* base) {
       c->tw.rowop_x = take((size_t)K * 32);
       c->tw.colop = take((size_t)c->n_local * K * (D == 1 ? 64 : 128));  // TcGeo<D>::COL
       c->tw.colaux = reinterpret_cast<float*>(take((size_t)c->n_local * K * 8));
-      c->tw.gmode = reinterpret_cast<int*>(take(sizeof(int) * (size_t)c->n_local));
       c->tw.rowop_b = take((size_t)K * 96);
       c->tw.bgam = reinterpret_cast<float*>(take(sizeof(float) * K));
     }
     c->tw.gstat = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local));
+    c->tw.gmode = reinterpret_cast<int*>(take(sizeof(int) * (size_t)c->n_local));  // TC forward tile modes
+    c->tw.gtb = reinterpret_cast<float*>(take(sizeof(float) * (size_t)c->n_local));  // FFMA d = 1 bounds
     c->tw.cvec = reinterpret_cast<double*>(take(sizeof(double) * (size_t)c->n_local));
     c->tw.perm = reinterpret_cast<int*>(take(sizeof(int) * K));
     c->tw.alpha_d = reinterpret_cast<double*>(take(sizeof(double) * K));

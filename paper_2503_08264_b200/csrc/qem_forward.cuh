@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(256, (D <= 4 && RP == 1) ? 4 : 2) k_forward(TL
     tma_bulk_g2s(smem, a.ws.colrec + (size_t)i0 * FwdLayout<D>::group_floats(K), sbytes, &bar[0]);
   }
   __shared__ int s_mode[2][8];
+  __shared__ float s_tb[2][8];  // d = 1: per-warp |D'| bounds (the backward's moment-tile decision)
   // Groups past the first wave come from a device-wide queue (one atomic per group): per-group cost
   // depends on the tile mode, so a static stride leaves CTAs idle at the end of the launch.
   __shared__ int64_t s_next[2];
@@ -546,6 +547,10 @@ __global__ void __launch_bounds__(256, (D <= 4 && RP == 1) ? 4 : 2) k_forward(TL
     int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
     md = __reduce_max_sync(0xffffffffu, md);
     if ((tid & 31) == 0) s_mode[st][tid >> 5] = md;
+    if constexpr (D == 1) {  // tb >= 0: its bits order like unsigned integers
+      const float tbw = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tb)));
+      if ((tid & 31) == 0) s_tb[st][tid >> 5] = tbw;
+    }
 
     // all warps are done with the other stage (group j-1): refill it with group j+1
     __syncthreads();
@@ -557,6 +562,13 @@ __global__ void __launch_bounds__(256, (D <= 4 && RP == 1) ? 4 : 2) k_forward(TL
     }
     // CTA-uniform mode: every warp does the same work per group (no barrier skew)
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) md = max(md, s_mode[st][w]);
+    if constexpr (D == 1) {
+      if (tid == 0) {
+        float tbg = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tbg = fmaxf(tbg, s_tb[st][w]);
+        a.ws.gtb[i] = tbg;
+      }
+    }
     mc0 += md == 0;
     mc1 += md == 1;
     mc2 += md == 2;

@@ -42,6 +42,7 @@ struct TwoLevelWs {
   void* colop;        // [n_local][K] x 128 B  u = z - mu_ref split + column extra slab
   float* colaux;      // [n_local][2][K] SoA {P, ln P}
   int* gmode;         // [n_local]  forward tile mode of the group (decided in k_colprep_tc)
+  float* gtb;         // [n_local]  FFMA d = 1: the forward's bound on |D'| over the group (k_forward), 2x bounds the backward's |E|
   double* tA;         // [n_local][K] t_ref(k') = B(k_ref,k') + A_i(k'), A = sum_j log p(x_ij|z^k') - log q(z^k') (fp64)
   void* rowop_b;      // [K] x 96 B  backward rows: log2e (e_k mu_k - e_* mu_*) split (k_star-differenced)
   float* bgam;        // [K]        backward log2e gamma*_k = -log2e (e_k - e_*) / 2

@@ -345,6 +345,112 @@ __global__ void __launch_bounds__(1024) k_root(TLArgs a) {
   }
 }
 
+// Taylor degree slot (0-4: degree 3/4/5/7/9, 5: none) for a bound on |exponent| (the forward's thresholds)
+__device__ __forceinline__ int bwd_mom_mode(const TLArgs& a, float tb) {
+  return tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
+}
+
+// Column constants of the backward, log P(k'|k*): softmax over the group's columns of the fp64 logits
+// t_ref(k') + B(k*,k') - B(k_ref,k') (t_ref from the column prep); thread t holds columns t + NT (2p + h).
+template <int D, int CP>
+__device__ __forceinline__ double bwd_col_logits(const TLArgs& a, int64_t i, double (&tl)[CP][2], double* red) {
+  const int K = a.K, tid = threadIdx.x, NT = blockDim.x;
+  double tmx = -CUDART_INF;
+  {
+    const double es = a.ws.ref->e_star, bs = a.ws.ref->bstar_const;
+#pragma unroll
+    for (int p = 0; p < CP; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kc = tid + NT * (2 * p + h);
+        tl[p][h] = -CUDART_INF;
+        if (kc < K) {
+          double d2 = 0.0, g2 = 0.0;
+#pragma unroll
+          for (int r = 0; r < D; ++r) {
+            const double zz = (double)a.z[((size_t)i * D + r) * K + kc];
+            const double dz = zz - (double)a.ws.ref->mu_star[r], gz = zz - (double)a.ws.ref->mu_ref[r];
+            d2 += dz * dz;
+            g2 += gz * gz;
+          }
+          // t_ref + B(k*,k') - B(k_ref,k')
+          tl[p][h] = (bs - 0.5 * es * d2) - (a.ws.ref->bref_const - 0.5 * a.ws.ref->e_ref * g2) +
+                     a.ws.tA[(size_t)i * K + kc];
+          tmx = fmax(tmx, tl[p][h]);
+        }
+      }
+  }
+  tmx = block_max(tmx, red);
+  double tse = 0.0;
+#pragma unroll
+  for (int p = 0; p < CP; ++p)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (tid + NT * (2 * p + h) < K) tse += exp(tl[p][h] - tmx);
+  return tmx + log(block_sum(tse, red));
+}
+
+// Weights out + moments of one group (fp64), one pass shifted by the Q mean c = m_i (see k_backward).
+template <int D, int CP>
+__device__ __forceinline__ void bwd_out_moments(const TLArgs& a, int64_t i, const float2 (&acc)[CP], double* red) {
+  const int K = a.K, tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
+  // ---- weights out + moments (fp64), one pass shifted by the Q mean c = m_i:
+  // S0 = sum w, S1 = sum w (z - c), S2 = sum w (z - c)^2, then E z = c S0 + S1 and
+  // sum w (z - E z)^2 = S2 - 2 (E z - c) S1 + (E z - c)^2 S0 (exact algebra; one z conversion
+  // per column and dimension instead of two, and one block reduction instead of two)
+  double s0 = 0.0, s1[D], s2[D], cq[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    s1[r] = 0.0;
+    s2[r] = 0.0;
+    cq[r] = (double)a.q_m[i * D + r];
+  }
+  bool bad = false;
+#pragma unroll
+  for (int p = 0; p < CP; ++p)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kc = tid + NT * (2 * p + h);
+      if (kc < K) {
+        const float wf = h ? acc[p].y : acc[p].x;
+        bad |= isnan(wf);
+        a.w[(size_t)i * K + kc] = wf;
+        const double wv = wf;
+        s0 += wv;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          const double e = (double)a.z[((size_t)i * D + r) * K + kc] - cq[r];
+          const double we = wv * e;
+          s1[r] += we;
+          s2[r] = fma(we, e, s2[r]);
+        }
+      }
+    }
+  if (bad) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+  s0 = warp_sum(s0);
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    const double v1 = warp_sum(s1[r]), v2 = warp_sum(s2[r]);
+    if (lane == 0) {
+      red[wid * D + r] = v1;
+      red[(nw + wid) * D + r] = v2;
+    }
+  }
+  if (lane == 0) red[32 * D + wid] = s0;  // red: [32 D] (S1, S2: 2 nw D <= 32 D, nw <= 16) + [32] (S0)
+  __syncthreads();
+  if (tid < D) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      t0 += red[32 * D + w];
+      t1 += red[w * D + tid];
+      t2 += red[(nw + w) * D + tid];
+    }
+    const double m1 = cq[tid] * t0 + t1, dm = m1 - cq[tid];
+    a.m1[i * D + tid] = m1;
+    a.v[i * D + tid] = t2 - 2.0 * dm * t1 + dm * dm * t0;
+  }
+}
+
 // ----------------------------------------------------------- backward (K4)
 // Thread t owns columns k' = t + NT*(2p+h); the row table (alpha'', gamma',
 // c', w_root) is in shared memory and read as warp-broadcasts.
@@ -365,6 +471,13 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
   for (int64_t i = blockIdx.x; i < a.n_local;) {
     __syncthreads();
     if (tid == 0) s_next = (int64_t)gridDim.x + atomicAdd(&a.cnt->claim_bwd, 1u);
+    if constexpr (D == 1 && kMomentTiles) {
+      if (bwd_mom_mode(a, 2.f * a.ws.gtb[i]) < 5) {  // k_backward_mom1's group (launched just before)
+        __syncthreads();
+        i = s_next;
+        continue;
+      }
+    }
     // row table re-centred on the group's Q mean and referenced to the backward row k*
     // (DESIGN.md "Backward reference"):  log P(k'|k) = log P(k'|k*) + E_k(k') - (l_k - l_*),
     // E_k(z) = B(k,z) - B(k*,z) = E'a_ik + c''_k . w + Eg_k |w|^2 with c'' = Eb_k + 2 Eg_k m_i,
@@ -391,39 +504,7 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
     // column constants log P(k'|k*): softmax over the group's columns of the fp64 logits
     // B(k*,k') + A_i(k') (A from the column prep)
     double tl[CP][2];
-    double tmx = -CUDART_INF;
-    {
-      const double es = a.ws.ref->e_star, bs = a.ws.ref->bstar_const;
-#pragma unroll
-      for (int p = 0; p < CP; ++p)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kc = tid + NT * (2 * p + h);
-          tl[p][h] = -CUDART_INF;
-          if (kc < K) {
-            double d2 = 0.0, g2 = 0.0;
-#pragma unroll
-            for (int r = 0; r < D; ++r) {
-              const double zz = (double)a.z[((size_t)i * D + r) * K + kc];
-              const double dz = zz - (double)a.ws.ref->mu_star[r], gz = zz - (double)a.ws.ref->mu_ref[r];
-              d2 += dz * dz;
-              g2 += gz * gz;
-            }
-            // t_ref + B(k*,k') - B(k_ref,k')
-            tl[p][h] = (bs - 0.5 * es * d2) - (a.ws.ref->bref_const - 0.5 * a.ws.ref->e_ref * g2) +
-                       a.ws.tA[(size_t)i * K + kc];
-            tmx = fmax(tmx, tl[p][h]);
-          }
-        }
-    }
-    tmx = block_max(tmx, red);
-    double tse = 0.0;
-#pragma unroll
-    for (int p = 0; p < CP; ++p)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (tid + NT * (2 * p + h) < K) tse += exp(tl[p][h] - tmx);
-    const double tlse = tmx + log(block_sum(tse, red));
+    const double tlse = bwd_col_logits<D, CP>(a, i, tl, red);
 #pragma unroll
     for (int p = 0; p < CP; ++p) {
       float uu[2][D], u2[2], lc[2];
@@ -489,63 +570,135 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
       for (int kk = 0; kk < kBwdUnroll; ++kk) row(k + kk, kk >= kBwdUnroll - bwd_soft<D>());
     }
     for (; k < K; ++k) row(k, false);
-    // ---- weights out + moments (fp64), one pass shifted by the Q mean c = m_i:
-    // S0 = sum w, S1 = sum w (z - c), S2 = sum w (z - c)^2, then E z = c S0 + S1 and
-    // sum w (z - E z)^2 = S2 - 2 (E z - c) S1 + (E z - c)^2 S0 (exact algebra; one z conversion
-    // per column and dimension instead of two, and one block reduction instead of two)
-    double s0 = 0.0, s1[D], s2[D], cq[D];
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-      s1[r] = 0.0;
-      s2[r] = 0.0;
-      cq[r] = (double)a.q_m[i * D + r];
-    }
-    bool bad = false;
-#pragma unroll
-    for (int p = 0; p < CP; ++p)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int kc = tid + NT * (2 * p + h);
-        if (kc < K) {
-          const float wf = h ? acc[p].y : acc[p].x;
-          bad |= isnan(wf);
-          a.w[(size_t)i * K + kc] = wf;
-          const double wv = wf;
-          s0 += wv;
-#pragma unroll
-          for (int r = 0; r < D; ++r) {
-            const double e = (double)a.z[((size_t)i * D + r) * K + kc] - cq[r];
-            const double we = wv * e;
-            s1[r] += we;
-            s2[r] = fma(we, e, s2[r]);
-          }
-        }
-      }
-    if (bad) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
-    s0 = warp_sum(s0);
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-      const double v1 = warp_sum(s1[r]), v2 = warp_sum(s2[r]);
-      if (lane == 0) {
-        red[wid * D + r] = v1;
-        red[(nw + wid) * D + r] = v2;
-      }
-    }
-    if (lane == 0) red[32 * D + wid] = s0;  // red: [32 D] (S1, S2: 2 nw D <= 32 D, nw <= 16) + [32] (S0)
-    __syncthreads();
-    if (tid < D) {
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-      for (int w = 0; w < nw; ++w) {
-        t0 += red[32 * D + w];
-        t1 += red[w * D + tid];
-        t2 += red[(nw + w) * D + tid];
-      }
-      const double m1 = cq[tid] * t0 + t1, dm = m1 - cq[tid];
-      a.m1[i * D + tid] = m1;
-      a.v[i * D + tid] = t2 - 2.0 * dm * t1 + dm * dm * t0;
-    }
+    bwd_out_moments<D, CP>(a, i, acc, red);
     i = s_next;
   }
+}
+
+// ----------------------------------------------------- backward moment tiles (K4, d = 1)
+// The backward for d = 1 groups whose |E| bound admits a Taylor mode (the backward twin of the forward's
+// tile_moments1), one warp per group.  Per column k',
+//   w(k') = P(k'|k*) sum_k a_k e^{E_k(w)},  a_k = w_root(k) 2^{rho_k},  E_k(w) = beta_k w + gamma_k w^2
+// (k_backward's row table: rho_k = -log2e (h_k - h_*), in natural units for E), and with
+// e^E = sum_{n<=N} E^n / n! (degree N from the bound on |E| over the group's rows and columns, with the
+// forward's thresholds; the groups are those whose 2 x forward bound admits a mode, k_backward skips them):
+//   sum_k a_k e^{E_k(w)} = sum_{p=0..2N} A_p w^p,  A_p = sum_{n+j=p, j<=n<=N} C(n,j)/n! sum_k a_k gamma_k^j beta_k^(n-j)
+// -- the pair sum rearranged (exact algebra): O(K N^2) per group + O(N) per column in fp64 instead of
+// one exponential per pair; the coefficients are reduced in a fixed order (warp butterflies).
+template <int N>
+__device__ __forceinline__ void bwd_mom_group(const TLArgs& a, int64_t i, float mi) {
+  constexpr int NC = 2 * N + 1;
+  const int K = a.K, lane = threadIdx.x & 31;
+  const float hs = a.ws.hmsg[(size_t)i * K + a.ws.ref->k_star];
+  double A[NC];
+#pragma unroll
+  for (int p = 0; p < NC; ++p) A[p] = 0.0;
+  for (int k = lane; k < K; k += 32) {
+    const float wr = a.w_root[k];
+    if (wr == 0.f) continue;
+    const float g = a.ws.bwd_coef[(size_t)k * 2 + 1];
+    const double ak = (double)(wr * ex2(-(a.ws.hmsg[(size_t)i * K + k] - hs) * kLog2e));  // as the pair path
+    const double ga = g, be = fmaf(2.f * g, mi, a.ws.bwd_coef[(size_t)k * 2]);
+    double gp[N + 1], bp[N + 1];
+    gp[0] = ak;  // a_k rides on the gamma powers
+    bp[0] = 1.0;
+#pragma unroll
+    for (int j = 1; j <= N; ++j) {
+      gp[j] = gp[j - 1] * ga;
+      bp[j] = bp[j - 1] * be;
+    }
+    double fact = 1.0;
+#pragma unroll
+    for (int n = 0; n <= N; ++n) {
+      if (n > 0) fact *= n;
+      double bin = 1.0 / fact;  // C(n, j) / n!
+#pragma unroll
+      for (int j = 0; j <= n; ++j) {
+        A[n + j] = fma(bin * gp[j], bp[n - j], A[n + j]);
+        bin = bin * (n - j) / (j + 1);
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < NC; ++p) A[p] = warp_sum(A[p]);
+  // column logits t_ref + B(k*,.) - B(k_ref,.) and their softmax (fp64, as bwd_col_logits)
+  const double es = a.ws.ref->e_star, bs = a.ws.ref->bstar_const;
+  const double er = a.ws.ref->e_ref, br = a.ws.ref->bref_const;
+  const double mus = a.ws.ref->mu_star[0], mur = a.ws.ref->mu_ref[0];
+  const float* zg = a.z + (size_t)i * K;
+  const double* tA = a.ws.tA + (size_t)i * K;
+  auto logit = [&](int kc) {
+    const double zz = zg[kc], dz = zz - mus, gz = zz - mur;
+    return (bs - 0.5 * es * dz * dz) - (br - 0.5 * er * gz * gz) + tA[kc];
+  };
+  double tmx = -CUDART_INF;
+  for (int kc = lane; kc < K; kc += 32) tmx = fmax(tmx, logit(kc));
+  tmx = warp_max(tmx);
+  double tse = 0.0;
+  for (int kc = lane; kc < K; kc += 32) tse += exp(logit(kc) - tmx);
+  const double tlse = tmx + log(warp_sum(tse));
+  // weights and the moments (one pass shifted by the Q mean, as bwd_out_moments)
+  const float* rec = a.ws.colrec + (size_t)i * FwdLayout<1>::group_floats(K);
+  const double cq = mi;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  bool bad = false;
+  for (int kc = lane; kc < K; kc += 32) {
+    const double w = rec[(size_t)kc * FwdLayout<1>::CS];
+    double sp = A[NC - 1];
+#pragma unroll
+    for (int q = NC - 2; q >= 0; --q) sp = fma(sp, w, A[q]);
+    const float wf = ex2((float)((logit(kc) - tlse) * kLog2eD)) * (float)sp;  // P(k'|k*) as the pair path's Lc
+    bad |= isnan(wf);
+    a.w[(size_t)i * K + kc] = wf;
+    const double wv = wf, e = (double)zg[kc] - cq, we = wv * e;
+    s0 += wv;
+    s1 += we;
+    s2 = fma(we, e, s2);
+  }
+  if (bad) atomicOr(&a.cnt->flags, (uint32_t)QEM_FLAG_NAN);
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    const double m1 = cq * s0 + s1, dm = m1 - cq;
+    a.m1[i] = m1;
+    a.v[i] = s2 - 2.0 * dm * s1 + dm * dm * s0;
+  }
+}
+
+template <int D>  // D = 1 (a template so each per-d translation unit has its own instance)
+__global__ void __launch_bounds__(256) k_backward_mom1(TLArgs a) {
+  const int K = a.K, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t nmom = 0;
+  // warp gw owns groups gw + j TW (TW warps in the grid) and scans 32 of them at a time (one load of
+  // their bounds per lane, a ballot), then works its moment groups one by one.  E_k = D'_k - D'_{k*}
+  // (both re-centred on m_i), so 2x the forward's bound on |D'| bounds |E|: the cheap decision
+  // k_backward takes too; the degree below comes from the group's own bound.
+  const int64_t gw = (int64_t)blockIdx.x * nw + wid, TW = (int64_t)gridDim.x * nw;
+  for (int64_t j0 = 0; gw + j0 * TW < a.n_local; j0 += 32) {
+    const int64_t il = gw + (j0 + lane) * TW;
+    const bool mine = il < a.n_local && bwd_mom_mode(a, 2.f * a.ws.gtb[il]) < 5;
+    for (uint32_t bits = __ballot_sync(0xffffffffu, mine); bits; bits &= bits - 1) {
+      const int64_t i = gw + (j0 + __ffs(bits) - 1) * TW;
+      const float mi = a.q_m[i], W2m = a.ws.gstat[i], wm = sqrtf(W2m);
+      // bound on |E_k(w)| = |beta_k w + gamma_k w^2| over the rows and the group's columns
+      float tbb = 0.f;
+      for (int k = lane; k < K; k += 32) {
+        const float g = a.ws.bwd_coef[(size_t)k * 2 + 1];
+        tbb = fmaxf(tbb, fabsf(fmaf(2.f * g, mi, a.ws.bwd_coef[(size_t)k * 2])) * wm + fabsf(g) * W2m);
+      }
+      const int md = bwd_mom_mode(a, fminf(warp_maxf(tbb), 2.f * a.ws.gtb[i]));
+      ++nmom;
+      switch (md) {
+        case 0: bwd_mom_group<3>(a, i, mi); break;
+        case 1: bwd_mom_group<4>(a, i, mi); break;
+        case 2: bwd_mom_group<5>(a, i, mi); break;
+        case 3: bwd_mom_group<7>(a, i, mi); break;
+        default: bwd_mom_group<9>(a, i, mi); break;
+      }
+    }
+  }
+  if (lane == 0 && nmom) atomicAdd(&a.cnt->mode_hist[6], (unsigned long long)nmom);  // diagnostics slot 6
 }
 
 // ---------------------------------------------------------------- launchers
@@ -761,8 +914,13 @@ static cudaError_t bwd_dispatch(qem_ctx* c, const TLArgs& a, cudaStream_t st) {
   if (c->ev[2]) cudaEventRecord((cudaEvent_t)c->ev[2], st);
   if (tc)
     k_backward_tc<DT><<<c->grid_bwd, kBwdThreads, BwdTcL<DT>::bytes(K), st>>>(a);
-  else
+  else {
+    if constexpr (D == 1 && kMomentTiles) {
+      k_backward_mom1<D><<<c->grid_prep, 256, 0, st>>>(a);  // one warp per group, like the column prep
+      c->launches += 1;
+    }
     bwd_fn<D>(cp)<<<c->grid_bwd, rows_threads(K, cp), bwd_smem<D>(K), st>>>(a);
+  }
   if (c->ev[3]) cudaEventRecord((cudaEvent_t)c->ev[3], st);
   if (tc) {
     if constexpr (TcGeo<DT>::COMPACT)
