@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
 // added back to dg at the end (exact algebra).
 template <int D, int RP>
 // Register budget (min resident blocks of 256 threads): d <= 4 runs 2 rows per thread in <= 64
-// registers (config 4: 16 CTAs of 128 threads per SM; 4 rows in 124 registers at 8 CTAs measured
+// registers (config 4: 8 CTAs of 128 threads = 32 warps per SM; 4 rows in 124 registers at 8 CTAs of 64 measured
 // 1.998 ms against 1.886), wider latents keep the 128-register budget.  QEM_FWD_MINB overrides.
 #ifdef QEM_FWD_MINB
 __global__ void __launch_bounds__(256, QEM_FWD_MINB) k_forward(TLArgs a) {

@@ -32,6 +32,7 @@ def _gpu_estep(m, data, q, eps):
     dg, c = g.messages()
     out["dg"], out["c"] = dg.cpu().numpy(), c.cpu().numpy()
     out["flags"] = g.read_flags()[0]
+    out["mode_hist"] = g.mode_hist()
     g.close()
     return out
 
@@ -61,6 +62,8 @@ def test_config4_full_size(regime):
     out = _gpu_estep(m, data, q, eps)
     check_estep(m, out, ref, note=f"config4 full/{regime}")
     assert out["flags"] & 2 == 0
+    if regime == "converged":  # the d = 1 moment tiles ran: forward Taylor modes and backward moment groups
+        assert sum(out["mode_hist"][:5]) > 0 and out["mode_hist"][6] > 0, out["mode_hist"]
     if regime == "iteration1":
         # one-hot regime: far rows carry O(100) log-factors that fp32 resolves to ~1e-5;
         # only the contract quantities above are gated there
