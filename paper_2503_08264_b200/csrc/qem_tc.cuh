@@ -396,6 +396,12 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
   }
   unsigned char* colop = reinterpret_cast<unsigned char*>(a.ws.colop);
   const int64_t gstride = (int64_t)gridDim.x * PrepTc::WARPS;
+  // max_k |gamma_k| (the rows are the same for every group): the tile-mode bound below is >= max_k
+  // |gamma_k| max |w|^2, so a group whose that alone passes the highest Taylor threshold is online
+  // without the bound's K x D pass over the rows
+  float gmax = 0.f;
+  for (int k = lane; k < K; k += 32) gmax = fmaxf(gmax, fabsf(__ldg(a.ws.fwd_coef + (size_t)k * (D + 2) + 1)));
+  gmax = warp_maxf(gmax);
   if (!fuse && (int64_t)blockIdx.x * PrepTc::WARPS + wid < a.n_local)
     stage_z((int64_t)blockIdx.x * PrepTc::WARPS + wid, 0, 0);
   for (int64_t i = (int64_t)blockIdx.x * PrepTc::WARPS + wid; i < a.n_local; i += gstride) {
@@ -576,9 +582,9 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
 #pragma unroll
     for (int r = 0; r < D; ++r) u0[r] = u0f[r];
     const float wmax = sqrtf(W2max);
-    float tb = 0.f;
+    float tb = gmax * W2max;
 #pragma unroll 4  // fwd_coef rows stream from L2: keep several rows' loads in flight
-    for (int k = lane; k < K; k += 32) {
+    for (int k = tb > a.thr[4] ? K : lane; k < K; k += 32) {
       const float2* fc = reinterpret_cast<const float2*>(a.ws.fwd_coef + (size_t)k * (D + 2));  // D even
       const float2 h = __ldg(fc);
       const float g = h.y;
