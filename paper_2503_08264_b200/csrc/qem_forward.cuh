@@ -598,13 +598,22 @@ __global__ void __launch_bounds__(256, (D <= 4 && RP == 1) ? 4 : 2) k_forward(TL
     i = inext;
   }
 
-  // ---- per-CTA partial plate sums (split on fixed grids, Fx2: the groups a CTA drew from the queue
-  // vary from run to run, the sums do not), then the last CTA adds them up and rounds once to fp64.
-  Fx2* part = reinterpret_cast<Fx2*>(a.ws.partial) + (size_t)blockIdx.x * (K + 1);
+  // ---- plate sums: each CTA adds its rows' split sums (Fx2) into the (K + 1) x {h, m} accumulators
+  // k_root_prep zeroed; the parts are exact sums on fixed grids, so the atomics' order (which CTA
+  // drew which groups from the queue, which CTA adds first) cannot change a bit (R39), and
+  // no CTA has to walk every CTA's partials at the end (1184 of them on config 4).
+  double* acc_h = a.ws.partial;
+  double* acc_m = a.ws.partial + (K + 1);
 #pragma unroll
   for (int q = 0; q < 2 * RP; ++q)
-    if (kid[q] >= 0) part[kid[q]] = G[kid[q]];
-  if (tid == 0) part[K] = G[K];
+    if (kid[q] >= 0) {
+      atomicAdd(&acc_h[kid[q]], G[kid[q]].h);
+      atomicAdd(&acc_m[kid[q]], G[kid[q]].m);
+    }
+  if (tid == 0) {
+    atomicAdd(&acc_h[K], G[K].h);
+    atomicAdd(&acc_m[K], G[K].m);
+  }
   if ((tid & 31) == 0)
   {
     const uint32_t mcs[6] = {mc0, mc1, mc2, mc3, mc4, mc5};
@@ -619,15 +628,7 @@ __global__ void __launch_bounds__(256, (D <= 4 && RP == 1) ? 4 : 2) k_forward(TL
   __syncthreads();
   if (s_last) {
     __threadfence();
-    const Fx2* parts = reinterpret_cast<const Fx2*>(a.ws.partial);
-    for (int k = tid; k <= K; k += blockDim.x) {
-      Fx2 sum;
-      for (unsigned b = 0; b < gridDim.x; ++b) {
-        const Fx2* pb = parts + (size_t)b * (K + 1) + k;
-        sum.add(Fx2{__ldcg(&pb->h), __ldcg(&pb->m)});
-      }
-      a.ws.red[k] = sum.value();
-    }
+    for (int k = tid; k <= K; k += blockDim.x) a.ws.red[k] = __ldcg(acc_h + k) + __ldcg(acc_m + k);
     if (tid == 0) {
       a.cnt->ticket_fwd = 0;
       a.cnt->claim_fwd = 0;

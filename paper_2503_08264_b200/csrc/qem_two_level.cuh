@@ -76,6 +76,8 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a, int phase) {
   __shared__ float s_key[QEM_MAX_K];
   const int K = a.K, tid = threadIdx.x;
   const int R = D + (a.scale_kind != QEM_SCALE_FIXED);
+  if (phase == 0)  // the FFMA forward's plate-sum accumulators (Fx2 parts, added atomically by its CTAs)
+    for (int k = tid; k < 2 * (K + 1); k += blockDim.x) a.ws.partial[k] = 0.0;
   if (phase == 2) {  // k_ref from phase 1
     if (tid == 0) {
       const int kr = a.ws.ref->k_ref;
