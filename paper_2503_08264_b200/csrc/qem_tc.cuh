@@ -395,16 +395,22 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     gc1 = 0.5 / a.obs_var;
   }
   unsigned char* colop = reinterpret_cast<unsigned char*>(a.ws.colop);
-  const int64_t gstride = (int64_t)gridDim.x * PrepTc::WARPS;
+  // S = a.prep_split warps share a group (1, 2, 4 or 8, <= K/64; more when the rank's groups are too
+  // few to fill the SMs one warp each): warp slice sl takes the column iterations it = sl, sl + S, ...
+  // Every group-wide quantity is formed in an order that does not depend on S (the softmax over the
+  // t_ref the slices wrote, max reductions), so the results are bit-identical for every S.
+  const int S = a.prep_split, gslot = wid / S, sl = wid % S;
+  const int64_t gstride = (int64_t)gridDim.x * (PrepTc::WARPS / S);
+  const int64_t gfirst = (int64_t)blockIdx.x * (PrepTc::WARPS / S) + gslot;
+  __shared__ float s_w2[PrepTc::WARPS];
   // max_k |gamma_k| (the rows are the same for every group): the tile-mode bound below is >= max_k
   // |gamma_k| max |w|^2, so a group whose that alone passes the highest Taylor threshold is online
   // without the bound's K x D pass over the rows
   float gmax = 0.f;
   for (int k = lane; k < K; k += 32) gmax = fmaxf(gmax, fabsf(__ldg(a.ws.fwd_coef + (size_t)k * (D + 2) + 1)));
   gmax = warp_maxf(gmax);
-  if (!fuse && (int64_t)blockIdx.x * PrepTc::WARPS + wid < a.n_local)
-    stage_z((int64_t)blockIdx.x * PrepTc::WARPS + wid, 0, 0);
-  for (int64_t i = (int64_t)blockIdx.x * PrepTc::WARPS + wid; i < a.n_local; i += gstride) {
+  if (!fuse && gfirst < a.n_local) stage_z(gfirst, sl, 0);
+  for (int64_t i = gfirst; i < a.n_local; i += gstride) {
     __syncwarp();
     double sx = 0.0, sxx = 0.0;
     int yxi = 0;  // sum_j y_j x_j,lane (integer)
@@ -441,7 +447,6 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     const double Ci = bref_const + warp_sum(ci);
     __syncwarp();
     unsigned char* cop = colop + (size_t)i * K * kTcColBytes;
-    double tmax = -CUDART_INF, tsum = 0.0;  // the lane's online (max, sum of e^(t - max)) over its columns
     float w2max = 0.f;
     // the rest of a column once its likelihood is known: log q, the column operand, t_ref
     auto finish = [&](int kc, const float (&zr)[D], double ll) {
@@ -499,27 +504,21 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
       // t_ref(k') = B(k_ref,k') + A_i(k') (fp64; the backward rebuilds A from it)
       const double t = quad + ll;
       a.ws.tA[(size_t)i * K + kc] = t;
-      if (t > tmax) {
-        tsum = fma(tsum, (double)expf((float)(tmax - t)), 1.0);
-        tmax = t;
-      } else {
-        tsum += (double)expf((float)(t - tmax));
-      }
       w2max = fmaxf(w2max, W2);
     };
     // Two columns per lane at a time (kc and kc + K/2): the per-observation feature loads are
     // shared and the two likelihood chains hide each other's latency.
-    for (int it = 0; it < NIT; ++it) {
+    for (int it = sl, li = 0; it < NIT; it += S, ++li) {
       if (fuse) {
-        gen_z(i, it, it & 1);
-      } else if (it + 1 < NIT) {
-        stage_z(i, it + 1, (it + 1) & 1);
+        gen_z(i, it, li & 1);
+      } else if (it + S < NIT) {
+        stage_z(i, it + S, (li + 1) & 1);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncwarp();
-      const float* zst = zs + (it & 1) * (2 * kTcD * 32);
+      const float* zst = zs + (li & 1) * (2 * kTcD * 32);
       const int kcA = it * 32 + lane, kcB = kcA + K / 2;
       float zA[D], zB[D];
 #pragma unroll
@@ -572,11 +571,24 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
       finish(kcB, zB, llB);
       __syncwarp();  // the stage is refilled two iterations on
     }
-    if (!fuse && i + gstride < a.n_local) stage_z(i + gstride, 0, 0);  // next group's first stage, under the passes below
+    if (!fuse && i + gstride < a.n_local) stage_z(i + gstride, sl, 0);  // next group's first stage, under the passes below
+    // the group's slices meet: t_ref (global) and the slices' max |w|^2 (shared) visible to all of them
+    float W2max = warp_maxf(w2max);
+    if (S > 1) {
+      if (lane == 0) s_w2[wid] = W2max;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + gslot), "r"(32 * S) : "memory");
+      W2max = 0.f;
+      for (int q = 0; q < S; ++q) W2max = fmaxf(W2max, s_w2[gslot * S + q]);
+    }
+    // softmax over the group's columns from t_ref in a fixed order (lane l: columns l, l + 32, ...;
+    // then the warp tree), whatever S wrote them: M, then sum of e^(t - M)
+    const double* tref = a.ws.tA + (size_t)i * K;
+    double tmax = -CUDART_INF;
+    for (int kc = lane; kc < K; kc += 32) tmax = fmax(tmax, __ldcg(tref + kc));
     const double M = warp_max(tmax);
-    const float W2max = warp_maxf(w2max);
-    const double* tref = a.ws.tA + (size_t)i * K;  // written above by this lane (program order)
-    const double logS = log(warp_sum(tsum * (double)expf((float)(tmax - M))));
+    double tsum = 0.0;
+    for (int kc = lane; kc < K; kc += 32) tsum += (double)expf((float)(__ldcg(tref + kc) - M));
+    const double logS = log(warp_sum(tsum));
     // tile mode: bound on |D'_k(k')| = |c'_k . w + gamma_k |w|^2|, c' = c0 + 2 gamma m_i
     float u0[D];
 #pragma unroll
@@ -601,13 +613,13 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     tb = warp_maxf(tb);
     const int md = tb <= a.thr[0] ? 0 : (tb <= a.thr[1] ? 1 : (tb <= a.thr[2] ? 2 : (tb <= a.thr[3] ? 3 : (tb <= a.thr[4] ? 4 : 5))));
     float* aux = a.ws.colaux + (size_t)i * 2 * K;  // P (the forward's poly modes), first K slots
-    for (int kb = lane; kb < K; kb += 256) {  // 8 columns per lane per batch: their loads in flight together
+    for (int kb = lane + 32 * sl; kb < K; kb += 256 * S) {  // 8 columns per lane per batch: loads in flight together
       double tb4[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) tb4[u] = kb + 32 * u < K ? tref[kb + 32 * u] : 0.0;  // coherent: written above
+      for (int u = 0; u < 8; ++u) tb4[u] = kb + 32 * S * u < K ? __ldcg(tref + kb + 32 * S * u) : 0.0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int kc = kb + 32 * u;
+        const int kc = kb + 32 * S * u;
         if (kc >= K) break;
         const double lpd = tb4[u] - M - logS;
         // the forward's per-column weight: P (polynomial modes) or log2e ln P (online mode), which the
@@ -622,11 +634,12 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         *reinterpret_cast<uint4*>(cop + tc_col_offset(kc, 56)) = c1;  // chunk 7: 1 lP0 lP1 lP2 0...
       }
     }
-    if (lane == 0) {
+    if (lane == 0 && sl == 0) {
       a.ws.cvec[i] = M + logS - logK;
       a.ws.gstat[i] = W2max;
       a.ws.gmode[i] = md;
     }
+    if (S > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + gslot), "r"(32 * S) : "memory");  // s_w2 reuse
   }
 }
 

@@ -51,6 +51,7 @@ struct TLArgs {
   int t_host;
   int tc;        // tensor-core pair kernels in use (d = 16)
   int evidence_only;  // k_root: log Pe only (fresh-denominator pass)
+  int prep_split;     // k_colprep_tc: warps per group (1, 2, 4, 8)
   int fuse_sample;    // k_colprep_tc draws the level-1 samples itself (qem_sample_estep_forward, qem_iterate)
   int t_sample;       // its iteration (0: the device counter, graph mode)
   uint2 skey;         // its Philox key (the seed)
@@ -739,6 +740,12 @@ inline TLArgs make_args(qem_ctx* c) {
   a.tc = c->tc;
   a.evidence_only = c->evidence_only;
   a.fuse_sample = c->fuse_sample;
+  {  // column prep: enough warps per group that the rank's groups cover the colprep grid's warps ~4x
+    const int64_t warps = (int64_t)c->grid_prep * 8, nit = d.K / 64;
+    int sp = 1;
+    while (sp < 8 && 2 * sp <= nit && c->n_local * sp < 4 * warps) sp *= 2;
+    a.prep_split = sp;
+  }
   a.t_sample = c->fuse_iter;
   a.skey = make_uint2((uint32_t)c->fuse_seed, (uint32_t)(c->fuse_seed >> 32));
   a.g_begin = c->g_begin;
