@@ -212,7 +212,11 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
     const int ks = s_i[0];
     RefInfo* ref = a.ws.ref;
     ref->k_star = ks;
-    for (int r = 0; r < D; ++r) ref->mu_star[r] = a.z_root[r * K + ks];
+    float mu[D];  // loads before stores (they could alias)
+#pragma unroll
+    for (int r = 0; r < D; ++r) mu[r] = a.z_root[r * K + ks];
+#pragma unroll
+    for (int r = 0; r < D; ++r) ref->mu_star[r] = mu[r];
     const double lnv = root_lnv<D>(a, ks);
     ref->e_star = exp(-lnv);
     ref->bstar_const = -0.5 * D * (kLn2Pi + lnv);
@@ -220,13 +224,23 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
   __syncthreads();
   const int ks = s_i[0];
   const double es = exp(-root_lnv<D>(a, ks));
+  // the reference rows' coordinates in registers before the row loop (its stores could alias them)
+  float zs_[D], zref_[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    zs_[r] = a.z_root[r * K + ks];
+    zref_[r] = a.ws.ref->mu_ref[r];
+  }
   for (int k = tid; k < K; k += blockDim.x) {
     const double ek = exp(-root_lnv<D>(a, k));
+    float zk_[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) zk_[r] = a.z_root[r * K + k];
     if constexpr (TcGeo<D>::COMPACT) {
       if (a.tc) {  // Eb and Eg both in the compact c-region; the per-group slab's gamma stays 0
         uint4 c0, c1;
-        const double zr0 = a.ws.ref->mu_ref[0];
-        compact_row((float)((ek * ((double)a.z_root[k] - zr0) - es * ((double)a.z_root[ks] - zr0)) * kLog2eD),
+        const double zr0 = zref_[0];
+        compact_row((float)((ek * ((double)zk_[0] - zr0) - es * ((double)zs_[0] - zr0)) * kLog2eD),
                     (float)(-0.5 * (ek - es) * kLog2eD), c0, c1);
         unsigned char* rb = reinterpret_cast<unsigned char*>(a.ws.rowop_b);
         *reinterpret_cast<uint4*>(rb + TcGeo<D>::row_off(k, 0)) = c0;
@@ -239,8 +253,8 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
         float v[kTcD];
 #pragma unroll
         for (int r = 0; r < kTcD; ++r)
-          v[r] = r < D ? (float)((ek * ((double)a.z_root[r * K + k] - (double)a.ws.ref->mu_ref[r]) -
-                                  es * ((double)a.z_root[r * K + ks] - (double)a.ws.ref->mu_ref[r])) * kLog2eD)
+          v[r] = r < D ? (float)((ek * ((double)zk_[r] - (double)zref_[r]) - es * ((double)zs_[r] - (double)zref_[r])) *
+                                 kLog2eD)
                        : 0.f;
         store_row_split16(reinterpret_cast<unsigned char*>(a.ws.rowop_b), k, v);
         a.ws.bgam[k] = (float)(-0.5 * (ek - es) * kLog2eD);
@@ -248,7 +262,7 @@ __device__ void k_root_star(const TLArgs& a, const double* w) {
       }
     }
     float* bc = a.ws.bwd_coef + (size_t)k * (D + 1);
-    for (int r = 0; r < D; ++r) bc[r] = (float)(ek * (double)a.z_root[r * K + k] - es * (double)a.z_root[r * K + ks]);
+    for (int r = 0; r < D; ++r) bc[r] = (float)(ek * (double)zk_[r] - es * (double)zs_[r]);
     bc[D] = (float)(-0.5 * (ek - es));
   }
 }
@@ -1193,9 +1207,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
   tc_fence_before();
   __syncthreads();
   if (warp == kTcEpiWarps + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  double* part = a.ws.partial + (size_t)blockIdx.x * (K + 1);
-  for (int k = tid; k < K; k += blockDim.x) part[k] = s_g[k];
-  if (tid == kTcThreads) part[K] = csum;  // the first aux thread accumulated sum_i c_i
+  // the CTA's plate sums (fixed order within the CTA: its static group stride) go to the (K + 1) x
+  // {h, m} accumulators k_root_prep zeroed, split on fixed grids (Fx2, R39) so that the
+  // atomics' order cannot change a bit; no CTA walks the 148 CTAs' partials at the end
+  double* acc_h = a.ws.partial;
+  double* acc_m = a.ws.partial + (K + 1);
+  for (int k = tid; k < K; k += blockDim.x) {
+    Fx2 f;
+    f.add(s_g[k]);
+    atomicAdd(&acc_h[k], f.h);
+    atomicAdd(&acc_m[k], f.m);
+  }
+  if (tid == kTcThreads) {  // the first aux thread accumulated sum_i c_i
+    Fx2 f;
+    f.add(csum);
+    atomicAdd(&acc_h[K], f.h);
+    atomicAdd(&acc_m[K], f.m);
+  }
   __threadfence();
   __syncthreads();
   __shared__ uint32_t s_last;
@@ -1203,11 +1231,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
   __syncthreads();
   if (s_last) {
     __threadfence();
-    for (int k = tid; k <= K; k += blockDim.x) {
-      double sum = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(a.ws.partial + (size_t)b * (K + 1) + k);
-      a.ws.red[k] = sum;
-    }
+    for (int k = tid; k <= K; k += blockDim.x) a.ws.red[k] = __ldcg(acc_h + k) + __ldcg(acc_m + k);
     if (tid == 0) a.cnt->ticket_fwd = 0;
   }
 }

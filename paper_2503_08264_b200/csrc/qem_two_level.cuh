@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a, int phase) {
   __shared__ float s_key[QEM_MAX_K];
   const int K = a.K, tid = threadIdx.x;
   const int R = D + (a.scale_kind != QEM_SCALE_FIXED);
-  if (phase == 0)  // the FFMA forward's plate-sum accumulators (Fx2 parts, added atomically by its CTAs)
+  if (phase <= 1)  // the forward's plate-sum accumulators (Fx2 parts, added atomically by its CTAs)
     for (int k = tid; k < 2 * (K + 1); k += blockDim.x) a.ws.partial[k] = 0.0;
   if (phase == 2) {  // k_ref from phase 1
     if (tid == 0) {
@@ -137,7 +137,11 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a, int phase) {
     if (bi >= K) bi = 0;  // every distance NaN (degenerate Q, flagged by the M-step): stay in range
     RefInfo* ref = a.ws.ref;
     ref->k_ref = bi;
-    for (int r = 0; r < D; ++r) ref->mu_ref[r] = a.z_root[r * K + bi];
+    float mu[D];  // loads before stores (see phase 2)
+#pragma unroll
+    for (int r = 0; r < D; ++r) mu[r] = a.z_root[r * K + bi];
+#pragma unroll
+    for (int r = 0; r < D; ++r) ref->mu_ref[r] = mu[r];
     double lnv;
     if (a.scale_kind == QEM_SCALE_FIXED)
       lnv = log(a.fixed_var);
@@ -182,8 +186,17 @@ __global__ void __launch_bounds__(1024) k_root_prep(TLArgs a, int phase) {
     // u = z - mu_ref differenced rows D_k = alpha_k + gamma_k |u|^2 + c_k . u (both pair paths; the
     // tensor-core columns carry S = |w|^2 + 2 u0_i . w with u0_i = m_i - mu_ref, so the fp32 rounding
     // of c_k multiplies u, not z: it averages out over the groups instead of adding up coherently)
+    // every load before the first store (the stores could alias z_root: interleaved, each dimension
+    // would wait for a round trip -- ~12 us per launch at d = 16)
+    float zkr[D], zrr[D];
+#pragma unroll
     for (int r = 0; r < D; ++r) {
-      const double del = (double)a.z_root[r * K + k] - (double)a.z_root[r * K + kref];
+      zkr[r] = a.z_root[r * K + k];
+      zrr[r] = a.z_root[r * K + kref];
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      const double del = (double)zkr[r] - (double)zrr[r];
       dd += del * del;
       const double cr = ek * del;
       fc[2 + r] = (float)cr;
