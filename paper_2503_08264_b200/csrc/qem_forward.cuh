@@ -25,9 +25,18 @@
 #endif
 template <int D>
 struct FwdLayout {
-  static constexpr int CS = pad4(D + 3);  // u[D], U2, P, lnP (d = 1: u, lnP, U2, P)
-  // record slots: for d = 1 ln P sits next to u, so the online tile's two fields are one 8-byte load
-  static constexpr int IU2 = D == 1 ? 2 : D, IP = D == 1 ? 3 : D + 1, ILP = D == 1 ? 1 : D + 2;
+  static constexpr int CS = pad4(D + 3);  // floats per column: u[D], U2, P, lnP
+  // field ids after u[0 .. D-1], and each field's float offset in the group's block.  d = 1 lays
+  // columns out in pairs, [u0 lnP0 u1 lnP1 | U2_0 P0 U2_1 P1], so the online tile reads both fields
+  // of two columns with one 16-byte load.
+  static constexpr int FU2 = D, FP = D + 1, FLP = D + 2;
+  __host__ __device__ static int off(int kc, int f) {
+    if (D == 1) {
+      const int slot = f == 0 ? 0 : (f == FLP ? 1 : (f == FU2 ? 2 : 3));
+      return (kc >> 1) * 8 + (slot >> 1) * 4 + (kc & 1) * 2 + (slot & 1);
+    }
+    return kc * CS + f;
+  }
   static constexpr int CH = QEM_FWD_CH;   // column chunk of the online log-sum-exp (one max per chunk)
   __host__ __device__ static int kpad(int K) { return (K + CH - 1) / CH * CH; }
   // group trailer after the Kp column records: [0] max |w|^2, [2..3] c_i (fp64), [4..4+D) Q mean m_i
@@ -74,9 +83,18 @@ __device__ __forceinline__ float2 pair_D(float2 base, const float2 (&ga)[RP], co
   }
 }
 
+// column kc's fields (col = the group's block)
 template <int D>
-__device__ __forceinline__ void load_col(const float* cr, float (&u)[D], float& U2, float& P, float& lnP) {
+__device__ __forceinline__ void load_col(const float* col, int kc, float (&u)[D], float& U2, float& P, float& lnP) {
+  if constexpr (D == 1) {
+    u[0] = col[FwdLayout<1>::off(kc, 0)];
+    U2 = col[FwdLayout<1>::off(kc, FwdLayout<1>::FU2)];
+    P = col[FwdLayout<1>::off(kc, FwdLayout<1>::FP)];
+    lnP = col[FwdLayout<1>::off(kc, FwdLayout<1>::FLP)];
+    return;
+  }
   constexpr int CS = pad4(D + 3);
+  const float* cr = col + (size_t)kc * CS;
   float buf[CS];
 #pragma unroll
   for (int q = 0; q < CS / 4; ++q) {
@@ -88,9 +106,9 @@ __device__ __forceinline__ void load_col(const float* cr, float (&u)[D], float& 
   }
 #pragma unroll
   for (int r = 0; r < D; ++r) u[r] = buf[r];
-  U2 = buf[FwdLayout<D>::IU2];
-  P = buf[FwdLayout<D>::IP];
-  lnP = buf[FwdLayout<D>::ILP];
+  U2 = buf[FwdLayout<D>::FU2];
+  P = buf[FwdLayout<D>::FP];
+  lnP = buf[FwdLayout<D>::FLP];
 }
 
 __device__ __forceinline__ float2 max2(float2 a, float2 b) { return make_float2(fmaxf(a.x, b.x), fmaxf(a.y, b.y)); }
@@ -105,7 +123,7 @@ __device__ __forceinline__ void tile_poly(const float* col, int Kp, const float2
 #pragma unroll 2
   for (int kc = 0; kc < Kp; ++kc) {
     float u[D], U2, P, lnP;
-    load_col<D>(col + (size_t)kc * CS, u, U2, P, lnP);
+    load_col<D>(col, kc, u, U2, P, lnP);
 #pragma unroll
     for (int p = 0; p < RP; ++p) acc[p] = fma2(f2(P), expm1_poly<N>(pair_D<D, RP>(f2(0.f), ga, cc, p, u, U2)), acc[p]);
   }
@@ -158,7 +176,7 @@ __device__ __forceinline__ void tile_moments1(const float* col, int K, const flo
 #pragma unroll
   for (int p = 0; p < NM; ++p) m[p] = 0.0;
   for (int kc = tid; kc < K; kc += blockDim.x) {
-    const double w = col[(size_t)kc * CS], P = col[(size_t)kc * CS + FwdLayout<1>::IP];
+    const double w = col[FwdLayout<1>::off(kc, 0)], P = col[FwdLayout<1>::off(kc, FwdLayout<1>::FP)];
     double pw = P;
 #pragma unroll
     for (int p = 0; p < NM; ++p) {
@@ -232,16 +250,24 @@ __device__ __forceinline__ void tile_online(const float* col, int Kp, const floa
   }
   for (int kc0 = 0; kc0 < Kp; kc0 += CH) {
     float2 tv[CH][RP];
+    if constexpr (D == 1) {  // two columns' (w, ln P) per 16-byte load; ln P rides in the last FMA
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      float u[D], U2, P, lnP;
-      load_col<D>(col + (size_t)(kc0 + c) * CS, u, U2, P, lnP);
+      for (int c = 0; c < CH; c += 2) {
+        const float4 v = *reinterpret_cast<const float4*>(col + (size_t)((kc0 + c) >> 1) * 8);
+        const float u0[1] = {v.x}, u1[1] = {v.z};
 #pragma unroll
-      for (int p = 0; p < RP; ++p) {  // d = 1: ln P rides in the contraction's last FMA
-        if constexpr (D == 1)
-          tv[c][p] = pair_D<D, RP>(f2(lnP), ga, cc, p, u, U2);
-        else
-          tv[c][p] = add2(pair_D<D, RP>(f2(0.f), ga, cc, p, u, U2), f2(lnP));
+        for (int p = 0; p < RP; ++p) {
+          tv[c][p] = pair_D<D, RP>(f2(v.y), ga, cc, p, u0, 0.f);
+          tv[c + 1][p] = pair_D<D, RP>(f2(v.w), ga, cc, p, u1, 0.f);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        float u[D], U2, P, lnP;
+        load_col<D>(col, kc0 + c, u, U2, P, lnP);
+#pragma unroll
+        for (int p = 0; p < RP; ++p) tv[c][p] = add2(pair_D<D, RP>(f2(0.f), ga, cc, p, u, U2), f2(lnP));
       }
     }
 #pragma unroll
@@ -374,10 +400,13 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
         const double u = (double)zr[r] - (double)mu_ref[r];
         U2d += u * u;
       }
-      {
+      if constexpr (D == 1) {  // pair layout: (w, ln P) and (U2, P) are 8-byte halves (P, ln P below)
+        *reinterpret_cast<float2*>(rec0 + FwdLayout<1>::off(kc, 0)) = make_float2(rec[0], 0.f);
+        *reinterpret_cast<float2*>(rec0 + FwdLayout<1>::off(kc, FwdLayout<1>::FU2)) = make_float2(W2, 0.f);
+      } else {
 #pragma unroll
         for (int r = D; r < CS; ++r) rec[r] = 0.f;
-        rec[FwdLayout<D>::IU2] = W2;
+        rec[FwdLayout<D>::FU2] = W2;
         float4* dst = reinterpret_cast<float4*>(rec0 + (size_t)kc * CS);
 #pragma unroll
         for (int q = 0; q < CS / 4; ++q)
@@ -392,10 +421,9 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
     // padding columns: P = 0, ln P = -inf (contribute nothing)
     {
       for (int kc = K + lane; kc < Kp; kc += 32) {
-        float4* dst = reinterpret_cast<float4*>(rec0 + (size_t)kc * CS);
 #pragma unroll
-        for (int q = 0; q < CS / 4; ++q) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        rec0[(size_t)kc * CS + FwdLayout<D>::ILP] = -CUDART_INF_F;
+        for (int f = 0; f < D + 3; ++f) rec0[FwdLayout<D>::off(kc, f)] = 0.f;
+        rec0[FwdLayout<D>::off(kc, FwdLayout<D>::FLP)] = -CUDART_INF_F;
       }
     }
     const double M = warp_max(tmax);
@@ -406,9 +434,8 @@ __global__ void __launch_bounds__(256) k_colprep(TLArgs a) {
     for (int kc = lane; kc < K; kc += 32) {
       const float lp = (float)(tref[kc] - M - logS);
       {
-        float* pc = rec0 + (size_t)kc * CS;
-        pc[FwdLayout<D>::IP] = expf(lp);
-        pc[FwdLayout<D>::ILP] = lp;
+        rec0[FwdLayout<D>::off(kc, FwdLayout<D>::FP)] = expf(lp);
+        rec0[FwdLayout<D>::off(kc, FwdLayout<D>::FLP)] = lp;
       }
     }
     if (lane == 0) {

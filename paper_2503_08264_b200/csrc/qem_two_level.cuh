@@ -529,20 +529,12 @@ __global__ void __launch_bounds__(256) k_backward(TLArgs a) {
         // column record (w, |w|^2, P, ln P) written by the column prep (K2a)
         const int kc = tid + NT * (2 * p + h);
         const bool ok = kc < K;
-        float rec[CS];
-        const float4* src = reinterpret_cast<const float4*>(a.ws.colrec + (size_t)i * FwdLayout<D>::group_floats(K) +
-                                                            (size_t)(ok ? kc : 0) * CS);
+        const float* gcol = a.ws.colrec + (size_t)i * FwdLayout<D>::group_floats(K);
+        float urec[D], u2rec, prec, lrec;
+        load_col<D>(gcol, ok ? kc : 0, urec, u2rec, prec, lrec);
 #pragma unroll
-        for (int q = 0; q < CS / 4; ++q) {
-          const float4 v = src[q];
-          rec[4 * q] = v.x;
-          rec[4 * q + 1] = v.y;
-          rec[4 * q + 2] = v.z;
-          rec[4 * q + 3] = v.w;
-        }
-#pragma unroll
-        for (int r = 0; r < D; ++r) uu[h][r] = ok ? rec[r] : 0.f;
-        u2[h] = ok ? rec[FwdLayout<D>::IU2] : 0.f;
+        for (int r = 0; r < D; ++r) uu[h][r] = ok ? urec[r] : 0.f;
+        u2[h] = ok ? u2rec : 0.f;
         lc[h] = ok ? (float)((tl[p][h] - tlse) * kLog2eD) : -CUDART_INF_F;
       }
 #pragma unroll
@@ -659,7 +651,7 @@ __device__ __forceinline__ void bwd_mom_group(const TLArgs& a, int64_t i, float 
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   bool bad = false;
   for (int kc = lane; kc < K; kc += 32) {
-    const double w = rec[(size_t)kc * FwdLayout<1>::CS];
+    const double w = rec[FwdLayout<1>::off(kc, 0)];
     double sp = A[NC - 1];
 #pragma unroll
     for (int q = NC - 2; q >= 0; --q) sp = fma(sp, w, A[q]);
