@@ -332,9 +332,13 @@ __device__ __forceinline__ float softplus_pair(float2 eta, bool two) {
 #ifndef QEM_COLPREP_MINB
 #define QEM_COLPREP_MINB 2  // resident CTAs per SM the column prep is compiled for (register budget)
 #endif
+#ifndef QEM_PREP_ZST
+#define QEM_PREP_ZST 2  // z stages per warp (1: the loads of a bound z are not prefetched, less SMEM)
+#endif
 struct PrepTc {
   static constexpr int WARPS = 8;
-  static constexpr int ZS_FLOATS = 2 * 2 * kTcD * 32;  // z ring: [stage][half][r][32 columns]
+  static constexpr int ZST = QEM_PREP_ZST;
+  static constexpr int ZS_FLOATS = ZST * 2 * kTcD * 32;  // z ring: [stage][half][r][32 columns]
   static constexpr size_t ZS_BYTES = ZS_FLOATS * 4;
   __host__ __device__ static size_t warp_bytes(int K, int J) {
     size_t b = 3 * kTcD * 8 + 3 * kTcD * 4 + (size_t)((J + 1) / 2) * kTcD * 8 + ZS_BYTES;
@@ -423,7 +427,8 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
   float gmax = 0.f;
   for (int k = lane; k < K; k += 32) gmax = fmaxf(gmax, fabsf(__ldg(a.ws.fwd_coef + (size_t)k * (D + 2) + 1)));
   gmax = warp_maxf(gmax);
-  if (!fuse && gfirst < a.n_local) stage_z(gfirst, sl, 0);
+  constexpr int ZST = PrepTc::ZST;
+  if (ZST == 2 && !fuse && gfirst < a.n_local) stage_z(gfirst, sl, 0);
   for (int64_t i = gfirst; i < a.n_local; i += gstride) {
     __syncwarp();
     double sx = 0.0, sxx = 0.0;
@@ -524,7 +529,10 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
     // shared and the two likelihood chains hide each other's latency.
     for (int it = sl, li = 0; it < NIT; it += S, ++li) {
       if (fuse) {
-        gen_z(i, it, li & 1);
+        gen_z(i, it, (li & 1) & (ZST - 1));
+      } else if (ZST == 1) {
+        stage_z(i, it, 0);
+        cp_async_wait<0>();
       } else if (it + S < NIT) {
         stage_z(i, it + S, (li + 1) & 1);
         cp_async_wait<1>();
@@ -532,7 +540,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
         cp_async_wait<0>();
       }
       __syncwarp();
-      const float* zst = zs + (li & 1) * (2 * kTcD * 32);
+      const float* zst = zs + ((li & 1) & (ZST - 1)) * (2 * kTcD * 32);
       const int kcA = it * 32 + lane, kcB = kcA + K / 2;
       float zA[D], zB[D];
 #pragma unroll
@@ -585,7 +593,7 @@ __global__ void __launch_bounds__(256, QEM_COLPREP_MINB) k_colprep_tc(TLArgs a) 
       finish(kcB, zB, llB);
       __syncwarp();  // the stage is refilled two iterations on
     }
-    if (!fuse && i + gstride < a.n_local) stage_z(i + gstride, sl, 0);  // next group's first stage, under the passes below
+    if (ZST == 2 && !fuse && i + gstride < a.n_local) stage_z(i + gstride, sl, 0);  // next group's first stage, under the passes below
     // the group's slices meet: t_ref (global) and the slices' max |w|^2 (shared) visible to all of them
     float W2max = warp_maxf(w2max);
     if (S > 1) {
@@ -896,6 +904,48 @@ __device__ __forceinline__ void fwd_epi_online(uint32_t taddr, const float* lpp,
   s += t.x + t.y;
 }
 
+// Forward epilogue, online mode past a row's first column block: no max pass.  The exponentials are
+// taken against the running max m the earlier blocks left (2^(v - m) may exceed 1; fp32 holds it up
+// to 2^128, and a sum is as accurate at any scale), so the FMNMX3 chains and the max's dependency go.
+// Should a chunk overflow (v - m >= 128 somewhere, or s itself), the warp re-reads its TMEM columns
+// and takes the exact path (warp-uniform: tcgen05.ld is .sync.aligned).
+#ifndef QEM_FWD_LAZY
+#define QEM_FWD_LAZY 0
+#endif
+__device__ __forceinline__ void fwd_epi_online_nomax(uint32_t taddr, const float* lpp, float& m, float& s) {
+  uint32_t r[4][16];
+  tmem_ld64(taddr, r);
+#pragma unroll
+  for (int q = 0; q < 4 && kLpEpi; ++q)
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const float4 l = reinterpret_cast<const float4*>(lpp + q * 16)[c4];
+      r[q][4 * c4] = __float_as_uint(__uint_as_float(r[q][4 * c4]) + l.x);
+      r[q][4 * c4 + 1] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 1]) + l.y);
+      r[q][4 * c4 + 2] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 2]) + l.z);
+      r[q][4 * c4 + 3] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 3]) + l.w);
+    }
+  const float2 nm = f2(-m);
+  float2 acc[4] = {f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) {
+      const float2 e = add2(make_float2(__uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1])), nm);
+      // the software exponential's exponent add wraps past 2^128: clamp so an overflow stays >= 2^128
+      const float2 x = c >= 16 - kPolyExpFwd ? exp2_poly2(make_float2(fminf(e.x, 128.f), fminf(e.y, 128.f)))
+                                             : make_float2(ex2(e.x), ex2(e.y));
+      acc[q] = add2(acc[q], x);
+    }
+  const float2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+  const float sn = s + (t.x + t.y);
+  if (__any_sync(0xffffffffu, !(sn <= 1.0e30f))) {  // near overflow / NaN (the aux merge adds 4 slices): exact path
+    fwd_epi_online(taddr, lpp, m, s);
+    return;
+  }
+  s = sn;
+}
+
 // Forward epilogue, polynomial mode: acc += sum P (2^v - 1), v = log2e D' = c2.w + g2 S.
 template <int N, int NC16>
 __device__ __forceinline__ void fwd_epi_poly(uint32_t taddr, const float* pp, float& acc) {
@@ -1172,7 +1222,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
       const float* pp = s_p + (J & 1) * 256 + cq * 64;
       if (md != 5 || kLpEpi) mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));  // P / lP of this block in SMEM
       if (md == 5) {
-        fwd_epi_online(taddr, pp, st0, st1);
+        if (QEM_FWD_LAZY && cb > 0)
+          fwd_epi_online_nomax(taddr, pp, st0, st1);
+        else
+          fwd_epi_online(taddr, pp, st0, st1);
       } else {
         switch (md) {
           case 0: fwd_epi_poly<3, 4>(taddr, pp, st0); break;

@@ -90,6 +90,7 @@ def _check_messages(m, out, ref, z, q, note):
                               float(np.abs(out["dg"] - dref).max()), float(np.abs(dref).max()))
 
 
+@pytest.mark.timeout(900)
 def test_config5_full_size():
     """All 1e4 groups of config 5 (K = 1024, d = 16, the tcgen05 pair tiles) in the spread-root-weight
     regime: log Pe, every weight (1.0e7 group weights + the root's), every moment and every group's
@@ -106,6 +107,7 @@ def test_config5_full_size():
     _check_messages(m, out, ref, z, q, "config5 full")
 
 
+@pytest.mark.timeout(1200)  # config 5: three full fp64 oracle E-steps (~2 min each on the box's host)
 @pytest.mark.parametrize("cid", [4, 5])
 def test_teacher_forced_full_size_first_iterations(cid):
     """SURVEY.md §8(d) parity protocol for the large configs: the first 3 QEM iterations at full size
