@@ -313,7 +313,8 @@ def measure_step(m, args, world, rank, dev, in_library, seed):
             "kernels_ms": {"forward": fwd_ms, "backward": bwd_ms, "allreduce": comm_ms},
             "forward_mode_hist": dict(zip(["expm1_deg3", "deg4", "deg5", "deg7", "deg9", "online_lse"],
                                           [int(x) for x in hist[:6]])),
-            "backward_moment_groups": int(hist[6])}
+            "backward_moment_groups": int(hist[6]),
+            "forward_lazy_max_redos": int(hist[7])}
     out = dict(g=g, data=data, gb=gb, ge=ge, ms_step=ms_step, value=m.pairs / (ms_step * 1e-3),
                launched=launched[0], flags=flags, clamps=clamps, clocks=clk, roofline=roof, tc=tc, t=t,
                allreduce=runner.allreduce_plate_sum, nccl=g.nccl_info() if in_library else None)
@@ -876,13 +877,13 @@ def run_converged_variant(args, dev, steps=5):
         en.record()
         torch.cuda.synchronize()
         ms = st.elapsed_time(en) / steps
-        tot = max(1, sum(hist))
+        tot = max(1, sum(hist[:6]))  # forward modes only (slot 6: backward moment groups, 7: lazy-max redos)
         tc = g.pair_path() == 1
         base = 2.0 if tc else m.d + 2.0   # the log-factor (FFMA path) or the TMEM value (TC) per pair
         # clocks per pair per SM from the mode mix: poly mode n: (base + n + 2) FMA lane-ops / 128;
         # online mode: 1 exp / 16 (SFU) vs base + 2 FMA lane-ops
         cyc = 0.0
-        for md, c in enumerate(hist):
+        for md, c in enumerate(hist[:6]):
             frac = c / tot
             if md < 5:
                 cyc += frac * (base + degs[md] + 2.0) / FP32_PER_SM_CLK

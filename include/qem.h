@@ -570,8 +570,10 @@ qem_status qem_read_flags(qem_ctx* ctx, void* stream, uint32_t* flags, int64_t* 
 /* Synchronises `stream`, copies the forward tile-mode histogram (counts of
    (CTA-warp, group) tiles evaluated in mode 0..6: 0-4 expm1 polynomial of
    degree 3/4/5/7/9, 5 online log-sum-exp; slot 6: groups whose FFMA backward ran through the
-   d = 1 moment tiles (k_backward_mom1), 0 elsewhere) into h_hist[7] and clears it.  Two-level
-   only; diagnostics. */
+   d = 1 moment tiles (k_backward_mom1), 0 elsewhere; slot 7: tensor-core forward 64-column
+   chunks (per warp) whose max-free pass came near fp32 overflow and were redone with the exact
+   row max) into h_hist[8] and clears it.  Two-level only;
+   diagnostics. */
 qem_status qem_read_mode_hist(qem_ctx* ctx, void* stream, uint64_t* h_hist);
 
 /* Optional cudaEvent_t handles (as void*, NULL = off) that the library

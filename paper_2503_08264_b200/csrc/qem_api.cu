@@ -970,7 +970,7 @@ qem_status qem_read_mode_hist(qem_ctx* c, void* stream, uint64_t* h) {
   if (e == cudaSuccess) e = cudaMemcpy(tmp, c->cnt->mode_hist, sizeof tmp, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemset(c->cnt->mode_hist, 0, sizeof tmp);
   if (e != cudaSuccess) return cuda_fail(e, "qem_read_mode_hist");
-  for (int m = 0; m < 7; ++m) h[m] = tmp[m];
+  for (int m = 0; m < 8; ++m) h[m] = tmp[m];
   return QEM_OK;
 }
 

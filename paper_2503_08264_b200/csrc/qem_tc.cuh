@@ -861,89 +861,70 @@ __device__ __forceinline__ float2 expm1_2_poly(float2 x) {
 // Forward epilogue, online mode: (m, s) = running max / sum of 2^(v - m) over
 // v = c2.u + g2 U + lP (log2 domain; the row constant is added at the end).
 // The max is lazy: s is rescaled only when a chunk raises it.
-__device__ __forceinline__ void fwd_epi_online(uint32_t taddr, const float* lpp, float& m, float& s) {
-  uint32_t r[4][16];
-  tmem_ld64(taddr, r);  // the thread's 64 columns of this tile, one TMEM round trip
-  // + log2e ln P of the columns (SMEM broadcast: every lane of the warp reads the same columns), in
-  // fp32 round to nearest (QEM_LP_EPI; else the MMA added it)
-#pragma unroll
-  for (int q = 0; q < 4 && kLpEpi; ++q)
-#pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-      const float4 l = reinterpret_cast<const float4*>(lpp + q * 16)[c4];
-      r[q][4 * c4] = __float_as_uint(__uint_as_float(r[q][4 * c4]) + l.x);
-      r[q][4 * c4 + 1] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 1]) + l.y);
-      r[q][4 * c4 + 2] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 2]) + l.z);
-      r[q][4 * c4 + 3] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 3]) + l.w);
-    }
-  // four independent FMNMX3 chains (one per 16-column load), then combined: a dependency chain
-  // of 8 + 2 instead of 32
-  float mq[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    mq[q] = fmaxf(__uint_as_float(r[q][0]), __uint_as_float(r[q][1]));
-#pragma unroll
-    for (int c = 2; c < 16; c += 2) mq[q] = fmax3f(mq[q], __uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1]));
-  }
-  const float mx = fmax3f(m, fmax3f(mq[0], mq[1], mq[2]), mq[3]);
-  if (mx > m) {  // exact running max (see kLazy in qem_forward.cuh)
-    s *= ex2(m - mx);
-    m = mx;
-  }
-  const float2 nm = f2(-m);
-  float2 acc[4] = {f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int c = 0; c < 16; c += 2) {
-      const float2 e = add2(make_float2(__uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1])), nm);
-      const float2 x = c >= 16 - kPolyExpFwd ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y));
-      acc[q] = add2(acc[q], x);
-    }
-  const float2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
-  s += t.x + t.y;
-}
-
-// Forward epilogue, online mode past a row's first column block: no max pass.  The exponentials are
-// taken against the running max m the earlier blocks left (2^(v - m) may exceed 1; fp32 holds it up
-// to 2^128, and a sum is as accurate at any scale), so the FMNMX3 chains and the max's dependency go.
-// Should a chunk overflow (v - m >= 128 somewhere, or s itself), the warp re-reads its TMEM columns
-// and takes the exact path (warp-uniform: tcgen05.ld is .sync.aligned).
-#ifndef QEM_FWD_LAZY
-#define QEM_FWD_LAZY 0
+// QEM_FWD_LAZY: past a row's first column block (`nomax`) the max pass is skipped and the exponentials
+// are taken against the running max the earlier blocks left (2^(v - m) may exceed 1; a sum is as
+// accurate at any scale); should a chunk come near overflow (or NaN), the warp re-reads its TMEM
+// columns and takes the exact pass (warp-uniform: tcgen05.ld is .sync.aligned).
+#ifndef QEM_FWD_REDO_COUNT
+#define QEM_FWD_REDO_COUNT 0  // 1: count the epilogue warps that redid a chunk in mode-hist slot 7 (costs 1 %)
 #endif
-__device__ __forceinline__ void fwd_epi_online_nomax(uint32_t taddr, const float* lpp, float& m, float& s) {
-  uint32_t r[4][16];
-  tmem_ld64(taddr, r);
+#ifndef QEM_FWD_LAZY
+#define QEM_FWD_LAZY 1  // config 5 forward 2.66 -> 2.60 ms (interleaved A/B); fallbacks: 0.6 % of chunks at t = 1, 0 from t = 3
+#endif
+__device__ __forceinline__ void fwd_epi_online(uint32_t taddr, const float* lpp, float& m, float& s, bool nomax,
+                                               float redo_thr, bool& redo) {
+  for (;;) {
+    uint32_t r[4][16];
+    tmem_ld64(taddr, r);  // the thread's 64 columns of this tile, one TMEM round trip
+    // + log2e ln P of the columns (SMEM broadcast: every lane of the warp reads the same columns), in
+    // fp32 round to nearest (QEM_LP_EPI; else the MMA added it)
 #pragma unroll
-  for (int q = 0; q < 4 && kLpEpi; ++q)
+    for (int q = 0; q < 4 && kLpEpi; ++q)
 #pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-      const float4 l = reinterpret_cast<const float4*>(lpp + q * 16)[c4];
-      r[q][4 * c4] = __float_as_uint(__uint_as_float(r[q][4 * c4]) + l.x);
-      r[q][4 * c4 + 1] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 1]) + l.y);
-      r[q][4 * c4 + 2] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 2]) + l.z);
-      r[q][4 * c4 + 3] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 3]) + l.w);
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const float4 l = reinterpret_cast<const float4*>(lpp + q * 16)[c4];
+        r[q][4 * c4] = __float_as_uint(__uint_as_float(r[q][4 * c4]) + l.x);
+        r[q][4 * c4 + 1] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 1]) + l.y);
+        r[q][4 * c4 + 2] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 2]) + l.z);
+        r[q][4 * c4 + 3] = __float_as_uint(__uint_as_float(r[q][4 * c4 + 3]) + l.w);
+      }
+    if (!QEM_FWD_LAZY || !nomax) {
+      // four independent FMNMX3 chains (one per 16-column load), then combined: a dependency chain
+      // of 8 + 2 instead of 32
+      float mq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        mq[q] = fmaxf(__uint_as_float(r[q][0]), __uint_as_float(r[q][1]));
+#pragma unroll
+        for (int c = 2; c < 16; c += 2) mq[q] = fmax3f(mq[q], __uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1]));
+      }
+      const float mx = fmax3f(m, fmax3f(mq[0], mq[1], mq[2]), mq[3]);
+      if (mx > m) {  // exact running max (see kLazy in qem_forward.cuh)
+        s *= ex2(m - mx);
+        m = mx;
+      }
     }
-  const float2 nm = f2(-m);
-  float2 acc[4] = {f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
+    const float2 nm = f2(-m);
+    float2 acc[4] = {f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int c = 0; c < 16; c += 2) {
-      const float2 e = add2(make_float2(__uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1])), nm);
-      // the software exponential's exponent add wraps past 2^128: clamp so an overflow stays >= 2^128
-      const float2 x = c >= 16 - kPolyExpFwd ? exp2_poly2(make_float2(fminf(e.x, 128.f), fminf(e.y, 128.f)))
-                                             : make_float2(ex2(e.x), ex2(e.y));
-      acc[q] = add2(acc[q], x);
+      for (int c = 0; c < 16; c += 2) {
+        float2 e = add2(make_float2(__uint_as_float(r[q][c]), __uint_as_float(r[q][c + 1])), nm);
+        if (QEM_FWD_LAZY && c >= 16 - kPolyExpFwd)  // the software exponent add would wrap past 2^128
+          e = make_float2(fminf(e.x, 128.f), fminf(e.y, 128.f));
+        const float2 x = c >= 16 - kPolyExpFwd ? exp2_poly2(e) : make_float2(ex2(e.x), ex2(e.y));
+        acc[q] = add2(acc[q], x);
+      }
+    const float2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+    const float sn = s + (t.x + t.y);
+    if (!QEM_FWD_LAZY || !nomax || !__any_sync(0xffffffffu, !(sn <= redo_thr))) {
+      s = sn;
+      return;
     }
-  const float2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
-  const float sn = s + (t.x + t.y);
-  if (__any_sync(0xffffffffu, !(sn <= 1.0e30f))) {  // near overflow / NaN (the aux merge adds 4 slices): exact path
-    fwd_epi_online(taddr, lpp, m, s);
-    return;
+    nomax = false;  // near overflow / NaN (the aux merge adds 4 slices' sums): the exact pass
+    redo = true;  // QEM_FWD_REDO_COUNT builds count it per epilogue warp at the end of the kernel
   }
-  s = sn;
 }
 
 // Forward epilogue, polynomial mode: acc += sum P (2^v - 1), v = log2e D' = c2.w + g2 S.
@@ -968,6 +949,17 @@ __device__ __forceinline__ void fwd_epi_poly(uint32_t taddr, const float* pp, fl
   });
   const float2 t = add2(a2[0], a2[1]);
   acc += t.x + t.y;
+}
+
+// The polynomial modes' epilogues (out of line was measured 3 % slower on the online mode too)
+__device__ __forceinline__ void fwd_epi_poly_any(int md, uint32_t taddr, const float* pp, float& acc) {
+  switch (md) {
+    case 0: fwd_epi_poly<3, 4>(taddr, pp, acc); break;
+    case 1: fwd_epi_poly<4, 4>(taddr, pp, acc); break;
+    case 2: fwd_epi_poly<5, 4>(taddr, pp, acc); break;
+    case 3: fwd_epi_poly<7, 4>(taddr, pp, acc); break;
+    default: fwd_epi_poly<9, 4>(taddr, pp, acc); break;
+  }
 }
 
 // Tile walk of a persistent CTA (no integer division in the loop): group j (instance i =
@@ -1202,6 +1194,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3, cq = warp >> 2;
     int md = 5;
+    bool redo = false;  // some chunk of this warp took the exact redo (R41)
     int64_t u = 0;  // finalised row blocks so far
     for (TileWalk tw(RB, NB); tw.T < ntiles; tw.next()) {
       const int64_t T = tw.T, J = tw.J;
@@ -1222,18 +1215,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
       const float* pp = s_p + (J & 1) * 256 + cq * 64;
       if (md != 5 || kLpEpi) mbar_wait(&b_full[J & 1], (uint32_t)((J >> 1) & 1));  // P / lP of this block in SMEM
       if (md == 5) {
-        if (QEM_FWD_LAZY && cb > 0)
-          fwd_epi_online_nomax(taddr, pp, st0, st1);
-        else
-          fwd_epi_online(taddr, pp, st0, st1);
+        fwd_epi_online(taddr, pp, st0, st1, cb > 0, a.redo_thr, redo);
       } else {
-        switch (md) {
-          case 0: fwd_epi_poly<3, 4>(taddr, pp, st0); break;
-          case 1: fwd_epi_poly<4, 4>(taddr, pp, st0); break;
-          case 2: fwd_epi_poly<5, 4>(taddr, pp, st0); break;
-          case 3: fwd_epi_poly<7, 4>(taddr, pp, st0); break;
-          default: fwd_epi_poly<9, 4>(taddr, pp, st0); break;
-        }
+        fwd_epi_poly_any(md, taddr, pp, st0);
       }
       tc_fence_before();
       __syncwarp();
@@ -1254,6 +1238,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_forward_tc(TLArgs a) {
         ++u;
       }
     }
+    if (QEM_FWD_REDO_COUNT && redo && lane == 0) atomicAdd(&a.cnt->mode_hist[7], 1ull);
   }
 
   // ---- teardown, per-CTA partial plate sums, last-CTA fixed-order reduce

@@ -57,6 +57,7 @@ struct TLArgs {
   uint2 skey;         // its Philox key (the seed)
   int64_t g_begin;    // global index of local group 0 (the Philox counters)
   float thr[5];  // forward tile-mode bounds for expm1 degrees 3/4/5/7/9
+  float redo_thr;  // tensor-core forward: a max-free chunk whose running sum passes this is redone exactly (R41)
   TwoLevelWs ws;
   Counters* cnt;
 };
@@ -760,6 +761,10 @@ inline TLArgs make_args(qem_ctx* c) {
   }
   // |D'| bound below which the degree-n Taylor remainder |D'|^{n+1}/(n+1)!,
   // accumulated over all N groups of the plate, stays under 2e-6
+  {  // R41: 1e30 keeps the aux merge of 4 slices' sums finite; QEM_FWD_REDO_THR (tests) forces redos
+    static const float thr = getenv("QEM_FWD_REDO_THR") ? (float)atof(getenv("QEM_FWD_REDO_THR")) : 1.0e30f;
+    a.redo_thr = thr;
+  }
   const int degs[5] = {3, 4, 5, 7, 9};
   for (int q = 0; q < 5; ++q) {
     double f = 1.0;

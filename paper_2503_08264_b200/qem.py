@@ -346,7 +346,7 @@ class QEM:
 
     def mode_hist(self, stream=None):
         """Forward tile-mode histogram since the last call (diagnostics)."""
-        h = (ctypes.c_uint64 * 7)()
+        h = (ctypes.c_uint64 * 8)()
         check(lib().qem_read_mode_hist(self.ctx, _stream(stream), h), "qem_read_mode_hist")
         return [int(v) for v in h]
 

@@ -38,7 +38,7 @@ CASES = {
     "n60_K256_post0.0004": (60, 256, 0.0004),
 }
 
-_seen_modes = {4: np.zeros(7, np.int64), 5: np.zeros(7, np.int64)}
+_seen_modes = {4: np.zeros(8, np.int64), 5: np.zeros(8, np.int64)}
 
 
 @pytest.mark.parametrize("case", list(CASES))
@@ -64,7 +64,7 @@ def test_tc_estep_parity(cid, case):
     flags, _ = g.read_flags()
     g.close()
     _seen_modes[cid][:] += hist
-    assert hist.sum() == n, hist  # one mode per group
+    assert hist[:6].sum() == n, hist  # one mode per group
     check_estep(m, out, ref, note=f"tc/{case}")
     assert flags & 2 == 0
     if shrink is None or shrink > 3:
@@ -84,7 +84,7 @@ def test_tc_estep_parity(cid, case):
 def test_tc_modes_covered(cid):
     """The sweep above must have exercised the online mode and the polynomial modes."""
     seen = _seen_modes[cid]
-    if seen.sum() == 0:
+    if seen[:6].sum() == 0:
         pytest.skip("run with the parity sweep")
     assert seen[5] > 0, seen
     assert (seen[:5] > 0).sum() >= 1, seen
@@ -110,7 +110,7 @@ def test_compact_tc_path_d1_opt_in():
         "from paper_2503_08264_b200 import synth\n"
         "from paper_2503_08264_b200.qem import QEM\n"
         "from test_gpu_parity import check_estep\n"
-        "seen = np.zeros(7, np.int64)\n"
+        "seen = np.zeros(8, np.int64)\n"
         "for name, (n, K, shrink) in %r.items():\n"
         "    m = synth.config(4, n=n, K=K); data = synth.make_data(m)\n"
         "    q = synth.random_q(m, 11) if shrink is None else posterior_like_q(m, data, seed=7, shrink=shrink)\n"
@@ -119,7 +119,7 @@ def test_compact_tc_path_d1_opt_in():
         "    g.set_data(data); g.set_q(q); g.sample_q(eps=eps); g.estep(); out = g.result()\n"
         "    seen += np.asarray(g.mode_hist()); g.close()\n"
         "    check_estep(m, out, orc.estep(m, z, q, data), note='compact ' + name)\n"
-        "assert seen[5:].sum() > 0 and seen[:5].sum() > 0, seen\n"
+        "assert seen[5:7].sum() > 0 and seen[:5].sum() > 0, seen\n"
         "print('COMPACT_OK', seen)\n" % (os.path.dirname(here), here, cases))
     env = dict(os.environ, QEM_TC1="1")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
@@ -165,3 +165,45 @@ def test_fused_sampler_is_bit_identical(n, K):
             for l in range(2):
                 np.testing.assert_array_equal(a["w"][l], f["w"][l])
                 np.testing.assert_array_equal(a["m1"][l], f["m1"][l])
+
+
+def _lazy_cases(m):
+    return (("initial", synth.initial_q(m)), ("random11", synth.random_q(m, 11)), ("random3", synth.random_q(m, 3)))
+
+
+@pytest.mark.parametrize("forced", [False, True], ids=["default", "all_redone"])
+def test_tc_lazy_max_redo_parity(forced):
+    """The forward's max-free pass past a row's first column block (R41)
+    redoes a 64-column chunk with the exact row max when its running sum passes 1e30.  In the one-hot
+    regime (Q = N(0,1) and random Q, K = 1024: four column blocks) both the max-free chunks and
+    (QEM_FWD_REDO_THR=0, read once per process: every max-free chunk redone) the redo path must meet
+    the north-star tolerances.  (How often the default threshold redoes: tools/lazy_count.py with a
+    QEM_FWD_REDO_COUNT=1 build -- 0.6 % of chunks at t = 1 of config 5, none from t = 3.)"""
+    import os
+    import subprocess
+    import sys
+    if not forced:
+        from paper_2503_08264_b200.qem import QEM
+        m = synth.config(5, n=200, K=1024)
+        data = synth.make_data(m)
+        for name, q in _lazy_cases(m):
+            _, _, eps, _ = make_case(m, q=q)
+            z = [orc.sample(qm, qv, e) for (qm, qv), e in zip(q, eps)]
+            g = QEM(m)
+            g.set_data(data)
+            g.set_q(q)
+            g.sample_q(eps=eps)
+            g.estep()
+            out = g.result()
+            g.close()
+            check_estep(m, out, orc.estep(m, z, q, data), note=f"lazy/{name}")
+        return
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import test_gpu_tc as T\n"
+        "T.test_tc_lazy_max_redo_parity(False)\n"
+        "print('REDO_OK')\n" % (os.path.dirname(here), here))
+    env = dict(os.environ, QEM_FWD_REDO_THR="0")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
+    assert "REDO_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
