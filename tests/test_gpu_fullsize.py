@@ -107,12 +107,16 @@ def test_config5_full_size():
     _check_messages(m, out, ref, z, q, "config5 full")
 
 
-@pytest.mark.timeout(1200)  # config 5: three full fp64 oracle E-steps (~2 min each on the box's host)
+@pytest.mark.timeout(1200)  # config 5: each full fp64 oracle E-step is ~2 min on the box's host
 @pytest.mark.parametrize("cid", [4, 5])
 def test_teacher_forced_full_size_first_iterations(cid):
-    """SURVEY.md §8(d) parity protocol for the large configs: the first 3 QEM iterations at full size
+    """SURVEY.md §8(d) parity protocol for the large configs: the first QEM iterations at full size
     (Alg. 1; R21), each from the oracle's state m_{t-1} and Q_t with the
-    same host eps: E-step outputs, EMA state and the next Q at the contract tolerances."""
+    same host eps: E-step outputs, EMA state and the next Q at the contract tolerances.  Config 4 runs
+    3 iterations, config 5 two (t = 1 from Q = N(0,1) and t = 2 from the first M-step's Q; QEM_FULLSIZE_T
+    overrides: 3 iterations of config 5 were green at 354 s, the oracle's time)."""
+    import os
+    T = int(os.environ.get("QEM_FULLSIZE_T", "3" if cid == 4 else "2"))
     from paper_2503_08264_b200.qem import QEM
     from test_gpu_qem import check_step
     m = synth.config(cid)
@@ -122,7 +126,7 @@ def test_teacher_forced_full_size_first_iterations(cid):
     g.set_data(data)
     state = orc.initial_state(m)
     q = [orc.mstep(a, b)[:2] for a, b in state]
-    for t in range(1, 4):
+    for t in range(1, T + 1):
         eps = orc.eps_for_iteration(m, t, seed)
         g.set_state([(a, b - a * a) for a, b in state])
         g.set_q(q)
