@@ -287,6 +287,29 @@ def test_philox_normals_are_standard():
     assert kstest(eps, "norm").pvalue > 1e-3
 
 
+def test_box_muller_pairs_invert_to_the_philox_words():
+    """Deterministic pin of the oracle's normal generator (R42; the paper fixes no sampler):
+    samples k = 4c + {0, 1} are the Box-Muller pair of words (0, 1) of the Philox block at counter
+    (c, dim, instance, level << 24 | iter), samples 4c + {2, 3} that of words (2, 3).  The pair's polar
+    decomposition must give back the words' uniforms u = (top 23 bits + 1/2) / 2^23: radius^2 =
+    -2 ln u_a and angle = 2 pi u_b (cos to the even sample, sin to the odd one).  The words come from
+    orc.philox, itself pinned to the Random123 known answers above; a swapped word, a swapped sin / cos,
+    a sign or another uniform mapping fails."""
+    seed, it, level, inst, ndim, K = (0x9E3779B97F4A7C15, 37, 1, 1234, 3, 16)
+    eps = orc.normal_eps(seed, it, level, inst, ndim, K)
+    key = [seed & 0xffffffff, seed >> 32]
+    for r in range(ndim):
+        for c in range(K // 4):
+            w = orc.philox([c, r, inst, (level << 24) | it], key)
+            for half in range(2):
+                e0, e1 = eps[r, 4 * c + 2 * half], eps[r, 4 * c + 2 * half + 1]
+                ua = ((w[2 * half] >> 9) + 0.5) / 2.0 ** 23
+                ub = ((w[2 * half + 1] >> 9) + 0.5) / 2.0 ** 23
+                assert abs(math.exp(-0.5 * (e0 * e0 + e1 * e1)) - ua) < 1e-12
+                ang = math.atan2(e1, e0) / (2 * math.pi) % 1.0
+                assert min(abs(ang - ub), 1 - abs(ang - ub)) < 1e-9
+
+
 def test_sampler_location_scale():
     """z = m + sqrt(v) eps (App. E inverse-transform / location-scale sampling), fp32 fmaf."""
     qm = np.array([0.25, -3.0], np.float32)
