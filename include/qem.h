@@ -202,7 +202,11 @@ qem_status qem_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begi
    model (global indices key the Philox counters, so samples do not depend on
    the world size).  world > 1 is supported for the two-level family only.
    Device workspace is allocated here (O(n_local*K) floats) and freed by
-   qem_destroy.  opts may be NULL (w=0.3, no schedule, floor 1e-8). */
+   qem_destroy.  opts may be NULL (w=0.3, no schedule, floor 1e-8).
+   Errors: QEM_INVALID_MODEL as qem_model_validate; QEM_INVALID_ARGUMENT for an
+   empty, reversed or out-of-range block (a rank of a world larger than n owns no
+   groups and creates no context) or bad opts; QEM_UNSUPPORTED for a proper
+   sub-block of a three-level model; QEM_CUDA_ERROR if the allocation fails. */
 qem_status qem_create(const qem_model_desc* desc, const qem_opts* opts, int64_t group_begin,
                       int64_t group_end, qem_ctx** out);
 /* Caller-owned workspace variant (serving deployments that pool device memory):

@@ -73,6 +73,25 @@ def test_validate_and_shard_range(lib):
         qem.shard_range(10, 3, 2)
 
 
+def test_empty_and_out_of_range_group_blocks_are_rejected(lib):
+    """Error behaviour of the boundary on degenerate shards (include/qem.h, qem_create): a context owns a
+    non-empty block [group_begin, group_end) inside [0, n); an empty, reversed or out-of-range block --
+    e.g. a rank of a world larger than n, whose qem_shard_range block is empty -- is
+    QEM_INVALID_ARGUMENT before any device call (checked here on the CPU through qem_workspace_bytes,
+    the host-only arithmetic of qem_create)."""
+    from paper_2503_08264_b200 import _lib, qem, synth
+    m = synth.config(1)  # n = 4 groups
+    for gb, ge in ((0, 0), (2, 2), (3, 1), (-1, 2), (0, m.n + 1), (m.n, m.n)):
+        with pytest.raises(_lib.QemError, match="QEM_INVALID_ARGUMENT"):
+            qem.workspace_bytes(m, gb, ge)
+    # world = 8 > n = 4: the blocks still tile [0, n) and half of them are empty (those ranks make no context)
+    blocks = [qem.shard_range(m.n, r, 8) for r in range(8)]
+    assert sum(e - b for b, e in blocks) == m.n and sum(1 for b, e in blocks if e == b) == 4
+    m3 = synth.config(3)  # three-level: replicas only, a proper sub-block is QEM_UNSUPPORTED
+    with pytest.raises(_lib.QemError, match="QEM_UNSUPPORTED"):
+        qem.workspace_bytes(m3, 0, 3)
+
+
 def test_product_fails_loudly_without_extension(tmp_path):
     """With libqem.so absent, the binding raises instead of falling back."""
     code = (
