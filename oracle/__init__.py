@@ -18,4 +18,5 @@ Modules:
   predict.py     backward index resampling + predictive log-likelihood (numpy).
   gamma.py       Gamma- and Beta-Q E-steps (Gamma-Poisson, Beta-Binomial; numpy/scipy).
   crossed.py     crossed effects (Bus-shaped company / journey-type tables; numpy/scipy).
+  qmp.py         non-factorised Q_MP with the permutation / mixture parent-copy schemes (numpy/scipy).
 """
