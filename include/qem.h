@@ -33,6 +33,7 @@
  *    qem_loglik_bernoulli_states, qem_sample_normal), Gamma / Beta Q (qem_sample_gamma,
  *    qem_tables_gamma_poisson, qem_moments_gamma, qem_sample_beta, qem_tables_beta_binomial,
  *    qem_moments_beta), crossed effects (qem_tables_crossed, qem_moments_gaussian), the
+ *    non-factorised Q_MP with parent-copy schemes (qem_cols_qmp_gaussian, qem_moments_qmp), the
  *    predictive log-likelihood (qem_backward_resample, qem_predictive_loglik,
  *    qem_logmeanexp) and the global-IW baseline (qem_global_iw).
  *
@@ -538,6 +539,35 @@ qem_status qem_cols_beta_binomial(int64_t n, int32_t K, double kappa, const floa
                                   const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
                                   const int32_t* d_N, const double* d_q, const double* d_z, double* d_f_root,
                                   double* d_rows, double* d_cols, void* stream);
+
+/* ---- Non-factorised Q_MP with parent-copy schemes (App. A; NEXT row f4; R43) ----
+   Conjugate two-level Gaussian hierarchy mu ~ N(0, prior_var), z_i | mu ~ N(mu, group_var),
+   x_ij | z_i ~ N(z_i, obs_var) with a proposal whose child depends on its parent:
+   Q(mu) = N(d_root_mean[0], d_root_var[0]), Q(z_i | mu) = N(alpha_i + beta_i mu, s_i),
+   d_q [n][3] = (alpha_i, beta_i, s_i > 0) fp64.  qem_cols_qmp_gaussian draws the child copies
+     d_z[i][k'] = alpha_i + beta_i mu^c + sqrt(s_i) d_eps[i][k'],  c = d_copy[i][k'] in [0, K)
+   (mu^k = d_root_z[k] fp32; d_eps [n][K] fp32 standard normals, e.g. qem_sample_normal with mean 0,
+   variance 1; d_copy [n][K] int32, drawn by the caller: a uniformly random permutation per group
+   for QEM_QMP_PERMUTATION -- the scheme the paper used, PAPER.md:479 --, iid uniform indices for
+   QEM_QMP_MIXTURE) and writes the separable factors of
+     f_i(k, k') = log N(z_i^k'; mu^k, group_var) + sum_j log N(x_ij; z_i^k', obs_var) - log q_MP,i(k'),
+     q_MP,i(k') = N(z_i^k'; alpha_i + beta_i mu^c, s_i)                    (permutation)
+                = (1/K) sum_k N(z_i^k'; alpha_i + beta_i mu^k, s_i)        (mixture)
+   as d_rows [K][2] = (a_k, b_k), d_cols [n][K][2] = (z_i^k', psi_i(k')) for qem_estep_separable
+   (R = 1), plus d_f_root [K] = log N(mu^k; 0, prior_var) - log q(mu^k); d_x [n][J] fp32.  fp64.
+   qem_moments_qmp: d_gm [n][2] = (E z_i, E z_i^2) under d_w [n][K], d_root_m [2] = (E mu, E mu^2)
+   under d_w_root [K].  beta_i = 0 is the factorised Q of the hot path.  Device arrays,
+   caller-owned, asynchronous on `stream`; QEM_INVALID_ARGUMENT on bad sizes, a bad scheme, a
+   non-positive variance or a null array (indices in d_copy are not range-checked). */
+#define QEM_QMP_PERMUTATION 0
+#define QEM_QMP_MIXTURE 1
+qem_status qem_cols_qmp_gaussian(int64_t n, int32_t K, int32_t J, int32_t scheme, double prior_var, double group_var,
+                                 double obs_var, const float* d_root_z, const float* d_root_mean,
+                                 const float* d_root_var, const double* d_q, const int32_t* d_copy, const float* d_eps,
+                                 const float* d_x, double* d_z, double* d_f_root, double* d_rows, double* d_cols,
+                                 void* stream);
+qem_status qem_moments_qmp(int64_t n, int32_t K, const double* d_w_root, const float* d_root_z, const double* d_w,
+                           const double* d_z, double* d_root_m, double* d_gm, void* stream);
 
 /* EMA over mean parameters + M-step for non-Gaussian Q families (Alg. 1 lines 3, 6; Eq. 9;
    PAPER.md:218 "a Beta's parameters are recovered from expectations of log transformations",

@@ -22,6 +22,7 @@ EXPORTS = [
     "qem_estep", "qem_estep_forward", "qem_reduce_buffer", "qem_estep_reduce", "qem_estep_backward", "qem_estep_evidence",
     "qem_nccl_unique_id", "qem_nccl_init", "qem_set_nccl_comm", "qem_nccl_info",
     "qem_estep_separable", "qem_cols_gamma_poisson", "qem_cols_beta_binomial", "qem_mstep_gaussian",
+    "qem_cols_qmp_gaussian", "qem_moments_qmp",
     "qem_history_weight", "qem_estep_crossed", "qem_sample_estep_forward",
     "qem_evidence_root", "qem_mstep", "qem_mstep_family", "qem_estep_tables", "qem_sample_normal",
     "qem_sample_categorical", "qem_tables_categorical", "qem_estep_categorical", "qem_moments_categorical", "qem_mstep_categorical",
@@ -90,6 +91,8 @@ def lib() -> ctypes.CDLL:
         L.qem_history_weight.restype = ctypes.c_double
         L.qem_cols_gamma_poisson.argtypes = [i64, i32, i32, ctypes.c_double] + [vp] * 10
         L.qem_cols_beta_binomial.argtypes = [i64, i32, ctypes.c_double] + [vp] * 11
+        L.qem_cols_qmp_gaussian.argtypes = [i64, i32, i32, i32] + [ctypes.c_double] * 3 + [vp] * 12
+        L.qem_moments_qmp.argtypes = [i64, i32] + [vp] * 7
         L.qem_sample_normal.argtypes = [i64, i32, i32, u64, i32, vp, vp, vp, vp, vp]
         L.qem_sample_categorical.argtypes = [i64, i32, i32, u64, i32, vp, vp, vp]
         L.qem_tables_categorical.argtypes = [i64, i32, i32, i32] + [vp] * 10
@@ -154,7 +157,7 @@ def lib() -> ctypes.CDLL:
                      "qem_tables_beta_binomial", "qem_moments_beta", "qem_tables_crossed",
                      "qem_moments_gaussian", "qem_estep_separable", "qem_cols_gamma_poisson",
                      "qem_cols_beta_binomial", "qem_mstep_gaussian", "qem_estep_crossed",
-                     "qem_sample_estep_forward"]:
+                     "qem_sample_estep_forward", "qem_cols_qmp_gaussian", "qem_moments_qmp"]:
             getattr(L, name).restype = i32
         _lib = L
     return _lib

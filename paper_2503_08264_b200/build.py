@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 D_MENU = [1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 14, 16, 18, 20, 24, 32]  # qem_two_level.cu's QEM_D_LIST
-SOURCES = ["qem_api.cu", "qem_common.cu", "qem_two_level.cu"] + [f"qem_tl_d{d}.cu" for d in D_MENU] + [ "qem_three_level.cu", "qem_expfam.cu", "qem_tables.cu", "qem_discrete.cu", "qem_predict.cu", "qem_gamma.cu", "qem_crossed.cu", "qem_nccl.cu", "qem_separable.cu"]
+SOURCES = ["qem_api.cu", "qem_common.cu", "qem_two_level.cu"] + [f"qem_tl_d{d}.cu" for d in D_MENU] + [ "qem_three_level.cu", "qem_expfam.cu", "qem_tables.cu", "qem_discrete.cu", "qem_predict.cu", "qem_gamma.cu", "qem_crossed.cu", "qem_nccl.cu", "qem_separable.cu", "qem_qmp.cu"]
 HEADERS = ["qem_internal.h", "qem_device.cuh", "qem_forward.cuh", "qem_tc.cuh", "qem_two_level.cuh", os.path.join("..", "..", "include", "qem.h")]
 LIB = os.path.join(HERE, "libqem.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

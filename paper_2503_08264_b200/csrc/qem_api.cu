@@ -562,6 +562,33 @@ qem_status qem_cols_gamma_poisson(int64_t n, int32_t K, int32_t J, double alpha,
   return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_cols_gamma_poisson");
 }
 
+qem_status qem_cols_qmp_gaussian(int64_t n, int32_t K, int32_t J, int32_t scheme, double prior_var, double group_var,
+                                 double obs_var, const float* d_root_z, const float* d_root_mean,
+                                 const float* d_root_var, const double* d_q, const int32_t* d_copy, const float* d_eps,
+                                 const float* d_x, double* d_z, double* d_f_root, double* d_rows, double* d_cols,
+                                 void* stream) {
+  if (n < 0 || n > 0x7fffffffLL || K < 1 || K > QEM_MAX_K || J < 0 || (scheme != QEM_QMP_PERMUTATION && scheme != QEM_QMP_MIXTURE) ||
+      !(prior_var > 0.0) || !(group_var > 0.0) || !(obs_var > 0.0))
+    return fail(QEM_INVALID_ARGUMENT, "need 0 <= n < 2^31, 1 <= K <= %d, J >= 0, a scheme and positive variances",
+                QEM_MAX_K);
+  if (!d_root_z || !d_root_mean || !d_root_var || !d_f_root || !d_rows ||
+      (n > 0 && (!d_q || !d_copy || !d_eps || !d_z || !d_cols || (J > 0 && !d_x))))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_qmp_cols(n, K, J, scheme, prior_var, group_var, obs_var, d_root_z, d_root_mean,
+                                             d_root_var, d_q, d_copy, d_eps, d_x, d_z, d_f_root, d_rows, d_cols,
+                                             (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_cols_qmp_gaussian");
+}
+
+qem_status qem_moments_qmp(int64_t n, int32_t K, const double* d_w_root, const float* d_root_z, const double* d_w,
+                           const double* d_z, double* d_root_m, double* d_gm, void* stream) {
+  if (n < 0 || K < 1) return fail(QEM_INVALID_ARGUMENT, "bad sizes");
+  if (!d_w_root || !d_root_z || !d_root_m || (n > 0 && (!d_w || !d_z || !d_gm)))
+    return fail(QEM_INVALID_ARGUMENT, "null array");
+  const cudaError_t e = qem::launch_qmp_moments(n, K, d_w_root, d_root_z, d_w, d_z, d_root_m, d_gm, (cudaStream_t)stream);
+  return e == cudaSuccess ? QEM_OK : cuda_fail(e, "qem_moments_qmp");
+}
+
 qem_status qem_cols_beta_binomial(int64_t n, int32_t K, double kappa, const float* d_root_z,
                                   const float* d_root_mean, const float* d_root_var, const int32_t* d_y,
                                   const int32_t* d_N, const double* d_q, const double* d_z, double* d_f_root,

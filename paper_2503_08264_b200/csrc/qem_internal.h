@@ -142,6 +142,11 @@ cudaError_t launch_estep_tables(int64_t n, int K, const double* f_root, const do
 cudaError_t launch_estep_separable(int64_t n, int K, int R, const double* f_root, const double* rows,
                                    const double* cols, double* g, double* log_pe, double* w_root, double* w,
                                    cudaStream_t st);
+cudaError_t launch_qmp_cols(int64_t n, int K, int J, int scheme, double pv, double gv, double ov, const float* mu,
+                            const float* rm, const float* rv, const double* q, const int32_t* copy, const float* eps,
+                            const float* x, double* z, double* f_root, double* rows, double* cols, cudaStream_t st);
+cudaError_t launch_qmp_moments(int64_t n, int K, const double* w_root, const float* mu, const double* w,
+                               const double* z, double* root_m, double* gm, cudaStream_t st);
 cudaError_t launch_gamma_cols(int64_t n, int K, int J, double alpha, const float* mu, const float* rm, const float* rv,
                               const int32_t* y, const double* q, const double* z, double* f_root, double* rows,
                               double* cols, cudaStream_t st);

@@ -86,6 +86,38 @@ def estep_separable(f_root: torch.Tensor, rows: torch.Tensor, cols: torch.Tensor
     return out
 
 
+QMP_PERMUTATION, QMP_MIXTURE = 0, 1
+
+
+def estep_qmp_gaussian(mu: torch.Tensor, root_mean: torch.Tensor, root_var: torch.Tensor, q: torch.Tensor,
+                       copy: torch.Tensor, eps: torch.Tensor, x: torch.Tensor, scheme: int, *, prior_var=1.0,
+                       group_var=1.0, obs_var=1.0, stream=None):
+    """MPIW E-step under the non-factorised Q_MP with a parent-copy scheme (App. A):
+    qem_cols_qmp_gaussian (child draws + separable factors) -> qem_estep_separable -> qem_moments_qmp.
+    mu [K] f32 root samples, root_mean / root_var [1] f32, q [n][3] f64 (alpha, beta, s), copy [n][K]
+    int32, eps [n][K] f32, x [n][J] f32, all on the device.  Returns the E-step dict plus z [n][K],
+    root_m [2], gm [n][2] (argument marshalling only: every step runs in libqem)."""
+    K, n = mu.shape[0], q.shape[0]
+    J = x.shape[1] if x.numel() else 0
+    assert mu.dtype == eps.dtype == x.dtype == root_mean.dtype == root_var.dtype == torch.float32 and mu.is_cuda
+    assert q.dtype == torch.float64 and copy.dtype == torch.int32
+    assert tuple(q.shape) == (n, 3) and tuple(copy.shape) == (n, K) and tuple(eps.shape) == (n, K)
+    mu, q, copy, eps, x = mu.contiguous(), q.contiguous(), copy.contiguous(), eps.contiguous(), x.contiguous()
+    f64 = dict(dtype=torch.float64, device=mu.device)
+    z, f_root = torch.empty(n, K, **f64), torch.empty(K, **f64)
+    rows, cols = torch.empty(K, 2, **f64), torch.empty(n, K, 2, **f64)
+    check(lib().qem_cols_qmp_gaussian(n, K, J, int(scheme), float(prior_var), float(group_var), float(obs_var),
+                                      _ptr(mu), _ptr(root_mean), _ptr(root_var), _ptr(q), _ptr(copy), _ptr(eps),
+                                      _ptr(x), _ptr(z), _ptr(f_root), _ptr(rows), _ptr(cols), _stream(stream)),
+          "qem_cols_qmp_gaussian")
+    out = estep_separable(f_root, rows, cols, stream=stream)
+    out["z"], out["f_root"] = z, f_root
+    out["root_m"], out["gm"] = torch.empty(2, **f64), torch.empty(n, 2, **f64)
+    check(lib().qem_moments_qmp(n, K, _ptr(out["w_root"]), _ptr(mu), _ptr(out["w"]), _ptr(z), _ptr(out["root_m"]),
+                                _ptr(out["gm"]), _stream(stream)), "qem_moments_qmp")
+    return out
+
+
 def logmeanexp(x: torch.Tensor, stream=None) -> torch.Tensor:
     """log (1/n) sum exp(x) of a float64 device vector (qem_logmeanexp); returns a [1] tensor."""
     assert x.dtype == torch.float64 and x.is_cuda
