@@ -40,7 +40,7 @@ PERMUTATION, MIXTURE = 0, 1
 def draw_copies(rng, n, K, scheme):
     """Parent-copy indices [n][K]: a random permutation per group, or iid uniform indices."""
     if scheme == PERMUTATION:
-        return np.stack([rng.permutation(K) for _ in range(n)]).astype(np.int32)
+        return np.array([rng.permutation(K) for _ in range(n)], np.int32).reshape(n, K)
     return rng.integers(0, K, size=(n, K)).astype(np.int32)
 
 
