@@ -371,6 +371,7 @@ def run_gpu(args):
             variants["predictive_loglik"] = run_predictive_variant(m, main_m["data"], dev, seed)
             variants["gamma_poisson"] = run_gamma_variant(dev)
             variants["crossed_bus"] = run_crossed_variant(dev)
+            variants["qmp_nonfactorised"] = run_qmp_variant(dev)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -696,6 +697,44 @@ def run_gamma_variant(dev, steps=10):
             res[path] = {"ms_per_step": ms, "factor_pairs_per_s": model.n * model.K * model.K / (ms * 1e-3),
                          "qem_iters_per_s": 1e3 / ms}
         out[name] = res
+    return out
+
+
+def run_qmp_variant(dev, n=20_000, K=256, J=32, steps=10):
+    """NEXT row f4, second half (R43): one MPIW E-step under the non-factorised Q_MP
+    (child drawn at a copy of its parent; permutation and mixture densities) on a config-4-shaped
+    Gaussian hierarchy: qem_cols_qmp_gaussian -> qem_estep_separable -> qem_moments_qmp, all fp64,
+    no n x K x K table; CUDA events after 3 warm-up E-steps.  Inputs drawn with torch on the device."""
+    import torch
+    from paper_2503_08264_b200.qem import QMP_MIXTURE, QMP_PERMUTATION, estep_qmp_gaussian
+    gen = torch.Generator(device=dev).manual_seed(4)
+    f32 = dict(dtype=torch.float32, device=dev)
+    zt = torch.randn(n, 1, generator=gen, **f32) + 0.3
+    x = zt + torch.randn(n, J, generator=gen, **f32)
+    mu = 0.3 + torch.randn(K, generator=gen, **f32)
+    prec = 1.0 + J
+    q = torch.stack([x.sum(1).double() / prec, torch.full((n,), 0.8 / prec, dtype=torch.float64, device=dev),
+                     torch.full((n,), 1.0 / prec, dtype=torch.float64, device=dev)], 1)
+    eps = torch.randn(n, K, generator=gen, **f32)
+    rm, rv = torch.full((1,), 0.3, **f32), torch.ones(1, **f32)
+    out = {"workload": f"qmp-gaussian n={n} K={K} J={J} (fp64)"}
+    for name, scheme in (("permutation", QMP_PERMUTATION), ("mixture", QMP_MIXTURE)):
+        if scheme == QMP_PERMUTATION:
+            copy = torch.argsort(torch.rand(n, K, generator=gen, device=dev), dim=1).to(torch.int32)
+        else:
+            copy = torch.randint(0, K, (n, K), generator=gen, device=dev, dtype=torch.int32)
+        for _ in range(3):
+            r = estep_qmp_gaussian(mu, rm, rv, q, copy, eps, x, scheme)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        st.record()
+        for _ in range(steps):
+            r = estep_qmp_gaussian(mu, rm, rv, q, copy, eps, x, scheme)
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / steps
+        out[name] = {"ms_per_estep": ms, "factor_pairs_per_s": n * K * K / (ms * 1e-3),
+                     "log_pe": float(r["log_pe"][0])}
     return out
 
 
