@@ -8,9 +8,8 @@ timeout 600 python bench.py > gpurun_out/r02_bench_c5.json 2> gpurun_out/bench_c
 timeout 600 python bench.py --config 4 > gpurun_out/r02_bench_c4.json 2> gpurun_out/bench_c4.err; echo "bench4 rc=$?"
 timeout 600 python bench.py --impl reference > gpurun_out/r02_bench_reference_c5.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 10 --warmup 3 --no-cpu --no-variants > gpurun_out/r02_bench_c5_torchrun1.json 2> gpurun_out/bench_tr.err; echo "torchrun1 rc=$?"
-timeout 600 python tools/shard_proxy.py --config 5 --out gpurun_out/r02_shard_proxy.json > gpurun_out/shard5.log 2>&1; echo "shard5 rc=$?"
-timeout 600 python tools/shard_proxy.py --config 4 --out gpurun_out/r02_shard_proxy.json >> gpurun_out/shard5.log 2>&1; echo "shard4 rc=$?"
-tail -12 gpurun_out/shard5.log
+timeout 600 python tools/shard_proxy.py 5 4 > gpurun_out/r02_shard_proxy.json 2> gpurun_out/shard.err; echo "shard proxy rc=$?"
+cat gpurun_out/r02_shard_proxy.json
 python - <<'P'
 import json
 for f in ("r02_bench_c5", "r02_bench_c4", "r02_bench_reference_c5", "r02_bench_c5_torchrun1"):
