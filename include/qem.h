@@ -15,7 +15,7 @@
  *   Eq. 9     (Sec. 4)    EMA over mean parameters
  *   PAPER.md:393-394 (Limitations)          elimination over the plate tree,
  *                                           grouping, chunking
- * Readings of ambiguous points (R1..R33) are listed in DESIGN.md.
+ * Readings of ambiguous points (R1..R43) are listed in DESIGN.md.
  *
  * ENTRY POINTS
  *  - the hot path (context-based, two- and three-level Gaussian models):
